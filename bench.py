@@ -1,0 +1,555 @@
+#!/usr/bin/env python3
+"""Benchmark of the fused-multiloop executor on B200 (driver contract: one JSON line).
+
+Default workload = BASELINE.json's headline: k-means iterations/sec, N=16,777,216 samples,
+d=64, k=64, fp64 (config C4), samples sharded contiguously across the ranks; one step = one
+k-means iteration = the fused {argmin collect + k*(d+1) predicated reduces} multiloop, the
+NCCL allReduce of (counts, sums) across ranks, and the centroid update.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dlx|reference] [--config c4|c1|c2|c3|c5]
+
+--impl reference times the reference's CPU path (the oracle restatement of the reference
+loop semantics, oracle/, with all host threads) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (family, params, metric, unit)
+    "c4": ("kmeans", dict(n=16_777_216, d=64, k=64),
+           "k-means iters/sec (N=16M,d=64,k=64) at 1/2/4/8 B200; fused-op HBM GB/s vs peak", "it/s"),
+    "c1": ("kmeans", dict(n=65_536, d=16, k=8), "k-means iters/sec (N=65536,d=16,k=8)", "it/s"),
+    "c2": ("logreg", dict(n=1_048_576, d=64), "logistic-regression BGD iters/sec (N=1M,d=64)", "it/s"),
+    "l16": ("logreg", dict(n=16_777_216, d=64), "logistic-regression BGD iters/sec (N=16M,d=64)", "it/s"),
+    "c3": ("gda", dict(n=1_048_576, d=64), "GDA fits/sec (N=1M,d=64)", "fits/s"),
+    "c5": ("groupby", dict(n=1_000_000_000, K=64), "GroupBy bucket-count passes/sec (1e9 keys, K=64)", "passes/s"),
+}
+
+# algorithmic bytes per unit: k-means sample d*8 + 4 (int32 assignment write);
+# logreg sample 8d + 8; GDA sample 2 * (8d + 8) (two passes); GroupBy key 8.
+
+
+def algorithmic_bytes(family, p, n_local):
+    if family == "kmeans":
+        return n_local * (p["d"] * 8 + 4)
+    if family == "logreg":
+        return n_local * (p["d"] * 8 + 8)
+    if family == "gda":
+        return n_local * (p["d"] * 8 + 8)  # per pass (dominant kernel = one pass)
+    if family == "groupby":
+        return n_local * 8
+    raise ValueError(family)
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(config_name):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(config_name)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.out = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.out, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.out.close()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [s.strip() for s in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = sorted(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for nm, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------------------------
+
+def run_reference(args, family, p, metric, unit):
+    """The reference CPU path (oracle restatement of the reference multiloop semantics,
+    SPEC.md executeDEG chunking, all host threads) on a bounded sample per step."""
+    import numpy as np
+
+    import oracle as O
+    threads = O.threads()
+    t_steps = []
+    if family == "kmeans":
+        n_s = min(p["n"], int(os.environ.get("DLX_REF_SAMPLE", 1 << 21)))
+        x = O.rng_units(1, 0, n_s * p["d"]).reshape(n_s, p["d"])
+        mu = x[: p["k"]].copy()
+        scale = p["n"] / n_s
+        for s in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            a, c, sm = O.kmeans_step(x, p["k"], mu, workers=threads, chunks=4 * threads)
+            mu = O.kmeans_update(c, sm)
+            dt = time.perf_counter() - t0
+            if s >= args.warmup:
+                t_steps.append(dt * scale)
+        sample = f"{n_s} of {p['n']} samples per step (d={p['d']}, k={p['k']}), time scaled by N/n_sample"
+    elif family == "logreg":
+        n_s = min(p["n"], 1 << 21)
+        x = O.rng_units(1, 0, n_s * p["d"]).reshape(n_s, p["d"])
+        y = O.rng_ints(1, n_s * p["d"], n_s, 2)
+        th = np.zeros(p["d"])
+        scale = p["n"] / n_s
+        for s in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            th = th - (1.0 / p["n"]) * O.logreg_grad(x, y, th, workers=threads, chunks=4 * threads)
+            dt = time.perf_counter() - t0
+            if s >= args.warmup:
+                t_steps.append(dt * scale)
+        sample = f"{n_s} of {p['n']} samples per step, scaled"
+    elif family == "gda":
+        n_s = min(p["n"], 1 << 19)
+        x = O.rng_units(1, 0, n_s * p["d"]).reshape(n_s, p["d"])
+        y = O.rng_ints(1, n_s * p["d"], n_s, 2)
+        scale = p["n"] / n_s
+        for s in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            n1, s0, s1 = O.gda_pass1(x, y, workers=threads, chunks=4 * threads)
+            O.gda_pass2(x, y, s0 / (n_s - n1), s1 / n1, workers=threads, chunks=4 * threads)
+            dt = time.perf_counter() - t0
+            if s >= args.warmup:
+                t_steps.append(dt * scale)
+        sample = f"{n_s} of {p['n']} samples per step, scaled"
+    else:
+        n_s = min(p["n"], 1 << 27)
+        keys = O.rng_ints(1, 0, n_s, p["K"])
+        scale = p["n"] / n_s
+        for s in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            O.groupby_count(keys, p["K"], workers=threads, chunks=4 * threads)
+            dt = time.perf_counter() - t0
+            if s >= args.warmup:
+                t_steps.append(dt * scale)
+        sample = f"{n_s} of {p['n']} keys per step, scaled"
+    t = sum(t_steps) / len(t_steps)
+    value = 1.0 / t
+    return {
+        "metric": metric, "value": value, "unit": unit, "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64" if family != "groupby" else "int64",
+        "data": "synthetic (reference Rng, seed 1)",
+        "config": {"workload": args.config, **p},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def cpu_baseline_kmeans(p, budget_s=15.0):
+    import oracle as O
+    threads = O.threads()
+    n_s = min(p["n"], 1 << 20)
+    x = O.rng_units(1, 0, n_s * p["d"]).reshape(n_s, p["d"])
+    mu = x[: p["k"]].copy()
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < 3 and (time.perf_counter() - t_start) < budget_s:
+        t0 = time.perf_counter()
+        O.kmeans_step(x, p["k"], mu, workers=threads, chunks=4 * threads)
+        times.append(time.perf_counter() - t0)
+    t = min(times) * p["n"] / n_s
+    return {"value": 1.0 / t, "unit": "it/s", "cores": threads, "kind": "port",
+            "sample": f"1 k-means iteration over {n_s} of {p['n']} samples (d={p['d']}, k={p['k']}), "
+                      f"executeDEG chunking {4 * threads} chunks, time scaled by N/n_sample"}
+
+
+def cpu_baseline_generic(family, p):
+    import numpy as np
+
+    import oracle as O
+    threads = O.threads()
+    if family == "logreg":
+        n_s = min(p["n"], 1 << 20)
+        x = O.rng_units(1, 0, n_s * p["d"]).reshape(n_s, p["d"])
+        y = O.rng_ints(1, n_s * p["d"], n_s, 2)
+        t0 = time.perf_counter()
+        O.logreg_grad(x, y, np.zeros(p["d"]), workers=threads, chunks=4 * threads)
+        t = (time.perf_counter() - t0) * p["n"] / n_s
+        unit, smp = "it/s", f"1 gradient over {n_s} samples, scaled"
+    elif family == "gda":
+        n_s = min(p["n"], 1 << 18)
+        x = O.rng_units(1, 0, n_s * p["d"]).reshape(n_s, p["d"])
+        y = O.rng_ints(1, n_s * p["d"], n_s, 2)
+        t0 = time.perf_counter()
+        n1, s0, s1 = O.gda_pass1(x, y, workers=threads, chunks=4 * threads)
+        O.gda_pass2(x, y, s0 / (n_s - n1), s1 / n1, workers=threads, chunks=4 * threads)
+        t = (time.perf_counter() - t0) * p["n"] / n_s
+        unit, smp = "fits/s", f"1 GDA fit over {n_s} samples, scaled"
+    else:
+        n_s = min(p["n"], 1 << 27)
+        keys = O.rng_ints(1, 0, n_s, p["K"])
+        t0 = time.perf_counter()
+        O.groupby_count(keys, p["K"], workers=threads, chunks=4 * threads)
+        t = (time.perf_counter() - t0) * p["n"] / n_s
+        unit, smp = "passes/s", f"1 pass over {n_s} keys, scaled"
+    return {"value": 1.0 / t, "unit": unit, "cores": threads, "kind": "port", "sample": smp}
+
+
+def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
+    import torch
+
+    from paper_1109_0778_b200 import _lib
+    from paper_1109_0778_b200 import multiloops as ml
+    from paper_1109_0778_b200.comm import Comm, shard_range
+    from paper_1109_0778_b200.programs import KMeansProgram, LogRegProgram
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        comm = Comm.from_torch_distributed()
+    _lib.load()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    n = p["n"]
+    lo, hi = shard_range(n, rank, world)
+    n_local = hi - lo
+    stream = torch.cuda.current_stream()
+    launches_per_step = 0
+    d = p.get("d", 0)
+
+    if family == "kmeans":
+        k = p["k"]
+        x = ml.rng_units(n_local * d, seed=1, first_draw=lo * d, device=dev).view(n_local, d)
+        mu0 = ml.rng_units(k * d, seed=1, first_draw=0, device=dev).view(k, d)  # first k rows of x
+        prog = KMeansProgram(x, k, mu0, comm=comm, method=args.method)
+        kernel_fn = lambda: ml.kmeans_step(x, prog.mu, prog.assign, prog.counts, prog.sums,  # noqa: E731
+                                           method=args.method)
+
+        def step():
+            kernel_fn()
+            if comm is not None:
+                comm.allreduce_(prog.counts)
+                comm.allreduce_(prog.sums)
+            ml.kmeans_update(prog.counts, prog.sums, prog.mu)
+        launches_per_step = 3
+    elif family == "logreg":
+        x = ml.rng_units(n_local * d, seed=1, first_draw=lo * d, device=dev).view(n_local, d)
+        y = ml.rng_ints(n_local, 2, seed=1, first_draw=n * d + lo, device=dev)
+        prog = LogRegProgram(x, y, torch.zeros(d, dtype=torch.float64, device=dev), 1.0 / n, comm=comm)
+        kernel_fn = lambda: ml.logreg_grad(x, y, prog.theta, prog.grad)  # noqa: E731
+
+        def step():
+            kernel_fn()
+            if comm is not None:
+                comm.allreduce_(prog.grad)
+            ml.axpy_inplace(prog.theta, prog.grad, prog.alpha)
+        launches_per_step = 3
+    elif family == "gda":
+        x = ml.rng_units(n_local * d, seed=1, first_draw=lo * d, device=dev).view(n_local, d)
+        y = ml.rng_ints(n_local, 2, seed=1, first_draw=n * d + lo, device=dev)
+        holder = {}
+
+        def kernel_fn():
+            holder["r"] = ml.gda_pass1(x, y)
+
+        def step():
+            kernel_fn()
+            n1, s0, s1 = holder["r"]
+            if comm is not None:
+                comm.allreduce_(n1); comm.allreduce_(s0); comm.allreduce_(s1)
+            mu0, mu1 = ml.gda_means(n1, s0, s1, n)
+            S = ml.gda_pass2(x, y, mu0, mu1)
+            if comm is not None:
+                comm.allreduce_(S)
+        launches_per_step = 8
+    else:
+        K = p["K"]
+        keys = ml.rng_ints(n_local, K, seed=1, first_draw=lo, device=dev)
+        counts = torch.empty(K, dtype=torch.int64, device=dev)
+        kernel_fn = lambda: ml.groupby_count(keys, K, counts)  # noqa: E731
+
+        def step():
+            kernel_fn()
+            if comm is not None:
+                comm.allreduce_(counts)
+        launches_per_step = 2
+
+    # warm-up
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for s in range(args.steps):
+        ev[s][0].record(stream)
+        # dominant kernel timed on its own stream with events around it
+        if family in ("kmeans", "logreg", "groupby"):
+            kernel_fn()
+            ev[s][1].record(stream)
+            # remainder of the step (allreduce + update)
+            if family == "kmeans":
+                if comm is not None:
+                    comm.allreduce_(prog.counts)
+                    comm.allreduce_(prog.sums)
+                ml.kmeans_update(prog.counts, prog.sums, prog.mu)
+            elif family == "logreg":
+                if comm is not None:
+                    comm.allreduce_(prog.grad)
+                ml.axpy_inplace(prog.theta, prog.grad, prog.alpha)
+            else:
+                if comm is not None:
+                    comm.allreduce_(counts)
+        else:
+            kernel_fn()
+            ev[s][1].record(stream)
+            n1, s0, s1 = holder["r"]
+            if comm is not None:
+                comm.allreduce_(n1); comm.allreduce_(s0); comm.allreduce_(s1)
+            mu0, mu1 = ml.gda_means(n1, s0, s1, n)
+            S = ml.gda_pass2(x, y, mu0, mu1)
+            if comm is not None:
+                comm.allreduce_(S)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    kern_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    if dist is not None:
+        t = torch.tensor([total_ms, kern_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, kern_ms = float(t[0]), float(t[1])
+    ms_per_step = total_ms / args.steps
+    value = 1000.0 / ms_per_step
+
+    # ---- end to end through the public API with host buffers ----------------------------------
+    e2e = None
+    if family == "kmeans":
+        e2e = e2e_kmeans(args, p, n_local, lo, comm, dist, dev)
+    elif family == "logreg":
+        e2e = e2e_logreg(args, p, n_local, lo, comm, dist, dev)
+
+    result = None
+    if rank == 0:
+        peak, peak_kind = measured_peaks()
+        bytes_launch = algorithmic_bytes(family, p, n_local)
+        achieved = bytes_launch / (kern_ms * 1e-3) / 1e9
+        result = {
+            "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if family != "groupby" else "int64",
+            "data": "synthetic (reference Rng LCG, seed 1, generated on device, bit-identical to host)",
+            "config": {"workload": args.config, **p, "parallelism": f"sample-sharded dp{world}",
+                       "l2": "inputs larger than L2 (no flush needed)" if bytes_launch > 256e6 else
+                             "inputs L2-resident (launch-bound config)",
+                       "method": {0: "auto", 1: "direct", 2: "screened"}[args.method]},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(args.config),
+                         "peak_kind": peak_kind, "kernel_ms": kern_ms,
+                         "algorithmic_bytes_per_launch": bytes_launch},
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                result["cpu_baseline"] = (cpu_baseline_kmeans(p) if family == "kmeans"
+                                          else cpu_baseline_generic(family, p))
+            except Exception as exc:  # report, never fake
+                result["cpu_baseline"] = {"value": None, "error": str(exc)}
+    if comm is not None:
+        comm.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return result
+
+
+def e2e_kmeans(args, p, n_local, lo, comm, dist, dev, iters_per_job=10):
+    """One e2e step = one k-means job through the public API from HOST data: H2D of the
+    (pinned) sample shard, `iters_per_job` iterations, D2H of assignments + centroids."""
+    import torch
+
+    from paper_1109_0778_b200 import multiloops as ml
+    from paper_1109_0778_b200.programs import KMeansProgram
+    d, k = p["d"], p["k"]
+    x_dev = torch.empty((n_local, d), dtype=torch.float64, device=dev)
+    ml.rng_units(n_local * d, seed=1, first_draw=lo * d, device=dev, out=x_dev.view(-1))
+    x_host = torch.empty((n_local, d), dtype=torch.float64, pin_memory=True)
+    x_host.copy_(x_dev)
+    mu0_dev = ml.rng_units(k * d, seed=1, device=dev).view(k, d)
+    a_host = torch.empty(n_local, dtype=torch.int32, pin_memory=True)
+    mu_host = torch.empty((k, d), dtype=torch.float64, pin_memory=True)
+    stream = torch.cuda.current_stream()
+    jobs = max(1, min(3, args.steps // 4 or 1))
+
+    def job():
+        x_dev.copy_(x_host, non_blocking=True)
+        prog = KMeansProgram(x_dev, k, mu0_dev, comm=comm, method=args.method)
+        prog.run(iters_per_job)
+        a_host.copy_(prog.assign, non_blocking=True)
+        mu_host.copy_(prog.mu, non_blocking=True)
+
+    job()  # warm-up
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(jobs):
+        job()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    it_s = jobs * iters_per_job / (ms * 1e-3)
+    del x_dev, x_host
+    torch.cuda.empty_cache()
+    return {"value": it_s, "unit": "it/s", "h2d_bytes_per_step": n_local * d * 8,
+            "d2h_bytes_per_step": n_local * 4 + k * d * 8,
+            "step": f"one job = H2D x shard (pinned) + {iters_per_job} iterations + D2H assignments and centroids",
+            "iters_per_step": iters_per_job}
+
+
+def e2e_logreg(args, p, n_local, lo, comm, dist, dev, iters_per_job=20):
+    import torch
+
+    from paper_1109_0778_b200 import multiloops as ml
+    from paper_1109_0778_b200.programs import LogRegProgram
+    d, n = p["d"], p["n"]
+    x_dev = ml.rng_units(n_local * d, seed=1, first_draw=lo * d, device=dev).view(n_local, d)
+    y_dev = ml.rng_ints(n_local, 2, seed=1, first_draw=n * d + lo, device=dev)
+    x_host = torch.empty_like(x_dev, device="cpu").pin_memory()
+    y_host = torch.empty_like(y_dev, device="cpu").pin_memory()
+    x_host.copy_(x_dev)
+    y_host.copy_(y_dev)
+    th_host = torch.empty(d, dtype=torch.float64, pin_memory=True)
+    stream = torch.cuda.current_stream()
+
+    def job():
+        x_dev.copy_(x_host, non_blocking=True)
+        y_dev.copy_(y_host, non_blocking=True)
+        prog = LogRegProgram(x_dev, y_dev, torch.zeros(d, dtype=torch.float64, device=dev), 1.0 / n, comm=comm)
+        for _ in range(iters_per_job):
+            prog.step()
+        th_host.copy_(prog.theta, non_blocking=True)
+
+    job()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    job()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    return {"value": iters_per_job / (ms * 1e-3), "unit": "it/s", "h2d_bytes_per_step": n_local * (d * 8 + 8),
+            "d2h_bytes_per_step": d * 8,
+            "step": f"one job = H2D x,y shard (pinned) + {iters_per_job} BGD iterations + D2H theta",
+            "iters_per_step": iters_per_job}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="dlx", choices=["dlx", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--method", type=int, default=0, help="k-means: 0 auto, 1 direct fp64, 2 screened")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    family, p, metric, unit = CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        res = run_reference(args, family, dict(p), metric, unit)
+        res["n_gpus"] = world
+        print(json.dumps(res), flush=True)
+        return 0
+    res = run_dlx(args, family, dict(p), metric, unit, rank, world, local_rank)
+    if rank == 0 and res is not None:
+        print(json.dumps(res), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

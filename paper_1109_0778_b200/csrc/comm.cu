@@ -1,0 +1,76 @@
+// comm.cu — sample-sharded multi-GPU mode: one process per GPU, each rank runs
+// the fused multiloop on its contiguous sample shard, then the partial activation records
+// (k-means counts/sums, logreg gradient, GDA class sums / scatter, GroupBy counts) are
+// summed across ranks with NCCL allReduce over NVLink / NVSwitch.  The unique id is
+// exchanged by the caller (torch.distributed store / broadcast in the Python host layer).
+#include <nccl.h>
+
+#include <cstring>
+
+#include "common.cuh"
+
+struct dlx_comm_s {
+  ncclComm_t comm;
+  int nranks;
+  int rank;
+};
+
+static_assert(sizeof(ncclUniqueId) == DLX_COMM_ID_BYTES, "ncclUniqueId size");
+
+#define DLX_NCCL(call)                                                         \
+  do {                                                                         \
+    ncclResult_t _r = (call);                                                  \
+    if (_r != ncclSuccess) {                                                   \
+      ::dlx::set_error("%s: %s", #call, ncclGetErrorString(_r));               \
+      return DLX_ERR_COMM;                                                     \
+    }                                                                          \
+  } while (0)
+
+extern "C" {
+
+int dlx_comm_unique_id(uint8_t* h_id) {
+  DLX_REQUIRE(h_id, DLX_ERR_ARG, "null id");
+  ncclUniqueId id;
+  DLX_NCCL(ncclGetUniqueId(&id));
+  std::memcpy(h_id, &id, sizeof(id));
+  return DLX_OK;
+}
+
+int dlx_comm_init(dlx_comm_t* comm, const uint8_t* h_id, int nranks, int rank) {
+  DLX_REQUIRE(comm && h_id && nranks > 0 && rank >= 0 && rank < nranks, DLX_ERR_ARG,
+              "comm init: bad args");
+  ncclUniqueId id;
+  std::memcpy(&id, h_id, sizeof(id));
+  auto* c = new dlx_comm_s{nullptr, nranks, rank};
+  ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    dlx::set_error("ncclCommInitRank: %s", ncclGetErrorString(r));
+    return DLX_ERR_COMM;
+  }
+  *comm = c;
+  return DLX_OK;
+}
+
+int dlx_comm_destroy(dlx_comm_t comm) {
+  if (!comm) return DLX_OK;
+  ncclResult_t r = ncclCommDestroy(comm->comm);
+  delete comm;
+  if (r != ncclSuccess) {
+    dlx::set_error("ncclCommDestroy: %s", ncclGetErrorString(r));
+    return DLX_ERR_COMM;
+  }
+  return DLX_OK;
+}
+
+int dlx_comm_allreduce_sum(dlx_comm_t comm, void* d_buf, int64_t count, int dtype,
+                           dlx_stream_t stream) {
+  DLX_REQUIRE(comm && (d_buf || count == 0) && count >= 0, DLX_ERR_ARG, "allreduce: bad args");
+  DLX_REQUIRE(dtype == 0 || dtype == 1, DLX_ERR_ARG, "allreduce: dtype must be 0 (f64) or 1 (i64)");
+  if (comm->nranks == 1 || count == 0) return DLX_OK;
+  DLX_NCCL(ncclAllReduce(d_buf, d_buf, static_cast<size_t>(count),
+                         dtype == 0 ? ncclFloat64 : ncclInt64, ncclSum, comm->comm, stream));
+  return DLX_OK;
+}
+
+}  // extern "C"

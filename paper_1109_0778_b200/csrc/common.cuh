@@ -1,0 +1,102 @@
+// common.cuh — shared helpers for the dlx CUDA sources (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/dlx.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "dlx kernels target sm_100a only"
+#endif
+
+namespace dlx {
+
+// Thread-local last-error text, returned by dlx_last_error().
+void set_error(const char* fmt, ...);
+
+inline int cuda_fail(cudaError_t e, const char* what) {
+  set_error("%s: %s", what, cudaGetErrorString(e));
+  return DLX_ERR_CUDA;
+}
+
+#define DLX_CUDA(call)                                    \
+  do {                                                    \
+    cudaError_t _e = (call);                              \
+    if (_e != cudaSuccess) return ::dlx::cuda_fail(_e, #call); \
+  } while (0)
+
+#define DLX_LAUNCHED(name)                                \
+  do {                                                    \
+    cudaError_t _e = cudaGetLastError();                  \
+    if (_e != cudaSuccess) return ::dlx::cuda_fail(_e, name); \
+  } while (0)
+
+#define DLX_REQUIRE(cond, code, ...)                      \
+  do {                                                    \
+    if (!(cond)) {                                        \
+      ::dlx::set_error(__VA_ARGS__);                      \
+      return (code);                                      \
+    }                                                     \
+  } while (0)
+
+// Number of SMs of the current device (cached per device).
+int sm_count();
+
+// Workspace carving: 256-byte aligned sub-allocations out of one caller buffer.
+struct Carve {
+  char* base;
+  size_t used = 0;
+  explicit Carve(void* p) : base(static_cast<char*>(p)) {}
+  template <class T>
+  T* take(size_t count) {
+    used = (used + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base ? base + used : nullptr);
+    used += count * sizeof(T);
+    return p;
+  }
+};
+
+// LCG constants of the reference Rng (runtime.hpp:90).
+constexpr uint64_t kRngMul = 6364136223846793005ULL;
+constexpr uint64_t kRngInc = 1442695040888963407ULL;
+
+__host__ __device__ inline uint64_t rng_advance(uint64_t state, uint64_t n) {
+  uint64_t am = 1, aa = 0, cm = kRngMul, ca = kRngInc;
+  while (n) {
+    if (n & 1) {
+      am = am * cm;
+      aa = aa * cm + ca;
+    }
+    ca = (cm + 1) * ca;
+    cm = cm * cm;
+    n >>= 1;
+  }
+  return am * state + aa;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Streaming 128-bit load that does not allocate in L1 (each sample row is read once).
+__device__ __forceinline__ double2 ld_stream_f64x2(const double* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(r.x), "=d"(r.y)
+               : "l"(p));
+  return r;
+}
+
+}  // namespace dlx

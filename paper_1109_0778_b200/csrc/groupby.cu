@@ -1,0 +1,169 @@
+// groupby.cu — GroupBy / bucket-count multiloop.
+//
+// Reference formulation: nbuckets predicated count reduces `if (key(i) == b) cnt_b += 1`
+// over one index traversal (count_where, proj/src/vectordsl.cpp:138-151), O(N*K) guards.
+// Device plan: one pass over the keys with 128-bit loads; shared-memory privatised
+// counters (several sub-histograms per CTA, one per warp group, to spread same-bucket
+// contention), merged per CTA into uint32 partials and combined across CTAs in ascending
+// order.  Buckets too many for shared memory use 64-bit global reductions.  Integer
+// arithmetic, so results are exact and independent of the reduction order.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace dlx {
+
+constexpr int kGbThreads = 512;
+constexpr size_t kGbSmemBudget = 96 * 1024;
+
+struct GroupbyPlan {
+  bool shared;   // shared-memory privatised path
+  int copies;    // sub-histograms per CTA
+  int grid;
+  size_t smem;
+};
+
+static GroupbyPlan groupby_plan(int64_t n, int64_t nb) {
+  GroupbyPlan p{};
+  const size_t one = static_cast<size_t>(nb) * sizeof(unsigned);
+  p.shared = one <= kGbSmemBudget;
+  int per_sm = 2;
+  if (p.shared) {
+    p.copies = static_cast<int>(std::min<size_t>(kGbThreads / 32, kGbSmemBudget / one));
+    p.copies = std::max(1, p.copies);
+    // power of two so warp -> copy is a mask
+    int c = 1;
+    while (c * 2 <= p.copies) c *= 2;
+    p.copies = c;
+    p.smem = one * p.copies;
+  } else {
+    p.copies = 0;
+    p.smem = 0;
+    per_sm = 4;
+  }
+  int64_t grid = static_cast<int64_t>(sm_count()) * per_sm;
+  const int64_t need = (n / 2 + kGbThreads - 1) / kGbThreads;
+  grid = std::max<int64_t>(1, std::min(grid, need));
+  p.grid = static_cast<int>(grid);
+  return p;
+}
+
+__device__ __forceinline__ void count_key(unsigned* h, long long key, long long nb) {
+  if (static_cast<unsigned long long>(key) < static_cast<unsigned long long>(nb))
+    atomicAdd(h + key, 1u);
+}
+
+__global__ void __launch_bounds__(kGbThreads)
+groupby_smem_kernel(const long long* __restrict__ keys, int64_t n, long long nb, int copies,
+                    unsigned* __restrict__ partials) {
+  extern __shared__ unsigned hist[];
+  const int tid = threadIdx.x;
+  const int total = static_cast<int>(nb) * copies;
+  for (int e = tid; e < total; e += kGbThreads) hist[e] = 0;
+  __syncthreads();
+  unsigned* h = hist + static_cast<size_t>((tid >> 5) & (copies - 1)) * nb;
+
+  // pairs of keys via 128-bit loads; 4 pairs in flight per thread
+  const int64_t npairs = n >> 1;
+  const longlong2* kp = reinterpret_cast<const longlong2*>(keys);
+  const int64_t T = static_cast<int64_t>(gridDim.x) * kGbThreads;
+  int64_t q = static_cast<int64_t>(blockIdx.x) * kGbThreads + tid;
+  for (; q + 3 * T < npairs; q += 4 * T) {
+    longlong2 v0 = __ldg(kp + q), v1 = __ldg(kp + q + T), v2 = __ldg(kp + q + 2 * T),
+              v3 = __ldg(kp + q + 3 * T);
+    count_key(h, v0.x, nb); count_key(h, v0.y, nb);
+    count_key(h, v1.x, nb); count_key(h, v1.y, nb);
+    count_key(h, v2.x, nb); count_key(h, v2.y, nb);
+    count_key(h, v3.x, nb); count_key(h, v3.y, nb);
+  }
+  for (; q < npairs; q += T) {
+    longlong2 v = __ldg(kp + q);
+    count_key(h, v.x, nb);
+    count_key(h, v.y, nb);
+  }
+  if ((n & 1) && blockIdx.x == 0 && tid == 0) count_key(h, keys[n - 1], nb);
+  __syncthreads();
+  unsigned* out = partials + static_cast<size_t>(blockIdx.x) * nb;
+  for (long long b = tid; b < nb; b += kGbThreads) {
+    unsigned acc = 0;
+    for (int c = 0; c < copies; ++c) acc += hist[static_cast<size_t>(c) * nb + b];
+    out[b] = acc;
+  }
+}
+
+__global__ void groupby_finalize_kernel(const unsigned* __restrict__ partials, int parts,
+                                        long long nb, long long* __restrict__ counts) {
+  for (long long b = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; b < nb;
+       b += static_cast<long long>(gridDim.x) * blockDim.x) {
+    long long acc = 0;
+    for (int p = 0; p < parts; ++p) acc += partials[static_cast<size_t>(p) * nb + b];
+    counts[b] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(kGbThreads)
+groupby_global_kernel(const long long* __restrict__ keys, int64_t n, long long nb,
+                      unsigned long long* __restrict__ counts) {
+  const int64_t T = static_cast<int64_t>(gridDim.x) * kGbThreads;
+  const int64_t npairs = n >> 1;
+  const longlong2* kp = reinterpret_cast<const longlong2*>(keys);
+  for (int64_t q = static_cast<int64_t>(blockIdx.x) * kGbThreads + threadIdx.x; q < npairs;
+       q += T) {
+    longlong2 v = __ldg(kp + q);
+    if (static_cast<unsigned long long>(v.x) < static_cast<unsigned long long>(nb))
+      atomicAdd(counts + v.x, 1ull);
+    if (static_cast<unsigned long long>(v.y) < static_cast<unsigned long long>(nb))
+      atomicAdd(counts + v.y, 1ull);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    long long key = keys[n - 1];
+    if (static_cast<unsigned long long>(key) < static_cast<unsigned long long>(nb))
+      atomicAdd(counts + key, 1ull);
+  }
+}
+
+}  // namespace dlx
+
+using namespace dlx;
+
+extern "C" {
+
+size_t dlx_groupby_workspace_bytes(int64_t n, int64_t nbuckets) {
+  GroupbyPlan p = groupby_plan(n, nbuckets);
+  if (!p.shared) return 256;
+  return static_cast<size_t>(p.grid) * nbuckets * sizeof(unsigned) + 256;
+}
+
+int dlx_groupby_count(const int64_t* d_keys, int64_t n, int64_t nbuckets, int64_t* d_counts,
+                      void* d_workspace, size_t workspace_bytes, dlx_stream_t stream) {
+  DLX_REQUIRE(n >= 0 && nbuckets > 0, DLX_ERR_ARG, "groupby: bad shape");
+  DLX_REQUIRE(d_counts && (d_keys || n == 0), DLX_ERR_ARG, "groupby: null buffer");
+  DLX_REQUIRE((reinterpret_cast<uintptr_t>(d_keys) & 15) == 0, DLX_ERR_ARG,
+              "groupby: keys must be 16-byte aligned");
+  GroupbyPlan p = groupby_plan(n, nbuckets);
+  if (!p.shared) {
+    DLX_CUDA(cudaMemsetAsync(d_counts, 0, sizeof(int64_t) * nbuckets, stream));
+    if (n == 0) return DLX_OK;
+    groupby_global_kernel<<<p.grid, kGbThreads, 0, stream>>>(
+        reinterpret_cast<const long long*>(d_keys), n, nbuckets,
+        reinterpret_cast<unsigned long long*>(d_counts));
+    DLX_LAUNCHED("groupby_global_kernel");
+    return DLX_OK;
+  }
+  const size_t need = static_cast<size_t>(p.grid) * nbuckets * sizeof(unsigned);
+  DLX_REQUIRE(d_workspace && workspace_bytes >= need, DLX_ERR_ARG,
+              "groupby: workspace too small (%zu < %zu)", workspace_bytes, need);
+  unsigned* partials = static_cast<unsigned*>(d_workspace);
+  DLX_CUDA(cudaFuncSetAttribute(groupby_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(p.smem)));
+  groupby_smem_kernel<<<p.grid, kGbThreads, p.smem, stream>>>(
+      reinterpret_cast<const long long*>(d_keys), n, nbuckets, p.copies, partials);
+  DLX_LAUNCHED("groupby_smem_kernel");
+  const int fb = static_cast<int>(std::min<int64_t>((nbuckets + 255) / 256, 1024));
+  groupby_finalize_kernel<<<fb, 256, 0, stream>>>(partials, p.grid, nbuckets,
+                                                  reinterpret_cast<long long*>(d_counts));
+  DLX_LAUNCHED("groupby_finalize_kernel");
+  return DLX_OK;
+}
+
+}  // extern "C"

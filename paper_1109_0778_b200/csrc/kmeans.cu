@@ -1,0 +1,300 @@
+// kmeans.cu — the fused k-means multiloop, exact fp64 direct form.
+//
+// Reference semantics (what one fused ParallelLoop of the staged k-means iteration does,
+// rendered by emit_parallel_loop, proj/src/codegen.cpp:345-433):
+//   collect elem : a_i = argmin chain over c of  sum_j (x_ij - mu_cj)^2
+//                  (inner mk_reduce over j, loops.cpp:111-174: sequential left fold from 0.0,
+//                   separate multiply and add; staged_if chain, stage.cpp:73-104:
+//                   `if (dist_c < best) {best = dist_c; idx = c}` from best = 1e300, idx = 0)
+//   reduce elems : counts_c = sum_i [a_i == c] * 1,  sums_cj = sum_i [a_i == c] * x_ij
+//                  (k*(d+1) predicated mk_reduce elems, filtered-out index = identity).
+//
+// Device plan (direct kernel):
+//   * persistent CTAs (grid = SMs x occupancy) walk sample tiles;
+//   * mu (k x d) lives in shared memory for the whole kernel, x tiles are staged through
+//     shared memory with coalesced 128-bit loads;
+//   * thread (group g, sample s): distances of sample s to the centroids of group g, each
+//     a sequential j-order chain computed with __dsub_rn/__dmul_rn/__dadd_rn (no FMA
+//     contraction, bit-identical to the reference), strict-< chain per group, groups merged
+//     in ascending order => identical to the single chain;
+//   * bucket-reduce: the CTA's sums (k x d) and counts (k) sit in shared memory; each (c, j)
+//     cell has exactly one owner thread, which folds the tile's samples in order — no
+//     atomics, deterministic;
+//   * per-CTA partial activation records go to the workspace, and a finalize kernel combines
+//     them in ascending CTA order (SPEC.md:648's ascending-chunk combine, CTA = chunk).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace dlx {
+
+constexpr int kThreads = 256;
+constexpr int kCpt = 8;  // centroids per register chunk
+
+struct KmeansPlan {
+  int groups;        // centroid groups per CTA (power of two, <= 8)
+  int tile;          // samples per tile = kThreads / groups
+  int cpg;           // centroids per group
+  int xstride;       // padded row stride (doubles) of the staged x tile (odd => fewer conflicts)
+  int residues;      // bucket-reduce owners per column
+  size_t smem;       // dynamic shared memory bytes
+  int grid;          // persistent CTAs
+};
+
+static bool make_plan(int64_t n, int d, int k, KmeansPlan* p) {
+  int g = (k + kCpt - 1) / kCpt;
+  int groups = 1;
+  while (groups < g && groups < 8) groups <<= 1;
+  p->groups = groups;
+  p->tile = kThreads / groups;
+  p->cpg = (k + groups - 1) / groups;
+  p->xstride = d | 1;
+  p->residues = std::max(1, kThreads / d);
+  size_t smem = 0;
+  smem += static_cast<size_t>(k) * d * sizeof(double);           // mu
+  smem += static_cast<size_t>(k) * d * sizeof(double);           // sums
+  smem += static_cast<size_t>(p->tile) * p->xstride * sizeof(double);  // x tile
+  smem += static_cast<size_t>(groups) * p->tile * (sizeof(double) + sizeof(int));  // per-group best
+  smem += static_cast<size_t>(k) * sizeof(long long);            // counts
+  smem += static_cast<size_t>(p->tile) * sizeof(int);            // tile assignments
+  smem += 64;
+  p->smem = smem;
+  if (smem > 227 * 1024) return false;
+  int per_sm = static_cast<int>((227 * 1024) / (smem + 1024));
+  per_sm = std::max(1, std::min(per_sm, 4));
+  const int64_t tiles = (n + p->tile - 1) / p->tile;
+  int64_t grid = static_cast<int64_t>(sm_count()) * per_sm;
+  if (grid > tiles) grid = std::max<int64_t>(1, tiles);
+  p->grid = static_cast<int>(grid);
+  return true;
+}
+
+__global__ void __launch_bounds__(kThreads)
+kmeans_direct_kernel(const double* __restrict__ x, int64_t n, int d, int k,
+                     const double* __restrict__ mu, int32_t* __restrict__ assign,
+                     long long* __restrict__ part_counts, double* __restrict__ part_sums,
+                     KmeansPlan p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* mu_s = reinterpret_cast<double*>(smem_raw);
+  double* sums_s = mu_s + static_cast<size_t>(k) * d;
+  double* x_s = sums_s + static_cast<size_t>(k) * d;
+  double* best_s = x_s + static_cast<size_t>(p.tile) * p.xstride;
+  int* bidx_s = reinterpret_cast<int*>(best_s + p.groups * p.tile);
+  long long* counts_s = reinterpret_cast<long long*>(
+      (reinterpret_cast<uintptr_t>(bidx_s + p.groups * p.tile) + 7) & ~uintptr_t(7));
+  int* tassign_s = reinterpret_cast<int*>(counts_s + k);
+
+  const int tid = threadIdx.x;
+  const int kd = k * d;
+  for (int e = tid; e < kd; e += kThreads) {
+    mu_s[e] = mu[e];
+    sums_s[e] = 0.0;
+  }
+  for (int c = tid; c < k; c += kThreads) counts_s[c] = 0;
+
+  const int g = tid / p.tile;
+  const int s = tid % p.tile;
+  const int c_lo = g * p.cpg;
+  const int c_hi = min(k, c_lo + p.cpg);
+  const int64_t ntiles = (n + p.tile - 1) / p.tile;
+
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t i0 = t * p.tile;
+    const int rows = static_cast<int>(n - i0 < p.tile ? n - i0 : p.tile);
+    __syncthreads();  // previous tile fully consumed (also orders the mu/sums init)
+    // stage x tile: rows*d contiguous doubles -> padded rows
+    const double* xt = x + i0 * d;
+    const int tot = rows * d;
+    for (int e = tid; e < tot; e += kThreads) {
+      const int r = e / d, j = e - r * d;
+      x_s[r * p.xstride + j] = __ldg(xt + e);
+    }
+    __syncthreads();
+
+    double best = 1e300;
+    int bi = -1;
+    if (s < rows) {
+      const double* xr = x_s + s * p.xstride;
+      for (int c0 = c_lo; c0 < c_hi; c0 += kCpt) {
+        double acc[kCpt];
+#pragma unroll
+        for (int u = 0; u < kCpt; ++u) acc[u] = 0.0;
+        const int cl = min(kCpt, c_hi - c0);
+        if (cl == kCpt) {
+          for (int j = 0; j < d; ++j) {
+            const double xv = xr[j];
+#pragma unroll
+            for (int u = 0; u < kCpt; ++u) {
+              const double diff = __dsub_rn(xv, mu_s[(c0 + u) * d + j]);
+              acc[u] = __dadd_rn(acc[u], __dmul_rn(diff, diff));
+            }
+          }
+        } else {
+          for (int j = 0; j < d; ++j) {
+            const double xv = xr[j];
+#pragma unroll
+            for (int u = 0; u < kCpt; ++u) {
+              if (u < cl) {
+                const double diff = __dsub_rn(xv, mu_s[(c0 + u) * d + j]);
+                acc[u] = __dadd_rn(acc[u], __dmul_rn(diff, diff));
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kCpt; ++u)
+          if (u < cl && acc[u] < best) {
+            best = acc[u];
+            bi = c0 + u;
+          }
+      }
+    }
+    best_s[g * p.tile + s] = best;
+    bidx_s[g * p.tile + s] = bi;
+    __syncthreads();
+    if (g == 0 && s < rows) {
+      // merge group chains in ascending centroid order: global chain from (1e300, 0)
+      double b = 1e300;
+      int idx = 0;
+      for (int gg = 0; gg < p.groups; ++gg) {
+        const double v = best_s[gg * p.tile + s];
+        if (v < b) {
+          b = v;
+          idx = bidx_s[gg * p.tile + s];
+        }
+      }
+      tassign_s[s] = idx;
+      if (assign) assign[i0 + s] = idx;
+    }
+    __syncthreads();
+    // bucket-reduce: cell (c, j) with c % residues == r is owned by column thread r*d + j
+    for (int col = tid; col < d * p.residues; col += kThreads) {
+      const int r = col / d, j = col - r * d;
+      for (int q = 0; q < rows; ++q) {
+        const int a = tassign_s[q];
+        if (a % p.residues == r) {
+          sums_s[a * d + j] += x_s[q * p.xstride + j];
+          if (j == 0) counts_s[a] += 1;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  double* ps = part_sums + static_cast<size_t>(blockIdx.x) * kd;
+  for (int e = tid; e < kd; e += kThreads) ps[e] = sums_s[e];
+  long long* pc = part_counts + static_cast<size_t>(blockIdx.x) * k;
+  for (int c = tid; c < k; c += kThreads) pc[c] = counts_s[c];
+}
+
+// Ascending-CTA combine of the partial activation records.
+__global__ void kmeans_finalize_kernel(const long long* __restrict__ part_counts,
+                                       const double* __restrict__ part_sums, int parts, int k,
+                                       int d, long long* __restrict__ counts,
+                                       double* __restrict__ sums) {
+  const int kd = k * d;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kd + k; e += gridDim.x * blockDim.x) {
+    if (e < kd) {
+      double acc = part_sums[e];
+      for (int b = 1; b < parts; ++b) acc += part_sums[static_cast<size_t>(b) * kd + e];
+      sums[e] = acc;
+    } else {
+      const int c = e - kd;
+      long long acc = 0;
+      for (int b = 0; b < parts; ++b) acc += part_counts[static_cast<size_t>(b) * k + c];
+      counts[c] = acc;
+    }
+  }
+}
+
+__global__ void kmeans_update_kernel(const long long* __restrict__ counts,
+                                     const double* __restrict__ sums, int k, int d,
+                                     double* __restrict__ mu) {
+  const int kd = k * d;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kd; e += gridDim.x * blockDim.x) {
+    const int c = e / d;
+    mu[e] = sums[e] / static_cast<double>(counts[c]);  // IEEE: 0/0 -> NaN, no trap
+  }
+}
+
+// Screened tcgen05 path (kmeans_screened.cu).  Returns DLX_ERR_GENERATION when the shape
+// is outside its plan so AUTO can fall back to the direct kernel.
+int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double* mu,
+                         int32_t* assign, long long* counts, double* sums, void* ws,
+                         size_t ws_bytes, cudaStream_t stream, bool probe_only);
+size_t kmeans_screened_workspace_bytes(int64_t n, int d, int k);
+
+static size_t direct_workspace_bytes(int64_t n, int d, int k) {
+  KmeansPlan p;
+  if (!make_plan(n, d, k, &p)) return 0;
+  Carve c(nullptr);
+  c.take<long long>(static_cast<size_t>(p.grid) * k);
+  c.take<double>(static_cast<size_t>(p.grid) * k * d);
+  return c.used + 256;
+}
+
+static int kmeans_direct_step(const double* x, int64_t n, int d, int k, const double* mu,
+                              int32_t* assign, long long* counts, double* sums, void* ws,
+                              size_t ws_bytes, cudaStream_t stream) {
+  KmeansPlan p;
+  DLX_REQUIRE(make_plan(n, d, k, &p), DLX_ERR_GENERATION,
+              "GenerationFailed: k-means k=%d d=%d exceeds the shared-memory plan", k, d);
+  Carve c(ws);
+  long long* pc = c.take<long long>(static_cast<size_t>(p.grid) * k);
+  double* psum = c.take<double>(static_cast<size_t>(p.grid) * k * d);
+  DLX_REQUIRE(c.used <= ws_bytes, DLX_ERR_ARG, "k-means workspace too small (%zu < %zu)",
+              ws_bytes, c.used);
+  DLX_CUDA(cudaFuncSetAttribute(kmeans_direct_kernel,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(p.smem)));
+  kmeans_direct_kernel<<<p.grid, kThreads, p.smem, stream>>>(x, n, d, k, mu, assign, pc, psum, p);
+  DLX_LAUNCHED("kmeans_direct_kernel");
+  const int kd = k * d;
+  kmeans_finalize_kernel<<<(kd + k + 255) / 256, 256, 0, stream>>>(pc, psum, p.grid, k, d, counts,
+                                                                  sums);
+  DLX_LAUNCHED("kmeans_finalize_kernel");
+  return DLX_OK;
+}
+
+}  // namespace dlx
+
+using namespace dlx;
+
+extern "C" {
+
+size_t dlx_kmeans_workspace_bytes(int64_t n, int32_t d, int32_t k) {
+  return std::max(direct_workspace_bytes(n, d, k), kmeans_screened_workspace_bytes(n, d, k));
+}
+
+int dlx_kmeans_step(const double* d_x, int64_t n, int32_t d, int32_t k, const double* d_mu,
+                    int32_t* d_assign, int64_t* d_counts, double* d_sums, void* d_workspace,
+                    size_t workspace_bytes, int method, dlx_stream_t stream) {
+  DLX_REQUIRE(n >= 0 && d > 0 && k > 0, DLX_ERR_ARG, "k-means: bad shape n=%lld d=%d k=%d",
+              (long long)n, d, k);
+  DLX_REQUIRE(d_mu && d_counts && d_sums && (d_x || n == 0), DLX_ERR_ARG,
+              "k-means: null buffer");
+  long long* counts = reinterpret_cast<long long*>(d_counts);
+  if (n == 0) {
+    DLX_CUDA(cudaMemsetAsync(d_counts, 0, sizeof(int64_t) * k, stream));
+    DLX_CUDA(cudaMemsetAsync(d_sums, 0, sizeof(double) * k * d, stream));
+    return DLX_OK;
+  }
+  if (method == DLX_KMEANS_SCREENED || method == DLX_KMEANS_AUTO) {
+    int rc = kmeans_screened_step(d_x, n, d, k, d_mu, d_assign, counts, d_sums, d_workspace,
+                                  workspace_bytes, stream, false);
+    if (rc != DLX_ERR_GENERATION || method == DLX_KMEANS_SCREENED) return rc;
+  }
+  return kmeans_direct_step(d_x, n, d, k, d_mu, d_assign, counts, d_sums, d_workspace,
+                            workspace_bytes, stream);
+}
+
+int dlx_kmeans_update(const int64_t* d_counts, const double* d_sums, int32_t k, int32_t d,
+                      double* d_mu, dlx_stream_t stream) {
+  DLX_REQUIRE(k > 0 && d > 0 && d_counts && d_sums && d_mu, DLX_ERR_ARG, "k-means update: bad args");
+  const int kd = k * d;
+  kmeans_update_kernel<<<(kd + 255) / 256, 256, 0, stream>>>(
+      reinterpret_cast<const long long*>(d_counts), d_sums, k, d, d_mu);
+  DLX_LAUNCHED("kmeans_update_kernel");
+  return DLX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,367 @@
+// rows.cu — row-streaming multiloops over a row-major DenseMatrix: the logistic-regression
+// gradient and GDA passes 1 and 2 (§8 a6).
+//
+// Shared device plan for the streaming families: one warp per sample row, lane l holds
+// columns {2l, 2l+1} + 64m (128-bit loads, so a d=64 fp64 row = one warp-wide load);
+// several rows in flight per warp; every reduce slot that all samples feed (gradient,
+// per-class sums) is a per-lane register accumulator, reduced across warps through shared
+// memory in ascending warp order, written as a per-CTA partial and combined across CTAs in
+// ascending order.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace dlx {
+
+constexpr int kRowThreads = 256;
+constexpr int kRowWarps = kRowThreads / 32;
+constexpr int kMaxM = 4;  // 128-bit column groups per lane => d <= 64*kMaxM
+
+static int row_grid(int64_t n) {
+  int64_t grid = static_cast<int64_t>(sm_count()) * 4;
+  const int64_t need = (n + kRowWarps - 1) / kRowWarps;
+  return static_cast<int>(std::max<int64_t>(1, std::min(grid, need)));
+}
+
+// CTA-wide ascending-warp reduction of per-lane column accumulators into out[d].
+template <int M>
+__device__ void cta_reduce_columns(double (&acc)[M][2], int d, double* red_s, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int j = 64 * m + 2 * lane;
+    if (j < d) red_s[warp * d + j] = acc[m][0];
+    if (j + 1 < d) red_s[warp * d + j + 1] = acc[m][1];
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < d; j += kRowThreads) {
+    double v = red_s[j];
+    for (int w = 1; w < kRowWarps; ++w) v += red_s[w * d + j];
+    out[j] = v;
+  }
+  __syncthreads();
+}
+
+__global__ void combine_parts_kernel(const double* __restrict__ parts, int nparts, int width,
+                                     double* __restrict__ out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < width; e += gridDim.x * blockDim.x) {
+    double v = parts[e];
+    for (int p = 1; p < nparts; ++p) v += parts[static_cast<size_t>(p) * width + e];
+    out[e] = v;
+  }
+}
+
+__global__ void combine_parts_ll_kernel(const long long* __restrict__ parts, int nparts,
+                                        long long* __restrict__ out) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    long long v = 0;
+    for (int p = 0; p < nparts; ++p) v += parts[p];
+    *out = v;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// logistic regression: g_j = sum_i (sigmoid(theta . x_i) - y_i) x_ij
+template <int M>
+__global__ void __launch_bounds__(kRowThreads)
+logreg_grad_kernel(const double* __restrict__ x, const long long* __restrict__ y, int64_t n,
+                   int d, const double* __restrict__ theta, double* __restrict__ parts) {
+  extern __shared__ double red_s[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double th[M][2], acc[M][2];
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int j = 64 * m + 2 * lane;
+    th[m][0] = j < d ? theta[j] : 0.0;
+    th[m][1] = j + 1 < d ? theta[j + 1] : 0.0;
+    acc[m][0] = acc[m][1] = 0.0;
+  }
+  const int64_t W = static_cast<int64_t>(gridDim.x) * kRowWarps;
+  constexpr int R = 4;  // rows in flight per warp
+  for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * kRowWarps + warp; i0 < n; i0 += R * W) {
+    double2 v[R][M];
+    double yv[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t i = i0 + r * W;
+      yv[r] = i < n ? static_cast<double>(__ldg(y + i)) : 0.0;
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const int j = 64 * m + 2 * lane;
+        v[r][m] = (i < n && j < d) ? ld_stream_f64x2(x + i * d + j) : make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t i = i0 + r * W;
+      double z = 0.0;
+#pragma unroll
+      for (int m = 0; m < M; ++m) z += th[m][0] * v[r][m].x + th[m][1] * v[r][m].y;
+      z = warp_sum(z);
+      const double h = 1.0 / (1.0 + exp(-z));
+      const double res = (i < n) ? h - yv[r] : 0.0;
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        acc[m][0] += res * v[r][m].x;
+        acc[m][1] += res * v[r][m].y;
+      }
+    }
+  }
+  cta_reduce_columns<M>(acc, d, red_s, parts + static_cast<size_t>(blockIdx.x) * d);
+}
+
+// ---------------------------------------------------------------------------------------
+// GDA pass 1: n1 = #{y == 1}, sum_c[j] = sum_{y_i == c} x_ij  (c in {0, 1})
+template <int M>
+__global__ void __launch_bounds__(kRowThreads)
+gda_pass1_kernel(const double* __restrict__ x, const long long* __restrict__ y, int64_t n, int d,
+                 double* __restrict__ parts0, double* __restrict__ parts1,
+                 long long* __restrict__ parts_n1) {
+  extern __shared__ double red_s[];
+  __shared__ long long n1_s[kRowWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double a0[M][2], a1[M][2];
+#pragma unroll
+  for (int m = 0; m < M; ++m) a0[m][0] = a0[m][1] = a1[m][0] = a1[m][1] = 0.0;
+  long long n1 = 0;
+  const int64_t W = static_cast<int64_t>(gridDim.x) * kRowWarps;
+  constexpr int R = 4;
+  for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * kRowWarps + warp; i0 < n; i0 += R * W) {
+    double2 v[R][M];
+    long long yv[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t i = i0 + r * W;
+      yv[r] = i < n ? __ldg(y + i) : -1;
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const int j = 64 * m + 2 * lane;
+        v[r][m] = (i < n && j < d) ? ld_stream_f64x2(x + i * d + j) : make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (yv[r] == 1) {
+        n1 += 1;
+#pragma unroll
+        for (int m = 0; m < M; ++m) { a1[m][0] += v[r][m].x; a1[m][1] += v[r][m].y; }
+      } else if (yv[r] == 0) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) { a0[m][0] += v[r][m].x; a0[m][1] += v[r][m].y; }
+      }
+    }
+  }
+  if (lane == 0) n1_s[warp] = n1;  // every lane counted the same rows
+  cta_reduce_columns<M>(a0, d, red_s, parts0 + static_cast<size_t>(blockIdx.x) * d);
+  cta_reduce_columns<M>(a1, d, red_s, parts1 + static_cast<size_t>(blockIdx.x) * d);
+  if (threadIdx.x == 0) {
+    long long t = 0;
+    for (int w = 0; w < kRowWarps; ++w) t += n1_s[w];
+    parts_n1[blockIdx.x] = t;
+  }
+}
+
+__global__ void gda_means_kernel(const long long* __restrict__ n1p, const double* __restrict__ s0,
+                                 const double* __restrict__ s1, long long n_total, int d,
+                                 double* __restrict__ mu0, double* __restrict__ mu1) {
+  const long long n1 = *n1p;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < d; j += gridDim.x * blockDim.x) {
+    mu0[j] = s0[j] / static_cast<double>(n_total - n1);
+    mu1[j] = s1[j] / static_cast<double>(n1);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// GDA pass 2: S[a][b] = sum_i (x_ia - mu_{y_i,a}) (x_ib - mu_{y_i,b}).
+// CTA tile of kTs centred rows in shared memory; the 16x16 thread grid owns B x B output
+// blocks (register tiles), one fp64 FMA per (sample, cell).
+constexpr int kTs = 32;
+
+template <int B>
+__global__ void __launch_bounds__(kRowThreads)
+gda_pass2_kernel(const double* __restrict__ x, const long long* __restrict__ y, int64_t n, int d,
+                 const double* __restrict__ mu0, const double* __restrict__ mu1,
+                 double* __restrict__ parts) {
+  extern __shared__ double sm[];
+  const int D = 16 * B;           // padded dimension
+  double* mu_s = sm;              // 2 * D
+  double* diff_s = sm + 2 * D;    // kTs * D
+  const int tid = threadIdx.x;
+  for (int j = tid; j < 2 * D; j += kRowThreads) {
+    const int c = j / D, jj = j - c * D;
+    mu_s[j] = jj < d ? (c ? mu1[jj] : mu0[jj]) : 0.0;
+  }
+  const int ta = tid >> 4, tb = tid & 15;
+  double acc[B][B];
+#pragma unroll
+  for (int u = 0; u < B; ++u)
+#pragma unroll
+    for (int v = 0; v < B; ++v) acc[u][v] = 0.0;
+  const int64_t ntiles = (n + kTs - 1) / kTs;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t i0 = t * kTs;
+    __syncthreads();
+    for (int e = tid; e < kTs * D; e += kRowThreads) {
+      const int r = e / D, j = e - r * D;
+      const int64_t i = i0 + r;
+      double v = 0.0;
+      if (i < n && j < d) {
+        const long long yy = __ldg(y + i);
+        v = __ldg(x + i * d + j) - mu_s[(yy == 1 ? D : 0) + j];
+      }
+      diff_s[r * D + j] = v;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int r = 0; r < kTs; ++r) {
+      double da[B], db[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        da[u] = diff_s[r * D + ta * B + u];
+        db[u] = diff_s[r * D + tb * B + u];
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u)
+#pragma unroll
+        for (int v = 0; v < B; ++v) acc[u][v] = fma(da[u], db[v], acc[u][v]);
+    }
+  }
+  double* out = parts + static_cast<size_t>(blockIdx.x) * d * d;
+#pragma unroll
+  for (int u = 0; u < B; ++u)
+#pragma unroll
+    for (int v = 0; v < B; ++v) {
+      const int a = ta * B + u, b = tb * B + v;
+      if (a < d && b < d) out[a * d + b] = acc[u][v];
+    }
+}
+
+}  // namespace dlx
+
+using namespace dlx;
+
+namespace {
+
+int m_for(int d) { return (d + 63) / 64; }
+
+template <template <int> class K>
+struct Dispatch;
+
+int gda2_grid(int64_t n) {
+  int64_t grid = static_cast<int64_t>(sm_count()) * 2;
+  const int64_t tiles = (n + kTs - 1) / kTs;
+  return static_cast<int>(std::max<int64_t>(1, std::min(grid, tiles)));
+}
+
+int gda2_b(int d) {
+  if (d <= 16) return 1;
+  if (d <= 32) return 2;
+  if (d <= 64) return 4;
+  if (d <= 128) return 8;
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t dlx_logreg_workspace_bytes(int64_t n, int32_t d) {
+  return static_cast<size_t>(row_grid(n)) * d * sizeof(double) + 256;
+}
+
+int dlx_logreg_grad(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
+                    const double* d_theta, double* d_grad, void* d_workspace,
+                    size_t workspace_bytes, dlx_stream_t stream) {
+  DLX_REQUIRE(n >= 0 && d > 0, DLX_ERR_ARG, "logreg: bad shape");
+  DLX_REQUIRE(d % 2 == 0 && m_for(d) <= kMaxM, DLX_ERR_GENERATION,
+              "GenerationFailed: logreg needs even d <= %d (got %d)", 64 * kMaxM, d);
+  const int grid = row_grid(n);
+  const size_t need = static_cast<size_t>(grid) * d * sizeof(double);
+  DLX_REQUIRE(d_workspace && workspace_bytes >= need, DLX_ERR_ARG, "logreg: workspace too small");
+  double* parts = static_cast<double*>(d_workspace);
+  const size_t smem = static_cast<size_t>(kRowWarps) * d * sizeof(double);
+  const long long* y = reinterpret_cast<const long long*>(d_y);
+  switch (m_for(d)) {
+    case 1: logreg_grad_kernel<1><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, d_theta, parts); break;
+    case 2: logreg_grad_kernel<2><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, d_theta, parts); break;
+    case 3: logreg_grad_kernel<3><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, d_theta, parts); break;
+    default: logreg_grad_kernel<4><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, d_theta, parts); break;
+  }
+  DLX_LAUNCHED("logreg_grad_kernel");
+  combine_parts_kernel<<<(d + 127) / 128, 128, 0, stream>>>(parts, grid, d, d_grad);
+  DLX_LAUNCHED("combine_parts_kernel");
+  return DLX_OK;
+}
+
+size_t dlx_gda_workspace_bytes(int64_t n, int32_t d) {
+  const size_t p1 = static_cast<size_t>(row_grid(n)) * (2 * d * sizeof(double) + sizeof(long long)) + 1024;
+  const size_t p2 = static_cast<size_t>(gda2_grid(n)) * d * d * sizeof(double) + 256;
+  return std::max(p1, p2);
+}
+
+int dlx_gda_pass1(const double* d_x, const int64_t* d_y, int64_t n, int32_t d, int64_t* d_n1,
+                  double* d_sum0, double* d_sum1, void* d_workspace, size_t workspace_bytes,
+                  dlx_stream_t stream) {
+  DLX_REQUIRE(n >= 0 && d > 0, DLX_ERR_ARG, "gda: bad shape");
+  DLX_REQUIRE(d % 2 == 0 && m_for(d) <= kMaxM, DLX_ERR_GENERATION,
+              "GenerationFailed: gda needs even d <= %d (got %d)", 64 * kMaxM, d);
+  const int grid = row_grid(n);
+  Carve c(d_workspace);
+  double* p0 = c.take<double>(static_cast<size_t>(grid) * d);
+  double* p1 = c.take<double>(static_cast<size_t>(grid) * d);
+  long long* pn = c.take<long long>(grid);
+  DLX_REQUIRE(d_workspace && c.used <= workspace_bytes, DLX_ERR_ARG, "gda: workspace too small");
+  const size_t smem = static_cast<size_t>(kRowWarps) * d * sizeof(double);
+  const long long* y = reinterpret_cast<const long long*>(d_y);
+  switch (m_for(d)) {
+    case 1: gda_pass1_kernel<1><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, p0, p1, pn); break;
+    case 2: gda_pass1_kernel<2><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, p0, p1, pn); break;
+    case 3: gda_pass1_kernel<3><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, p0, p1, pn); break;
+    default: gda_pass1_kernel<4><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, p0, p1, pn); break;
+  }
+  DLX_LAUNCHED("gda_pass1_kernel");
+  combine_parts_kernel<<<(d + 127) / 128, 128, 0, stream>>>(p0, grid, d, d_sum0);
+  combine_parts_kernel<<<(d + 127) / 128, 128, 0, stream>>>(p1, grid, d, d_sum1);
+  combine_parts_ll_kernel<<<1, 32, 0, stream>>>(pn, grid, reinterpret_cast<long long*>(d_n1));
+  DLX_LAUNCHED("gda combine");
+  return DLX_OK;
+}
+
+int dlx_gda_means(const int64_t* d_n1, const double* d_sum0, const double* d_sum1,
+                  int64_t n_total, int32_t d, double* d_mu0, double* d_mu1, dlx_stream_t stream) {
+  DLX_REQUIRE(d > 0, DLX_ERR_ARG, "gda means: bad d");
+  gda_means_kernel<<<(d + 127) / 128, 128, 0, stream>>>(
+      reinterpret_cast<const long long*>(d_n1), d_sum0, d_sum1, n_total, d, d_mu0, d_mu1);
+  DLX_LAUNCHED("gda_means_kernel");
+  return DLX_OK;
+}
+
+int dlx_gda_pass2(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
+                  const double* d_mu0, const double* d_mu1, double* d_scatter, void* d_workspace,
+                  size_t workspace_bytes, dlx_stream_t stream) {
+  DLX_REQUIRE(n >= 0 && d > 0, DLX_ERR_ARG, "gda: bad shape");
+  const int B = gda2_b(d);
+  DLX_REQUIRE(B > 0, DLX_ERR_GENERATION, "GenerationFailed: gda pass 2 needs d <= 128 (got %d)", d);
+  const int grid = gda2_grid(n);
+  const size_t need = static_cast<size_t>(grid) * d * d * sizeof(double);
+  DLX_REQUIRE(d_workspace && workspace_bytes >= need, DLX_ERR_ARG, "gda: workspace too small");
+  double* parts = static_cast<double*>(d_workspace);
+  const size_t smem = static_cast<size_t>(2 + kTs) * 16 * B * sizeof(double);
+  const long long* y = reinterpret_cast<const long long*>(d_y);
+  switch (B) {
+    case 1: gda_pass2_kernel<1><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, d_mu0, d_mu1, parts); break;
+    case 2: gda_pass2_kernel<2><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, d_mu0, d_mu1, parts); break;
+    case 4: gda_pass2_kernel<4><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, d_mu0, d_mu1, parts); break;
+    default: gda_pass2_kernel<8><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, d_mu0, d_mu1, parts); break;
+  }
+  DLX_LAUNCHED("gda_pass2_kernel");
+  const int dd = d * d;
+  combine_parts_kernel<<<(dd + 255) / 256, 256, 0, stream>>>(parts, grid, dd, d_scatter);
+  DLX_LAUNCHED("combine_parts_kernel");
+  return DLX_OK;
+}
+
+int dlx_axpy_inplace(double* d_theta, const double* d_grad, double alpha, int64_t n,
+                     dlx_stream_t stream);
+
+}  // extern "C"

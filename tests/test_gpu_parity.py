@@ -1,0 +1,246 @@
+"""GPU parity: every CUDA family against the CPU oracle on the same seeded inputs, through the
+C ABI.  Bit-exact for integer / index results (assignments, counts, GroupBy); rtol 1e-9 for
+fp64 sums (north-star tolerance; the reduction order differs from the sequential fold)."""
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-9  # fp64 sums (north_star: "1e-9 fp64")
+
+
+@pytest.fixture(scope="module")
+def ml():
+    assert torch.cuda.is_available()
+    from paper_1109_0778_b200 import multiloops
+    return multiloops
+
+
+def dev_units(ml, n, d, seed=1, first=0):
+    return ml.rng_units(n * d, seed=seed, first_draw=first).view(n, d)
+
+
+# ---- Rng ------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n,seed,first", [(1, 1, 0), (1000, 1, 0), (123457, 42, 99), (3_000_001, 7, 10 ** 9)])
+def test_rng_bit_identical(ml, n, seed, first):
+    assert np.array_equal(ml.rng_units(n, seed=seed, first_draw=first).cpu().numpy(), O.rng_units(seed, first, n))
+    for b in (2, 64, 65536):
+        assert np.array_equal(ml.rng_ints(n, b, seed=seed, first_draw=first).cpu().numpy(),
+                              O.rng_ints(seed, first, n, b))
+
+
+# ---- k-means ----------------------------------------------------------------------------------
+
+def check_step(ml, x, mu, method=0):
+    xh, muh = x.cpu().numpy(), mu.cpu().numpy()
+    a, c, s = ml.kmeans_step(x, mu, method=method)
+    a_ref, c_ref, s_ref = O.kmeans_step(np.ascontiguousarray(xh), mu.shape[0], muh)
+    assert np.array_equal(a.cpu().numpy().astype(np.int64), a_ref)
+    assert np.array_equal(c.cpu().numpy(), c_ref)
+    np.testing.assert_allclose(s.cpu().numpy(), s_ref, rtol=RTOL, atol=0)
+    return a_ref, c_ref, s_ref
+
+
+@pytest.mark.parametrize("method", [0, 1])
+def test_c1_stepwise_ten_iterations(ml, golden, method):
+    """at every iteration run the GPU step from the oracle's centroids."""
+    g = golden["c1_kmeans"]
+    x = dev_units(ml, g["n"], g["d"])
+    mu = x[: g["k"]].clone()
+    for it in range(g["iters"]):
+        _, c_ref, s_ref = check_step(ml, x, mu, method)
+        assert c_ref.tolist() == g["counts"][it]
+        mu = torch.from_numpy(O.kmeans_update(c_ref, s_ref)).cuda()
+
+
+def test_c1_free_running(ml, golden):
+    from paper_1109_0778_b200.programs import KMeansProgram
+    g = golden["c1_kmeans"]
+    x = dev_units(ml, g["n"], g["d"])
+    prog = KMeansProgram(x, g["k"], x[: g["k"]])
+    for it in range(g["iters"]):
+        prog.step()
+        assert prog.counts.cpu().tolist() == g["counts"][it]
+    mu = prog.mu.cpu().numpy()
+    assert O.format_double(mu[0, 0]) == g["mu00"][-1] or abs(mu[0, 0] - float(g["mu00"][-1])) < 1e-12
+    text = O.kmeans_canonical_text(prog.counts.cpu().numpy(), mu)
+    print("C1 GPU free-running text sha256:", hashlib.sha256(text.encode()).hexdigest())
+
+
+def test_kmeans_graph_equals_eager(ml):
+    from paper_1109_0778_b200.programs import KMeansProgram
+    x = dev_units(ml, 50_000, 32, seed=5)
+    e = KMeansProgram(x, 16, x[:16]).run(4)
+    gph = KMeansProgram(x, 16, x[:16]).capture().run(4)
+    assert torch.equal(e.mu, gph.mu) and torch.equal(e.counts, gph.counts)
+
+
+@pytest.mark.parametrize("n,d,k", [(1, 16, 8), (37, 5, 3), (1000, 64, 64), (5000, 33, 17), (3000, 130, 10),
+                                   (2048, 16, 1), (4099, 64, 64), (10_000, 2, 70), (777, 96, 24)])
+@pytest.mark.parametrize("method", [0, 1])
+def test_kmeans_shapes(ml, n, d, k, method):
+    x = dev_units(ml, n, d, seed=n + d + k)
+    mu = dev_units(ml, k, d, seed=99)
+    check_step(ml, x, mu, method)
+
+
+def test_kmeans_ties_and_nan(ml):
+    x = dev_units(ml, 4000, 16, seed=3)
+    mu = x[:8].clone()
+    mu[5] = mu[2]          # duplicate centroid: lower index must win every tie
+    mu[7] = float("nan")   # empty-cluster centroid: never wins
+    check_step(ml, x, mu)
+    check_step(ml, x, torch.full_like(mu, float("nan")))   # all NaN -> chain start index 0
+    xi = torch.zeros(64, 4, dtype=torch.float64, device="cuda")
+    check_step(ml, xi, torch.zeros(3, 4, dtype=torch.float64, device="cuda"))  # exact ties
+
+
+def test_kmeans_empty_cluster_update(ml):
+    counts = torch.tensor([3, 0], dtype=torch.int64, device="cuda")
+    sums = torch.tensor([[1.0, 2.0], [0.0, 0.0]], dtype=torch.float64, device="cuda")
+    mu = ml.kmeans_update(counts, sums).cpu().numpy()
+    assert np.isnan(mu[1]).all() and mu[0].tolist() == [1.0 / 3.0, 2.0 / 3.0]
+
+
+def test_c4_first_two_iterations(ml, golden, oracle_hashes):
+    g = golden["c4_kmeans"]
+    x = dev_units(ml, g["n"], g["d"])
+    mu = x[: g["k"]].clone()
+    xh = x.cpu().numpy()
+    for it in range(2):
+        a, c, s = ml.kmeans_step(x, mu)
+        a_h = a.cpu().numpy().astype(np.int64)
+        assert hex(O.fnv64w(a_h)) == oracle_hashes["c4_assign_fnv64w"][it]
+        assert c.cpu().tolist()[:4] == g["counts_prefix"][it]
+        sums = s.cpu().numpy()
+        np.testing.assert_allclose(sums[0, 0], float(g["sum_c0_d0"][it]), rtol=RTOL)
+        # the oracle's sums for the same assignments (chunked; rtol) drive the next step
+        _, c_ref, s_ref = O.kmeans_step(xh, g["k"], mu.cpu().numpy(), workers=O.threads(), chunks=4 * O.threads())
+        np.testing.assert_allclose(sums, s_ref, rtol=RTOL)
+        mu = torch.from_numpy(O.kmeans_update(c_ref, s_ref)).cuda()
+
+
+# ---- GroupBy ------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n,K", [(1, 64), (1001, 64), (1_000_003, 64), (1_000_000, 4096), (999_999, 65536),
+                                 (500_000, 200_000), (100, 1)])
+def test_groupby(ml, n, K):
+    keys = ml.rng_ints(n, K, seed=K)
+    assert np.array_equal(ml.groupby_count(keys, K).cpu().numpy(), O.groupby_count(keys.cpu().numpy(), K))
+
+
+def test_groupby_out_of_range(ml):
+    keys = torch.tensor([0, 1, 1, -1, 5, 4, 2, 1 << 40, 3], dtype=torch.int64, device="cuda")
+    assert ml.groupby_count(keys, 5).cpu().tolist() == [1, 2, 1, 1, 1]
+    assert ml.groupby_count(keys, 300_000).cpu().numpy()[:6].tolist() == [1, 2, 1, 1, 1, 1]
+
+
+@pytest.mark.parametrize("K", ["64", "4096", "65536"])
+def test_c5_groupby(ml, golden, oracle_hashes, K):
+    g = golden["c5_groupby"]["by_k"][K]
+    keys = ml.rng_ints(golden["c5_groupby"]["n"], int(K), seed=1)
+    c = ml.groupby_count(keys, int(K)).cpu().numpy()
+    assert [c[0], c[-1], c.min(), c.max()] == [g["first"], g["last"], g["min"], g["max"]]
+    assert hex(O.fnv64w(c)) == oracle_hashes["c5_counts_fnv64w"][K]
+    del keys
+    torch.cuda.empty_cache()
+
+
+# ---- logistic regression --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n,d", [(1, 64), (1000, 64), (1_048_576, 64), (3001, 2), (5000, 130), (4096, 256)])
+def test_logreg_grad(ml, n, d):
+    x = dev_units(ml, n, d, seed=4)
+    y = ml.rng_ints(n, 2, seed=4, first_draw=n * d)
+    th = torch.linspace(-0.3, 0.3, d, dtype=torch.float64, device="cuda")
+    g = ml.logreg_grad(x, y, th).cpu().numpy()
+    ref = O.logreg_grad(x.cpu().numpy(), y.cpu().numpy(), th.cpu().numpy(), workers=O.threads(), chunks=4 * O.threads())
+    np.testing.assert_allclose(g, ref, rtol=RTOL, atol=1e-9 * np.abs(ref).max())
+
+
+def test_c2_logreg_bgd_20_iterations(ml):
+    from paper_1109_0778_b200.programs import LogRegProgram
+    n, d, iters = 1_048_576, 64, 20
+    alpha = 1.0 / n
+    x = dev_units(ml, n, d)
+    y = ml.rng_ints(n, 2, seed=1, first_draw=n * d)
+    prog = LogRegProgram(x, y, torch.zeros(d, dtype=torch.float64, device="cuda"), alpha).capture()
+    xh, yh = x.cpu().numpy(), y.cpu().numpy()
+    th = np.zeros(d)
+    for _ in range(iters):
+        prog.step()
+        th = th - alpha * O.logreg_grad(xh, yh, th, workers=O.threads(), chunks=4 * O.threads())
+    np.testing.assert_allclose(prog.theta.cpu().numpy(), th, rtol=1e-9, atol=1e-13)
+
+
+# ---- GDA ---------------------------------------------------------------------------------------------
+
+def test_c3_gda(ml, golden):
+    g = golden["c3_gda"]
+    n, d = g["n"], g["d"]
+    x = dev_units(ml, n, d)
+    y = ml.rng_ints(n, 2, seed=1, first_draw=n * d)
+    n1, mu0, mu1, S = ml.gda(x, y)
+    assert int(n1.item()) == g["n1"]
+    mu0, mu1, S = mu0.cpu().numpy(), mu1.cpu().numpy(), S.cpu().numpy()
+    np.testing.assert_allclose(mu0[0], float(g["mu0_0"]), rtol=RTOL)
+    np.testing.assert_allclose(mu1[0], float(g["mu1_0"]), rtol=RTOL)
+    np.testing.assert_allclose([S[0, 0], S[0, 1], S[63, 63]], [float(g["S00"]), float(g["S01"]), float(g["S6363"])],
+                               rtol=RTOL)
+    xh, yh = x.cpu().numpy(), y.cpu().numpy()
+    n1r, s0, s1 = O.gda_pass1(xh, yh, workers=O.threads(), chunks=4 * O.threads())
+    m0, m1 = s0 / float(n - n1r), s1 / float(n1r)
+    np.testing.assert_allclose(mu0, m0, rtol=RTOL)
+    np.testing.assert_allclose(mu1, m1, rtol=RTOL)
+    Sr = O.gda_pass2(xh, yh, m0, m1, workers=O.threads(), chunks=4 * O.threads())
+    np.testing.assert_allclose(S, Sr, rtol=RTOL, atol=1e-9 * np.abs(Sr).max())
+
+
+@pytest.mark.parametrize("n,d", [(1, 2), (999, 16), (5000, 30), (4097, 100), (2000, 128)])
+def test_gda_shapes(ml, n, d):
+    x = dev_units(ml, n, d, seed=8)
+    y = ml.rng_ints(n, 2, seed=8, first_draw=n * d)
+    n1, mu0, mu1, S = ml.gda(x, y)
+    xh, yh = x.cpu().numpy(), y.cpu().numpy()
+    n1r, s0, s1 = O.gda_pass1(xh, yh)
+    assert int(n1.item()) == n1r
+    with np.errstate(all="ignore"):
+        m0, m1 = s0 / float(n - n1r), s1 / float(n1r)
+    np.testing.assert_allclose(mu0.cpu().numpy(), m0, rtol=RTOL)
+    np.testing.assert_allclose(mu1.cpu().numpy(), m1, rtol=RTOL)
+    if np.isfinite(m0).all() and np.isfinite(m1).all():
+        Sr = O.gda_pass2(xh, yh, m0, m1)
+        np.testing.assert_allclose(S.cpu().numpy(), Sr, rtol=RTOL, atol=1e-9 * max(1.0, np.abs(Sr).max()))
+
+
+# ---- generic collect / reduce -------------------------------------------------------------------------
+
+def test_generic_families(ml):
+    n = 1_000_003
+    x = ml.rng_units(n, seed=11)
+    y = ml.rng_units(n, seed=12)
+    xh, yh = x.cpu().numpy(), y.cpu().numpy()
+    assert np.array_equal(ml.map_axpy(2.5, x, y).cpu().numpy(), O.axpy(2.5, xh, yh))   # SPEC.md:642 exact
+    np.testing.assert_allclose(ml.reduce_sum(x).item(), O.sum_f64(xh), rtol=1e-12)
+    ints = torch.arange(1, 10 ** 6 + 1, dtype=torch.int64, device="cuda")
+    assert ml.reduce_sum(ints).item() == 500000500000
+    assert ml.count_where_gt(x * 10, 7.0).item() == O.count_gt_f64(xh * 10, 7.0)
+    m, v = ml.mean_variance(x)
+    s, sq = O.sum_sumsq_f64(xh)
+    np.testing.assert_allclose([m, v], [s / n, sq / n - (s / n) ** 2], rtol=1e-9)
+    m, v = ml.mean_variance(torch.full((1000,), 0.3, dtype=torch.float64, device="cuda"))
+    assert abs(v) < 1e-12
+
+
+def test_generation_failed_is_loud(ml):
+    from paper_1109_0778_b200 import GenerationFailed
+    x = dev_units(ml, 10, 129 * 4, seed=1)   # odd-size row groups beyond the row kernel plan
+    y = ml.rng_ints(10, 2, seed=1)
+    with pytest.raises(GenerationFailed):
+        ml.logreg_grad(x, y, torch.zeros(129 * 4, dtype=torch.float64, device="cuda"))
