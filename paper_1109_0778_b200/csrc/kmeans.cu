@@ -216,6 +216,15 @@ __global__ void kmeans_update_kernel(const long long* __restrict__ counts,
   }
 }
 
+int kmeans_finalize(const long long* part_counts, const double* part_sums, int parts, int k, int d,
+                    long long* counts, double* sums, cudaStream_t stream) {
+  const int kd = k * d;
+  kmeans_finalize_kernel<<<(kd + k + 255) / 256, 256, 0, stream>>>(part_counts, part_sums, parts, k, d,
+                                                                  counts, sums);
+  DLX_LAUNCHED("kmeans_finalize_kernel");
+  return DLX_OK;
+}
+
 // Screened tcgen05 path (kmeans_screened.cu).  Returns DLX_ERR_GENERATION when the shape
 // is outside its plan so AUTO can fall back to the direct kernel.
 int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double* mu,
@@ -248,11 +257,7 @@ static int kmeans_direct_step(const double* x, int64_t n, int d, int k, const do
                                 static_cast<int>(p.smem)));
   kmeans_direct_kernel<<<p.grid, kThreads, p.smem, stream>>>(x, n, d, k, mu, assign, pc, psum, p);
   DLX_LAUNCHED("kmeans_direct_kernel");
-  const int kd = k * d;
-  kmeans_finalize_kernel<<<(kd + k + 255) / 256, 256, 0, stream>>>(pc, psum, p.grid, k, d, counts,
-                                                                  sums);
-  DLX_LAUNCHED("kmeans_finalize_kernel");
-  return DLX_OK;
+  return kmeans_finalize(pc, psum, p.grid, k, d, counts, sums, stream);
 }
 
 }  // namespace dlx

@@ -1,19 +1,511 @@
-// kmeans_screened.cu — tcgen05 screened k-means (placeholder until the kernel lands).
+// kmeans_screened.cu — the k-means fused multiloop with a tcgen05 int8 distance screen and an
+// exact fp64 recheck.  Assignments stay bit-identical to the reference argmin chain
+// (proj/src/stage.cpp:73-104 staged_if chain over the inner mk_reduce distances,
+// loops.cpp:111-174), while the per-sample work drops from k*d fp64 (x-mu)^2 chains to one
+// small integer GEMM tile plus, for the rare near-ties, a few exact chains.
+//
+// Why a screen: the direct form costs 3*N*k*d fp64 ops (2.1e11 per C4 iteration, ~11 ms at
+// the FP64 pipe peak) against 1.34 ms of HBM time.  argmin_c (x-mu_c)^2 =
+// argmin_c (|mu_c|^2 - 2 x.mu_c), and x.mu_c is a GEMM.  We compute it EXACTLY on integer
+// tensor cores for 16-bit fixed-point copies of x and mu, bound the fixed-point error
+// rigorously, and only re-evaluate the reference's own fp64 chain where the bound cannot
+// separate the best centroid from the others.
+//
+// Fixed point.  Per tile (128 samples) e_t with |x| < 2^e_t; per launch e_m with |mu| < 2^e_m
+// over finite centroids.  X = floor(x * 2^(15-e_t)) in [-2^15, 2^15), split X = 256*h + l
+// with h in s8, l in u8 (same for M from mu).  The tcgen05.mma kind::i8 products
+//   HH = sum h_x h_m,  CROSS = sum (h_x l_m + l_x h_m),  LL = sum l_x l_m
+// are exact int32 and S = 65536 HH + 256 CROSS + LL = sum_j X_j M_j exactly.
+// With x = (X + f)/sx, mu = (M + g)/sm, f,g in [0,1):
+//   x.mu * sx*sm = S + E,  E in [sum min(0,X) + sum min(0,M),  sum max(0,X) + sum max(0,M) + d]
+// so the width of E is  sum|X| + sum|M| + d.  In units U = 2^(e_t+e_m-22) the screened
+// score  T_c = floor(|mu_c|^2 / U) - 2*(256 HH + CROSS + (LL >> 8))  satisfies
+//   |mu_c|^2/U - 2 x.mu_c/U  in  [T_c - 2 r_hi, T_c + 1 - 2 r_lo],  r_hi - r_lo <= 1 + width/256,
+// and the reference's fp64 chain differs from the real distance by < 1 unit (guarded by
+// -8 <= e_m - e_t <= 2).  Hence every centroid with  T_c > min_c T_c + W,  W = 6 + ceil((sum|X|
+// + max_c sum max(0,M_c) + max_c sum max(0,-M_c) + d)/128),  has a strictly larger reference distance than some other centroid
+// and cannot be the argmin.  If exactly one centroid survives it IS the reference argmin; if
+// several survive they are re-evaluated with the reference chain (sequential j, no FMA,
+// strict <, ascending c).  Tiles with non-finite values, |exponents| > 400 or e_m - e_t
+// outside [-8, 2] run the exact chain for every centroid.  NaN / inf centroids never win the reference chain
+// and are excluded from the screen.
+//
+// Kernel shape: one persistent CTA per SM, 14 warps, warp-specialised around mbarriers:
+//   warp 0      TMA producer: 1-D bulk copies of 128-sample x tiles into a 3-stage ring
+//   warp 1      TMEM owner + MMA issuer (one thread): 8 tcgen05.mma per tile into a
+//               double-buffered 3 x 64-column int32 accumulator
+//   warps 2-5   converters: tile exponent, fixed-point split into the SW128 K-major A operand
+//   warps 6-13  epilogue + bucket-reduce: tcgen05.ld the scores, screen / recheck, then
+//               fold the tile's rows into register-resident per-centroid sums (each (c, j)
+//               cell owned by one thread, samples folded in order: deterministic, no atomics)
+#include <algorithm>
+#include <climits>
+
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace dlx {
 
-size_t kmeans_screened_workspace_bytes(int64_t, int, int) { return 0; }
+int kmeans_finalize(const long long* part_counts, const double* part_sums, int parts, int k, int d,
+                    long long* counts, double* sums, cudaStream_t stream);
 
-int kmeans_screened_step(const double*, int64_t, int, int, const double*, int32_t*, long long*,
-                         double*, void*, size_t, cudaStream_t, bool) {
-  set_error("GenerationFailed: screened k-means not built");
-  return DLX_ERR_GENERATION;
+namespace sk {
+
+using namespace sm100;
+
+constexpr int kThreads = 448;
+constexpr int kTile = 128;
+constexpr int kStages = 3;
+constexpr int kMaxD = 64;
+constexpr int kMaxK = 64;
+constexpr int kWarpProd = 0, kWarpMma = 1, kWarpC0 = 2, kWarpE0 = 6;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kAccCols = 192;
+constexpr uint32_t kXStage = kTile * kMaxD * 8;  // 64 KiB
+constexpr uint32_t kOffA = kStages * kXStage;      // 196608
+constexpr uint32_t kOffB = kOffA + kTile * 128;    // 212992
+constexpr uint32_t kOffMisc = kOffB + kMaxK * 128; // 221184
+
+struct Misc {
+  uint64_t full[kStages], sempty[kStages], cfull[kStages];
+  uint64_t a_full, a_empty, tfull[2], tempty[2];
+  unsigned long long valid;
+  uint32_t tmem_base;
+  int em, mpos, mneg, disabled;
+  uint32_t mu_maxhi;
+  int tile_e[kStages], tile_flag[kStages];
+  int absx[kStages][kTile];
+  double nmf[kMaxK];
+  int hmin[2][kTile];
+  uint32_t cmask[2][kTile];
+  int assign[kTile];
+  int counts[kMaxK];
+  uint32_t cscr[2][8];
+  unsigned int recheck;
+};
+constexpr uint32_t kSmemBytes = kOffMisc + sizeof(Misc);
+static_assert(kSmemBytes <= 232448, "shared-memory plan exceeds 227 KiB");
+
+__device__ __forceinline__ int exp_bound(uint32_t maxhi) {
+  // smallest e with |v| < 2^e for the largest |v| whose high word (sans sign) is maxhi
+  return static_cast<int>(maxhi >> 20) - 1022;
+}
+
+__device__ int exact_argmin(const double* xrow, const double* __restrict__ mu, int d,
+                            unsigned long long mask) {
+  double best = 1e300;
+  int bi = 0;
+  while (mask) {
+    const int c = __ffsll(static_cast<long long>(mask)) - 1;
+    mask &= mask - 1;
+    const double* m = mu + c * d;
+    double acc = 0.0;
+    for (int j = 0; j < d; ++j) {
+      const double diff = __dsub_rn(xrow[j], __ldg(m + j));
+      acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+    }
+    if (acc < best) {
+      best = acc;
+      bi = c;
+    }
+  }
+  return bi;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
+                       const double* __restrict__ mu, int32_t* __restrict__ assign,
+                       long long* __restrict__ part_counts, double* __restrict__ part_sums,
+                       unsigned long long* __restrict__ recheck_total) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  Misc& S = *reinterpret_cast<Misc*>(smem + kOffMisc);
+  unsigned char* A = smem + kOffA;
+  unsigned char* B = smem + kOffB;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int64_t ntiles = (n + kTile - 1) / kTile;
+  const int mtiles = static_cast<int>((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
+
+  // ---- prologue: barriers, scratch, B operand (fixed-point centroids) -----------------------
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.sempty[s], 8);
+      mbar_init(&S.cfull[s], 4);
+    }
+    mbar_init(&S.a_full, 4);
+    mbar_init(&S.a_empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&S.tfull[b], 1);
+      mbar_init(&S.tempty[b], 8);
+    }
+    S.valid = 0;
+    S.mpos = 0;
+    S.mneg = 0;
+    S.mu_maxhi = 0;
+    S.recheck = 0;
+    fence_mbar_init();
+  }
+  for (int c = tid; c < kMaxK; c += kThreads) S.counts[c] = 0;
+  __syncthreads();
+  if (tid < kMaxK) {  // per centroid: validity (all finite), max |mu| high word, |mu|^2
+    const int c = tid;
+    uint32_t mx = 0;
+    bool ok = c < k;
+    double nm = 0.0;
+    if (ok) {
+      for (int j = 0; j < d; ++j) {
+        const double v = mu[c * d + j];
+        const uint32_t hw = static_cast<uint32_t>(__double2hiint(v)) & 0x7fffffffu;
+        if (hw >= 0x7ff00000u) ok = false;
+        mx = max(mx, hw);
+        nm += v * v;
+      }
+    }
+    S.nmf[c] = nm;
+    if (ok) {
+      atomicOr(&S.valid, 1ull << c);
+      atomicMax(&S.mu_maxhi, mx);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const int em = S.mu_maxhi == 0 ? 0 : exp_bound(S.mu_maxhi);
+    S.em = em;
+    S.disabled = (em > 400 || em < -400) ? 1 : 0;
+  }
+  __syncthreads();
+  {
+    const int em = S.em;
+    const double scale = S.disabled ? 0.0 : ldexp(1.0, 15 - em);
+    const unsigned long long valid = S.valid;
+    for (int e = tid; e < kMaxK * kMaxD; e += kThreads) {
+      const int c = e / kMaxD, j = e - c * kMaxD;
+      int X = 0;
+      if (((valid >> c) & 1) && j < d) X = __double2int_rd(mu[c * d + j] * scale);
+      B[sw128_offset(c, j)] = static_cast<unsigned char>((X >> 8) & 0xff);
+      B[sw128_offset(c, 64 + j)] = static_cast<unsigned char>(X & 0xff);
+    }
+    if (tid < kMaxK && ((valid >> tid) & 1)) {
+      int pos = 0, neg = 0;
+      for (int j = 0; j < d; ++j) {
+        const int X = __double2int_rd(mu[tid * d + j] * scale);
+        pos += max(X, 0);
+        neg += max(-X, 0);
+      }
+      atomicMax(&S.mpos, pos);
+      atomicMax(&S.mneg, neg);
+    }
+  }
+  fence_proxy_async_smem();
+  if (warp == kWarpMma) tmem_alloc<kTmemCols>(&S.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = S.tmem_base;
+
+  if (warp == kWarpProd) {
+    // ======================= TMA producer =======================
+    if (lane == 0) {
+      for (int m = 0; m < mtiles; ++m) {
+        const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
+        const int s = m % kStages;
+        if (m >= kStages) mbar_wait(&S.sempty[s], ((m / kStages) - 1) & 1);
+        const int rows = static_cast<int>(n - t * kTile < kTile ? n - t * kTile : kTile);
+        const uint32_t bytes = static_cast<uint32_t>(rows) * d * 8u;
+        mbar_arrive_expect_tx(&S.full[s], bytes);
+        bulk_g2s(smem + s * kXStage, x + t * kTile * d, bytes, &S.full[s]);
+      }
+    }
+  } else if (warp == kWarpMma) {
+    // ======================= MMA issuer =======================
+    if (lane == 0) {
+      constexpr uint32_t ID_SS = idesc_i8(128, 64, 1, 1);
+      constexpr uint32_t ID_SU = idesc_i8(128, 64, 1, 0);
+      constexpr uint32_t ID_US = idesc_i8(128, 64, 0, 1);
+      constexpr uint32_t ID_UU = idesc_i8(128, 64, 0, 0);
+      const uint32_t a0 = smem_addr(A), b0 = smem_addr(B);
+      const int nk = (d + 31) / 32;
+      for (int m = 0; m < mtiles; ++m) {
+        const int b = m & 1;
+        mbar_wait(&S.a_full, m & 1);
+        if (m >= 2) mbar_wait(&S.tempty[b], ((m >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t dt = tmem + b * kAccCols;
+        for (int kk = 0; kk < nk; ++kk) {
+          const uint64_t aH = sw128_kmajor_desc(a0 + 32 * kk), aL = sw128_kmajor_desc(a0 + 64 + 32 * kk);
+          const uint64_t bH = sw128_kmajor_desc(b0 + 32 * kk), bL = sw128_kmajor_desc(b0 + 64 + 32 * kk);
+          mma_i8(dt + 0, aH, bH, ID_SS, kk > 0);
+          mma_i8(dt + 64, aH, bL, ID_SU, kk > 0);
+          mma_i8(dt + 64, aL, bH, ID_US, 1);
+          mma_i8(dt + 128, aL, bL, ID_UU, kk > 0);
+        }
+        mma_commit(&S.a_empty);
+        mma_commit(&S.tfull[b]);
+      }
+    }
+  } else if (warp >= kWarpC0 && warp < kWarpE0) {
+    // ======================= converters (128 threads) =======================
+    const int ct = tid - kWarpC0 * 32;
+    const int cw = ct >> 5;
+    const int em = S.em, disabled = S.disabled;
+    for (int m = 0; m < mtiles; ++m) {
+      const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
+      const int s = m % kStages;
+      const int rows = static_cast<int>(n - t * kTile < kTile ? n - t * kTile : kTile);
+      mbar_wait(&S.full[s], (m / kStages) & 1);
+      const double* xs = reinterpret_cast<const double*>(smem + s * kXStage);
+      // pass 1: tile exponent and finiteness
+      uint32_t mx = 0, bad = 0;
+      const int pairs = rows * d / 2;
+      const double2* xs2 = reinterpret_cast<const double2*>(xs);
+      for (int p = ct; p < pairs; p += 128) {
+        const double2 v = xs2[p];
+        const uint32_t h0 = static_cast<uint32_t>(__double2hiint(v.x)) & 0x7fffffffu;
+        const uint32_t h1 = static_cast<uint32_t>(__double2hiint(v.y)) & 0x7fffffffu;
+        mx = max(mx, max(h0, h1));
+        bad |= (h0 >= 0x7ff00000u) | (h1 >= 0x7ff00000u);
+      }
+      mx = __reduce_max_sync(0xffffffffu, mx);
+      bad = __reduce_or_sync(0xffffffffu, bad);
+      if (lane == 0) {
+        S.cscr[m & 1][cw] = mx;
+        S.cscr[m & 1][4 + cw] = bad;
+      }
+      named_bar(2, 128);
+      uint32_t tmx = 0, tbad = 0;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        tmx = max(tmx, S.cscr[m & 1][w]);
+        tbad |= S.cscr[m & 1][4 + w];
+      }
+      const int et = tmx == 0 ? em : exp_bound(tmx);
+      const int flag = (tbad || disabled || et > 400 || et < -400 || em - et > 2 || et - em > 8) ? 1 : 0;
+      if (m >= 1) mbar_wait(&S.a_empty, (m - 1) & 1);
+      // pass 2: fixed-point split into A (row q = cw*32 + r; lane owns columns 2l, 2l+1)
+      const double scale = flag ? 0.0 : ldexp(1.0, 15 - et);
+      const int j0 = 2 * lane;
+      for (int r = 0; r < 32; ++r) {
+        const int q = cw * 32 + r;
+        int X0 = 0, X1 = 0;
+        if (!flag && q < rows && j0 < d) {
+          const double2 v = *reinterpret_cast<const double2*>(xs + q * d + j0);
+          X0 = __double2int_rd(v.x * scale);
+          X1 = __double2int_rd(v.y * scale);
+        }
+        const uint32_t hi = ((X0 >> 8) & 0xff) | (((X1 >> 8) & 0xff) << 8);
+        const uint32_t lo = (X0 & 0xff) | ((X1 & 0xff) << 8);
+        *reinterpret_cast<uint16_t*>(A + sw128_offset(q, j0)) = static_cast<uint16_t>(hi);
+        *reinterpret_cast<uint16_t*>(A + sw128_offset(q, 64 + j0)) = static_cast<uint16_t>(lo);
+        const int sa = __reduce_add_sync(0xffffffffu, abs(X0) + abs(X1));
+        if (lane == 0) S.absx[s][q] = sa;
+      }
+      if (ct == 0) {
+        S.tile_e[s] = et;
+        S.tile_flag[s] = flag;
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&S.a_full);
+        mbar_arrive(&S.cfull[s]);
+      }
+    }
+  } else if (warp >= kWarpE0) {
+    // ======================= epilogue + bucket-reduce (256 threads) =======================
+    const int ew = warp - kWarpE0;          // 0..7
+    const int quarter = warp & 3;           // TMEM lane quarter this warp may access
+    const int h = ew >> 2;                  // centroid half
+    const int q = quarter * 32 + lane;      // sample row within the tile
+    const int rt = ew * 32 + lane;          // 0..255
+    const int jcol = rt & 63, res = rt >> 6;
+    const int em = S.em;
+    const int mabs = S.mpos + S.mneg;  // >= max_c Mpos_c - min_c' Mneg_c'
+    const unsigned long long valid = S.valid;
+    const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+    double acc[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc[u] = 0.0;
+    unsigned int rechecks = 0;
+    for (int m = 0; m < mtiles; ++m) {
+      const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
+      const int s = m % kStages, b = m & 1;
+      const int rows = static_cast<int>(n - t * kTile < kTile ? n - t * kTile : kTile);
+      mbar_wait(&S.cfull[s], (m / kStages) & 1);
+      mbar_wait(&S.full[s], (m / kStages) & 1);
+      const int et = S.tile_e[s], flag = S.tile_flag[s];
+      const double* xs = reinterpret_cast<const double*>(smem + s * kXStage);
+      mbar_wait(&S.tfull[b], (m >> 1) & 1);
+      tc_fence_after();
+      int tv[32];
+      int lmin = INT_MAX;
+      if (!flag) {
+        const double nscale = ldexp(1.0, 22 - et - em);
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          const uint32_t col = b * kAccCols + 32 * h + 16 * ch;
+          int hh[16], cr[16], ll[16];
+          tmem_ld16(tmem + lane_base + col, hh);
+          tmem_ld16(tmem + lane_base + col + 64, cr);
+          tmem_ld16(tmem + lane_base + col + 128, ll);
+          tmem_ld_wait();
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int c = 32 * h + 16 * ch + u;
+            const int Q = hh[u] * 256 + cr[u] + (ll[u] >> 8);
+            const int nm = __double2int_rd(S.nmf[c] * nscale);
+            const int v = ((valid >> c) & 1) ? nm - 2 * Q : INT_MAX;
+            tv[16 * ch + u] = v;
+            lmin = min(lmin, v);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.tempty[b]);
+      S.hmin[h][q] = lmin;
+      named_bar(1, 256);
+      uint32_t mask = 0;
+      if (!flag) {
+        const int tmin = min(S.hmin[0][q], S.hmin[1][q]);
+        if (tmin != INT_MAX) {
+          const int w = 6 + (S.absx[s][q] + mabs + d + 127) / 128;
+          const int thr = tmin + w;
+#pragma unroll
+          for (int u = 0; u < 32; ++u) mask |= (tv[u] <= thr ? 1u : 0u) << u;
+        }
+      }
+      S.cmask[h][q] = mask;
+      named_bar(1, 256);
+      if (h == 0 && q < rows) {
+        const double* xrow = xs + q * d;
+        int a;
+        if (flag) {
+          a = exact_argmin(xrow, mu, d, k == 64 ? ~0ull : ((1ull << k) - 1));
+        } else {
+          const unsigned long long full =
+              static_cast<unsigned long long>(S.cmask[0][q]) |
+              (static_cast<unsigned long long>(S.cmask[1][q]) << 32);
+          if (full == 0) {
+            a = 0;  // no finite centroid: the chain keeps its start index
+          } else if ((full & (full - 1)) == 0) {
+            a = __ffsll(static_cast<long long>(full)) - 1;
+          } else {
+            a = exact_argmin(xrow, mu, d, full);
+            ++rechecks;
+          }
+        }
+        S.assign[q] = a;
+        if (assign) assign[t * kTile + q] = a;
+      }
+      named_bar(1, 256);
+      // bucket-reduce: thread (res, jcol) owns sums[c][jcol] for c = 4u + res
+#pragma unroll 1
+      for (int i = 0; i < 4; ++i) {
+        const int qq = 32 * i + lane;
+        const int av = qq < rows ? S.assign[qq] : -1;
+        unsigned mm = __ballot_sync(0xffffffffu, av >= 0 && (av & 3) == res);
+        while (mm) {
+          const int l = __ffs(mm) - 1;
+          mm &= mm - 1;
+          const int row = 32 * i + l;
+          const int a = S.assign[row];
+          const double xv = jcol < d ? xs[row * d + jcol] : 0.0;
+          switch (a >> 2) {
+            case 0: acc[0] += xv; break;
+            case 1: acc[1] += xv; break;
+            case 2: acc[2] += xv; break;
+            case 3: acc[3] += xv; break;
+            case 4: acc[4] += xv; break;
+            case 5: acc[5] += xv; break;
+            case 6: acc[6] += xv; break;
+            case 7: acc[7] += xv; break;
+            case 8: acc[8] += xv; break;
+            case 9: acc[9] += xv; break;
+            case 10: acc[10] += xv; break;
+            case 11: acc[11] += xv; break;
+            case 12: acc[12] += xv; break;
+            case 13: acc[13] += xv; break;
+            case 14: acc[14] += xv; break;
+            default: acc[15] += xv; break;
+          }
+          if (jcol == 0) S.counts[a] += 1;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.sempty[s]);
+    }
+    // flush this CTA's partial activation record
+    double* ps = part_sums + static_cast<size_t>(blockIdx.x) * k * d;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int c = 4 * u + res;
+      if (c < k && jcol < d) ps[c * d + jcol] = acc[u];
+    }
+    if (rechecks) atomicAdd(&S.recheck, rechecks);
+    named_bar(1, 256);
+    if (rt < k) part_counts[static_cast<size_t>(blockIdx.x) * k + rt] = S.counts[rt];
+    if (rt == 0 && S.recheck) atomicAdd(recheck_total, static_cast<unsigned long long>(S.recheck));
+  }
+  __syncthreads();
+  if (warp == kWarpMma) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem);
+  }
+}
+
+}  // namespace sk
+
+static int screened_grid(int64_t n) {
+  const int64_t tiles = (n + sk::kTile - 1) / sk::kTile;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, sm_count())));
+}
+
+size_t kmeans_screened_workspace_bytes(int64_t n, int d, int k) {
+  if (d < 2 || d > sk::kMaxD || (d & 1) || k < 1 || k > sk::kMaxK) return 0;
+  const int grid = screened_grid(n);
+  Carve c(nullptr);
+  c.take<unsigned long long>(1);
+  c.take<long long>(static_cast<size_t>(grid) * k);
+  c.take<double>(static_cast<size_t>(grid) * k * d);
+  return c.used + 256;
+}
+
+int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double* mu,
+                         int32_t* assign, long long* counts, double* sums, void* ws,
+                         size_t ws_bytes, cudaStream_t stream, bool probe_only) {
+  DLX_REQUIRE(d >= 2 && d <= sk::kMaxD && (d & 1) == 0 && k >= 1 && k <= sk::kMaxK,
+              DLX_ERR_GENERATION,
+              "GenerationFailed: screened k-means needs even d <= %d and k <= %d (got d=%d k=%d)",
+              sk::kMaxD, sk::kMaxK, d, k);
+  DLX_REQUIRE((reinterpret_cast<uintptr_t>(x) & 15) == 0, DLX_ERR_GENERATION,
+              "GenerationFailed: screened k-means needs 16-byte aligned samples");
+  if (probe_only) return DLX_OK;
+  const int grid = screened_grid(n);
+  Carve c(ws);
+  unsigned long long* counter = c.take<unsigned long long>(1);
+  long long* pc = c.take<long long>(static_cast<size_t>(grid) * k);
+  double* psum = c.take<double>(static_cast<size_t>(grid) * k * d);
+  DLX_REQUIRE(ws && c.used <= ws_bytes, DLX_ERR_ARG, "k-means workspace too small (%zu < %zu)",
+              ws_bytes, c.used);
+  DLX_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream));
+  DLX_CUDA(cudaFuncSetAttribute(sk::kmeans_screened_kernel,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(sk::kSmemBytes)));
+  sk::kmeans_screened_kernel<<<grid, sk::kThreads, sk::kSmemBytes, stream>>>(
+      x, n, d, k, mu, assign, pc, psum, counter);
+  DLX_LAUNCHED("kmeans_screened_kernel");
+  return kmeans_finalize(pc, psum, grid, k, d, counts, sums, stream);
 }
 
 }  // namespace dlx
 
-extern "C" int dlx_kmeans_last_recheck_count(const void*, int64_t* h_count, dlx_stream_t) {
-  if (h_count) *h_count = -1;
+extern "C" int dlx_kmeans_last_recheck_count(const void* d_workspace, int64_t* h_count,
+                                             dlx_stream_t stream) {
+  DLX_REQUIRE(d_workspace && h_count, DLX_ERR_ARG, "recheck count: null argument");
+  unsigned long long v = 0;
+  DLX_CUDA(cudaMemcpyAsync(&v, d_workspace, sizeof(v), cudaMemcpyDeviceToHost, stream));
+  DLX_CUDA(cudaStreamSynchronize(stream));
+  *h_count = static_cast<int64_t>(v);
   return DLX_OK;
 }

@@ -2,6 +2,7 @@
 C ABI.  Bit-exact for integer / index results (assignments, counts, GroupBy); rtol 1e-9 for
 fp64 sums (north-star tolerance; the reduction order differs from the sequential fold)."""
 import hashlib
+import zlib
 
 import numpy as np
 import pytest
@@ -12,6 +13,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 RTOL = 1e-9  # fp64 sums (north_star: "1e-9 fp64")
+SCREENED = 2  # dlx_kmeans_step method: tcgen05 screen + exact recheck
 
 
 @pytest.fixture(scope="module")
@@ -47,7 +49,7 @@ def check_step(ml, x, mu, method=0):
     return a_ref, c_ref, s_ref
 
 
-@pytest.mark.parametrize("method", [0, 1])
+@pytest.mark.parametrize("method", [0, 1, SCREENED])
 def test_c1_stepwise_ten_iterations(ml, golden, method):
     """at every iteration run the GPU step from the oracle's centroids."""
     g = golden["c1_kmeans"]
@@ -90,6 +92,86 @@ def test_kmeans_shapes(ml, n, d, k, method):
     check_step(ml, x, mu, method)
 
 
+
+@pytest.mark.parametrize("n,d,k", [(1, 16, 8), (1000, 64, 64), (4099, 64, 64), (2048, 16, 1), (300_001, 64, 64),
+                                   (70_000, 2, 3), (5000, 40, 33), (129, 64, 64), (100_000, 32, 16)])
+def test_kmeans_screened_shapes(ml, n, d, k):
+    x = dev_units(ml, n, d, seed=n + 7 * d + k)
+    mu = dev_units(ml, k, d, seed=5)
+    check_step(ml, x, mu, SCREENED)
+
+
+def _stress_inputs(kind, n=20_000, d=64, k=64):
+    g = torch.Generator(device="cpu").manual_seed(zlib.crc32(kind.encode()))
+    x = torch.rand(n, d, generator=g, dtype=torch.float64)
+    mu = x[torch.randperm(n, generator=g)[:k]].clone()
+    if kind == "signed":
+        x = 2 * x - 1
+        mu = 2 * mu - 1
+    elif kind == "scaled_rows":
+        x = x * torch.pow(10.0, torch.randint(-3, 4, (n, 1), generator=g).double())
+    elif kind == "integer_ties":
+        x = torch.floor(x * 4)
+        mu = torch.floor(mu * 4)
+    elif kind == "dup_centroids":
+        mu[1::2] = mu[0::2]
+    elif kind == "points_on_centroids":
+        x[: 2 * k] = mu.repeat(2, 1)
+    elif kind == "nonfinite_rows":
+        x[5, 3] = float("nan")
+        x[777, 0] = float("inf")
+        x[12345, 63] = -float("inf")
+    elif kind == "nonfinite_centroids":
+        mu[3] = float("nan")
+        mu[9, 5] = float("inf")
+    elif kind == "huge":
+        x = x * 1e200
+        mu = mu * 1e200
+    elif kind == "tiny":
+        x = x * 1e-300
+        mu = mu * 1e-300
+    elif kind == "zeros":
+        x = torch.zeros_like(x)
+        mu = torch.zeros_like(mu)
+    elif kind == "centroids_far":
+        mu = mu * 1e3
+    elif kind == "samples_far":
+        x = x * 1e4
+    return x.cuda(), mu.cuda()
+
+
+@pytest.mark.parametrize("kind", ["signed", "scaled_rows", "integer_ties", "dup_centroids", "points_on_centroids",
+                                  "nonfinite_rows", "nonfinite_centroids", "huge", "tiny", "zeros", "centroids_far",
+                                  "samples_far"])
+@pytest.mark.parametrize("method", [0, SCREENED])
+def test_kmeans_screened_stress(ml, kind, method):
+    x, mu = _stress_inputs(kind)
+    xh, muh = x.cpu().numpy(), mu.cpu().numpy()
+    a, c, s = ml.kmeans_step(x, mu, method=method)
+    a_ref, c_ref, s_ref = O.kmeans_step(np.ascontiguousarray(xh), mu.shape[0], muh)
+    assert np.array_equal(a.cpu().numpy().astype(np.int64), a_ref)
+    assert np.array_equal(c.cpu().numpy(), c_ref)
+    np.testing.assert_allclose(s.cpu().numpy(), s_ref, rtol=RTOL, atol=0, equal_nan=True)
+
+
+def test_kmeans_screened_recheck_fraction(ml):
+    x = dev_units(ml, 1 << 20, 64, seed=1)
+    ml.kmeans_step(x, x[:64].clone(), method=SCREENED)
+    r = ml.kmeans_last_recheck_count()
+    print(f"screened recheck fraction at N=2^20, d=k=64: {r / (1 << 20):.5f}")
+    assert 0 <= r < (1 << 20) // 10
+
+
+def test_screened_rejects_unsupported(ml):
+    from paper_1109_0778_b200 import GenerationFailed
+    x = dev_units(ml, 100, 65, seed=1)
+    with pytest.raises(GenerationFailed):
+        ml.kmeans_step(x, x[:4].clone(), method=SCREENED)
+    x = dev_units(ml, 100, 16, seed=1)
+    with pytest.raises(GenerationFailed):
+        ml.kmeans_step(x, dev_units(ml, 65, 16), method=SCREENED)
+
+
 def test_kmeans_ties_and_nan(ml):
     x = dev_units(ml, 4000, 16, seed=3)
     mu = x[:8].clone()
@@ -108,13 +190,14 @@ def test_kmeans_empty_cluster_update(ml):
     assert np.isnan(mu[1]).all() and mu[0].tolist() == [1.0 / 3.0, 2.0 / 3.0]
 
 
-def test_c4_first_two_iterations(ml, golden, oracle_hashes):
+@pytest.mark.parametrize("method", [0, 1])
+def test_c4_first_two_iterations(ml, golden, oracle_hashes, method):
     g = golden["c4_kmeans"]
     x = dev_units(ml, g["n"], g["d"])
     mu = x[: g["k"]].clone()
     xh = x.cpu().numpy()
     for it in range(2):
-        a, c, s = ml.kmeans_step(x, mu)
+        a, c, s = ml.kmeans_step(x, mu, method=method)
         a_h = a.cpu().numpy().astype(np.int64)
         assert hex(O.fnv64w(a_h)) == oracle_hashes["c4_assign_fnv64w"][it]
         assert c.cpu().tolist()[:4] == g["counts_prefix"][it]
