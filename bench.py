@@ -387,6 +387,13 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
     ms_per_step = total_ms / args.steps
     value = 1000.0 / ms_per_step
 
+    pending = None
+    if family == "kmeans" and args.method != 1:
+        try:
+            pending = ml.kmeans_last_recheck_count(n_local, d, p["k"]) / max(1, n_local)
+        except Exception:
+            pending = None
+
     # ---- end to end through the public API with host buffers ----------------------------------
     e2e = None
     if family == "kmeans":
@@ -408,7 +415,8 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             "config": {"workload": args.config, **p, "parallelism": f"sample-sharded dp{world}",
                        "l2": "inputs larger than L2 (no flush needed)" if bytes_launch > 256e6 else
                              "inputs L2-resident (launch-bound config)",
-                       "method": {0: "auto", 1: "direct", 2: "screened"}[args.method]},
+                       "method": {0: "auto", 1: "direct", 2: "screened"}[args.method],
+                       "screen_recheck_fraction": pending},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(args.config),
                          "peak_kind": peak_kind, "kernel_ms": kern_ms,

@@ -87,9 +87,10 @@ int dlx_kmeans_step(const double* d_x, int64_t n, int32_t d, int32_t k, const do
 /* mu[c*d+j] = sums[c*d+j] / (double)counts[c]  (empty cluster -> 0/0 = NaN) */
 int dlx_kmeans_update(const int64_t* d_counts, const double* d_sums, int32_t k, int32_t d,
                       double* d_mu, dlx_stream_t stream);
-/* Number of samples the last screened step had to re-check exactly (diagnostic). */
-int dlx_kmeans_last_recheck_count(const void* d_workspace, int64_t* h_count,
-                                  dlx_stream_t stream);
+/* Number of samples the last screened step on this workspace (same n, d, k) re-evaluated
+ * with the exact reference chain (diagnostic; synchronises the stream). */
+int dlx_kmeans_last_recheck_count(const void* d_workspace, int64_t n, int32_t d, int32_t k,
+                                  int64_t* h_count, dlx_stream_t stream);
 
 /* ---- GroupBy / bucket-reduce: counts[b] = #{i : keys[i] == b}, b in [0, nbuckets) ------ */
 /* (the reference expresses this as nbuckets predicated count reduces).

@@ -1,0 +1,45 @@
+# Structural oracle: build the reference library (stagekit, /root/reference/proj) out of tree
+# into oracle/_ref/.  Never copies reference sources into the repo: every object is compiled
+# from the file where it lies under /root/reference; the one source that does not compile as
+# shipped (proj/src/codegen.cpp: `using minic::Expr;` clashes with stagekit::Expr)
+# is sed-patched into oracle/_ref/ at build time (git-ignored, never committed).  The vendored
+# JSON header the reference expects (proj/.gitignore:2) comes from the image's cudnn_frontend.
+REF      ?= /root/reference/proj
+OUT      := _ref
+JSON_HPP ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann/json.hpp
+CXX      ?= g++
+CXXFLAGS ?= -std=c++20 -O2 -fPIC -w -I$(REF)/include -I$(OUT)/vendor
+TUS      := expr graph stage records loops vectordsl schedule fusion dump minic
+OBJS     := $(addprefix $(OUT)/,$(addsuffix .o,$(TUS))) $(OUT)/codegen.o
+
+all: $(OUT)/libstagekit.a $(OUT)/stage_programs
+
+$(OUT)/vendor/json.hpp:
+	@mkdir -p $(OUT)/vendor
+	cp $(JSON_HPP) $@
+
+$(OUT)/%.o: $(REF)/src/%.cpp $(OUT)/vendor/json.hpp
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(OUT)/codegen_patched.cpp: $(REF)/src/codegen.cpp
+	@mkdir -p $(OUT)
+	sed -e 's/^using minic::Expr;/namespace mc = minic;/' \
+	    -e 's/\bExpr::\(int_lit\|double_lit\|bool_lit\|str_lit\|unit\|ref\|unary\|binary\|call\|index\|cond\|K\)\b/mc::Expr::\1/g' \
+	    -e 's/std::make_shared<Expr>/std::make_shared<mc::Expr>/g' $< > $@
+
+$(OUT)/codegen.o: $(OUT)/codegen_patched.cpp $(OUT)/vendor/json.hpp
+	$(CXX) $(CXXFLAGS) -I$(REF)/src -c $< -o $@
+
+$(OUT)/libstagekit.a: $(OBJS)
+	ar rcs $@ $^
+
+# stage_programs: stages the hot-path programs through the reference DSL (fuse_loops with
+# motion off, build_schedule, run_codegen), prints MiniC + DEG and emits the executor's
+# multiloop descriptors (adapter/stage_programs.cpp, our code).
+$(OUT)/stage_programs: adapter/stage_programs.cpp adapter/minic_eval.hpp $(OUT)/libstagekit.a
+	$(CXX) $(CXXFLAGS) -I. -o $@ adapter/stage_programs.cpp $(OUT)/libstagekit.a
+
+clean:
+	rm -rf $(OUT)
+
+.PHONY: all clean

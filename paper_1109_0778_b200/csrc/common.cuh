@@ -43,6 +43,11 @@ inline int cuda_fail(cudaError_t e, const char* what) {
     }                                                     \
   } while (0)
 
+// Deterministic combine of per-CTA partial activation records (combine.cu).
+int combine_f64(const double* parts, int nparts, long long width, double* out, cudaStream_t s);
+int combine_i64(const long long* parts, int nparts, long long width, long long* out, cudaStream_t s);
+int combine_u32_i64(const unsigned* parts, int nparts, long long width, long long* out, cudaStream_t s);
+
 // Number of SMs of the current device (cached per device).
 int sm_count();
 

@@ -91,16 +91,6 @@ groupby_smem_kernel(const long long* __restrict__ keys, int64_t n, long long nb,
   }
 }
 
-__global__ void groupby_finalize_kernel(const unsigned* __restrict__ partials, int parts,
-                                        long long nb, long long* __restrict__ counts) {
-  for (long long b = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; b < nb;
-       b += static_cast<long long>(gridDim.x) * blockDim.x) {
-    long long acc = 0;
-    for (int p = 0; p < parts; ++p) acc += partials[static_cast<size_t>(p) * nb + b];
-    counts[b] = acc;
-  }
-}
-
 __global__ void __launch_bounds__(kGbThreads)
 groupby_global_kernel(const long long* __restrict__ keys, int64_t n, long long nb,
                       unsigned long long* __restrict__ counts) {
@@ -159,11 +149,7 @@ int dlx_groupby_count(const int64_t* d_keys, int64_t n, int64_t nbuckets, int64_
   groupby_smem_kernel<<<p.grid, kGbThreads, p.smem, stream>>>(
       reinterpret_cast<const long long*>(d_keys), n, nbuckets, p.copies, partials);
   DLX_LAUNCHED("groupby_smem_kernel");
-  const int fb = static_cast<int>(std::min<int64_t>((nbuckets + 255) / 256, 1024));
-  groupby_finalize_kernel<<<fb, 256, 0, stream>>>(partials, p.grid, nbuckets,
-                                                  reinterpret_cast<long long*>(d_counts));
-  DLX_LAUNCHED("groupby_finalize_kernel");
-  return DLX_OK;
+  return combine_u32_i64(partials, p.grid, nbuckets, reinterpret_cast<long long*>(d_counts), stream);
 }
 
 }  // extern "C"

@@ -20,8 +20,8 @@
 //   * bucket-reduce: the CTA's sums (k x d) and counts (k) sit in shared memory; each (c, j)
 //     cell has exactly one owner thread, which folds the tile's samples in order — no
 //     atomics, deterministic;
-//   * per-CTA partial activation records go to the workspace, and a finalize kernel combines
-//     them in ascending CTA order (SPEC.md:648's ascending-chunk combine, CTA = chunk).
+//   * per-CTA partial activation records go to the workspace and are folded by the
+//     deterministic combine kernel (combine.cu; SPEC.md:648's fixed-order combine, CTA = chunk).
 #include <algorithm>
 
 #include "common.cuh"
@@ -186,26 +186,6 @@ kmeans_direct_kernel(const double* __restrict__ x, int64_t n, int d, int k,
   for (int c = tid; c < k; c += kThreads) pc[c] = counts_s[c];
 }
 
-// Ascending-CTA combine of the partial activation records.
-__global__ void kmeans_finalize_kernel(const long long* __restrict__ part_counts,
-                                       const double* __restrict__ part_sums, int parts, int k,
-                                       int d, long long* __restrict__ counts,
-                                       double* __restrict__ sums) {
-  const int kd = k * d;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kd + k; e += gridDim.x * blockDim.x) {
-    if (e < kd) {
-      double acc = part_sums[e];
-      for (int b = 1; b < parts; ++b) acc += part_sums[static_cast<size_t>(b) * kd + e];
-      sums[e] = acc;
-    } else {
-      const int c = e - kd;
-      long long acc = 0;
-      for (int b = 0; b < parts; ++b) acc += part_counts[static_cast<size_t>(b) * k + c];
-      counts[c] = acc;
-    }
-  }
-}
-
 __global__ void kmeans_update_kernel(const long long* __restrict__ counts,
                                      const double* __restrict__ sums, int k, int d,
                                      double* __restrict__ mu) {
@@ -218,11 +198,9 @@ __global__ void kmeans_update_kernel(const long long* __restrict__ counts,
 
 int kmeans_finalize(const long long* part_counts, const double* part_sums, int parts, int k, int d,
                     long long* counts, double* sums, cudaStream_t stream) {
-  const int kd = k * d;
-  kmeans_finalize_kernel<<<(kd + k + 255) / 256, 256, 0, stream>>>(part_counts, part_sums, parts, k, d,
-                                                                  counts, sums);
-  DLX_LAUNCHED("kmeans_finalize_kernel");
-  return DLX_OK;
+  int rc = combine_i64(part_counts, parts, k, counts, stream);
+  if (rc != DLX_OK) return rc;
+  return combine_f64(part_sums, parts, static_cast<long long>(k) * d, sums, stream);
 }
 
 // Screened tcgen05 path (kmeans_screened.cu).  Returns DLX_ERR_GENERATION when the shape

@@ -35,11 +35,17 @@
 //   warp 1      TMEM owner + MMA issuer (one thread): 8 tcgen05.mma per tile into a
 //               double-buffered 3 x 64-column int32 accumulator
 //   warps 2-5   converters: tile exponent, fixed-point split into the SW128 K-major A operand
-//   warps 6-13  epilogue + bucket-reduce: tcgen05.ld the scores, screen / recheck, then
-//               fold the tile's rows into register-resident per-centroid sums (each (c, j)
-//               cell owned by one thread, samples folded in order: deterministic, no atomics)
+//   warps 6-13  epilogue + bucket-reduce: tcgen05.ld the scores and screen; samples with a
+//               unique survivor are folded into register-resident per-centroid sums (warp w
+//               owns centroids w, w+8, ...; lane l owns columns 2l, 2l+1; rows folded in
+//               ascending order: deterministic, no atomics); samples with several survivors
+//               (and every sample of a guarded tile) go to a per-CTA pending list
+//   resolve     a second small kernel evaluates the reference chain for the pending samples
+//               (one lane per candidate centroid), writes their assignments and folds their
+//               rows into a second per-CTA partial record, in list order (deterministic).
 #include <algorithm>
 #include <climits>
+#include <vector>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -75,13 +81,13 @@ struct Misc {
   uint32_t mu_maxhi;
   int tile_e[kStages], tile_flag[kStages];
   int absx[kStages][kTile];
+  int nmt[kStages][kMaxK];  // floor(|mu_c|^2 / U_t) per stage (U_t depends on the tile exponent)
   double nmf[kMaxK];
   int hmin[2][kTile];
   uint32_t cmask[2][kTile];
   int assign[kTile];
-  int counts[kMaxK];
+  int pcount[4];
   uint32_t cscr[2][8];
-  unsigned int recheck;
 };
 constexpr uint32_t kSmemBytes = kOffMisc + sizeof(Misc);
 static_assert(kSmemBytes <= 232448, "shared-memory plan exceeds 227 KiB");
@@ -91,32 +97,12 @@ __device__ __forceinline__ int exp_bound(uint32_t maxhi) {
   return static_cast<int>(maxhi >> 20) - 1022;
 }
 
-__device__ int exact_argmin(const double* xrow, const double* __restrict__ mu, int d,
-                            unsigned long long mask) {
-  double best = 1e300;
-  int bi = 0;
-  while (mask) {
-    const int c = __ffsll(static_cast<long long>(mask)) - 1;
-    mask &= mask - 1;
-    const double* m = mu + c * d;
-    double acc = 0.0;
-    for (int j = 0; j < d; ++j) {
-      const double diff = __dsub_rn(xrow[j], __ldg(m + j));
-      acc = __dadd_rn(acc, __dmul_rn(diff, diff));
-    }
-    if (acc < best) {
-      best = acc;
-      bi = c;
-    }
-  }
-  return bi;
-}
-
 __global__ void __launch_bounds__(kThreads, 1)
 kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
                        const double* __restrict__ mu, int32_t* __restrict__ assign,
                        long long* __restrict__ part_counts, double* __restrict__ part_sums,
-                       unsigned long long* __restrict__ recheck_total) {
+                       long long* __restrict__ pend_idx, unsigned long long* __restrict__ pend_mask,
+                       long long* __restrict__ pend_count, long long pend_cap) {
   extern __shared__ __align__(1024) unsigned char smem[];
   Misc& S = *reinterpret_cast<Misc*>(smem + kOffMisc);
   unsigned char* A = smem + kOffA;
@@ -143,10 +129,8 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     S.mpos = 0;
     S.mneg = 0;
     S.mu_maxhi = 0;
-    S.recheck = 0;
     fence_mbar_init();
   }
-  for (int c = tid; c < kMaxK; c += kThreads) S.counts[c] = 0;
   __syncthreads();
   if (tid < kMaxK) {  // per centroid: validity (all finite), max |mu| high word, |mu|^2
     const int c = tid;
@@ -304,6 +288,9 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         S.tile_e[s] = et;
         S.tile_flag[s] = flag;
       }
+      if (ct < kMaxK) {  // |mu_c|^2 in units U_t = 2^(e_t+e_m-22): < 2^30 under the gap guard
+        S.nmt[s][ct] = flag ? 0 : __double2int_rd(S.nmf[ct] * ldexp(1.0, 22 - et - em));
+      }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
@@ -317,30 +304,30 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     const int quarter = warp & 3;           // TMEM lane quarter this warp may access
     const int h = ew >> 2;                  // centroid half
     const int q = quarter * 32 + lane;      // sample row within the tile
-    const int rt = ew * 32 + lane;          // 0..255
-    const int jcol = rt & 63, res = rt >> 6;
-    const int em = S.em;
-    const int mabs = S.mpos + S.mneg;  // >= max_c Mpos_c - min_c' Mneg_c'
+    const int mabs = S.mpos + S.mneg;       // >= max_c Mpos_c - min_c' Mneg_c'
     const unsigned long long valid = S.valid;
+    const unsigned long long kmask = k == 64 ? ~0ull : ((1ull << k) - 1);
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-    double acc[16];
+    long long* my_pidx = pend_idx + static_cast<size_t>(blockIdx.x) * pend_cap;
+    unsigned long long* my_pmask = pend_mask + static_cast<size_t>(blockIdx.x) * pend_cap;
+    long long pending = 0;
+    double acc[8][2];
+    int cnt[8];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) acc[u] = 0.0;
-    unsigned int rechecks = 0;
+    for (int u = 0; u < 8; ++u) acc[u][0] = acc[u][1] = 0.0, cnt[u] = 0;
     for (int m = 0; m < mtiles; ++m) {
       const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
       const int s = m % kStages, b = m & 1;
       const int rows = static_cast<int>(n - t * kTile < kTile ? n - t * kTile : kTile);
       mbar_wait(&S.cfull[s], (m / kStages) & 1);
       mbar_wait(&S.full[s], (m / kStages) & 1);
-      const int et = S.tile_e[s], flag = S.tile_flag[s];
+      const int flag = S.tile_flag[s];
       const double* xs = reinterpret_cast<const double*>(smem + s * kXStage);
       mbar_wait(&S.tfull[b], (m >> 1) & 1);
       tc_fence_after();
       int tv[32];
       int lmin = INT_MAX;
       if (!flag) {
-        const double nscale = ldexp(1.0, 22 - et - em);
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
           const uint32_t col = b * kAccCols + 32 * h + 16 * ch;
@@ -353,8 +340,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
           for (int u = 0; u < 16; ++u) {
             const int c = 32 * h + 16 * ch + u;
             const int Q = hh[u] * 256 + cr[u] + (ll[u] >> 8);
-            const int nm = __double2int_rd(S.nmf[c] * nscale);
-            const int v = ((valid >> c) & 1) ? nm - 2 * Q : INT_MAX;
+            const int v = ((valid >> c) & 1) ? S.nmt[s][c] - 2 * Q : INT_MAX;
             tv[16 * ch + u] = v;
             lmin = min(lmin, v);
           }
@@ -377,59 +363,64 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       }
       S.cmask[h][q] = mask;
       named_bar(1, 256);
-      if (h == 0 && q < rows) {
-        const double* xrow = xs + q * d;
-        int a;
-        if (flag) {
-          a = exact_argmin(xrow, mu, d, k == 64 ? ~0ull : ((1ull << k) - 1));
-        } else {
-          const unsigned long long full =
-              static_cast<unsigned long long>(S.cmask[0][q]) |
-              (static_cast<unsigned long long>(S.cmask[1][q]) << 32);
+      unsigned long long full = 0;
+      bool pend = false;
+      if (h == 0) {
+        int a = -1;
+        if (q < rows) {
+          if (flag) {
+            full = kmask;  // guarded tile: the reference chain over every centroid
+          } else {
+            full = static_cast<unsigned long long>(S.cmask[0][q]) |
+                   (static_cast<unsigned long long>(S.cmask[1][q]) << 32);
+          }
           if (full == 0) {
             a = 0;  // no finite centroid: the chain keeps its start index
-          } else if ((full & (full - 1)) == 0) {
+          } else if (!flag && (full & (full - 1)) == 0) {
             a = __ffsll(static_cast<long long>(full)) - 1;
           } else {
-            a = exact_argmin(xrow, mu, d, full);
-            ++rechecks;
+            pend = true;  // several survivors: resolved by the exact chain (resolve kernel)
           }
+          if (a >= 0 && assign) assign[t * kTile + q] = a;
         }
         S.assign[q] = a;
-        if (assign) assign[t * kTile + q] = a;
       }
+      const unsigned pb = __ballot_sync(0xffffffffu, pend);
+      if (h == 0 && lane == 0) S.pcount[quarter] = __popc(pb);
       named_bar(1, 256);
-      // bucket-reduce: thread (res, jcol) owns sums[c][jcol] for c = 4u + res
-#pragma unroll 1
-      for (int i = 0; i < 4; ++i) {
-        const int qq = 32 * i + lane;
-        const int av = qq < rows ? S.assign[qq] : -1;
-        unsigned mm = __ballot_sync(0xffffffffu, av >= 0 && (av & 3) == res);
-        while (mm) {
-          const int l = __ffs(mm) - 1;
-          mm &= mm - 1;
-          const int row = 32 * i + l;
-          const int a = S.assign[row];
-          const double xv = jcol < d ? xs[row * d + jcol] : 0.0;
-          switch (a >> 2) {
-            case 0: acc[0] += xv; break;
-            case 1: acc[1] += xv; break;
-            case 2: acc[2] += xv; break;
-            case 3: acc[3] += xv; break;
-            case 4: acc[4] += xv; break;
-            case 5: acc[5] += xv; break;
-            case 6: acc[6] += xv; break;
-            case 7: acc[7] += xv; break;
-            case 8: acc[8] += xv; break;
-            case 9: acc[9] += xv; break;
-            case 10: acc[10] += xv; break;
-            case 11: acc[11] += xv; break;
-            case 12: acc[12] += xv; break;
-            case 13: acc[13] += xv; break;
-            case 14: acc[14] += xv; break;
-            default: acc[15] += xv; break;
+      {
+        // deterministic pending-list append, ordered by sample row
+        const int p0 = S.pcount[0], p1 = S.pcount[1], p2 = S.pcount[2];
+        if (pend) {
+          const int before = (quarter > 0 ? p0 : 0) + (quarter > 1 ? p1 : 0) + (quarter > 2 ? p2 : 0);
+          const long long slot = pending + before + __popc(pb & ((1u << lane) - 1));
+          my_pidx[slot] = t * kTile + q;
+          my_pmask[slot] = full;
+        }
+        pending += p0 + p1 + p2 + S.pcount[3];
+      }
+      // bucket-reduce: warp ew owns centroids ew + 8u, lane owns columns 2*lane, 2*lane+1
+      int av[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = S.assign[32 * i + lane];
+      const int j0 = 2 * lane;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = ew + 8 * u;
+        if (c >= k) break;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          unsigned mm = __ballot_sync(0xffffffffu, av[i] == c);
+          cnt[u] += __popc(mm);
+          while (mm) {
+            const int row = 32 * i + __ffs(mm) - 1;
+            mm &= mm - 1;
+            if (j0 < d) {
+              const double2 v = *reinterpret_cast<const double2*>(xs + row * d + j0);
+              acc[u][0] += v.x;
+              acc[u][1] += v.y;
+            }
           }
-          if (jcol == 0) S.counts[a] += 1;
         }
       }
       __syncwarp();
@@ -437,21 +428,130 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     }
     // flush this CTA's partial activation record
     double* ps = part_sums + static_cast<size_t>(blockIdx.x) * k * d;
+    const int j0 = 2 * lane;
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int c = 4 * u + res;
-      if (c < k && jcol < d) ps[c * d + jcol] = acc[u];
+    for (int u = 0; u < 8; ++u) {
+      const int c = ew + 8 * u;
+      if (c < k) {
+        if (j0 < d) ps[c * d + j0] = acc[u][0];
+        if (j0 + 1 < d) ps[c * d + j0 + 1] = acc[u][1];
+        if (lane == 0) part_counts[static_cast<size_t>(blockIdx.x) * k + c] = cnt[u];
+      }
     }
-    if (rechecks) atomicAdd(&S.recheck, rechecks);
-    named_bar(1, 256);
-    if (rt < k) part_counts[static_cast<size_t>(blockIdx.x) * k + rt] = S.counts[rt];
-    if (rt == 0 && S.recheck) atomicAdd(recheck_total, static_cast<unsigned long long>(S.recheck));
+    if (ew == 0 && lane == 0) pend_count[blockIdx.x] = pending;
   }
   __syncthreads();
   if (warp == kWarpMma) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
   }
+}
+
+// ---------------------------------------------------------------------------------------
+// resolve: the reference chain for the pending samples.  Resolve CTA rb handles slice
+// rb % kResSplit of main-kernel CTA rb / kResSplit's pending list: warps take samples, lanes
+// take candidate centroids (ascending), the chain merge keeps the reference order; the rows
+// are then gathered into shared memory and folded into this CTA's partial record in list
+// order (deterministic).
+constexpr int kResThreads = 512;
+constexpr int kResSplit = 4;
+constexpr int kResChunk = 128;
+
+__global__ void __launch_bounds__(kResThreads)
+kmeans_resolve_kernel(const double* __restrict__ x, int d, int k, const double* __restrict__ mu,
+                      int32_t* __restrict__ assign, const long long* __restrict__ pend_idx,
+                      unsigned long long* __restrict__ pend_mask,
+                      const long long* __restrict__ pend_count, long long pend_cap,
+                      long long* __restrict__ part_counts, double* __restrict__ part_sums) {
+  extern __shared__ double rsm[];
+  double* sums_s = rsm;                          // k*d
+  double* rows_s = rsm + k * d;                  // kResChunk*d
+  __shared__ long long idx_s[kResChunk];
+  __shared__ int a_s[kResChunk];
+  __shared__ long long cnt_s[kMaxK];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int src = blockIdx.x / kResSplit, slice = blockIdx.x % kResSplit;
+  const long long total = pend_count[src];
+  const long long lo = total * slice / kResSplit, hi = total * (slice + 1) / kResSplit;
+  const long long* pidx = pend_idx + static_cast<size_t>(src) * pend_cap;
+  unsigned long long* pmask = pend_mask + static_cast<size_t>(src) * pend_cap;
+  for (int e = tid; e < k * d; e += kResThreads) sums_s[e] = 0.0;
+  for (int c = tid; c < k; c += kResThreads) cnt_s[c] = 0;
+  // phase 1: one warp per pending sample, one lane per candidate centroid
+  for (long long e = lo + warp; e < hi; e += kResThreads / 32) {
+    const long long i = pidx[e];
+    const double* xr = x + i * d;
+    unsigned long long mask = pmask[e];
+    double best = 1e300;
+    int bi = 0;
+    while (mask) {  // rounds of up to 32 candidates, ascending centroid index
+      unsigned long long rest = mask;
+      int c = -1;
+      for (int r = 0; r <= lane && rest; ++r) {  // c = the lane-th remaining candidate
+        const int cc = __ffsll(static_cast<long long>(rest)) - 1;
+        rest &= rest - 1;
+        if (r == lane) c = cc;
+      }
+      double v = 1e300;
+      if (c >= 0) {
+        const double* m = mu + c * d;
+        double acc = 0.0;
+#pragma unroll 8
+        for (int j = 0; j < d; ++j) {
+          const double diff = __dsub_rn(__ldg(xr + j), __ldg(m + j));
+          acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+        }
+        v = acc;
+      }
+      // chain merge in ascending lane (= ascending centroid) order: strict <, NaN never wins
+      const unsigned live = __ballot_sync(0xffffffffu, c >= 0);
+      for (int l = 0; l < 32; ++l) {
+        if (!((live >> l) & 1)) break;
+        const double vl = __shfl_sync(0xffffffffu, v, l);
+        const int cl = __shfl_sync(0xffffffffu, c, l);
+        if (vl < best) {
+          best = vl;
+          bi = cl;
+        }
+      }
+      for (int r = 0; r < 32 && mask; ++r) mask &= mask - 1;  // drop this round's candidates
+    }
+    if (lane == 0) {
+      if (assign) assign[i] = bi;
+      pmask[e] = static_cast<unsigned long long>(bi);  // reuse the slot for phase 2
+    }
+  }
+  __syncthreads();
+  // phase 2: gather the rows chunk by chunk, fold them in list order; thread (r, j) owns
+  // cells (c, j) with c % (kResThreads/64) == r
+  constexpr int R = kResThreads / 64;
+  const int j = tid & 63, r = tid >> 6;
+  for (long long base = lo; base < hi; base += kResChunk) {
+    const int nrow = static_cast<int>(hi - base < kResChunk ? hi - base : kResChunk);
+    for (int e = tid; e < nrow; e += kResThreads) {
+      idx_s[e] = pidx[base + e];
+      a_s[e] = static_cast<int>(pmask[base + e]);
+    }
+    __syncthreads();
+    for (int e = tid; e < nrow * d; e += kResThreads) {
+      const int rr = e / d, jj = e - rr * d;
+      rows_s[e] = __ldg(x + idx_s[rr] * d + jj);
+    }
+    __syncthreads();
+    if (j < d) {
+      for (int e = 0; e < nrow; ++e) {
+        const int a = a_s[e];
+        if (a % R == r) {
+          sums_s[a * d + j] += rows_s[e * d + j];
+          if (j == 0) cnt_s[a] += 1;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  double* ps = part_sums + static_cast<size_t>(blockIdx.x) * k * d;
+  for (int e = tid; e < k * d; e += kResThreads) ps[e] = sums_s[e];
+  for (int c = tid; c < k; c += kResThreads) part_counts[static_cast<size_t>(blockIdx.x) * k + c] = cnt_s[c];
 }
 
 }  // namespace sk
@@ -461,14 +561,37 @@ static int screened_grid(int64_t n) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, sm_count())));
 }
 
+static long long pend_capacity(int64_t n, int grid) {
+  const int64_t tiles = (n + sk::kTile - 1) / sk::kTile;
+  return ((tiles + grid - 1) / grid) * sk::kTile;
+}
+
+struct ScreenedWs {
+  long long* pend_count;
+  long long* part_counts;  // [(1+kResSplit)*grid][k]: main kernel, then resolve kernel
+  double* part_sums;       // [(1+kResSplit)*grid][k*d]
+  long long* pend_idx;     // [grid][cap]
+  unsigned long long* pend_mask;
+  size_t used;
+};
+
+static ScreenedWs carve_screened(void* base, int64_t n, int d, int k, int grid) {
+  const long long cap = pend_capacity(n, grid);
+  Carve c(base);
+  ScreenedWs w;
+  w.pend_count = c.take<long long>(grid);
+  const int parts = (1 + sk::kResSplit) * grid;
+  w.part_counts = c.take<long long>(static_cast<size_t>(parts) * k);
+  w.part_sums = c.take<double>(static_cast<size_t>(parts) * k * d);
+  w.pend_idx = c.take<long long>(static_cast<size_t>(grid) * cap);
+  w.pend_mask = c.take<unsigned long long>(static_cast<size_t>(grid) * cap);
+  w.used = c.used;
+  return w;
+}
+
 size_t kmeans_screened_workspace_bytes(int64_t n, int d, int k) {
   if (d < 2 || d > sk::kMaxD || (d & 1) || k < 1 || k > sk::kMaxK) return 0;
-  const int grid = screened_grid(n);
-  Carve c(nullptr);
-  c.take<unsigned long long>(1);
-  c.take<long long>(static_cast<size_t>(grid) * k);
-  c.take<double>(static_cast<size_t>(grid) * k * d);
-  return c.used + 256;
+  return carve_screened(nullptr, n, d, k, screened_grid(n)).used + 256;
 }
 
 int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double* mu,
@@ -482,30 +605,45 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
               "GenerationFailed: screened k-means needs 16-byte aligned samples");
   if (probe_only) return DLX_OK;
   const int grid = screened_grid(n);
-  Carve c(ws);
-  unsigned long long* counter = c.take<unsigned long long>(1);
-  long long* pc = c.take<long long>(static_cast<size_t>(grid) * k);
-  double* psum = c.take<double>(static_cast<size_t>(grid) * k * d);
-  DLX_REQUIRE(ws && c.used <= ws_bytes, DLX_ERR_ARG, "k-means workspace too small (%zu < %zu)",
-              ws_bytes, c.used);
-  DLX_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream));
+  const long long cap = pend_capacity(n, grid);
+  ScreenedWs w = carve_screened(ws, n, d, k, grid);
+  DLX_REQUIRE(ws && w.used <= ws_bytes, DLX_ERR_ARG, "k-means workspace too small (%zu < %zu)",
+              ws_bytes, w.used);
   DLX_CUDA(cudaFuncSetAttribute(sk::kmeans_screened_kernel,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sk::kSmemBytes)));
   sk::kmeans_screened_kernel<<<grid, sk::kThreads, sk::kSmemBytes, stream>>>(
-      x, n, d, k, mu, assign, pc, psum, counter);
+      x, n, d, k, mu, assign, w.part_counts, w.part_sums, w.pend_idx, w.pend_mask, w.pend_count, cap);
   DLX_LAUNCHED("kmeans_screened_kernel");
-  return kmeans_finalize(pc, psum, grid, k, d, counts, sums, stream);
+  const size_t rsmem = static_cast<size_t>(k + sk::kResChunk) * d * sizeof(double);
+  DLX_CUDA(cudaFuncSetAttribute(sk::kmeans_resolve_kernel,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsmem)));
+  sk::kmeans_resolve_kernel<<<grid * sk::kResSplit, sk::kResThreads, rsmem, stream>>>(
+      x, d, k, mu, assign, w.pend_idx, w.pend_mask, w.pend_count, cap,
+      w.part_counts + static_cast<size_t>(grid) * k, w.part_sums + static_cast<size_t>(grid) * k * d);
+  DLX_LAUNCHED("kmeans_resolve_kernel");
+  return kmeans_finalize(w.part_counts, w.part_sums, (1 + sk::kResSplit) * grid, k, d, counts, sums,
+                         stream);
+}
+
+// pending (re-checked) samples of the last screened step on this workspace
+int kmeans_screened_pending(const void* ws, int64_t n, int d, int k, int64_t* out, cudaStream_t stream) {
+  const int grid = screened_grid(n);
+  std::vector<long long> h(grid);
+  DLX_CUDA(cudaMemcpyAsync(h.data(), ws, sizeof(long long) * grid, cudaMemcpyDeviceToHost, stream));
+  DLX_CUDA(cudaStreamSynchronize(stream));
+  long long s = 0;
+  for (long long v : h) s += v;
+  *out = s;
+  (void)d;
+  (void)k;
+  return DLX_OK;
 }
 
 }  // namespace dlx
 
-extern "C" int dlx_kmeans_last_recheck_count(const void* d_workspace, int64_t* h_count,
-                                             dlx_stream_t stream) {
+extern "C" int dlx_kmeans_last_recheck_count(const void* d_workspace, int64_t n, int32_t d,
+                                             int32_t k, int64_t* h_count, dlx_stream_t stream) {
   DLX_REQUIRE(d_workspace && h_count, DLX_ERR_ARG, "recheck count: null argument");
-  unsigned long long v = 0;
-  DLX_CUDA(cudaMemcpyAsync(&v, d_workspace, sizeof(v), cudaMemcpyDeviceToHost, stream));
-  DLX_CUDA(cudaStreamSynchronize(stream));
-  *h_count = static_cast<int64_t>(v);
-  return DLX_OK;
+  return dlx::kmeans_screened_pending(d_workspace, n, d, k, h_count, stream);
 }

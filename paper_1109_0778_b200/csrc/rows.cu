@@ -1,12 +1,13 @@
 // rows.cu — row-streaming multiloops over a row-major DenseMatrix: the logistic-regression
 // gradient and GDA passes 1 and 2 (§8 a6).
 //
-// Shared device plan for the streaming families: one warp per sample row, lane l holds
-// columns {2l, 2l+1} + 64m (128-bit loads, so a d=64 fp64 row = one warp-wide load);
-// several rows in flight per warp; every reduce slot that all samples feed (gradient,
+// Shared device plan for the streaming families: a warp streams blocks of 8 consecutive
+// rows, lane l holding columns {2l, 2l+1} + 64m of each (128-bit loads, so a d=64 fp64 row is
+// one warp-wide load and 8 are in flight per lane); every reduce slot that all samples feed (gradient,
 // per-class sums) is a per-lane register accumulator, reduced across warps through shared
-// memory in ascending warp order, written as a per-CTA partial and combined across CTAs in
-// ascending order.
+// memory in ascending warp order, written as a per-CTA partial and folded across CTAs by the
+// deterministic combine kernel (combine.cu).  Pass 2 (d <= 64) runs on the fp64 tensor cores
+// (gda_dmma.cu); the CUDA-core register-tile kernel below covers 64 < d <= 128.
 #include <algorithm>
 
 #include "common.cuh"
@@ -42,26 +43,57 @@ __device__ void cta_reduce_columns(double (&acc)[M][2], int d, double* red_s, do
   __syncthreads();
 }
 
-__global__ void combine_parts_kernel(const double* __restrict__ parts, int nparts, int width,
-                                     double* __restrict__ out) {
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < width; e += gridDim.x * blockDim.x) {
-    double v = parts[e];
-    for (int p = 1; p < nparts; ++p) v += parts[static_cast<size_t>(p) * width + e];
-    out[e] = v;
+// 8 rows in flight per warp: lane l holds columns {2l, 2l+1} + 64m of rows r0..r0+7.
+constexpr int kRows = 8;
+
+template <int M>
+__device__ __forceinline__ void load_rows(const double* __restrict__ x, int64_t i0, int64_t n, int d,
+                                          int lane, double2 (&v)[kRows][M]) {
+#pragma unroll
+  for (int r = 0; r < kRows; ++r) {
+    const int64_t i = i0 + r;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const int j = 64 * m + 2 * lane;
+      v[r][m] = (i < n && j < d) ? ld_stream_f64x2(x + i * d + j) : make_double2(0.0, 0.0);
+    }
   }
 }
 
-__global__ void combine_parts_ll_kernel(const long long* __restrict__ parts, int nparts,
-                                        long long* __restrict__ out) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    long long v = 0;
-    for (int p = 0; p < nparts; ++p) v += parts[p];
-    *out = v;
+// Reduce-scatter of 8 per-lane partial dot products: 9 fp64 shuffles instead of 8 x 5.
+// Returns the full dot of row  row_of_lane(lane) = 4*b4 + 2*b3 + b2  (b_k = bit k of lane);
+// every row ends up on the 4 lanes that differ in bits 0-1.
+__device__ __forceinline__ double reduce_scatter8(const double (&p)[kRows], int lane) {
+  const bool b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1;
+  double q4[4], q2[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double send = b4 ? p[i] : p[i + 4];
+    const double keep = b4 ? p[i + 4] : p[i];
+    q4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
   }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double send = b3 ? q4[i] : q4[i + 2];
+    const double keep = b3 ? q4[i + 2] : q4[i];
+    q2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  const double send = b2 ? q2[0] : q2[1];
+  const double keep = b2 ? q2[1] : q2[0];
+  double z = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  z += __shfl_xor_sync(0xffffffffu, z, 2);
+  z += __shfl_xor_sync(0xffffffffu, z, 1);
+  return z;
+}
+
+__device__ __forceinline__ int lane_of_row(int r) {
+  return (((r >> 2) & 1) << 4) | (((r >> 1) & 1) << 3) | ((r & 1) << 2);
 }
 
 // ---------------------------------------------------------------------------------------
 // logistic regression: g_j = sum_i (sigmoid(theta . x_i) - y_i) x_ij
+// One fused pass: dot (FMA partials + reduce-scatter), sigmoid once per row on 4 lanes,
+// residual broadcast, gradient FMAs into per-lane registers.
 template <int M>
 __global__ void __launch_bounds__(kRowThreads)
 logreg_grad_kernel(const double* __restrict__ x, const long long* __restrict__ y, int64_t n,
@@ -76,34 +108,32 @@ logreg_grad_kernel(const double* __restrict__ x, const long long* __restrict__ y
     th[m][1] = j + 1 < d ? theta[j + 1] : 0.0;
     acc[m][0] = acc[m][1] = 0.0;
   }
+  const int64_t nblk = (n + kRows - 1) / kRows;
   const int64_t W = static_cast<int64_t>(gridDim.x) * kRowWarps;
-  constexpr int R = 4;  // rows in flight per warp
-  for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * kRowWarps + warp; i0 < n; i0 += R * W) {
-    double2 v[R][M];
-    double yv[R];
+  const int my_row = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+  for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kRowWarps + warp; blk < nblk; blk += W) {
+    const int64_t i0 = blk * kRows;
+    double2 v[kRows][M];
+    load_rows<M>(x, i0, n, d, lane, v);
+    const int64_t iy = i0 + my_row;
+    const double yv = iy < n ? static_cast<double>(__ldg(y + iy)) : 0.0;
+    double p[kRows];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int64_t i = i0 + r * W;
-      yv[r] = i < n ? static_cast<double>(__ldg(y + i)) : 0.0;
+    for (int r = 0; r < kRows; ++r) {
+      double a = 0.0;
 #pragma unroll
-      for (int m = 0; m < M; ++m) {
-        const int j = 64 * m + 2 * lane;
-        v[r][m] = (i < n && j < d) ? ld_stream_f64x2(x + i * d + j) : make_double2(0.0, 0.0);
-      }
+      for (int m = 0; m < M; ++m) a = fma(th[m][0], v[r][m].x, fma(th[m][1], v[r][m].y, a));
+      p[r] = a;
     }
+    const double z = reduce_scatter8(p, lane);
+    const double res = iy < n ? 1.0 / (1.0 + exp(-z)) - yv : 0.0;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int64_t i = i0 + r * W;
-      double z = 0.0;
-#pragma unroll
-      for (int m = 0; m < M; ++m) z += th[m][0] * v[r][m].x + th[m][1] * v[r][m].y;
-      z = warp_sum(z);
-      const double h = 1.0 / (1.0 + exp(-z));
-      const double res = (i < n) ? h - yv[r] : 0.0;
+    for (int r = 0; r < kRows; ++r) {
+      const double rr = __shfl_sync(0xffffffffu, res, lane_of_row(r));
 #pragma unroll
       for (int m = 0; m < M; ++m) {
-        acc[m][0] += res * v[r][m].x;
-        acc[m][1] += res * v[r][m].y;
+        acc[m][0] = fma(rr, v[r][m].x, acc[m][0]);
+        acc[m][1] = fma(rr, v[r][m].y, acc[m][1]);
       }
     }
   }
@@ -124,30 +154,25 @@ gda_pass1_kernel(const double* __restrict__ x, const long long* __restrict__ y, 
 #pragma unroll
   for (int m = 0; m < M; ++m) a0[m][0] = a0[m][1] = a1[m][0] = a1[m][1] = 0.0;
   long long n1 = 0;
+  const int64_t nblk = (n + kRows - 1) / kRows;
   const int64_t W = static_cast<int64_t>(gridDim.x) * kRowWarps;
-  constexpr int R = 4;
-  for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * kRowWarps + warp; i0 < n; i0 += R * W) {
-    double2 v[R][M];
-    long long yv[R];
+  for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kRowWarps + warp; blk < nblk; blk += W) {
+    const int64_t i0 = blk * kRows;
+    double2 v[kRows][M];
+    load_rows<M>(x, i0, n, d, lane, v);
+    // lanes 0..7 fetch the 8 labels, then broadcast
+    const long long ylane = (lane < kRows && i0 + lane < n) ? __ldg(y + i0 + lane) : -1;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int64_t i = i0 + r * W;
-      yv[r] = i < n ? __ldg(y + i) : -1;
+    for (int r = 0; r < kRows; ++r) {
+      const long long yv = __shfl_sync(0xffffffffu, ylane, r);
+      const double w1 = yv == 1 ? 1.0 : 0.0, w0 = yv == 0 ? 1.0 : 0.0;
+      n1 += (yv == 1);
 #pragma unroll
       for (int m = 0; m < M; ++m) {
-        const int j = 64 * m + 2 * lane;
-        v[r][m] = (i < n && j < d) ? ld_stream_f64x2(x + i * d + j) : make_double2(0.0, 0.0);
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (yv[r] == 1) {
-        n1 += 1;
-#pragma unroll
-        for (int m = 0; m < M; ++m) { a1[m][0] += v[r][m].x; a1[m][1] += v[r][m].y; }
-      } else if (yv[r] == 0) {
-#pragma unroll
-        for (int m = 0; m < M; ++m) { a0[m][0] += v[r][m].x; a0[m][1] += v[r][m].y; }
+        a1[m][0] = fma(w1, v[r][m].x, a1[m][0]);
+        a1[m][1] = fma(w1, v[r][m].y, a1[m][1]);
+        a0[m][0] = fma(w0, v[r][m].x, a0[m][0]);
+        a0[m][1] = fma(w0, v[r][m].y, a0[m][1]);
       }
     }
   }
@@ -238,14 +263,18 @@ gda_pass2_kernel(const double* __restrict__ x, const long long* __restrict__ y, 
 
 }  // namespace dlx
 
+namespace dlx {
+int gda_pass2_dmma_grid(int64_t n);
+int gda_pass2_dmma(const double* x, const long long* y, int64_t n, int d, const double* mu0,
+                   const double* mu1, double* parts, size_t parts_bytes, double* out,
+                   cudaStream_t stream);
+}  // namespace dlx
+
 using namespace dlx;
 
 namespace {
 
 int m_for(int d) { return (d + 63) / 64; }
-
-template <template <int> class K>
-struct Dispatch;
 
 int gda2_grid(int64_t n) {
   int64_t grid = static_cast<int64_t>(sm_count()) * 2;
@@ -288,14 +317,13 @@ int dlx_logreg_grad(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
     default: logreg_grad_kernel<4><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, d_theta, parts); break;
   }
   DLX_LAUNCHED("logreg_grad_kernel");
-  combine_parts_kernel<<<(d + 127) / 128, 128, 0, stream>>>(parts, grid, d, d_grad);
-  DLX_LAUNCHED("combine_parts_kernel");
-  return DLX_OK;
+  return combine_f64(parts, grid, d, d_grad, stream);
 }
 
 size_t dlx_gda_workspace_bytes(int64_t n, int32_t d) {
   const size_t p1 = static_cast<size_t>(row_grid(n)) * (2 * d * sizeof(double) + sizeof(long long)) + 1024;
-  const size_t p2 = static_cast<size_t>(gda2_grid(n)) * d * d * sizeof(double) + 256;
+  const size_t p2 = static_cast<size_t>(std::max(gda2_grid(n), gda_pass2_dmma_grid(n))) * d * d *
+                        sizeof(double) + 256;
   return std::max(p1, p2);
 }
 
@@ -320,11 +348,10 @@ int dlx_gda_pass1(const double* d_x, const int64_t* d_y, int64_t n, int32_t d, i
     default: gda_pass1_kernel<4><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, p0, p1, pn); break;
   }
   DLX_LAUNCHED("gda_pass1_kernel");
-  combine_parts_kernel<<<(d + 127) / 128, 128, 0, stream>>>(p0, grid, d, d_sum0);
-  combine_parts_kernel<<<(d + 127) / 128, 128, 0, stream>>>(p1, grid, d, d_sum1);
-  combine_parts_ll_kernel<<<1, 32, 0, stream>>>(pn, grid, reinterpret_cast<long long*>(d_n1));
-  DLX_LAUNCHED("gda combine");
-  return DLX_OK;
+  int rc = combine_f64(p0, grid, d, d_sum0, stream);
+  if (rc == DLX_OK) rc = combine_f64(p1, grid, d, d_sum1, stream);
+  if (rc == DLX_OK) rc = combine_i64(pn, grid, 1, reinterpret_cast<long long*>(d_n1), stream);
+  return rc;
 }
 
 int dlx_gda_means(const int64_t* d_n1, const double* d_sum0, const double* d_sum1,
@@ -340,6 +367,9 @@ int dlx_gda_pass2(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
                   const double* d_mu0, const double* d_mu1, double* d_scatter, void* d_workspace,
                   size_t workspace_bytes, dlx_stream_t stream) {
   DLX_REQUIRE(n >= 0 && d > 0, DLX_ERR_ARG, "gda: bad shape");
+  if (d <= 64)  // fp64 tensor-core (DMMA) scatter
+    return gda_pass2_dmma(d_x, reinterpret_cast<const long long*>(d_y), n, d, d_mu0, d_mu1,
+                          static_cast<double*>(d_workspace), workspace_bytes, d_scatter, stream);
   const int B = gda2_b(d);
   DLX_REQUIRE(B > 0, DLX_ERR_GENERATION, "GenerationFailed: gda pass 2 needs d <= 128 (got %d)", d);
   const int grid = gda2_grid(n);
@@ -355,10 +385,7 @@ int dlx_gda_pass2(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
     default: gda_pass2_kernel<8><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, d_mu0, d_mu1, parts); break;
   }
   DLX_LAUNCHED("gda_pass2_kernel");
-  const int dd = d * d;
-  combine_parts_kernel<<<(dd + 255) / 256, 256, 0, stream>>>(parts, grid, dd, d_scatter);
-  DLX_LAUNCHED("combine_parts_kernel");
-  return DLX_OK;
+  return combine_f64(parts, grid, static_cast<long long>(d) * d, d_scatter, stream);
 }
 
 int dlx_axpy_inplace(double* d_theta, const double* d_grad, double alpha, int64_t n,

@@ -28,15 +28,17 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  // try_wait with a suspend-time hint: the warp sleeps in hardware until the phase flips
+  // (or the hint expires) instead of spinning on the issue slots other roles need.
   const uint32_t a = smem_addr(bar);
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(a),
-      "r"(parity)
+      "r"(parity), "r"(0x989680u)
       : "memory");
 }
 

@@ -150,11 +150,12 @@ def kmeans_update(counts: torch.Tensor, sums: torch.Tensor, mu: torch.Tensor | N
     return mu
 
 
-def kmeans_last_recheck_count(device=None) -> int:
+def kmeans_last_recheck_count(n: int, d: int, k: int, device=None) -> int:
+    """Samples the last screened step (shape n, d, k) re-evaluated with the exact chain."""
     L = _lib.load()
-    ws, _ = _WS.get(256, _dev(device))
+    ws, _ = _WS.get(L.dlx_kmeans_workspace_bytes(n, d, k), _dev(device))
     v = ctypes.c_int64()
-    check(L.dlx_kmeans_last_recheck_count(ws, ctypes.byref(v), _stream()))
+    check(L.dlx_kmeans_last_recheck_count(ws, n, d, k, ctypes.byref(v), _stream()))
     return v.value
 
 

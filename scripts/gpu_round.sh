@@ -13,6 +13,13 @@ python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || echo
 for w in $WHAT; do
   case $w in
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log ;;
+    ktests) timeout 600 python -m pytest tests -m gpu -q -rf -x -k "screened or c1_step or c4 or kmeans" > $OUT/pytest_kmeans.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_kmeans.log ;;
+    benchk) timeout 600 python bench.py --config c4 --steps 20 --warmup 3 > $OUT/bench_c4.json 2> $OUT/bench_c4.err
+            timeout 600 python bench.py --config c1 --steps 20 --warmup 3 --no-cpu-baseline > $OUT/bench_c1.json 2> $OUT/bench_c1.err ;;
+    ncuk) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file $OUT/launches_c4.csv \
+           python bench.py --config c4 --steps 4 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch_bench.log 2>&1
+         timeout 1200 ncu --set full --clock-control none --import-source on -k regex:kmeans_screened -s 3 -c 1 -o $OUT/prof_kmeans \
+           python bench.py --config c4 --steps 4 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_kmeans.log 2>&1 ;;
     tests) timeout 1800 python -m pytest tests -m gpu -q -rf --durations=15 > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log ;;
     bench) for c in c4 c1 c2 l16 c3 c5; do
              timeout 600 python bench.py --config $c --steps 10 --warmup 3 > $OUT/bench_$c.json 2> $OUT/bench_$c.err

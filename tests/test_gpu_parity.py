@@ -157,7 +157,7 @@ def test_kmeans_screened_stress(ml, kind, method):
 def test_kmeans_screened_recheck_fraction(ml):
     x = dev_units(ml, 1 << 20, 64, seed=1)
     ml.kmeans_step(x, x[:64].clone(), method=SCREENED)
-    r = ml.kmeans_last_recheck_count()
+    r = ml.kmeans_last_recheck_count(1 << 20, 64, 64)
     print(f"screened recheck fraction at N=2^20, d=k=64: {r / (1 << 20):.5f}")
     assert 0 <= r < (1 << 20) // 10
 
