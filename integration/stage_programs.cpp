@@ -1,0 +1,217 @@
+// stage_programs.cpp — stages the hot-path programs through the reference DSL (stagekit,
+// built out of tree by oracle/ref.mk), fuses them with the reference's own fuse_loops (code
+// motion off: SURVEY §0.3), schedules, runs the reference's run_codegen, and writes for each
+// program one fixture JSON under tests/golden/staged/:
+//   - "program":  the executor descriptor (integration/stagekit_dlx.cpp::to_dlx_program)
+//   - "deg":      the reference's DEG JSON (codegen.cpp:569-588)
+//   - "minic":    the reference's emitted MiniC text
+//   - "expected": the output text of that MiniC program, executed by the oracle's MiniC
+//                 evaluator (oracle/minic_eval.hpp, the restated missing interp.cpp)
+// The GPU tests run "program" through dlx_program_run and compare with "expected".
+//
+//   oracle/_ref/stage_programs OUT_DIR        (built by `make -C oracle -f ref.mk`)
+#include <chrono>
+#include <cstdio>
+#include <fstream>
+#include <functional>
+#include <iostream>
+#include <json.hpp>
+#include <string>
+#include <vector>
+
+#include "integration/stagekit_dlx.hpp"
+#include "oracle/minic_eval.hpp"
+#include "stagekit/codegen.hpp"
+#include "stagekit/fusion.hpp"
+#include "stagekit/loops.hpp"
+#include "stagekit/stage.hpp"
+#include "stagekit/vectordsl.hpp"
+
+using namespace stagekit;
+using json = nlohmann::ordered_json;
+
+namespace {
+
+DVal plus(Stage& st, DVal a, DVal b) { return DVal{&st, st.numeric(Op::Plus, a.e, b.e)}; }
+
+// k-means: one collect (argmin chain over k inner distance reduces) + k*(d+1) predicated
+// reduces per iteration; mu is a mutable vector updated from sums/counts; the assignment
+// vector escapes (printed) so fusion keeps its elem live.
+void kmeans(Stage& st, int64_t n, int d, int k, int iters) {
+  DVec x = vec_rand(st, st.lit(n * d));
+  DVec mu = vec_alloc(st, st.lit(int64_t{k} * d), SemType::f64());
+  for (int e = 0; e < k * d; ++e) mu.update(st.lit(int64_t{e}), x.at(st.lit(int64_t{e})));
+  for (int it = 0; it < iters; ++it) {
+    DVec assign = mk_collect(st, st.lit(n), [&](DInt i) -> DVal {
+      DDouble best = st.lit(1e300);
+      DInt idx = st.lit(int64_t{0});
+      for (int c = 0; c < k; ++c) {
+        DDouble dist(mk_reduce(
+            st, st.lit(int64_t{d}), st.lit(0.0),
+            [&](DInt j) -> DVal {
+              DDouble xv = x.at_d(i * st.lit(int64_t{d}) + j);
+              DDouble mv = mu.at_d(st.lit(int64_t{c} * d) + j);
+              DDouble diff = xv - mv;
+              return diff * diff;
+            },
+            [&](DVal l, DVal r) { return plus(st, l, r); }));
+        DBool lt = dist < best;
+        best = st.if_then_else<DDouble>(lt, [&] { return dist; }, [&] { return best; });
+        idx = st.if_then_else<DInt>(lt, [&] { return st.lit(int64_t{c}); }, [&] { return idx; });
+      }
+      return idx;
+    });
+    st.print(assign.at_i(st.lit(int64_t{0})));
+    std::vector<DInt> counts;
+    std::vector<DDouble> sums;
+    for (int c = 0; c < k; ++c) {
+      std::function<DBool(DInt)> in_c = [&, c](DInt i) { return assign.at_i(i) == st.lit(int64_t{c}); };
+      counts.push_back(DInt(mk_reduce(
+          st, st.lit(n), st.lit(int64_t{0}), [&](DInt) -> DVal { return st.lit(int64_t{1}); },
+          [&](DVal l, DVal r) { return plus(st, l, r); }, &in_c)));
+      for (int j = 0; j < d; ++j)
+        sums.push_back(DDouble(mk_reduce(
+            st, st.lit(n), st.lit(0.0),
+            [&, j](DInt i) -> DVal { return x.at(i * st.lit(int64_t{d}) + st.lit(int64_t{j})); },
+            [&](DVal l, DVal r) { return plus(st, l, r); }, &in_c)));
+    }
+    for (int c = 0; c < k; ++c) {
+      st.print(counts[c]);
+      DDouble cnt = st.to_double(counts[c]);
+      for (int j = 0; j < d; ++j) mu.update(st.lit(int64_t{c} * d + j), sums[c * d + j] / cnt);
+    }
+  }
+  for (int e = 0; e < k * d; ++e) st.print(mu.at(st.lit(int64_t{e})));
+}
+
+// GroupBy / Naive-Bayes counts: K predicated count reduces keyed on a random int vector.
+void groupby(Stage& st, int64_t n, int K) {
+  DVec keys = vec_rand_int(st, st.lit(n), st.lit(int64_t{K}));
+  std::vector<DInt> cnt;
+  for (int b = 0; b < K; ++b) {
+    std::function<DBool(DInt)> is_b = [&, b](DInt i) { return keys.at_i(i) == st.lit(int64_t{b}); };
+    cnt.push_back(DInt(mk_reduce(
+        st, st.lit(n), st.lit(int64_t{0}), [&](DInt) -> DVal { return st.lit(int64_t{1}); },
+        [&](DVal l, DVal r) { return plus(st, l, r); }, &is_b)));
+  }
+  for (auto& c : cnt) st.print(c);
+}
+
+// GDA: pass 1 (class count + per-class sums), pass 2 (d*d scatter with per-class mean select).
+void gda(Stage& st, int64_t n, int d) {
+  DVec x = vec_rand(st, st.lit(n * d));
+  DVec y = vec_rand_int(st, st.lit(n), st.lit(int64_t{2}));
+  std::function<DBool(DInt)> is1 = [&](DInt i) { return y.at_i(i) == st.lit(int64_t{1}); };
+  std::function<DBool(DInt)> is0 = [&](DInt i) { return y.at_i(i) == st.lit(int64_t{0}); };
+  DInt n1(mk_reduce(st, st.lit(n), st.lit(int64_t{0}), [&](DInt) -> DVal { return st.lit(int64_t{1}); },
+                    [&](DVal l, DVal r) { return plus(st, l, r); }, &is1));
+  std::vector<DDouble> mu0, mu1;
+  DDouble nn1 = st.to_double(n1);
+  DDouble nn0 = st.to_double(st.lit(n) - n1);
+  for (int j = 0; j < d; ++j) {
+    auto xj = [&, j](DInt i) -> DVal { return x.at(i * st.lit(int64_t{d}) + st.lit(int64_t{j})); };
+    DDouble s0(mk_reduce(st, st.lit(n), st.lit(0.0), xj, [&](DVal l, DVal r) { return plus(st, l, r); }, &is0));
+    DDouble s1(mk_reduce(st, st.lit(n), st.lit(0.0), xj, [&](DVal l, DVal r) { return plus(st, l, r); }, &is1));
+    mu0.push_back(s0 / nn0);
+    mu1.push_back(s1 / nn1);
+  }
+  st.print(n1);
+  for (int j = 0; j < d; ++j) {
+    st.print(mu0[j]);
+    st.print(mu1[j]);
+  }
+  for (int a = 0; a < d; ++a)
+    for (int b = 0; b < d; ++b) {
+      DDouble s(mk_reduce(
+          st, st.lit(n), st.lit(0.0),
+          [&, a, b](DInt i) -> DVal {
+            DBool c1 = y.at_i(i) == st.lit(int64_t{1});
+            DDouble ma = st.if_then_else<DDouble>(c1, [&] { return mu1[a]; }, [&] { return mu0[a]; });
+            DDouble mb = st.if_then_else<DDouble>(c1, [&] { return mu1[b]; }, [&] { return mu0[b]; });
+            DDouble da = x.at_d(i * st.lit(int64_t{d}) + st.lit(int64_t{a})) - ma;
+            DDouble db = x.at_d(i * st.lit(int64_t{d}) + st.lit(int64_t{b})) - mb;
+            return da * db;
+          },
+          [&](DVal l, DVal r) { return plus(st, l, r); }));
+      st.print(s);
+    }
+}
+
+// mean_variance demo: mean and variance fuse into one loop.
+void mean_variance(Stage& st, int64_t n) {
+  DVec x = vec_rand(st, st.lit(n));
+  st.print(mean(st, x));
+  st.print(variance(st, x));
+}
+
+// axpy demo: a*x + y collect, then a sum and two element reads.
+void axpy(Stage& st, int64_t n) {
+  DVec x = vec_rand(st, st.lit(n));
+  DVec y = vec_rand(st, st.lit(n));
+  DDouble a = st.lit(2.5);
+  DVec z = x.zip_with(y, [&](DVal u, DVal v) -> DVal { return a * DDouble(u) + DDouble(v); });
+  st.print(z.at(st.lit(int64_t{0})));
+  st.print(z.at(st.lit(n - 1)));
+  st.print(z.sum());
+}
+
+// count_gt7 demo family: a predicated count over a scaled random vector.
+void count_gt(Stage& st, int64_t n) {
+  DVec x = vec_rand(st, st.lit(n));
+  st.print(x.count_where([&](DVal v) { return st.lit(0.7) < DDouble(v); }));
+  st.print(x.sum());
+}
+
+struct Spec {
+  std::string name;
+  std::function<void(Stage&)> body;
+};
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  const std::string out_dir = argc > 1 ? argv[1] : "tests/golden/staged";
+  const uint64_t seed = 1;
+  std::vector<Spec> specs = {
+      {"kmeans_n4096_d16_k8_it2", [](Stage& st) { kmeans(st, 4096, 16, 8, 2); }},
+      {"kmeans_n65536_d16_k8_it1", [](Stage& st) { kmeans(st, 65536, 16, 8, 1); }},
+      {"groupby_n100000_k16", [](Stage& st) { groupby(st, 100000, 16); }},
+      {"gda_n20000_d4", [](Stage& st) { gda(st, 20000, 4); }},
+      {"mean_variance_n100000", [](Stage& st) { mean_variance(st, 100000); }},
+      {"axpy_n100000", [](Stage& st) { axpy(st, 100000); }},
+      {"count_gt_n100000", [](Stage& st) { count_gt(st, 100000); }},
+  };
+  for (const Spec& sp : specs) {
+    const auto t0 = std::chrono::steady_clock::now();
+    Stage st;
+    st.begin();
+    sp.body(st);
+    st.finish();
+    auto g = st.take_graph();
+    FusionOutcome fo = fuse_loops(g, /*with_motion=*/false);
+    Schedule s = build_schedule(*fo.graph, ScheduleOptions{true, false});
+    CodegenResult cg = run_codegen(*fo.graph, s);
+    const auto t1 = std::chrono::steady_clock::now();
+    oracle_minic::Evaluator ev(seed);
+    oracle_minic::EvalResult r = ev.run(cg.program);
+    const auto t2 = std::chrono::steady_clock::now();
+    int loops = 0;
+    for (int32_t idx : s.block_stmts(fo.graph->root()))
+      if (fo.graph->stmts()[idx].is_loop()) ++loops;
+    json fx;
+    fx["name"] = sp.name;
+    fx["seed"] = seed;
+    fx["fused_pairs"] = fo.fused_pairs;
+    fx["root_loops"] = loops;
+    fx["program"] = json::parse(stagekit_dlx::to_dlx_program(*fo.graph, s));
+    fx["deg"] = json::parse(cg.deg_json);
+    fx["minic"] = cg.minic_text;
+    fx["expected"] = r.output;
+    std::ofstream(out_dir + "/" + sp.name + ".json") << fx.dump(1) << "\n";
+    std::printf("%-28s fused_pairs=%d root_loops=%d stage+fuse+codegen %.2fs  minic eval %.2fs\n",
+                sp.name.c_str(), fo.fused_pairs, loops,
+                std::chrono::duration<double>(t1 - t0).count(),
+                std::chrono::duration<double>(t2 - t1).count());
+  }
+  return 0;
+}

@@ -1,0 +1,134 @@
+// stagekit_dlx.cpp — serialiser from the reference IR (stagekit Graph + Schedule) to the
+// executor's multiloop descriptor.  See stagekit_dlx.hpp.  Written against the reference's
+// public headers only (proj/include/stagekit/*.hpp).
+#include "stagekit_dlx.hpp"
+
+#include <json.hpp>
+#include <set>
+
+#include "stagekit/node.hpp"
+
+namespace stagekit_dlx {
+
+using namespace stagekit;
+using json = nlohmann::ordered_json;
+
+namespace {
+
+json expr_json(const Expr& e) {
+  json j;
+  if (e.is_sym()) {
+    j["s"] = e.sym;
+  } else if (e.lit.is_int()) {
+    j["i"] = e.lit.i();
+  } else if (e.lit.is_double()) {
+    j["d"] = e.lit.d();
+  } else if (e.lit.is_bool()) {
+    j["b"] = e.lit.b();
+  } else if (e.lit.is_str()) {
+    j["str"] = e.lit.s();
+  } else {
+    j["u"] = 1;
+  }
+  j["t"] = e.ty.to_string();
+  return j;
+}
+
+struct Writer {
+  const Graph& g;
+  const Schedule& s;
+  json stmts = json::object();
+  json blocks = json::object();
+  std::set<BlockId> seen;
+
+  void block(BlockId b) {
+    if (b == kNoBlock || seen.count(b)) return;
+    seen.insert(b);
+    const BlockData& bd = g.block(b);
+    json jb;
+    jb["stmts"] = json::array();
+    for (int32_t idx : s.block_stmts(b)) {
+      jb["stmts"].push_back(g.stmts()[idx].sym);
+      stmt(idx);
+    }
+    jb["result"] = expr_json(bd.result);
+    jb["bound"] = bd.bound;
+    blocks[std::to_string(b)] = std::move(jb);
+  }
+
+  void stmt(int32_t idx) {
+    const Statement& st = g.stmts()[idx];
+    json js;
+    js["op"] = op_name(st.def.op);
+    js["ty"] = st.ty.to_string();
+    js["args"] = json::array();
+    for (const Expr& a : st.def.args) js["args"].push_back(expr_json(a));
+    if (!st.def.blocks.empty()) js["blocks"] = st.def.blocks;
+    if (!st.def.aux_ty.is(Ty::Unit)) js["aux_ty"] = st.def.aux_ty.to_string();
+    if (!st.def.str.empty()) js["str"] = st.def.str;
+    if (!st.def.lits.empty()) {
+      js["lits"] = json::array();
+      for (const Lit& l : st.def.lits) {
+        json jl;
+        if (l.is_int()) jl["i"] = l.i();
+        else if (l.is_double()) jl["d"] = l.d();
+        else if (l.is_bool()) jl["b"] = l.b();
+        js["lits"].push_back(jl);
+      }
+    }
+    for (BlockId b : st.def.blocks) block(b);
+    if (st.def.loop) {
+      const LoopPayload& lp = *st.def.loop;
+      json jl;
+      jl["range"] = expr_json(lp.range);
+      jl["index"] = lp.index_var;
+      jl["body"] = lp.body_scope;
+      block(lp.body_scope);
+      jl["elems"] = json::array();
+      for (size_t k = 0; k < lp.elems.size(); ++k) {
+        const LoopElem& el = lp.elems[k];
+        json je;
+        je["kind"] = el.kind == LoopElem::K::Collect ? "collect"
+                     : el.kind == LoopElem::K::Reduce ? "reduce"
+                                                      : "foreach";
+        je["live"] = s.elem_live(idx, k);
+        je["out"] = el.out;
+        je["out_ty"] = el.out_ty.to_string();
+        je["elem"] = el.elem;
+        je["cond"] = el.cond;
+        je["combine"] = el.combine;
+        je["append"] = el.append;
+        if (el.kind == LoopElem::K::Reduce) {
+          je["zero"] = expr_json(el.zero);
+          je["rv_left"] = el.rv_left;
+          je["rv_right"] = el.rv_right;
+        }
+        if (s.elem_live(idx, k)) {
+          block(el.elem);
+          block(el.cond);
+          block(el.combine);
+        }
+        jl["elems"].push_back(std::move(je));
+      }
+      js["loop"] = std::move(jl);
+    }
+    stmts[std::to_string(st.sym)] = std::move(js);
+  }
+};
+
+}  // namespace
+
+std::string to_dlx_program(const Graph& g, const Schedule& s) {
+  Writer w{g, s};
+  w.block(g.root());
+  json j;
+  j["format"] = "dlx-program/1";
+  j["root"] = g.root();
+  j["stmts"] = std::move(w.stmts);
+  j["blocks"] = std::move(w.blocks);
+  // the DEG exactly as the reference builds it (codegen.cpp:497-588)
+  j["deg"] = json::parse(deg_to_json(build_kernels(g, s)));
+  return j.dump();
+}
+
+}  // namespace stagekit_dlx

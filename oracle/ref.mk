@@ -34,10 +34,13 @@ $(OUT)/libstagekit.a: $(OBJS)
 	ar rcs $@ $^
 
 # stage_programs: stages the hot-path programs through the reference DSL (fuse_loops with
-# motion off, build_schedule, run_codegen), prints MiniC + DEG and emits the executor's
-# multiloop descriptors (adapter/stage_programs.cpp, our code).
-$(OUT)/stage_programs: adapter/stage_programs.cpp adapter/minic_eval.hpp $(OUT)/libstagekit.a
-	$(CXX) $(CXXFLAGS) -I. -o $@ adapter/stage_programs.cpp $(OUT)/libstagekit.a
+# motion off, build_schedule, run_codegen) and writes the staged fixtures under
+# tests/golden/staged/ (integration/stage_programs.cpp + the serializer
+# integration/stagekit_dlx.cpp + the MiniC evaluator oracle/minic_eval.hpp: our code).
+$(OUT)/stage_programs: ../integration/stage_programs.cpp ../integration/stagekit_dlx.cpp \
+                      ../integration/stagekit_dlx.hpp minic_eval.hpp $(OUT)/libstagekit.a
+	$(CXX) $(CXXFLAGS) -I.. -o $@ ../integration/stage_programs.cpp ../integration/stagekit_dlx.cpp \
+	    $(OUT)/libstagekit.a
 
 clean:
 	rm -rf $(OUT)

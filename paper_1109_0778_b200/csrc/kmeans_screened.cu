@@ -88,7 +88,13 @@ struct Misc {
   int assign[kTile];
   int pcount[4];
   uint32_t cscr[2][8];
+  int wcnt[4][kMaxK];       // per quarter: samples of the tile assigned to c
+  int woff[4][kMaxK];       // per quarter: first slot of its c-samples in `sorted`
+  int cstart[kMaxK + 1];    // per centroid: [cstart[c], cstart[c+1]) in `sorted`
+  int sorted[kTile];        // the tile's resolved samples, stably sorted by centroid
 };
+constexpr int kInvalidNm = 0x70000000;  // > any valid score (|Q| < 2^28, nm < 2^30)
+constexpr int kNoCandidate = 0x60000000;
 constexpr uint32_t kSmemBytes = kOffMisc + sizeof(Misc);
 static_assert(kSmemBytes <= 232448, "shared-memory plan exceeds 227 KiB");
 
@@ -289,7 +295,9 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         S.tile_flag[s] = flag;
       }
       if (ct < kMaxK) {  // |mu_c|^2 in units U_t = 2^(e_t+e_m-22): < 2^30 under the gap guard
-        S.nmt[s][ct] = flag ? 0 : __double2int_rd(S.nmf[ct] * ldexp(1.0, 22 - et - em));
+        S.nmt[s][ct] = (flag || !((S.valid >> ct) & 1))
+                           ? kInvalidNm
+                           : __double2int_rd(S.nmf[ct] * ldexp(1.0, 22 - et - em));
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -305,7 +313,6 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     const int h = ew >> 2;                  // centroid half
     const int q = quarter * 32 + lane;      // sample row within the tile
     const int mabs = S.mpos + S.mneg;       // >= max_c Mpos_c - min_c' Mneg_c'
-    const unsigned long long valid = S.valid;
     const unsigned long long kmask = k == 64 ? ~0ull : ((1ull << k) - 1);
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
     long long* my_pidx = pend_idx + static_cast<size_t>(blockIdx.x) * pend_cap;
@@ -326,8 +333,9 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       mbar_wait(&S.tfull[b], (m >> 1) & 1);
       tc_fence_after();
       int tv[32];
-      int lmin = INT_MAX;
+      int lmin = kInvalidNm;
       if (!flag) {
+        const int4* nm4 = reinterpret_cast<const int4*>(&S.nmt[s][32 * h]);
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
           const uint32_t col = b * kAccCols + 32 * h + 16 * ch;
@@ -335,12 +343,20 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
           tmem_ld16(tmem + lane_base + col, hh);
           tmem_ld16(tmem + lane_base + col + 64, cr);
           tmem_ld16(tmem + lane_base + col + 128, ll);
+          int nm[16];
+#pragma unroll
+          for (int u4 = 0; u4 < 4; ++u4) {
+            const int4 v4 = nm4[4 * ch + u4];
+            nm[4 * u4 + 0] = v4.x;
+            nm[4 * u4 + 1] = v4.y;
+            nm[4 * u4 + 2] = v4.z;
+            nm[4 * u4 + 3] = v4.w;
+          }
           tmem_ld_wait();
 #pragma unroll
           for (int u = 0; u < 16; ++u) {
-            const int c = 32 * h + 16 * ch + u;
-            const int Q = hh[u] * 256 + cr[u] + (ll[u] >> 8);
-            const int v = ((valid >> c) & 1) ? S.nmt[s][c] - 2 * Q : INT_MAX;
+            // invalid centroids: zero B rows (Q = 0) and nm = kInvalidNm
+            const int v = nm[u] - 2 * (hh[u] * 256 + cr[u] + (ll[u] >> 8));
             tv[16 * ch + u] = v;
             lmin = min(lmin, v);
           }
@@ -354,19 +370,19 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       uint32_t mask = 0;
       if (!flag) {
         const int tmin = min(S.hmin[0][q], S.hmin[1][q]);
-        if (tmin != INT_MAX) {
-          const int w = 6 + (S.absx[s][q] + mabs + d + 127) / 128;
-          const int thr = tmin + w;
+        if (tmin < kNoCandidate) {
+          const int thr = tmin + 6 + (S.absx[s][q] + mabs + d + 127) / 128;
 #pragma unroll
-          for (int u = 0; u < 32; ++u) mask |= (tv[u] <= thr ? 1u : 0u) << u;
+          for (int u = 0; u < 32; ++u)
+            if (tv[u] <= thr) mask |= 1u << u;
         }
       }
       S.cmask[h][q] = mask;
       named_bar(1, 256);
       unsigned long long full = 0;
       bool pend = false;
+      int a = -1, rank = 0;
       if (h == 0) {
-        int a = -1;
         if (q < rows) {
           if (flag) {
             full = kmask;  // guarded tile: the reference chain over every centroid
@@ -383,7 +399,14 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
           }
           if (a >= 0 && assign) assign[t * kTile + q] = a;
         }
-        S.assign[q] = a;
+        // stable counting sort of the quarter's samples by centroid: rank within the warp
+        const unsigned grp = __match_any_sync(0xffffffffu, a);
+        const unsigned lower = grp & ((1u << lane) - 1);
+        rank = __popc(lower);
+        S.wcnt[quarter][lane] = 0;
+        S.wcnt[quarter][lane + 32] = 0;
+        __syncwarp();
+        if (lower == 0 && a >= 0) S.wcnt[quarter][a] = __popc(grp);
       }
       const unsigned pb = __ballot_sync(0xffffffffu, pend);
       if (h == 0 && lane == 0) S.pcount[quarter] = __popc(pb);
@@ -399,27 +422,48 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         }
         pending += p0 + p1 + p2 + S.pcount[3];
       }
-      // bucket-reduce: warp ew owns centroids ew + 8u, lane owns columns 2*lane, 2*lane+1
-      int av[4];
+      if (ew == 0) {  // one warp: per-centroid totals, exclusive scan, per-quarter offsets
+        const int c0 = 2 * lane, c1 = c0 + 1;
+        int w0[4], w1[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) av[i] = S.assign[32 * i + lane];
+        for (int Q = 0; Q < 4; ++Q) w0[Q] = S.wcnt[Q][c0], w1[Q] = S.wcnt[Q][c1];
+        const int t0 = w0[0] + w0[1] + w0[2] + w0[3], t1 = w1[0] + w1[1] + w1[2] + w1[3];
+        int incl = t0 + t1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const int s0 = incl - t0 - t1, s1 = s0 + t0;
+        S.cstart[c0] = s0;
+        S.cstart[c1] = s1;
+        if (lane == 31) S.cstart[kMaxK] = incl;
+        int r0 = s0, r1 = s1;
+#pragma unroll
+        for (int Q = 0; Q < 4; ++Q) {
+          S.woff[Q][c0] = r0;
+          S.woff[Q][c1] = r1;
+          r0 += w0[Q];
+          r1 += w1[Q];
+        }
+      }
+      named_bar(1, 256);
+      if (h == 0 && a >= 0) S.sorted[S.woff[quarter][a] + rank] = q;
+      named_bar(1, 256);
+      // bucket-reduce: warp ew owns centroids ew + 8u, lane owns columns 2*lane, 2*lane+1;
+      // each centroid's samples are contiguous in `sorted`, in ascending row order
       const int j0 = 2 * lane;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int c = ew + 8 * u;
         if (c >= k) break;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          unsigned mm = __ballot_sync(0xffffffffu, av[i] == c);
-          cnt[u] += __popc(mm);
-          while (mm) {
-            const int row = 32 * i + __ffs(mm) - 1;
-            mm &= mm - 1;
-            if (j0 < d) {
-              const double2 v = *reinterpret_cast<const double2*>(xs + row * d + j0);
-              acc[u][0] += v.x;
-              acc[u][1] += v.y;
-            }
+        const int beg = S.cstart[c], end = S.cstart[c + 1];
+        cnt[u] += end - beg;
+        if (j0 < d) {
+          for (int p = beg; p < end; ++p) {
+            const double2 v = *reinterpret_cast<const double2*>(xs + S.sorted[p] * d + j0);
+            acc[u][0] += v.x;
+            acc[u][1] += v.y;
           }
         }
       }
@@ -449,106 +493,120 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
 
 // ---------------------------------------------------------------------------------------
 // resolve: the reference chain for the pending samples.  Resolve CTA rb handles slice
-// rb % kResSplit of main-kernel CTA rb / kResSplit's pending list: warps take samples, lanes
-// take candidate centroids (ascending), the chain merge keeps the reference order; the rows
-// are then gathered into shared memory and folded into this CTA's partial record in list
+// rb % kResSplit of main-kernel CTA rb / kResSplit's pending list, in chunks of kResChunk
+// samples: the chunk's rows are gathered into shared memory next to the fp64 centroids,
+// every (sample, candidate) pair is one thread's exact chain (sequential j, no FMA), each
+// sample then merges its candidates in ascending centroid order (strict <, NaN never
+// wins, start (1e300, 0)), and the rows are folded into this CTA's partial record in list
 // order (deterministic).
-constexpr int kResThreads = 512;
+constexpr int kResThreads = 256;
 constexpr int kResSplit = 4;
-constexpr int kResChunk = 128;
+constexpr int kResChunk = 64;
+constexpr int kResMaxPairs = kResChunk * kMaxK;
 
 __global__ void __launch_bounds__(kResThreads)
 kmeans_resolve_kernel(const double* __restrict__ x, int d, int k, const double* __restrict__ mu,
                       int32_t* __restrict__ assign, const long long* __restrict__ pend_idx,
-                      unsigned long long* __restrict__ pend_mask,
+                      const unsigned long long* __restrict__ pend_mask,
                       const long long* __restrict__ pend_count, long long pend_cap,
                       long long* __restrict__ part_counts, double* __restrict__ part_sums) {
   extern __shared__ double rsm[];
-  double* sums_s = rsm;                          // k*d
-  double* rows_s = rsm + k * d;                  // kResChunk*d
+  double* mu_s = rsm;                          // k*d
+  double* sums_s = mu_s + k * d;               // k*d
+  double* rows_s = sums_s + k * d;             // kResChunk*d
+  double* dist_s = rows_s + kResChunk * d;     // kResMaxPairs
   __shared__ long long idx_s[kResChunk];
+  __shared__ unsigned long long mask_s[kResChunk];
+  __shared__ int first_s[kResChunk + 1];
   __shared__ int a_s[kResChunk];
   __shared__ long long cnt_s[kMaxK];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int src = blockIdx.x / kResSplit, slice = blockIdx.x % kResSplit;
   const long long total = pend_count[src];
   const long long lo = total * slice / kResSplit, hi = total * (slice + 1) / kResSplit;
   const long long* pidx = pend_idx + static_cast<size_t>(src) * pend_cap;
-  unsigned long long* pmask = pend_mask + static_cast<size_t>(src) * pend_cap;
-  for (int e = tid; e < k * d; e += kResThreads) sums_s[e] = 0.0;
+  const unsigned long long* pmask = pend_mask + static_cast<size_t>(src) * pend_cap;
+  for (int e = tid; e < k * d; e += kResThreads) {
+    mu_s[e] = mu[e];
+    sums_s[e] = 0.0;
+  }
   for (int c = tid; c < k; c += kResThreads) cnt_s[c] = 0;
-  // phase 1: one warp per pending sample, one lane per candidate centroid
-  for (long long e = lo + warp; e < hi; e += kResThreads / 32) {
-    const long long i = pidx[e];
-    const double* xr = x + i * d;
-    unsigned long long mask = pmask[e];
-    double best = 1e300;
-    int bi = 0;
-    while (mask) {  // rounds of up to 32 candidates, ascending centroid index
-      unsigned long long rest = mask;
-      int c = -1;
-      for (int r = 0; r <= lane && rest; ++r) {  // c = the lane-th remaining candidate
-        const int cc = __ffsll(static_cast<long long>(rest)) - 1;
-        rest &= rest - 1;
-        if (r == lane) c = cc;
-      }
-      double v = 1e300;
-      if (c >= 0) {
-        const double* m = mu + c * d;
-        double acc = 0.0;
-#pragma unroll 8
-        for (int j = 0; j < d; ++j) {
-          const double diff = __dsub_rn(__ldg(xr + j), __ldg(m + j));
-          acc = __dadd_rn(acc, __dmul_rn(diff, diff));
-        }
-        v = acc;
-      }
-      // chain merge in ascending lane (= ascending centroid) order: strict <, NaN never wins
-      const unsigned live = __ballot_sync(0xffffffffu, c >= 0);
-      for (int l = 0; l < 32; ++l) {
-        if (!((live >> l) & 1)) break;
-        const double vl = __shfl_sync(0xffffffffu, v, l);
-        const int cl = __shfl_sync(0xffffffffu, c, l);
-        if (vl < best) {
-          best = vl;
-          bi = cl;
-        }
-      }
-      for (int r = 0; r < 32 && mask; ++r) mask &= mask - 1;  // drop this round's candidates
+  constexpr int R = kResThreads / 64;
+  const int jj = tid & 63, rr = tid >> 6;
+  for (long long base = lo; base < hi; base += kResChunk) {
+    const int nrow = static_cast<int>(hi - base < kResChunk ? hi - base : kResChunk);
+    __syncthreads();
+    for (int e = tid; e < nrow; e += kResThreads) {
+      idx_s[e] = pidx[base + e];
+      mask_s[e] = pmask[base + e];
     }
-    if (lane == 0) {
-      if (assign) assign[i] = bi;
-      pmask[e] = static_cast<unsigned long long>(bi);  // reuse the slot for phase 2
+    __syncthreads();
+    if (tid < 32) {  // exclusive scan of candidate counts -> pair offsets
+      int run = 0;
+      for (int e0 = 0; e0 < nrow; e0 += 32) {
+        const int e = e0 + tid;
+        const int c = e < nrow ? __popcll(mask_s[e]) : 0;
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (tid >= o) incl += t;
+        }
+        if (e < nrow) first_s[e] = run + incl - c;
+        run += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (tid == 0) first_s[nrow] = run;
+    }
+    for (int e = tid; e < nrow * d; e += kResThreads) {
+      const int r = e / d, j = e - r * d;
+      rows_s[e] = __ldg(x + idx_s[r] * d + j);
+    }
+    __syncthreads();
+    const int npairs = first_s[nrow];
+    for (int p = tid; p < npairs; p += kResThreads) {
+      int r = 0;  // owning sample: last r with first_s[r] <= p
+      for (int step = kResChunk; step > 0; step >>= 1)
+        if (r + step < nrow && first_s[r + step] <= p) r += step;
+      unsigned long long m = mask_s[r];
+      for (int t = p - first_s[r]; t > 0; --t) m &= m - 1;  // the t-th candidate of r
+      const int c = __ffsll(static_cast<long long>(m)) - 1;
+      const double* xr = rows_s + r * d;
+      const double* mr = mu_s + c * d;
+      double acc = 0.0;
+      for (int j = 0; j < d; ++j) {
+        const double diff = __dsub_rn(xr[j], mr[j]);
+        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+      }
+      dist_s[p] = acc;
+    }
+    __syncthreads();
+    for (int r = tid; r < nrow; r += kResThreads) {
+      double best = 1e300;
+      int bi = 0;
+      unsigned long long m = mask_s[r];
+      for (int p = first_s[r]; p < first_s[r + 1]; ++p) {
+        const int c = __ffsll(static_cast<long long>(m)) - 1;
+        m &= m - 1;
+        if (dist_s[p] < best) {
+          best = dist_s[p];
+          bi = c;
+        }
+      }
+      a_s[r] = bi;
+      if (assign) assign[idx_s[r]] = bi;
+    }
+    __syncthreads();
+    if (jj < d) {  // fold rows in list order; thread (rr, jj) owns cells (c, jj), c % R == rr
+      for (int r = 0; r < nrow; ++r) {
+        const int a = a_s[r];
+        if (a % R == rr) {
+          sums_s[a * d + jj] += rows_s[r * d + jj];
+          if (jj == 0) cnt_s[a] += 1;
+        }
+      }
     }
   }
   __syncthreads();
-  // phase 2: gather the rows chunk by chunk, fold them in list order; thread (r, j) owns
-  // cells (c, j) with c % (kResThreads/64) == r
-  constexpr int R = kResThreads / 64;
-  const int j = tid & 63, r = tid >> 6;
-  for (long long base = lo; base < hi; base += kResChunk) {
-    const int nrow = static_cast<int>(hi - base < kResChunk ? hi - base : kResChunk);
-    for (int e = tid; e < nrow; e += kResThreads) {
-      idx_s[e] = pidx[base + e];
-      a_s[e] = static_cast<int>(pmask[base + e]);
-    }
-    __syncthreads();
-    for (int e = tid; e < nrow * d; e += kResThreads) {
-      const int rr = e / d, jj = e - rr * d;
-      rows_s[e] = __ldg(x + idx_s[rr] * d + jj);
-    }
-    __syncthreads();
-    if (j < d) {
-      for (int e = 0; e < nrow; ++e) {
-        const int a = a_s[e];
-        if (a % R == r) {
-          sums_s[a * d + j] += rows_s[e * d + j];
-          if (j == 0) cnt_s[a] += 1;
-        }
-      }
-    }
-    __syncthreads();
-  }
   double* ps = part_sums + static_cast<size_t>(blockIdx.x) * k * d;
   for (int e = tid; e < k * d; e += kResThreads) ps[e] = sums_s[e];
   for (int c = tid; c < k; c += kResThreads) part_counts[static_cast<size_t>(blockIdx.x) * k + c] = cnt_s[c];
@@ -615,7 +673,8 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
   sk::kmeans_screened_kernel<<<grid, sk::kThreads, sk::kSmemBytes, stream>>>(
       x, n, d, k, mu, assign, w.part_counts, w.part_sums, w.pend_idx, w.pend_mask, w.pend_count, cap);
   DLX_LAUNCHED("kmeans_screened_kernel");
-  const size_t rsmem = static_cast<size_t>(k + sk::kResChunk) * d * sizeof(double);
+  const size_t rsmem =
+      (static_cast<size_t>(2 * k + sk::kResChunk) * d + sk::kResMaxPairs) * sizeof(double);
   DLX_CUDA(cudaFuncSetAttribute(sk::kmeans_resolve_kernel,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsmem)));
   sk::kmeans_resolve_kernel<<<grid * sk::kResSplit, sk::kResThreads, rsmem, stream>>>(
