@@ -124,6 +124,9 @@ int dlx_gda_pass2(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
                   const double* d_mu0, const double* d_mu1, double* d_scatter, void* d_workspace,
                   size_t workspace_bytes, dlx_stream_t stream);
 
+/* Vector[Int] from the int32 device assignments (reference Int is int64, types.hpp:11-20). */
+int dlx_widen_i32_i64(const int32_t* d_in, int64_t n, int64_t* d_out, dlx_stream_t stream);
+
 /* ---- generic Collect / Reduce families (map, zipWith, sum, count_where, mean/variance) -- */
 int dlx_map_axpy(double a, const double* d_x, const double* d_y, int64_t n, double* d_out,
                  dlx_stream_t stream);

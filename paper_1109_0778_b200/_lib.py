@@ -84,6 +84,11 @@ _SIGS = {
     "dlx_reduce_sum_i64": (_int, [_vp, _i64, _vp, _vp, _sz, _vp]),
     "dlx_reduce_sum_sumsq_f64": (_int, [_vp, _i64, _vp, _vp, _sz, _vp]),
     "dlx_reduce_count_gt_f64": (_int, [_vp, _i64, _dbl, _vp, _vp, _sz, _vp]),
+    "dlx_widen_i32_i64": (_int, [_vp, _i64, _vp, _vp]),
+    "dlx_vm_workspace_bytes": (_sz, [_i64]),
+    "dlx_vm_run_loop": (_int, [_vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "dlx_program_run": (_int, [ctypes.c_char_p, _u64, _int, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p)]),
+    "dlx_string_free": (None, [_vp]),
     "dlx_comm_unique_id": (_int, [ctypes.c_char_p]),
     "dlx_comm_init": (_int, [ctypes.POINTER(_vp), ctypes.c_char_p, _int, _int]),
     "dlx_comm_destroy": (_int, [_vp]),

@@ -28,6 +28,12 @@ __global__ void axpy_kernel(double a, const double* __restrict__ x, const double
     out[i] = __dadd_rn(__dmul_rn(a, x[i]), y[i]);
 }
 
+__global__ void widen_kernel(const int32_t* __restrict__ a, int64_t n, long long* __restrict__ out) {
+  const int64_t T = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += T)
+    out[i] = a[i];
+}
+
 __global__ void axpy_inplace_kernel(double* __restrict__ t, const double* __restrict__ g,
                                     double alpha, int64_t n) {
   const int64_t T = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -152,6 +158,15 @@ int dlx_axpy_inplace(double* d_theta, const double* d_grad, double alpha, int64_
   const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, sm_count() * 8));
   axpy_inplace_kernel<<<grid, 256, 0, stream>>>(d_theta, d_grad, alpha, n);
   DLX_LAUNCHED("axpy_inplace_kernel");
+  return DLX_OK;
+}
+
+int dlx_widen_i32_i64(const int32_t* d_in, int64_t n, int64_t* d_out, dlx_stream_t stream) {
+  DLX_REQUIRE(n >= 0 && ((d_in && d_out) || n == 0), DLX_ERR_ARG, "widen: bad args");
+  if (n == 0) return DLX_OK;
+  const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, sm_count() * 8));
+  widen_kernel<<<grid, 256, 0, stream>>>(d_in, n, reinterpret_cast<long long*>(d_out));
+  DLX_LAUNCHED("widen_kernel");
   return DLX_OK;
 }
 

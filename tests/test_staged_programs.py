@@ -1,0 +1,132 @@
+"""Programs staged through the REFERENCE's own DSL, fusion and codegen (oracle/_ref build of
+/root/reference/proj, integration/stage_programs.cpp), with expected output produced by
+executing the reference's emitted MiniC (oracle/minic_eval.hpp).  CPU tests pin those
+fixtures against the oracle port; GPU tests run the same descriptors through the B200
+executor (dlx_program_run) and compare with the reference's output."""
+import glob
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+FIXTURES = sorted(glob.glob(os.path.join(HERE, "golden", "staged", "*.json")))
+
+
+def load(name):
+    with open(os.path.join(HERE, "golden", "staged", name + ".json")) as f:
+        return json.load(f)
+
+
+def lines(text):
+    return [s for s in text.split("\n") if s != ""]
+
+
+def same_value(a: str, b: str, rtol=1e-9) -> bool:
+    if a == b:
+        return True
+    try:
+        ia, ib = int(a), int(b)
+        return ia == ib
+    except ValueError:
+        pass
+    fa, fb = float(a), float(b)
+    if math.isnan(fa) and math.isnan(fb):
+        return True
+    return abs(fa - fb) <= rtol * max(abs(fa), abs(fb))
+
+
+def test_fixtures_present():
+    names = {os.path.basename(f)[:-5] for f in FIXTURES}
+    for n in ("kmeans_n65536_d16_k8_it1", "kmeans_n4096_d16_k8_it2", "groupby_n100000_k16", "gda_n20000_d4",
+              "mean_variance_n100000", "axpy_n100000", "count_gt_n100000"):
+        assert n in names
+    for f in FIXTURES:
+        with open(f) as fh:
+            fx = json.load(fh)
+        assert fx["program"]["format"] == "dlx-program/1"
+        assert fx["expected"]
+
+
+def test_staged_kmeans_matches_appendix_b(golden):
+    fx = load("kmeans_n65536_d16_k8_it1")
+    out = lines(fx["expected"])
+    assert [int(v) for v in out[1:9]] == golden["c1_kmeans"]["counts"][0]
+    assert out[9] == golden["c1_kmeans"]["mu00"][0]
+    assert fx["root_loops"] == 1  # one fused multiloop per iteration
+
+
+def test_staged_kmeans_matches_oracle_port():
+    fx = load("kmeans_n4096_d16_k8_it2")
+    x, mu0 = O.kmeans_inputs(4096, 16, 8)
+    hist = O.kmeans_run(x, 8, 2, mu0)
+    exp = lines(fx["expected"])
+    got = []
+    for counts, _, _, _, assign in hist:
+        got.append(str(int(assign[0])))
+        got += [str(int(c)) for c in counts]
+    got += [O.format_double(v) for v in hist[-1][2].reshape(-1)]
+    assert exp == got
+
+
+def test_staged_groupby_gda_stats_match_oracle_port():
+    exp = lines(load("groupby_n100000_k16")["expected"])
+    keys = O.rng_ints(1, 0, 100000, 16)
+    assert [int(v) for v in exp] == O.groupby_count(keys, 16).tolist()
+    exp = lines(load("gda_n20000_d4")["expected"])
+    n, d = 20000, 4
+    x = O.rng_units(1, 0, n * d).reshape(n, d)
+    y = O.rng_ints(1, n * d, n, 2)
+    n1, s0, s1 = O.gda_pass1(x, y)
+    mu0, mu1 = s0 / float(n - n1), s1 / float(n1)
+    S = O.gda_pass2(x, y, mu0, mu1)
+    got = [str(n1)] + [O.format_double(v) for pair in zip(mu0, mu1) for v in pair] + [O.format_double(v) for v in S.reshape(-1)]
+    assert exp == got
+    exp = lines(load("mean_variance_n100000")["expected"])
+    xv = O.rng_units(1, 0, 100000)
+    s, sq = O.sum_sumsq_f64(xv)
+    mean = s / 100000
+    assert exp[0] == O.format_double(mean)
+    assert same_value(exp[1], O.format_double(sq / 100000 - mean * mean), rtol=1e-12)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", FIXTURES, ids=[os.path.basename(f)[:-5] for f in FIXTURES])
+def test_staged_program_on_b200(path):
+    from paper_1109_0778_b200.program import run_program
+    with open(path) as f:
+        fx = json.load(f)
+    text, report = run_program(fx["program"], seed=fx["seed"])
+    got, exp = lines(text), lines(fx["expected"])
+    assert len(got) == len(exp)
+    bad = [(i, g, e) for i, (g, e) in enumerate(zip(got, exp)) if not same_value(g, e)]
+    assert not bad, bad[:5]
+    fams = [r["family"] for r in report]
+    print(os.path.basename(path), fams)
+    name = os.path.basename(path)
+    if name.startswith("kmeans"):
+        assert "kmeans" in fams
+    if name.startswith("groupby"):
+        assert fams == ["groupby"]
+    if name.startswith("gda"):
+        assert "gda_scatter" in fams
+
+
+@pytest.mark.gpu
+def test_unlowerable_loop_fails_loudly():
+    from paper_1109_0778_b200 import GenerationFailed
+    from paper_1109_0778_b200.program import run_program
+    fx = load("count_gt_n100000")
+    prog = json.loads(json.dumps(fx["program"]))
+    # turn the loop's first live elem into a filter-collect (append): not lowered yet
+    for st in prog["stmts"].values():
+        if "loop" in st:
+            st["loop"]["elems"][0]["kind"] = "collect"
+            st["loop"]["elems"][0]["append"] = True
+            break
+    with pytest.raises(GenerationFailed):
+        run_program(prog, seed=1)
