@@ -1,5 +1,6 @@
 """The C-ABI library loads on CPU and exports every symbol include/dlx.h declares.  No
 compute calls (there is no GPU here)."""
+import glob
 import os
 import re
 import subprocess
@@ -12,10 +13,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def declared_symbols():
-    with open(os.path.join(ROOT, "include", "dlx.h")) as f:
-        text = f.read()
-    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(dlx_[a-z0-9_]+)\s*\(", text)))
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        with open(h) as f:
+            text = f.read()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        names |= set(re.findall(r"\b(dlx_[a-z0-9_]+)\s*\(", text))
+    return sorted(names)
 
 
 def test_header_matches_bindings():
