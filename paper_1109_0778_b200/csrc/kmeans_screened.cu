@@ -7,42 +7,46 @@
 // Why a screen: the direct form costs 3*N*k*d fp64 ops (2.1e11 per C4 iteration, ~11 ms at
 // the FP64 pipe peak) against 1.34 ms of HBM time.  argmin_c (x-mu_c)^2 =
 // argmin_c (|mu_c|^2 - 2 x.mu_c), and x.mu_c is a GEMM.  We compute it EXACTLY on integer
-// tensor cores for 16-bit fixed-point copies of x and mu, bound the fixed-point error
+// tensor cores for 23-bit fixed-point copies of x and mu, bound the fixed-point error
 // rigorously, and only re-evaluate the reference's own fp64 chain where the bound cannot
 // separate the best centroid from the others.
 //
-// Fixed point.  Per tile (128 samples) e_t with |x| < 2^e_t; per launch e_m with |mu| < 2^e_m
-// over finite centroids.  X = floor(x * 2^(15-e_t)) in [-2^15, 2^15), split X = 256*h + l
-// with h in s8, l in u8 (same for M from mu).  The tcgen05.mma kind::i8 products
-//   HH = sum h_x h_m,  CROSS = sum (h_x l_m + l_x h_m),  LL = sum l_x l_m
-// are exact int32 and S = 65536 HH + 256 CROSS + LL = sum_j X_j M_j exactly.
-// With x = (X + f)/sx, mu = (M + g)/sm, f,g in [0,1):
-//   x.mu * sx*sm = S + E,  E in [sum min(0,X) + sum min(0,M),  sum max(0,X) + sum max(0,M) + d]
-// so the width of E is  sum|X| + sum|M| + d.  In units U = 2^(e_t+e_m-22) the screened
-// score  T_c = floor(|mu_c|^2 / U) - 2*(256 HH + CROSS + (LL >> 8))  satisfies
-//   |mu_c|^2/U - 2 x.mu_c/U  in  [T_c - 2 r_hi, T_c + 1 - 2 r_lo],  r_hi - r_lo <= 1 + width/256,
-// and the reference's fp64 chain differs from the real distance by < 1 unit (guarded by
-// -8 <= e_m - e_t <= 2).  Hence every centroid with  T_c > min_c T_c + W,  W = 6 + ceil((sum|X|
-// + max_c sum max(0,M_c) + max_c sum max(0,-M_c) + d)/128),  has a strictly larger reference distance than some other centroid
-// and cannot be the argmin.  If exactly one centroid survives it IS the reference argmin; if
-// several survive they are re-evaluated with the reference chain (sequential j, no FMA,
-// strict <, ascending c).  Tiles with non-finite values, |exponents| > 400 or e_m - e_t
-// outside [-8, 2] run the exact chain for every centroid.  NaN / inf centroids never win the reference chain
+// Fixed point.  Per tile e_t with |x| < 2^e_t; per launch e_m with |mu| < 2^e_m over finite
+// centroids.  Y = rint(x * 2^(22-e_t)), |Y| <= 2^22, split Y = 65536 h + 256 l + F with h in
+// s8 and l, F in u8 (same for mu: Y' = 65536 h' + 256 l' + G).  tcgen05.mma kind::i8 computes
+// exact int32 accumulators
+//   HH = sum h h',  CR = sum (h l' + l h'),  W1 = sum (h G + F h' + l l'),  W2 = sum (l G + F l')
+// so sum Y Y' = 2^32 HH + 2^24 CR + 2^16 W1 + 2^8 W2 + sum F G  (the last term, in [0, d*255^2],
+// is dropped).  With x~ = Y + phi, mu~ = Y' + gamma, |phi|,|gamma| <= 1/2:
+//   sum x~ mu~ = sum Y Y' + E,  |E| <= (sum|Y| + sum|Y'|)/2 + d/4.
+// In units U = 2^(e_t+e_m-20), x.mu/U = sum x~ mu~ / 2^24 and Q = 256 HH + CR + (W1>>8) +
+// (W2>>16) satisfies x.mu/U in [Q - e, Q + 2.25 + e], e = ((sum|Y|+sum|Y'|)/2 + d/4)/2^24.
+// The screened score T_c = floor(|mu_c|^2/U) - 2 Q_c brackets |mu_c|^2/U - 2 x.mu_c/U within
+// [T_c - 4.5 - 2e, T_c + 1 + 2e], and the reference's fp64 chain differs from the real
+// distance by < 1 unit (guarded by -8 <= e_m - e_t <= 2, |e| <= 400).  So every centroid with
+//   T_c > min_c T_c + W,   W = 9 + ceil(4 e),   (sum|Y| <= d 2^22 per sample, sum|Y'| <= max_c)
+// has a strictly larger reference distance than some other centroid and cannot be the argmin.
+// One survivor => it IS the reference argmin.  Several survivors => the sample goes to the
+// pending list and is re-evaluated with the reference chain (sequential j, no FMA, strict <,
+// ascending c, start (1e300, 0)).  Tiles with non-finite values or out-of-range exponents
+// send every sample to the exact chain.  NaN / inf centroids never win the reference chain
 // and are excluded from the screen.
 //
 // Kernel shape: one persistent CTA per SM, 14 warps, warp-specialised around mbarriers:
-//   warp 0      TMA producer: 1-D bulk copies of 128-sample x tiles into a 3-stage ring
-//   warp 1      TMEM owner + MMA issuer (one thread): 8 tcgen05.mma per tile into a
-//               double-buffered 3 x 64-column int32 accumulator
-//   warps 2-5   converters: tile exponent, fixed-point split into the SW128 K-major A operand
-//   warps 6-13  epilogue + bucket-reduce: tcgen05.ld the scores and screen; samples with a
-//               unique survivor are folded into register-resident per-centroid sums (warp w
-//               owns centroids w, w+8, ...; lane l owns columns 2l, 2l+1; rows folded in
-//               ascending order: deterministic, no atomics); samples with several survivors
-//               (and every sample of a guarded tile) go to a per-CTA pending list
+//   warp 0      TMA producer: 1-D bulk copies of 112-sample x tiles into a 3-stage ring
+//   warp 1      TMEM owner + MMA issuer (one thread): 16 tcgen05.mma per tile into a
+//               double-buffered 4 x 64-column int32 accumulator
+//   warps 2-5   converters: tile exponent, rint(x*2^(22-e)) via the fp64 magic-number add,
+//               byte split into the SW128 [h|l] and SW64 [F] K-major A operands
+//   warps 6-13  epilogue + bucket-reduce: tcgen05.ld the accumulators and screen; samples with
+//               a unique survivor are stably counting-sorted by centroid and folded into
+//               register-resident per-centroid sums (warp w owns centroids w, w+8, ...; lane
+//               l owns columns 2l, 2l+1; rows folded in ascending order: deterministic, no
+//               atomics); samples with several survivors (and every sample of a guarded
+//               tile) go to a per-CTA pending list
 //   resolve     a second small kernel evaluates the reference chain for the pending samples
-//               (one lane per candidate centroid), writes their assignments and folds their
-//               rows into a second per-CTA partial record, in list order (deterministic).
+//               (one thread per (sample, candidate) pair), writes their assignments and folds
+//               their rows into per-CTA partial records, in list order (deterministic).
 #include <algorithm>
 #include <climits>
 #include <vector>
@@ -60,47 +64,63 @@ namespace sk {
 using namespace sm100;
 
 constexpr int kThreads = 448;
-constexpr int kTile = 128;
+constexpr int kTile = 112;        // samples per tile (the MMA runs M=128; rows 112..127 are zero)
+constexpr int kMmaM = 128;
 constexpr int kStages = 3;
 constexpr int kMaxD = 64;
 constexpr int kMaxK = 64;
 constexpr int kWarpProd = 0, kWarpMma = 1, kWarpC0 = 2, kWarpE0 = 6;
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kAccCols = 192;
-constexpr uint32_t kXStage = kTile * kMaxD * 8;  // 64 KiB
-constexpr uint32_t kOffA = kStages * kXStage;      // 196608
-constexpr uint32_t kOffB = kOffA + kTile * 128;    // 212992
-constexpr uint32_t kOffMisc = kOffB + kMaxK * 128; // 221184
+constexpr uint32_t kAccCols = 256;                        // 4 accumulators x 64 columns
+constexpr uint32_t kXStage = kTile * kMaxD * 8;           // 56 KiB
+constexpr uint32_t kOffA1 = kStages * kXStage;            // [h|l]  128 x 128 B, SW128
+constexpr uint32_t kOffA2 = kOffA1 + kMmaM * 128;         // [F]    128 x 64 B,  SW64
+constexpr uint32_t kOffB1 = kOffA2 + kMmaM * 64;          // [h'|l'] 64 x 128 B, SW128
+constexpr uint32_t kOffB2 = kOffB1 + kMaxK * 128;         // [G]     64 x 64 B,  SW64
+constexpr uint32_t kOffMisc = kOffB2 + kMaxK * 64;
+static_assert(kOffA1 % 1024 == 0 && kOffB1 % 1024 == 0 && kOffA2 % 512 == 0 && kOffB2 % 512 == 0,
+              "UMMA operand alignment");
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: x + kMagic rounds x to an integer
 
 struct Misc {
   uint64_t full[kStages], sempty[kStages], cfull[kStages];
   uint64_t a_full, a_empty, tfull[2], tempty[2];
   unsigned long long valid;
   uint32_t tmem_base;
-  int em, mpos, mneg, disabled;
+  int em, yabs, disabled;
   uint32_t mu_maxhi;
-  int tile_e[kStages], tile_flag[kStages];
-  int absx[kStages][kTile];
+  int tile_flag[kStages];
+  int tile_w[kStages];      // screen window W in score units
   int nmt[kStages][kMaxK];  // floor(|mu_c|^2 / U_t) per stage (U_t depends on the tile exponent)
   double nmf[kMaxK];
-  int hmin[2][kTile];
-  uint32_t cmask[2][kTile];
-  int assign[kTile];
+  int hmin[2][kMmaM];
+  uint32_t cmask[2][kMmaM];
   int pcount[4];
   uint32_t cscr[2][8];
   int wcnt[4][kMaxK];       // per quarter: samples of the tile assigned to c
   int woff[4][kMaxK];       // per quarter: first slot of its c-samples in `sorted`
   int cstart[kMaxK + 1];    // per centroid: [cstart[c], cstart[c+1]) in `sorted`
-  int sorted[kTile];        // the tile's resolved samples, stably sorted by centroid
+  int sorted[kMmaM];        // the tile's resolved samples, stably sorted by centroid
 };
-constexpr int kInvalidNm = 0x70000000;  // > any valid score (|Q| < 2^28, nm < 2^30)
-constexpr int kNoCandidate = 0x60000000;
 constexpr uint32_t kSmemBytes = kOffMisc + sizeof(Misc);
 static_assert(kSmemBytes <= 232448, "shared-memory plan exceeds 227 KiB");
+constexpr int kInvalidNm = 0x70000000;  // > any valid score (|Q| < 2^26, nm <= 2^28)
+constexpr int kNoCandidate = 0x60000000;
 
 __device__ __forceinline__ int exp_bound(uint32_t maxhi) {
   // smallest e with |v| < 2^e for the largest |v| whose high word (sans sign) is maxhi
   return static_cast<int>(maxhi >> 20) - 1022;
+}
+
+// byte offset of (row, byte k) inside a K-major SWIZZLE_64B operand with 64-byte rows
+__device__ __forceinline__ uint32_t sw64_offset(uint32_t row, uint32_t kbyte) {
+  const uint32_t chunk = (kbyte >> 4) ^ ((row & 7) >> 1);
+  return (row >> 3) * 512u + (row & 7) * 64u + (chunk << 4) + (kbyte & 15);
+}
+
+// rint(v) for |v| < 2^31 as the low word of v + 1.5*2^52 (one fp64 add, exact scaling before)
+__device__ __forceinline__ int rint_magic(double scaled) {
+  return __double2loint(__dadd_rn(scaled, kMagic));
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -111,14 +131,16 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
                        long long* __restrict__ pend_count, long long pend_cap) {
   extern __shared__ __align__(1024) unsigned char smem[];
   Misc& S = *reinterpret_cast<Misc*>(smem + kOffMisc);
-  unsigned char* A = smem + kOffA;
-  unsigned char* B = smem + kOffB;
+  unsigned char* A1 = smem + kOffA1;
+  unsigned char* A2 = smem + kOffA2;
+  unsigned char* B1 = smem + kOffB1;
+  unsigned char* B2 = smem + kOffB2;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int64_t ntiles = (n + kTile - 1) / kTile;
   const int mtiles = static_cast<int>((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
 
-  // ---- prologue: barriers, scratch, B operand (fixed-point centroids) -----------------------
+  // ---- prologue: barriers, B operands (fixed-point centroids), per-centroid constants ------
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&S.full[s], 1);
@@ -132,8 +154,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       mbar_init(&S.tempty[b], 8);
     }
     S.valid = 0;
-    S.mpos = 0;
-    S.mneg = 0;
+    S.yabs = 0;
     S.mu_maxhi = 0;
     fence_mbar_init();
   }
@@ -166,25 +187,20 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
   }
   __syncthreads();
   {
-    const int em = S.em;
-    const double scale = S.disabled ? 0.0 : ldexp(1.0, 15 - em);
+    const double scale = S.disabled ? 0.0 : ldexp(1.0, 22 - S.em);
     const unsigned long long valid = S.valid;
     for (int e = tid; e < kMaxK * kMaxD; e += kThreads) {
       const int c = e / kMaxD, j = e - c * kMaxD;
-      int X = 0;
-      if (((valid >> c) & 1) && j < d) X = __double2int_rd(mu[c * d + j] * scale);
-      B[sw128_offset(c, j)] = static_cast<unsigned char>((X >> 8) & 0xff);
-      B[sw128_offset(c, 64 + j)] = static_cast<unsigned char>(X & 0xff);
+      int Y = 0;
+      if (((valid >> c) & 1) && j < d) Y = rint_magic(mu[c * d + j] * scale);
+      B1[sw128_offset(c, j)] = static_cast<unsigned char>(Y >> 16);
+      B1[sw128_offset(c, 64 + j)] = static_cast<unsigned char>(Y >> 8);
+      B2[sw64_offset(c, j)] = static_cast<unsigned char>(Y);
     }
     if (tid < kMaxK && ((valid >> tid) & 1)) {
-      int pos = 0, neg = 0;
-      for (int j = 0; j < d; ++j) {
-        const int X = __double2int_rd(mu[tid * d + j] * scale);
-        pos += max(X, 0);
-        neg += max(-X, 0);
-      }
-      atomicMax(&S.mpos, pos);
-      atomicMax(&S.mneg, neg);
+      int sa = 0;
+      for (int j = 0; j < d; ++j) sa += abs(rint_magic(mu[tid * d + j] * scale));
+      atomicMax(&S.yabs, sa);
     }
   }
   fence_proxy_async_smem();
@@ -210,11 +226,12 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
   } else if (warp == kWarpMma) {
     // ======================= MMA issuer =======================
     if (lane == 0) {
-      constexpr uint32_t ID_SS = idesc_i8(128, 64, 1, 1);
-      constexpr uint32_t ID_SU = idesc_i8(128, 64, 1, 0);
-      constexpr uint32_t ID_US = idesc_i8(128, 64, 0, 1);
-      constexpr uint32_t ID_UU = idesc_i8(128, 64, 0, 0);
-      const uint32_t a0 = smem_addr(A), b0 = smem_addr(B);
+      // A pieces: h (s8), l (u8), F (u8); B pieces: h' (s8), l' (u8), G (u8)
+      constexpr uint32_t ID_hh = idesc_i8(kMmaM, 64, 1, 1);
+      constexpr uint32_t ID_hu = idesc_i8(kMmaM, 64, 1, 0);
+      constexpr uint32_t ID_uh = idesc_i8(kMmaM, 64, 0, 1);
+      constexpr uint32_t ID_uu = idesc_i8(kMmaM, 64, 0, 0);
+      const uint32_t a1 = smem_addr(A1), a2 = smem_addr(A2), b1 = smem_addr(B1), b2 = smem_addr(B2);
       const int nk = (d + 31) / 32;
       for (int m = 0; m < mtiles; ++m) {
         const int b = m & 1;
@@ -223,12 +240,19 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         tc_fence_after();
         const uint32_t dt = tmem + b * kAccCols;
         for (int kk = 0; kk < nk; ++kk) {
-          const uint64_t aH = sw128_kmajor_desc(a0 + 32 * kk), aL = sw128_kmajor_desc(a0 + 64 + 32 * kk);
-          const uint64_t bH = sw128_kmajor_desc(b0 + 32 * kk), bL = sw128_kmajor_desc(b0 + 64 + 32 * kk);
-          mma_i8(dt + 0, aH, bH, ID_SS, kk > 0);
-          mma_i8(dt + 64, aH, bL, ID_SU, kk > 0);
-          mma_i8(dt + 64, aL, bH, ID_US, 1);
-          mma_i8(dt + 128, aL, bL, ID_UU, kk > 0);
+          const uint64_t xh = sw128_kmajor_desc(a1 + 32 * kk), xl = sw128_kmajor_desc(a1 + 64 + 32 * kk);
+          const uint64_t xf = sw64_kmajor_desc(a2 + 32 * kk);
+          const uint64_t mh = sw128_kmajor_desc(b1 + 32 * kk), ml = sw128_kmajor_desc(b1 + 64 + 32 * kk);
+          const uint64_t mg = sw64_kmajor_desc(b2 + 32 * kk);
+          const uint32_t acc = kk > 0;
+          mma_i8(dt + 0, xh, mh, ID_hh, acc);      // HH
+          mma_i8(dt + 64, xh, ml, ID_hu, acc);     // CR = h l' + l h'
+          mma_i8(dt + 64, xl, mh, ID_uh, 1);
+          mma_i8(dt + 128, xh, mg, ID_hu, acc);    // W1 = h G + F h' + l l'
+          mma_i8(dt + 128, xf, mh, ID_uh, 1);
+          mma_i8(dt + 128, xl, ml, ID_uu, 1);
+          mma_i8(dt + 192, xl, mg, ID_uu, acc);    // W2 = l G + F l'
+          mma_i8(dt + 192, xf, ml, ID_uu, 1);
         }
         mma_commit(&S.a_empty);
         mma_commit(&S.tfull[b]);
@@ -238,7 +262,9 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     // ======================= converters (128 threads) =======================
     const int ct = tid - kWarpC0 * 32;
     const int cw = ct >> 5;
-    const int em = S.em, disabled = S.disabled;
+    const int em = S.em, disabled = S.disabled, yabs = S.yabs;
+    const unsigned long long valid = S.valid;
+    const int half = lane >> 4, j0 = 4 * (lane & 15);
     for (int m = 0; m < mtiles; ++m) {
       const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
       const int s = m % kStages;
@@ -272,32 +298,43 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       const int et = tmx == 0 ? em : exp_bound(tmx);
       const int flag = (tbad || disabled || et > 400 || et < -400 || em - et > 2 || et - em > 8) ? 1 : 0;
       if (m >= 1) mbar_wait(&S.a_empty, (m - 1) & 1);
-      // pass 2: fixed-point split into A (row q = cw*32 + r; lane owns columns 2l, 2l+1)
-      const double scale = flag ? 0.0 : ldexp(1.0, 15 - et);
-      const int j0 = 2 * lane;
-      for (int r = 0; r < 32; ++r) {
-        const int q = cw * 32 + r;
-        int X0 = 0, X1 = 0;
-        if (!flag && q < rows && j0 < d) {
-          const double2 v = *reinterpret_cast<const double2*>(xs + q * d + j0);
-          X0 = __double2int_rd(v.x * scale);
-          X1 = __double2int_rd(v.y * scale);
+      // pass 2: Y = rint(x * 2^(22-e_t)); warp cw owns rows cw*32 .. +31, two rows per step,
+      // lane owns columns 4*(lane%16) .. +3 of row (step*2 + lane/16)
+      const double scale = flag ? 0.0 : ldexp(1.0, 22 - et);
+#pragma unroll 2
+      for (int r = 0; r < 16; ++r) {
+        const int q = cw * 32 + 2 * r + half;
+        int Y0 = 0, Y1 = 0, Y2 = 0, Y3 = 0;
+        if (q < rows && j0 < d) {
+          const double2 v0 = *reinterpret_cast<const double2*>(xs + q * d + j0);
+          Y0 = rint_magic(v0.x * scale);
+          Y1 = rint_magic(v0.y * scale);
+          if (j0 + 2 < d) {
+            const double2 v1 = *reinterpret_cast<const double2*>(xs + q * d + j0 + 2);
+            Y2 = rint_magic(v1.x * scale);
+            Y3 = rint_magic(v1.y * scale);
+          }
         }
-        const uint32_t hi = ((X0 >> 8) & 0xff) | (((X1 >> 8) & 0xff) << 8);
-        const uint32_t lo = (X0 & 0xff) | ((X1 & 0xff) << 8);
-        *reinterpret_cast<uint16_t*>(A + sw128_offset(q, j0)) = static_cast<uint16_t>(hi);
-        *reinterpret_cast<uint16_t*>(A + sw128_offset(q, 64 + j0)) = static_cast<uint16_t>(lo);
-        const int sa = __reduce_add_sync(0xffffffffu, abs(X0) + abs(X1));
-        if (lane == 0) S.absx[s][q] = sa;
+        // bytes of Y (little endian): b0 = F, b1 = l, b2 = h (low byte of Y >> 16)
+        const uint32_t p01 = __byte_perm(Y0, Y1, 0x6240), p23 = __byte_perm(Y2, Y3, 0x6240);
+        const uint32_t q01 = __byte_perm(Y0, Y1, 0x0051), q23 = __byte_perm(Y2, Y3, 0x0051);
+        const uint32_t hw = __byte_perm(p01, p23, 0x7632);  // h0 h1 h2 h3
+        const uint32_t fw = __byte_perm(p01, p23, 0x5410);  // F0 F1 F2 F3
+        const uint32_t lw = __byte_perm(q01, q23, 0x5410);  // l0 l1 l2 l3
+        *reinterpret_cast<uint32_t*>(A1 + sw128_offset(q, j0)) = hw;
+        *reinterpret_cast<uint32_t*>(A1 + sw128_offset(q, 64 + j0)) = lw;
+        *reinterpret_cast<uint32_t*>(A2 + sw64_offset(q, j0)) = fw;
       }
       if (ct == 0) {
-        S.tile_e[s] = et;
         S.tile_flag[s] = flag;
+        // W = 9 + ceil(4e), e = ((d*2^22 + max_c sum|Y'|)/2 + d/4) / 2^24
+        const long long num = (static_cast<long long>(d) << 22) + yabs;
+        S.tile_w[s] = 10 + static_cast<int>((2 * num + d + (1ll << 24) - 1) >> 24);
       }
-      if (ct < kMaxK) {  // |mu_c|^2 in units U_t = 2^(e_t+e_m-22): < 2^30 under the gap guard
-        S.nmt[s][ct] = (flag || !((S.valid >> ct) & 1))
+      if (ct < kMaxK) {  // |mu_c|^2 in units U_t = 2^(e_t+e_m-20): <= 2^28 under the gap guard
+        S.nmt[s][ct] = (flag || !((valid >> ct) & 1))
                            ? kInvalidNm
-                           : __double2int_rd(S.nmf[ct] * ldexp(1.0, 22 - et - em));
+                           : __double2int_rd(S.nmf[ct] * ldexp(1.0, 20 - et - em));
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -311,8 +348,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     const int ew = warp - kWarpE0;          // 0..7
     const int quarter = warp & 3;           // TMEM lane quarter this warp may access
     const int h = ew >> 2;                  // centroid half
-    const int q = quarter * 32 + lane;      // sample row within the tile
-    const int mabs = S.mpos + S.mneg;       // >= max_c Mpos_c - min_c' Mneg_c'
+    const int q = quarter * 32 + lane;      // sample row within the tile (M row)
     const unsigned long long kmask = k == 64 ? ~0ull : ((1ull << k) - 1);
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
     long long* my_pidx = pend_idx + static_cast<size_t>(blockIdx.x) * pend_cap;
@@ -339,10 +375,11 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
           const uint32_t col = b * kAccCols + 32 * h + 16 * ch;
-          int hh[16], cr[16], ll[16];
+          int hh[16], cr[16], w1[16], w2[16];
           tmem_ld16(tmem + lane_base + col, hh);
           tmem_ld16(tmem + lane_base + col + 64, cr);
-          tmem_ld16(tmem + lane_base + col + 128, ll);
+          tmem_ld16(tmem + lane_base + col + 128, w1);
+          tmem_ld16(tmem + lane_base + col + 192, w2);
           int nm[16];
 #pragma unroll
           for (int u4 = 0; u4 < 4; ++u4) {
@@ -356,7 +393,8 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
 #pragma unroll
           for (int u = 0; u < 16; ++u) {
             // invalid centroids: zero B rows (Q = 0) and nm = kInvalidNm
-            const int v = nm[u] - 2 * (hh[u] * 256 + cr[u] + (ll[u] >> 8));
+            const int Q = hh[u] * 256 + cr[u] + (w1[u] >> 8) + (w2[u] >> 16);
+            const int v = nm[u] - 2 * Q;
             tv[16 * ch + u] = v;
             lmin = min(lmin, v);
           }
@@ -371,7 +409,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       if (!flag) {
         const int tmin = min(S.hmin[0][q], S.hmin[1][q]);
         if (tmin < kNoCandidate) {
-          const int thr = tmin + 6 + (S.absx[s][q] + mabs + d + 127) / 128;
+          const int thr = tmin + S.tile_w[s];
 #pragma unroll
           for (int u = 0; u < 32; ++u)
             if (tv[u] <= thr) mask |= 1u << u;
@@ -426,7 +464,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         const int c0 = 2 * lane, c1 = c0 + 1;
         int w0[4], w1[4];
 #pragma unroll
-        for (int Q = 0; Q < 4; ++Q) w0[Q] = S.wcnt[Q][c0], w1[Q] = S.wcnt[Q][c1];
+        for (int Qr = 0; Qr < 4; ++Qr) w0[Qr] = S.wcnt[Qr][c0], w1[Qr] = S.wcnt[Qr][c1];
         const int t0 = w0[0] + w0[1] + w0[2] + w0[3], t1 = w1[0] + w1[1] + w1[2] + w1[3];
         int incl = t0 + t1;
 #pragma unroll
@@ -440,11 +478,11 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         if (lane == 31) S.cstart[kMaxK] = incl;
         int r0 = s0, r1 = s1;
 #pragma unroll
-        for (int Q = 0; Q < 4; ++Q) {
-          S.woff[Q][c0] = r0;
-          S.woff[Q][c1] = r1;
-          r0 += w0[Q];
-          r1 += w1[Q];
+        for (int Qr = 0; Qr < 4; ++Qr) {
+          S.woff[Qr][c0] = r0;
+          S.woff[Qr][c1] = r1;
+          r0 += w0[Qr];
+          r1 += w1[Qr];
         }
       }
       named_bar(1, 256);
@@ -452,16 +490,16 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       named_bar(1, 256);
       // bucket-reduce: warp ew owns centroids ew + 8u, lane owns columns 2*lane, 2*lane+1;
       // each centroid's samples are contiguous in `sorted`, in ascending row order
-      const int j0 = 2 * lane;
+      const int jc = 2 * lane;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int c = ew + 8 * u;
         if (c >= k) break;
         const int beg = S.cstart[c], end = S.cstart[c + 1];
         cnt[u] += end - beg;
-        if (j0 < d) {
+        if (jc < d) {
           for (int p = beg; p < end; ++p) {
-            const double2 v = *reinterpret_cast<const double2*>(xs + S.sorted[p] * d + j0);
+            const double2 v = *reinterpret_cast<const double2*>(xs + S.sorted[p] * d + jc);
             acc[u][0] += v.x;
             acc[u][1] += v.y;
           }
@@ -472,13 +510,13 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     }
     // flush this CTA's partial activation record
     double* ps = part_sums + static_cast<size_t>(blockIdx.x) * k * d;
-    const int j0 = 2 * lane;
+    const int jc = 2 * lane;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int c = ew + 8 * u;
       if (c < k) {
-        if (j0 < d) ps[c * d + j0] = acc[u][0];
-        if (j0 + 1 < d) ps[c * d + j0 + 1] = acc[u][1];
+        if (jc < d) ps[c * d + jc] = acc[u][0];
+        if (jc + 1 < d) ps[c * d + jc + 1] = acc[u][1];
         if (lane == 0) part_counts[static_cast<size_t>(blockIdx.x) * k + c] = cnt[u];
       }
     }

@@ -130,6 +130,17 @@ __device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t smem_byte_addr) {
   return d;
 }
 
+// K-major SWIZZLE_64B (rows of 64 B, 8-row / 512 B atoms, SBO = 512 B).
+__device__ __forceinline__ uint64_t sw64_kmajor_desc(uint32_t smem_byte_addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_byte_addr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1u) << 16;
+  d |= static_cast<uint64_t>(512u >> 4) << 32;
+  d |= static_cast<uint64_t>(1u) << 46;
+  d |= static_cast<uint64_t>(4u) << 61;                           // SWIZZLE_64B
+  return d;
+}
+
 // Instruction descriptor for kind::i8: S32 accumulator, K-major A and B.
 // a_signed/b_signed: 1 = s8, 0 = u8.
 __host__ __device__ constexpr uint32_t idesc_i8(int m, int n, int a_signed, int b_signed) {
