@@ -132,3 +132,4 @@ std::string to_dlx_program(const Graph& g, const Schedule& s) {
 }
 
 }  // namespace stagekit_dlx
+

@@ -12,7 +12,7 @@ CXXFLAGS ?= -std=c++20 -O2 -fPIC -w -I$(REF)/include -I$(OUT)/vendor
 TUS      := expr graph stage records loops vectordsl schedule fusion dump minic
 OBJS     := $(addprefix $(OUT)/,$(addsuffix .o,$(TUS))) $(OUT)/codegen.o
 
-all: $(OUT)/libstagekit.a $(OUT)/stage_programs
+all: $(OUT)/libstagekit.a $(OUT)/stage_programs $(OUT)/run_staged
 
 $(OUT)/vendor/json.hpp:
 	@mkdir -p $(OUT)/vendor
@@ -41,6 +41,15 @@ $(OUT)/stage_programs: ../integration/stage_programs.cpp ../integration/stagekit
                       ../integration/stagekit_dlx.hpp minic_eval.hpp $(OUT)/libstagekit.a
 	$(CXX) $(CXXFLAGS) -I.. -o $@ ../integration/stage_programs.cpp ../integration/stagekit_dlx.cpp \
 	    $(OUT)/libstagekit.a
+
+# run_staged: the C++ end-to-end drop-in check (reference DSL -> fuse -> schedule ->
+# stagekit_dlx::run_on_b200 vs the reference MiniC evaluated on the CPU); links libdlx.so.
+DLX_DIR := $(abspath ../paper_1109_0778_b200)
+$(OUT)/run_staged: ../integration/run_staged.cpp ../integration/stagekit_dlx.cpp \
+                   ../integration/stagekit_dlx_run.cpp ../integration/stagekit_dlx.hpp minic_eval.hpp \
+                   $(OUT)/libstagekit.a $(DLX_DIR)/libdlx.so
+	$(CXX) $(CXXFLAGS) -I.. -o $@ ../integration/run_staged.cpp ../integration/stagekit_dlx.cpp ../integration/stagekit_dlx_run.cpp \
+	    $(OUT)/libstagekit.a -L$(DLX_DIR) -ldlx -Wl,-rpath,'$$ORIGIN/../../paper_1109_0778_b200'
 
 clean:
 	rm -rf $(OUT)

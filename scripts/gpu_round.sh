@@ -13,7 +13,7 @@ python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || echo
 for w in $WHAT; do
   case $w in
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log ;;
-    ktests) timeout 600 python -m pytest tests -m gpu -q -rf -x -k "screened or c1_step or c4 or kmeans" > $OUT/pytest_kmeans.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_kmeans.log ;;
+    ktests) timeout 600 python -m pytest tests -m gpu -q -rf -x -k "screened or c1_step or c4 or kmeans or staged" > $OUT/pytest_kmeans.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_kmeans.log ;;
     benchk) timeout 600 python bench.py --config c4 --steps 20 --warmup 3 > $OUT/bench_c4.json 2> $OUT/bench_c4.err
             timeout 600 python bench.py --config c1 --steps 20 --warmup 3 --no-cpu-baseline > $OUT/bench_c1.json 2> $OUT/bench_c1.err ;;
     ncuk) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file $OUT/launches_c4.csv \
