@@ -91,7 +91,7 @@ struct Misc {
   uint32_t mu_maxhi;
   int tile_flag[kStages];
   int tile_w[kStages];      // screen window W in score units
-  int nmt[kStages][kMaxK];  // floor(|mu_c|^2 / U_t) per stage (U_t depends on the tile exponent)
+  alignas(16) int nmt[kStages][kMaxK];  // floor(|mu_c|^2 / U_t) per stage (int4-loaded)
   double nmf[kMaxK];
   int hmin[2][kMmaM];
   uint32_t cmask[2][kMmaM];
@@ -121,6 +121,10 @@ __device__ __forceinline__ uint32_t sw64_offset(uint32_t row, uint32_t kbyte) {
 // rint(v) for |v| < 2^31 as the low word of v + 1.5*2^52 (one fp64 add, exact scaling before)
 __device__ __forceinline__ int rint_magic(double scaled) {
   return __double2loint(__dadd_rn(scaled, kMagic));
+}
+// rint(x * scale) for a power-of-two scale: the product is exact, so one fma rounds once
+__device__ __forceinline__ int rint_fma(double x, double scale) {
+  return __double2loint(__fma_rn(x, scale, kMagic));
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -265,65 +269,60 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     const int em = S.em, disabled = S.disabled, yabs = S.yabs;
     const unsigned long long valid = S.valid;
     const int half = lane >> 4, j0 = 4 * (lane & 15);
+    const int key = cw + 4 * half;  // row & 7 of every row this thread converts
+    const uint32_t off_h = sw128_offset(key, j0), off_l = sw128_offset(key, 64 + j0);
+    const uint32_t off_f = sw64_offset(key, j0);
     for (int m = 0; m < mtiles; ++m) {
       const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
       const int s = m % kStages;
       const int rows = static_cast<int>(n - t * kTile < kTile ? n - t * kTile : kTile);
       mbar_wait(&S.full[s], (m / kStages) & 1);
       const double* xs = reinterpret_cast<const double*>(smem + s * kXStage);
-      // pass 1: tile exponent and finiteness
-      uint32_t mx = 0, bad = 0;
+      // pass 1: tile exponent (max |x| high word; >= 0x7ff00000 means inf / NaN present)
+      uint32_t mx = 0;
       const int pairs = rows * d / 2;
       const double2* xs2 = reinterpret_cast<const double2*>(xs);
+#pragma unroll 4
       for (int p = ct; p < pairs; p += 128) {
         const double2 v = xs2[p];
-        const uint32_t h0 = static_cast<uint32_t>(__double2hiint(v.x)) & 0x7fffffffu;
-        const uint32_t h1 = static_cast<uint32_t>(__double2hiint(v.y)) & 0x7fffffffu;
-        mx = max(mx, max(h0, h1));
-        bad |= (h0 >= 0x7ff00000u) | (h1 >= 0x7ff00000u);
+        mx = max(mx, max(static_cast<uint32_t>(__double2hiint(v.x)) & 0x7fffffffu,
+                         static_cast<uint32_t>(__double2hiint(v.y)) & 0x7fffffffu));
       }
       mx = __reduce_max_sync(0xffffffffu, mx);
-      bad = __reduce_or_sync(0xffffffffu, bad);
-      if (lane == 0) {
-        S.cscr[m & 1][cw] = mx;
-        S.cscr[m & 1][4 + cw] = bad;
-      }
+      if (lane == 0) S.cscr[m & 1][cw] = mx;
       named_bar(2, 128);
-      uint32_t tmx = 0, tbad = 0;
+      uint32_t tmx = 0;
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        tmx = max(tmx, S.cscr[m & 1][w]);
-        tbad |= S.cscr[m & 1][4 + w];
-      }
+      for (int w = 0; w < 4; ++w) tmx = max(tmx, S.cscr[m & 1][w]);
+      const bool tbad = tmx >= 0x7ff00000u;
       const int et = tmx == 0 ? em : exp_bound(tmx);
       const int flag = (tbad || disabled || et > 400 || et < -400 || em - et > 2 || et - em > 8) ? 1 : 0;
       if (m >= 1) mbar_wait(&S.a_empty, (m - 1) & 1);
-      // pass 2: Y = rint(x * 2^(22-e_t)); warp cw owns rows cw*32 .. +31, two rows per step,
-      // lane owns columns 4*(lane%16) .. +3 of row (step*2 + lane/16)
+      // pass 2: Y = rint(x * 2^(22-e_t)).  Thread (cw, half, lane16) converts columns
+      // 4*lane16 .. +3 of rows q = 8*mm + key, key = cw + 4*half (mm = 0..15), so its swizzle
+      // key is fixed and its operand offsets advance by a constant per row.
       const double scale = flag ? 0.0 : ldexp(1.0, 22 - et);
-#pragma unroll 2
-      for (int r = 0; r < 16; ++r) {
-        const int q = cw * 32 + 2 * r + half;
+      const double* xrow = xs + key * d + j0;
+#pragma unroll 4
+      for (int mm = 0; mm < kMmaM / 8; ++mm) {
+        const int q = 8 * mm + key;
         int Y0 = 0, Y1 = 0, Y2 = 0, Y3 = 0;
         if (q < rows && j0 < d) {
-          const double2 v0 = *reinterpret_cast<const double2*>(xs + q * d + j0);
-          Y0 = rint_magic(v0.x * scale);
-          Y1 = rint_magic(v0.y * scale);
+          const double2 v0 = *reinterpret_cast<const double2*>(xrow + mm * 8 * d);
+          Y0 = rint_fma(v0.x, scale);
+          Y1 = rint_fma(v0.y, scale);
           if (j0 + 2 < d) {
-            const double2 v1 = *reinterpret_cast<const double2*>(xs + q * d + j0 + 2);
-            Y2 = rint_magic(v1.x * scale);
-            Y3 = rint_magic(v1.y * scale);
+            const double2 v1 = *reinterpret_cast<const double2*>(xrow + mm * 8 * d + 2);
+            Y2 = rint_fma(v1.x, scale);
+            Y3 = rint_fma(v1.y, scale);
           }
         }
         // bytes of Y (little endian): b0 = F, b1 = l, b2 = h (low byte of Y >> 16)
         const uint32_t p01 = __byte_perm(Y0, Y1, 0x6240), p23 = __byte_perm(Y2, Y3, 0x6240);
         const uint32_t q01 = __byte_perm(Y0, Y1, 0x0051), q23 = __byte_perm(Y2, Y3, 0x0051);
-        const uint32_t hw = __byte_perm(p01, p23, 0x7632);  // h0 h1 h2 h3
-        const uint32_t fw = __byte_perm(p01, p23, 0x5410);  // F0 F1 F2 F3
-        const uint32_t lw = __byte_perm(q01, q23, 0x5410);  // l0 l1 l2 l3
-        *reinterpret_cast<uint32_t*>(A1 + sw128_offset(q, j0)) = hw;
-        *reinterpret_cast<uint32_t*>(A1 + sw128_offset(q, 64 + j0)) = lw;
-        *reinterpret_cast<uint32_t*>(A2 + sw64_offset(q, j0)) = fw;
+        *reinterpret_cast<uint32_t*>(A1 + off_h + mm * 1024) = __byte_perm(p01, p23, 0x7632);  // h
+        *reinterpret_cast<uint32_t*>(A1 + off_l + mm * 1024) = __byte_perm(q01, q23, 0x5410);  // l
+        *reinterpret_cast<uint32_t*>(A2 + off_f + mm * 512) = __byte_perm(p01, p23, 0x5410);   // F
       }
       if (ct == 0) {
         S.tile_flag[s] = flag;
@@ -355,9 +354,9 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     unsigned long long* my_pmask = pend_mask + static_cast<size_t>(blockIdx.x) * pend_cap;
     long long pending = 0;
     double acc[8][2];
-    int cnt[8];
+    long long ctot0 = 0, ctot1 = 0;  // scan warp: samples folded per centroid 2*lane, 2*lane+1
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc[u][0] = acc[u][1] = 0.0, cnt[u] = 0;
+    for (int u = 0; u < 8; ++u) acc[u][0] = acc[u][1] = 0.0;
     for (int m = 0; m < mtiles; ++m) {
       const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
       const int s = m % kStages, b = m & 1;
@@ -466,6 +465,8 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
 #pragma unroll
         for (int Qr = 0; Qr < 4; ++Qr) w0[Qr] = S.wcnt[Qr][c0], w1[Qr] = S.wcnt[Qr][c1];
         const int t0 = w0[0] + w0[1] + w0[2] + w0[3], t1 = w1[0] + w1[1] + w1[2] + w1[3];
+        ctot0 += t0;
+        ctot1 += t1;
         int incl = t0 + t1;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -490,18 +491,30 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       named_bar(1, 256);
       // bucket-reduce: warp ew owns centroids ew + 8u, lane owns columns 2*lane, 2*lane+1;
       // each centroid's samples are contiguous in `sorted`, in ascending row order
-      const int jc = 2 * lane;
+      {
+        const int jc = 2 * lane;
+        const int cc = ew + 8 * (lane >> 1) + (lane & 1);
+        const int bounds = (lane < 16 && cc <= kMaxK) ? S.cstart[cc] : 0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int c = ew + 8 * u;
-        if (c >= k) break;
-        const int beg = S.cstart[c], end = S.cstart[c + 1];
-        cnt[u] += end - beg;
-        if (jc < d) {
-          for (int p = beg; p < end; ++p) {
-            const double2 v = *reinterpret_cast<const double2*>(xs + S.sorted[p] * d + jc);
-            acc[u][0] += v.x;
-            acc[u][1] += v.y;
+        for (int u = 0; u < 8; ++u) {
+          const int beg = __shfl_sync(0xffffffffu, bounds, 2 * u);
+          const int end = __shfl_sync(0xffffffffu, bounds, 2 * u + 1);
+          if (jc < d) {
+            int p = beg;
+            for (; p + 1 < end; p += 2) {
+              const int r0 = S.sorted[p], r1 = S.sorted[p + 1];
+              const double2 v0 = *reinterpret_cast<const double2*>(xs + r0 * d + jc);
+              const double2 v1 = *reinterpret_cast<const double2*>(xs + r1 * d + jc);
+              acc[u][0] += v0.x;
+              acc[u][1] += v0.y;
+              acc[u][0] += v1.x;
+              acc[u][1] += v1.y;
+            }
+            if (p < end) {
+              const double2 v0 = *reinterpret_cast<const double2*>(xs + S.sorted[p] * d + jc);
+              acc[u][0] += v0.x;
+              acc[u][1] += v0.y;
+            }
           }
         }
       }
@@ -517,8 +530,12 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       if (c < k) {
         if (jc < d) ps[c * d + jc] = acc[u][0];
         if (jc + 1 < d) ps[c * d + jc + 1] = acc[u][1];
-        if (lane == 0) part_counts[static_cast<size_t>(blockIdx.x) * k + c] = cnt[u];
       }
+    }
+    if (ew == 0) {
+      long long* pc = part_counts + static_cast<size_t>(blockIdx.x) * k;
+      if (2 * lane < k) pc[2 * lane] = ctot0;
+      if (2 * lane + 1 < k) pc[2 * lane + 1] = ctot1;
     }
     if (ew == 0 && lane == 0) pend_count[blockIdx.x] = pending;
   }

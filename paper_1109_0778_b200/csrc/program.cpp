@@ -535,6 +535,7 @@ class Executor {
         s->ci = a.b;
         return s;
       }
+      case Atom::Unit: return mk(SE::Const, Ty::Unit);  // body-scope results are Unit
       default: gen_fail("non-scalar constant in a loop body");
     }
   }
