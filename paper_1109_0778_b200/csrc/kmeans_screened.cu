@@ -49,6 +49,8 @@
 //               their rows into per-CTA partial records, in list order (deterministic).
 #include <algorithm>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -132,9 +134,14 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
                        const double* __restrict__ mu, int32_t* __restrict__ assign,
                        long long* __restrict__ part_counts, double* __restrict__ part_sums,
                        long long* __restrict__ pend_idx, unsigned long long* __restrict__ pend_mask,
-                       long long* __restrict__ pend_count, long long pend_cap) {
+                       long long* __restrict__ pend_count, long long pend_cap,
+                       long long* __restrict__ trace) {
   extern __shared__ __align__(1024) unsigned char smem[];
   Misc& S = *reinterpret_cast<Misc*>(smem + kOffMisc);
+  // optional per-role cycle accounting (DLX_KMEANS_TRACE=1): lane 0 of one warp per role
+  long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long t0 = clock64();
+#define TR(slot) do { const long long _t = clock64(); tr[slot] += _t - t0; t0 = _t; } while (0)
   unsigned char* A1 = smem + kOffA1;
   unsigned char* A2 = smem + kOffA2;
   unsigned char* B1 = smem + kOffB1;
@@ -220,7 +227,9 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       for (int m = 0; m < mtiles; ++m) {
         const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
         const int s = m % kStages;
+        TR(1);
         if (m >= kStages) mbar_wait(&S.sempty[s], ((m / kStages) - 1) & 1);
+        TR(0);
         const int rows = static_cast<int>(n - t * kTile < kTile ? n - t * kTile : kTile);
         const uint32_t bytes = static_cast<uint32_t>(rows) * d * 8u;
         mbar_arrive_expect_tx(&S.full[s], bytes);
@@ -239,8 +248,11 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       const int nk = (d + 31) / 32;
       for (int m = 0; m < mtiles; ++m) {
         const int b = m & 1;
+        TR(2);
         mbar_wait(&S.a_full, m & 1);
+        TR(0);
         if (m >= 2) mbar_wait(&S.tempty[b], ((m >> 1) - 1) & 1);
+        TR(1);
         tc_fence_after();
         const uint32_t dt = tmem + b * kAccCols;
         for (int kk = 0; kk < nk; ++kk) {
@@ -276,7 +288,9 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
       const int s = m % kStages;
       const int rows = static_cast<int>(n - t * kTile < kTile ? n - t * kTile : kTile);
+      TR(4);
       mbar_wait(&S.full[s], (m / kStages) & 1);
+      TR(0);
       const double* xs = reinterpret_cast<const double*>(smem + s * kXStage);
       // pass 1: tile exponent (max |x| high word; >= 0x7ff00000 means inf / NaN present)
       uint32_t mx = 0;
@@ -297,7 +311,9 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       const bool tbad = tmx >= 0x7ff00000u;
       const int et = tmx == 0 ? em : exp_bound(tmx);
       const int flag = (tbad || disabled || et > 400 || et < -400 || em - et > 2 || et - em > 8) ? 1 : 0;
+      TR(1);
       if (m >= 1) mbar_wait(&S.a_empty, (m - 1) & 1);
+      TR(2);
       // pass 2: Y = rint(x * 2^(22-e_t)).  Thread (cw, half, lane16) converts columns
       // 4*lane16 .. +3 of rows q = 8*mm + key, key = cw + 4*half (mm = 0..15), so its swizzle
       // key is fixed and its operand offsets advance by a constant per row.
@@ -335,6 +351,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
                            ? kInvalidNm
                            : __double2int_rd(S.nmf[ct] * ldexp(1.0, 20 - et - em));
       }
+      TR(3);
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
@@ -361,11 +378,14 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
       const int s = m % kStages, b = m & 1;
       const int rows = static_cast<int>(n - t * kTile < kTile ? n - t * kTile : kTile);
+      TR(6);
       mbar_wait(&S.cfull[s], (m / kStages) & 1);
       mbar_wait(&S.full[s], (m / kStages) & 1);
+      TR(0);
       const int flag = S.tile_flag[s];
       const double* xs = reinterpret_cast<const double*>(smem + s * kXStage);
       mbar_wait(&S.tfull[b], (m >> 1) & 1);
+      TR(1);
       tc_fence_after();
       int tv[32];
       int lmin = kInvalidNm;
@@ -403,6 +423,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.tempty[b]);
       S.hmin[h][q] = lmin;
+      TR(2);
       named_bar(1, 256);
       uint32_t mask = 0;
       if (!flag) {
@@ -489,6 +510,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       named_bar(1, 256);
       if (h == 0 && a >= 0) S.sorted[S.woff[quarter][a] + rank] = q;
       named_bar(1, 256);
+      TR(3);
       // bucket-reduce: warp ew owns centroids ew + 8u, lane owns columns 2*lane, 2*lane+1;
       // each centroid's samples are contiguous in `sorted`, in ascending row order
       {
@@ -518,6 +540,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
           }
         }
       }
+      TR(4);
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.sempty[s]);
     }
@@ -539,6 +562,11 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     }
     if (ew == 0 && lane == 0) pend_count[blockIdx.x] = pending;
   }
+  if (trace && lane == 0 && (warp == kWarpProd || warp == kWarpMma || warp == kWarpC0 || warp == kWarpE0)) {
+    const int role = warp == kWarpProd ? 0 : warp == kWarpMma ? 1 : warp == kWarpC0 ? 2 : 3;
+    for (int i = 0; i < 8; ++i) trace[(static_cast<size_t>(blockIdx.x) * 4 + role) * 8 + i] = tr[i];
+  }
+#undef TR
   __syncthreads();
   if (warp == kWarpMma) {
     tc_fence_after();
@@ -725,9 +753,28 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
   DLX_CUDA(cudaFuncSetAttribute(sk::kmeans_screened_kernel,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sk::kSmemBytes)));
+  static const bool tracing = getenv("DLX_KMEANS_TRACE") != nullptr;
+  long long* trace = nullptr;
+  if (tracing) DLX_CUDA(cudaMalloc(&trace, sizeof(long long) * grid * 32));
   sk::kmeans_screened_kernel<<<grid, sk::kThreads, sk::kSmemBytes, stream>>>(
-      x, n, d, k, mu, assign, w.part_counts, w.part_sums, w.pend_idx, w.pend_mask, w.pend_count, cap);
+      x, n, d, k, mu, assign, w.part_counts, w.part_sums, w.pend_idx, w.pend_mask, w.pend_count, cap,
+      trace);
   DLX_LAUNCHED("kmeans_screened_kernel");
+  if (tracing) {  // debug only: per-role cycle split averaged over CTAs
+    std::vector<long long> h(static_cast<size_t>(grid) * 32);
+    DLX_CUDA(cudaStreamSynchronize(stream));
+    DLX_CUDA(cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+    cudaFree(trace);
+    const char* names[4] = {"producer", "mma", "convert", "epilogue"};
+    for (int r = 0; r < 4; ++r) {
+      double avg[8] = {0};
+      for (int b = 0; b < grid; ++b)
+        for (int i = 0; i < 8; ++i) avg[i] += static_cast<double>(h[(static_cast<size_t>(b) * 4 + r) * 8 + i]) / grid;
+      fprintf(stderr, "[dlx trace] %-9s", names[r]);
+      for (int i = 0; i < 8; ++i) fprintf(stderr, " %10.0f", avg[i]);
+      fprintf(stderr, "\n");
+    }
+  }
   const size_t rsmem =
       (static_cast<size_t>(2 * k + sk::kResChunk) * d + sk::kResMaxPairs) * sizeof(double);
   DLX_CUDA(cudaFuncSetAttribute(sk::kmeans_resolve_kernel,

@@ -360,7 +360,14 @@ class Executor {
 
   Val exec_block(int b) {
     const Block& bl = P.blocks.at(b);
-    for (int s : bl.stmts) env_[s] = exec_stmt(P.stmts.at(s));
+    for (int s : bl.stmts) {
+      const Stmt& st = P.stmts.at(s);
+      if (st.op == "ParallelLoop") {
+        run_loop(st);  // binds every live elem's `out` (elems[0].out is the statement's own sym)
+      } else {
+        env_[s] = exec_stmt(st);
+      }
+    }
     return atom(bl.result);
   }
 
@@ -584,15 +591,9 @@ class Executor {
       return e;
     }
     if (op == "ParallelLoop") {
-      // nested loop: only a single live Reduce elem over a loop-invariant range
+      // nested (possibly horizontally fused) loop: every live elem must be a plain reduce over
+      // a loop-invariant range; each becomes one Red node bound to its elem's `out`
       const Loop& L = *s.loop;
-      const Elem* el = nullptr;
-      for (const Elem& e : L.elems)
-        if (e.live) {
-          if (el) gen_fail("nested multiloop with several elems");
-          el = &e;
-        }
-      if (!el || el->kind != "reduce" || el->cond >= 0) gen_fail("nested loop other than a plain reduce");
       auto rng = sym_atom(L.range);
       int64_t range;
       if (!is_const_int(rng, &range)) gen_fail("nested reduce over a non-constant range");
@@ -600,16 +601,24 @@ class Executor {
       idx->sym = L.index;
       sym_[L.index] = idx;
       sym_block(L.body);
-      auto elem = sym_block(el->elem);
-      sym_[el->rv_left] = mk(SE::RvL, el->out_ty.t);
-      sym_[el->rv_right] = mk(SE::RvR, el->out_ty.t);
-      auto comb = sym_block(el->combine);
-      auto r = mk(SE::Red, el->out_ty.t);
-      r->range = range;
-      r->zero = el->zero;
-      r->sym = L.index;
-      r->a = {elem, comb};
-      return r;
+      SEP first;
+      for (const Elem& e : L.elems) {
+        if (!e.live) continue;
+        if (e.kind != "reduce" || e.cond >= 0) gen_fail("nested loop elem other than a plain reduce");
+        auto elem = sym_block(e.elem);
+        sym_[e.rv_left] = mk(SE::RvL, e.out_ty.t);
+        sym_[e.rv_right] = mk(SE::RvR, e.out_ty.t);
+        auto comb = sym_block(e.combine);
+        auto r = mk(SE::Red, e.out_ty.t);
+        r->range = range;
+        r->zero = e.zero;
+        r->sym = L.index;
+        r->a = {elem, comb};
+        sym_[e.out] = r;
+        if (!first) first = r;
+      }
+      if (!first) gen_fail("nested loop without live elems");
+      return first;
     }
     gen_fail("don't know how to generate code for: " + op + " inside a multiloop");
   }
