@@ -84,29 +84,27 @@ static_assert(kOffA1 % 1024 == 0 && kOffB1 % 1024 == 0 && kOffA2 % 512 == 0 && k
               "UMMA operand alignment");
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: x + kMagic rounds x to an integer
 
+constexpr int kListCap = 16;  // fold list slots per (warp, owned centroid) per tile
+
 struct Misc {
   uint64_t full[kStages], sempty[kStages], cfull[kStages];
   uint64_t a_full, a_empty, tfull[2], tempty[2];
   unsigned long long valid;
   uint32_t tmem_base;
-  int em, yabs, disabled;
+  int em, yabs, disabled, window;
   uint32_t mu_maxhi;
-  int tile_flag[kStages];
-  int tile_w[kStages];      // screen window W in score units
-  alignas(16) int nmt[kStages][kMaxK];  // floor(|mu_c|^2 / U_t) per stage (int4-loaded)
+  alignas(16) int nm0[kMaxK];             // floor(|mu_c|^2 / U), U = 2^(e_t + e_m - 20), e_t = e_m + 1
   double nmf[kMaxK];
   int hmin[2][kMmaM];
   uint32_t cmask[2][kMmaM];
+  unsigned char rowflag[kStages][kMmaM];  // sample needs the exact chain (|x| >= 2^e_t, inf, NaN)
   int pcount[4];
-  uint32_t cscr[2][8];
-  int wcnt[4][kMaxK];       // per quarter: samples of the tile assigned to c
-  int woff[4][kMaxK];       // per quarter: first slot of its c-samples in `sorted`
-  int cstart[kMaxK + 1];    // per centroid: [cstart[c], cstart[c+1]) in `sorted`
-  int sorted[kMmaM];        // the tile's resolved samples, stably sorted by centroid
+  uint32_t gm[4][kMaxK];                  // per quarter: lanes (rows) of the tile assigned to c
+  unsigned char list[8][8][kListCap];     // per fold warp, per owned centroid: rows, ascending
 };
 constexpr uint32_t kSmemBytes = kOffMisc + sizeof(Misc);
 static_assert(kSmemBytes <= 232448, "shared-memory plan exceeds 227 KiB");
-constexpr int kInvalidNm = 0x70000000;  // > any valid score (|Q| < 2^26, nm <= 2^28)
+constexpr int kInvalidNm = 0x70000000;  // > any valid score (|Q| < 2^26, nm <= 2^25)
 constexpr int kNoCandidate = 0x60000000;
 
 __device__ __forceinline__ int exp_bound(uint32_t maxhi) {
@@ -138,10 +136,15 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
                        long long* __restrict__ trace) {
   extern __shared__ __align__(1024) unsigned char smem[];
   Misc& S = *reinterpret_cast<Misc*>(smem + kOffMisc);
-  // optional per-role cycle accounting (DLX_KMEANS_TRACE=1): lane 0 of one warp per role
+  // optional per-role cycle accounting (build with -DDLX_KMEANS_TRACE, run with
+  // DLX_KMEANS_TRACE=1): lane 0 of one warp per role
+#ifdef DLX_KMEANS_TRACE
   long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long t0 = clock64();
 #define TR(slot) do { const long long _t = clock64(); tr[slot] += _t - t0; t0 = _t; } while (0)
+#else
+#define TR(slot) do { } while (0)
+#endif
   unsigned char* A1 = smem + kOffA1;
   unsigned char* A2 = smem + kOffA2;
   unsigned char* B1 = smem + kOffB1;
@@ -214,6 +217,18 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       atomicMax(&S.yabs, sa);
     }
   }
+  __syncthreads();
+  if (tid < kMaxK) {  // per-launch score constants (the sample exponent is fixed at e_t = e_m + 1)
+    const unsigned long long valid = S.valid;
+    S.nm0[tid] = (S.disabled || !((valid >> tid) & 1))
+                     ? kInvalidNm
+                     : __double2int_rd(S.nmf[tid] * ldexp(1.0, 19 - 2 * S.em));
+    if (tid == 0) {
+      // W = 9 + ceil(4e), e = ((d*2^22 + max_c sum|Y'|)/2 + d/4) / 2^24  (+1 margin)
+      const long long num = (static_cast<long long>(d) << 22) + S.yabs;
+      S.window = 10 + static_cast<int>((2 * num + d + (1ll << 24) - 1) >> 24);
+    }
+  }
   fence_proxy_async_smem();
   if (warp == kWarpMma) tmem_alloc<kTmemCols>(&S.tmem_base);
   tc_fence_before();
@@ -278,8 +293,9 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     // ======================= converters (128 threads) =======================
     const int ct = tid - kWarpC0 * 32;
     const int cw = ct >> 5;
-    const int em = S.em, disabled = S.disabled, yabs = S.yabs;
-    const unsigned long long valid = S.valid;
+    const int em = S.em, disabled = S.disabled;
+    const double scale = disabled ? 0.0 : ldexp(1.0, 21 - em);   // 2^(22 - e_t), e_t = e_m + 1
+    const uint32_t hw_limit = static_cast<uint32_t>(1023 + em + 1) << 20;  // |x| >= 2^e_t
     const int half = lane >> 4, j0 = 4 * (lane & 15);
     const int key = cw + 4 * half;  // row & 7 of every row this thread converts
     const uint32_t off_h = sw128_offset(key, j0), off_l = sw128_offset(key, 64 + j0);
@@ -292,64 +308,38 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       mbar_wait(&S.full[s], (m / kStages) & 1);
       TR(0);
       const double* xs = reinterpret_cast<const double*>(smem + s * kXStage);
-      // pass 1: tile exponent (max |x| high word; >= 0x7ff00000 means inf / NaN present)
-      uint32_t mx = 0;
-      const int pairs = rows * d / 2;
-      const double2* xs2 = reinterpret_cast<const double2*>(xs);
-#pragma unroll 4
-      for (int p = ct; p < pairs; p += 128) {
-        const double2 v = xs2[p];
-        mx = max(mx, max(static_cast<uint32_t>(__double2hiint(v.x)) & 0x7fffffffu,
-                         static_cast<uint32_t>(__double2hiint(v.y)) & 0x7fffffffu));
-      }
-      mx = __reduce_max_sync(0xffffffffu, mx);
-      if (lane == 0) S.cscr[m & 1][cw] = mx;
-      named_bar(2, 128);
-      uint32_t tmx = 0;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) tmx = max(tmx, S.cscr[m & 1][w]);
-      const bool tbad = tmx >= 0x7ff00000u;
-      const int et = tmx == 0 ? em : exp_bound(tmx);
-      const int flag = (tbad || disabled || et > 400 || et < -400 || em - et > 2 || et - em > 8) ? 1 : 0;
       TR(1);
       if (m >= 1) mbar_wait(&S.a_empty, (m - 1) & 1);
       TR(2);
-      // pass 2: Y = rint(x * 2^(22-e_t)).  Thread (cw, half, lane16) converts columns
-      // 4*lane16 .. +3 of rows q = 8*mm + key, key = cw + 4*half (mm = 0..15), so its swizzle
-      // key is fixed and its operand offsets advance by a constant per row.
-      const double scale = flag ? 0.0 : ldexp(1.0, 22 - et);
+      // Y = rint(x * 2^(22-e_t)) with e_t = e_m + 1 fixed per launch.  Thread (cw, half,
+      // lane16) converts columns 4*lane16 .. +3 of rows q = 8*mm + key, key = cw + 4*half
+      // (mm = 0..15), so its swizzle key is fixed and its operand offsets advance by a
+      // constant per row.  A row with |x| >= 2^e_t, inf or NaN is flagged (exact chain).
       const double* xrow = xs + key * d + j0;
+      const bool colok = j0 < d, col2ok = j0 + 2 < d;
 #pragma unroll 4
       for (int mm = 0; mm < kMmaM / 8; ++mm) {
         const int q = 8 * mm + key;
-        int Y0 = 0, Y1 = 0, Y2 = 0, Y3 = 0;
-        if (q < rows && j0 < d) {
-          const double2 v0 = *reinterpret_cast<const double2*>(xrow + mm * 8 * d);
-          Y0 = rint_fma(v0.x, scale);
-          Y1 = rint_fma(v0.y, scale);
-          if (j0 + 2 < d) {
-            const double2 v1 = *reinterpret_cast<const double2*>(xrow + mm * 8 * d + 2);
-            Y2 = rint_fma(v1.x, scale);
-            Y3 = rint_fma(v1.y, scale);
-          }
-        }
+        const bool ok = q < rows && colok;
+        const double* src = ok ? xrow + mm * 8 * d : xs;
+        const double2 v0 = *reinterpret_cast<const double2*>(src);
+        const double2 v1 = (ok && col2ok) ? *reinterpret_cast<const double2*>(src + 2) : make_double2(0.0, 0.0);
+        const double a0 = ok ? v0.x : 0.0, a1 = ok ? v0.y : 0.0;
+        const uint32_t hx = max(max(static_cast<uint32_t>(__double2hiint(a0)) & 0x7fffffffu,
+                                    static_cast<uint32_t>(__double2hiint(a1)) & 0x7fffffffu),
+                                max(static_cast<uint32_t>(__double2hiint(v1.x)) & 0x7fffffffu,
+                                    static_cast<uint32_t>(__double2hiint(v1.y)) & 0x7fffffffu));
+        const unsigned badm = __ballot_sync(0xffffffffu, hx >= hw_limit);
+        if ((lane & 15) == 0) S.rowflag[s][q] = static_cast<unsigned char>(
+            disabled || ((badm >> (16 * half)) & 0xffffu) != 0);
+        const int Y0 = rint_fma(a0, scale), Y1 = rint_fma(a1, scale);
+        const int Y2 = rint_fma(v1.x, scale), Y3 = rint_fma(v1.y, scale);
         // bytes of Y (little endian): b0 = F, b1 = l, b2 = h (low byte of Y >> 16)
         const uint32_t p01 = __byte_perm(Y0, Y1, 0x6240), p23 = __byte_perm(Y2, Y3, 0x6240);
         const uint32_t q01 = __byte_perm(Y0, Y1, 0x0051), q23 = __byte_perm(Y2, Y3, 0x0051);
         *reinterpret_cast<uint32_t*>(A1 + off_h + mm * 1024) = __byte_perm(p01, p23, 0x7632);  // h
         *reinterpret_cast<uint32_t*>(A1 + off_l + mm * 1024) = __byte_perm(q01, q23, 0x5410);  // l
         *reinterpret_cast<uint32_t*>(A2 + off_f + mm * 512) = __byte_perm(p01, p23, 0x5410);   // F
-      }
-      if (ct == 0) {
-        S.tile_flag[s] = flag;
-        // W = 9 + ceil(4e), e = ((d*2^22 + max_c sum|Y'|)/2 + d/4) / 2^24
-        const long long num = (static_cast<long long>(d) << 22) + yabs;
-        S.tile_w[s] = 10 + static_cast<int>((2 * num + d + (1ll << 24) - 1) >> 24);
-      }
-      if (ct < kMaxK) {  // |mu_c|^2 in units U_t = 2^(e_t+e_m-20): <= 2^28 under the gap guard
-        S.nmt[s][ct] = (flag || !((valid >> ct) & 1))
-                           ? kInvalidNm
-                           : __double2int_rd(S.nmf[ct] * ldexp(1.0, 20 - et - em));
       }
       TR(3);
       fence_proxy_async_smem();
@@ -367,13 +357,18 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     const int q = quarter * 32 + lane;      // sample row within the tile (M row)
     const unsigned long long kmask = k == 64 ? ~0ull : ((1ull << k) - 1);
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+    const int window = S.window;
     long long* my_pidx = pend_idx + static_cast<size_t>(blockIdx.x) * pend_cap;
     unsigned long long* my_pmask = pend_mask + static_cast<size_t>(blockIdx.x) * pend_cap;
     long long pending = 0;
+    // fold ownership: warp ew owns centroids ew + 8u (u = 0..7), lane owns columns 2l, 2l+1
+    const int jc = 2 * lane;
+    const int uu = lane >> 2, Qq = lane & 3;  // this lane's (owned centroid, quarter) mask slot
     double acc[8][2];
-    long long ctot0 = 0, ctot1 = 0;  // scan warp: samples folded per centroid 2*lane, 2*lane+1
+    long long cnt_lane = 0;                   // samples of (centroid ew + 8uu, quarter Qq)
 #pragma unroll
     for (int u = 0; u < 8; ++u) acc[u][0] = acc[u][1] = 0.0;
+    const int4* nm4 = reinterpret_cast<const int4*>(&S.nm0[32 * h]);
     for (int m = 0; m < mtiles; ++m) {
       const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
       const int s = m % kStages, b = m & 1;
@@ -382,41 +377,37 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       mbar_wait(&S.cfull[s], (m / kStages) & 1);
       mbar_wait(&S.full[s], (m / kStages) & 1);
       TR(0);
-      const int flag = S.tile_flag[s];
       const double* xs = reinterpret_cast<const double*>(smem + s * kXStage);
       mbar_wait(&S.tfull[b], (m >> 1) & 1);
       TR(1);
       tc_fence_after();
       int tv[32];
       int lmin = kInvalidNm;
-      if (!flag) {
-        const int4* nm4 = reinterpret_cast<const int4*>(&S.nmt[s][32 * h]);
 #pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
-          const uint32_t col = b * kAccCols + 32 * h + 16 * ch;
-          int hh[16], cr[16], w1[16], w2[16];
-          tmem_ld16(tmem + lane_base + col, hh);
-          tmem_ld16(tmem + lane_base + col + 64, cr);
-          tmem_ld16(tmem + lane_base + col + 128, w1);
-          tmem_ld16(tmem + lane_base + col + 192, w2);
-          int nm[16];
+      for (int ch = 0; ch < 2; ++ch) {
+        const uint32_t col = b * kAccCols + 32 * h + 16 * ch;
+        int hh[16], cr[16], w1[16], w2[16];
+        tmem_ld16(tmem + lane_base + col, hh);
+        tmem_ld16(tmem + lane_base + col + 64, cr);
+        tmem_ld16(tmem + lane_base + col + 128, w1);
+        tmem_ld16(tmem + lane_base + col + 192, w2);
+        int nm[16];
 #pragma unroll
-          for (int u4 = 0; u4 < 4; ++u4) {
-            const int4 v4 = nm4[4 * ch + u4];
-            nm[4 * u4 + 0] = v4.x;
-            nm[4 * u4 + 1] = v4.y;
-            nm[4 * u4 + 2] = v4.z;
-            nm[4 * u4 + 3] = v4.w;
-          }
-          tmem_ld_wait();
+        for (int u4 = 0; u4 < 4; ++u4) {
+          const int4 v4 = nm4[4 * ch + u4];
+          nm[4 * u4 + 0] = v4.x;
+          nm[4 * u4 + 1] = v4.y;
+          nm[4 * u4 + 2] = v4.z;
+          nm[4 * u4 + 3] = v4.w;
+        }
+        tmem_ld_wait();
 #pragma unroll
-          for (int u = 0; u < 16; ++u) {
-            // invalid centroids: zero B rows (Q = 0) and nm = kInvalidNm
-            const int Q = hh[u] * 256 + cr[u] + (w1[u] >> 8) + (w2[u] >> 16);
-            const int v = nm[u] - 2 * Q;
-            tv[16 * ch + u] = v;
-            lmin = min(lmin, v);
-          }
+        for (int u = 0; u < 16; ++u) {
+          // invalid centroids: zero B rows (Q = 0) and nm = kInvalidNm
+          const int Q = hh[u] * 256 + cr[u] + (w1[u] >> 8) + (w2[u] >> 16);
+          const int v = nm[u] - 2 * Q;
+          tv[16 * ch + u] = v;
+          lmin = min(lmin, v);
         }
       }
       tc_fence_before();
@@ -426,10 +417,10 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       TR(2);
       named_bar(1, 256);
       uint32_t mask = 0;
-      if (!flag) {
+      {
         const int tmin = min(S.hmin[0][q], S.hmin[1][q]);
         if (tmin < kNoCandidate) {
-          const int thr = tmin + S.tile_w[s];
+          const int thr = tmin + window;
 #pragma unroll
           for (int u = 0; u < 32; ++u)
             if (tv[u] <= thr) mask |= 1u << u;
@@ -439,32 +430,31 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       named_bar(1, 256);
       unsigned long long full = 0;
       bool pend = false;
-      int a = -1, rank = 0;
       if (h == 0) {
+        int a = -1;
         if (q < rows) {
-          if (flag) {
-            full = kmask;  // guarded tile: the reference chain over every centroid
+          if (S.rowflag[s][q]) {
+            full = kmask;  // |x| out of the screen's range, inf or NaN: the exact chain over all c
+            pend = true;
           } else {
             full = static_cast<unsigned long long>(S.cmask[0][q]) |
                    (static_cast<unsigned long long>(S.cmask[1][q]) << 32);
-          }
-          if (full == 0) {
-            a = 0;  // no finite centroid: the chain keeps its start index
-          } else if (!flag && (full & (full - 1)) == 0) {
-            a = __ffsll(static_cast<long long>(full)) - 1;
-          } else {
-            pend = true;  // several survivors: resolved by the exact chain (resolve kernel)
+            if (full == 0) {
+              a = 0;  // no finite centroid: the chain keeps its start index
+            } else if ((full & (full - 1)) == 0) {
+              a = __ffsll(static_cast<long long>(full)) - 1;
+            } else {
+              pend = true;  // several survivors: resolved by the exact chain (resolve kernel)
+            }
           }
           if (a >= 0 && assign) assign[t * kTile + q] = a;
         }
-        // stable counting sort of the quarter's samples by centroid: rank within the warp
+        // group masks: gm[quarter][c] = this quarter's rows resolved to centroid c
         const unsigned grp = __match_any_sync(0xffffffffu, a);
-        const unsigned lower = grp & ((1u << lane) - 1);
-        rank = __popc(lower);
-        S.wcnt[quarter][lane] = 0;
-        S.wcnt[quarter][lane + 32] = 0;
+        S.gm[quarter][lane] = 0u;
+        S.gm[quarter][lane + 32] = 0u;
         __syncwarp();
-        if (lower == 0 && a >= 0) S.wcnt[quarter][a] = __popc(grp);
+        if ((grp & ((1u << lane) - 1)) == 0 && a >= 0) S.gm[quarter][a] = grp;
       }
       const unsigned pb = __ballot_sync(0xffffffffu, pend);
       if (h == 0 && lane == 0) S.pcount[quarter] = __popc(pb);
@@ -480,62 +470,76 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         }
         pending += p0 + p1 + p2 + S.pcount[3];
       }
-      if (ew == 0) {  // one warp: per-centroid totals, exclusive scan, per-quarter offsets
-        const int c0 = 2 * lane, c1 = c0 + 1;
-        int w0[4], w1[4];
-#pragma unroll
-        for (int Qr = 0; Qr < 4; ++Qr) w0[Qr] = S.wcnt[Qr][c0], w1[Qr] = S.wcnt[Qr][c1];
-        const int t0 = w0[0] + w0[1] + w0[2] + w0[3], t1 = w1[0] + w1[1] + w1[2] + w1[3];
-        ctot0 += t0;
-        ctot1 += t1;
-        int incl = t0 + t1;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int v = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += v;
-        }
-        const int s0 = incl - t0 - t1, s1 = s0 + t0;
-        S.cstart[c0] = s0;
-        S.cstart[c1] = s1;
-        if (lane == 31) S.cstart[kMaxK] = incl;
-        int r0 = s0, r1 = s1;
-#pragma unroll
-        for (int Qr = 0; Qr < 4; ++Qr) {
-          S.woff[Qr][c0] = r0;
-          S.woff[Qr][c1] = r1;
-          r0 += w0[Qr];
-          r1 += w1[Qr];
-        }
-      }
-      named_bar(1, 256);
-      if (h == 0 && a >= 0) S.sorted[S.woff[quarter][a] + rank] = q;
-      named_bar(1, 256);
       TR(3);
-      // bucket-reduce: warp ew owns centroids ew + 8u, lane owns columns 2*lane, 2*lane+1;
-      // each centroid's samples are contiguous in `sorted`, in ascending row order
+      // ---- bucket-reduce.  Lane (uu, Qq) expands its mask into the warp's per-centroid row
+      // list (rows ascending: quarter-major, then lane), then every owned centroid folds up
+      // to four rows with independent loads before its adds (ILP across centroids).
       {
-        const int jc = 2 * lane;
-        const int cc = ew + 8 * (lane >> 1) + (lane & 1);
-        const int bounds = (lane < 16 && cc <= kMaxK) ? S.cstart[cc] : 0;
+        const unsigned gmv = S.gm[Qq][ew + 8 * uu];
+        const int pc = __popc(gmv);
+        cnt_lane += pc;
+        int incl = pc;
+        {
+          int v = __shfl_up_sync(0xffffffffu, incl, 1);
+          if (Qq >= 1) incl += v;
+          v = __shfl_up_sync(0xffffffffu, incl, 2);
+          if (Qq >= 2) incl += v;
+        }
+        int slot = incl - pc;
+        unsigned mm = gmv;
+        while (mm) {
+          const int l = __ffs(mm) - 1;
+          mm &= mm - 1;
+          if (slot < kListCap) S.list[ew][uu][slot] = static_cast<unsigned char>(32 * Qq + l);
+          ++slot;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, lane | 3);  // samples of centroid uu
+        __syncwarp();
+        int nu[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int beg = __shfl_sync(0xffffffffu, bounds, 2 * u);
-          const int end = __shfl_sync(0xffffffffu, bounds, 2 * u + 1);
-          if (jc < d) {
-            int p = beg;
-            for (; p + 1 < end; p += 2) {
-              const int r0 = S.sorted[p], r1 = S.sorted[p + 1];
-              const double2 v0 = *reinterpret_cast<const double2*>(xs + r0 * d + jc);
-              const double2 v1 = *reinterpret_cast<const double2*>(xs + r1 * d + jc);
-              acc[u][0] += v0.x;
-              acc[u][1] += v0.y;
-              acc[u][0] += v1.x;
-              acc[u][1] += v1.y;
-            }
-            if (p < end) {
-              const double2 v0 = *reinterpret_cast<const double2*>(xs + S.sorted[p] * d + jc);
-              acc[u][0] += v0.x;
-              acc[u][1] += v0.y;
+        for (int u = 0; u < 8; ++u) nu[u] = __shfl_sync(0xffffffffu, tot, 4 * u);
+        if (jc < d) {
+#pragma unroll
+          for (int u0 = 0; u0 < 8; u0 += 2) {
+            double2 v[2][4];
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+#pragma unroll
+              for (int t4 = 0; t4 < 4; ++t4)
+                v[e][t4] = t4 < nu[u0 + e]
+                               ? *reinterpret_cast<const double2*>(xs + S.list[ew][u0 + e][t4] * d + jc)
+                               : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+#pragma unroll
+              for (int t4 = 0; t4 < 4; ++t4)
+                if (t4 < nu[u0 + e]) {
+                  acc[u0 + e][0] += v[e][t4].x;
+                  acc[u0 + e][1] += v[e][t4].y;
+                }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (nu[u] <= 4) continue;
+            if (nu[u] <= kListCap) {
+              for (int t4 = 4; t4 < nu[u]; ++t4) {
+                const double2 w = *reinterpret_cast<const double2*>(xs + S.list[ew][u][t4] * d + jc);
+                acc[u][0] += w.x;
+                acc[u][1] += w.y;
+              }
+            } else {  // crowded centroid: walk the quarter masks directly (same row order)
+              int seen = 0;
+              for (int Qr = 0; Qr < 4; ++Qr) {
+                unsigned g = S.gm[Qr][ew + 8 * u];
+                while (g) {
+                  const int row = 32 * Qr + __ffs(g) - 1;
+                  g &= g - 1;
+                  if (seen++ < 4) continue;
+                  const double2 w = *reinterpret_cast<const double2*>(xs + row * d + jc);
+                  acc[u][0] += w.x;
+                  acc[u][1] += w.y;
+                }
+              }
             }
           }
         }
@@ -546,7 +550,6 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     }
     // flush this CTA's partial activation record
     double* ps = part_sums + static_cast<size_t>(blockIdx.x) * k * d;
-    const int jc = 2 * lane;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int c = ew + 8 * u;
@@ -555,17 +558,18 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         if (jc + 1 < d) ps[c * d + jc + 1] = acc[u][1];
       }
     }
-    if (ew == 0) {
-      long long* pc = part_counts + static_cast<size_t>(blockIdx.x) * k;
-      if (2 * lane < k) pc[2 * lane] = ctot0;
-      if (2 * lane + 1 < k) pc[2 * lane + 1] = ctot1;
-    }
+    long long ct = cnt_lane;  // sum the four quarter lanes of each owned centroid
+    ct += __shfl_xor_sync(0xffffffffu, ct, 1);
+    ct += __shfl_xor_sync(0xffffffffu, ct, 2);
+    if (Qq == 0 && ew + 8 * uu < k) part_counts[static_cast<size_t>(blockIdx.x) * k + ew + 8 * uu] = ct;
     if (ew == 0 && lane == 0) pend_count[blockIdx.x] = pending;
   }
+#ifdef DLX_KMEANS_TRACE
   if (trace && lane == 0 && (warp == kWarpProd || warp == kWarpMma || warp == kWarpC0 || warp == kWarpE0)) {
     const int role = warp == kWarpProd ? 0 : warp == kWarpMma ? 1 : warp == kWarpC0 ? 2 : 3;
     for (int i = 0; i < 8; ++i) trace[(static_cast<size_t>(blockIdx.x) * 4 + role) * 8 + i] = tr[i];
   }
+#endif
 #undef TR
   __syncthreads();
   if (warp == kWarpMma) {

@@ -24,6 +24,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstdarg>
+#include <cstdio>
 #include <cstring>
 #include <json.hpp>
 #include <map>
@@ -208,6 +209,16 @@ Program parse_program(const std::string& text) {
 }
 
 // ---- runtime values ---------------------------------------------------------------------------
+// Dry run (DLX_PROGRAM_DRYRUN=1, CPU-only diagnostics): no device memory and no launches; loops
+// are still parsed, symbolically evaluated and matched, so the report shows which lowering
+// each loop would get.  Printed values are meaningless in a dry run.
+static bool g_dry = false;
+static bool g_debug = false;  // DLX_PROGRAM_DEBUG=1: why a specialised family did not match
+#define MISS(why)                                                        \
+  do {                                                                   \
+    if (g_debug) fprintf(stderr, "[dlx program] %s: %s\n", __func__, why); \
+    return false;                                                        \
+  } while (0)
 struct DevVec {
   void* p = nullptr;
   int64_t n = 0;
@@ -239,6 +250,7 @@ VecP new_vec(int64_t n, Ty elem, cudaStream_t st, bool zero) {
   auto v = std::make_shared<DevVec>();
   v->n = n;
   v->elem = elem;
+  if (g_dry) return v;
   ckc(cudaMalloc(&v->p, std::max<size_t>(16, static_cast<size_t>(n) * v->esize())), "cudaMalloc");
   if (zero) ckc(cudaMemsetAsync(v->p, 0, static_cast<size_t>(n) * v->esize(), st), "cudaMemset");
   return v;
@@ -298,6 +310,14 @@ bool is_const_dbl(const SEP& s, double* v = nullptr) {
   return false;
 }
 
+// the same value: one node, or two literal nodes with equal payloads (literals are not shared)
+bool same_se(const SEP& x, const SEP& y) {
+  if (x == y) return true;
+  if (x->k == SE::Const && y->k == SE::Const && x->ty == y->ty)
+    return x->ty == Ty::Double ? std::memcmp(&x->cd, &y->cd, 8) == 0 : x->ci == y->ci;
+  return false;
+}
+
 // affine form a*Idx + b*Inner(sym) + c
 struct Affine {
   int64_t a = 0, b = 0, c = 0;
@@ -340,6 +360,7 @@ class Executor {
 
   // symbolic state of the loop being lowered
   int loop_index_ = -1;
+  int64_t dry_n_ = 0;
   std::unordered_map<int, SEP> sym_;
 
   // ---- host interpretation ----------------------------------------------------------------------
@@ -403,6 +424,7 @@ class Executor {
 
   Val vec_get(const VecP& v, int64_t i) {
     if (i < 0 || i >= v->n) trap("TrapIndexOutOfBounds: index " + std::to_string(i));
+    if (g_dry) return v->elem == Ty::Double ? Val{0.5} : v->elem == Ty::Bool ? Val{false} : Val{int64_t{1}};
     ckc(cudaStreamSynchronize(st_), "sync");
     if (v->elem == Ty::Double) {
       double x;
@@ -421,6 +443,7 @@ class Executor {
 
   void vec_set(const VecP& v, int64_t i, const Val& x) {
     if (i < 0 || i >= v->n) trap("TrapIndexOutOfBounds: store index " + std::to_string(i));
+    if (g_dry) return;
     if (v->elem == Ty::Double) {
       const double d = x.d();
       ckc(cudaMemcpyAsync(static_cast<double*>(v->p) + i, &d, 8, cudaMemcpyHostToDevice, st_), "h2d");
@@ -470,7 +493,8 @@ class Executor {
       const int64_t n = atom(s.args[0]).i();
       const bool ints = op == "VectorRandInt";
       VecP v = new_vec(n, ints ? Ty::Int : Ty::Double, st_, false);
-      if (ints)
+      if (g_dry) {
+      } else if (ints)
         ck(dlx_rng_ints(static_cast<int64_t*>(v->p), n, atom(s.args[1]).i(), seed_, draws_, st_));
       else
         ck(dlx_rng_units(static_cast<double*>(v->p), n, seed_, draws_, st_));
@@ -494,8 +518,10 @@ class Executor {
           raw[q] = s.lits[q].i;
         }
       }
-      ckc(cudaMemcpyAsync(v->p, raw.data(), raw.size() * 8, cudaMemcpyHostToDevice, st_), "h2d");
-      ckc(cudaStreamSynchronize(st_), "sync");
+      if (!g_dry) {
+        ckc(cudaMemcpyAsync(v->p, raw.data(), raw.size() * 8, cudaMemcpyHostToDevice, st_), "h2d");
+        ckc(cudaStreamSynchronize(st_), "sync");
+      }
       return Val{v};
     }
     if (op == "VectorLength") return Val{atom(s.args[0]).vec()->n};
@@ -644,20 +670,20 @@ class Executor {
   };
   // D = Red(range d, zero 0.0, Plus, Times(t, t), t = Load(X, d*Idx + J) - Load(M, c*d + J))
   bool match_distance(const SEP& D, int64_t c, KmeansShape* ks) {
-    if (D->k != SE::Red || D->ty != Ty::Double || !is_plus_combine(D->a[1])) return false;
-    if (D->zero.k != Atom::Double || D->zero.d != 0.0) return false;
+    if (D->k != SE::Red || D->ty != Ty::Double || !is_plus_combine(D->a[1])) MISS("match_distance#1");
+    if (D->zero.k != Atom::Double || D->zero.d != 0.0) MISS("match_distance#2");
     const SEP& el = D->a[0];
-    if (el->k != SE::Bin || el->op != "Times" || el->a[0] != el->a[1]) return false;
+    if (el->k != SE::Bin || el->op != "Times" || !same_se(el->a[0], el->a[1])) MISS("match_distance#3");
     const SEP& t = el->a[0];
-    if (t->k != SE::Bin || t->op != "Minus" || t->a[0]->k != SE::Load || t->a[1]->k != SE::Load) return false;
+    if (t->k != SE::Bin || t->op != "Minus" || t->a[0]->k != SE::Load || t->a[1]->k != SE::Load) MISS("match_distance#4");
     auto ax = affine(t->a[0]->a[1]), am = affine(t->a[1]->a[1]);
-    if (!ax || !am) return false;
+    if (!ax || !am) MISS("match_distance#5");
     const int64_t d = D->range;
-    if (ax->a != d || ax->b != 1 || ax->c != 0 || ax->inner != D->sym) return false;
-    if (am->a != 0 || am->b != 1 || am->c != c * d || am->inner != D->sym) return false;
+    if (ax->a != d || ax->b != 1 || ax->c != 0 || ax->inner != D->sym) MISS("match_distance#6");
+    if (am->a != 0 || am->b != 1 || am->c != c * d || am->inner != D->sym) MISS("match_distance#7");
     VecP X = t->a[0]->a[0]->vec, M = t->a[1]->a[0]->vec;
-    if (X->elem != Ty::Double || M->elem != Ty::Double) return false;
-    if (ks->x && (ks->x != X || ks->mu != M || ks->d != d)) return false;
+    if (X->elem != Ty::Double || M->elem != Ty::Double) MISS("match_distance#8");
+    if (ks->x && (ks->x != X || ks->mu != M || ks->d != d)) MISS("match_distance#9");
     ks->x = X;
     ks->mu = M;
     ks->d = d;
@@ -673,33 +699,34 @@ class Executor {
       cur = cur->a[2];
     }
     int64_t z;
-    if (!is_const_int(cur, &z) || z != 0 || levels.empty()) return false;
+    if (!is_const_int(cur, &z) || z != 0 || levels.empty()) MISS("match_argmin#1");
     const int64_t k = static_cast<int64_t>(levels.size());
     SEP best_prev;  // best_c
     for (int64_t c = 0; c < k; ++c) {
       const SEP& lv = levels[k - 1 - c];
       int64_t cv;
-      if (!is_const_int(lv->a[1], &cv) || cv != c) return false;
+      if (!is_const_int(lv->a[1], &cv) || cv != c) MISS("match_argmin#2");
       const SEP& lt = lv->a[0];
-      if (lt->k != SE::Bin || lt->op != "Lt") return false;
+      if (lt->k != SE::Bin || lt->op != "Lt") MISS("match_argmin#3");
       const SEP& D = lt->a[0];
       const SEP& B = lt->a[1];
       if (c == 0) {
         double bd;
-        if (!is_const_dbl(B, &bd) || bd != 1e300) return false;
-      } else if (B != best_prev) {
-        return false;
+        if (!is_const_dbl(B, &bd) || bd != 1e300) MISS("match_argmin#4");
+      } else if (!same_se(B, best_prev)) {
+        MISS("match_argmin#5");
       }
-      if (!match_distance(D, c, ks)) return false;
+      if (!match_distance(D, c, ks)) MISS("match_argmin#6");
       // best_{c+1}: the Sel(lt, D, best_c) that the next level compares against
       auto nb = mk(SE::Sel, Ty::Double);
       nb->a = {lt, D, B};
       best_prev = nullptr;
       if (c + 1 < k) {
         const SEP& nlt = levels[k - 2 - c]->a[0];
-        if (nlt->k != SE::Bin || nlt->op != "Lt") return false;
+        if (nlt->k != SE::Bin || nlt->op != "Lt") MISS("match_argmin#7");
         const SEP& nB = nlt->a[1];
-        if (nB->k != SE::Sel || nB->a[0] != lt || nB->a[1] != D || nB->a[2] != B) return false;
+        if (nB->k != SE::Sel || !same_se(nB->a[0], lt) || !same_se(nB->a[1], D) || !same_se(nB->a[2], B))
+          MISS("match_argmin#8");
         best_prev = nB;
       }
     }
@@ -711,13 +738,13 @@ class Executor {
     int ci = -1;
     for (size_t q = 0; q < els.size(); ++q)
       if (els[q].e->kind == "collect") {
-        if (ci >= 0) return false;
+        if (ci >= 0) MISS("try_kmeans#1");
         ci = static_cast<int>(q);
       }
-    if (ci < 0 || els[ci].cond || els[ci].e->append) return false;
+    if (ci < 0 || els[ci].cond || els[ci].e->append) MISS("try_kmeans#2");
     KmeansShape ks;
-    if (!match_argmin(els[ci].value, &ks)) return false;
-    if (n * ks.d > ks.x->n || ks.k * ks.d > ks.mu->n) return false;
+    if (!match_argmin(els[ci].value, &ks)) MISS("try_kmeans#3");
+    if (n * ks.d > ks.x->n || ks.k * ks.d > ks.mu->n) MISS("try_kmeans#4");
     const SEP key = els[ci].value;
     // reduce elems: cond Eq(key, c); value 1 (count) or Load(X, d*Idx + j) (sum)
     struct Slot { int kind; int64_t c, j; };
@@ -725,30 +752,36 @@ class Executor {
     for (size_t q = 0; q < els.size(); ++q) {
       if (static_cast<int>(q) == ci) continue;
       const LElem& le = els[q];
-      if (le.e->kind != "reduce" || !le.cond || !is_plus_combine(le.combine)) return false;
+      if (le.e->kind != "reduce" || !le.cond || !is_plus_combine(le.combine)) MISS("try_kmeans#5");
       const SEP& cd = le.cond;
-      if (cd->k != SE::Bin || cd->op != "Eq") return false;
+      if (cd->k != SE::Bin || cd->op != "Eq") MISS("try_kmeans#6");
       int64_t c;
       if (cd->a[0] == key && is_const_int(cd->a[1], &c)) {
       } else if (cd->a[1] == key && is_const_int(cd->a[0], &c)) {
       } else {
-        return false;
+        MISS("try_kmeans#7");
       }
-      if (c < 0 || c >= ks.k) return false;
+      if (c < 0 || c >= ks.k) MISS("try_kmeans#8");
       int64_t one;
       if (is_const_int(le.value, &one) && one == 1 && le.e->zero.k == Atom::Int && le.e->zero.i == 0) {
         slots[q] = {0, c, 0};
       } else if (le.value->k == SE::Load && le.value->a[0]->vec == ks.x && le.e->zero.k == Atom::Double &&
                  le.e->zero.d == 0.0) {
         auto af = affine(le.value->a[1]);
-        if (!af || af->a != ks.d || af->b != 0 || af->c < 0 || af->c >= ks.d) return false;
+        if (!af || af->a != ks.d || af->b != 0 || af->c < 0 || af->c >= ks.d) MISS("try_kmeans#9");
         slots[q] = {1, c, af->c};
       } else {
-        return false;
+        MISS("try_kmeans#10");
       }
     }
     // launch the fused multiloop kernel
     const int d = static_cast<int>(ks.d), k = static_cast<int>(ks.k);
+    rep["family"] = "kmeans";
+    rep["n"] = n;
+    rep["d"] = d;
+    rep["k"] = k;
+    rep["launch"] = "dlx_kmeans_step";
+    if (g_dry) return dry_bind(els), true;
     void* ws = nullptr;
     const size_t wsb = dlx_kmeans_workspace_bytes(n, d, k);
     ckc(cudaMalloc(&ws, wsb), "cudaMalloc ws");
@@ -813,6 +846,11 @@ class Executor {
       nb = std::max(nb, b + 1);
     }
     if (!keys || n > keys->n || nb > (1 << 24)) return false;
+    rep["family"] = "groupby";
+    rep["n"] = n;
+    rep["buckets"] = nb;
+    rep["launch"] = "dlx_groupby_count";
+    if (g_dry) return dry_bind(els), true;
     void* ws = nullptr;
     int64_t* counts = nullptr;
     const size_t wsb = dlx_groupby_workspace_bytes(n, nb);
@@ -898,6 +936,11 @@ class Executor {
       cell[q] = {a, b};
     }
     if (X->elem != Ty::Double || Y->elem != Ty::Int || n * d > X->n || n > Y->n) return false;
+    rep["family"] = "gda_scatter";
+    rep["n"] = n;
+    rep["d"] = d;
+    rep["launch"] = "dlx_gda_pass2";
+    if (g_dry) return dry_bind(els), true;
     double *dm0 = nullptr, *dm1 = nullptr, *S = nullptr;
     void* ws = nullptr;
     const size_t wsb = dlx_gda_workspace_bytes(n, static_cast<int32_t>(d));
@@ -1077,6 +1120,12 @@ class Executor {
       L.vec_len[q] = B.vecs[q]->n;
       L.vec_kind[q] = vm_ty(B.vecs[q]->elem);
     }
+    rep["family"] = "generic";
+    rep["n"] = n;
+    rep["elems"] = static_cast<int>(els.size());
+    rep["instructions"] = static_cast<int>(B.code.size());
+    rep["launch"] = "dlx_vm_run_loop";
+    if (g_dry) return dry_bind(els), true;
     dlx_vm_instr* dcode = nullptr;
     int64_t* dres = nullptr;
     int* dtrap = nullptr;
@@ -1129,10 +1178,20 @@ class Executor {
     return true;
   }
 
+  void dry_bind(const std::vector<LElem>& els) {
+    for (const LElem& le : els) {
+      if (le.e->kind == "collect") env_[le.e->out] = Val{new_vec(dry_n_, le.e->out_ty.elem, st_, false)};
+      else if (le.e->out_ty.t == Ty::Double) env_[le.e->out] = Val{1.0};
+      else if (le.e->out_ty.t == Ty::Bool) env_[le.e->out] = Val{false};
+      else env_[le.e->out] = Val{int64_t{1}};
+    }
+  }
+
   // ---- one root ParallelLoop -------------------------------------------------------------------
   Val run_loop(const Stmt& s) {
     const Loop& L = *s.loop;
     const int64_t n = atom(L.range).i();
+    dry_n_ = n;
     loop_index_ = L.index;
     sym_.clear();
     sym_block(L.body);
@@ -1175,28 +1234,34 @@ class Executor {
 }  // namespace
 
 RunResult run_program(const std::string& program_json, uint64_t seed, int device) {
-  cudaError_t e = cudaSetDevice(device);
-  if (e != cudaSuccess) throw std::runtime_error(std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  g_dry = getenv("DLX_PROGRAM_DRYRUN") != nullptr;
+  g_debug = getenv("DLX_PROGRAM_DEBUG") != nullptr;
   Program p = parse_program(program_json);
-  cudaStream_t st;
-  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
-    throw std::runtime_error("cudaStreamCreate failed");
+  cudaStream_t st = nullptr;
+  if (!g_dry) {
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
+      throw std::runtime_error("cudaStreamCreate failed");
+  }
   RunResult r;
   try {
     Executor ex(p, seed, st);
     Val v = ex.run();
-    cudaStreamSynchronize(st);
+    if (!g_dry) cudaStreamSynchronize(st);
     r.output = ex.output;
     r.result = format_val(v);
     r.report = ex.report.dump();
   } catch (const Fail& f) {
-    cudaStreamSynchronize(st);
-    cudaStreamDestroy(st);
+    if (!g_dry) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
     if (f.code == DLX_ERR_GENERATION) throw GenerationFailed(f.what());
     if (f.code == DLX_ERR_TRAP) throw TrapError(f.what());
     throw std::runtime_error(f.what());
   }
-  cudaStreamDestroy(st);
+  if (!g_dry) cudaStreamDestroy(st);
   return r;
 }
 

@@ -130,3 +130,24 @@ def test_unlowerable_loop_fails_loudly():
             break
     with pytest.raises(GenerationFailed):
         run_program(prog, seed=1)
+
+
+EXPECTED_FAMILIES = {
+    "axpy_n100000": ["generic", "generic"],
+    "count_gt_n100000": ["generic"],
+    "gda_n20000_d4": ["generic", "gda_scatter"],
+    "groupby_n100000_k16": ["groupby"],
+    "kmeans_n4096_d16_k8_it2": ["kmeans", "kmeans"],
+    "kmeans_n65536_d16_k8_it1": ["kmeans"],
+    "mean_variance_n100000": ["generic"],
+}
+
+
+@pytest.mark.parametrize("name", sorted(EXPECTED_FAMILIES))
+def test_lowering_families_dry_run(name, monkeypatch):
+    """CPU: parse + symbolically evaluate + match every loop of the reference-staged program
+    (DLX_PROGRAM_DRYRUN: no device memory, no launches) and check the lowering chosen."""
+    from paper_1109_0778_b200.program import run_program
+    monkeypatch.setenv("DLX_PROGRAM_DRYRUN", "1")
+    _, report = run_program(load(name)["program"], seed=1)
+    assert [r["family"] for r in report] == EXPECTED_FAMILIES[name]
