@@ -361,9 +361,10 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     long long* my_pidx = pend_idx + static_cast<size_t>(blockIdx.x) * pend_cap;
     unsigned long long* my_pmask = pend_mask + static_cast<size_t>(blockIdx.x) * pend_cap;
     long long pending = 0;
-    // fold ownership: warp ew owns centroids ew + 8u (u = 0..7), lane owns columns 2l, 2l+1
-    const int jc = 2 * lane;
-    const int uu = lane >> 2, Qq = lane & 3;  // this lane's (owned centroid, quarter) mask slot
+    // fold ownership: warp ew owns centroids ew + 8u (u = 0..7); lane (uu, g) = (lane >> 2,
+    // lane & 3) owns centroid ew + 8uu, columns 16g .. 16g+15 (8 pairs, rotated by `rot`)
+    const int uu = lane >> 2, Qq = lane & 3;  // also: this lane's (owned centroid, quarter) mask slot
+    const int rot = (2 * (lane & 3) + uu) & 7;
     double acc[8][2];
     long long cnt_lane = 0;                   // samples of (centroid ew + 8uu, quarter Qq)
 #pragma unroll
@@ -471,9 +472,11 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         pending += p0 + p1 + p2 + S.pcount[3];
       }
       TR(3);
-      // ---- bucket-reduce.  Lane (uu, Qq) expands its mask into the warp's per-centroid row
-      // list (rows ascending: quarter-major, then lane), then every owned centroid folds up
-      // to four rows with independent loads before its adds (ILP across centroids).
+      // ---- bucket-reduce.  Lane (uu, Qq) expands its quarter mask into the warp's row list for
+      // owned centroid uu (rows ascending: quarter-major, then lane).  Then, round by round,
+      // the four lanes of centroid uu fold that centroid's t-th row: lane (uu, g) owns columns
+      // 16g .. 16g+15 as 8 column pairs, visited in the lane-rotated order (i + rot) % 8 so the
+      // 32 lanes of one LDS.128 spread over all banks; acc[i] always holds pair (i + rot) % 8.
       {
         const unsigned gmv = S.gm[Qq][ew + 8 * uu];
         const int pc = __popc(gmv);
@@ -493,51 +496,42 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
           if (slot < kListCap) S.list[ew][uu][slot] = static_cast<unsigned char>(32 * Qq + l);
           ++slot;
         }
-        const int tot = __shfl_sync(0xffffffffu, incl, lane | 3);  // samples of centroid uu
+        const int nu = __shfl_sync(0xffffffffu, incl, lane | 3);  // rows of my centroid uu
+        const int rounds = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(nu)));
         __syncwarp();
-        int nu[8];
+        const int g = lane & 3;
+        const int lim = min(rounds, kListCap);
+        for (int t4 = 0; t4 < lim; ++t4) {
+          if (t4 < nu) {
+            const double* xr = xs + S.list[ew][uu][t4] * d + 16 * g;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) nu[u] = __shfl_sync(0xffffffffu, tot, 4 * u);
-        if (jc < d) {
-#pragma unroll
-          for (int u0 = 0; u0 < 8; u0 += 2) {
-            double2 v[2][4];
-#pragma unroll
-            for (int e = 0; e < 2; ++e)
-#pragma unroll
-              for (int t4 = 0; t4 < 4; ++t4)
-                v[e][t4] = t4 < nu[u0 + e]
-                               ? *reinterpret_cast<const double2*>(xs + S.list[ew][u0 + e][t4] * d + jc)
-                               : make_double2(0.0, 0.0);
-#pragma unroll
-            for (int e = 0; e < 2; ++e)
-#pragma unroll
-              for (int t4 = 0; t4 < 4; ++t4)
-                if (t4 < nu[u0 + e]) {
-                  acc[u0 + e][0] += v[e][t4].x;
-                  acc[u0 + e][1] += v[e][t4].y;
-                }
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            if (nu[u] <= 4) continue;
-            if (nu[u] <= kListCap) {
-              for (int t4 = 4; t4 < nu[u]; ++t4) {
-                const double2 w = *reinterpret_cast<const double2*>(xs + S.list[ew][u][t4] * d + jc);
-                acc[u][0] += w.x;
-                acc[u][1] += w.y;
+            for (int i = 0; i < 8; ++i) {
+              const int pr = (i + rot) & 7;
+              if (16 * g + 2 * pr < d) {
+                const double2 w = *reinterpret_cast<const double2*>(xr + 2 * pr);
+                acc[i][0] += w.x;
+                acc[i][1] += w.y;
               }
-            } else {  // crowded centroid: walk the quarter masks directly (same row order)
-              int seen = 0;
-              for (int Qr = 0; Qr < 4; ++Qr) {
-                unsigned g = S.gm[Qr][ew + 8 * u];
-                while (g) {
-                  const int row = 32 * Qr + __ffs(g) - 1;
-                  g &= g - 1;
-                  if (seen++ < 4) continue;
-                  const double2 w = *reinterpret_cast<const double2*>(xs + row * d + jc);
-                  acc[u][0] += w.x;
-                  acc[u][1] += w.y;
+            }
+          }
+        }
+        if (rounds > kListCap) {  // crowded centroid: walk the quarter masks directly (same order)
+          const int c = ew + 8 * uu;
+          int seen = 0;
+          for (int Qr = 0; Qr < 4; ++Qr) {
+            unsigned gg = S.gm[Qr][c];
+            while (gg) {
+              const int row = 32 * Qr + __ffs(gg) - 1;
+              gg &= gg - 1;
+              if (seen++ < kListCap) continue;
+              const double* xr = xs + row * d + 16 * g;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int pr = (i + rot) & 7;
+                if (16 * g + 2 * pr < d) {
+                  const double2 w = *reinterpret_cast<const double2*>(xr + 2 * pr);
+                  acc[i][0] += w.x;
+                  acc[i][1] += w.y;
                 }
               }
             }
@@ -549,13 +543,16 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       if (lane == 0) mbar_arrive(&S.sempty[s]);
     }
     // flush this CTA's partial activation record
-    double* ps = part_sums + static_cast<size_t>(blockIdx.x) * k * d;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int c = ew + 8 * u;
+    {
+      const int c = ew + 8 * uu, g = lane & 3;
+      double* ps = part_sums + static_cast<size_t>(blockIdx.x) * k * d;
       if (c < k) {
-        if (jc < d) ps[c * d + jc] = acc[u][0];
-        if (jc + 1 < d) ps[c * d + jc + 1] = acc[u][1];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int col = 16 * g + 2 * ((i + rot) & 7);
+          if (col < d) ps[c * d + col] = acc[i][0];
+          if (col + 1 < d) ps[c * d + col + 1] = acc[i][1];
+        }
       }
     }
     long long ct = cnt_lane;  // sum the four quarter lanes of each owned centroid
