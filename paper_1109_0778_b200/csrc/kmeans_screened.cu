@@ -65,13 +65,15 @@ namespace sk {
 
 using namespace sm100;
 
-constexpr int kThreads = 448;
+constexpr int kThreads = 512;
 constexpr int kTile = 112;        // samples per tile (the MMA runs M=128; rows 112..127 are zero)
 constexpr int kMmaM = 128;
 constexpr int kStages = 3;
 constexpr int kMaxD = 64;
 constexpr int kMaxK = 64;
-constexpr int kWarpProd = 0, kWarpMma = 1, kWarpC0 = 2, kWarpE0 = 6;
+// warp roles: 0 = TMA producer; 1 = TMEM owner + MMA issuer; 2-7 converters; 8-11 epilogue
+// (TMEM lane quarters 0-3); 12-15 fold
+constexpr int kWarpProd = 0, kWarpMma = 1, kWarpC0 = 2, kNumC = 6, kWarpE0 = 8, kWarpR0 = 12;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kAccCols = 256;                        // 4 accumulators x 64 columns
 constexpr uint32_t kXStage = kTile * kMaxD * 8;           // 56 KiB
@@ -84,10 +86,10 @@ static_assert(kOffA1 % 1024 == 0 && kOffB1 % 1024 == 0 && kOffA2 % 512 == 0 && k
               "UMMA operand alignment");
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: x + kMagic rounds x to an integer
 
-constexpr int kListCap = 16;  // fold list slots per (warp, owned centroid) per tile
+constexpr int kListCap = 16;  // fold list slots per owned centroid per tile
 
 struct Misc {
-  uint64_t full[kStages], sempty[kStages], cfull[kStages];
+  uint64_t full[kStages], sempty[kStages], cfull[kStages], efull[kStages];
   uint64_t a_full, a_empty, tfull[2], tempty[2];
   unsigned long long valid;
   uint32_t tmem_base;
@@ -95,12 +97,10 @@ struct Misc {
   uint32_t mu_maxhi;
   alignas(16) int nm0[kMaxK];             // floor(|mu_c|^2 / U), U = 2^(e_t + e_m - 20), e_t = e_m + 1
   double nmf[kMaxK];
-  int hmin[2][kMmaM];
-  uint32_t cmask[2][kMmaM];
   unsigned char rowflag[kStages][kMmaM];  // sample needs the exact chain (|x| >= 2^e_t, inf, NaN)
-  int pcount[4];
-  uint32_t gm[4][kMaxK];                  // per quarter: lanes (rows) of the tile assigned to c
-  unsigned char list[8][8][kListCap];     // per fold warp, per owned centroid: rows, ascending
+  int pcount[2][4];
+  uint32_t gm[kStages][4][kMaxK];         // per stage, per quarter: rows of the tile resolved to c
+  unsigned char list[4][16][kListCap];    // per fold warp, per owned centroid: rows, ascending
 };
 constexpr uint32_t kSmemBytes = kOffMisc + sizeof(Misc);
 static_assert(kSmemBytes <= 232448, "shared-memory plan exceeds 227 KiB");
@@ -158,14 +158,15 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&S.full[s], 1);
-      mbar_init(&S.sempty[s], 8);
-      mbar_init(&S.cfull[s], 4);
+      mbar_init(&S.sempty[s], 4);
+      mbar_init(&S.cfull[s], kNumC);
+      mbar_init(&S.efull[s], 4);
     }
-    mbar_init(&S.a_full, 4);
+    mbar_init(&S.a_full, kNumC);
     mbar_init(&S.a_empty, 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&S.tfull[b], 1);
-      mbar_init(&S.tempty[b], 8);
+      mbar_init(&S.tempty[b], 4);
     }
     S.valid = 0;
     S.yabs = 0;
@@ -289,17 +290,14 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         mma_commit(&S.tfull[b]);
       }
     }
-  } else if (warp >= kWarpC0 && warp < kWarpE0) {
-    // ======================= converters (128 threads) =======================
-    const int ct = tid - kWarpC0 * 32;
-    const int cw = ct >> 5;
+  } else if (warp >= kWarpC0 && warp < kWarpC0 + kNumC) {
+    // ======================= converters (6 warps) =======================
+    const int cw = warp - kWarpC0;
     const int em = S.em, disabled = S.disabled;
     const double scale = disabled ? 0.0 : ldexp(1.0, 21 - em);   // 2^(22 - e_t), e_t = e_m + 1
     const uint32_t hw_limit = static_cast<uint32_t>(1023 + em + 1) << 20;  // |x| >= 2^e_t
     const int half = lane >> 4, j0 = 4 * (lane & 15);
-    const int key = cw + 4 * half;  // row & 7 of every row this thread converts
-    const uint32_t off_h = sw128_offset(key, j0), off_l = sw128_offset(key, 64 + j0);
-    const uint32_t off_f = sw64_offset(key, j0);
+    const bool colok = j0 < d, col2ok = j0 + 2 < d;
     for (int m = 0; m < mtiles; ++m) {
       const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
       const int s = m % kStages;
@@ -308,20 +306,16 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       mbar_wait(&S.full[s], (m / kStages) & 1);
       TR(0);
       const double* xs = reinterpret_cast<const double*>(smem + s * kXStage);
-      TR(1);
       if (m >= 1) mbar_wait(&S.a_empty, (m - 1) & 1);
       TR(2);
-      // Y = rint(x * 2^(22-e_t)) with e_t = e_m + 1 fixed per launch.  Thread (cw, half,
-      // lane16) converts columns 4*lane16 .. +3 of rows q = 8*mm + key, key = cw + 4*half
-      // (mm = 0..15), so its swizzle key is fixed and its operand offsets advance by a
-      // constant per row.  A row with |x| >= 2^e_t, inf or NaN is flagged (exact chain).
-      const double* xrow = xs + key * d + j0;
-      const bool colok = j0 < d, col2ok = j0 + 2 < d;
-#pragma unroll 4
-      for (int mm = 0; mm < kMmaM / 8; ++mm) {
-        const int q = 8 * mm + key;
+      // Y = rint(x * 2^(22-e_t)) with e_t = e_m + 1 fixed per launch; row pairs (2p, 2p+1),
+      // p = cw, cw + 6, ...; lane (half, lane16) converts columns 4*lane16 .. +3 of row 2p+half.
+      // A row with |x| >= 2^e_t, inf or NaN is flagged (exact chain).
+#pragma unroll 2
+      for (int pp = cw; pp < kMmaM / 2; pp += kNumC) {
+        const int q = 2 * pp + half;
         const bool ok = q < rows && colok;
-        const double* src = ok ? xrow + mm * 8 * d : xs;
+        const double* src = ok ? xs + q * d + j0 : xs;
         const double2 v0 = *reinterpret_cast<const double2*>(src);
         const double2 v1 = (ok && col2ok) ? *reinterpret_cast<const double2*>(src + 2) : make_double2(0.0, 0.0);
         const double a0 = ok ? v0.x : 0.0, a1 = ok ? v0.y : 0.0;
@@ -337,9 +331,10 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         // bytes of Y (little endian): b0 = F, b1 = l, b2 = h (low byte of Y >> 16)
         const uint32_t p01 = __byte_perm(Y0, Y1, 0x6240), p23 = __byte_perm(Y2, Y3, 0x6240);
         const uint32_t q01 = __byte_perm(Y0, Y1, 0x0051), q23 = __byte_perm(Y2, Y3, 0x0051);
-        *reinterpret_cast<uint32_t*>(A1 + off_h + mm * 1024) = __byte_perm(p01, p23, 0x7632);  // h
-        *reinterpret_cast<uint32_t*>(A1 + off_l + mm * 1024) = __byte_perm(q01, q23, 0x5410);  // l
-        *reinterpret_cast<uint32_t*>(A2 + off_f + mm * 512) = __byte_perm(p01, p23, 0x5410);   // F
+        const uint32_t oh = sw128_offset(q, j0);
+        *reinterpret_cast<uint32_t*>(A1 + oh) = __byte_perm(p01, p23, 0x7632);                 // h
+        *reinterpret_cast<uint32_t*>(A1 + (oh ^ 64u)) = __byte_perm(q01, q23, 0x5410);         // l
+        *reinterpret_cast<uint32_t*>(A2 + sw64_offset(q, j0)) = __byte_perm(p01, p23, 0x5410);  // F
       }
       TR(3);
       fence_proxy_async_smem();
@@ -349,190 +344,174 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         mbar_arrive(&S.cfull[s]);
       }
     }
-  } else if (warp >= kWarpE0) {
-    // ======================= epilogue + bucket-reduce (256 threads) =======================
-    const int ew = warp - kWarpE0;          // 0..7
-    const int quarter = warp & 3;           // TMEM lane quarter this warp may access
-    const int h = ew >> 2;                  // centroid half
-    const int q = quarter * 32 + lane;      // sample row within the tile (M row)
+  } else if (warp >= kWarpE0 && warp < kWarpR0) {
+    // ======================= epilogue: screen + decide (4 warps, one per lane quarter) ===========
+    const int quarter = warp & 3;
+    const int q = quarter * 32 + lane;  // sample row within the tile (M row)
     const unsigned long long kmask = k == 64 ? ~0ull : ((1ull << k) - 1);
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
     const int window = S.window;
     long long* my_pidx = pend_idx + static_cast<size_t>(blockIdx.x) * pend_cap;
     unsigned long long* my_pmask = pend_mask + static_cast<size_t>(blockIdx.x) * pend_cap;
     long long pending = 0;
-    // fold ownership: warp ew owns centroids ew + 8u (u = 0..7); lane (uu, g) = (lane >> 2,
-    // lane & 3) owns centroid ew + 8uu, columns 16g .. 16g+15 (8 pairs, rotated by `rot`)
-    const int uu = lane >> 2, Qq = lane & 3;  // also: this lane's (owned centroid, quarter) mask slot
-    const int rot = (2 * (lane & 3) + uu) & 7;
-    double acc[8][2];
-    long long cnt_lane = 0;                   // samples of (centroid ew + 8uu, quarter Qq)
-#pragma unroll
-    for (int u = 0; u < 8; ++u) acc[u][0] = acc[u][1] = 0.0;
-    const int4* nm4 = reinterpret_cast<const int4*>(&S.nm0[32 * h]);
+    const int4* nm4 = reinterpret_cast<const int4*>(S.nm0);
     for (int m = 0; m < mtiles; ++m) {
       const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
       const int s = m % kStages, b = m & 1;
       const int rows = static_cast<int>(n - t * kTile < kTile ? n - t * kTile : kTile);
       TR(6);
       mbar_wait(&S.cfull[s], (m / kStages) & 1);
-      mbar_wait(&S.full[s], (m / kStages) & 1);
       TR(0);
-      const double* xs = reinterpret_cast<const double*>(smem + s * kXStage);
       mbar_wait(&S.tfull[b], (m >> 1) & 1);
       TR(1);
       tc_fence_after();
-      int tv[32];
+      int tv[64];
       int lmin = kInvalidNm;
 #pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {
-        const uint32_t col = b * kAccCols + 32 * h + 16 * ch;
-        int hh[16], cr[16], w1[16], w2[16];
-        tmem_ld16(tmem + lane_base + col, hh);
-        tmem_ld16(tmem + lane_base + col + 64, cr);
-        tmem_ld16(tmem + lane_base + col + 128, w1);
-        tmem_ld16(tmem + lane_base + col + 192, w2);
-        int nm[16];
-#pragma unroll
-        for (int u4 = 0; u4 < 4; ++u4) {
-          const int4 v4 = nm4[4 * ch + u4];
-          nm[4 * u4 + 0] = v4.x;
-          nm[4 * u4 + 1] = v4.y;
-          nm[4 * u4 + 2] = v4.z;
-          nm[4 * u4 + 3] = v4.w;
-        }
+      for (int ch = 0; ch < 8; ++ch) {
+        const uint32_t col = b * kAccCols + 8 * ch;
+        int hh[8], cr[8], w1[8], w2[8];
+        tmem_ld8(tmem + lane_base + col, hh);
+        tmem_ld8(tmem + lane_base + col + 64, cr);
+        tmem_ld8(tmem + lane_base + col + 128, w1);
+        tmem_ld8(tmem + lane_base + col + 192, w2);
+        const int4 n0 = nm4[2 * ch], n1 = nm4[2 * ch + 1];
+        const int nm[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
         tmem_ld_wait();
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
+        for (int u = 0; u < 8; ++u) {
           // invalid centroids: zero B rows (Q = 0) and nm = kInvalidNm
           const int Q = hh[u] * 256 + cr[u] + (w1[u] >> 8) + (w2[u] >> 16);
           const int v = nm[u] - 2 * Q;
-          tv[16 * ch + u] = v;
+          tv[8 * ch + u] = v;
           lmin = min(lmin, v);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.tempty[b]);
-      S.hmin[h][q] = lmin;
       TR(2);
-      named_bar(1, 256);
-      uint32_t mask = 0;
-      {
-        const int tmin = min(S.hmin[0][q], S.hmin[1][q]);
-        if (tmin < kNoCandidate) {
-          const int thr = tmin + window;
-#pragma unroll
-          for (int u = 0; u < 32; ++u)
-            if (tv[u] <= thr) mask |= 1u << u;
-        }
-      }
-      S.cmask[h][q] = mask;
-      named_bar(1, 256);
       unsigned long long full = 0;
       bool pend = false;
-      if (h == 0) {
-        int a = -1;
-        if (q < rows) {
-          if (S.rowflag[s][q]) {
-            full = kmask;  // |x| out of the screen's range, inf or NaN: the exact chain over all c
-            pend = true;
+      int a = -1;
+      if (q < rows) {
+        if (S.rowflag[s][q]) {
+          full = kmask;  // |x| out of the screen's range, inf or NaN: the exact chain over all c
+          pend = true;
+        } else if (lmin < kNoCandidate) {
+          const int thr = lmin + window;
+#pragma unroll
+          for (int u = 0; u < 64; ++u)
+            if (tv[u] <= thr) full |= 1ull << u;
+          if ((full & (full - 1)) == 0) {
+            a = __ffsll(static_cast<long long>(full)) - 1;
           } else {
-            full = static_cast<unsigned long long>(S.cmask[0][q]) |
-                   (static_cast<unsigned long long>(S.cmask[1][q]) << 32);
-            if (full == 0) {
-              a = 0;  // no finite centroid: the chain keeps its start index
-            } else if ((full & (full - 1)) == 0) {
-              a = __ffsll(static_cast<long long>(full)) - 1;
-            } else {
-              pend = true;  // several survivors: resolved by the exact chain (resolve kernel)
+            pend = true;  // several survivors: resolved by the exact chain (resolve kernel)
+          }
+        } else {
+          a = 0;  // no finite centroid: the chain keeps its start index
+        }
+        if (a >= 0 && assign) assign[t * kTile + q] = a;
+      }
+      // group masks for the fold: gm[s][quarter][c] = this quarter's rows resolved to c
+      const unsigned grp = __match_any_sync(0xffffffffu, a);
+      S.gm[s][quarter][lane] = 0u;
+      S.gm[s][quarter][lane + 32] = 0u;
+      __syncwarp();
+      if ((grp & ((1u << lane) - 1)) == 0 && a >= 0) S.gm[s][quarter][a] = grp;
+      // deterministic pending-list append, ordered by sample row
+      const unsigned pb = __ballot_sync(0xffffffffu, pend);
+      if (lane == 0) S.pcount[m & 1][quarter] = __popc(pb);
+      named_bar(1, 128);
+      const int p0 = S.pcount[m & 1][0], p1 = S.pcount[m & 1][1], p2 = S.pcount[m & 1][2];
+      if (pend) {
+        const int before = (quarter > 0 ? p0 : 0) + (quarter > 1 ? p1 : 0) + (quarter > 2 ? p2 : 0);
+        const long long slot = pending + before + __popc(pb & ((1u << lane) - 1));
+        my_pidx[slot] = t * kTile + q;
+        my_pmask[slot] = full;
+      }
+      pending += p0 + p1 + p2 + S.pcount[m & 1][3];
+      TR(3);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.efull[s]);
+    }
+    if (quarter == 0 && lane == 0) pend_count[blockIdx.x] = pending;
+  } else {
+    // ======================= fold: bucket-reduce (4 warps) =======================
+    // Warp rw owns centroids rw + 4u (u = 0..15); lane (u, g) = (lane >> 1, lane & 1) owns
+    // columns 32g .. 32g+31 of centroid rw + 4u as 16 pairs visited in the rotated order
+    // (i + u) % 16, so one LDS.128 of the warp spreads over all banks; acc[i] holds pair
+    // (i + u) % 16.  Rows are folded in ascending order: deterministic, no atomics.
+    const int rw = warp - kWarpR0;
+    const int u = lane >> 1, g = lane & 1;
+    const int c = rw + 4 * u;
+    double acc[16][2];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = 0.0;
+    long long cnt_lane = 0;  // rows of centroid c in quarters 2g, 2g+1
+    for (int m = 0; m < mtiles; ++m) {
+      const int s = m % kStages;
+      TR(6);
+      mbar_wait(&S.efull[s], (m / kStages) & 1);
+      mbar_wait(&S.full[s], (m / kStages) & 1);
+      TR(0);
+      const double* xs = reinterpret_cast<const double*>(smem + s * kXStage);
+      // row list of centroid c: quarters 0,1 (lane 2u) then 2,3 (lane 2u+1), lanes ascending
+      const unsigned ma = S.gm[s][2 * g][c], mb = S.gm[s][2 * g + 1][c];
+      const int pc = __popc(ma) + __popc(mb);
+      cnt_lane += pc;
+      const int up = __shfl_up_sync(0xffffffffu, pc, 1), dn = __shfl_down_sync(0xffffffffu, pc, 1);
+      const int before = g ? up : 0;          // rows of quarters 0,1 precede quarters 2,3
+      const int nu = g ? up + pc : pc + dn;   // rows of centroid c this tile
+      int slot = before;
+      unsigned mm = ma;
+      while (mm) {
+        const int l = __ffs(mm) - 1;
+        mm &= mm - 1;
+        if (slot < kListCap) S.list[rw][u][slot] = static_cast<unsigned char>(64 * g + l);
+        ++slot;
+      }
+      mm = mb;
+      while (mm) {
+        const int l = __ffs(mm) - 1;
+        mm &= mm - 1;
+        if (slot < kListCap) S.list[rw][u][slot] = static_cast<unsigned char>(64 * g + 32 + l);
+        ++slot;
+      }
+      const int rounds = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(nu)));
+      __syncwarp();
+      TR(1);
+      const int lim = min(rounds, kListCap);
+      for (int t4 = 0; t4 < lim; ++t4) {
+        if (t4 < nu) {
+          const double* xr = xs + S.list[rw][u][t4] * d + 32 * g;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int pr = (i + u) & 15;
+            if (32 * g + 2 * pr < d) {
+              const double2 w = *reinterpret_cast<const double2*>(xr + 2 * pr);
+              acc[i][0] += w.x;
+              acc[i][1] += w.y;
             }
           }
-          if (a >= 0 && assign) assign[t * kTile + q] = a;
         }
-        // group masks: gm[quarter][c] = this quarter's rows resolved to centroid c
-        const unsigned grp = __match_any_sync(0xffffffffu, a);
-        S.gm[quarter][lane] = 0u;
-        S.gm[quarter][lane + 32] = 0u;
-        __syncwarp();
-        if ((grp & ((1u << lane) - 1)) == 0 && a >= 0) S.gm[quarter][a] = grp;
       }
-      const unsigned pb = __ballot_sync(0xffffffffu, pend);
-      if (h == 0 && lane == 0) S.pcount[quarter] = __popc(pb);
-      named_bar(1, 256);
-      {
-        // deterministic pending-list append, ordered by sample row
-        const int p0 = S.pcount[0], p1 = S.pcount[1], p2 = S.pcount[2];
-        if (pend) {
-          const int before = (quarter > 0 ? p0 : 0) + (quarter > 1 ? p1 : 0) + (quarter > 2 ? p2 : 0);
-          const long long slot = pending + before + __popc(pb & ((1u << lane) - 1));
-          my_pidx[slot] = t * kTile + q;
-          my_pmask[slot] = full;
-        }
-        pending += p0 + p1 + p2 + S.pcount[3];
-      }
-      TR(3);
-      // ---- bucket-reduce.  Lane (uu, Qq) expands its quarter mask into the warp's row list for
-      // owned centroid uu (rows ascending: quarter-major, then lane).  Then, round by round,
-      // the four lanes of centroid uu fold that centroid's t-th row: lane (uu, g) owns columns
-      // 16g .. 16g+15 as 8 column pairs, visited in the lane-rotated order (i + rot) % 8 so the
-      // 32 lanes of one LDS.128 spread over all banks; acc[i] always holds pair (i + rot) % 8.
-      {
-        const unsigned gmv = S.gm[Qq][ew + 8 * uu];
-        const int pc = __popc(gmv);
-        cnt_lane += pc;
-        int incl = pc;
-        {
-          int v = __shfl_up_sync(0xffffffffu, incl, 1);
-          if (Qq >= 1) incl += v;
-          v = __shfl_up_sync(0xffffffffu, incl, 2);
-          if (Qq >= 2) incl += v;
-        }
-        int slot = incl - pc;
-        unsigned mm = gmv;
-        while (mm) {
-          const int l = __ffs(mm) - 1;
-          mm &= mm - 1;
-          if (slot < kListCap) S.list[ew][uu][slot] = static_cast<unsigned char>(32 * Qq + l);
-          ++slot;
-        }
-        const int nu = __shfl_sync(0xffffffffu, incl, lane | 3);  // rows of my centroid uu
-        const int rounds = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(nu)));
-        __syncwarp();
-        const int g = lane & 3;
-        const int lim = min(rounds, kListCap);
-        for (int t4 = 0; t4 < lim; ++t4) {
-          if (t4 < nu) {
-            const double* xr = xs + S.list[ew][uu][t4] * d + 16 * g;
+      if (rounds > kListCap) {  // crowded centroid: walk the quarter masks directly (same order)
+        int seen = 0;
+        for (int Qr = 0; Qr < 4; ++Qr) {
+          unsigned gg = S.gm[s][Qr][c];
+          while (gg) {
+            const int row = 32 * Qr + __ffs(gg) - 1;
+            gg &= gg - 1;
+            if (seen++ < kListCap) continue;
+            const double* xr = xs + row * d + 32 * g;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int pr = (i + rot) & 7;
-              if (16 * g + 2 * pr < d) {
+            for (int i = 0; i < 16; ++i) {
+              const int pr = (i + u) & 15;
+              if (32 * g + 2 * pr < d) {
                 const double2 w = *reinterpret_cast<const double2*>(xr + 2 * pr);
                 acc[i][0] += w.x;
                 acc[i][1] += w.y;
-              }
-            }
-          }
-        }
-        if (rounds > kListCap) {  // crowded centroid: walk the quarter masks directly (same order)
-          const int c = ew + 8 * uu;
-          int seen = 0;
-          for (int Qr = 0; Qr < 4; ++Qr) {
-            unsigned gg = S.gm[Qr][c];
-            while (gg) {
-              const int row = 32 * Qr + __ffs(gg) - 1;
-              gg &= gg - 1;
-              if (seen++ < kListCap) continue;
-              const double* xr = xs + row * d + 16 * g;
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const int pr = (i + rot) & 7;
-                if (16 * g + 2 * pr < d) {
-                  const double2 w = *reinterpret_cast<const double2*>(xr + 2 * pr);
-                  acc[i][0] += w.x;
-                  acc[i][1] += w.y;
-                }
               }
             }
           }
@@ -543,28 +522,23 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       if (lane == 0) mbar_arrive(&S.sempty[s]);
     }
     // flush this CTA's partial activation record
-    {
-      const int c = ew + 8 * uu, g = lane & 3;
-      double* ps = part_sums + static_cast<size_t>(blockIdx.x) * k * d;
-      if (c < k) {
+    if (c < k) {
+      double* ps = part_sums + static_cast<size_t>(blockIdx.x) * k * d + static_cast<size_t>(c) * d;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int col = 16 * g + 2 * ((i + rot) & 7);
-          if (col < d) ps[c * d + col] = acc[i][0];
-          if (col + 1 < d) ps[c * d + col + 1] = acc[i][1];
-        }
+      for (int i = 0; i < 16; ++i) {
+        const int col = 32 * g + 2 * ((i + u) & 15);
+        if (col < d) ps[col] = acc[i][0];
+        if (col + 1 < d) ps[col + 1] = acc[i][1];
       }
     }
-    long long ct = cnt_lane;  // sum the four quarter lanes of each owned centroid
-    ct += __shfl_xor_sync(0xffffffffu, ct, 1);
-    ct += __shfl_xor_sync(0xffffffffu, ct, 2);
-    if (Qq == 0 && ew + 8 * uu < k) part_counts[static_cast<size_t>(blockIdx.x) * k + ew + 8 * uu] = ct;
-    if (ew == 0 && lane == 0) pend_count[blockIdx.x] = pending;
+    const long long ct = cnt_lane + __shfl_xor_sync(0xffffffffu, cnt_lane, 1);
+    if (g == 0 && c < k) part_counts[static_cast<size_t>(blockIdx.x) * k + c] = ct;
   }
 #ifdef DLX_KMEANS_TRACE
-  if (trace && lane == 0 && (warp == kWarpProd || warp == kWarpMma || warp == kWarpC0 || warp == kWarpE0)) {
-    const int role = warp == kWarpProd ? 0 : warp == kWarpMma ? 1 : warp == kWarpC0 ? 2 : 3;
-    for (int i = 0; i < 8; ++i) trace[(static_cast<size_t>(blockIdx.x) * 4 + role) * 8 + i] = tr[i];
+  if (trace && lane == 0 &&
+      (warp == kWarpProd || warp == kWarpMma || warp == kWarpC0 || warp == kWarpE0 || warp == kWarpR0)) {
+    const int role = warp == kWarpProd ? 0 : warp == kWarpMma ? 1 : warp == kWarpC0 ? 2 : warp == kWarpE0 ? 3 : 4;
+    for (int i = 0; i < 8; ++i) trace[(static_cast<size_t>(blockIdx.x) * 5 + role) * 8 + i] = tr[i];
   }
 #endif
 #undef TR
@@ -756,21 +730,21 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
                                 static_cast<int>(sk::kSmemBytes)));
   static const bool tracing = getenv("DLX_KMEANS_TRACE") != nullptr;
   long long* trace = nullptr;
-  if (tracing) DLX_CUDA(cudaMalloc(&trace, sizeof(long long) * grid * 32));
+  if (tracing) DLX_CUDA(cudaMalloc(&trace, sizeof(long long) * grid * 40));
   sk::kmeans_screened_kernel<<<grid, sk::kThreads, sk::kSmemBytes, stream>>>(
       x, n, d, k, mu, assign, w.part_counts, w.part_sums, w.pend_idx, w.pend_mask, w.pend_count, cap,
       trace);
   DLX_LAUNCHED("kmeans_screened_kernel");
   if (tracing) {  // debug only: per-role cycle split averaged over CTAs
-    std::vector<long long> h(static_cast<size_t>(grid) * 32);
+    std::vector<long long> h(static_cast<size_t>(grid) * 40);
     DLX_CUDA(cudaStreamSynchronize(stream));
     DLX_CUDA(cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
     cudaFree(trace);
-    const char* names[4] = {"producer", "mma", "convert", "epilogue"};
-    for (int r = 0; r < 4; ++r) {
+    const char* names[5] = {"producer", "mma", "convert", "epilogue", "fold"};
+    for (int r = 0; r < 5; ++r) {
       double avg[8] = {0};
       for (int b = 0; b < grid; ++b)
-        for (int i = 0; i < 8; ++i) avg[i] += static_cast<double>(h[(static_cast<size_t>(b) * 4 + r) * 8 + i]) / grid;
+        for (int i = 0; i < 8; ++i) avg[i] += static_cast<double>(h[(static_cast<size_t>(b) * 5 + r) * 8 + i]) / grid;
       fprintf(stderr, "[dlx trace] %-9s", names[r]);
       for (int i = 0; i < 8; ++i) fprintf(stderr, " %10.0f", avg[i]);
       fprintf(stderr, "\n");
