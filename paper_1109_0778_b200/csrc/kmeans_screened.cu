@@ -1,8 +1,8 @@
-// kmeans_screened.cu — the k-means fused multiloop with a tcgen05 int8 distance screen and an
-// exact fp64 recheck.  Assignments stay bit-identical to the reference argmin chain
+// kmeans_screened.cu — the k-means fused multiloop with a tcgen05 integer distance screen, an
+// exact fp64 recheck, and the bucket-reduce as an exact integer one-hot GEMM on the same
+// tensor cores.  Assignments stay bit-identical to the reference argmin chain
 // (proj/src/stage.cpp:73-104 staged_if chain over the inner mk_reduce distances,
-// loops.cpp:111-174), while the per-sample work drops from k*d fp64 (x-mu)^2 chains to one
-// small integer GEMM tile plus, for the rare near-ties, a few exact chains.
+// loops.cpp:111-174); per-centroid sums are exact fixed-point sums rounded once.
 //
 // Why a screen: the direct form costs 3*N*k*d fp64 ops (2.1e11 per C4 iteration, ~11 ms at
 // the FP64 pipe peak) against 1.34 ms of HBM time.  argmin_c (x-mu_c)^2 =
@@ -11,42 +11,54 @@
 // rigorously, and only re-evaluate the reference's own fp64 chain where the bound cannot
 // separate the best centroid from the others.
 //
-// Fixed point.  Per tile e_t with |x| < 2^e_t; per launch e_m with |mu| < 2^e_m over finite
-// centroids.  Y = rint(x * 2^(22-e_t)), |Y| <= 2^22, split Y = 65536 h + 256 l + F with h in
-// s8 and l, F in u8 (same for mu: Y' = 65536 h' + 256 l' + G).  tcgen05.mma kind::i8 computes
-// exact int32 accumulators
-//   HH = sum h h',  CR = sum (h l' + l h'),  W1 = sum (h G + F h' + l l'),  W2 = sum (l G + F l')
-// so sum Y Y' = 2^32 HH + 2^24 CR + 2^16 W1 + 2^8 W2 + sum F G  (the last term, in [0, d*255^2],
-// is dropped).  With x~ = Y + phi, mu~ = Y' + gamma, |phi|,|gamma| <= 1/2:
-//   sum x~ mu~ = sum Y Y' + E,  |E| <= (sum|Y| + sum|Y'|)/2 + d/4.
-// In units U = 2^(e_t+e_m-20), x.mu/U = sum x~ mu~ / 2^24 and Q = 256 HH + CR + (W1>>8) +
-// (W2>>16) satisfies x.mu/U in [Q - e, Q + 2.25 + e], e = ((sum|Y|+sum|Y'|)/2 + d/4)/2^24.
-// The screened score T_c = floor(|mu_c|^2/U) - 2 Q_c brackets |mu_c|^2/U - 2 x.mu_c/U within
-// [T_c - 4.5 - 2e, T_c + 1 + 2e], and the reference's fp64 chain differs from the real
-// distance by < 1 unit (guarded by -8 <= e_m - e_t <= 2, |e| <= 400).  So every centroid with
-//   T_c > min_c T_c + W,   W = 9 + ceil(4 e),   (sum|Y| <= d 2^22 per sample, sum|Y'| <= max_c)
-// has a strictly larger reference distance than some other centroid and cannot be the argmin.
-// One survivor => it IS the reference argmin.  Several survivors => the sample goes to the
-// pending list and is re-evaluated with the reference chain (sequential j, no FMA, strict <,
-// ascending c, start (1e300, 0)).  Tiles with non-finite values or out-of-range exponents
-// send every sample to the exact chain.  NaN / inf centroids never win the reference chain
+// Fixed point.  Per launch e_m with |mu| < 2^e_m over finite centroids and e_t = e_m + 1.
+// Each sample element becomes the 64-bit word
+//   Z'' = floor(x * 2^(62-e_t)) + 2^63 + 2^39           (unsigned; bytes b7 .. b0)
+// computed with three directed-rounding fp64 fmas (floor(x*2^(30-e_t)) and the floor of the
+// remainder * 2^32).  Its top 24 bits are X'' = 2^23 + X with X = rint(x * 2^(22-e_t)) (+-2^-40),
+// so the screen reads the planes h'' = b7, l = b6, F = b5 (all u8) and mu is split as before:
+// M = rint(mu * 2^(22-e_m)) = 65536 h' + 256 l' + G (h' s8; l', G u8).  tcgen05.mma kind::i8
+// computes exact int32 accumulators
+//   HH = sum h'' h',  CR = sum (h'' l' + l h'),  W1 = sum (h'' G + F h' + l l'),  W2 = sum (l G + F l')
+// so sum X'' M = 2^32 HH + 2^24 CR + 2^16 W1 + 2^8 W2 + sum F G (the last term, in
+// [0, d*255^2], is dropped).  Q'' = 256 HH + CR + (W1>>8) + (W2>>16) satisfies
+// sum X'' M / 2^24 in [Q'', Q'' + 2.25], and sum X M = sum X'' M - 2^23 sum_j M_j.  In units
+// U = 2^(e_t+e_m-20) the score T_c = floor(|mu_c|^2/U) + sum_j M_cj - 2 Q''_c brackets
+// |mu_c|^2/U - 2 x.mu_c/U within [T_c - 4.5 - 2e, T_c + 1 + 2e], e = ((sum|X| + sum|M|)/2 +
+// d/4 + 2^-40 sum|M|)/2^24, and the reference's fp64 chain differs from the real distance by
+// < 1 unit (|e_m| <= 400).  So every centroid with T_c > min_c T_c + W, W = 10 + ceil(4e),
+// has a strictly larger reference distance than some other centroid and cannot be the
+// argmin.  One survivor => it IS the reference argmin.  Several survivors => the sample goes
+// to the pending list and is re-evaluated with the reference chain (sequential j, no FMA,
+// strict <, ascending c, start (1e300, 0)).  Rows with |x| >= 2^e_t, inf or NaN send the
+// sample to the exact chain over every centroid.  NaN / inf centroids never win the chain
 // and are excluded from the screen.
 //
+// Bucket-reduce.  The eight planes of a 128-sample tile are stored as four SW128 buffers of
+// 128-byte rows [b7|b6], [b5|b4], [b3|b2], [b1|b0] (row = sample).  Read K-major they are the
+// screen's A operand; read MN-major (M = plane x column, K = sample) the SAME bytes are the A
+// operand of D[(plane, j)][c] += sum_q plane(x_qj) * onehot(a_q == c), whose B operand is the
+// tile's one-hot assignment matrix (MN-major [q][c]).  The int32 accumulators live in TMEM
+// for the whole launch (<= 128*255 per tile, < 2^31 for up to 65,793 tiles per CTA), so the
+// per-centroid sums sum_q Z''_q = sum_p 2^(8p) D_p are EXACT integers, minus count_c *
+// (2^63 + 2^39), times 2^(e_t-62), rounded once to fp64.  The fixed-point rounding is below
+// 2^(e_t-62) per element; rows holding a nonzero |x| < 2^(e_t-30) (where that could exceed a
+// 2^-32 relative error) take the exact fp64 fold in the resolve kernel instead.  The fold is
+// order-free, hence deterministic.
+//
 // Kernel shape: one persistent CTA per SM, 14 warps, warp-specialised around mbarriers:
-//   warp 0      TMA producer: 1-D bulk copies of 112-sample x tiles into a 3-stage ring
-//   warp 1      TMEM owner + MMA issuer (one thread): 16 tcgen05.mma per tile into a
-//               double-buffered 4 x 64-column int32 accumulator
-//   warps 2-5   converters: tile exponent, rint(x*2^(22-e)) via the fp64 magic-number add,
-//               byte split into the SW128 [h|l] and SW64 [F] K-major A operands
-//   warps 6-13  epilogue + bucket-reduce: tcgen05.ld the accumulators and screen; samples with
-//               a unique survivor are stably counting-sorted by centroid and folded into
-//               register-resident per-centroid sums (warp w owns centroids w, w+8, ...; lane
-//               l owns columns 2l, 2l+1; rows folded in ascending order: deterministic, no
-//               atomics); samples with several survivors (and every sample of a guarded
-//               tile) go to a per-CTA pending list
+//   warp 0      TMA producer: bulk copies of 64-sample halves into a 2-stage ring, plus bulk
+//               L2 prefetches two tiles ahead
+//   warp 1      TMEM owner + MMA issuer (one thread): 16 screen MMAs per tile into 4 x 64
+//               int32 columns, then the previous tile's 16 fold MMAs into the persistent
+//               4 x 64 fold columns
+//   warps 2-9   converters: conflict-free row loads, Z'' via directed-rounding fmas, lane-pair
+//               exchange and byte-plane transpose into the double-buffered SW128 planes
+//   warps 10-13 epilogue: tcgen05.ld the screen accumulators, decide, write assignments,
+//               counts and the tile's one-hot rows; at the end read the fold accumulators
 //   resolve     a second small kernel evaluates the reference chain for the pending samples
 //               (one thread per (sample, candidate) pair), writes their assignments and folds
-//               their rows into per-CTA partial records, in list order (deterministic).
+//               their rows into per-CTA partial records in fp64, in list order.
 #include <algorithm>
 #include <climits>
 #include <cstdio>
@@ -65,46 +77,47 @@ namespace sk {
 
 using namespace sm100;
 
-constexpr int kThreads = 512;
-constexpr int kTile = 112;        // samples per tile (the MMA runs M=128; rows 112..127 are zero)
-constexpr int kMmaM = 128;
-constexpr int kStages = 3;
+constexpr int kTile = 128;   // samples per tile = MMA M
 constexpr int kMaxD = 64;
 constexpr int kMaxK = 64;
-// warp roles: 0 = TMA producer; 1 = TMEM owner + MMA issuer; 2-7 converters; 8-11 epilogue
-// (TMEM lane quarters 0-3); 12-15 fold
-constexpr int kWarpProd = 0, kWarpMma = 1, kWarpC0 = 2, kNumC = 6, kWarpE0 = 8, kWarpR0 = 12;
+constexpr int kNumC = 8;     // converter warps (16 rows of every tile each)
+constexpr int kNumA = 3;     // plane buffers in flight
+constexpr int kWarpMma = 0, kWarpC0 = 1, kWarpE0 = kWarpC0 + kNumC;
+constexpr int kThreads = (kWarpE0 + 4) * 32;              // 416
+constexpr int kPf = 3;                                    // L2 prefetch distance (tiles)
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kAccCols = 256;                        // 4 accumulators x 64 columns
-constexpr uint32_t kXStage = kTile * kMaxD * 8;           // 56 KiB
-constexpr uint32_t kOffA1 = kStages * kXStage;            // [h|l]  128 x 128 B, SW128
-constexpr uint32_t kOffA2 = kOffA1 + kMmaM * 128;         // [F]    128 x 64 B,  SW64
-constexpr uint32_t kOffB1 = kOffA2 + kMmaM * 64;          // [h'|l'] 64 x 128 B, SW128
+constexpr uint32_t kFoldCol = 256;                        // fold accumulators: columns 256..511
+constexpr uint32_t kPlane2 = kTile * 128;                 // one [b_hi|b_lo] SW128 buffer, 16 KiB
+constexpr uint32_t kABuf = 4 * kPlane2;                   // eight planes, 64 KiB
+constexpr uint32_t kOffA = 0;
+constexpr uint32_t kOffB1 = kOffA + kNumA * kABuf;        // [h'|l'] 64 x 128 B, SW128
 constexpr uint32_t kOffB2 = kOffB1 + kMaxK * 128;         // [G]     64 x 64 B,  SW64
-constexpr uint32_t kOffMisc = kOffB2 + kMaxK * 64;
-static_assert(kOffA1 % 1024 == 0 && kOffB1 % 1024 == 0 && kOffA2 % 512 == 0 && kOffB2 % 512 == 0,
+constexpr uint32_t kOffOH = kOffB2 + kMaxK * 64;          // one-hot [q][c] 128 x 64 B, SW64, x2
+constexpr uint32_t kOHBuf = kTile * 64;
+constexpr uint32_t kOffMisc = kOffOH + 2 * kOHBuf;
+static_assert(kOffA % 1024 == 0 && kOffB1 % 1024 == 0 && kOffB2 % 512 == 0 && kOffOH % 512 == 0,
               "UMMA operand alignment");
-constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: x + kMagic rounds x to an integer
-
-constexpr int kListCap = 16;  // fold list slots per owned centroid per tile
+static_assert(kNumA * kABuf >= 2u * kMaxK * 64 * 16, "final fold scratch must fit the plane buffers");
+constexpr double kMagic = 6755399441055744.0;        // 1.5 * 2^52: x + kMagic rounds x to an integer
+constexpr double kMagicZ = 6755401588539520.0;       // kMagic + 2^31 + 2^7: low word = floor + offset
+constexpr int kFoldBits = 30;  // rows with a nonzero |x| < 2^(e_t - 30) take the exact fp64 fold
 
 struct Misc {
-  uint64_t full[kStages], sempty[kStages], cfull[kStages], efull[kStages];
-  uint64_t a_full, a_empty, tfull[2], tempty[2];
+  uint64_t a_full[kNumA], c_full[kNumA], a_empty[kNumA], oh_full[2], oh_empty[2];
+  uint64_t t_full, t_empty, fold_done;
   unsigned long long valid;
   uint32_t tmem_base;
   int em, yabs, disabled, window;
   uint32_t mu_maxhi;
-  alignas(16) int nm0[kMaxK];             // floor(|mu_c|^2 / U), U = 2^(e_t + e_m - 20), e_t = e_m + 1
+  alignas(16) int nm0[kMaxK];             // floor(|mu_c|^2 / U) + sum_j M_cj
   double nmf[kMaxK];
-  unsigned char rowflag[kStages][kMmaM];  // sample needs the exact chain (|x| >= 2^e_t, inf, NaN)
+  int cnt[kMaxK];                         // screened rows folded per centroid (this CTA)
+  alignas(16) unsigned char rowflag[kNumA][kTile];  // 1: exact chain over every centroid; 2: exact fold
   int pcount[2][4];
-  uint32_t gm[kStages][4][kMaxK];         // per stage, per quarter: rows of the tile resolved to c
-  unsigned char list[4][16][kListCap];    // per fold warp, per owned centroid: rows, ascending
 };
 constexpr uint32_t kSmemBytes = kOffMisc + sizeof(Misc);
 static_assert(kSmemBytes <= 232448, "shared-memory plan exceeds 227 KiB");
-constexpr int kInvalidNm = 0x70000000;  // > any valid score (|Q| < 2^26, nm <= 2^25)
+constexpr int kInvalidNm = 0x70000000;  // > any valid score (|T| < 1.4e9)
 constexpr int kNoCandidate = 0x60000000;
 
 __device__ __forceinline__ int exp_bound(uint32_t maxhi) {
@@ -122,9 +135,39 @@ __device__ __forceinline__ uint32_t sw64_offset(uint32_t row, uint32_t kbyte) {
 __device__ __forceinline__ int rint_magic(double scaled) {
   return __double2loint(__dadd_rn(scaled, kMagic));
 }
-// rint(x * scale) for a power-of-two scale: the product is exact, so one fma rounds once
-__device__ __forceinline__ int rint_fma(double x, double scale) {
-  return __double2loint(__fma_rn(x, scale, kMagic));
+
+// Z'' = floor(x * 2^32 * s) + 2^63 + 2^39 as (hi, lo) words, s = 2^(30 - e_t), |x * s| < 2^30
+__device__ __forceinline__ void zsplit(double x, double s, uint32_t& hi, uint32_t& lo) {
+  const double t1 = __fma_rd(x, s, kMagicZ);            // kMagicZ + floor(x s)
+  const double hd = __dsub_rn(t1, kMagicZ);              // floor(x s), exact
+  const double r = __fma_rn(x, s, -hd);                  // x s - floor(x s) in [0, 1), exact
+  const double t2 = __fma_rd(r, 4294967296.0, kMagic);   // kMagic + floor(r 2^32)
+  hi = static_cast<uint32_t>(__double2loint(t1));        // floor(x s) + 2^31 + 2^7
+  lo = static_cast<uint32_t>(__double2loint(t2));
+}
+
+// streaming 32-byte / 16-byte loads of sample rows (read once: no L1 allocation)
+__device__ __forceinline__ void ldg256(const double* p, double& a, double& b, double& c, double& d) {
+  asm("ld.global.nc.L1::no_allocate.L2::256B.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+__device__ __forceinline__ void ldg128(const double* p, double& a, double& b) {
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "l"(p));
+}
+
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok) : "r"(smem_addr(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+
+// 1: |x| >= 2^e_t, inf or NaN (screen out of range); 2: 0 < |x| < 2^(e_t - 30) (fold precision)
+__device__ __forceinline__ int elem_flag(double x, uint32_t hw_hi, uint32_t hw_lo) {
+  const uint32_t hw = static_cast<uint32_t>(__double2hiint(x)) & 0x7fffffffu;
+  const uint32_t lw = static_cast<uint32_t>(__double2loint(x));
+  return (hw >= hw_hi ? 1 : 0) | ((hw < hw_lo && (hw | lw) != 0u) ? 2 : 0);
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -132,21 +175,9 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
                        const double* __restrict__ mu, int32_t* __restrict__ assign,
                        long long* __restrict__ part_counts, double* __restrict__ part_sums,
                        long long* __restrict__ pend_idx, unsigned long long* __restrict__ pend_mask,
-                       long long* __restrict__ pend_count, long long pend_cap,
-                       long long* __restrict__ trace) {
+                       long long* __restrict__ pend_count, long long pend_cap) {
   extern __shared__ __align__(1024) unsigned char smem[];
   Misc& S = *reinterpret_cast<Misc*>(smem + kOffMisc);
-  // optional per-role cycle accounting (build with -DDLX_KMEANS_TRACE, run with
-  // DLX_KMEANS_TRACE=1): lane 0 of one warp per role
-#ifdef DLX_KMEANS_TRACE
-  long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long t0 = clock64();
-#define TR(slot) do { const long long _t = clock64(); tr[slot] += _t - t0; t0 = _t; } while (0)
-#else
-#define TR(slot) do { } while (0)
-#endif
-  unsigned char* A1 = smem + kOffA1;
-  unsigned char* A2 = smem + kOffA2;
   unsigned char* B1 = smem + kOffB1;
   unsigned char* B2 = smem + kOffB2;
   const int tid = threadIdx.x;
@@ -156,23 +187,24 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
 
   // ---- prologue: barriers, B operands (fixed-point centroids), per-centroid constants ------
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&S.full[s], 1);
-      mbar_init(&S.sempty[s], 4);
-      mbar_init(&S.cfull[s], kNumC);
-      mbar_init(&S.efull[s], 4);
+    for (int s = 0; s < kNumA; ++s) {
+      mbar_init(&S.a_full[s], kNumC);
+      mbar_init(&S.c_full[s], kNumC);
+      mbar_init(&S.a_empty[s], 1);
     }
-    mbar_init(&S.a_full, kNumC);
-    mbar_init(&S.a_empty, 1);
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&S.tfull[b], 1);
-      mbar_init(&S.tempty[b], 4);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&S.oh_full[s], 4);
+      mbar_init(&S.oh_empty[s], 1);
     }
+    mbar_init(&S.t_full, 1);
+    mbar_init(&S.t_empty, 4);
+    mbar_init(&S.fold_done, 1);
     S.valid = 0;
     S.yabs = 0;
     S.mu_maxhi = 0;
     fence_mbar_init();
   }
+  if (tid < kMaxK) S.cnt[tid] = 0;
   __syncthreads();
   if (tid < kMaxK) {  // per centroid: validity (all finite), max |mu| high word, |mu|^2
     const int c = tid;
@@ -212,23 +244,27 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       B1[sw128_offset(c, 64 + j)] = static_cast<unsigned char>(Y >> 8);
       B2[sw64_offset(c, j)] = static_cast<unsigned char>(Y);
     }
-    if (tid < kMaxK && ((valid >> tid) & 1)) {
-      int sa = 0;
-      for (int j = 0; j < d; ++j) sa += abs(rint_magic(mu[tid * d + j] * scale));
-      atomicMax(&S.yabs, sa);
+    if (tid < kMaxK) {
+      int sa = 0, ssum = 0;
+      if ((valid >> tid) & 1) {
+        for (int j = 0; j < d; ++j) {
+          const int Y = rint_magic(mu[tid * d + j] * scale);
+          sa += abs(Y);
+          ssum += Y;
+        }
+        atomicMax(&S.yabs, sa);
+      }
+      // per-launch score constants (the sample exponent is fixed at e_t = e_m + 1)
+      S.nm0[tid] = (S.disabled || !((valid >> tid) & 1))
+                       ? kInvalidNm
+                       : __double2int_rd(S.nmf[tid] * ldexp(1.0, 19 - 2 * S.em)) + ssum;
     }
   }
   __syncthreads();
-  if (tid < kMaxK) {  // per-launch score constants (the sample exponent is fixed at e_t = e_m + 1)
-    const unsigned long long valid = S.valid;
-    S.nm0[tid] = (S.disabled || !((valid >> tid) & 1))
-                     ? kInvalidNm
-                     : __double2int_rd(S.nmf[tid] * ldexp(1.0, 19 - 2 * S.em));
-    if (tid == 0) {
-      // W = 9 + ceil(4e), e = ((d*2^22 + max_c sum|Y'|)/2 + d/4) / 2^24  (+1 margin)
-      const long long num = (static_cast<long long>(d) << 22) + S.yabs;
-      S.window = 10 + static_cast<int>((2 * num + d + (1ll << 24) - 1) >> 24);
-    }
+  if (tid == 0) {
+    // W = 10 + ceil(4e), e = ((d*2^22 + max_c sum|M|)/2 + d/4) / 2^24  (+1 margin covers 2^-40 terms)
+    const long long num = (static_cast<long long>(d) << 22) + S.yabs;
+    S.window = 10 + static_cast<int>((2 * num + d + (1ll << 24) - 1) >> 24);
   }
   fence_proxy_async_smem();
   if (warp == kWarpMma) tmem_alloc<kTmemCols>(&S.tmem_base);
@@ -237,115 +273,181 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
 
-  if (warp == kWarpProd) {
-    // ======================= TMA producer =======================
-    if (lane == 0) {
-      for (int m = 0; m < mtiles; ++m) {
-        const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
-        const int s = m % kStages;
-        TR(1);
-        if (m >= kStages) mbar_wait(&S.sempty[s], ((m / kStages) - 1) & 1);
-        TR(0);
-        const int rows = static_cast<int>(n - t * kTile < kTile ? n - t * kTile : kTile);
-        const uint32_t bytes = static_cast<uint32_t>(rows) * d * 8u;
-        mbar_arrive_expect_tx(&S.full[s], bytes);
-        bulk_g2s(smem + s * kXStage, x + t * kTile * d, bytes, &S.full[s]);
-      }
-    }
-  } else if (warp == kWarpMma) {
+  if (warp == kWarpMma) {
     // ======================= MMA issuer =======================
+    // Polls both kinds of work so neither waits behind the other: the screen of the next
+    // converted tile (its planes ready and the screen columns released by the epilogue) and
+    // the fold of the oldest screened tile whose one-hot rows are written.
     if (lane == 0) {
-      // A pieces: h (s8), l (u8), F (u8); B pieces: h' (s8), l' (u8), G (u8)
-      constexpr uint32_t ID_hh = idesc_i8(kMmaM, 64, 1, 1);
-      constexpr uint32_t ID_hu = idesc_i8(kMmaM, 64, 1, 0);
-      constexpr uint32_t ID_uh = idesc_i8(kMmaM, 64, 0, 1);
-      constexpr uint32_t ID_uu = idesc_i8(kMmaM, 64, 0, 0);
-      const uint32_t a1 = smem_addr(A1), a2 = smem_addr(A2), b1 = smem_addr(B1), b2 = smem_addr(B2);
+      constexpr uint32_t ID_us = idesc_i8(kTile, 64, 0, 1);   // u8 sample plane x s8 h'
+      constexpr uint32_t ID_uu = idesc_i8(kTile, 64, 0, 0);
+      constexpr uint32_t ID_fold = idesc_i8_major(kTile, 64, 0, 0, 1, 1);
+      const uint32_t b1 = smem_addr(B1), b2 = smem_addr(B2);
       const int nk = (d + 31) / 32;
-      for (int m = 0; m < mtiles; ++m) {
-        const int b = m & 1;
-        TR(2);
-        mbar_wait(&S.a_full, m & 1);
-        TR(0);
-        if (m >= 2) mbar_wait(&S.tempty[b], ((m >> 1) - 1) & 1);
-        TR(1);
-        tc_fence_after();
-        const uint32_t dt = tmem + b * kAccCols;
-        for (int kk = 0; kk < nk; ++kk) {
-          const uint64_t xh = sw128_kmajor_desc(a1 + 32 * kk), xl = sw128_kmajor_desc(a1 + 64 + 32 * kk);
-          const uint64_t xf = sw64_kmajor_desc(a2 + 32 * kk);
-          const uint64_t mh = sw128_kmajor_desc(b1 + 32 * kk), ml = sw128_kmajor_desc(b1 + 64 + 32 * kk);
-          const uint64_t mg = sw64_kmajor_desc(b2 + 32 * kk);
-          const uint32_t acc = kk > 0;
-          mma_i8(dt + 0, xh, mh, ID_hh, acc);      // HH
-          mma_i8(dt + 64, xh, ml, ID_hu, acc);     // CR = h l' + l h'
-          mma_i8(dt + 64, xl, mh, ID_uh, 1);
-          mma_i8(dt + 128, xh, mg, ID_hu, acc);    // W1 = h G + F h' + l l'
-          mma_i8(dt + 128, xf, mh, ID_uh, 1);
-          mma_i8(dt + 128, xl, ml, ID_uu, 1);
-          mma_i8(dt + 192, xl, mg, ID_uu, acc);    // W2 = l G + F l'
-          mma_i8(dt + 192, xf, ml, ID_uu, 1);
+      int ns = 0, nf = 0;
+      while (nf < mtiles) {
+        bool progress = false;
+        if (ns < mtiles && mbar_test(&S.a_full[ns % kNumA], (ns / kNumA) & 1) &&
+            (ns == 0 || mbar_test(&S.t_empty, (ns - 1) & 1))) {
+          tc_fence_after();
+          const uint32_t a0 = smem_addr(smem + kOffA + (ns % kNumA) * kABuf);
+          for (int kk = 0; kk < nk; ++kk) {
+            const uint64_t xh = sw128_kmajor_desc(a0 + 32 * kk);             // b7 = h''
+            const uint64_t xl = sw128_kmajor_desc(a0 + 64 + 32 * kk);        // b6 = l
+            const uint64_t xf = sw128_kmajor_desc(a0 + kPlane2 + 32 * kk);   // b5 = F
+            const uint64_t mh = sw128_kmajor_desc(b1 + 32 * kk), ml = sw128_kmajor_desc(b1 + 64 + 32 * kk);
+            const uint64_t mg = sw64_kmajor_desc(b2 + 32 * kk);
+            const uint32_t acc = kk > 0;
+            mma_i8(tmem + 0, xh, mh, ID_us, acc);      // HH
+            mma_i8(tmem + 64, xh, ml, ID_uu, acc);     // CR = h'' l' + l h'
+            mma_i8(tmem + 64, xl, mh, ID_us, 1);
+            mma_i8(tmem + 128, xh, mg, ID_uu, acc);    // W1 = h'' G + F h' + l l'
+            mma_i8(tmem + 128, xf, mh, ID_us, 1);
+            mma_i8(tmem + 128, xl, ml, ID_uu, 1);
+            mma_i8(tmem + 192, xl, mg, ID_uu, acc);    // W2 = l G + F l'
+            mma_i8(tmem + 192, xf, ml, ID_uu, 1);
+          }
+          mma_commit(&S.t_full);
+          ++ns;
+          progress = true;
         }
-        mma_commit(&S.a_empty);
-        mma_commit(&S.tfull[b]);
+        if (nf < ns && mbar_test(&S.oh_full[nf & 1], (nf >> 1) & 1)) {
+          tc_fence_after();
+          const uint32_t a0 = smem_addr(smem + kOffA + (nf % kNumA) * kABuf);
+          const uint32_t oh = smem_addr(smem + kOffOH + (nf & 1) * kOHBuf);
+#pragma unroll
+          for (int kk = 0; kk < kTile / 32; ++kk) {
+            const uint64_t bdesc = sw64_kmajor_desc(oh + kk * 2048);   // MN-major [q][c], SW64
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              const uint64_t adesc = sw128_kmajor_desc(a0 + g * kPlane2 + kk * 4096);  // MN-major
+              mma_i8(tmem + kFoldCol + 64 * g, adesc, bdesc, ID_fold, (nf > 0 || kk > 0) ? 1u : 0u);
+            }
+          }
+          mma_commit(&S.a_empty[nf % kNumA]);
+          mma_commit(&S.oh_empty[nf & 1]);
+          ++nf;
+          progress = true;
+        }
+        if (!progress) __nanosleep(32);
       }
+      mma_commit(&S.fold_done);
     }
-  } else if (warp >= kWarpC0 && warp < kWarpC0 + kNumC) {
-    // ======================= converters (6 warps) =======================
+  } else if (warp < kWarpE0) {
+    // ======================= converters (8 warps) =======================
+    // Warp cw owns rows 16 cw .. 16 cw + 15 of every tile as eight row pairs (r, r + 4) of an
+    // 8-row SW128 atom.  Lane (hl, p) = (lane >> 4, lane & 15) holds columns 4p .. 4p+3 of row
+    // r + 4 hl: one coalesced 32-byte load per pair, issued a whole tile ahead into registers
+    // (64 KiB in flight per SM, on top of a bulk L2 prefetch kPf tiles ahead).  Rows r and
+    // r + 4 land in disjoint bank halves, so every plane store is one wavefront.
     const int cw = warp - kWarpC0;
     const int em = S.em, disabled = S.disabled;
-    const double scale = disabled ? 0.0 : ldexp(1.0, 21 - em);   // 2^(22 - e_t), e_t = e_m + 1
-    const uint32_t hw_limit = static_cast<uint32_t>(1023 + em + 1) << 20;  // |x| >= 2^e_t
-    const int half = lane >> 4, j0 = 4 * (lane & 15);
-    const bool colok = j0 < d, col2ok = j0 + 2 < d;
-    for (int m = 0; m < mtiles; ++m) {
-      const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
-      const int s = m % kStages;
-      const int rows = static_cast<int>(n - t * kTile < kTile ? n - t * kTile : kTile);
-      TR(4);
-      mbar_wait(&S.full[s], (m / kStages) & 1);
-      TR(0);
-      const double* xs = reinterpret_cast<const double*>(smem + s * kXStage);
-      if (m >= 1) mbar_wait(&S.a_empty, (m - 1) & 1);
-      TR(2);
-      // Y = rint(x * 2^(22-e_t)) with e_t = e_m + 1 fixed per launch; row pairs (2p, 2p+1),
-      // p = cw, cw + 6, ...; lane (half, lane16) converts columns 4*lane16 .. +3 of row 2p+half.
-      // A row with |x| >= 2^e_t, inf or NaN is flagged (exact chain).
-#pragma unroll 2
-      for (int pp = cw; pp < kMmaM / 2; pp += kNumC) {
-        const int q = 2 * pp + half;
-        const bool ok = q < rows && colok;
-        const double* src = ok ? xs + q * d + j0 : xs;
-        const double2 v0 = *reinterpret_cast<const double2*>(src);
-        const double2 v1 = (ok && col2ok) ? *reinterpret_cast<const double2*>(src + 2) : make_double2(0.0, 0.0);
-        const double a0 = ok ? v0.x : 0.0, a1 = ok ? v0.y : 0.0;
-        const uint32_t hx = max(max(static_cast<uint32_t>(__double2hiint(a0)) & 0x7fffffffu,
-                                    static_cast<uint32_t>(__double2hiint(a1)) & 0x7fffffffu),
-                                max(static_cast<uint32_t>(__double2hiint(v1.x)) & 0x7fffffffu,
-                                    static_cast<uint32_t>(__double2hiint(v1.y)) & 0x7fffffffu));
-        const unsigned badm = __ballot_sync(0xffffffffu, hx >= hw_limit);
-        if ((lane & 15) == 0) S.rowflag[s][q] = static_cast<unsigned char>(
-            disabled || ((badm >> (16 * half)) & 0xffffu) != 0);
-        const int Y0 = rint_fma(a0, scale), Y1 = rint_fma(a1, scale);
-        const int Y2 = rint_fma(v1.x, scale), Y3 = rint_fma(v1.y, scale);
-        // bytes of Y (little endian): b0 = F, b1 = l, b2 = h (low byte of Y >> 16)
-        const uint32_t p01 = __byte_perm(Y0, Y1, 0x6240), p23 = __byte_perm(Y2, Y3, 0x6240);
-        const uint32_t q01 = __byte_perm(Y0, Y1, 0x0051), q23 = __byte_perm(Y2, Y3, 0x0051);
-        const uint32_t oh = sw128_offset(q, j0);
-        *reinterpret_cast<uint32_t*>(A1 + oh) = __byte_perm(p01, p23, 0x7632);                 // h
-        *reinterpret_cast<uint32_t*>(A1 + (oh ^ 64u)) = __byte_perm(q01, q23, 0x5410);         // l
-        *reinterpret_cast<uint32_t*>(A2 + sw64_offset(q, j0)) = __byte_perm(p01, p23, 0x5410);  // F
+    const int et = em + 1;
+    const double s_hi = disabled ? 0.0 : ldexp(1.0, 30 - et);
+    const uint32_t hw_hi = static_cast<uint32_t>(1023 + et) << 20;          // |x| >= 2^e_t, inf, NaN
+    const int lo_e = 1023 + et - kFoldBits;
+    const uint32_t hw_lo = lo_e > 0 ? static_cast<uint32_t>(lo_e) << 20 : 0u;  // nonzero |x| < 2^(e_t-30)
+    const int hl = lane >> 4, p = lane & 15;
+    const int col0 = 4 * p;
+    const int nvalid = col0 + 4 <= d ? 4 : (col0 + 2 <= d ? 2 : 0);
+    const bool wide = ((d & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 31) == 0);
+    const uint32_t chunk0 = static_cast<uint32_t>((p >> 2) ^ (4 * hl));
+    double v[8][4];
+    auto load_tile = [&](int mm) {
+      const int64_t t = blockIdx.x + static_cast<int64_t>(mm) * gridDim.x;
+      const int64_t rows = n - t * kTile;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int row = 16 * cw + 8 * (i >> 2) + (i & 3) + 4 * hl;
+        v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0.0;
+        if (row < rows && nvalid) {
+          const double* src = x + (t * kTile + row) * d + col0;
+          if (wide) {
+            ldg256(src, v[i][0], v[i][1], v[i][2], v[i][3]);
+          } else {
+            ldg128(src, v[i][0], v[i][1]);
+            if (nvalid == 4) ldg128(src + 2, v[i][2], v[i][3]);
+          }
+        }
       }
-      TR(3);
+    };
+    if (cw == 0 && lane == 0)
+      for (int mm = 1; mm < kPf && mm < mtiles; ++mm) {
+        const int64_t t = blockIdx.x + static_cast<int64_t>(mm) * gridDim.x;
+        const int64_t rows = n - t * kTile < kTile ? n - t * kTile : kTile;
+        bulk_prefetch_l2(x + t * kTile * d, static_cast<uint32_t>(rows * d * 8));
+      }
+    if (mtiles > 0) load_tile(0);
+    for (int m = 0; m < mtiles; ++m) {
+      const int b = m % kNumA;
+      if (cw == 0 && lane == 0 && m + kPf < mtiles) {
+        const int64_t t = blockIdx.x + static_cast<int64_t>(m + kPf) * gridDim.x;
+        const int64_t rows = n - t * kTile < kTile ? n - t * kTile : kTile;
+        bulk_prefetch_l2(x + t * kTile * d, static_cast<uint32_t>(rows * d * 8));
+      }
+      // row flags: a cheap conservative test over the lane's 32 values; only if some lane
+      // sees a value outside [2^(e_t-30), 2^e_t) (zeros included) classify row by row
+      uint32_t mx = 0, mn = 0xffffffffu;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t hw = static_cast<uint32_t>(__double2hiint(v[i][e])) & 0x7fffffffu;
+          mx = max(mx, hw);
+          mn = min(mn, hw);
+        }
+      const bool odd = disabled || mx >= hw_hi || mn < hw_lo;
+      if (m >= kNumA) mbar_wait(&S.a_empty[b], ((m / kNumA) - 1) & 1);
+      if (__any_sync(0xffffffffu, odd)) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          int f = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) f |= elem_flag(v[i][e], hw_hi, hw_lo);
+          const int f0 = static_cast<int>(__reduce_or_sync(0xffffffffu, static_cast<unsigned>(hl ? 0 : f)));
+          const int f1 = static_cast<int>(__reduce_or_sync(0xffffffffu, static_cast<unsigned>(hl ? f : 0)));
+          const int r = 16 * cw + 8 * (i >> 2) + (i & 3);
+          if (lane == 0) S.rowflag[b][r] = static_cast<unsigned char>(disabled ? 1 : (f0 & 1 ? 1 : f0));
+          if (lane == 16) S.rowflag[b][r + 4] = static_cast<unsigned char>(disabled ? 1 : (f1 & 1 ? 1 : f1));
+        }
+      } else if (lane == 0) {
+        *reinterpret_cast<uint4*>(&S.rowflag[b][16 * cw]) = make_uint4(0u, 0u, 0u, 0u);
+      }
+      unsigned char* Ab = smem + kOffA + b * kABuf;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint32_t H[4], L[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) zsplit(v[i][e], s_hi, H[e], L[e]);
+        // 4x4 byte transposes: plane word = that byte of the four consecutive columns
+        const uint32_t ha = __byte_perm(H[0], H[1], 0x5140), hb = __byte_perm(H[0], H[1], 0x7362);
+        const uint32_t hc = __byte_perm(H[2], H[3], 0x5140), hd = __byte_perm(H[2], H[3], 0x7362);
+        const uint32_t la = __byte_perm(L[0], L[1], 0x5140), lb = __byte_perm(L[0], L[1], 0x7362);
+        const uint32_t lc = __byte_perm(L[2], L[3], 0x5140), ld = __byte_perm(L[2], L[3], 0x7362);
+        const int r4 = i & 3;
+        const uint32_t off = static_cast<uint32_t>(2 * cw + (i >> 2)) * 1024u +
+                             static_cast<uint32_t>(r4 + 4 * hl) * 128u +
+                             ((chunk0 ^ static_cast<uint32_t>(r4)) << 4) + 4u * (p & 3);
+        const uint32_t off2 = off ^ 64u;
+        *reinterpret_cast<uint32_t*>(Ab + off) = __byte_perm(hb, hd, 0x7632);                  // b7
+        *reinterpret_cast<uint32_t*>(Ab + off2) = __byte_perm(hb, hd, 0x5410);                 // b6
+        *reinterpret_cast<uint32_t*>(Ab + kPlane2 + off) = __byte_perm(ha, hc, 0x7632);        // b5
+        *reinterpret_cast<uint32_t*>(Ab + kPlane2 + off2) = __byte_perm(ha, hc, 0x5410);       // b4
+        *reinterpret_cast<uint32_t*>(Ab + 2 * kPlane2 + off) = __byte_perm(lb, ld, 0x7632);    // b3
+        *reinterpret_cast<uint32_t*>(Ab + 2 * kPlane2 + off2) = __byte_perm(lb, ld, 0x5410);   // b2
+        *reinterpret_cast<uint32_t*>(Ab + 3 * kPlane2 + off) = __byte_perm(la, lc, 0x7632);    // b1
+        *reinterpret_cast<uint32_t*>(Ab + 3 * kPlane2 + off2) = __byte_perm(la, lc, 0x5410);   // b0
+      }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&S.a_full);
-        mbar_arrive(&S.cfull[s]);
+        mbar_arrive(&S.a_full[b]);
+        mbar_arrive(&S.c_full[b]);
       }
+      if (m + 1 < mtiles) load_tile(m + 1);
     }
-  } else if (warp >= kWarpE0 && warp < kWarpR0) {
-    // ======================= epilogue: screen + decide (4 warps, one per lane quarter) ===========
+  } else {
+    // ======================= epilogue (4 warps, one per TMEM lane quarter) ===========
     const int quarter = warp & 3;
     const int q = quarter * 32 + lane;  // sample row within the tile (M row)
     const unsigned long long kmask = k == 64 ? ~0ull : ((1ull << k) - 1);
@@ -355,21 +457,19 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     unsigned long long* my_pmask = pend_mask + static_cast<size_t>(blockIdx.x) * pend_cap;
     long long pending = 0;
     const int4* nm4 = reinterpret_cast<const int4*>(S.nm0);
+    const uint32_t oh_row = (static_cast<uint32_t>(q) >> 3) * 512u + (q & 7) * 64u;
+    const uint32_t oh_sw = (q & 7) >> 1;
     for (int m = 0; m < mtiles; ++m) {
       const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
-      const int s = m % kStages, b = m & 1;
+      const int b = m & 1;
       const int rows = static_cast<int>(n - t * kTile < kTile ? n - t * kTile : kTile);
-      TR(6);
-      mbar_wait(&S.cfull[s], (m / kStages) & 1);
-      TR(0);
-      mbar_wait(&S.tfull[b], (m >> 1) & 1);
-      TR(1);
+      mbar_wait(&S.t_full, m & 1);
       tc_fence_after();
       int tv[64];
       int lmin = kInvalidNm;
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
-        const uint32_t col = b * kAccCols + 8 * ch;
+        const uint32_t col = 8 * ch;
         int hh[8], cr[8], w1[8], w2[8];
         tmem_ld8(tmem + lane_base + col, hh);
         tmem_ld8(tmem + lane_base + col + 64, cr);
@@ -389,13 +489,16 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.tempty[b]);
-      TR(2);
+      if (lane == 0) mbar_arrive(&S.t_empty);
+      const int b3 = m % kNumA;
+      mbar_wait(&S.c_full[b3], (m / kNumA) & 1);
       unsigned long long full = 0;
       bool pend = false;
-      int a = -1;
+      int hot = -1;
       if (q < rows) {
-        if (S.rowflag[s][q]) {
+        const int flag = S.rowflag[b3][q];
+        int a = -1;
+        if (flag & 1) {
           full = kmask;  // |x| out of the screen's range, inf or NaN: the exact chain over all c
           pend = true;
         } else if (lmin < kNoCandidate) {
@@ -411,14 +514,35 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         } else {
           a = 0;  // no finite centroid: the chain keeps its start index
         }
-        if (a >= 0 && assign) assign[t * kTile + q] = a;
+        if (flag & 2) pend = true;  // exact fp64 fold (the chain over the survivors re-derives a)
+        if (!pend) {
+          if (assign) assign[t * kTile + q] = a;
+          hot = a;
+          atomicAdd(&S.cnt[a], 1);
+        }
       }
-      // group masks for the fold: gm[s][quarter][c] = this quarter's rows resolved to c
-      const unsigned grp = __match_any_sync(0xffffffffu, a);
-      S.gm[s][quarter][lane] = 0u;
-      S.gm[s][quarter][lane + 32] = 0u;
+      // this tile's one-hot row q (MN-major [q][c], SW64); zero for pending / padding rows
+      if (m >= 2) mbar_wait(&S.oh_empty[b], ((m >> 1) - 1) & 1);
+      {
+        unsigned char* ohb = smem + kOffOH + b * kOHBuf + oh_row;
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          uint4 w = make_uint4(0u, 0u, 0u, 0u);
+          const int rel = hot - 16 * ch;
+          const uint32_t bit = 1u << (8 * (rel & 3));
+          if (rel >= 0 && rel < 16) {
+            const int wi = rel >> 2;
+            w.x = wi == 0 ? bit : 0u;
+            w.y = wi == 1 ? bit : 0u;
+            w.z = wi == 2 ? bit : 0u;
+            w.w = wi == 3 ? bit : 0u;
+          }
+          *reinterpret_cast<uint4*>(ohb + ((ch ^ oh_sw) << 4)) = w;
+        }
+      }
+      fence_proxy_async_smem();
       __syncwarp();
-      if ((grp & ((1u << lane) - 1)) == 0 && a >= 0) S.gm[s][quarter][a] = grp;
+      if (lane == 0) mbar_arrive(&S.oh_full[b]);
       // deterministic pending-list append, ordered by sample row
       const unsigned pb = __ballot_sync(0xffffffffu, pend);
       if (lane == 0) S.pcount[m & 1][quarter] = __popc(pb);
@@ -431,117 +555,63 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         my_pmask[slot] = full;
       }
       pending += p0 + p1 + p2 + S.pcount[m & 1][3];
-      TR(3);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.efull[s]);
     }
     if (quarter == 0 && lane == 0) pend_count[blockIdx.x] = pending;
-  } else {
-    // ======================= fold: bucket-reduce (4 warps) =======================
-    // Warp rw owns centroids rw + 4u (u = 0..15); lane (u, g) = (lane >> 1, lane & 1) owns
-    // columns 32g .. 32g+31 of centroid rw + 4u as 16 pairs visited in the rotated order
-    // (i + u) % 16, so one LDS.128 of the warp spreads over all banks; acc[i] holds pair
-    // (i + u) % 16.  Rows are folded in ascending order: deterministic, no atomics.
-    const int rw = warp - kWarpR0;
-    const int u = lane >> 1, g = lane & 1;
-    const int c = rw + 4 * u;
-    double acc[16][2];
+
+    // ---- flush: exact per-centroid sums from the fold accumulators ------------------------
+    // TMEM lane q < 64 holds planes b7, b5, b3, b1 of column j = q; lane 64 + j planes b6, b4,
+    // b2, b0 (fold group g = columns 256 + 64 g).  Each thread forms its planes' partial sum
+    // as an integer for every centroid into scratch (the plane buffers, free once every fold
+    // MMA has completed); then every (c, j) cell adds the two halves, removes the per-row
+    // offset count_c * (2^63 + 2^39) and scales by 2^(e_t - 62).
+    mbar_wait(&S.fold_done, 0);
+    tc_fence_after();
+    named_bar(1, 128);
+    unsigned long long* scratch = reinterpret_cast<unsigned long long*>(smem + kOffA);
+    {
+      const int half = q >> 6, j = q & 63;
+      for (int cc = 0; cc < 8; ++cc) {
+        int acc[4][8];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = 0.0;
-    long long cnt_lane = 0;  // rows of centroid c in quarters 2g, 2g+1
-    for (int m = 0; m < mtiles; ++m) {
-      const int s = m % kStages;
-      TR(6);
-      mbar_wait(&S.efull[s], (m / kStages) & 1);
-      mbar_wait(&S.full[s], (m / kStages) & 1);
-      TR(0);
-      const double* xs = reinterpret_cast<const double*>(smem + s * kXStage);
-      // row list of centroid c: quarters 0,1 (lane 2u) then 2,3 (lane 2u+1), lanes ascending
-      const unsigned ma = S.gm[s][2 * g][c], mb = S.gm[s][2 * g + 1][c];
-      const int pc = __popc(ma) + __popc(mb);
-      cnt_lane += pc;
-      const int up = __shfl_up_sync(0xffffffffu, pc, 1), dn = __shfl_down_sync(0xffffffffu, pc, 1);
-      const int before = g ? up : 0;          // rows of quarters 0,1 precede quarters 2,3
-      const int nu = g ? up + pc : pc + dn;   // rows of centroid c this tile
-      int slot = before;
-      unsigned mm = ma;
-      while (mm) {
-        const int l = __ffs(mm) - 1;
-        mm &= mm - 1;
-        if (slot < kListCap) S.list[rw][u][slot] = static_cast<unsigned char>(64 * g + l);
-        ++slot;
-      }
-      mm = mb;
-      while (mm) {
-        const int l = __ffs(mm) - 1;
-        mm &= mm - 1;
-        if (slot < kListCap) S.list[rw][u][slot] = static_cast<unsigned char>(64 * g + 32 + l);
-        ++slot;
-      }
-      const int rounds = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(nu)));
-      __syncwarp();
-      TR(1);
-      const int lim = min(rounds, kListCap);
-      for (int t4 = 0; t4 < lim; ++t4) {
-        if (t4 < nu) {
-          const double* xr = xs + S.list[rw][u][t4] * d + 32 * g;
+        for (int g = 0; g < 4; ++g) tmem_ld8(tmem + lane_base + kFoldCol + 64 * g + 8 * cc, acc[g]);
+        tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int pr = (i + u) & 15;
-            if (32 * g + 2 * pr < d) {
-              const double2 w = *reinterpret_cast<const double2*>(xr + 2 * pr);
-              acc[i][0] += w.x;
-              acc[i][1] += w.y;
-            }
-          }
+        for (int u = 0; u < 8; ++u) {
+          // planes 7-2g (half 0) or 6-2g (half 1): sum_g acc_g * 2^(8 (7 - 2g - half))
+          unsigned __int128 s = 0;
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            s += static_cast<unsigned __int128>(static_cast<uint32_t>(acc[g][u])) << (8 * (7 - 2 * g - half));
+          const int c = 8 * cc + u;
+          unsigned long long* dst = scratch + 2 * ((half * kMaxK + c) * 64 + j);
+          dst[0] = static_cast<unsigned long long>(s);
+          dst[1] = static_cast<unsigned long long>(s >> 64);
         }
       }
-      if (rounds > kListCap) {  // crowded centroid: walk the quarter masks directly (same order)
-        int seen = 0;
-        for (int Qr = 0; Qr < 4; ++Qr) {
-          unsigned gg = S.gm[s][Qr][c];
-          while (gg) {
-            const int row = 32 * Qr + __ffs(gg) - 1;
-            gg &= gg - 1;
-            if (seen++ < kListCap) continue;
-            const double* xr = xs + row * d + 32 * g;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int pr = (i + u) & 15;
-              if (32 * g + 2 * pr < d) {
-                const double2 w = *reinterpret_cast<const double2*>(xr + 2 * pr);
-                acc[i][0] += w.x;
-                acc[i][1] += w.y;
-              }
-            }
-          }
-        }
-      }
-      TR(4);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.sempty[s]);
     }
-    // flush this CTA's partial activation record
-    if (c < k) {
-      double* ps = part_sums + static_cast<size_t>(blockIdx.x) * k * d + static_cast<size_t>(c) * d;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int col = 32 * g + 2 * ((i + u) & 15);
-        if (col < d) ps[col] = acc[i][0];
-        if (col + 1 < d) ps[col + 1] = acc[i][1];
+    tc_fence_before();
+    named_bar(1, 128);
+    {
+      const int et = S.em + 1;
+      const double unit = ldexp(1.0, et - 62);
+      const unsigned __int128 off = (static_cast<unsigned __int128>(1) << 63) + (static_cast<unsigned __int128>(1) << 39);
+      double* ps = part_sums + static_cast<size_t>(blockIdx.x) * k * d;
+      for (int e = q; e < kMaxK * 64; e += 128) {
+        const int c = e >> 6, j = e & 63;
+        if (c >= k || j >= d) continue;
+        const unsigned long long* s0 = scratch + 2 * (c * 64 + j);
+        const unsigned long long* s1 = scratch + 2 * ((kMaxK + c) * 64 + j);
+        const unsigned __int128 hi = (static_cast<unsigned __int128>(s0[1]) << 64) | s0[0];
+        const unsigned __int128 lo = (static_cast<unsigned __int128>(s1[1]) << 64) | s1[0];
+        const __int128 tot = static_cast<__int128>(hi + lo - static_cast<unsigned __int128>(S.cnt[c]) * off);
+        const long long th = static_cast<long long>(tot >> 64);
+        const unsigned long long tl = static_cast<unsigned long long>(tot);
+        const double v = __fma_rn(static_cast<double>(th), 18446744073709551616.0, static_cast<double>(tl));
+        ps[c * d + j] = v * unit;
       }
+      for (int c = q; c < k; c += 128) part_counts[static_cast<size_t>(blockIdx.x) * k + c] = S.cnt[c];
     }
-    const long long ct = cnt_lane + __shfl_xor_sync(0xffffffffu, cnt_lane, 1);
-    if (g == 0 && c < k) part_counts[static_cast<size_t>(blockIdx.x) * k + c] = ct;
   }
-#ifdef DLX_KMEANS_TRACE
-  if (trace && lane == 0 &&
-      (warp == kWarpProd || warp == kWarpMma || warp == kWarpC0 || warp == kWarpE0 || warp == kWarpR0)) {
-    const int role = warp == kWarpProd ? 0 : warp == kWarpMma ? 1 : warp == kWarpC0 ? 2 : warp == kWarpE0 ? 3 : 4;
-    for (int i = 0; i < 8; ++i) trace[(static_cast<size_t>(blockIdx.x) * 5 + role) * 8 + i] = tr[i];
-  }
-#endif
-#undef TR
   __syncthreads();
   if (warp == kWarpMma) {
     tc_fence_after();
@@ -719,6 +789,10 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
               sk::kMaxD, sk::kMaxK, d, k);
   DLX_REQUIRE((reinterpret_cast<uintptr_t>(x) & 15) == 0, DLX_ERR_GENERATION,
               "GenerationFailed: screened k-means needs 16-byte aligned samples");
+  // the fold accumulators hold <= 128*255 per tile in int32: at most 65,793 tiles per CTA
+  DLX_REQUIRE(n <= (static_cast<int64_t>(60000) * sk::kTile) * sm_count(), DLX_ERR_GENERATION,
+              "GenerationFailed: screened k-means takes at most %lld samples per launch",
+              static_cast<long long>(60000) * sk::kTile * sm_count());
   if (probe_only) return DLX_OK;
   const int grid = screened_grid(n);
   const long long cap = pend_capacity(n, grid);
@@ -728,28 +802,9 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
   DLX_CUDA(cudaFuncSetAttribute(sk::kmeans_screened_kernel,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sk::kSmemBytes)));
-  static const bool tracing = getenv("DLX_KMEANS_TRACE") != nullptr;
-  long long* trace = nullptr;
-  if (tracing) DLX_CUDA(cudaMalloc(&trace, sizeof(long long) * grid * 40));
   sk::kmeans_screened_kernel<<<grid, sk::kThreads, sk::kSmemBytes, stream>>>(
-      x, n, d, k, mu, assign, w.part_counts, w.part_sums, w.pend_idx, w.pend_mask, w.pend_count, cap,
-      trace);
+      x, n, d, k, mu, assign, w.part_counts, w.part_sums, w.pend_idx, w.pend_mask, w.pend_count, cap);
   DLX_LAUNCHED("kmeans_screened_kernel");
-  if (tracing) {  // debug only: per-role cycle split averaged over CTAs
-    std::vector<long long> h(static_cast<size_t>(grid) * 40);
-    DLX_CUDA(cudaStreamSynchronize(stream));
-    DLX_CUDA(cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
-    cudaFree(trace);
-    const char* names[5] = {"producer", "mma", "convert", "epilogue", "fold"};
-    for (int r = 0; r < 5; ++r) {
-      double avg[8] = {0};
-      for (int b = 0; b < grid; ++b)
-        for (int i = 0; i < 8; ++i) avg[i] += static_cast<double>(h[(static_cast<size_t>(b) * 5 + r) * 8 + i]) / grid;
-      fprintf(stderr, "[dlx trace] %-9s", names[r]);
-      for (int i = 0; i < 8; ++i) fprintf(stderr, " %10.0f", avg[i]);
-      fprintf(stderr, "\n");
-    }
-  }
   const size_t rsmem =
       (static_cast<size_t>(2 * k + sk::kResChunk) * d + sk::kResMaxPairs) * sizeof(double);
   DLX_CUDA(cudaFuncSetAttribute(sk::kmeans_resolve_kernel,

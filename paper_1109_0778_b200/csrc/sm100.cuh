@@ -52,6 +52,11 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, u
       : "memory");
 }
 
+// bulk prefetch of a global range into L2 (no completion tracking; a hint the TMA unit honours)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* gmem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem_src), "r"(bytes) : "memory");
+}
+
 // generic-proxy smem writes -> visible to the async proxy (tensor core operand reads)
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -155,6 +160,15 @@ __host__ __device__ constexpr uint32_t idesc_i8(int m, int n, int a_signed, int 
   return (2u << 4) | (static_cast<uint32_t>(a_signed) << 7) |
          (static_cast<uint32_t>(b_signed) << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
          (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+// Same, with the operand majors: a_mn / b_mn = 1 selects MN-major (valid for 8-bit integers).
+// An MN-major SW128 operand whose M extent is exactly 128 bytes has the same bytes as a K-major
+// SW128 operand with 128-byte rows: row = K index, the 128 bytes = M (8-row atoms, SBO 1024).
+__host__ __device__ constexpr uint32_t idesc_i8_major(int m, int n, int a_signed, int b_signed,
+                                                      int a_mn, int b_mn) {
+  return idesc_i8(m, n, a_signed, b_signed) | (static_cast<uint32_t>(a_mn) << 15) |
+         (static_cast<uint32_t>(b_mn) << 16);
 }
 
 // byte offset of (row, byte k) inside a K-major SWIZZLE_128B operand with 128-byte rows
