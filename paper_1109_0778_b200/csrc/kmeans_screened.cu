@@ -170,6 +170,7 @@ __device__ __forceinline__ int elem_flag(double x, uint32_t hw_hi, uint32_t hw_l
   return (hw >= hw_hi ? 1 : 0) | ((hw < hw_lo && (hw | lw) != 0u) ? 2 : 0);
 }
 
+template <bool kWide>
 __global__ void __launch_bounds__(kThreads, 1)
 kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
                        const double* __restrict__ mu, int32_t* __restrict__ assign,
@@ -350,75 +351,64 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     const int hl = lane >> 4, p = lane & 15;
     const int col0 = 4 * p;
     const int nvalid = col0 + 4 <= d ? 4 : (col0 + 2 <= d ? 2 : 0);
-    const bool wide = ((d & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 31) == 0);
+    // load column of this lane (clamped into the row) and the offset of its second pair
+    const int lcol = nvalid ? col0 : 0;
+    const int lcol2 = nvalid == 4 ? 2 : 0;
     const uint32_t chunk0 = static_cast<uint32_t>((p >> 2) ^ (4 * hl));
-    double v[8][4];
-    auto load_tile = [&](int mm) {
-      const int64_t t = blockIdx.x + static_cast<int64_t>(mm) * gridDim.x;
-      const int64_t rows = n - t * kTile;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int row = 16 * cw + 8 * (i >> 2) + (i & 3) + 4 * hl;
-        v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0.0;
-        if (row < rows && nvalid) {
-          const double* src = x + (t * kTile + row) * d + col0;
-          if (wide) {
-            ldg256(src, v[i][0], v[i][1], v[i][2], v[i][3]);
-          } else {
-            ldg128(src, v[i][0], v[i][1]);
-            if (nvalid == 4) ldg128(src + 2, v[i][2], v[i][3]);
-          }
-        }
+    // rolling 4-pair register buffer: slot i & 3 holds pair i while it is converted, then
+    // receives pair i + 4 (half a tile of lookahead; the L2 prefetch covers HBM latency)
+    double v[4][4];
+    auto tile_of = [&](int mm) { return static_cast<int64_t>(blockIdx.x) + static_cast<int64_t>(mm) * gridDim.x; };
+    // unconditional, branch-free loads (clamped to valid addresses) so the loaded registers
+    // need no phi copies, which would wait on the load right after issuing it
+    auto load_pair = [&](int mm, int i, double (&dst)[4]) {
+      const int64_t t = tile_of(mm);
+      const int64_t rows = n - t * kTile;   // >= 1
+      int row = 16 * cw + 8 * (i >> 2) + (i & 3) + 4 * hl;
+      row = row < rows ? row : static_cast<int>(rows - 1);   // padding rows repeat a real row
+      const double* src = x + (t * kTile + row) * d + lcol;
+      if constexpr (kWide) {
+        ldg256(src, dst[0], dst[1], dst[2], dst[3]);
+      } else {
+        ldg128(src, dst[0], dst[1]);
+        ldg128(src + lcol2, dst[2], dst[3]);
       }
     };
+    auto prefetch = [&](int mm) {
+      const int64_t t = tile_of(mm);
+      const int64_t rows = n - t * kTile < kTile ? n - t * kTile : kTile;
+      bulk_prefetch_l2(x + t * kTile * d, static_cast<uint32_t>(rows * d * 8));
+    };
     if (cw == 0 && lane == 0)
-      for (int mm = 1; mm < kPf && mm < mtiles; ++mm) {
-        const int64_t t = blockIdx.x + static_cast<int64_t>(mm) * gridDim.x;
-        const int64_t rows = n - t * kTile < kTile ? n - t * kTile : kTile;
-        bulk_prefetch_l2(x + t * kTile * d, static_cast<uint32_t>(rows * d * 8));
-      }
-    if (mtiles > 0) load_tile(0);
+      for (int mm = 1; mm < kPf && mm < mtiles; ++mm) prefetch(mm);
+    if (mtiles > 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) load_pair(0, i, v[i]);
+    }
     for (int m = 0; m < mtiles; ++m) {
       const int b = m % kNumA;
-      if (cw == 0 && lane == 0 && m + kPf < mtiles) {
-        const int64_t t = blockIdx.x + static_cast<int64_t>(m + kPf) * gridDim.x;
-        const int64_t rows = n - t * kTile < kTile ? n - t * kTile : kTile;
-        bulk_prefetch_l2(x + t * kTile * d, static_cast<uint32_t>(rows * d * 8));
-      }
-      // row flags: a cheap conservative test over the lane's 32 values; only if some lane
-      // sees a value outside [2^(e_t-30), 2^e_t) (zeros included) classify row by row
+      if (cw == 0 && lane == 0 && m + kPf < mtiles) prefetch(m + kPf);
+      if (m >= kNumA) mbar_wait(&S.a_empty[b], ((m / kNumA) - 1) & 1);
+      unsigned char* Ab = smem + kOffA + b * kABuf;
+      // conservative range test over the lane's values (exact row classification below, only
+      // if some lane saw a value outside [2^(e_t-30), 2^e_t), zeros included); columns past d
+      // hold copies and are not tested
       uint32_t mx = 0, mn = 0xffffffffu;
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint32_t hw = static_cast<uint32_t>(__double2hiint(v[i][e])) & 0x7fffffffu;
-          mx = max(mx, hw);
-          mn = min(mn, hw);
-        }
-      const bool odd = disabled || mx >= hw_hi || mn < hw_lo;
-      if (m >= kNumA) mbar_wait(&S.a_empty[b], ((m / kNumA) - 1) & 1);
-      if (__any_sync(0xffffffffu, odd)) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          int f = 0;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) f |= elem_flag(v[i][e], hw_hi, hw_lo);
-          const int f0 = static_cast<int>(__reduce_or_sync(0xffffffffu, static_cast<unsigned>(hl ? 0 : f)));
-          const int f1 = static_cast<int>(__reduce_or_sync(0xffffffffu, static_cast<unsigned>(hl ? f : 0)));
-          const int r = 16 * cw + 8 * (i >> 2) + (i & 3);
-          if (lane == 0) S.rowflag[b][r] = static_cast<unsigned char>(disabled ? 1 : (f0 & 1 ? 1 : f0));
-          if (lane == 16) S.rowflag[b][r + 4] = static_cast<unsigned char>(disabled ? 1 : (f1 & 1 ? 1 : f1));
-        }
-      } else if (lane == 0) {
-        *reinterpret_cast<uint4*>(&S.rowflag[b][16 * cw]) = make_uint4(0u, 0u, 0u, 0u);
-      }
-      unsigned char* Ab = smem + kOffA + b * kABuf;
-#pragma unroll
       for (int i = 0; i < 8; ++i) {
+        double (&w)[4] = v[i & 3];
         uint32_t H[4], L[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) zsplit(v[i][e], s_hi, H[e], L[e]);
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t hw = static_cast<uint32_t>(__double2hiint(w[e])) & 0x7fffffffu;
+          if (e < nvalid) {
+            mx = max(mx, hw);
+            mn = min(mn, hw);
+          }
+          zsplit(w[e], s_hi, H[e], L[e]);
+        }
+        if (i < 4) load_pair(m, i + 4, w);
+        else load_pair(m + 1 < mtiles ? m + 1 : m, i - 4, w);
         // 4x4 byte transposes: plane word = that byte of the four consecutive columns
         const uint32_t ha = __byte_perm(H[0], H[1], 0x5140), hb = __byte_perm(H[0], H[1], 0x7362);
         const uint32_t hc = __byte_perm(H[2], H[3], 0x5140), hd = __byte_perm(H[2], H[3], 0x7362);
@@ -438,13 +428,33 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         *reinterpret_cast<uint32_t*>(Ab + 3 * kPlane2 + off) = __byte_perm(la, lc, 0x7632);    // b1
         *reinterpret_cast<uint32_t*>(Ab + 3 * kPlane2 + off2) = __byte_perm(la, lc, 0x5410);   // b0
       }
+      const bool odd = disabled || (nvalid && (mx >= hw_hi || mn < hw_lo));
+      if (__any_sync(0xffffffffu, odd)) {
+        // rare: classify row by row, re-reading this tile's values (the registers already hold
+        // the next pairs)
+        const int64_t t = tile_of(m);
+#pragma unroll 1
+        for (int i = 0; i < 8; ++i) {
+          const int row = 16 * cw + 8 * (i >> 2) + (i & 3) + 4 * hl;
+          int f = 0;
+          if (row < n - t * kTile)
+            for (int e = 0; e < 4; ++e)
+              if (col0 + e < d) f |= elem_flag(x[(t * kTile + row) * d + col0 + e], hw_hi, hw_lo);
+          const int f0 = static_cast<int>(__reduce_or_sync(0xffffffffu, static_cast<unsigned>(hl ? 0 : f)));
+          const int f1 = static_cast<int>(__reduce_or_sync(0xffffffffu, static_cast<unsigned>(hl ? f : 0)));
+          const int r = 16 * cw + 8 * (i >> 2) + (i & 3);
+          if (lane == 0) S.rowflag[b][r] = static_cast<unsigned char>(disabled ? 1 : (f0 & 1 ? 1 : f0));
+          if (lane == 16) S.rowflag[b][r + 4] = static_cast<unsigned char>(disabled ? 1 : (f1 & 1 ? 1 : f1));
+        }
+      } else if (lane == 0) {
+        *reinterpret_cast<uint4*>(&S.rowflag[b][16 * cw]) = make_uint4(0u, 0u, 0u, 0u);
+      }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&S.a_full[b]);
         mbar_arrive(&S.c_full[b]);
       }
-      if (m + 1 < mtiles) load_tile(m + 1);
     }
   } else {
     // ======================= epilogue (4 warps, one per TMEM lane quarter) ===========
@@ -799,10 +809,12 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
   ScreenedWs w = carve_screened(ws, n, d, k, grid);
   DLX_REQUIRE(ws && w.used <= ws_bytes, DLX_ERR_ARG, "k-means workspace too small (%zu < %zu)",
               ws_bytes, w.used);
-  DLX_CUDA(cudaFuncSetAttribute(sk::kmeans_screened_kernel,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+  // 32-byte row loads when every lane's four columns are 32-byte aligned
+  const bool wide = (d % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 32 == 0);
+  auto kern = wide ? sk::kmeans_screened_kernel<true> : sk::kmeans_screened_kernel<false>;
+  DLX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sk::kSmemBytes)));
-  sk::kmeans_screened_kernel<<<grid, sk::kThreads, sk::kSmemBytes, stream>>>(
+  kern<<<grid, sk::kThreads, sk::kSmemBytes, stream>>>(
       x, n, d, k, mu, assign, w.part_counts, w.part_sums, w.pend_idx, w.pend_mask, w.pend_count, cap);
   DLX_LAUNCHED("kmeans_screened_kernel");
   const size_t rsmem =
