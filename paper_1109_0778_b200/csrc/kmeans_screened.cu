@@ -82,9 +82,11 @@ constexpr int kMaxD = 64;
 constexpr int kMaxK = 64;
 constexpr int kNumC = 8;     // converter warps (16 rows of every tile each)
 constexpr int kNumA = 3;     // plane buffers in flight
-constexpr int kWarpMma = 0, kWarpC0 = 1, kWarpE0 = kWarpC0 + kNumC;
-constexpr int kThreads = (kWarpE0 + 4) * 32;              // 416
-constexpr int kPf = 3;                                    // L2 prefetch distance (tiles)
+// warp 0 issues the screen MMAs, warp 1 the fold MMAs (each sleeps on its own barriers)
+constexpr int kWarpMma = 0, kWarpFold = 1, kWarpC0 = 2, kWarpE0 = kWarpC0 + kNumC;
+constexpr int kThreads = (kWarpE0 + 4) * 32;              // 448
+constexpr int kZConv = 2;                                 // 1: fp64 magic-number split, 2: F2I.S64
+constexpr int kPfDefault = 0;                             // L2 prefetch distance (tiles)
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kFoldCol = 256;                        // fold accumulators: columns 256..511
 constexpr uint32_t kPlane2 = kTile * 128;                 // one [b_hi|b_lo] SW128 buffer, 16 KiB
@@ -117,6 +119,7 @@ struct Misc {
 };
 constexpr uint32_t kSmemBytes = kOffMisc + sizeof(Misc);
 static_assert(kSmemBytes <= 232448, "shared-memory plan exceeds 227 KiB");
+constexpr int kTraceTiles = 64;
 constexpr int kInvalidNm = 0x70000000;  // > any valid score (|T| < 1.4e9)
 constexpr int kNoCandidate = 0x60000000;
 
@@ -170,13 +173,21 @@ __device__ __forceinline__ int elem_flag(double x, uint32_t hw_hi, uint32_t hw_l
   return (hw >= hw_hi ? 1 : 0) | ((hw < hw_lo && (hw | lw) != 0u) ? 2 : 0);
 }
 
-template <bool kWide>
+template <int kD, bool kWide>
 __global__ void __launch_bounds__(kThreads, 1)
 kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
                        const double* __restrict__ mu, int32_t* __restrict__ assign,
                        long long* __restrict__ part_counts, double* __restrict__ part_sums,
                        long long* __restrict__ pend_idx, unsigned long long* __restrict__ pend_mask,
-                       long long* __restrict__ pend_count, long long pend_cap) {
+                       long long* __restrict__ pend_count, long long pend_cap,
+                       long long* __restrict__ trace, int kPf) {
+  // optional per-tile event clocks (build with -DDLX_KMEANS_TRACE, run with DLX_KMEANS_TRACE=1):
+  // trace[(cta * kTraceTiles + m) * 8 + event]
+#ifdef DLX_KMEANS_TRACE
+#define TRACE_EV(m, ev) do { if (trace && (m) < kTraceTiles) trace[(static_cast<size_t>(blockIdx.x) * kTraceTiles + (m)) * 16 + (ev)] = clock64(); } while (0)
+#else
+#define TRACE_EV(m, ev) do { } while (0)
+#endif
   extern __shared__ __align__(1024) unsigned char smem[];
   Misc& S = *reinterpret_cast<Misc*>(smem + kOffMisc);
   unsigned char* B1 = smem + kOffB1;
@@ -275,62 +286,61 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
   const uint32_t tmem = S.tmem_base;
 
   if (warp == kWarpMma) {
-    // ======================= MMA issuer =======================
-    // Polls both kinds of work so neither waits behind the other: the screen of the next
-    // converted tile (its planes ready and the screen columns released by the epilogue) and
-    // the fold of the oldest screened tile whose one-hot rows are written.
+    // ======================= screen MMA issuer =======================
     if (lane == 0) {
       constexpr uint32_t ID_us = idesc_i8(kTile, 64, 0, 1);   // u8 sample plane x s8 h'
       constexpr uint32_t ID_uu = idesc_i8(kTile, 64, 0, 0);
-      constexpr uint32_t ID_fold = idesc_i8_major(kTile, 64, 0, 0, 1, 1);
       const uint32_t b1 = smem_addr(B1), b2 = smem_addr(B2);
       const int nk = (d + 31) / 32;
-      int ns = 0, nf = 0;
-      while (nf < mtiles) {
-        bool progress = false;
-        if (ns < mtiles && mbar_test(&S.a_full[ns % kNumA], (ns / kNumA) & 1) &&
-            (ns == 0 || mbar_test(&S.t_empty, (ns - 1) & 1))) {
-          tc_fence_after();
-          const uint32_t a0 = smem_addr(smem + kOffA + (ns % kNumA) * kABuf);
-          for (int kk = 0; kk < nk; ++kk) {
-            const uint64_t xh = sw128_kmajor_desc(a0 + 32 * kk);             // b7 = h''
-            const uint64_t xl = sw128_kmajor_desc(a0 + 64 + 32 * kk);        // b6 = l
-            const uint64_t xf = sw128_kmajor_desc(a0 + kPlane2 + 32 * kk);   // b5 = F
-            const uint64_t mh = sw128_kmajor_desc(b1 + 32 * kk), ml = sw128_kmajor_desc(b1 + 64 + 32 * kk);
-            const uint64_t mg = sw64_kmajor_desc(b2 + 32 * kk);
-            const uint32_t acc = kk > 0;
-            mma_i8(tmem + 0, xh, mh, ID_us, acc);      // HH
-            mma_i8(tmem + 64, xh, ml, ID_uu, acc);     // CR = h'' l' + l h'
-            mma_i8(tmem + 64, xl, mh, ID_us, 1);
-            mma_i8(tmem + 128, xh, mg, ID_uu, acc);    // W1 = h'' G + F h' + l l'
-            mma_i8(tmem + 128, xf, mh, ID_us, 1);
-            mma_i8(tmem + 128, xl, ml, ID_uu, 1);
-            mma_i8(tmem + 192, xl, mg, ID_uu, acc);    // W2 = l G + F l'
-            mma_i8(tmem + 192, xf, ml, ID_uu, 1);
-          }
-          mma_commit(&S.t_full);
-          ++ns;
-          progress = true;
+      for (int ns = 0; ns < mtiles; ++ns) {
+        mbar_wait(&S.a_full[ns % kNumA], (ns / kNumA) & 1);
+        TRACE_EV(ns, 8);
+        if (ns >= 1) mbar_wait(&S.t_empty, (ns - 1) & 1);
+        TRACE_EV(ns, 9);
+        tc_fence_after();
+        const uint32_t a0 = smem_addr(smem + kOffA + (ns % kNumA) * kABuf);
+        for (int kk = 0; kk < nk; ++kk) {
+          const uint64_t xh = sw128_kmajor_desc(a0 + 32 * kk);             // b7 = h''
+          const uint64_t xl = sw128_kmajor_desc(a0 + 64 + 32 * kk);        // b6 = l
+          const uint64_t xf = sw128_kmajor_desc(a0 + kPlane2 + 32 * kk);   // b5 = F
+          const uint64_t mh = sw128_kmajor_desc(b1 + 32 * kk), ml = sw128_kmajor_desc(b1 + 64 + 32 * kk);
+          const uint64_t mg = sw64_kmajor_desc(b2 + 32 * kk);
+          const uint32_t acc = kk > 0;
+          mma_i8(tmem + 0, xh, mh, ID_us, acc);      // HH
+          mma_i8(tmem + 64, xh, ml, ID_uu, acc);     // CR = h'' l' + l h'
+          mma_i8(tmem + 64, xl, mh, ID_us, 1);
+          mma_i8(tmem + 128, xh, mg, ID_uu, acc);    // W1 = h'' G + F h' + l l'
+          mma_i8(tmem + 128, xf, mh, ID_us, 1);
+          mma_i8(tmem + 128, xl, ml, ID_uu, 1);
+          mma_i8(tmem + 192, xl, mg, ID_uu, acc);    // W2 = l G + F l'
+          mma_i8(tmem + 192, xf, ml, ID_uu, 1);
         }
-        if (nf < ns && mbar_test(&S.oh_full[nf & 1], (nf >> 1) & 1)) {
-          tc_fence_after();
-          const uint32_t a0 = smem_addr(smem + kOffA + (nf % kNumA) * kABuf);
-          const uint32_t oh = smem_addr(smem + kOffOH + (nf & 1) * kOHBuf);
+        mma_commit(&S.t_full);
+        TRACE_EV(ns, 0);
+      }
+    }
+  } else if (warp == kWarpFold) {
+    // ======================= fold MMA issuer =======================
+    if (lane == 0) {
+      constexpr uint32_t ID_fold = idesc_i8_major(kTile, 64, 0, 0, 1, 1);
+      for (int nf = 0; nf < mtiles; ++nf) {
+        mbar_wait(&S.oh_full[nf & 1], (nf >> 1) & 1);
+        TRACE_EV(nf, 13);
+        tc_fence_after();
+        const uint32_t a0 = smem_addr(smem + kOffA + (nf % kNumA) * kABuf);
+        const uint32_t oh = smem_addr(smem + kOffOH + (nf & 1) * kOHBuf);
 #pragma unroll
-          for (int kk = 0; kk < kTile / 32; ++kk) {
-            const uint64_t bdesc = sw64_kmajor_desc(oh + kk * 2048);   // MN-major [q][c], SW64
+        for (int kk = 0; kk < kTile / 32; ++kk) {
+          const uint64_t bdesc = sw64_kmajor_desc(oh + kk * 2048);   // MN-major [q][c], SW64
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              const uint64_t adesc = sw128_kmajor_desc(a0 + g * kPlane2 + kk * 4096);  // MN-major
-              mma_i8(tmem + kFoldCol + 64 * g, adesc, bdesc, ID_fold, (nf > 0 || kk > 0) ? 1u : 0u);
-            }
+          for (int g = 0; g < 4; ++g) {
+            const uint64_t adesc = sw128_kmajor_desc(a0 + g * kPlane2 + kk * 4096);  // MN-major
+            mma_i8(tmem + kFoldCol + 64 * g, adesc, bdesc, ID_fold, (nf > 0 || kk > 0) ? 1u : 0u);
           }
-          mma_commit(&S.a_empty[nf % kNumA]);
-          mma_commit(&S.oh_empty[nf & 1]);
-          ++nf;
-          progress = true;
         }
-        if (!progress) __nanosleep(32);
+        mma_commit(&S.a_empty[nf % kNumA]);
+        mma_commit(&S.oh_empty[nf & 1]);
+        TRACE_EV(nf, 1);
       }
       mma_commit(&S.fold_done);
     }
@@ -342,31 +352,37 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     // (64 KiB in flight per SM, on top of a bulk L2 prefetch kPf tiles ahead).  Rows r and
     // r + 4 land in disjoint bank halves, so every plane store is one wavefront.
     const int cw = warp - kWarpC0;
+    const int D = kD ? kD : d;
     const int em = S.em, disabled = S.disabled;
     const int et = em + 1;
     const double s_hi = disabled ? 0.0 : ldexp(1.0, 30 - et);
+    const double s_z = disabled ? 0.0 : ldexp(1.0, 62 - et);   // Z = floor(x * 2^(62 - e_t)), exact product
     const uint32_t hw_hi = static_cast<uint32_t>(1023 + et) << 20;          // |x| >= 2^e_t, inf, NaN
     const int lo_e = 1023 + et - kFoldBits;
     const uint32_t hw_lo = lo_e > 0 ? static_cast<uint32_t>(lo_e) << 20 : 0u;  // nonzero |x| < 2^(e_t-30)
     const int hl = lane >> 4, p = lane & 15;
     const int col0 = 4 * p;
-    const int nvalid = col0 + 4 <= d ? 4 : (col0 + 2 <= d ? 2 : 0);
+    const int nvalid = col0 + 4 <= D ? 4 : (col0 + 2 <= D ? 2 : 0);
     // load column of this lane (clamped into the row) and the offset of its second pair
     const int lcol = nvalid ? col0 : 0;
     const int lcol2 = nvalid == 4 ? 2 : 0;
-    const uint32_t chunk0 = static_cast<uint32_t>((p >> 2) ^ (4 * hl));
+    const int rbase = 16 * cw + 4 * hl;   // tile row of this lane's pair 0
+    // plane-store offsets of pair i: soff[i & 3] + (i >> 2) * 1024 (row r4 + 4 hl of atom 2 cw + (i >> 2))
+    uint32_t soff[4];
+#pragma unroll
+    for (int r4 = 0; r4 < 4; ++r4)
+      soff[r4] = static_cast<uint32_t>(2 * cw) * 1024u + static_cast<uint32_t>(r4 + 4 * hl) * 128u +
+                 (((static_cast<uint32_t>(p >> 2) ^ (4u * hl)) ^ static_cast<uint32_t>(r4)) << 4) + 4u * (p & 3);
     // rolling 4-pair register buffer: slot i & 3 holds pair i while it is converted, then
     // receives pair i + 4 (half a tile of lookahead; the L2 prefetch covers HBM latency)
     double v[4][4];
     auto tile_of = [&](int mm) { return static_cast<int64_t>(blockIdx.x) + static_cast<int64_t>(mm) * gridDim.x; };
-    // unconditional, branch-free loads (clamped to valid addresses) so the loaded registers
-    // need no phi copies, which would wait on the load right after issuing it
-    auto load_pair = [&](int mm, int i, double (&dst)[4]) {
-      const int64_t t = tile_of(mm);
-      const int64_t rows = n - t * kTile;   // >= 1
-      int row = 16 * cw + 8 * (i >> 2) + (i & 3) + 4 * hl;
-      row = row < rows ? row : static_cast<int>(rows - 1);   // padding rows repeat a real row
-      const double* src = x + (t * kTile + row) * d + lcol;
+    // unconditional loads from clamped addresses (the loaded registers need no phi copies,
+    // which would wait on a load right after issuing it)
+    auto load_pair = [&](const double* base, int64_t rows, int i, double (&dst)[4]) {
+      int off = 8 * (i >> 2) + (i & 3);
+      if (rbase + off >= rows) off = static_cast<int>(rows - 1) - rbase;   // padding rows repeat the last row
+      const double* src = base + off * D;
       if constexpr (kWide) {
         ldg256(src, dst[0], dst[1], dst[2], dst[3]);
       } else {
@@ -374,21 +390,32 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         ldg128(src + lcol2, dst[2], dst[3]);
       }
     };
+    auto base_of = [&](int mm, int64_t& rows) {
+      const int64_t t = tile_of(mm);
+      rows = n - t * kTile;
+      return x + (t * kTile + rbase) * D + lcol;
+    };
     auto prefetch = [&](int mm) {
       const int64_t t = tile_of(mm);
       const int64_t rows = n - t * kTile < kTile ? n - t * kTile : kTile;
-      bulk_prefetch_l2(x + t * kTile * d, static_cast<uint32_t>(rows * d * 8));
+      bulk_prefetch_l2(x + t * kTile * D, static_cast<uint32_t>(rows * D * 8));
     };
     if (cw == 0 && lane == 0)
       for (int mm = 1; mm < kPf && mm < mtiles; ++mm) prefetch(mm);
+    int64_t cur_rows = 0;
+    const double* cur = base_of(0, cur_rows);
     if (mtiles > 0) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) load_pair(0, i, v[i]);
+      for (int i = 0; i < 4; ++i) load_pair(cur, cur_rows, i, v[i]);
     }
     for (int m = 0; m < mtiles; ++m) {
       const int b = m % kNumA;
       if (cw == 0 && lane == 0 && m + kPf < mtiles) prefetch(m + kPf);
+      int64_t nxt_rows = 0;
+      const double* nxt = base_of(m + 1 < mtiles ? m + 1 : m, nxt_rows);
+      if (cw == 0 && lane == 0) TRACE_EV(m, 2);
       if (m >= kNumA) mbar_wait(&S.a_empty[b], ((m / kNumA) - 1) & 1);
+      if (cw == 0 && lane == 0) TRACE_EV(m, 3);
       unsigned char* Ab = smem + kOffA + b * kABuf;
       // conservative range test over the lane's values (exact row classification below, only
       // if some lane saw a value outside [2^(e_t-30), 2^e_t), zeros included); columns past d
@@ -401,34 +428,39 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const uint32_t hw = static_cast<uint32_t>(__double2hiint(w[e])) & 0x7fffffffu;
-          if (e < nvalid) {
+          if (kD == 64 || e < nvalid) {
             mx = max(mx, hw);
             mn = min(mn, hw);
           }
-          zsplit(w[e], s_hi, H[e], L[e]);
+          if (kZConv == 1) {
+            zsplit(w[e], s_hi, H[e], L[e]);
+          } else {  // one exact DMUL + F2I.S64.FLOOR; the offset 2^63 + 2^39 touches the high word only
+            const long long z = __double2ll_rd(w[e] * s_z);
+            H[e] = static_cast<uint32_t>(static_cast<unsigned long long>(z) >> 32) + 0x80000080u;
+            L[e] = static_cast<uint32_t>(z);
+          }
         }
-        if (i < 4) load_pair(m, i + 4, w);
-        else load_pair(m + 1 < mtiles ? m + 1 : m, i - 4, w);
+        if (i < 4) load_pair(cur, cur_rows, i + 4, w);
+        else load_pair(nxt, nxt_rows, i - 4, w);
         // 4x4 byte transposes: plane word = that byte of the four consecutive columns
         const uint32_t ha = __byte_perm(H[0], H[1], 0x5140), hb = __byte_perm(H[0], H[1], 0x7362);
         const uint32_t hc = __byte_perm(H[2], H[3], 0x5140), hd = __byte_perm(H[2], H[3], 0x7362);
         const uint32_t la = __byte_perm(L[0], L[1], 0x5140), lb = __byte_perm(L[0], L[1], 0x7362);
         const uint32_t lc = __byte_perm(L[2], L[3], 0x5140), ld = __byte_perm(L[2], L[3], 0x7362);
-        const int r4 = i & 3;
-        const uint32_t off = static_cast<uint32_t>(2 * cw + (i >> 2)) * 1024u +
-                             static_cast<uint32_t>(r4 + 4 * hl) * 128u +
-                             ((chunk0 ^ static_cast<uint32_t>(r4)) << 4) + 4u * (p & 3);
-        const uint32_t off2 = off ^ 64u;
-        *reinterpret_cast<uint32_t*>(Ab + off) = __byte_perm(hb, hd, 0x7632);                  // b7
-        *reinterpret_cast<uint32_t*>(Ab + off2) = __byte_perm(hb, hd, 0x5410);                 // b6
-        *reinterpret_cast<uint32_t*>(Ab + kPlane2 + off) = __byte_perm(ha, hc, 0x7632);        // b5
-        *reinterpret_cast<uint32_t*>(Ab + kPlane2 + off2) = __byte_perm(ha, hc, 0x5410);       // b4
-        *reinterpret_cast<uint32_t*>(Ab + 2 * kPlane2 + off) = __byte_perm(lb, ld, 0x7632);    // b3
-        *reinterpret_cast<uint32_t*>(Ab + 2 * kPlane2 + off2) = __byte_perm(lb, ld, 0x5410);   // b2
-        *reinterpret_cast<uint32_t*>(Ab + 3 * kPlane2 + off) = __byte_perm(la, lc, 0x7632);    // b1
-        *reinterpret_cast<uint32_t*>(Ab + 3 * kPlane2 + off2) = __byte_perm(la, lc, 0x5410);   // b0
+        unsigned char* A0 = Ab + soff[i & 3] + (i >> 2) * 1024;
+        unsigned char* A1 = Ab + (soff[i & 3] ^ 64u) + (i >> 2) * 1024;
+        *reinterpret_cast<uint32_t*>(A0) = __byte_perm(hb, hd, 0x7632);                  // b7
+        *reinterpret_cast<uint32_t*>(A1) = __byte_perm(hb, hd, 0x5410);                  // b6
+        *reinterpret_cast<uint32_t*>(A0 + kPlane2) = __byte_perm(ha, hc, 0x7632);        // b5
+        *reinterpret_cast<uint32_t*>(A1 + kPlane2) = __byte_perm(ha, hc, 0x5410);        // b4
+        *reinterpret_cast<uint32_t*>(A0 + 2 * kPlane2) = __byte_perm(lb, ld, 0x7632);    // b3
+        *reinterpret_cast<uint32_t*>(A1 + 2 * kPlane2) = __byte_perm(lb, ld, 0x5410);    // b2
+        *reinterpret_cast<uint32_t*>(A0 + 3 * kPlane2) = __byte_perm(la, lc, 0x7632);    // b1
+        *reinterpret_cast<uint32_t*>(A1 + 3 * kPlane2) = __byte_perm(la, lc, 0x5410);    // b0
       }
-      const bool odd = disabled || (nvalid && (mx >= hw_hi || mn < hw_lo));
+      cur = nxt;
+      cur_rows = nxt_rows;
+      const bool odd = disabled || ((kD == 64 || nvalid) && (mx >= hw_hi || mn < hw_lo));
       if (__any_sync(0xffffffffu, odd)) {
         // rare: classify row by row, re-reading this tile's values (the registers already hold
         // the next pairs)
@@ -453,6 +485,9 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&S.a_full[b]);
+        if (cw == 0) TRACE_EV(m, 4);
+        if (cw == 7) TRACE_EV(m, 10);
+        if (cw == 3) TRACE_EV(m, 11);
         mbar_arrive(&S.c_full[b]);
       }
     }
@@ -473,7 +508,9 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
       const int b = m & 1;
       const int rows = static_cast<int>(n - t * kTile < kTile ? n - t * kTile : kTile);
+      if (quarter == 0 && lane == 0) TRACE_EV(m, 5);
       mbar_wait(&S.t_full, m & 1);
+      if (quarter == 0 && lane == 0) TRACE_EV(m, 6);
       tc_fence_after();
       int tv[64];
       int lmin = kInvalidNm;
@@ -500,6 +537,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.t_empty);
+      if (quarter == 0 && lane == 0) TRACE_EV(m, 12);
       const int b3 = m % kNumA;
       mbar_wait(&S.c_full[b3], (m / kNumA) & 1);
       unsigned long long full = 0;
@@ -553,6 +591,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.oh_full[b]);
+      if (quarter == 0 && lane == 0) TRACE_EV(m, 7);
       // deterministic pending-list append, ordered by sample row
       const unsigned pb = __ballot_sync(0xffffffffu, pend);
       if (lane == 0) S.pcount[m & 1][quarter] = __popc(pb);
@@ -809,14 +848,48 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
   ScreenedWs w = carve_screened(ws, n, d, k, grid);
   DLX_REQUIRE(ws && w.used <= ws_bytes, DLX_ERR_ARG, "k-means workspace too small (%zu < %zu)",
               ws_bytes, w.used);
+  static const bool tracing = getenv("DLX_KMEANS_TRACE") != nullptr;
+  static const int pf = getenv("DLX_KMEANS_PF") ? atoi(getenv("DLX_KMEANS_PF")) : sk::kPfDefault;
+  long long* trace = nullptr;
+  if (tracing) {
+    DLX_CUDA(cudaMalloc(&trace, sizeof(long long) * grid * sk::kTraceTiles * 16));
+    DLX_CUDA(cudaMemsetAsync(trace, 0, sizeof(long long) * grid * sk::kTraceTiles * 16, stream));
+  }
   // 32-byte row loads when every lane's four columns are 32-byte aligned
   const bool wide = (d % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 32 == 0);
-  auto kern = wide ? sk::kmeans_screened_kernel<true> : sk::kmeans_screened_kernel<false>;
+  auto kern = !wide ? sk::kmeans_screened_kernel<0, false>
+                    : (d == 64 ? sk::kmeans_screened_kernel<64, true> : sk::kmeans_screened_kernel<0, true>);
   DLX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sk::kSmemBytes)));
   kern<<<grid, sk::kThreads, sk::kSmemBytes, stream>>>(
-      x, n, d, k, mu, assign, w.part_counts, w.part_sums, w.pend_idx, w.pend_mask, w.pend_count, cap);
+      x, n, d, k, mu, assign, w.part_counts, w.part_sums, w.pend_idx, w.pend_mask, w.pend_count, cap,
+      trace, pf);
   DLX_LAUNCHED("kmeans_screened_kernel");
+  if (trace) {  // debug only: mean event offsets (cycles) relative to the converter's tile start
+    std::vector<long long> h(static_cast<size_t>(grid) * sk::kTraceTiles * 16);
+    DLX_CUDA(cudaStreamSynchronize(stream));
+    DLX_CUDA(cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+    cudaFree(trace);
+    const char* names[14] = {"screen_issued", "fold_issued", "conv_begin", "conv_got_buf", "conv_done",
+                             "epi_begin", "epi_got_tfull", "epi_oh_done", "scr_got_afull", "scr_got_tempty",
+                             "conv7_done", "conv3_done", "epi_tmem_drained", "fold_got_oh"};
+    double avg[14] = {0}, per_tile = 0;
+    long cnt = 0;
+    for (int b = 0; b < grid; ++b)
+      for (int m = 8; m < sk::kTraceTiles - 1; ++m) {
+        const long long* r = &h[(static_cast<size_t>(b) * sk::kTraceTiles + m) * 16];
+        const long long* r1 = r + 16;
+        if (r[2] == 0 || r1[2] == 0) continue;
+        for (int e = 0; e < 14; ++e) avg[e] += static_cast<double>(r[e] - r[2]);
+        per_tile += static_cast<double>(r1[2] - r[2]);
+        ++cnt;
+      }
+    if (cnt) {
+      fprintf(stderr, "[dlx trace] tile period %.0f cycles;", per_tile / cnt);
+      for (int e = 0; e < 14; ++e) fprintf(stderr, " %s %+.0f", names[e], avg[e] / cnt);
+      fprintf(stderr, "\n");
+    }
+  }
   const size_t rsmem =
       (static_cast<size_t>(2 * k + sk::kResChunk) * d + sk::kResMaxPairs) * sizeof(double);
   DLX_CUDA(cudaFuncSetAttribute(sk::kmeans_resolve_kernel,
