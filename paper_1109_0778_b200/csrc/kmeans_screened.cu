@@ -80,11 +80,20 @@ using namespace sm100;
 constexpr int kTile = 128;   // samples per tile = MMA M
 constexpr int kMaxD = 64;
 constexpr int kMaxK = 64;
-constexpr int kNumC = 8;     // converter warps (16 rows of every tile each)
+constexpr int kNumC = 16;    // converter warps (8 rows = 4 row pairs of every tile each)
+constexpr int kConvRows = kTile / kNumC;
+constexpr int kPairs = kConvRows / 2;                      // row pairs per converter warp per tile
+constexpr int kBuf = kPairs < 4 ? kPairs : 4;             // rolling register buffer (pairs)
 constexpr int kNumA = 3;     // plane buffers in flight
 // warp 0 issues the screen MMAs, warp 1 the fold MMAs (each sleeps on its own barriers)
-constexpr int kWarpMma = 0, kWarpFold = 1, kWarpC0 = 2, kWarpE0 = kWarpC0 + kNumC;
-constexpr int kThreads = (kWarpE0 + 4) * 32;              // 448
+// warpgroup 0: warp 0 screen MMAs, warp 1 fold MMAs (warps 2-3 idle); warpgroup 1: epilogue;
+// warpgroups 2-5: converters.  Registers: 80 at launch; warpgroup 0 gives 48 per thread back
+// (setmaxnreg.dec 32) and the epilogue takes them (setmaxnreg.inc 128).
+constexpr int kWarpMma = 0, kWarpFold = 1, kWarpE0 = 4, kWarpC0 = 8;
+constexpr int kThreads = (kWarpC0 + kNumC) * 32;          // 768
+constexpr int kRegsLaunch = 80, kRegsIssuer = 32, kRegsEpi = 128;
+static_assert(kThreads * kRegsLaunch <= 65536 && 128 * (kRegsLaunch - kRegsIssuer) >= 128 * (kRegsEpi - kRegsLaunch),
+              "register plan");
 constexpr int kZConv = 2;                                 // 1: fp64 magic-number split, 2: F2I.S64
 constexpr int kPfDefault = 0;                             // L2 prefetch distance (tiles)
 constexpr uint32_t kTmemCols = 512;
@@ -285,6 +294,8 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
 
+  if (warp < kWarpE0) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsIssuer));
   if (warp == kWarpMma) {
     // ======================= screen MMA issuer =======================
     if (lane == 0) {
@@ -344,13 +355,14 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       }
       mma_commit(&S.fold_done);
     }
-  } else if (warp < kWarpE0) {
-    // ======================= converters (8 warps) =======================
-    // Warp cw owns rows 16 cw .. 16 cw + 15 of every tile as eight row pairs (r, r + 4) of an
+  }
+  } else if (warp >= kWarpC0) {
+    // ======================= converters (16 warps) =======================
+    // Warp cw owns rows kConvRows*cw .. +kConvRows-1 of every tile as row pairs (r, r + 4) of an
     // 8-row SW128 atom.  Lane (hl, p) = (lane >> 4, lane & 15) holds columns 4p .. 4p+3 of row
-    // r + 4 hl: one coalesced 32-byte load per pair, issued a whole tile ahead into registers
-    // (64 KiB in flight per SM, on top of a bulk L2 prefetch kPf tiles ahead).  Rows r and
-    // r + 4 land in disjoint bank halves, so every plane store is one wavefront.
+    // r + 4 hl: one coalesced 32-byte load per pair, issued kBuf pairs ahead into a rolling
+    // register buffer (with kPairs = kBuf = 4: a whole tile ahead).  Rows r and r + 4 land in
+    // disjoint bank halves, so every plane store is one wavefront.
     const int cw = warp - kWarpC0;
     const int D = kD ? kD : d;
     const int em = S.em, disabled = S.disabled;
@@ -366,21 +378,20 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     // load column of this lane (clamped into the row) and the offset of its second pair
     const int lcol = nvalid ? col0 : 0;
     const int lcol2 = nvalid == 4 ? 2 : 0;
-    const int rbase = 16 * cw + 4 * hl;   // tile row of this lane's pair 0
-    // plane-store offsets of pair i: soff[i & 3] + (i >> 2) * 1024 (row r4 + 4 hl of atom 2 cw + (i >> 2))
+    const int rbase = kConvRows * cw + 4 * hl;   // tile row of this lane's pair 0
+    auto pair_row = [](int i) { return 8 * (i >> 2) + (i & 3); };   // row offset of pair i
+    // plane-store offset of pair i: soff[i & 3] + (i >> 2) * 1024
     uint32_t soff[4];
 #pragma unroll
     for (int r4 = 0; r4 < 4; ++r4)
-      soff[r4] = static_cast<uint32_t>(2 * cw) * 1024u + static_cast<uint32_t>(r4 + 4 * hl) * 128u +
+      soff[r4] = static_cast<uint32_t>(kConvRows / 8 * cw) * 1024u + static_cast<uint32_t>(r4 + 4 * hl) * 128u +
                  (((static_cast<uint32_t>(p >> 2) ^ (4u * hl)) ^ static_cast<uint32_t>(r4)) << 4) + 4u * (p & 3);
-    // rolling 4-pair register buffer: slot i & 3 holds pair i while it is converted, then
-    // receives pair i + 4 (half a tile of lookahead; the L2 prefetch covers HBM latency)
-    double v[4][4];
+    double v[kBuf][4];
     auto tile_of = [&](int mm) { return static_cast<int64_t>(blockIdx.x) + static_cast<int64_t>(mm) * gridDim.x; };
     // unconditional loads from clamped addresses (the loaded registers need no phi copies,
     // which would wait on a load right after issuing it)
     auto load_pair = [&](const double* base, int64_t rows, int i, double (&dst)[4]) {
-      int off = 8 * (i >> 2) + (i & 3);
+      int off = pair_row(i);
       if (rbase + off >= rows) off = static_cast<int>(rows - 1) - rbase;   // padding rows repeat the last row
       const double* src = base + off * D;
       if constexpr (kWide) {
@@ -406,7 +417,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     const double* cur = base_of(0, cur_rows);
     if (mtiles > 0) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) load_pair(cur, cur_rows, i, v[i]);
+      for (int i = 0; i < kBuf; ++i) load_pair(cur, cur_rows, i, v[i]);
     }
     for (int m = 0; m < mtiles; ++m) {
       const int b = m % kNumA;
@@ -422,8 +433,8 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       // hold copies and are not tested
       uint32_t mx = 0, mn = 0xffffffffu;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        double (&w)[4] = v[i & 3];
+      for (int i = 0; i < kPairs; ++i) {
+        double (&w)[4] = v[i % kBuf];
         uint32_t H[4], L[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -440,8 +451,8 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
             L[e] = static_cast<uint32_t>(z);
           }
         }
-        if (i < 4) load_pair(cur, cur_rows, i + 4, w);
-        else load_pair(nxt, nxt_rows, i - 4, w);
+        if (i + kBuf < kPairs) load_pair(cur, cur_rows, i + kBuf, w);
+        else load_pair(nxt, nxt_rows, i + kBuf - kPairs, w);
         // 4x4 byte transposes: plane word = that byte of the four consecutive columns
         const uint32_t ha = __byte_perm(H[0], H[1], 0x5140), hb = __byte_perm(H[0], H[1], 0x7362);
         const uint32_t hc = __byte_perm(H[2], H[3], 0x5140), hd = __byte_perm(H[2], H[3], 0x7362);
@@ -466,32 +477,37 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         // the next pairs)
         const int64_t t = tile_of(m);
 #pragma unroll 1
-        for (int i = 0; i < 8; ++i) {
-          const int row = 16 * cw + 8 * (i >> 2) + (i & 3) + 4 * hl;
+        for (int i = 0; i < kPairs; ++i) {
+          const int row = rbase + pair_row(i);
           int f = 0;
           if (row < n - t * kTile)
             for (int e = 0; e < 4; ++e)
               if (col0 + e < d) f |= elem_flag(x[(t * kTile + row) * d + col0 + e], hw_hi, hw_lo);
           const int f0 = static_cast<int>(__reduce_or_sync(0xffffffffu, static_cast<unsigned>(hl ? 0 : f)));
           const int f1 = static_cast<int>(__reduce_or_sync(0xffffffffu, static_cast<unsigned>(hl ? f : 0)));
-          const int r = 16 * cw + 8 * (i >> 2) + (i & 3);
+          const int r = kConvRows * cw + pair_row(i);
           if (lane == 0) S.rowflag[b][r] = static_cast<unsigned char>(disabled ? 1 : (f0 & 1 ? 1 : f0));
           if (lane == 16) S.rowflag[b][r + 4] = static_cast<unsigned char>(disabled ? 1 : (f1 & 1 ? 1 : f1));
         }
       } else if (lane == 0) {
-        *reinterpret_cast<uint4*>(&S.rowflag[b][16 * cw]) = make_uint4(0u, 0u, 0u, 0u);
+        static_assert(kConvRows == 8 || kConvRows == 16, "row-flag store width");
+        if constexpr (kConvRows == 16)
+          *reinterpret_cast<uint4*>(&S.rowflag[b][kConvRows * cw]) = make_uint4(0u, 0u, 0u, 0u);
+        else
+          *reinterpret_cast<uint2*>(&S.rowflag[b][kConvRows * cw]) = make_uint2(0u, 0u);
       }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&S.a_full[b]);
+        mbar_arrive(&S.c_full[b]);
         if (cw == 0) TRACE_EV(m, 4);
         if (cw == 7) TRACE_EV(m, 10);
         if (cw == 3) TRACE_EV(m, 11);
-        mbar_arrive(&S.c_full[b]);
       }
     }
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsEpi));
     // ======================= epilogue (4 warps, one per TMEM lane quarter) ===========
     const int quarter = warp & 3;
     const int q = quarter * 32 + lane;  // sample row within the tile (M row)
