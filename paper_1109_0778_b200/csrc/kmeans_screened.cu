@@ -89,7 +89,7 @@ constexpr int kNumA = 3;     // plane buffers in flight
 // warpgroup 0: warp 0 screen MMAs, warp 1 fold MMAs (warps 2-3 idle); warpgroup 1: epilogue;
 // warpgroups 2-5: converters.  Registers: 80 at launch; warpgroup 0 gives 48 per thread back
 // (setmaxnreg.dec 32) and the epilogue takes them (setmaxnreg.inc 128).
-constexpr int kWarpMma = 0, kWarpFold = 1, kWarpE0 = 4, kWarpC0 = 8;
+constexpr int kWarpMma = 0, kWarpFold = 1, kWarpTail = 2, kWarpE0 = 4, kWarpC0 = 8;
 constexpr int kThreads = (kWarpC0 + kNumC) * 32;          // 768
 constexpr int kRegsLaunch = 80, kRegsIssuer = 32, kRegsEpi = 128;
 static_assert(kThreads * kRegsLaunch <= 65536 && 128 * (kRegsLaunch - kRegsIssuer) >= 128 * (kRegsEpi - kRegsLaunch),
@@ -125,6 +125,9 @@ struct Misc {
   int cnt[kMaxK];                         // screened rows folded per centroid (this CTA)
   alignas(16) unsigned char rowflag[kNumA][kTile];  // 1: exact chain over every centroid; 2: exact fold
   int pcount[2][4];
+  uint64_t dec_full[2], dec_empty[2];
+  int dec_a[2][kTile];                    // per row: assigned centroid (screened), -1 pending, -2 padding
+  unsigned long long dec_mask[2][kTile];  // candidate mask of pending rows
 };
 constexpr uint32_t kSmemBytes = kOffMisc + sizeof(Misc);
 static_assert(kSmemBytes <= 232448, "shared-memory plan exceeds 227 KiB");
@@ -216,6 +219,10 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     for (int s = 0; s < 2; ++s) {
       mbar_init(&S.oh_full[s], 4);
       mbar_init(&S.oh_empty[s], 1);
+    }
+    for (int s2 = 0; s2 < 2; ++s2) {
+      mbar_init(&S.dec_full[s2], 4);
+      mbar_init(&S.dec_empty[s2], 1);
     }
     mbar_init(&S.t_full, 1);
     mbar_init(&S.t_empty, 4);
@@ -355,6 +362,39 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       }
       mma_commit(&S.fold_done);
     }
+  } else if (warp == kWarpTail) {
+    // ======================= tail: assignments, counts, pending list =======================
+    // Off the critical path: consumes the epilogue's per-row decisions tile by tile, writes the
+    // screened assignments, counts them per centroid, and appends the pending rows to this
+    // CTA's list in row order (deterministic).
+    long long* my_pidx = pend_idx + static_cast<size_t>(blockIdx.x) * pend_cap;
+    unsigned long long* my_pmask = pend_mask + static_cast<size_t>(blockIdx.x) * pend_cap;
+    long long pending = 0;
+    for (int m = 0; m < mtiles; ++m) {
+      const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
+      const int b = m & 1;
+      mbar_wait(&S.dec_full[b], (m >> 1) & 1);
+#pragma unroll 1
+      for (int r0 = 0; r0 < kTile; r0 += 32) {
+        const int r = r0 + lane;
+        const int a = S.dec_a[b][r];
+        if (a >= 0) {
+          if (assign) assign[t * kTile + r] = a;
+          atomicAdd(&S.cnt[a], 1);
+        }
+        const unsigned pb = __ballot_sync(0xffffffffu, a == -1);
+        if (a == -1) {
+          const long long slot = pending + __popc(pb & ((1u << lane) - 1));
+          my_pidx[slot] = t * kTile + r;
+          my_pmask[slot] = S.dec_mask[b][r];
+        }
+        pending += __popc(pb);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.dec_empty[b]);
+    }
+    if (lane == 0) pend_count[blockIdx.x] = pending;
+    named_bar(7, 160);
   }
   } else if (warp >= kWarpC0) {
     // ======================= converters (16 warps) =======================
@@ -514,9 +554,6 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     const unsigned long long kmask = k == 64 ? ~0ull : ((1ull << k) - 1);
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
     const int window = S.window;
-    long long* my_pidx = pend_idx + static_cast<size_t>(blockIdx.x) * pend_cap;
-    unsigned long long* my_pmask = pend_mask + static_cast<size_t>(blockIdx.x) * pend_cap;
-    long long pending = 0;
     const int4* nm4 = reinterpret_cast<const int4*>(S.nm0);
     const uint32_t oh_row = (static_cast<uint32_t>(q) >> 3) * 512u + (q & 7) * 64u;
     const uint32_t oh_sw = (q & 7) >> 1;
@@ -557,10 +594,10 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       const int b3 = m % kNumA;
       mbar_wait(&S.c_full[b3], (m / kNumA) & 1);
       unsigned long long full = 0;
-      bool pend = false;
-      int hot = -1;
+      int hot = -2;   // -2 padding row, -1 pending, else the assigned centroid
       if (q < rows) {
         const int flag = S.rowflag[b3][q];
+        bool pend = false;
         int a = -1;
         if (flag & 1) {
           full = kmask;  // |x| out of the screen's range, inf or NaN: the exact chain over all c
@@ -579,11 +616,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
           a = 0;  // no finite centroid: the chain keeps its start index
         }
         if (flag & 2) pend = true;  // exact fp64 fold (the chain over the survivors re-derives a)
-        if (!pend) {
-          if (assign) assign[t * kTile + q] = a;
-          hot = a;
-          atomicAdd(&S.cnt[a], 1);
-        }
+        hot = pend ? -1 : a;
       }
       // this tile's one-hot row q (MN-major [q][c], SW64); zero for pending / padding rows
       if (m >= 2) mbar_wait(&S.oh_empty[b], ((m >> 1) - 1) & 1);
@@ -608,20 +641,14 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.oh_full[b]);
       if (quarter == 0 && lane == 0) TRACE_EV(m, 7);
-      // deterministic pending-list append, ordered by sample row
-      const unsigned pb = __ballot_sync(0xffffffffu, pend);
-      if (lane == 0) S.pcount[m & 1][quarter] = __popc(pb);
-      named_bar(1, 128);
-      const int p0 = S.pcount[m & 1][0], p1 = S.pcount[m & 1][1], p2 = S.pcount[m & 1][2];
-      if (pend) {
-        const int before = (quarter > 0 ? p0 : 0) + (quarter > 1 ? p1 : 0) + (quarter > 2 ? p2 : 0);
-        const long long slot = pending + before + __popc(pb & ((1u << lane) - 1));
-        my_pidx[slot] = t * kTile + q;
-        my_pmask[slot] = full;
-      }
-      pending += p0 + p1 + p2 + S.pcount[m & 1][3];
+      // hand the decision to the tail warp
+      if (m >= 2) mbar_wait(&S.dec_empty[b], ((m >> 1) - 1) & 1);
+      S.dec_a[b][q] = hot;
+      S.dec_mask[b][q] = full;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.dec_full[b]);
     }
-    if (quarter == 0 && lane == 0) pend_count[blockIdx.x] = pending;
+
 
     // ---- flush: exact per-centroid sums from the fold accumulators ------------------------
     // TMEM lane q < 64 holds planes b7, b5, b3, b1 of column j = q; lane 64 + j planes b6, b4,
@@ -631,7 +658,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     // offset count_c * (2^63 + 2^39) and scales by 2^(e_t - 62).
     mbar_wait(&S.fold_done, 0);
     tc_fence_after();
-    named_bar(1, 128);
+    named_bar(7, 160);   // with the tail warp: every count is in S.cnt
     unsigned long long* scratch = reinterpret_cast<unsigned long long*>(smem + kOffA);
     {
       const int half = q >> 6, j = q & 63;
