@@ -170,6 +170,20 @@ __device__ __forceinline__ void ldg128(const double* p, double& a, double& b) {
   asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "l"(p));
 }
 
+// Rows of tile t: global row of tile row q is row0 + q, valid for q in [qlo, qhi).  With kShift
+// (n >= kTile) the last tile is moved back to end at row n, so every tile is a full, unclamped
+// 128-row block; its first qlo rows repeat rows of the previous tile and are ignored.
+struct TileRows {
+  int64_t row0;
+  int qlo, qhi;
+};
+template <bool kShift>
+__device__ __forceinline__ TileRows tile_rows(int64_t t, int64_t n) {
+  const int64_t start = t * kTile;
+  if (kShift && start + kTile > n) return {n - kTile, static_cast<int>(start - (n - kTile)), kTile};
+  return {start, 0, static_cast<int>(n - start < kTile ? n - start : kTile)};
+}
+
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -202,6 +216,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
 #endif
   extern __shared__ __align__(1024) unsigned char smem[];
   Misc& S = *reinterpret_cast<Misc*>(smem + kOffMisc);
+  constexpr bool kShift = kD == 64;   // the host launches the d = 64 variant only for n >= kTile
   unsigned char* B1 = smem + kOffB1;
   unsigned char* B2 = smem + kOffB2;
   const int tid = threadIdx.x;
@@ -372,6 +387,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     long long pending = 0;
     for (int m = 0; m < mtiles; ++m) {
       const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
+      const int64_t row0 = tile_rows<kShift>(t, n).row0;
       const int b = m & 1;
       mbar_wait(&S.dec_full[b], (m >> 1) & 1);
 #pragma unroll 1
@@ -379,13 +395,13 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         const int r = r0 + lane;
         const int a = S.dec_a[b][r];
         if (a >= 0) {
-          if (assign) assign[t * kTile + r] = a;
+          if (assign) assign[row0 + r] = a;
           atomicAdd(&S.cnt[a], 1);
         }
         const unsigned pb = __ballot_sync(0xffffffffu, a == -1);
         if (a == -1) {
           const long long slot = pending + __popc(pb & ((1u << lane) - 1));
-          my_pidx[slot] = t * kTile + r;
+          my_pidx[slot] = row0 + r;
           my_pmask[slot] = S.dec_mask[b][r];
         }
         pending += __popc(pb);
@@ -432,7 +448,9 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     // which would wait on a load right after issuing it)
     auto load_pair = [&](const double* base, int64_t rows, int i, double (&dst)[4]) {
       int off = pair_row(i);
-      if (rbase + off >= rows) off = static_cast<int>(rows - 1) - rbase;   // padding rows repeat the last row
+      if constexpr (!kShift) {
+        if (rbase + off >= rows) off = static_cast<int>(rows - 1) - rbase;   // padding rows repeat the last row
+      }
       const double* src = base + off * D;
       if constexpr (kWide) {
         ldg256(src, dst[0], dst[1], dst[2], dst[3]);
@@ -442,9 +460,9 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       }
     };
     auto base_of = [&](int mm, int64_t& rows) {
-      const int64_t t = tile_of(mm);
-      rows = n - t * kTile;
-      return x + (t * kTile + rbase) * D + lcol;
+      const TileRows tr = tile_rows<kShift>(tile_of(mm), n);
+      rows = tr.qhi;
+      return x + (tr.row0 + rbase) * D + lcol;
     };
     auto prefetch = [&](int mm) {
       const int64_t t = tile_of(mm);
@@ -483,13 +501,11 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
             mx = max(mx, hw);
             mn = min(mn, hw);
           }
-          if (kZConv == 1) {
-            zsplit(w[e], s_hi, H[e], L[e]);
-          } else {  // one exact DMUL + F2I.S64.FLOOR; the offset 2^63 + 2^39 touches the high word only
-            const long long z = __double2ll_rd(w[e] * s_z);
-            H[e] = static_cast<uint32_t>(static_cast<unsigned long long>(z) >> 32) + 0x80000080u;
-            L[e] = static_cast<uint32_t>(z);
-          }
+          // Z + 2^39 = floor(x s + 2^39): one round-down fma (exact floor) + F2I.S64.FLOOR; the
+          // + 2^63 is the top-bit flip applied to the b7 plane below
+          const long long z = __double2ll_rd(__fma_rd(w[e], s_z, 549755813888.0));
+          H[e] = static_cast<uint32_t>(static_cast<unsigned long long>(z) >> 32);
+          L[e] = static_cast<uint32_t>(z);
         }
         if (i + kBuf < kPairs) load_pair(cur, cur_rows, i + kBuf, w);
         else load_pair(nxt, nxt_rows, i + kBuf - kPairs, w);
@@ -500,7 +516,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         const uint32_t lc = __byte_perm(L[2], L[3], 0x5140), ld = __byte_perm(L[2], L[3], 0x7362);
         unsigned char* A0 = Ab + soff[i & 3] + (i >> 2) * 1024;
         unsigned char* A1 = Ab + (soff[i & 3] ^ 64u) + (i >> 2) * 1024;
-        *reinterpret_cast<uint32_t*>(A0) = __byte_perm(hb, hd, 0x7632);                  // b7
+        *reinterpret_cast<uint32_t*>(A0) = __byte_perm(hb, hd, 0x7632) ^ 0x80808080u;    // b7
         *reinterpret_cast<uint32_t*>(A1) = __byte_perm(hb, hd, 0x5410);                  // b6
         *reinterpret_cast<uint32_t*>(A0 + kPlane2) = __byte_perm(ha, hc, 0x7632);        // b5
         *reinterpret_cast<uint32_t*>(A1 + kPlane2) = __byte_perm(ha, hc, 0x5410);        // b4
@@ -515,14 +531,14 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       if (__any_sync(0xffffffffu, odd)) {
         // rare: classify row by row, re-reading this tile's values (the registers already hold
         // the next pairs)
-        const int64_t t = tile_of(m);
+        const TileRows tr = tile_rows<kShift>(tile_of(m), n);
 #pragma unroll 1
         for (int i = 0; i < kPairs; ++i) {
           const int row = rbase + pair_row(i);
           int f = 0;
-          if (row < n - t * kTile)
+          if (row >= tr.qlo && row < tr.qhi)
             for (int e = 0; e < 4; ++e)
-              if (col0 + e < d) f |= elem_flag(x[(t * kTile + row) * d + col0 + e], hw_hi, hw_lo);
+              if (col0 + e < d) f |= elem_flag(x[(tr.row0 + row) * d + col0 + e], hw_hi, hw_lo);
           const int f0 = static_cast<int>(__reduce_or_sync(0xffffffffu, static_cast<unsigned>(hl ? 0 : f)));
           const int f1 = static_cast<int>(__reduce_or_sync(0xffffffffu, static_cast<unsigned>(hl ? f : 0)));
           const int r = kConvRows * cw + pair_row(i);
@@ -560,7 +576,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     for (int m = 0; m < mtiles; ++m) {
       const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
       const int b = m & 1;
-      const int rows = static_cast<int>(n - t * kTile < kTile ? n - t * kTile : kTile);
+      const TileRows tr = tile_rows<kShift>(t, n);
       if (quarter == 0 && lane == 0) TRACE_EV(m, 5);
       mbar_wait(&S.t_full, m & 1);
       if (quarter == 0 && lane == 0) TRACE_EV(m, 6);
@@ -595,7 +611,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       mbar_wait(&S.c_full[b3], (m / kNumA) & 1);
       unsigned long long full = 0;
       int hot = -2;   // -2 padding row, -1 pending, else the assigned centroid
-      if (q < rows) {
+      if (q >= tr.qlo && q < tr.qhi) {
         const int flag = S.rowflag[b3][q];
         bool pend = false;
         int a = -1;
@@ -603,10 +619,16 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
           full = kmask;  // |x| out of the screen's range, inf or NaN: the exact chain over all c
           pend = true;
         } else if (lmin < kNoCandidate) {
-          const int thr = lmin + window;
+          // survivors tv[u] <= lmin + window: collect the sign bits of tv[u] - (lmin + window + 1)
+          // with funnel shifts (|differences| < 2^31: scores lie in (-2^28, 2^28), invalid ones at
+          // kInvalidNm), then bit-reverse
+          const int thr1 = lmin + window + 1;
+          unsigned nlo = 0, nhi = 0;
 #pragma unroll
-          for (int u = 0; u < 64; ++u)
-            if (tv[u] <= thr) full |= 1ull << u;
+          for (int u = 0; u < 32; ++u) nlo = __funnelshift_l(static_cast<unsigned>(tv[u] - thr1), nlo, 1);
+#pragma unroll
+          for (int u = 32; u < 64; ++u) nhi = __funnelshift_l(static_cast<unsigned>(tv[u] - thr1), nhi, 1);
+          full = (static_cast<unsigned long long>(__brev(nhi)) << 32) | __brev(nlo);
           if ((full & (full - 1)) == 0) {
             a = __ffsll(static_cast<long long>(full)) - 1;
           } else {
@@ -901,7 +923,8 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
   // 32-byte row loads when every lane's four columns are 32-byte aligned
   const bool wide = (d % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 32 == 0);
   auto kern = !wide ? sk::kmeans_screened_kernel<0, false>
-                    : (d == 64 ? sk::kmeans_screened_kernel<64, true> : sk::kmeans_screened_kernel<0, true>);
+                    : (d == 64 && n >= sk::kTile ? sk::kmeans_screened_kernel<64, true>
+                                                 : sk::kmeans_screened_kernel<0, true>);
   DLX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sk::kSmemBytes)));
   kern<<<grid, sk::kThreads, sk::kSmemBytes, stream>>>(
