@@ -101,12 +101,11 @@ constexpr uint32_t kFoldCol = 256;                        // fold accumulators: 
 constexpr uint32_t kPlane2 = kTile * 128;                 // one [b_hi|b_lo] SW128 buffer, 16 KiB
 constexpr uint32_t kABuf = 4 * kPlane2;                   // eight planes, 64 KiB
 constexpr uint32_t kOffA = 0;
-constexpr uint32_t kOffB1 = kOffA + kNumA * kABuf;        // [h'|l'] 64 x 128 B, SW128
-constexpr uint32_t kOffB2 = kOffB1 + kMaxK * 128;         // [G]     64 x 64 B,  SW64
-constexpr uint32_t kOffOH = kOffB2 + kMaxK * 64;          // one-hot [q][c] 128 x 64 B, SW64, x2
+constexpr uint32_t kOffB = kOffA + kNumA * kABuf;         // centroid planes: rows [h'' | l' | G], 192 x 64 B, SW64
+constexpr uint32_t kOffOH = kOffB + 3 * kMaxK * 64;       // one-hot [q][c] 128 x 64 B, SW64, x2
 constexpr uint32_t kOHBuf = kTile * 64;
 constexpr uint32_t kOffMisc = kOffOH + 2 * kOHBuf;
-static_assert(kOffA % 1024 == 0 && kOffB1 % 1024 == 0 && kOffB2 % 512 == 0 && kOffOH % 512 == 0,
+static_assert(kOffA % 1024 == 0 && kOffB % 1024 == 0 && kOffOH % 512 == 0,
               "UMMA operand alignment");
 static_assert(kNumA * kABuf >= 2u * kMaxK * 64 * 16, "final fold scratch must fit the plane buffers");
 constexpr double kMagic = 6755399441055744.0;        // 1.5 * 2^52: x + kMagic rounds x to an integer
@@ -217,8 +216,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
   extern __shared__ __align__(1024) unsigned char smem[];
   Misc& S = *reinterpret_cast<Misc*>(smem + kOffMisc);
   constexpr bool kShift = kD == 64;   // the host launches the d = 64 variant only for n >= kTile
-  unsigned char* B1 = smem + kOffB1;
-  unsigned char* B2 = smem + kOffB2;
+  unsigned char* Bm = smem + kOffB;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int64_t ntiles = (n + kTile - 1) / kTile;
@@ -283,9 +281,12 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       const int c = e / kMaxD, j = e - c * kMaxD;
       int Y = 0;
       if (((valid >> c) & 1) && j < d) Y = rint_magic(mu[c * d + j] * scale);
-      B1[sw128_offset(c, j)] = static_cast<unsigned char>(Y >> 16);
-      B1[sw128_offset(c, 64 + j)] = static_cast<unsigned char>(Y >> 8);
-      B2[sw64_offset(c, j)] = static_cast<unsigned char>(Y);
+      // h'' = (Y >> 16) + 128 in [64, 192] (unsigned; the offset adds a per-sample constant to
+      // every centroid's score); invalid centroids and columns past d are all-zero rows
+      const bool live = ((valid >> c) & 1) && j < d;
+      Bm[sw64_offset(c, j)] = static_cast<unsigned char>(live ? (Y >> 16) + 128 : 0);
+      Bm[sw64_offset(64 + c, j)] = static_cast<unsigned char>(Y >> 8);
+      Bm[sw64_offset(128 + c, j)] = static_cast<unsigned char>(Y);
     }
     if (tid < kMaxK) {
       int sa = 0, ssum = 0;
@@ -321,9 +322,10 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
   if (warp == kWarpMma) {
     // ======================= screen MMA issuer =======================
     if (lane == 0) {
-      constexpr uint32_t ID_us = idesc_i8(kTile, 64, 0, 1);   // u8 sample plane x s8 h'
-      constexpr uint32_t ID_uu = idesc_i8(kTile, 64, 0, 0);
-      const uint32_t b1 = smem_addr(B1), b2 = smem_addr(B2);
+      // all operands unsigned: sample planes h'' = b7, l = b6, F = b5; centroid rows h'', l', G
+      constexpr uint32_t ID_64 = idesc_i8(kTile, 64, 0, 0), ID_128 = idesc_i8(kTile, 128, 0, 0);
+      constexpr uint32_t ID_192 = idesc_i8(kTile, 192, 0, 0);
+      const uint32_t bm = smem_addr(Bm);
       const int nk = (d + 31) / 32;
       for (int ns = 0; ns < mtiles; ++ns) {
         mbar_wait(&S.a_full[ns % kNumA], (ns / kNumA) & 1);
@@ -336,17 +338,14 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
           const uint64_t xh = sw128_kmajor_desc(a0 + 32 * kk);             // b7 = h''
           const uint64_t xl = sw128_kmajor_desc(a0 + 64 + 32 * kk);        // b6 = l
           const uint64_t xf = sw128_kmajor_desc(a0 + kPlane2 + 32 * kk);   // b5 = F
-          const uint64_t mh = sw128_kmajor_desc(b1 + 32 * kk), ml = sw128_kmajor_desc(b1 + 64 + 32 * kk);
-          const uint64_t mg = sw64_kmajor_desc(b2 + 32 * kk);
+          const uint64_t m0 = sw64_kmajor_desc(bm + 32 * kk);              // rows h'', l', G
+          const uint64_t m1 = sw64_kmajor_desc(bm + 64 * 64 + 32 * kk);    // rows l', G
           const uint32_t acc = kk > 0;
-          mma_i8(tmem + 0, xh, mh, ID_us, acc);      // HH
-          mma_i8(tmem + 64, xh, ml, ID_uu, acc);     // CR = h'' l' + l h'
-          mma_i8(tmem + 64, xl, mh, ID_us, 1);
-          mma_i8(tmem + 128, xh, mg, ID_uu, acc);    // W1 = h'' G + F h' + l l'
-          mma_i8(tmem + 128, xf, mh, ID_us, 1);
-          mma_i8(tmem + 128, xl, ml, ID_uu, 1);
-          mma_i8(tmem + 192, xl, mg, ID_uu, acc);    // W2 = l G + F l'
-          mma_i8(tmem + 192, xf, ml, ID_uu, 1);
+          // TMEM columns: HH 0-63, CR 64-127, W1 128-191, W2 192-255
+          mma_i8(tmem + 0, xh, m0, ID_64, acc);      // HH  = h'' h''
+          mma_i8(tmem + 64, xl, m0, ID_192, acc);    // CR += l h'',  W1 += l l',  W2 += l G
+          mma_i8(tmem + 64, xh, m1, ID_128, 1);      // CR += h'' l', W1 += h'' G
+          mma_i8(tmem + 128, xf, m0, ID_128, 1);     // W1 += F h'',  W2 += F l'
         }
         mma_commit(&S.t_full);
         TRACE_EV(ns, 0);
@@ -559,7 +558,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         mbar_arrive(&S.c_full[b]);
         if (cw == 0) TRACE_EV(m, 4);
         if (cw == 7) TRACE_EV(m, 10);
-        if (cw == 3) TRACE_EV(m, 11);
+
       }
     }
   } else {
@@ -568,6 +567,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     const int quarter = warp & 3;
     const int q = quarter * 32 + lane;  // sample row within the tile (M row)
     const unsigned long long kmask = k == 64 ? ~0ull : ((1ull << k) - 1);
+    const unsigned long long vmask = S.valid;   // finite centroids (the others never survive)
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
     const int window = S.window;
     const int4* nm4 = reinterpret_cast<const int4*>(S.nm0);
@@ -609,6 +609,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       if (quarter == 0 && lane == 0) TRACE_EV(m, 12);
       const int b3 = m % kNumA;
       mbar_wait(&S.c_full[b3], (m / kNumA) & 1);
+      if (quarter == 0 && lane == 0) TRACE_EV(m, 11);
       unsigned long long full = 0;
       int hot = -2;   // -2 padding row, -1 pending, else the assigned centroid
       if (q >= tr.qlo && q < tr.qhi) {
@@ -620,15 +621,15 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
           pend = true;
         } else if (lmin < kNoCandidate) {
           // survivors tv[u] <= lmin + window: collect the sign bits of tv[u] - (lmin + window + 1)
-          // with funnel shifts (|differences| < 2^31: scores lie in (-2^28, 2^28), invalid ones at
-          // kInvalidNm), then bit-reverse
+          // with funnel shifts (valid scores of a row differ by < 2^30, so the signs are exact;
+          // invalid centroids are masked out), then bit-reverse
           const int thr1 = lmin + window + 1;
           unsigned nlo = 0, nhi = 0;
 #pragma unroll
           for (int u = 0; u < 32; ++u) nlo = __funnelshift_l(static_cast<unsigned>(tv[u] - thr1), nlo, 1);
 #pragma unroll
           for (int u = 32; u < 64; ++u) nhi = __funnelshift_l(static_cast<unsigned>(tv[u] - thr1), nhi, 1);
-          full = (static_cast<unsigned long long>(__brev(nhi)) << 32) | __brev(nlo);
+          full = ((static_cast<unsigned long long>(__brev(nhi)) << 32) | __brev(nlo)) & vmask;
           if ((full & (full - 1)) == 0) {
             a = __ffsll(static_cast<long long>(full)) - 1;
           } else {
@@ -641,7 +642,9 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         hot = pend ? -1 : a;
       }
       // this tile's one-hot row q (MN-major [q][c], SW64); zero for pending / padding rows
+      if (quarter == 0 && lane == 0) TRACE_EV(m, 14);
       if (m >= 2) mbar_wait(&S.oh_empty[b], ((m >> 1) - 1) & 1);
+      if (quarter == 0 && lane == 0) TRACE_EV(m, 15);
       {
         unsigned char* ohb = smem + kOffOH + b * kOHBuf + oh_row;
 #pragma unroll
@@ -936,23 +939,24 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
     DLX_CUDA(cudaStreamSynchronize(stream));
     DLX_CUDA(cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
     cudaFree(trace);
-    const char* names[14] = {"screen_issued", "fold_issued", "conv_begin", "conv_got_buf", "conv_done",
+    const char* names[16] = {"screen_issued", "fold_issued", "conv_begin", "conv_got_buf", "conv_done",
                              "epi_begin", "epi_got_tfull", "epi_oh_done", "scr_got_afull", "scr_got_tempty",
-                             "conv7_done", "conv3_done", "epi_tmem_drained", "fold_got_oh"};
-    double avg[14] = {0}, per_tile = 0;
+                             "conv7_done", "epi_got_cfull", "epi_tmem_drained", "fold_got_oh",
+                             "epi_pre_ohwait", "epi_post_ohwait"};
+    double avg[16] = {0}, per_tile = 0;
     long cnt = 0;
     for (int b = 0; b < grid; ++b)
       for (int m = 8; m < sk::kTraceTiles - 1; ++m) {
         const long long* r = &h[(static_cast<size_t>(b) * sk::kTraceTiles + m) * 16];
         const long long* r1 = r + 16;
         if (r[2] == 0 || r1[2] == 0) continue;
-        for (int e = 0; e < 14; ++e) avg[e] += static_cast<double>(r[e] - r[2]);
+        for (int e = 0; e < 16; ++e) avg[e] += static_cast<double>(r[e] - r[2]);
         per_tile += static_cast<double>(r1[2] - r[2]);
         ++cnt;
       }
     if (cnt) {
       fprintf(stderr, "[dlx trace] tile period %.0f cycles;", per_tile / cnt);
-      for (int e = 0; e < 14; ++e) fprintf(stderr, " %s %+.0f", names[e], avg[e] / cnt);
+      for (int e = 0; e < 16; ++e) fprintf(stderr, " %s %+.0f", names[e], avg[e] / cnt);
       fprintf(stderr, "\n");
     }
   }
