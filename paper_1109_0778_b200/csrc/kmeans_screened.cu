@@ -80,20 +80,25 @@ using namespace sm100;
 constexpr int kTile = 128;   // samples per tile = MMA M
 constexpr int kMaxD = 64;
 constexpr int kMaxK = 64;
-constexpr int kNumC = 16;    // converter warps (8 rows = 4 row pairs of every tile each)
+#ifndef DLX_KMEANS_CONV_WARPS
+#define DLX_KMEANS_CONV_WARPS 16
+#endif
+constexpr int kNumC = DLX_KMEANS_CONV_WARPS;   // converter warps (kConvRows rows of every tile each)
 constexpr int kConvRows = kTile / kNumC;
 constexpr int kPairs = kConvRows / 2;                      // row pairs per converter warp per tile
-constexpr int kBuf = kPairs < 4 ? kPairs : 4;             // rolling register buffer (pairs)
+constexpr int kBuf = kNumC == 8 ? kPairs : 4;             // rolling register buffer (pairs)
 constexpr int kNumA = 3;     // plane buffers in flight
-// warp 0 issues the screen MMAs, warp 1 the fold MMAs (each sleeps on its own barriers)
-// warpgroup 0: warp 0 screen MMAs, warp 1 fold MMAs (warps 2-3 idle); warpgroup 1: epilogue;
-// warpgroups 2-5: converters.  Registers: 80 at launch; warpgroup 0 gives 48 per thread back
-// (setmaxnreg.dec 32) and the epilogue takes them (setmaxnreg.inc 128).
+// warpgroup 0: warp 0 screen MMAs, warp 1 fold MMAs, warp 2 tail (warp 3 idle); warpgroup 1:
+// epilogue; then the converter warpgroups.  Registers are rebalanced with setmaxnreg after the
+// prologue: warpgroup 0 drops to 32, the epilogue runs at 128, converters take the rest.
 constexpr int kWarpMma = 0, kWarpFold = 1, kWarpTail = 2, kWarpE0 = 4, kWarpC0 = 8;
-constexpr int kThreads = (kWarpC0 + kNumC) * 32;          // 768
-constexpr int kRegsLaunch = 80, kRegsIssuer = 32, kRegsEpi = 128;
-static_assert(kThreads * kRegsLaunch <= 65536 && 128 * (kRegsLaunch - kRegsIssuer) >= 128 * (kRegsEpi - kRegsLaunch),
-              "register plan");
+constexpr int kThreads = (kWarpC0 + kNumC) * 32;
+constexpr int kRegsLaunch = (65536 / kThreads) & ~7;
+constexpr int kRegsIssuer = 32, kRegsEpi = 128;
+constexpr int kRegsConvRaw = (kThreads * kRegsLaunch - 128 * kRegsIssuer - 128 * kRegsEpi) / (32 * kNumC);
+constexpr int kRegsConv = (kRegsConvRaw > 248 ? 248 : kRegsConvRaw) & ~7;
+static_assert(kNumC == 8 || kNumC == 16, "converter warps");
+static_assert(kRegsConv >= kRegsLaunch || kRegsEpi >= kRegsLaunch, "register plan");
 constexpr int kZConv = 2;                                 // 1: fp64 magic-number split, 2: F2I.S64
 constexpr int kPfDefault = 0;                             // L2 prefetch distance (tiles)
 constexpr uint32_t kTmemCols = 512;
@@ -412,6 +417,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     named_bar(7, 160);
   }
   } else if (warp >= kWarpC0) {
+    if constexpr (kRegsConv > kRegsLaunch) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsConv));
     // ======================= converters (16 warps) =======================
     // Warp cw owns rows kConvRows*cw .. +kConvRows-1 of every tile as row pairs (r, r + 4) of an
     // 8-row SW128 atom.  Lane (hl, p) = (lane >> 4, lane & 15) holds columns 4p .. 4p+3 of row
@@ -562,7 +568,8 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       }
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsEpi));
+    if constexpr (kRegsEpi > kRegsLaunch) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsEpi));
+    if constexpr (kRegsEpi < kRegsLaunch) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsEpi));
     // ======================= epilogue (4 warps, one per TMEM lane quarter) ===========
     const int quarter = warp & 3;
     const int q = quarter * 32 + lane;  // sample row within the tile (M row)
