@@ -46,16 +46,19 @@
 // 2^-32 relative error) take the exact fp64 fold in the resolve kernel instead.  The fold is
 // order-free, hence deterministic.
 //
-// Kernel shape: one persistent CTA per SM, 14 warps, warp-specialised around mbarriers:
-//   warp 0      TMA producer: bulk copies of 64-sample halves into a 2-stage ring, plus bulk
-//               L2 prefetches two tiles ahead
-//   warp 1      TMEM owner + MMA issuer (one thread): 16 screen MMAs per tile into 4 x 64
-//               int32 columns, then the previous tile's 16 fold MMAs into the persistent
-//               4 x 64 fold columns
-//   warps 2-9   converters: conflict-free row loads, Z'' via directed-rounding fmas, lane-pair
-//               exchange and byte-plane transpose into the double-buffered SW128 planes
-//   warps 10-13 epilogue: tcgen05.ld the screen accumulators, decide, write assignments,
-//               counts and the tile's one-hot rows; at the end read the fold accumulators
+// Kernel shape: one persistent CTA per SM (227 KiB smem: three 64 KiB plane buffers, the
+// centroid planes, two one-hot buffers), 24 warps, warp-specialised around mbarriers:
+//   warp 0      TMEM owner + screen MMA issuer: per tile 8 tcgen05.mma (N = 64/192/128/128,
+//               centroid planes concatenated along N) into 4 x 64 int32 screen columns
+//   warp 1      fold MMA issuer: per tile 16 MN-major tcgen05.mma into the persistent 4 x 64
+//               fold columns; its commits free the plane and one-hot buffers
+//   warp 2      tail: assignment stores, per-centroid counts, the ordered pending list
+//   warps 4-7   epilogue (TMEM lane quarters): tcgen05.ld the screen columns, scores, minimum,
+//               survivor mask (funnel-shifted sign bits), decision, the tile's one-hot rows;
+//               at the end the exact fold flush
+//   warps 8-23  converters: 32-byte row loads a whole tile ahead in registers, Z via one
+//               round-down fma + F2I.S64, byte-plane transposes (PRMT), conflict-free STS
+//   registers   80 at launch, rebalanced by setmaxnreg: warps 0-3 32, epilogue 128, converters 80
 //   resolve     a second small kernel evaluates the reference chain for the pending samples
 //               (one thread per (sample, candidate) pair), writes their assignments and folds
 //               their rows into per-CTA partial records in fp64, in list order.
