@@ -39,7 +39,9 @@ enum dlx_vm_op {
 };
 
 enum { DLX_VM_I64 = 0, DLX_VM_F64 = 1, DLX_VM_BOOL = 2 };
-enum { DLX_VM_COLLECT = 0, DLX_VM_REDUCE = 1 };
+/* DLX_VM_APPEND: filter-collect (LoopElem.append, codegen.cpp:357-360 / 404-405): the values of
+ * the indices whose cond holds, appended in index order; d_results[elem] receives the length. */
+enum { DLX_VM_COLLECT = 0, DLX_VM_REDUCE = 1, DLX_VM_APPEND = 2 };
 enum { DLX_VM_COMBINE_ADD = 0, DLX_VM_COMBINE_MUL = 1 };
 
 typedef struct {
@@ -55,7 +57,7 @@ typedef struct {
   int32_t cond_begin, cond_end, cond_reg;   /* empty range = no guard */
   int32_t value_begin, value_end, value_reg;
   int64_t zero;        /* reduce identity (bits) */
-  void* out;           /* collect: device output vector of `range` elements */
+  void* out;           /* collect / append: device output vector with room for `range` elements */
 } dlx_vm_elem;
 
 typedef struct {
@@ -67,6 +69,8 @@ typedef struct {
   dlx_vm_elem elem[DLX_VM_MAX_ELEMS];
 } dlx_vm_loop;
 
+/* workspace for one dlx_vm_run_loop of this range (per-CTA reduce partials, and for append
+ * elems the per-CTA counts and offsets) */
 size_t dlx_vm_workspace_bytes(int64_t range);
 /* d_code: ncode instructions in device memory; d_results: DLX_VM_MAX_ELEMS 64-bit slots;
  * d_trap: device int, OR-ed with 1 (int division by zero), 2 (index out of bounds). */

@@ -162,6 +162,19 @@ void count_gt(Stage& st, int64_t n) {
   st.print(x.sum());
 }
 
+// SPADE-style find + count: a filter-collect (find_indexes, an append
+// collect: loops.cpp:105-109, vectordsl.cpp:153-160) fused with a predicated count over the
+// same range, then reads of the appended vector (its length, first element, and a sum loop
+// over it).
+void find_count(Stage& st, int64_t n) {
+  DVec x = vec_rand(st, st.lit(n));
+  DVec hits = x.find_indexes([&](DVal v) { return st.lit(0.9) < DDouble(v); });
+  st.print(x.count_where([&](DVal v) { return st.lit(0.9) < DDouble(v); }));
+  st.print(hits.len());
+  st.print(hits.at(st.lit(int64_t{0})));
+  st.print(hits.sum());
+}
+
 struct Spec {
   std::string name;
   std::function<void(Stage&)> body;
@@ -180,6 +193,7 @@ int main(int argc, char** argv) {
       {"mean_variance_n100000", [](Stage& st) { mean_variance(st, 100000); }},
       {"axpy_n100000", [](Stage& st) { axpy(st, 100000); }},
       {"count_gt_n100000", [](Stage& st) { count_gt(st, 100000); }},
+      {"find_count_n100000", [](Stage& st) { find_count(st, 100000); }},
   };
   for (const Spec& sp : specs) {
     const auto t0 = std::chrono::steady_clock::now();

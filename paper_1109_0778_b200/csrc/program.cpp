@@ -1079,8 +1079,8 @@ class Executor {
       const LElem& le = els[q];
       dlx_vm_elem& ve = L.elem[q];
       if (le.e->kind == "collect") {
-        if (le.e->append) gen_fail("filter-collect (append) is not lowered yet");
-        ve.kind = DLX_VM_COLLECT;
+        // filter-collect (append): order-preserving compaction, length returned in d_results
+        ve.kind = le.e->append ? DLX_VM_APPEND : DLX_VM_COLLECT;
         ve.ty = vm_ty(le.e->out_ty.elem);
         outs[q] = new_vec(n, le.e->out_ty.elem == Ty::Double ? Ty::Double : le.e->out_ty.elem == Ty::Bool ? Ty::Bool : Ty::Int,
                           st_, true);
@@ -1159,6 +1159,7 @@ class Executor {
     for (size_t q = 0; q < els.size(); ++q) {
       const Elem& e = *els[q].e;
       if (e.kind == "collect") {
+        if (e.append) outs[q]->n = res[q];   // the builder's final length
         env_[e.out] = Val{outs[q]};
       } else if (e.out_ty.t == Ty::Double) {
         double dv;

@@ -9,6 +9,10 @@
 // per-CTA partials (combine.cu).  fp64 arithmetic uses explicit _rn intrinsics (no FMA
 // contraction) so collects are bit-identical to the reference; Int arithmetic wraps; Int
 // division by zero and out-of-range loads raise the trap flag (TrapError on the host).
+// Filter-collect (append) elems make the launch order-preserving: a count pass over contiguous
+// per-CTA index ranges, an exclusive scan of the per-CTA counts, then the main pass writes each
+// CTA's selected values at its offset with a block-wide ballot scan per 256-index step, so the
+// output is exactly the reference's builder contents in index order.
 #include <algorithm>
 
 #include "common.cuh"
@@ -79,31 +83,132 @@ __device__ __forceinline__ void vm_exec(const dlx_vm_instr* __restrict__ code, i
   }
 }
 
+__device__ __forceinline__ void vm_store(const dlx_vm_elem& el, long long at, Reg v) {
+  if (el.ty == DLX_VM_F64) static_cast<double*>(el.out)[at] = v.d;
+  else if (el.ty == DLX_VM_I64) static_cast<long long*>(el.out)[at] = v.i;
+  else static_cast<unsigned char*>(el.out)[at] = static_cast<unsigned char>(v.i != 0);
+}
+
+// contiguous index range of CTA b when the loop has append elems
+__device__ __forceinline__ void vm_chunk(long long range, long long chunk, long long& lo, long long& hi) {
+  lo = static_cast<long long>(blockIdx.x) * chunk;
+  hi = lo + chunk < range ? lo + chunk : range;
+}
+
+// count pass: how many indices of this CTA's range each append elem selects
 __global__ void __launch_bounds__(kVmThreads)
-vm_loop_kernel(const dlx_vm_instr* __restrict__ code, dlx_vm_loop L, Reg* __restrict__ parts,
-               int* __restrict__ trap) {
+vm_count_kernel(const dlx_vm_instr* __restrict__ code, dlx_vm_loop L, long long chunk,
+                long long* __restrict__ counts, int* __restrict__ trap) {
   __shared__ dlx_vm_instr code_s[DLX_VM_MAX_CODE];
-  __shared__ Reg red_s[kVmThreads / 32][DLX_VM_MAX_ELEMS];
+  __shared__ long long cnt_s[DLX_VM_MAX_ELEMS];
   for (int e = threadIdx.x; e < L.ncode; e += kVmThreads) code_s[e] = code[e];
+  if (threadIdx.x < DLX_VM_MAX_ELEMS) cnt_s[threadIdx.x] = 0;
   __syncthreads();
-  Reg acc[DLX_VM_MAX_ELEMS];
-  for (int e = 0; e < L.nelems; ++e) acc[e].i = L.elem[e].zero;
+  long long lo, hi;
+  vm_chunk(L.range, chunk, lo, hi);
   Reg r[DLX_VM_MAX_REGS];
-  const long long T = static_cast<long long>(gridDim.x) * kVmThreads;
-  for (long long i = static_cast<long long>(blockIdx.x) * kVmThreads + threadIdx.x; i < L.range; i += T) {
+  int my[DLX_VM_MAX_ELEMS];
+  for (int e = 0; e < L.nelems; ++e) my[e] = 0;
+  for (long long i = lo + threadIdx.x; i < hi; i += kVmThreads) {
     vm_exec(code_s, 0, L.body_end, r, i, &L, trap);
     for (int e = 0; e < L.nelems; ++e) {
       const dlx_vm_elem& el = L.elem[e];
+      if (el.kind != DLX_VM_APPEND) continue;
+      bool take = true;
       if (el.cond_end > el.cond_begin) {
         vm_exec(code_s, el.cond_begin, el.cond_end, r, i, &L, trap);
-        if (!r[el.cond_reg].i) continue;
+        take = r[el.cond_reg].i != 0;
       }
-      vm_exec(code_s, el.value_begin, el.value_end, r, i, &L, trap);
-      const Reg v = r[el.value_reg];
+      my[e] += take;
+    }
+  }
+  for (int e = 0; e < L.nelems; ++e) {
+    if (L.elem[e].kind != DLX_VM_APPEND) continue;
+    int v = my[e];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt_s[e]), static_cast<unsigned long long>(v));
+  }
+  __syncthreads();
+  if (threadIdx.x < L.nelems) counts[static_cast<size_t>(blockIdx.x) * DLX_VM_MAX_ELEMS + threadIdx.x] = cnt_s[threadIdx.x];
+}
+
+// exclusive scan of the per-CTA counts (ascending CTA = ascending index ranges) -> offsets,
+// and the total = the appended vector's length
+__global__ void vm_scan_kernel(const long long* __restrict__ counts, int nblocks, dlx_vm_loop L,
+                               long long* __restrict__ offsets, long long* __restrict__ out) {
+  const int e = threadIdx.x;
+  if (e >= L.nelems || L.elem[e].kind != DLX_VM_APPEND) return;
+  long long run = 0;
+  for (int b = 0; b < nblocks; ++b) {
+    offsets[static_cast<size_t>(b) * DLX_VM_MAX_ELEMS + e] = run;
+    run += counts[static_cast<size_t>(b) * DLX_VM_MAX_ELEMS + e];
+  }
+  out[e] = run;
+}
+
+__global__ void __launch_bounds__(kVmThreads)
+vm_loop_kernel(const dlx_vm_instr* __restrict__ code, dlx_vm_loop L, Reg* __restrict__ parts,
+               int* __restrict__ trap, long long chunk, const long long* __restrict__ offsets) {
+  __shared__ dlx_vm_instr code_s[DLX_VM_MAX_CODE];
+  __shared__ Reg red_s[kVmThreads / 32][DLX_VM_MAX_ELEMS];
+  __shared__ int wsum_s[kVmThreads / 32];
+  for (int e = threadIdx.x; e < L.ncode; e += kVmThreads) code_s[e] = code[e];
+  __syncthreads();
+  Reg acc[DLX_VM_MAX_ELEMS];
+  long long run[DLX_VM_MAX_ELEMS];   // append: next output slot of this CTA
+  for (int e = 0; e < L.nelems; ++e) {
+    acc[e].i = L.elem[e].zero;
+    run[e] = (chunk > 0 && L.elem[e].kind == DLX_VM_APPEND)
+                 ? offsets[static_cast<size_t>(blockIdx.x) * DLX_VM_MAX_ELEMS + e] : 0;
+  }
+  Reg r[DLX_VM_MAX_REGS];
+  // grid-stride without append elems; contiguous per-CTA ranges (all threads step together,
+  // so the append scan stays in index order) with them
+  long long i, stop, step;
+  if (chunk > 0) {
+    vm_chunk(L.range, chunk, i, stop);
+    step = kVmThreads;
+  } else {
+    i = static_cast<long long>(blockIdx.x) * kVmThreads;
+    stop = L.range;
+    step = static_cast<long long>(gridDim.x) * kVmThreads;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (; i < stop; i += step) {
+    const long long idx = i + threadIdx.x;
+    const bool live = idx < stop;
+    if (live) vm_exec(code_s, 0, L.body_end, r, idx, &L, trap);
+    for (int e = 0; e < L.nelems; ++e) {
+      const dlx_vm_elem& el = L.elem[e];
+      bool take = live;
+      if (live && el.cond_end > el.cond_begin) {
+        vm_exec(code_s, el.cond_begin, el.cond_end, r, idx, &L, trap);
+        take = r[el.cond_reg].i != 0;
+      }
+      Reg v;
+      v.i = 0;
+      if (take) {
+        vm_exec(code_s, el.value_begin, el.value_end, r, idx, &L, trap);
+        v = r[el.value_reg];
+      }
+      if (el.kind == DLX_VM_APPEND) {   // block-uniform branch: every thread reaches the scan
+        const unsigned bal = __ballot_sync(0xffffffffu, take);
+        if (lane == 0) wsum_s[warp] = __popc(bal);
+        __syncthreads();
+        int before = 0, total = 0;
+        for (int w = 0; w < kVmThreads / 32; ++w) {
+          const int c = wsum_s[w];
+          before += w < warp ? c : 0;
+          total += c;
+        }
+        if (take) vm_store(el, run[e] + before + __popc(bal & ((1u << lane) - 1)), v);
+        run[e] += total;
+        __syncthreads();
+        continue;
+      }
+      if (!take) continue;
       if (el.kind == DLX_VM_COLLECT) {
-        if (el.ty == DLX_VM_F64) static_cast<double*>(el.out)[i] = v.d;
-        else if (el.ty == DLX_VM_I64) static_cast<long long*>(el.out)[i] = v.i;
-        else static_cast<unsigned char*>(el.out)[i] = static_cast<unsigned char>(v.i != 0);
+        vm_store(el, idx, v);
       } else if (el.ty == DLX_VM_F64) {
         acc[e].d = el.combine == DLX_VM_COMBINE_MUL ? __dmul_rn(acc[e].d, v.d) : __dadd_rn(acc[e].d, v.d);
       } else {
@@ -114,7 +219,6 @@ vm_loop_kernel(const dlx_vm_instr* __restrict__ code, dlx_vm_loop L, Reg* __rest
     }
   }
   // warp tree, then ascending-warp fold, per reduce elem
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int e = 0; e < L.nelems; ++e) {
     const dlx_vm_elem& el = L.elem[e];
     if (el.kind != DLX_VM_REDUCE) continue;
@@ -171,7 +275,8 @@ using namespace dlx;
 extern "C" {
 
 size_t dlx_vm_workspace_bytes(int64_t range) {
-  return static_cast<size_t>(vm_grid(range)) * DLX_VM_MAX_ELEMS * sizeof(Reg) + 1024;
+  // reduce partials, append counts, append offsets
+  return 3 * static_cast<size_t>(vm_grid(range)) * DLX_VM_MAX_ELEMS * sizeof(Reg) + 1024;
 }
 
 int dlx_vm_run_loop(const dlx_vm_instr* d_code, const dlx_vm_loop* h_loop, int64_t* d_results,
@@ -185,10 +290,23 @@ int dlx_vm_run_loop(const dlx_vm_instr* d_code, const dlx_vm_loop* h_loop, int64
     return DLX_OK;
   }
   const int grid = vm_grid(L.range);
-  DLX_REQUIRE(d_workspace && workspace_bytes >= static_cast<size_t>(grid) * DLX_VM_MAX_ELEMS * sizeof(Reg),
+  DLX_REQUIRE(d_workspace && workspace_bytes >= 3 * static_cast<size_t>(grid) * DLX_VM_MAX_ELEMS * sizeof(Reg),
               DLX_ERR_ARG, "vm: workspace too small");
+  bool append = false;
+  for (int e = 0; e < L.nelems; ++e) append |= L.elem[e].kind == DLX_VM_APPEND;
   Reg* parts = static_cast<Reg*>(d_workspace);
-  vm_loop_kernel<<<grid, kVmThreads, 0, stream>>>(d_code, L, parts, d_trap);
+  long long* counts = reinterpret_cast<long long*>(parts + static_cast<size_t>(grid) * DLX_VM_MAX_ELEMS);
+  long long* offsets = counts + static_cast<size_t>(grid) * DLX_VM_MAX_ELEMS;
+  long long chunk = 0;
+  if (append) {
+    chunk = (L.range + grid - 1) / grid;
+    vm_count_kernel<<<grid, kVmThreads, 0, stream>>>(d_code, L, chunk, counts, d_trap);
+    DLX_LAUNCHED("vm_count_kernel");
+    vm_scan_kernel<<<1, DLX_VM_MAX_ELEMS, 0, stream>>>(counts, grid, L, offsets,
+                                                       reinterpret_cast<long long*>(d_results));
+    DLX_LAUNCHED("vm_scan_kernel");
+  }
+  vm_loop_kernel<<<grid, kVmThreads, 0, stream>>>(d_code, L, parts, d_trap, chunk, offsets);
   DLX_LAUNCHED("vm_loop_kernel");
   vm_final_kernel<<<1, DLX_VM_MAX_ELEMS, 0, stream>>>(parts, grid, L, reinterpret_cast<long long*>(d_results));
   DLX_LAUNCHED("vm_final_kernel");

@@ -1,0 +1,2 @@
+set -u
+bash scripts/gpu_round.sh r32 bench benchref ncu

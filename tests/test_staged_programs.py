@@ -43,7 +43,7 @@ def same_value(a: str, b: str, rtol=1e-9) -> bool:
 def test_fixtures_present():
     names = {os.path.basename(f)[:-5] for f in FIXTURES}
     for n in ("kmeans_n65536_d16_k8_it1", "kmeans_n4096_d16_k8_it2", "groupby_n100000_k16", "gda_n20000_d4",
-              "mean_variance_n100000", "axpy_n100000", "count_gt_n100000"):
+              "mean_variance_n100000", "axpy_n100000", "count_gt_n100000", "find_count_n100000"):
         assert n in names
     for f in FIXTURES:
         with open(f) as fh:
@@ -122,19 +122,59 @@ def test_unlowerable_loop_fails_loudly():
     from paper_1109_0778_b200.program import run_program
     fx = load("count_gt_n100000")
     prog = json.loads(json.dumps(fx["program"]))
-    # turn the loop's first live elem into a filter-collect (append): not lowered yet
+    # turn the loop's first live elem into a foreach (effectful disjoint writes): not lowered
     for st in prog["stmts"].values():
         if "loop" in st:
-            st["loop"]["elems"][0]["kind"] = "collect"
-            st["loop"]["elems"][0]["append"] = True
+            st["loop"]["elems"][0]["kind"] = "foreach"
             break
     with pytest.raises(GenerationFailed):
+        run_program(prog, seed=1)
+
+
+def _patch_literal(prog, old, new):
+    """Replace a double literal of the staged descriptor (the filter threshold)."""
+    txt = json.dumps(prog)
+    assert txt.count(json.dumps(old)) >= 1
+    return json.loads(txt.replace(json.dumps(old), json.dumps(new)))
+
+
+def _find_count_expected(n, thr):
+    import numpy as np
+    import oracle as O
+    x = O.rng_units(1, 0, n)
+    hits = np.nonzero(thr < x)[0]
+    return hits
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("thr", [0.9, 0.5, -1.0, 0.999999])
+def test_filter_collect_thresholds(thr):
+    """Filter-collect (append) through the generic kernel's ordered compaction: every
+    selected index, in index order, for sparse / half / all-selected filters."""
+    from paper_1109_0778_b200.program import run_program
+    prog = _patch_literal(load("find_count_n100000")["program"], 0.9, thr)
+    text, report = run_program(prog, seed=1)
+    hits = _find_count_expected(100000, thr)
+    got = lines(text)
+    assert [int(v) for v in got] == [len(hits), len(hits), int(hits[0]), int(hits.sum())]
+    assert [r["family"] for r in report] == ["generic", "generic"]
+
+
+@pytest.mark.gpu
+def test_filter_collect_empty_traps_on_read():
+    """Nothing selected: the appended vector is empty and reading element 0 traps
+    (TrapIndexOutOfBounds, as the reference's x(0) on an empty builder)."""
+    from paper_1109_0778_b200 import TrapError
+    from paper_1109_0778_b200.program import run_program
+    prog = _patch_literal(load("find_count_n100000")["program"], 0.9, 2.0)
+    with pytest.raises(TrapError):
         run_program(prog, seed=1)
 
 
 EXPECTED_FAMILIES = {
     "axpy_n100000": ["generic", "generic"],
     "count_gt_n100000": ["generic"],
+    "find_count_n100000": ["generic", "generic"],
     "gda_n20000_d4": ["generic", "gda_scatter"],
     "groupby_n100000_k16": ["groupby"],
     "kmeans_n4096_d16_k8_it2": ["kmeans", "kmeans"],
