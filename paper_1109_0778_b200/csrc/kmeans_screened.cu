@@ -593,6 +593,33 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       tc_fence_after();
       int tv[64];
       int lmin = kInvalidNm;
+#ifdef DLX_KMEANS_EPI_X16
+      // 16 centroids per step: two x16 TMEM loads (HH, CR), fold them, then W1, W2
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        const uint32_t col = 16 * ch;
+        int a16[16], b16[16], p16[16];
+        tmem_ld16(tmem + lane_base + col, a16);
+        tmem_ld16(tmem + lane_base + col + 64, b16);
+        tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 16; ++u) p16[u] = a16[u] * 256 + b16[u];
+        tmem_ld16(tmem + lane_base + col + 128, a16);
+        tmem_ld16(tmem + lane_base + col + 192, b16);
+        const int4 n0 = nm4[4 * ch], n1 = nm4[4 * ch + 1], n2 = nm4[4 * ch + 2], n3 = nm4[4 * ch + 3];
+        const int nm[16] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w,
+                            n2.x, n2.y, n2.z, n2.w, n3.x, n3.y, n3.z, n3.w};
+        tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          // invalid centroids: zero B rows (Q = 0) and nm = kInvalidNm
+          const int Q = p16[u] + (a16[u] >> 8) + (b16[u] >> 16);
+          const int v = nm[u] - 2 * Q;
+          tv[16 * ch + u] = v;
+          lmin = min(lmin, v);
+        }
+      }
+#else
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
         const uint32_t col = 8 * ch;
@@ -613,6 +640,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
           lmin = min(lmin, v);
         }
       }
+#endif
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.t_empty);

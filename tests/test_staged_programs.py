@@ -147,7 +147,7 @@ def _find_count_expected(n, thr):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("thr", [0.9, 0.5, -1.0, 0.999999])
+@pytest.mark.parametrize("thr", [0.9, 0.5, -1.0, 0.9999])
 def test_filter_collect_thresholds(thr):
     """Filter-collect (append) through the generic kernel's ordered compaction: every
     selected index, in index order, for sparse / half / all-selected filters."""
