@@ -270,7 +270,6 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
     lo, hi = shard_range(n, rank, world)
     n_local = hi - lo
     stream = torch.cuda.current_stream()
-    launches_per_step = 0
     d = p.get("d", 0)
 
     if family == "kmeans":
@@ -287,7 +286,6 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
                 comm.allreduce_(prog.counts)
                 comm.allreduce_(prog.sums)
             ml.kmeans_update(prog.counts, prog.sums, prog.mu)
-        launches_per_step = 3
     elif family == "logreg":
         x = ml.rng_units(n_local * d, seed=1, first_draw=lo * d, device=dev).view(n_local, d)
         y = ml.rng_ints(n_local, 2, seed=1, first_draw=n * d + lo, device=dev)
@@ -299,7 +297,6 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             if comm is not None:
                 comm.allreduce_(prog.grad)
             ml.axpy_inplace(prog.theta, prog.grad, prog.alpha)
-        launches_per_step = 3
     elif family == "gda":
         x = ml.rng_units(n_local * d, seed=1, first_draw=lo * d, device=dev).view(n_local, d)
         y = ml.rng_ints(n_local, 2, seed=1, first_draw=n * d + lo, device=dev)
@@ -317,7 +314,6 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             S = ml.gda_pass2(x, y, mu0, mu1)
             if comm is not None:
                 comm.allreduce_(S)
-        launches_per_step = 8
     else:
         K = p["K"]
         keys = ml.rng_ints(n_local, K, seed=1, first_draw=lo, device=dev)
@@ -328,7 +324,6 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             kernel_fn()
             if comm is not None:
                 comm.allreduce_(counts)
-        launches_per_step = 2
 
     # warm-up
     for _ in range(args.warmup):
@@ -344,6 +339,8 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
+    L = _lib.load()
+    launches0 = int(L.dlx_launch_count())
     t_start.record(stream)
     for s in range(args.steps):
         ev[s][0].record(stream)
@@ -375,6 +372,7 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             if comm is not None:
                 comm.allreduce_(S)
     t_end.record(stream)
+    launches = int(L.dlx_launch_count()) - launches0   # this library's kernels in the timed region
     torch.cuda.synchronize()
     barrier()
     clocks = sampler.stop()
@@ -422,7 +420,7 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
                          "peak_kind": peak_kind, "kernel_ms": kern_ms,
                          "algorithmic_bytes_per_launch": bytes_launch},
             "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": launches,
             "clocks": clocks,
         }
         if world == 1 and not args.no_cpu_baseline:

@@ -46,6 +46,8 @@ enum {
 
 const char* dlx_last_error(void);
 const char* dlx_version(void);
+/* kernels this library has launched since it was loaded (all devices, all threads) */
+uint64_t dlx_launch_count(void);
 
 /* ---- device / memory (device mirrors of VecData, runtime.hpp:44-72) ------------------ */
 int dlx_device_count(int* count);

@@ -50,6 +50,7 @@ _dbl = ctypes.c_double
 _SIGS = {
     "dlx_last_error": (ctypes.c_char_p, []),
     "dlx_version": (ctypes.c_char_p, []),
+    "dlx_launch_count": (_u64, []),
     "dlx_device_count": (_int, [ctypes.POINTER(_int)]),
     "dlx_set_device": (_int, [_int]),
     "dlx_sm_count": (_int, [ctypes.POINTER(_int)]),

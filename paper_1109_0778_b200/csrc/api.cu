@@ -1,4 +1,5 @@
 // api.cu — error state, device/memory/stream plumbing and the synthetic Rng sources.
+#include <atomic>
 #include <cstdarg>
 #include <mutex>
 #include <vector>
@@ -78,6 +79,9 @@ static int launch_rng(void* out, int64_t n, int64_t bound, uint64_t seed, uint64
   return DLX_OK;
 }
 
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 }  // namespace dlx
 
 using namespace dlx;
@@ -85,6 +89,7 @@ using namespace dlx;
 extern "C" {
 
 const char* dlx_last_error(void) { return g_last_error.c_str(); }
+uint64_t dlx_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 const char* dlx_version(void) { return "dlx 0.1 (sm_100a)"; }
 
 int dlx_device_count(int* count) {

@@ -18,6 +18,10 @@ namespace dlx {
 // Thread-local last-error text, returned by dlx_last_error().
 void set_error(const char* fmt, ...);
 
+// Kernels launched by this library since load (incremented by DLX_LAUNCHED on success):
+// the bench reports it as gpu_launches, evidence that the native path ran.
+void count_launch();
+
 inline int cuda_fail(cudaError_t e, const char* what) {
   set_error("%s: %s", what, cudaGetErrorString(e));
   return DLX_ERR_CUDA;
@@ -33,6 +37,7 @@ inline int cuda_fail(cudaError_t e, const char* what) {
   do {                                                    \
     cudaError_t _e = cudaGetLastError();                  \
     if (_e != cudaSuccess) return ::dlx::cuda_fail(_e, name); \
+    ::dlx::count_launch();                                \
   } while (0)
 
 #define DLX_REQUIRE(cond, code, ...)                      \
