@@ -101,6 +101,24 @@ def test_kmeans_screened_shapes(ml, n, d, k):
     check_step(ml, x, mu, SCREENED)
 
 
+@pytest.mark.parametrize("n,k", [(128, 64), (255, 64), (128 * 148 + 1, 64), (40_000, 32), (40_000, 1)])
+def test_kmeans_screened_tile_edges(ml, n, k):
+    """d = 64 tile edges: exactly one tile, a shifted last tile overlapping its predecessor,
+    one row past a full wave of CTAs, and fewer centroids than one N half."""
+    x = dev_units(ml, n, 64, seed=n + k)
+    mu = dev_units(ml, k, 64, seed=11)
+    check_step(ml, x, mu, SCREENED)
+
+
+def test_kmeans_screened_unaligned_rows(ml):
+    """Rows starting 16 bytes past a 32-byte boundary take the 16-byte-load variant."""
+    n, d, k = 30_001, 64, 64
+    base = dev_units(ml, n * d + 2, 1, seed=3).view(-1)
+    x = base[2:].view(n, d)
+    assert x.data_ptr() % 32 == 16
+    check_step(ml, x, dev_units(ml, k, d, seed=4), SCREENED)
+
+
 def _stress_inputs(kind, n=20_000, d=64, k=64):
     g = torch.Generator(device="cpu").manual_seed(zlib.crc32(kind.encode()))
     x = torch.rand(n, d, generator=g, dtype=torch.float64)
