@@ -1,37 +1,39 @@
 // combine.cu — the combine step of the activation-record protocol (the
 // runtime merges per-chunk records with combine(__act, rhs)).  Each multiloop kernel writes
-// one partial record per CTA; this kernel folds them with a fixed shape (8 warps x strided
-// partials, then an ordered 8-way sum), so results are deterministic for a given grid and
+// one partial record per CTA; this kernel folds them with a fixed shape (32 warps x strided
+// partials, then an ordered 32-way sum), so results are deterministic for a given grid and
 // the partial loads are coalesced and issued many at a time instead of as one sequential
 // chain per output.
 #include "common.cuh"
 
 namespace dlx {
 
+constexpr int kCombWarps = 32;   // warps per block: partial p goes to warp p % 32
+
 template <class Tin, class Tout>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kCombWarps * 32)
 combine_partials_kernel(const Tin* __restrict__ parts, int nparts, long long width,
                         Tout* __restrict__ out) {
-  __shared__ Tout red[8][33];
+  __shared__ Tout red[kCombWarps][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long e = static_cast<long long>(blockIdx.x) * 32 + lane;
   Tout a0 = 0, a1 = 0, a2 = 0, a3 = 0;
   if (e < width) {
     int p = warp;
-    for (; p + 24 < nparts; p += 32) {
+    for (; p + 3 * kCombWarps < nparts; p += 4 * kCombWarps) {
       a0 += static_cast<Tout>(parts[static_cast<size_t>(p) * width + e]);
-      a1 += static_cast<Tout>(parts[static_cast<size_t>(p + 8) * width + e]);
-      a2 += static_cast<Tout>(parts[static_cast<size_t>(p + 16) * width + e]);
-      a3 += static_cast<Tout>(parts[static_cast<size_t>(p + 24) * width + e]);
+      a1 += static_cast<Tout>(parts[static_cast<size_t>(p + kCombWarps) * width + e]);
+      a2 += static_cast<Tout>(parts[static_cast<size_t>(p + 2 * kCombWarps) * width + e]);
+      a3 += static_cast<Tout>(parts[static_cast<size_t>(p + 3 * kCombWarps) * width + e]);
     }
-    for (; p < nparts; p += 8) a0 += static_cast<Tout>(parts[static_cast<size_t>(p) * width + e]);
+    for (; p < nparts; p += kCombWarps) a0 += static_cast<Tout>(parts[static_cast<size_t>(p) * width + e]);
   }
   red[warp][lane] = (a0 + a1) + (a2 + a3);
   __syncthreads();
   if (warp == 0 && e < width) {
     Tout s = red[0][lane];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) s += red[w][lane];
+    for (int w = 1; w < kCombWarps; ++w) s += red[w][lane];
     out[e] = s;
   }
 }
@@ -41,7 +43,7 @@ static int launch_combine(const Tin* parts, int nparts, long long width, Tout* o
                           cudaStream_t stream) {
   if (width <= 0) return DLX_OK;
   const long long blocks = (width + 31) / 32;
-  combine_partials_kernel<Tin, Tout><<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+  combine_partials_kernel<Tin, Tout><<<static_cast<unsigned>(blocks), kCombWarps * 32, 0, stream>>>(
       parts, nparts, width, out);
   DLX_LAUNCHED("combine_partials_kernel");
   return DLX_OK;

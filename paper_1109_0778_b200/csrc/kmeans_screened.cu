@@ -775,15 +775,14 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
 }
 
 // ---------------------------------------------------------------------------------------
-// resolve: the reference chain for the pending samples.  Resolve CTA rb handles slice
-// rb % kResSplit of main-kernel CTA rb / kResSplit's pending list, in chunks of kResChunk
-// samples: the chunk's rows are gathered into shared memory next to the fp64 centroids,
-// every (sample, candidate) pair is one thread's exact chain (sequential j, no FMA), each
-// sample then merges its candidates in ascending centroid order (strict <, NaN never
-// wins, start (1e300, 0)), and the rows are folded into this CTA's partial record in list
-// order (deterministic).
+// resolve: the reference chain for the pending samples.  Resolve CTA rb handles main-kernel
+// CTA rb's pending list in chunks of kResChunk samples: the chunk's rows are gathered into
+// shared memory next to the fp64 centroids, every (sample, candidate) pair is one thread's
+// exact chain (sequential j, no FMA), each sample then merges its candidates in ascending
+// centroid order (strict <, NaN never wins, start (1e300, 0)), and the rows are folded, in
+// list order, into CTA rb's partial record (deterministic; CTAs without pending rows exit).
 constexpr int kResThreads = 256;
-constexpr int kResSplit = 4;
+constexpr int kResSplit = 1;   // one resolve CTA per main CTA: it folds into that CTA's record
 constexpr int kResChunk = 64;
 constexpr int kResMaxPairs = kResChunk * kMaxK;
 
@@ -806,14 +805,18 @@ kmeans_resolve_kernel(const double* __restrict__ x, int d, int k, const double* 
   const int tid = threadIdx.x;
   const int src = blockIdx.x / kResSplit, slice = blockIdx.x % kResSplit;
   const long long total = pend_count[src];
+  if (total == 0) return;   // the main kernel's record is already complete
   const long long lo = total * slice / kResSplit, hi = total * (slice + 1) / kResSplit;
   const long long* pidx = pend_idx + static_cast<size_t>(src) * pend_cap;
   const unsigned long long* pmask = pend_mask + static_cast<size_t>(src) * pend_cap;
+  // continue the main kernel's partial record of CTA src (its screened rows), then write it back
+  double* ps = part_sums + static_cast<size_t>(src) * k * d;
+  long long* pc = part_counts + static_cast<size_t>(src) * k;
   for (int e = tid; e < k * d; e += kResThreads) {
     mu_s[e] = mu[e];
-    sums_s[e] = 0.0;
+    sums_s[e] = ps[e];
   }
-  for (int c = tid; c < k; c += kResThreads) cnt_s[c] = 0;
+  for (int c = tid; c < k; c += kResThreads) cnt_s[c] = pc[c];
   constexpr int R = kResThreads / 64;
   const int jj = tid & 63, rr = tid >> 6;
   for (long long base = lo; base < hi; base += kResChunk) {
@@ -890,9 +893,8 @@ kmeans_resolve_kernel(const double* __restrict__ x, int d, int k, const double* 
     }
   }
   __syncthreads();
-  double* ps = part_sums + static_cast<size_t>(blockIdx.x) * k * d;
   for (int e = tid; e < k * d; e += kResThreads) ps[e] = sums_s[e];
-  for (int c = tid; c < k; c += kResThreads) part_counts[static_cast<size_t>(blockIdx.x) * k + c] = cnt_s[c];
+  for (int c = tid; c < k; c += kResThreads) pc[c] = cnt_s[c];
 }
 
 }  // namespace sk
@@ -909,8 +911,8 @@ static long long pend_capacity(int64_t n, int grid) {
 
 struct ScreenedWs {
   long long* pend_count;
-  long long* part_counts;  // [(1+kResSplit)*grid][k]: main kernel, then resolve kernel
-  double* part_sums;       // [(1+kResSplit)*grid][k*d]
+  long long* part_counts;  // [grid][k]: main kernel record, completed by the resolve kernel
+  double* part_sums;       // [grid][k*d]
   long long* pend_idx;     // [grid][cap]
   unsigned long long* pend_mask;
   size_t used;
@@ -921,7 +923,7 @@ static ScreenedWs carve_screened(void* base, int64_t n, int d, int k, int grid) 
   Carve c(base);
   ScreenedWs w;
   w.pend_count = c.take<long long>(grid);
-  const int parts = (1 + sk::kResSplit) * grid;
+  const int parts = grid;
   w.part_counts = c.take<long long>(static_cast<size_t>(parts) * k);
   w.part_sums = c.take<double>(static_cast<size_t>(parts) * k * d);
   w.pend_idx = c.take<long long>(static_cast<size_t>(grid) * cap);
@@ -1004,9 +1006,9 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsmem)));
   sk::kmeans_resolve_kernel<<<grid * sk::kResSplit, sk::kResThreads, rsmem, stream>>>(
       x, d, k, mu, assign, w.pend_idx, w.pend_mask, w.pend_count, cap,
-      w.part_counts + static_cast<size_t>(grid) * k, w.part_sums + static_cast<size_t>(grid) * k * d);
+      w.part_counts, w.part_sums);
   DLX_LAUNCHED("kmeans_resolve_kernel");
-  return kmeans_finalize(w.part_counts, w.part_sums, (1 + sk::kResSplit) * grid, k, d, counts, sums,
+  return kmeans_finalize(w.part_counts, w.part_sums, grid, k, d, counts, sums,
                          stream);
 }
 
