@@ -375,7 +375,11 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
             const uint64_t adesc = sw128_kmajor_desc(a0 + g * kPlane2 + kk * 4096);  // MN-major
+#ifndef DLX_KMEANS_DIAG_NOFOLD   // diagnostic only: times the pipeline without the fold MMAs
             mma_i8(tmem + kFoldCol + 64 * g, adesc, bdesc, ID_fold, (nf > 0 || kk > 0) ? 1u : 0u);
+#else
+            (void)adesc; (void)bdesc;
+#endif
           }
         }
         mma_commit(&S.a_empty[nf % kNumA]);
@@ -593,7 +597,37 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       tc_fence_after();
       int tv[64];
       int lmin = kInvalidNm;
-#ifdef DLX_KMEANS_EPI_X16
+#ifdef DLX_KMEANS_EPI_PIPE
+      // software-pipelined drain: the x4 loads of the next 4 centroids are in flight while the
+      // current 4 are scored (tcgen05.wait::ld waits for all outstanding loads)
+      int cur[4][4], nxt[4][4];
+#pragma unroll
+      for (int g4 = 0; g4 < 4; ++g4) tmem_ld4(tmem + lane_base + 64 * g4, cur[g4]);
+      tmem_ld_wait();
+#pragma unroll
+      for (int ch = 0; ch < 16; ++ch) {
+        if (ch + 1 < 16) {
+#pragma unroll
+          for (int g4 = 0; g4 < 4; ++g4) tmem_ld4(tmem + lane_base + 64 * g4 + 4 * (ch + 1), nxt[g4]);
+        }
+        const int4 n0 = nm4[ch];
+        const int nm[4] = {n0.x, n0.y, n0.z, n0.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int Q = cur[0][u] * 256 + cur[1][u] + (cur[2][u] >> 8) + (cur[3][u] >> 16);
+          const int v = nm[u] - 2 * Q;
+          tv[4 * ch + u] = v;
+          lmin = min(lmin, v);
+        }
+        if (ch + 1 < 16) {
+          tmem_ld_wait();
+#pragma unroll
+          for (int g4 = 0; g4 < 4; ++g4)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) cur[g4][u] = nxt[g4][u];
+        }
+      }
+#elif defined(DLX_KMEANS_EPI_X16)
       // 16 centroids per step: two x16 TMEM loads (HH, CR), fold them, then W1, W2
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
