@@ -283,8 +283,7 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
         def step():
             kernel_fn()
             if comm is not None:
-                comm.allreduce_(prog.counts)
-                comm.allreduce_(prog.sums)
+                comm.allreduce_many_([prog.counts, prog.sums])
             ml.kmeans_update(prog.counts, prog.sums, prog.mu)
     elif family == "logreg":
         x = ml.rng_units(n_local * d, seed=1, first_draw=lo * d, device=dev).view(n_local, d)
@@ -309,7 +308,7 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             kernel_fn()
             n1, s0, s1 = holder["r"]
             if comm is not None:
-                comm.allreduce_(n1); comm.allreduce_(s0); comm.allreduce_(s1)
+                comm.allreduce_many_([n1, s0, s1])
             mu0, mu1 = ml.gda_means(n1, s0, s1, n)
             S = ml.gda_pass2(x, y, mu0, mu1)
             if comm is not None:
@@ -351,8 +350,7 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             # remainder of the step (allreduce + update)
             if family == "kmeans":
                 if comm is not None:
-                    comm.allreduce_(prog.counts)
-                    comm.allreduce_(prog.sums)
+                    comm.allreduce_many_([prog.counts, prog.sums])
                 ml.kmeans_update(prog.counts, prog.sums, prog.mu)
             elif family == "logreg":
                 if comm is not None:
@@ -366,7 +364,7 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             ev[s][1].record(stream)
             n1, s0, s1 = holder["r"]
             if comm is not None:
-                comm.allreduce_(n1); comm.allreduce_(s0); comm.allreduce_(s1)
+                comm.allreduce_many_([n1, s0, s1])
             mu0, mu1 = ml.gda_means(n1, s0, s1, n)
             S = ml.gda_pass2(x, y, mu0, mu1)
             if comm is not None:

@@ -154,6 +154,10 @@ int dlx_comm_destroy(dlx_comm_t comm);
 /* in-place sum allreduce; dtype: 0 = fp64, 1 = int64 */
 int dlx_comm_allreduce_sum(dlx_comm_t comm, void* d_buf, int64_t count, int dtype,
                            dlx_stream_t stream);
+/* Several partial records reduced by one fused NCCL launch (ncclGroupStart/End): bufs[i] holds
+ * counts[i] elements of dtypes[i] (0 = f64, 1 = i64), each summed in place across ranks. */
+int dlx_comm_allreduce_sum_group(dlx_comm_t comm, void* const* d_bufs, const int64_t* counts,
+                                 const int* dtypes, int nbufs, dlx_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -94,6 +94,8 @@ _SIGS = {
     "dlx_comm_init": (_int, [ctypes.POINTER(_vp), ctypes.c_char_p, _int, _int]),
     "dlx_comm_destroy": (_int, [_vp]),
     "dlx_comm_allreduce_sum": (_int, [_vp, _vp, _i64, _int, _vp]),
+    "dlx_comm_allreduce_sum_group": (_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_i64),
+                                            ctypes.POINTER(_int), _int, _vp]),
 }
 
 # Every symbol include/dlx.h declares (checked by tests/test_abi.py).

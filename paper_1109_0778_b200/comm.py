@@ -53,6 +53,17 @@ class Comm:
                                                  ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
         return t
 
+    def allreduce_many_(self, tensors) -> None:
+        """Sum several records in place across ranks with one fused NCCL launch."""
+        if self.world == 1 or not tensors:
+            return
+        n = len(tensors)
+        bufs = (ctypes.c_void_p * n)(*[t.data_ptr() for t in tensors])
+        counts = (ctypes.c_int64 * n)(*[t.numel() for t in tensors])
+        dtypes = (ctypes.c_int * n)(*[{torch.float64: 0, torch.int64: 1}[t.dtype] for t in tensors])
+        check(_lib.load().dlx_comm_allreduce_sum_group(self._h, bufs, counts, dtypes, n,
+                                                       ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+
     def allreduce_int(self, v: int) -> int:
         if self.world == 1:
             return v

@@ -73,4 +73,27 @@ int dlx_comm_allreduce_sum(dlx_comm_t comm, void* d_buf, int64_t count, int dtyp
   return DLX_OK;
 }
 
+int dlx_comm_allreduce_sum_group(dlx_comm_t comm, void* const* d_bufs, const int64_t* counts,
+                                 const int* dtypes, int nbufs, dlx_stream_t stream) {
+  DLX_REQUIRE(comm && d_bufs && counts && dtypes && nbufs >= 0, DLX_ERR_ARG, "allreduce group: bad args");
+  for (int i = 0; i < nbufs; ++i)
+    DLX_REQUIRE((dtypes[i] == 0 || dtypes[i] == 1) && counts[i] >= 0 && (d_bufs[i] || counts[i] == 0),
+                DLX_ERR_ARG, "allreduce group: bad buffer %d", i);
+  if (comm->nranks == 1) return DLX_OK;
+  DLX_NCCL(ncclGroupStart());
+  for (int i = 0; i < nbufs; ++i) {
+    if (counts[i] == 0) continue;
+    const ncclResult_t r = ncclAllReduce(d_bufs[i], d_bufs[i], static_cast<size_t>(counts[i]),
+                                         dtypes[i] == 0 ? ncclFloat64 : ncclInt64, ncclSum,
+                                         comm->comm, stream);
+    if (r != ncclSuccess) {
+      ncclGroupEnd();
+      dlx::set_error("ncclAllReduce: %s", ncclGetErrorString(r));
+      return DLX_ERR_COMM;
+    }
+  }
+  DLX_NCCL(ncclGroupEnd());
+  return DLX_OK;
+}
+
 }  // extern "C"

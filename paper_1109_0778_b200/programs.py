@@ -37,8 +37,7 @@ class KMeansProgram:
         ml.kmeans_step(self.x, self.mu, self.assign, self.counts, self.sums, method=self.method,
                        want_assign=self.assign is not None)
         if self.comm is not None:
-            self.comm.allreduce_(self.counts)
-            self.comm.allreduce_(self.sums)
+            self.comm.allreduce_many_([self.counts, self.sums])
         ml.kmeans_update(self.counts, self.sums, self.mu)
 
     def capture(self):
