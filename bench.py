@@ -29,6 +29,9 @@ CONFIGS = {
     "c4": ("kmeans", dict(n=16_777_216, d=64, k=64),
            "k-means iters/sec (N=16M,d=64,k=64) at 1/2/4/8 B200; fused-op HBM GB/s vs peak", "it/s"),
     "c1": ("kmeans", dict(n=65_536, d=16, k=8), "k-means iters/sec (N=65536,d=16,k=8)", "it/s"),
+    # diagnostic: one rank's C4 shard at 8 GPUs (per-iteration fixed costs vs scaling)
+    "c4shard8": ("kmeans", dict(n=16_777_216 // 8, d=64, k=64),
+                 "k-means iters/sec (N=2M shard of C4 at 8 GPUs, d=64, k=64)", "it/s"),
     "c2": ("logreg", dict(n=1_048_576, d=64), "logistic-regression BGD iters/sec (N=1M,d=64)", "it/s"),
     "l16": ("logreg", dict(n=16_777_216, d=64), "logistic-regression BGD iters/sec (N=16M,d=64)", "it/s"),
     "c3": ("gda", dict(n=1_048_576, d=64), "GDA fits/sec (N=1M,d=64)", "fits/s"),

@@ -206,6 +206,16 @@ __device__ __forceinline__ int elem_flag(double x, uint32_t hw_hi, uint32_t hw_l
   return (hw >= hw_hi ? 1 : 0) | ((hw < hw_lo && (hw | lw) != 0u) ? 2 : 0);
 }
 
+constexpr int kResChunk = 64;
+template <int NT, class Sync>
+__device__ __forceinline__ void resolve_list(int tid, Sync sync, const double* __restrict__ x, int d,
+                                             const double* __restrict__ mu_s, int32_t* __restrict__ assign,
+                                             const long long* __restrict__ pidx,
+                                             const unsigned long long* __restrict__ pmask, long long lo,
+                                             long long hi, double* sums_s, long long* cnt_s, double* rows_s,
+                                             double* dist_s, long long* idx_s, unsigned long long* mask_s,
+                                             int* first_s, int* a_s);
+
 template <int kD, bool kWide>
 __global__ void __launch_bounds__(kThreads, 1)
 kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
@@ -780,11 +790,14 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     }
     tc_fence_before();
     named_bar(1, 128);
+    // the record in shared memory (beyond the scratch), completed below by this CTA's own
+    // pending rows, then written once
+    double* sums_s = reinterpret_cast<double*>(smem + kOffA + 2 * kABuf);          // k*d
+    double* mu_s = sums_s + kMaxK * kMaxD;                                          // k*d
     {
       const int et = S.em + 1;
       const double unit = ldexp(1.0, et - 62);
       const unsigned __int128 off = (static_cast<unsigned __int128>(1) << 63) + (static_cast<unsigned __int128>(1) << 39);
-      double* ps = part_sums + static_cast<size_t>(blockIdx.x) * k * d;
       for (int e = q; e < kMaxK * 64; e += 128) {
         const int c = e >> 6, j = e & 63;
         if (c >= k || j >= d) continue;
@@ -796,10 +809,34 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         const long long th = static_cast<long long>(tot >> 64);
         const unsigned long long tl = static_cast<unsigned long long>(tot);
         const double v = __fma_rn(static_cast<double>(th), 18446744073709551616.0, static_cast<double>(tl));
-        ps[c * d + j] = v * unit;
+        sums_s[c * d + j] = v * unit;
       }
-      for (int c = q; c < k; c += 128) part_counts[static_cast<size_t>(blockIdx.x) * k + c] = S.cnt[c];
     }
+    const long long npend = pend_count[blockIdx.x];   // written by the tail warp before barrier 7
+    long long* cnt_s = reinterpret_cast<long long*>(smem + kOffOH);   // the one-hot buffers are free now
+    if (npend > 0) {
+      // resolve this CTA's pending rows in list order into the record (the chain over their
+      // candidates, sequential j, no FMA; strict <; start (1e300, 0))
+      for (int e = q; e < k * d; e += 128) mu_s[e] = mu[e];
+      for (int c = q; c < k; c += 128) cnt_s[c] = S.cnt[c];
+      double* rows_s = reinterpret_cast<double*>(smem + kOffA);                     // 64*d (scratch is done)
+      double* dist_s = rows_s + kResChunk * kMaxD;                                    // 64*64
+      long long* idx_s = cnt_s + kMaxK;
+      unsigned long long* mask_s = reinterpret_cast<unsigned long long*>(idx_s + kResChunk);
+      int* first_s = reinterpret_cast<int*>(mask_s + kResChunk);
+      int* a_s = first_s + kResChunk + 1;
+      named_bar(1, 128);   // everyone is done reading the scratch
+      resolve_list<128>(q, [] { named_bar(1, 128); }, x, d, mu_s, assign,
+                        pend_idx + static_cast<size_t>(blockIdx.x) * pend_cap,
+                        pend_mask + static_cast<size_t>(blockIdx.x) * pend_cap, 0, npend, sums_s, cnt_s,
+                        rows_s, dist_s, idx_s, mask_s, first_s, a_s);
+    } else {
+      for (int c = q; c < k; c += 128) cnt_s[c] = S.cnt[c];
+      named_bar(1, 128);
+    }
+    double* ps = part_sums + static_cast<size_t>(blockIdx.x) * k * d;
+    for (int e = q; e < k * d; e += 128) ps[e] = sums_s[e];
+    for (int c = q; c < k; c += 128) part_counts[static_cast<size_t>(blockIdx.x) * k + c] = cnt_s[c];
   }
   __syncthreads();
   if (warp == kWarpMma) {
@@ -816,10 +853,98 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
 // centroid order (strict <, NaN never wins, start (1e300, 0)), and the rows are folded, in
 // list order, into CTA rb's partial record (deterministic; CTAs without pending rows exit).
 constexpr int kResThreads = 256;
-constexpr int kResSplit = 1;   // one resolve CTA per main CTA: it folds into that CTA's record
-constexpr int kResChunk = 64;
 constexpr int kResMaxPairs = kResChunk * kMaxK;
 
+// The exact chain for a pending list [lo, hi) of one CTA, folded in list order into the record
+// (sums_s, cnt_s) in shared memory.  NT threads (tid in [0, NT)) synchronise with `sync`.
+template <int NT, class Sync>
+__device__ __forceinline__ void resolve_list(int tid, Sync sync, const double* __restrict__ x, int d,
+                                             const double* __restrict__ mu_s, int32_t* __restrict__ assign,
+                                             const long long* __restrict__ pidx,
+                                             const unsigned long long* __restrict__ pmask, long long lo,
+                                             long long hi, double* sums_s, long long* cnt_s, double* rows_s,
+                                             double* dist_s, long long* idx_s, unsigned long long* mask_s,
+                                             int* first_s, int* a_s) {
+  constexpr int R = NT / 64;
+  const int jj = tid & 63, rr = tid >> 6;
+  for (long long base = lo; base < hi; base += kResChunk) {
+    const int nrow = static_cast<int>(hi - base < kResChunk ? hi - base : kResChunk);
+    sync();
+    for (int e = tid; e < nrow; e += NT) {
+      idx_s[e] = pidx[base + e];
+      mask_s[e] = pmask[base + e];
+    }
+    sync();
+    if (tid < 32) {  // exclusive scan of candidate counts -> pair offsets
+      int run = 0;
+      for (int e0 = 0; e0 < nrow; e0 += 32) {
+        const int e = e0 + tid;
+        const int c = e < nrow ? __popcll(mask_s[e]) : 0;
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (tid >= o) incl += t;
+        }
+        if (e < nrow) first_s[e] = run + incl - c;
+        run += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (tid == 0) first_s[nrow] = run;
+    }
+    for (int e = tid; e < nrow * d; e += NT) {
+      const int r = e / d, j = e - r * d;
+      rows_s[e] = __ldg(x + idx_s[r] * d + j);
+    }
+    sync();
+    const int npairs = first_s[nrow];
+    for (int p = tid; p < npairs; p += NT) {
+      int r = 0;  // owning sample: last r with first_s[r] <= p
+      for (int step = kResChunk; step > 0; step >>= 1)
+        if (r + step < nrow && first_s[r + step] <= p) r += step;
+      unsigned long long m = mask_s[r];
+      for (int t = p - first_s[r]; t > 0; --t) m &= m - 1;  // the t-th candidate of r
+      const int c = __ffsll(static_cast<long long>(m)) - 1;
+      const double* xr = rows_s + r * d;
+      const double* mr = mu_s + c * d;
+      double acc = 0.0;
+      for (int j = 0; j < d; ++j) {
+        const double diff = __dsub_rn(xr[j], mr[j]);
+        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+      }
+      dist_s[p] = acc;
+    }
+    sync();
+    for (int r = tid; r < nrow; r += NT) {
+      double best = 1e300;
+      int bi = 0;
+      unsigned long long m = mask_s[r];
+      for (int p = first_s[r]; p < first_s[r + 1]; ++p) {
+        const int c = __ffsll(static_cast<long long>(m)) - 1;
+        m &= m - 1;
+        if (dist_s[p] < best) {
+          best = dist_s[p];
+          bi = c;
+        }
+      }
+      a_s[r] = bi;
+      if (assign) assign[idx_s[r]] = bi;
+    }
+    sync();
+    if (jj < d) {  // fold rows in list order; thread (rr, jj) owns cells (c, jj), c % R == rr
+      for (int r = 0; r < nrow; ++r) {
+        const int a = a_s[r];
+        if (a % R == rr) {
+          sums_s[a * d + jj] += rows_s[r * d + jj];
+          if (jj == 0) cnt_s[a] += 1;
+        }
+      }
+    }
+  }
+  sync();
+}
+
+// Stand-alone form (the screened kernel resolves its own list in its epilogue; this kernel
+// serves callers that screen without folding, and keeps the chain testable on its own).
 __global__ void __launch_bounds__(kResThreads)
 kmeans_resolve_kernel(const double* __restrict__ x, int d, int k, const double* __restrict__ mu,
                       int32_t* __restrict__ assign, const long long* __restrict__ pend_idx,
@@ -837,13 +962,9 @@ kmeans_resolve_kernel(const double* __restrict__ x, int d, int k, const double* 
   __shared__ int a_s[kResChunk];
   __shared__ long long cnt_s[kMaxK];
   const int tid = threadIdx.x;
-  const int src = blockIdx.x / kResSplit, slice = blockIdx.x % kResSplit;
+  const int src = blockIdx.x;
   const long long total = pend_count[src];
   if (total == 0) return;   // the main kernel's record is already complete
-  const long long lo = total * slice / kResSplit, hi = total * (slice + 1) / kResSplit;
-  const long long* pidx = pend_idx + static_cast<size_t>(src) * pend_cap;
-  const unsigned long long* pmask = pend_mask + static_cast<size_t>(src) * pend_cap;
-  // continue the main kernel's partial record of CTA src (its screened rows), then write it back
   double* ps = part_sums + static_cast<size_t>(src) * k * d;
   long long* pc = part_counts + static_cast<size_t>(src) * k;
   for (int e = tid; e < k * d; e += kResThreads) {
@@ -851,82 +972,10 @@ kmeans_resolve_kernel(const double* __restrict__ x, int d, int k, const double* 
     sums_s[e] = ps[e];
   }
   for (int c = tid; c < k; c += kResThreads) cnt_s[c] = pc[c];
-  constexpr int R = kResThreads / 64;
-  const int jj = tid & 63, rr = tid >> 6;
-  for (long long base = lo; base < hi; base += kResChunk) {
-    const int nrow = static_cast<int>(hi - base < kResChunk ? hi - base : kResChunk);
-    __syncthreads();
-    for (int e = tid; e < nrow; e += kResThreads) {
-      idx_s[e] = pidx[base + e];
-      mask_s[e] = pmask[base + e];
-    }
-    __syncthreads();
-    if (tid < 32) {  // exclusive scan of candidate counts -> pair offsets
-      int run = 0;
-      for (int e0 = 0; e0 < nrow; e0 += 32) {
-        const int e = e0 + tid;
-        const int c = e < nrow ? __popcll(mask_s[e]) : 0;
-        int incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (tid >= o) incl += t;
-        }
-        if (e < nrow) first_s[e] = run + incl - c;
-        run += __shfl_sync(0xffffffffu, incl, 31);
-      }
-      if (tid == 0) first_s[nrow] = run;
-    }
-    for (int e = tid; e < nrow * d; e += kResThreads) {
-      const int r = e / d, j = e - r * d;
-      rows_s[e] = __ldg(x + idx_s[r] * d + j);
-    }
-    __syncthreads();
-    const int npairs = first_s[nrow];
-    for (int p = tid; p < npairs; p += kResThreads) {
-      int r = 0;  // owning sample: last r with first_s[r] <= p
-      for (int step = kResChunk; step > 0; step >>= 1)
-        if (r + step < nrow && first_s[r + step] <= p) r += step;
-      unsigned long long m = mask_s[r];
-      for (int t = p - first_s[r]; t > 0; --t) m &= m - 1;  // the t-th candidate of r
-      const int c = __ffsll(static_cast<long long>(m)) - 1;
-      const double* xr = rows_s + r * d;
-      const double* mr = mu_s + c * d;
-      double acc = 0.0;
-      for (int j = 0; j < d; ++j) {
-        const double diff = __dsub_rn(xr[j], mr[j]);
-        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
-      }
-      dist_s[p] = acc;
-    }
-    __syncthreads();
-    for (int r = tid; r < nrow; r += kResThreads) {
-      double best = 1e300;
-      int bi = 0;
-      unsigned long long m = mask_s[r];
-      for (int p = first_s[r]; p < first_s[r + 1]; ++p) {
-        const int c = __ffsll(static_cast<long long>(m)) - 1;
-        m &= m - 1;
-        if (dist_s[p] < best) {
-          best = dist_s[p];
-          bi = c;
-        }
-      }
-      a_s[r] = bi;
-      if (assign) assign[idx_s[r]] = bi;
-    }
-    __syncthreads();
-    if (jj < d) {  // fold rows in list order; thread (rr, jj) owns cells (c, jj), c % R == rr
-      for (int r = 0; r < nrow; ++r) {
-        const int a = a_s[r];
-        if (a % R == rr) {
-          sums_s[a * d + jj] += rows_s[r * d + jj];
-          if (jj == 0) cnt_s[a] += 1;
-        }
-      }
-    }
-  }
-  __syncthreads();
+  resolve_list<kResThreads>(tid, [] { __syncthreads(); }, x, d, mu_s, assign,
+                            pend_idx + static_cast<size_t>(src) * pend_cap,
+                            pend_mask + static_cast<size_t>(src) * pend_cap, 0, total, sums_s, cnt_s,
+                            rows_s, dist_s, idx_s, mask_s, first_s, a_s);
   for (int e = tid; e < k * d; e += kResThreads) ps[e] = sums_s[e];
   for (int c = tid; c < k; c += kResThreads) pc[c] = cnt_s[c];
 }
@@ -1034,14 +1083,6 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
       fprintf(stderr, "\n");
     }
   }
-  const size_t rsmem =
-      (static_cast<size_t>(2 * k + sk::kResChunk) * d + sk::kResMaxPairs) * sizeof(double);
-  DLX_CUDA(cudaFuncSetAttribute(sk::kmeans_resolve_kernel,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsmem)));
-  sk::kmeans_resolve_kernel<<<grid * sk::kResSplit, sk::kResThreads, rsmem, stream>>>(
-      x, d, k, mu, assign, w.pend_idx, w.pend_mask, w.pend_count, cap,
-      w.part_counts, w.part_sums);
-  DLX_LAUNCHED("kmeans_resolve_kernel");
   return kmeans_finalize(w.part_counts, w.part_sums, grid, k, d, counts, sums,
                          stream);
 }
