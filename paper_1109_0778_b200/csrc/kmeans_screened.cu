@@ -214,7 +214,7 @@ __device__ __forceinline__ void resolve_list(int tid, Sync sync, const double* _
                                              const unsigned long long* __restrict__ pmask, long long lo,
                                              long long hi, double* sums_s, long long* cnt_s, double* rows_s,
                                              double* dist_s, long long* idx_s, unsigned long long* mask_s,
-                                             int* first_s, int* a_s);
+                                             int* first_s, int* a_s, long long* tr = nullptr);
 
 template <int kD, bool kWide>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -227,12 +227,15 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
   // optional per-tile event clocks (build with -DDLX_KMEANS_TRACE, run with DLX_KMEANS_TRACE=1):
   // trace[(cta * kTraceTiles + m) * 8 + event]
 #ifdef DLX_KMEANS_TRACE
-#define TRACE_EV(m, ev) do { if (trace && (m) < kTraceTiles) trace[(static_cast<size_t>(blockIdx.x) * kTraceTiles + (m)) * 16 + (ev)] = clock64(); } while (0)
+#define TRACE_PH(ev) do { if (trace) trace[(static_cast<size_t>(blockIdx.x) * kTraceTiles + kTraceTiles - 1) * 16 + (ev)] = clock64(); } while (0)
+#define TRACE_EV(m, ev) do { if (trace && (m) < kTraceTiles - 1) trace[(static_cast<size_t>(blockIdx.x) * kTraceTiles + (m)) * 16 + (ev)] = clock64(); } while (0)
 #else
 #define TRACE_EV(m, ev) do { } while (0)
+#define TRACE_PH(ev) do { } while (0)
 #endif
   extern __shared__ __align__(1024) unsigned char smem[];
   Misc& S = *reinterpret_cast<Misc*>(smem + kOffMisc);
+  if (threadIdx.x == 0) TRACE_PH(0);
   constexpr bool kShift = kD == 64;   // the host launches the d = 64 variant only for n >= kTile
   unsigned char* Bm = smem + kOffB;
   const int tid = threadIdx.x;
@@ -264,25 +267,37 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     fence_mbar_init();
   }
   if (tid < kMaxK) S.cnt[tid] = 0;
+  // centroids into shared memory (the plane buffers are free until the first conversion), one
+  // coalesced pass; then one warp per centroid
+  double* mu_s = reinterpret_cast<double*>(smem + kOffA);   // [c][64]
+  for (int e = tid; e < k * d; e += kThreads) {
+    const int c = e / d, j = e - c * d;
+    mu_s[c * kMaxD + j] = __ldg(mu + e);
+  }
   __syncthreads();
-  if (tid < kMaxK) {  // per centroid: validity (all finite), max |mu| high word, |mu|^2
-    const int c = tid;
+  for (int c = warp; c < kMaxK; c += kThreads / 32) {  // validity (all finite), max |mu| high word, |mu|^2
     uint32_t mx = 0;
     bool ok = c < k;
     double nm = 0.0;
     if (ok) {
-      for (int j = 0; j < d; ++j) {
-        const double v = mu[c * d + j];
+      for (int j = lane; j < d; j += 32) {
+        const double v = mu_s[c * kMaxD + j];
         const uint32_t hw = static_cast<uint32_t>(__double2hiint(v)) & 0x7fffffffu;
         if (hw >= 0x7ff00000u) ok = false;
         mx = max(mx, hw);
-        nm += v * v;
+        nm += v * v;   // any summation order: |mu|^2 enters the bound through floor(.) with a unit of margin
       }
+      ok = __all_sync(0xffffffffu, ok);
+      mx = __reduce_max_sync(0xffffffffu, mx);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nm += __shfl_xor_sync(0xffffffffu, nm, o);
     }
-    S.nmf[c] = nm;
-    if (ok) {
-      atomicOr(&S.valid, 1ull << c);
-      atomicMax(&S.mu_maxhi, mx);
+    if (lane == 0) {
+      S.nmf[c] = nm;
+      if (ok) {
+        atomicOr(&S.valid, 1ull << c);
+        atomicMax(&S.mu_maxhi, mx);
+      }
     }
   }
   __syncthreads();
@@ -295,31 +310,28 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
   {
     const double scale = S.disabled ? 0.0 : ldexp(1.0, 22 - S.em);
     const unsigned long long valid = S.valid;
-    for (int e = tid; e < kMaxK * kMaxD; e += kThreads) {
-      const int c = e / kMaxD, j = e - c * kMaxD;
-      int Y = 0;
-      if (((valid >> c) & 1) && j < d) Y = rint_magic(mu[c * d + j] * scale);
-      // h'' = (Y >> 16) + 128 in [64, 192] (unsigned; the offset adds a per-sample constant to
-      // every centroid's score); invalid centroids and columns past d are all-zero rows
-      const bool live = ((valid >> c) & 1) && j < d;
-      Bm[sw64_offset(c, j)] = static_cast<unsigned char>(live ? (Y >> 16) + 128 : 0);
-      Bm[sw64_offset(64 + c, j)] = static_cast<unsigned char>(Y >> 8);
-      Bm[sw64_offset(128 + c, j)] = static_cast<unsigned char>(Y);
-    }
-    if (tid < kMaxK) {
+    for (int c = warp; c < kMaxK; c += kThreads / 32) {
+      const bool cv = (valid >> c) & 1;
       int sa = 0, ssum = 0;
-      if ((valid >> tid) & 1) {
-        for (int j = 0; j < d; ++j) {
-          const int Y = rint_magic(mu[tid * d + j] * scale);
-          sa += abs(Y);
-          ssum += Y;
-        }
-        atomicMax(&S.yabs, sa);
+      for (int j = lane; j < kMaxD; j += 32) {
+        // h'' = (Y >> 16) + 128 in [64, 192] (unsigned; the offset adds a per-sample constant to
+        // every centroid's score); invalid centroids and columns past d are all-zero rows
+        const bool live = cv && j < d;
+        const int Y = live ? rint_magic(mu_s[c * kMaxD + j] * scale) : 0;
+        Bm[sw64_offset(c, j)] = static_cast<unsigned char>(live ? (Y >> 16) + 128 : 0);
+        Bm[sw64_offset(64 + c, j)] = static_cast<unsigned char>(Y >> 8);
+        Bm[sw64_offset(128 + c, j)] = static_cast<unsigned char>(Y);
+        sa += abs(Y);
+        ssum += Y;
       }
-      // per-launch score constants (the sample exponent is fixed at e_t = e_m + 1)
-      S.nm0[tid] = (S.disabled || !((valid >> tid) & 1))
-                       ? kInvalidNm
-                       : __double2int_rd(S.nmf[tid] * ldexp(1.0, 19 - 2 * S.em)) + ssum;
+      sa = __reduce_add_sync(0xffffffffu, sa);
+      ssum = __reduce_add_sync(0xffffffffu, ssum);
+      if (lane == 0) {
+        if (cv) atomicMax(&S.yabs, sa);
+        // per-launch score constants (the sample exponent is fixed at e_t = e_m + 1)
+        S.nm0[c] = (S.disabled || !cv) ? kInvalidNm
+                                       : __double2int_rd(S.nmf[c] * ldexp(1.0, 19 - 2 * S.em)) + ssum;
+      }
     }
   }
   __syncthreads();
@@ -334,6 +346,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
+  if (threadIdx.x == 0) TRACE_PH(1);
 
   if (warp < kWarpE0) {
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsIssuer));
@@ -424,6 +437,9 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
           const long long slot = pending + __popc(pb & ((1u << lane) - 1));
           my_pidx[slot] = row0 + r;
           my_pmask[slot] = S.dec_mask[b][r];
+          // the exact re-check at the end of the launch gathers this row: keep it in L2
+          const char* xr = reinterpret_cast<const char*>(x + (row0 + r) * d);
+          for (int off = 0; off < d * 8; off += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(xr + off));
         }
         pending += __popc(pb);
       }
@@ -764,6 +780,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     // MMA has completed); then every (c, j) cell adds the two halves, removes the per-row
     // offset count_c * (2^63 + 2^39) and scales by 2^(e_t - 62).
     mbar_wait(&S.fold_done, 0);
+    if (q == 0) TRACE_PH(2);
     tc_fence_after();
     named_bar(7, 160);   // with the tail warp: every count is in S.cnt
     unsigned long long* scratch = reinterpret_cast<unsigned long long*>(smem + kOffA);
@@ -793,7 +810,6 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     // the record in shared memory (beyond the scratch), completed below by this CTA's own
     // pending rows, then written once
     double* sums_s = reinterpret_cast<double*>(smem + kOffA + 2 * kABuf);          // k*d
-    double* mu_s = sums_s + kMaxK * kMaxD;                                          // k*d
     {
       const int et = S.em + 1;
       const double unit = ldexp(1.0, et - 62);
@@ -812,28 +828,43 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         sums_s[c * d + j] = v * unit;
       }
     }
+    if (q == 0) TRACE_PH(3);
     const long long npend = pend_count[blockIdx.x];   // written by the tail warp before barrier 7
     long long* cnt_s = reinterpret_cast<long long*>(smem + kOffOH);   // the one-hot buffers are free now
     if (npend > 0) {
       // resolve this CTA's pending rows in list order into the record (the chain over their
       // candidates, sequential j, no FMA; strict <; start (1e300, 0))
-      for (int e = q; e < k * d; e += 128) mu_s[e] = mu[e];
       for (int c = q; c < k; c += 128) cnt_s[c] = S.cnt[c];
-      double* rows_s = reinterpret_cast<double*>(smem + kOffA);                     // 64*d (scratch is done)
-      double* dist_s = rows_s + kResChunk * kMaxD;                                    // 64*64
+      // the scratch is consumed: rows [64][d+1], distances, centroids [k][d+1] (padded strides)
+      double* rows_s = reinterpret_cast<double*>(smem + kOffA);
+      double* dist_s = rows_s + kResChunk * (kMaxD + 1);
+      double* mu_s = dist_s + kResChunk * kMaxK;
       long long* idx_s = cnt_s + kMaxK;
       unsigned long long* mask_s = reinterpret_cast<unsigned long long*>(idx_s + kResChunk);
       int* first_s = reinterpret_cast<int*>(mask_s + kResChunk);
       int* a_s = first_s + kResChunk + 1;
       named_bar(1, 128);   // everyone is done reading the scratch
+      {  // 16-byte loads, 8 per thread in flight
+        const double2* mu2 = reinterpret_cast<const double2*>(mu);
+        const int half = d / 2, total = k * half;
+#pragma unroll 8
+        for (int e = q; e < total; e += 128) {
+          const int c = e / half, j2 = e - c * half;
+          const double2 v = __ldg(mu2 + e);
+          mu_s[c * (d + 1) + 2 * j2] = v.x;
+          mu_s[c * (d + 1) + 2 * j2 + 1] = v.y;
+        }
+      }
       resolve_list<128>(q, [] { named_bar(1, 128); }, x, d, mu_s, assign,
                         pend_idx + static_cast<size_t>(blockIdx.x) * pend_cap,
                         pend_mask + static_cast<size_t>(blockIdx.x) * pend_cap, 0, npend, sums_s, cnt_s,
-                        rows_s, dist_s, idx_s, mask_s, first_s, a_s);
+                        rows_s, dist_s, idx_s, mask_s, first_s, a_s,
+                        trace ? trace + (static_cast<size_t>(blockIdx.x) * kTraceTiles + kTraceTiles - 1) * 16 + 8 : nullptr);
     } else {
       for (int c = q; c < k; c += 128) cnt_s[c] = S.cnt[c];
       named_bar(1, 128);
     }
+    if (q == 0) TRACE_PH(4);
     double* ps = part_sums + static_cast<size_t>(blockIdx.x) * k * d;
     for (int e = q; e < k * d; e += 128) ps[e] = sums_s[e];
     for (int c = q; c < k; c += 128) part_counts[static_cast<size_t>(blockIdx.x) * k + c] = cnt_s[c];
@@ -842,6 +873,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
   if (warp == kWarpMma) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem);
+    if (lane == 0) TRACE_PH(5);
   }
 }
 
@@ -852,8 +884,6 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
 // exact chain (sequential j, no FMA), each sample then merges its candidates in ascending
 // centroid order (strict <, NaN never wins, start (1e300, 0)), and the rows are folded, in
 // list order, into CTA rb's partial record (deterministic; CTAs without pending rows exit).
-constexpr int kResThreads = 256;
-constexpr int kResMaxPairs = kResChunk * kMaxK;
 
 // The exact chain for a pending list [lo, hi) of one CTA, folded in list order into the record
 // (sums_s, cnt_s) in shared memory.  NT threads (tid in [0, NT)) synchronise with `sync`.
@@ -864,8 +894,14 @@ __device__ __forceinline__ void resolve_list(int tid, Sync sync, const double* _
                                              const unsigned long long* __restrict__ pmask, long long lo,
                                              long long hi, double* sums_s, long long* cnt_s, double* rows_s,
                                              double* dist_s, long long* idx_s, unsigned long long* mask_s,
-                                             int* first_s, int* a_s) {
+                                             int* first_s, int* a_s, long long* tr) {
   constexpr int R = NT / 64;
+#ifdef DLX_KMEANS_TRACE
+  long long tacc[5] = {0, 0, 0, 0, 0}, t0 = clock64();
+#define RTR(i) do { const long long _t = clock64(); tacc[i] += _t - t0; t0 = _t; } while (0)
+#else
+#define RTR(i) do { } while (0)
+#endif
   const int jj = tid & 63, rr = tid >> 6;
   for (long long base = lo; base < hi; base += kResChunk) {
     const int nrow = static_cast<int>(hi - base < kResChunk ? hi - base : kResChunk);
@@ -875,6 +911,7 @@ __device__ __forceinline__ void resolve_list(int tid, Sync sync, const double* _
       mask_s[e] = pmask[base + e];
     }
     sync();
+    RTR(0);
     if (tid < 32) {  // exclusive scan of candidate counts -> pair offsets
       int run = 0;
       for (int e0 = 0; e0 < nrow; e0 += 32) {
@@ -891,11 +928,31 @@ __device__ __forceinline__ void resolve_list(int tid, Sync sync, const double* _
       }
       if (tid == 0) first_s[nrow] = run;
     }
-    for (int e = tid; e < nrow * d; e += NT) {
-      const int r = e / d, j = e - r * d;
-      rows_s[e] = __ldg(x + idx_s[r] * d + j);
+    {  // gather: 16-byte loads, up to 8 per thread in flight, into rows padded to stride d + 1
+      const int half = d / 2, total = nrow * half;
+      for (int e0 = tid; e0 < total; e0 += 8 * NT) {
+        double2 v[8];
+        int at[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = e0 + u * NT;
+          at[u] = -1;
+          if (e < total) {
+            const int r = e / half, j2 = e - r * half;
+            v[u] = __ldg(reinterpret_cast<const double2*>(x + idx_s[r] * d) + j2);
+            at[u] = r * (d + 1) + 2 * j2;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (at[u] >= 0) {
+            rows_s[at[u]] = v[u].x;
+            rows_s[at[u] + 1] = v[u].y;
+          }
+      }
     }
     sync();
+    RTR(1);
     const int npairs = first_s[nrow];
     for (int p = tid; p < npairs; p += NT) {
       int r = 0;  // owning sample: last r with first_s[r] <= p
@@ -904,16 +961,19 @@ __device__ __forceinline__ void resolve_list(int tid, Sync sync, const double* _
       unsigned long long m = mask_s[r];
       for (int t = p - first_s[r]; t > 0; --t) m &= m - 1;  // the t-th candidate of r
       const int c = __ffsll(static_cast<long long>(m)) - 1;
-      const double* xr = rows_s + r * d;
-      const double* mr = mu_s + c * d;
+      // padded stride d + 1: the lanes' rows / centroids fall in different banks
+      const double* xr = rows_s + r * (d + 1);
+      const double* mr = mu_s + c * (d + 1);
       double acc = 0.0;
-      for (int j = 0; j < d; ++j) {
+#pragma unroll 8
+      for (int j = 0; j < d; ++j) {   // the reference chain: sequential j, no FMA
         const double diff = __dsub_rn(xr[j], mr[j]);
         acc = __dadd_rn(acc, __dmul_rn(diff, diff));
       }
       dist_s[p] = acc;
     }
     sync();
+    RTR(2);
     for (int r = tid; r < nrow; r += NT) {
       double best = 1e300;
       int bi = 0;
@@ -930,54 +990,24 @@ __device__ __forceinline__ void resolve_list(int tid, Sync sync, const double* _
       if (assign) assign[idx_s[r]] = bi;
     }
     sync();
+    RTR(3);
     if (jj < d) {  // fold rows in list order; thread (rr, jj) owns cells (c, jj), c % R == rr
       for (int r = 0; r < nrow; ++r) {
         const int a = a_s[r];
         if (a % R == rr) {
-          sums_s[a * d + jj] += rows_s[r * d + jj];
+          sums_s[a * d + jj] += rows_s[r * (d + 1) + jj];
           if (jj == 0) cnt_s[a] += 1;
         }
       }
     }
+    RTR(4);
   }
   sync();
-}
-
-// Stand-alone form (the screened kernel resolves its own list in its epilogue; this kernel
-// serves callers that screen without folding, and keeps the chain testable on its own).
-__global__ void __launch_bounds__(kResThreads)
-kmeans_resolve_kernel(const double* __restrict__ x, int d, int k, const double* __restrict__ mu,
-                      int32_t* __restrict__ assign, const long long* __restrict__ pend_idx,
-                      const unsigned long long* __restrict__ pend_mask,
-                      const long long* __restrict__ pend_count, long long pend_cap,
-                      long long* __restrict__ part_counts, double* __restrict__ part_sums) {
-  extern __shared__ double rsm[];
-  double* mu_s = rsm;                          // k*d
-  double* sums_s = mu_s + k * d;               // k*d
-  double* rows_s = sums_s + k * d;             // kResChunk*d
-  double* dist_s = rows_s + kResChunk * d;     // kResMaxPairs
-  __shared__ long long idx_s[kResChunk];
-  __shared__ unsigned long long mask_s[kResChunk];
-  __shared__ int first_s[kResChunk + 1];
-  __shared__ int a_s[kResChunk];
-  __shared__ long long cnt_s[kMaxK];
-  const int tid = threadIdx.x;
-  const int src = blockIdx.x;
-  const long long total = pend_count[src];
-  if (total == 0) return;   // the main kernel's record is already complete
-  double* ps = part_sums + static_cast<size_t>(src) * k * d;
-  long long* pc = part_counts + static_cast<size_t>(src) * k;
-  for (int e = tid; e < k * d; e += kResThreads) {
-    mu_s[e] = mu[e];
-    sums_s[e] = ps[e];
-  }
-  for (int c = tid; c < k; c += kResThreads) cnt_s[c] = pc[c];
-  resolve_list<kResThreads>(tid, [] { __syncthreads(); }, x, d, mu_s, assign,
-                            pend_idx + static_cast<size_t>(src) * pend_cap,
-                            pend_mask + static_cast<size_t>(src) * pend_cap, 0, total, sums_s, cnt_s,
-                            rows_s, dist_s, idx_s, mask_s, first_s, a_s);
-  for (int e = tid; e < k * d; e += kResThreads) ps[e] = sums_s[e];
-  for (int c = tid; c < k; c += kResThreads) pc[c] = cnt_s[c];
+#ifdef DLX_KMEANS_TRACE
+  if (tr && tid == 0)
+    for (int i = 0; i < 5; ++i) tr[i] = tacc[i];
+#endif
+#undef RTR
 }
 
 }  // namespace sk
@@ -1027,8 +1057,8 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
               DLX_ERR_GENERATION,
               "GenerationFailed: screened k-means needs even d <= %d and k <= %d (got d=%d k=%d)",
               sk::kMaxD, sk::kMaxK, d, k);
-  DLX_REQUIRE((reinterpret_cast<uintptr_t>(x) & 15) == 0, DLX_ERR_GENERATION,
-              "GenerationFailed: screened k-means needs 16-byte aligned samples");
+  DLX_REQUIRE((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(mu) & 15) == 0,
+              DLX_ERR_GENERATION, "GenerationFailed: screened k-means needs 16-byte aligned samples and centroids");
   // the fold accumulators hold <= 128*255 per tile in int32: at most 65,793 tiles per CTA
   DLX_REQUIRE(n <= (static_cast<int64_t>(60000) * sk::kTile) * sm_count(), DLX_ERR_GENERATION,
               "GenerationFailed: screened k-means takes at most %lld samples per launch",
@@ -1069,7 +1099,7 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
     double avg[16] = {0}, per_tile = 0;
     long cnt = 0;
     for (int b = 0; b < grid; ++b)
-      for (int m = 8; m < sk::kTraceTiles - 1; ++m) {
+      for (int m = 8; m < sk::kTraceTiles - 2; ++m) {
         const long long* r = &h[(static_cast<size_t>(b) * sk::kTraceTiles + m) * 16];
         const long long* r1 = r + 16;
         if (r[2] == 0 || r1[2] == 0) continue;
@@ -1077,6 +1107,21 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
         per_tile += static_cast<double>(r1[2] - r[2]);
         ++cnt;
       }
+    {
+      double ph[6] = {0};
+      for (int b = 0; b < grid; ++b) {
+        const long long* r = &h[(static_cast<size_t>(b) * sk::kTraceTiles + sk::kTraceTiles - 1) * 16];
+        for (int e = 0; e < 6; ++e) ph[e] += static_cast<double>(r[e] - r[0]) / grid;
+      }
+      fprintf(stderr, "[dlx phases] prologue %.0f; tiles done (fold_done) %+.0f; flush %+.0f; resolve %+.0f; exit %+.0f cycles (mtiles %d)\n",
+              ph[1], ph[2], ph[3], ph[4], ph[5], static_cast<int>((n + sk::kTile - 1) / sk::kTile / grid));
+      double rt[5] = {0};
+      for (int b = 0; b < grid; ++b)
+        for (int e = 0; e < 5; ++e)
+          rt[e] += static_cast<double>(h[(static_cast<size_t>(b) * sk::kTraceTiles + sk::kTraceTiles - 1) * 16 + 8 + e]) / grid;
+      fprintf(stderr, "[dlx resolve] list %.0f gather %.0f chains %.0f merge %.0f fold %.0f cycles\n",
+              rt[0], rt[1], rt[2], rt[3], rt[4]);
+    }
     if (cnt) {
       fprintf(stderr, "[dlx trace] tile period %.0f cycles;", per_tile / cnt);
       for (int e = 0; e < 16; ++e) fprintf(stderr, " %s %+.0f", names[e], avg[e] / cnt);
