@@ -43,7 +43,7 @@
 // per-centroid sums sum_q Z''_q = sum_p 2^(8p) D_p are EXACT integers, minus count_c *
 // (2^63 + 2^39), times 2^(e_t-62), rounded once to fp64.  The fixed-point rounding is below
 // 2^(e_t-62) per element; rows holding a nonzero |x| < 2^(e_t-30) (where that could exceed a
-// 2^-32 relative error) take the exact fp64 fold in the resolve kernel instead.  The fold is
+// 2^-32 relative error) take the exact fp64 fold with the re-checked samples.  The fold is
 // order-free, hence deterministic.
 //
 // Kernel shape: one persistent CTA per SM (227 KiB smem: three 64 KiB plane buffers, the
@@ -59,9 +59,9 @@
 //   warps 8-23  converters: 32-byte row loads a whole tile ahead in registers, Z via one
 //               round-down fma + F2I.S64, byte-plane transposes (PRMT), conflict-free STS
 //   registers   80 at launch, rebalanced by setmaxnreg: warps 0-3 32, epilogue 128, converters 80
-//   resolve     a second small kernel evaluates the reference chain for the pending samples
-//               (one thread per (sample, candidate) pair), writes their assignments and folds
-//               their rows into per-CTA partial records in fp64, in list order.
+//   re-checks   after the CTA's last tile the epilogue warps evaluate the reference chain for
+//               the pending samples (one thread per (sample, candidate) pair), write their
+//               assignments and fold their rows into the CTA's record in fp64, in list order.
 #include <algorithm>
 #include <climits>
 #include <cstdio>
@@ -731,7 +731,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
           if ((full & (full - 1)) == 0) {
             a = __ffsll(static_cast<long long>(full)) - 1;
           } else {
-            pend = true;  // several survivors: resolved by the exact chain (resolve kernel)
+            pend = true;  // several survivors: resolved by the exact chain after the last tile
           }
         } else {
           a = 0;  // no finite centroid: the chain keeps its start index
@@ -878,15 +878,12 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
 }
 
 // ---------------------------------------------------------------------------------------
-// resolve: the reference chain for the pending samples.  Resolve CTA rb handles main-kernel
-// CTA rb's pending list in chunks of kResChunk samples: the chunk's rows are gathered into
-// shared memory next to the fp64 centroids, every (sample, candidate) pair is one thread's
-// exact chain (sequential j, no FMA), each sample then merges its candidates in ascending
-// centroid order (strict <, NaN never wins, start (1e300, 0)), and the rows are folded, in
-// list order, into CTA rb's partial record (deterministic; CTAs without pending rows exit).
-
-// The exact chain for a pending list [lo, hi) of one CTA, folded in list order into the record
-// (sums_s, cnt_s) in shared memory.  NT threads (tid in [0, NT)) synchronise with `sync`.
+// The exact re-check of one CTA's pending list [lo, hi), in chunks of kResChunk samples: the
+// chunk's rows are gathered into shared memory next to the fp64 centroids, every (sample,
+// candidate) pair is one thread's reference chain (sequential j, no FMA), each sample then
+// merges its candidates in ascending centroid order (strict <, NaN never wins, start
+// (1e300, 0)), and the rows are folded, in list order, into the record (sums_s, cnt_s) in
+// shared memory (deterministic).  NT threads (tid in [0, NT)) synchronise with `sync`.
 template <int NT, class Sync>
 __device__ __forceinline__ void resolve_list(int tid, Sync sync, const double* __restrict__ x, int d,
                                              const double* __restrict__ mu_s, int32_t* __restrict__ assign,
@@ -1024,7 +1021,7 @@ static long long pend_capacity(int64_t n, int grid) {
 
 struct ScreenedWs {
   long long* pend_count;
-  long long* part_counts;  // [grid][k]: main kernel record, completed by the resolve kernel
+  long long* part_counts;  // [grid][k]: per-CTA records (screened + re-checked samples)
   double* part_sums;       // [grid][k*d]
   long long* pend_idx;     // [grid][cap]
   unsigned long long* pend_mask;
@@ -1113,13 +1110,13 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
         const long long* r = &h[(static_cast<size_t>(b) * sk::kTraceTiles + sk::kTraceTiles - 1) * 16];
         for (int e = 0; e < 6; ++e) ph[e] += static_cast<double>(r[e] - r[0]) / grid;
       }
-      fprintf(stderr, "[dlx phases] prologue %.0f; tiles done (fold_done) %+.0f; flush %+.0f; resolve %+.0f; exit %+.0f cycles (mtiles %d)\n",
+      fprintf(stderr, "[dlx phases] prologue %.0f; tiles done (fold_done) %+.0f; flush %+.0f; re-checks %+.0f; exit %+.0f cycles (mtiles %d)\n",
               ph[1], ph[2], ph[3], ph[4], ph[5], static_cast<int>((n + sk::kTile - 1) / sk::kTile / grid));
       double rt[5] = {0};
       for (int b = 0; b < grid; ++b)
         for (int e = 0; e < 5; ++e)
           rt[e] += static_cast<double>(h[(static_cast<size_t>(b) * sk::kTraceTiles + sk::kTraceTiles - 1) * 16 + 8 + e]) / grid;
-      fprintf(stderr, "[dlx resolve] list %.0f gather %.0f chains %.0f merge %.0f fold %.0f cycles\n",
+      fprintf(stderr, "[dlx re-checks] list %.0f gather %.0f chains %.0f merge %.0f fold %.0f cycles\n",
               rt[0], rt[1], rt[2], rt[3], rt[4]);
     }
     if (cnt) {
