@@ -27,7 +27,7 @@ for w in $WHAT; do
     benchref) timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_ref_c4.json 2> $OUT/bench_ref_c4.err ;;
     ncu) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file $OUT/launches_c4.csv \
            python bench.py --config c4 --steps 4 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch_bench.log 2>&1
-         timeout 1200 ncu --set full --clock-control none --import-source on -k regex:kmeans -s 3 -c 1 -o $OUT/prof_kmeans \
+         timeout 1200 ncu --set full --clock-control none --import-source on -k regex:kmeans_screened -s 3 -c 1 -o $OUT/prof_kmeans \
            python bench.py --config c4 --steps 4 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_kmeans.log 2>&1
          for c in c5 l16; do
            timeout 900 ncu --set full --clock-control none --import-source on -k regex:"groupby_smem|logreg_grad" -s 3 -c 1 -o $OUT/prof_$c \
