@@ -26,7 +26,7 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(kGdThreads)
+__global__ void __launch_bounds__(kGdThreads, 3)
 gda_pass2_dmma_kernel(const double* __restrict__ x, const long long* __restrict__ y, int64_t n,
                       int d, const double* __restrict__ mu0, const double* __restrict__ mu1,
                       double* __restrict__ parts) {
@@ -57,15 +57,23 @@ gda_pass2_dmma_kernel(const double* __restrict__ x, const long long* __restrict_
     const int64_t i0 = tile * kGdTile;
     __syncthreads();
     // stage centred rows: diff[s][j] = x[i0+s][j] - mu_{y}[j]  (zero outside n / d)
-    for (int e = tid; e < kGdTile * 64; e += kGdThreads) {
-      const int s = e >> 6, j = e & 63;
-      const int64_t i = i0 + s;
-      double v = 0.0;
-      if (i < n && j < d) {
-        const long long yy = __ldg(y + i);
-        v = __ldg(x + i * d + j) - mu_s[yy == 1 ? 1 : 0][j];
+    // 8 independent loads per thread in flight before their stores (a load -> store loop
+    // would expose the full memory latency per element)
+    for (int e0 = tid; e0 < kGdTile * 64; e0 += 8 * kGdThreads) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * kGdThreads;
+        const int s = e >> 6, j = e & 63;
+        const int64_t i = i0 + s;
+        v[u] = 0.0;
+        if (i < n && j < d) v[u] = __ldg(x + i * d + j) - mu_s[__ldg(y + i) == 1 ? 1 : 0][j];
       }
-      diff_s[s * kGdStride + j] = v;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * kGdThreads;
+        diff_s[(e >> 6) * kGdStride + (e & 63)] = v[u];
+      }
     }
     __syncthreads();
 #pragma unroll 2
