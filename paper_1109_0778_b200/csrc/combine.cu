@@ -11,12 +11,11 @@ namespace dlx {
 constexpr int kCombWarps = 32;   // warps per block: partial p goes to warp p % 32
 
 template <class Tin, class Tout>
-__global__ void __launch_bounds__(kCombWarps * 32)
-combine_partials_kernel(const Tin* __restrict__ parts, int nparts, long long width,
-                        Tout* __restrict__ out) {
+__device__ __forceinline__ void combine_columns(const Tin* __restrict__ parts, int nparts, long long width,
+                                                Tout* __restrict__ out, long long block) {
   __shared__ Tout red[kCombWarps][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long e = static_cast<long long>(blockIdx.x) * 32 + lane;
+  const long long e = block * 32 + lane;
   Tout a0 = 0, a1 = 0, a2 = 0, a3 = 0;
   if (e < width) {
     int p = warp;
@@ -36,6 +35,24 @@ combine_partials_kernel(const Tin* __restrict__ parts, int nparts, long long wid
     for (int w = 1; w < kCombWarps; ++w) s += red[w][lane];
     out[e] = s;
   }
+}
+
+template <class Tin, class Tout>
+__global__ void __launch_bounds__(kCombWarps * 32)
+combine_partials_kernel(const Tin* __restrict__ parts, int nparts, long long width,
+                        Tout* __restrict__ out) {
+  combine_columns<Tin, Tout>(parts, nparts, width, out, blockIdx.x);
+}
+
+// two records of one multiloop (e.g. k-means sums and counts) in one launch: the first
+// blocks fold the fp64 record, the rest the int64 record
+__global__ void __launch_bounds__(kCombWarps * 32)
+combine_pair_kernel(const double* __restrict__ pf, long long wf, double* __restrict__ of,
+                    const long long* __restrict__ pi, long long wi, long long* __restrict__ oi,
+                    int nparts) {
+  const long long bf = (wf + 31) / 32;
+  if (blockIdx.x < bf) combine_columns<double, double>(pf, nparts, wf, of, blockIdx.x);
+  else combine_columns<long long, long long>(pi, nparts, wi, oi, blockIdx.x - bf);
 }
 
 template <class Tin, class Tout>
@@ -59,6 +76,14 @@ int combine_i64(const long long* parts, int nparts, long long width, long long* 
 int combine_u32_i64(const unsigned* parts, int nparts, long long width, long long* out,
                     cudaStream_t s) {
   return launch_combine<unsigned, long long>(parts, nparts, width, out, s);
+}
+int combine_f64_i64(const double* pf, long long wf, double* of, const long long* pi, long long wi,
+                    long long* oi, int nparts, cudaStream_t s) {
+  const long long blocks = (wf + 31) / 32 + (wi + 31) / 32;
+  if (blocks <= 0) return DLX_OK;
+  combine_pair_kernel<<<static_cast<unsigned>(blocks), kCombWarps * 32, 0, s>>>(pf, wf, of, pi, wi, oi, nparts);
+  DLX_LAUNCHED("combine_pair_kernel");
+  return DLX_OK;
 }
 
 }  // namespace dlx

@@ -51,7 +51,13 @@ inline int cuda_fail(cudaError_t e, const char* what) {
 // Deterministic combine of per-CTA partial activation records (combine.cu).
 int combine_f64(const double* parts, int nparts, long long width, double* out, cudaStream_t s);
 int combine_i64(const long long* parts, int nparts, long long width, long long* out, cudaStream_t s);
+// an fp64 and an int64 record (same number of partials) in one launch
+int combine_f64_i64(const double* pf, long long wf, double* of, const long long* pi, long long wi,
+                    long long* oi, int nparts, cudaStream_t s);
 int combine_u32_i64(const unsigned* parts, int nparts, long long width, long long* out, cudaStream_t s);
+// an fp64 and an int64 record with the same number of partials, in one launch
+int combine_f64_i64(const double* pf, long long wf, double* of, const long long* pi, long long wi,
+                    long long* oi, int nparts, cudaStream_t s);
 
 // Number of SMs of the current device (cached per device).
 int sm_count();

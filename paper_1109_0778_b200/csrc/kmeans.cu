@@ -198,9 +198,8 @@ __global__ void kmeans_update_kernel(const long long* __restrict__ counts,
 
 int kmeans_finalize(const long long* part_counts, const double* part_sums, int parts, int k, int d,
                     long long* counts, double* sums, cudaStream_t stream) {
-  int rc = combine_i64(part_counts, parts, k, counts, stream);
-  if (rc != DLX_OK) return rc;
-  return combine_f64(part_sums, parts, static_cast<long long>(k) * d, sums, stream);
+  return combine_f64_i64(part_sums, static_cast<long long>(k) * d, sums, part_counts, k, counts, parts,
+                         stream);
 }
 
 // Screened tcgen05 path (kmeans_screened.cu).  Returns DLX_ERR_GENERATION when the shape

@@ -348,9 +348,8 @@ int dlx_gda_pass1(const double* d_x, const int64_t* d_y, int64_t n, int32_t d, i
     default: gda_pass1_kernel<4><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, p0, p1, pn); break;
   }
   DLX_LAUNCHED("gda_pass1_kernel");
-  int rc = combine_f64(p0, grid, d, d_sum0, stream);
+  int rc = combine_f64_i64(p0, d, d_sum0, pn, 1, reinterpret_cast<long long*>(d_n1), grid, stream);
   if (rc == DLX_OK) rc = combine_f64(p1, grid, d, d_sum1, stream);
-  if (rc == DLX_OK) rc = combine_i64(pn, grid, 1, reinterpret_cast<long long*>(d_n1), stream);
   return rc;
 }
 
