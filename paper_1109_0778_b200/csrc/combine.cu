@@ -50,6 +50,8 @@ __global__ void __launch_bounds__(kCombWarps * 32)
 combine_pair_kernel(const double* __restrict__ pf, long long wf, double* __restrict__ of,
                     const long long* __restrict__ pi, long long wi, long long* __restrict__ oi,
                     int nparts) {
+  pdl_wait();   // the multiloop that wrote the partials has completed
+  pdl_trigger();
   const long long bf = (wf + 31) / 32;
   if (blockIdx.x < bf) combine_columns<double, double>(pf, nparts, wf, of, blockIdx.x);
   else combine_columns<long long, long long>(pi, nparts, wi, oi, blockIdx.x - bf);
@@ -81,7 +83,8 @@ int combine_f64_i64(const double* pf, long long wf, double* of, const long long*
                     long long* oi, int nparts, cudaStream_t s) {
   const long long blocks = (wf + 31) / 32 + (wi + 31) / 32;
   if (blocks <= 0) return DLX_OK;
-  combine_pair_kernel<<<static_cast<unsigned>(blocks), kCombWarps * 32, 0, s>>>(pf, wf, of, pi, wi, oi, nparts);
+  DLX_CUDA(launch_pdl(combine_pair_kernel, dim3(static_cast<unsigned>(blocks)), dim3(kCombWarps * 32), 0, s,
+                      pf, wf, of, pi, wi, oi, nparts));
   DLX_LAUNCHED("combine_pair_kernel");
   return DLX_OK;
 }

@@ -55,9 +55,29 @@ int combine_i64(const long long* parts, int nparts, long long width, long long* 
 int combine_f64_i64(const double* pf, long long wf, double* of, const long long* pi, long long wi,
                     long long* oi, int nparts, cudaStream_t s);
 int combine_u32_i64(const unsigned* parts, int nparts, long long width, long long* out, cudaStream_t s);
-// an fp64 and an int64 record with the same number of partials, in one launch
-int combine_f64_i64(const double* pf, long long wf, double* of, const long long* pi, long long wi,
-                    long long* oi, int nparts, cudaStream_t s);
+
+// Programmatic dependent launch (PDL): a kernel launched with launch_pdl may start while the
+// previous kernel on the stream is still running; it must call pdl_wait() before touching
+// anything that kernel writes (or that the kernel before it reads).  Both are no-ops for a
+// normal launch.  pdl_trigger() lets the next PDL kernel start early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 // Number of SMs of the current device (cached per device).
 int sm_count();

@@ -189,6 +189,8 @@ kmeans_direct_kernel(const double* __restrict__ x, int64_t n, int d, int k,
 __global__ void kmeans_update_kernel(const long long* __restrict__ counts,
                                      const double* __restrict__ sums, int k, int d,
                                      double* __restrict__ mu) {
+  pdl_wait();   // counts / sums of this iteration are final
+  pdl_trigger();
   const int kd = k * d;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kd; e += gridDim.x * blockDim.x) {
     const int c = e / d;
@@ -273,8 +275,8 @@ int dlx_kmeans_update(const int64_t* d_counts, const double* d_sums, int32_t k, 
                       double* d_mu, dlx_stream_t stream) {
   DLX_REQUIRE(k > 0 && d > 0 && d_counts && d_sums && d_mu, DLX_ERR_ARG, "k-means update: bad args");
   const int kd = k * d;
-  kmeans_update_kernel<<<(kd + 255) / 256, 256, 0, stream>>>(
-      reinterpret_cast<const long long*>(d_counts), d_sums, k, d, d_mu);
+  DLX_CUDA(launch_pdl(kmeans_update_kernel, dim3((kd + 255) / 256), dim3(256), 0, stream,
+                      reinterpret_cast<const long long*>(d_counts), d_sums, k, d, d_mu));
   DLX_LAUNCHED("kmeans_update_kernel");
   return DLX_OK;
 }

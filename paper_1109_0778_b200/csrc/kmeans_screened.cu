@@ -267,6 +267,10 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     fence_mbar_init();
   }
   if (tid < kMaxK) S.cnt[tid] = 0;
+  // launched with programmatic dependent launch: everything above overlaps the previous
+  // kernel (the centroid update); from here on we read what it wrote
+  pdl_wait();
+  pdl_trigger();
   // centroids into shared memory (the plane buffers are free until the first conversion), one
   // coalesced pass; then one warp per centroid
   double* mu_s = reinterpret_cast<double*>(smem + kOffA);   // [c][64]
@@ -1080,9 +1084,9 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
                                                  : sk::kmeans_screened_kernel<0, true>);
   DLX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sk::kSmemBytes)));
-  kern<<<grid, sk::kThreads, sk::kSmemBytes, stream>>>(
-      x, n, d, k, mu, assign, w.part_counts, w.part_sums, w.pend_idx, w.pend_mask, w.pend_count, cap,
-      trace, pf);
+  DLX_CUDA(launch_pdl(kern, dim3(grid), dim3(sk::kThreads), sk::kSmemBytes, stream,
+                      x, n, d, k, mu, assign, w.part_counts, w.part_sums, w.pend_idx, w.pend_mask,
+                      w.pend_count, cap, trace, pf));
   DLX_LAUNCHED("kmeans_screened_kernel");
   if (trace) {  // debug only: mean event offsets (cycles) relative to the converter's tile start
     std::vector<long long> h(static_cast<size_t>(grid) * sk::kTraceTiles * 16);
