@@ -41,6 +41,8 @@ template <class Tin, class Tout>
 __global__ void __launch_bounds__(kCombWarps * 32)
 combine_partials_kernel(const Tin* __restrict__ parts, int nparts, long long width,
                         Tout* __restrict__ out) {
+  pdl_wait();   // programmatic dependent launch: inputs are final from here on
+  pdl_trigger();
   combine_columns<Tin, Tout>(parts, nparts, width, out, blockIdx.x);
 }
 
@@ -62,8 +64,8 @@ static int launch_combine(const Tin* parts, int nparts, long long width, Tout* o
                           cudaStream_t stream) {
   if (width <= 0) return DLX_OK;
   const long long blocks = (width + 31) / 32;
-  combine_partials_kernel<Tin, Tout><<<static_cast<unsigned>(blocks), kCombWarps * 32, 0, stream>>>(
-      parts, nparts, width, out);
+  DLX_CUDA(launch_pdl(combine_partials_kernel<Tin, Tout>, dim3(static_cast<unsigned>(blocks)), dim3(kCombWarps * 32), 0, stream, 
+      parts, nparts, width, out));
   DLX_LAUNCHED("combine_partials_kernel");
   return DLX_OK;
 }

@@ -30,6 +30,8 @@ __global__ void __launch_bounds__(kGdThreads, 3)
 gda_pass2_dmma_kernel(const double* __restrict__ x, const long long* __restrict__ y, int64_t n,
                       int d, const double* __restrict__ mu0, const double* __restrict__ mu1,
                       double* __restrict__ parts) {
+  pdl_wait();   // programmatic dependent launch: inputs are final from here on
+  pdl_trigger();
   __shared__ double mu_s[2][64];
   extern __shared__ double diff_s[];  // [kGdTile][kGdStride]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -120,7 +122,7 @@ int gda_pass2_dmma(const double* x, const long long* y, int64_t n, int d, const 
   const size_t smem = static_cast<size_t>(kGdTile) * kGdStride * sizeof(double);
   DLX_CUDA(cudaFuncSetAttribute(gda_pass2_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
-  gda_pass2_dmma_kernel<<<grid, kGdThreads, smem, stream>>>(x, y, n, d, mu0, mu1, parts);
+  DLX_CUDA(launch_pdl(gda_pass2_dmma_kernel, dim3(grid), dim3(kGdThreads), smem, stream, x, y, n, d, mu0, mu1, parts));
   DLX_LAUNCHED("gda_pass2_dmma_kernel");
   return combine_f64(parts, grid, static_cast<long long>(d) * d, out, stream);
 }

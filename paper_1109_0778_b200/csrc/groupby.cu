@@ -56,6 +56,8 @@ __device__ __forceinline__ void count_key(unsigned* h, long long key, long long 
 __global__ void __launch_bounds__(kGbThreads)
 groupby_smem_kernel(const long long* __restrict__ keys, int64_t n, long long nb, int copies,
                     unsigned* __restrict__ partials) {
+  pdl_wait();   // programmatic dependent launch: inputs are final from here on
+  pdl_trigger();
   extern __shared__ unsigned hist[];
   const int tid = threadIdx.x;
   const int total = static_cast<int>(nb) * copies;
@@ -94,6 +96,8 @@ groupby_smem_kernel(const long long* __restrict__ keys, int64_t n, long long nb,
 __global__ void __launch_bounds__(kGbThreads)
 groupby_global_kernel(const long long* __restrict__ keys, int64_t n, long long nb,
                       unsigned long long* __restrict__ counts) {
+  pdl_wait();   // programmatic dependent launch: inputs are final from here on
+  pdl_trigger();
   const int64_t T = static_cast<int64_t>(gridDim.x) * kGbThreads;
   const int64_t npairs = n >> 1;
   const longlong2* kp = reinterpret_cast<const longlong2*>(keys);
@@ -134,9 +138,9 @@ int dlx_groupby_count(const int64_t* d_keys, int64_t n, int64_t nbuckets, int64_
   if (!p.shared) {
     DLX_CUDA(cudaMemsetAsync(d_counts, 0, sizeof(int64_t) * nbuckets, stream));
     if (n == 0) return DLX_OK;
-    groupby_global_kernel<<<p.grid, kGbThreads, 0, stream>>>(
+    DLX_CUDA(launch_pdl(groupby_global_kernel, dim3(p.grid), dim3(kGbThreads), 0, stream, 
         reinterpret_cast<const long long*>(d_keys), n, nbuckets,
-        reinterpret_cast<unsigned long long*>(d_counts));
+        reinterpret_cast<unsigned long long*>(d_counts)));
     DLX_LAUNCHED("groupby_global_kernel");
     return DLX_OK;
   }
@@ -146,8 +150,8 @@ int dlx_groupby_count(const int64_t* d_keys, int64_t n, int64_t nbuckets, int64_
   unsigned* partials = static_cast<unsigned*>(d_workspace);
   DLX_CUDA(cudaFuncSetAttribute(groupby_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(p.smem)));
-  groupby_smem_kernel<<<p.grid, kGbThreads, p.smem, stream>>>(
-      reinterpret_cast<const long long*>(d_keys), n, nbuckets, p.copies, partials);
+  DLX_CUDA(launch_pdl(groupby_smem_kernel, dim3(p.grid), dim3(kGbThreads), p.smem, stream, 
+      reinterpret_cast<const long long*>(d_keys), n, nbuckets, p.copies, partials));
   DLX_LAUNCHED("groupby_smem_kernel");
   return combine_u32_i64(partials, p.grid, nbuckets, reinterpret_cast<long long*>(d_counts), stream);
 }

@@ -36,6 +36,8 @@ __global__ void widen_kernel(const int32_t* __restrict__ a, int64_t n, long long
 
 __global__ void axpy_inplace_kernel(double* __restrict__ t, const double* __restrict__ g,
                                     double alpha, int64_t n) {
+  pdl_wait();   // programmatic dependent launch: inputs are final from here on
+  pdl_trigger();
   const int64_t T = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += T)
     t[i] = __dsub_rn(t[i], __dmul_rn(alpha, g[i]));
@@ -156,7 +158,7 @@ int dlx_axpy_inplace(double* d_theta, const double* d_grad, double alpha, int64_
   DLX_REQUIRE(n >= 0 && ((d_theta && d_grad) || n == 0), DLX_ERR_ARG, "axpy_inplace: bad args");
   if (n == 0) return DLX_OK;
   const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, sm_count() * 8));
-  axpy_inplace_kernel<<<grid, 256, 0, stream>>>(d_theta, d_grad, alpha, n);
+  DLX_CUDA(launch_pdl(axpy_inplace_kernel, dim3(grid), dim3(256), 0, stream, d_theta, d_grad, alpha, n));
   DLX_LAUNCHED("axpy_inplace_kernel");
   return DLX_OK;
 }

@@ -98,6 +98,8 @@ template <int M>
 __global__ void __launch_bounds__(kRowThreads)
 logreg_grad_kernel(const double* __restrict__ x, const long long* __restrict__ y, int64_t n,
                    int d, const double* __restrict__ theta, double* __restrict__ parts) {
+  pdl_wait();   // programmatic dependent launch: inputs are final from here on
+  pdl_trigger();
   extern __shared__ double red_s[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double th[M][2], acc[M][2];
@@ -147,6 +149,8 @@ __global__ void __launch_bounds__(kRowThreads)
 gda_pass1_kernel(const double* __restrict__ x, const long long* __restrict__ y, int64_t n, int d,
                  double* __restrict__ parts0, double* __restrict__ parts1,
                  long long* __restrict__ parts_n1) {
+  pdl_wait();   // programmatic dependent launch: inputs are final from here on
+  pdl_trigger();
   extern __shared__ double red_s[];
   __shared__ long long n1_s[kRowWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -189,6 +193,8 @@ gda_pass1_kernel(const double* __restrict__ x, const long long* __restrict__ y, 
 __global__ void gda_means_kernel(const long long* __restrict__ n1p, const double* __restrict__ s0,
                                  const double* __restrict__ s1, long long n_total, int d,
                                  double* __restrict__ mu0, double* __restrict__ mu1) {
+  pdl_wait();   // programmatic dependent launch: inputs are final from here on
+  pdl_trigger();
   const long long n1 = *n1p;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < d; j += gridDim.x * blockDim.x) {
     mu0[j] = s0[j] / static_cast<double>(n_total - n1);
@@ -207,6 +213,8 @@ __global__ void __launch_bounds__(kRowThreads)
 gda_pass2_kernel(const double* __restrict__ x, const long long* __restrict__ y, int64_t n, int d,
                  const double* __restrict__ mu0, const double* __restrict__ mu1,
                  double* __restrict__ parts) {
+  pdl_wait();   // programmatic dependent launch: inputs are final from here on
+  pdl_trigger();
   extern __shared__ double sm[];
   const int D = 16 * B;           // padded dimension
   double* mu_s = sm;              // 2 * D
@@ -311,10 +319,10 @@ int dlx_logreg_grad(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
   const size_t smem = static_cast<size_t>(kRowWarps) * d * sizeof(double);
   const long long* y = reinterpret_cast<const long long*>(d_y);
   switch (m_for(d)) {
-    case 1: logreg_grad_kernel<1><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, d_theta, parts); break;
-    case 2: logreg_grad_kernel<2><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, d_theta, parts); break;
-    case 3: logreg_grad_kernel<3><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, d_theta, parts); break;
-    default: logreg_grad_kernel<4><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, d_theta, parts); break;
+    case 1: DLX_CUDA(launch_pdl(logreg_grad_kernel<1>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, parts)); break;
+    case 2: DLX_CUDA(launch_pdl(logreg_grad_kernel<2>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, parts)); break;
+    case 3: DLX_CUDA(launch_pdl(logreg_grad_kernel<3>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, parts)); break;
+    default: DLX_CUDA(launch_pdl(logreg_grad_kernel<4>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, parts)); break;
   }
   DLX_LAUNCHED("logreg_grad_kernel");
   return combine_f64(parts, grid, d, d_grad, stream);
@@ -342,10 +350,10 @@ int dlx_gda_pass1(const double* d_x, const int64_t* d_y, int64_t n, int32_t d, i
   const size_t smem = static_cast<size_t>(kRowWarps) * d * sizeof(double);
   const long long* y = reinterpret_cast<const long long*>(d_y);
   switch (m_for(d)) {
-    case 1: gda_pass1_kernel<1><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, p0, p1, pn); break;
-    case 2: gda_pass1_kernel<2><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, p0, p1, pn); break;
-    case 3: gda_pass1_kernel<3><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, p0, p1, pn); break;
-    default: gda_pass1_kernel<4><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, p0, p1, pn); break;
+    case 1: DLX_CUDA(launch_pdl(gda_pass1_kernel<1>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, p0, p1, pn)); break;
+    case 2: DLX_CUDA(launch_pdl(gda_pass1_kernel<2>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, p0, p1, pn)); break;
+    case 3: DLX_CUDA(launch_pdl(gda_pass1_kernel<3>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, p0, p1, pn)); break;
+    default: DLX_CUDA(launch_pdl(gda_pass1_kernel<4>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, p0, p1, pn)); break;
   }
   DLX_LAUNCHED("gda_pass1_kernel");
   int rc = combine_f64_i64(p0, d, d_sum0, pn, 1, reinterpret_cast<long long*>(d_n1), grid, stream);
@@ -356,8 +364,8 @@ int dlx_gda_pass1(const double* d_x, const int64_t* d_y, int64_t n, int32_t d, i
 int dlx_gda_means(const int64_t* d_n1, const double* d_sum0, const double* d_sum1,
                   int64_t n_total, int32_t d, double* d_mu0, double* d_mu1, dlx_stream_t stream) {
   DLX_REQUIRE(d > 0, DLX_ERR_ARG, "gda means: bad d");
-  gda_means_kernel<<<(d + 127) / 128, 128, 0, stream>>>(
-      reinterpret_cast<const long long*>(d_n1), d_sum0, d_sum1, n_total, d, d_mu0, d_mu1);
+  DLX_CUDA(launch_pdl(gda_means_kernel, dim3((d + 127) / 128), dim3(128), 0, stream, 
+      reinterpret_cast<const long long*>(d_n1), d_sum0, d_sum1, n_total, d, d_mu0, d_mu1));
   DLX_LAUNCHED("gda_means_kernel");
   return DLX_OK;
 }
@@ -378,10 +386,10 @@ int dlx_gda_pass2(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
   const size_t smem = static_cast<size_t>(2 + kTs) * 16 * B * sizeof(double);
   const long long* y = reinterpret_cast<const long long*>(d_y);
   switch (B) {
-    case 1: gda_pass2_kernel<1><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, d_mu0, d_mu1, parts); break;
-    case 2: gda_pass2_kernel<2><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, d_mu0, d_mu1, parts); break;
-    case 4: gda_pass2_kernel<4><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, d_mu0, d_mu1, parts); break;
-    default: gda_pass2_kernel<8><<<grid, kRowThreads, smem, stream>>>(d_x, y, n, d, d_mu0, d_mu1, parts); break;
+    case 1: DLX_CUDA(launch_pdl(gda_pass2_kernel<1>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_mu0, d_mu1, parts)); break;
+    case 2: DLX_CUDA(launch_pdl(gda_pass2_kernel<2>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_mu0, d_mu1, parts)); break;
+    case 4: DLX_CUDA(launch_pdl(gda_pass2_kernel<4>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_mu0, d_mu1, parts)); break;
+    default: DLX_CUDA(launch_pdl(gda_pass2_kernel<8>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_mu0, d_mu1, parts)); break;
   }
   DLX_LAUNCHED("gda_pass2_kernel");
   return combine_f64(parts, grid, static_cast<long long>(d) * d, d_scatter, stream);
