@@ -1,0 +1,7 @@
+set -u
+OUT=gpurun_out/r59; mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q -rf > $OUT/pytest_gpu.log 2>&1; echo "rc=$?" >> $OUT/pytest_gpu.log
+for c in c4 c4shard8 c1 c3; do
+  timeout 300 python bench.py --config $c --steps 30 --warmup 3 --no-cpu-baseline > $OUT/bench_$c.json 2> $OUT/bench_$c.err
+done
