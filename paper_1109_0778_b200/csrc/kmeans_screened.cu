@@ -102,8 +102,6 @@ constexpr int kRegsConvRaw = (kThreads * kRegsLaunch - 128 * kRegsIssuer - 128 *
 constexpr int kRegsConv = (kRegsConvRaw > 248 ? 248 : kRegsConvRaw) & ~7;
 static_assert(kNumC == 8 || kNumC == 16, "converter warps");
 static_assert(kRegsConv >= kRegsLaunch || kRegsEpi >= kRegsLaunch, "register plan");
-constexpr int kZConv = 2;                                 // 1: fp64 magic-number split, 2: F2I.S64
-constexpr int kPfDefault = 0;                             // L2 prefetch distance (tiles)
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kFoldCol = 256;                        // fold accumulators: columns 256..511
 constexpr uint32_t kPlane2 = kTile * 128;                 // one [b_hi|b_lo] SW128 buffer, 16 KiB
@@ -117,7 +115,6 @@ static_assert(kOffA % 1024 == 0 && kOffB % 1024 == 0 && kOffOH % 512 == 0,
               "UMMA operand alignment");
 static_assert(kNumA * kABuf >= 2u * kMaxK * 64 * 16, "final fold scratch must fit the plane buffers");
 constexpr double kMagic = 6755399441055744.0;        // 1.5 * 2^52: x + kMagic rounds x to an integer
-constexpr double kMagicZ = 6755401588539520.0;       // kMagic + 2^31 + 2^7: low word = floor + offset
 constexpr int kFoldBits = 30;  // rows with a nonzero |x| < 2^(e_t - 30) take the exact fp64 fold
 
 struct Misc {
@@ -156,16 +153,6 @@ __device__ __forceinline__ uint32_t sw64_offset(uint32_t row, uint32_t kbyte) {
 // rint(v) for |v| < 2^31 as the low word of v + 1.5*2^52 (one fp64 add, exact scaling before)
 __device__ __forceinline__ int rint_magic(double scaled) {
   return __double2loint(__dadd_rn(scaled, kMagic));
-}
-
-// Z'' = floor(x * 2^32 * s) + 2^63 + 2^39 as (hi, lo) words, s = 2^(30 - e_t), |x * s| < 2^30
-__device__ __forceinline__ void zsplit(double x, double s, uint32_t& hi, uint32_t& lo) {
-  const double t1 = __fma_rd(x, s, kMagicZ);            // kMagicZ + floor(x s)
-  const double hd = __dsub_rn(t1, kMagicZ);              // floor(x s), exact
-  const double r = __fma_rn(x, s, -hd);                  // x s - floor(x s) in [0, 1), exact
-  const double t2 = __fma_rd(r, 4294967296.0, kMagic);   // kMagic + floor(r 2^32)
-  hi = static_cast<uint32_t>(__double2loint(t1));        // floor(x s) + 2^31 + 2^7
-  lo = static_cast<uint32_t>(__double2loint(t2));
 }
 
 // streaming 32-byte / 16-byte loads of sample rows (read once: no L1 allocation)
@@ -223,7 +210,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
                        long long* __restrict__ part_counts, double* __restrict__ part_sums,
                        long long* __restrict__ pend_idx, unsigned long long* __restrict__ pend_mask,
                        long long* __restrict__ pend_count, long long pend_cap,
-                       long long* __restrict__ trace, int kPf) {
+                       long long* __restrict__ trace) {
   // optional per-tile event clocks (build with -DDLX_KMEANS_TRACE, run with DLX_KMEANS_TRACE=1):
   // trace[(cta * kTraceTiles + m) * 8 + event]
 #ifdef DLX_KMEANS_TRACE
@@ -402,11 +389,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
             const uint64_t adesc = sw128_kmajor_desc(a0 + g * kPlane2 + kk * 4096);  // MN-major
-#ifndef DLX_KMEANS_DIAG_NOFOLD   // diagnostic only: times the pipeline without the fold MMAs
             mma_i8(tmem + kFoldCol + 64 * g, adesc, bdesc, ID_fold, (nf > 0 || kk > 0) ? 1u : 0u);
-#else
-            (void)adesc; (void)bdesc;
-#endif
           }
         }
         mma_commit(&S.a_empty[nf % kNumA]);
@@ -506,13 +489,6 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       rows = tr.qhi;
       return x + (tr.row0 + rbase) * D + lcol;
     };
-    auto prefetch = [&](int mm) {
-      const int64_t t = tile_of(mm);
-      const int64_t rows = n - t * kTile < kTile ? n - t * kTile : kTile;
-      bulk_prefetch_l2(x + t * kTile * D, static_cast<uint32_t>(rows * D * 8));
-    };
-    if (cw == 0 && lane == 0)
-      for (int mm = 1; mm < kPf && mm < mtiles; ++mm) prefetch(mm);
     int64_t cur_rows = 0;
     const double* cur = base_of(0, cur_rows);
     if (mtiles > 0) {
@@ -521,7 +497,6 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     }
     for (int m = 0; m < mtiles; ++m) {
       const int b = m % kNumA;
-      if (cw == 0 && lane == 0 && m + kPf < mtiles) prefetch(m + kPf);
       int64_t nxt_rows = 0;
       const double* nxt = base_of(m + 1 < mtiles ? m + 1 : m, nxt_rows);
       if (cw == 0 && lane == 0) TRACE_EV(m, 2);
@@ -627,63 +602,6 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       tc_fence_after();
       int tv[64];
       int lmin = kInvalidNm;
-#ifdef DLX_KMEANS_EPI_PIPE
-      // software-pipelined drain: the x4 loads of the next 4 centroids are in flight while the
-      // current 4 are scored (tcgen05.wait::ld waits for all outstanding loads)
-      int cur[4][4], nxt[4][4];
-#pragma unroll
-      for (int g4 = 0; g4 < 4; ++g4) tmem_ld4(tmem + lane_base + 64 * g4, cur[g4]);
-      tmem_ld_wait();
-#pragma unroll
-      for (int ch = 0; ch < 16; ++ch) {
-        if (ch + 1 < 16) {
-#pragma unroll
-          for (int g4 = 0; g4 < 4; ++g4) tmem_ld4(tmem + lane_base + 64 * g4 + 4 * (ch + 1), nxt[g4]);
-        }
-        const int4 n0 = nm4[ch];
-        const int nm[4] = {n0.x, n0.y, n0.z, n0.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int Q = cur[0][u] * 256 + cur[1][u] + (cur[2][u] >> 8) + (cur[3][u] >> 16);
-          const int v = nm[u] - 2 * Q;
-          tv[4 * ch + u] = v;
-          lmin = min(lmin, v);
-        }
-        if (ch + 1 < 16) {
-          tmem_ld_wait();
-#pragma unroll
-          for (int g4 = 0; g4 < 4; ++g4)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) cur[g4][u] = nxt[g4][u];
-        }
-      }
-#elif defined(DLX_KMEANS_EPI_X16)
-      // 16 centroids per step: two x16 TMEM loads (HH, CR), fold them, then W1, W2
-#pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
-        const uint32_t col = 16 * ch;
-        int a16[16], b16[16], p16[16];
-        tmem_ld16(tmem + lane_base + col, a16);
-        tmem_ld16(tmem + lane_base + col + 64, b16);
-        tmem_ld_wait();
-#pragma unroll
-        for (int u = 0; u < 16; ++u) p16[u] = a16[u] * 256 + b16[u];
-        tmem_ld16(tmem + lane_base + col + 128, a16);
-        tmem_ld16(tmem + lane_base + col + 192, b16);
-        const int4 n0 = nm4[4 * ch], n1 = nm4[4 * ch + 1], n2 = nm4[4 * ch + 2], n3 = nm4[4 * ch + 3];
-        const int nm[16] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w,
-                            n2.x, n2.y, n2.z, n2.w, n3.x, n3.y, n3.z, n3.w};
-        tmem_ld_wait();
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          // invalid centroids: zero B rows (Q = 0) and nm = kInvalidNm
-          const int Q = p16[u] + (a16[u] >> 8) + (b16[u] >> 16);
-          const int v = nm[u] - 2 * Q;
-          tv[16 * ch + u] = v;
-          lmin = min(lmin, v);
-        }
-      }
-#else
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
         const uint32_t col = 8 * ch;
@@ -704,7 +622,6 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
           lmin = min(lmin, v);
         }
       }
-#endif
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.t_empty);
@@ -1071,7 +988,6 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
   DLX_REQUIRE(ws && w.used <= ws_bytes, DLX_ERR_ARG, "k-means workspace too small (%zu < %zu)",
               ws_bytes, w.used);
   static const bool tracing = getenv("DLX_KMEANS_TRACE") != nullptr;
-  static const int pf = getenv("DLX_KMEANS_PF") ? atoi(getenv("DLX_KMEANS_PF")) : sk::kPfDefault;
   long long* trace = nullptr;
   if (tracing) {
     DLX_CUDA(cudaMalloc(&trace, sizeof(long long) * grid * sk::kTraceTiles * 16));
@@ -1086,7 +1002,7 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
                                 static_cast<int>(sk::kSmemBytes)));
   DLX_CUDA(launch_pdl(kern, dim3(grid), dim3(sk::kThreads), sk::kSmemBytes, stream,
                       x, n, d, k, mu, assign, w.part_counts, w.part_sums, w.pend_idx, w.pend_mask,
-                      w.pend_count, cap, trace, pf));
+                      w.pend_count, cap, trace));
   DLX_LAUNCHED("kmeans_screened_kernel");
   if (trace) {  // debug only: mean event offsets (cycles) relative to the converter's tile start
     std::vector<long long> h(static_cast<size_t>(grid) * sk::kTraceTiles * 16);
