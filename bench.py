@@ -252,7 +252,7 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
 
     from paper_1109_0778_b200 import _lib
     from paper_1109_0778_b200 import multiloops as ml
-    from paper_1109_0778_b200.comm import Comm, shard_range
+    from paper_1109_0778_b200.comm import Comm, PeerComm, shard_range
     from paper_1109_0778_b200.programs import KMeansProgram, LogRegProgram
 
     torch.cuda.set_device(local_rank)
@@ -262,7 +262,7 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-        comm = Comm.from_torch_distributed()
+        comm = PeerComm.from_torch_distributed() if args.comm == "peer" else Comm.from_torch_distributed()
     _lib.load()
 
     def barrier():
@@ -283,21 +283,34 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
         kernel_fn = lambda: ml.kmeans_step(x, prog.mu, prog.assign, prog.counts, prog.sums,  # noqa: E731
                                            method=args.method)
 
-        def step():
-            kernel_fn()
+        def rest():   # allreduce + update (one fused launch with --comm peer)
+            if isinstance(comm, PeerComm):
+                comm.kmeans_update_(prog.counts, prog.sums, prog.mu)
+                return
             if comm is not None:
                 comm.allreduce_many_([prog.counts, prog.sums])
             ml.kmeans_update(prog.counts, prog.sums, prog.mu)
+
+        def step():
+            kernel_fn()
+            rest()
     elif family == "logreg":
         x = ml.rng_units(n_local * d, seed=1, first_draw=lo * d, device=dev).view(n_local, d)
         y = ml.rng_ints(n_local, 2, seed=1, first_draw=n * d + lo, device=dev)
         prog = LogRegProgram(x, y, torch.zeros(d, dtype=torch.float64, device=dev), 1.0 / n, comm=comm)
         kernel_fn = lambda: ml.logreg_grad(x, y, prog.theta, prog.grad)  # noqa: E731
 
-        def step():
-            kernel_fn()
+        def rest():
+            if isinstance(comm, PeerComm):
+                comm.bgd_step_(prog.grad, prog.theta, prog.alpha)
+                return
             if comm is not None:
                 comm.allreduce_(prog.grad)
+            ml.axpy_inplace(prog.theta, prog.grad, prog.alpha)
+
+        def step():
+            kernel_fn()
+            rest()
             ml.axpy_inplace(prog.theta, prog.grad, prog.alpha)
     elif family == "gda":
         x = ml.rng_units(n_local * d, seed=1, first_draw=lo * d, device=dev).view(n_local, d)
@@ -351,14 +364,8 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             kernel_fn()
             ev[s][1].record(stream)
             # remainder of the step (allreduce + update)
-            if family == "kmeans":
-                if comm is not None:
-                    comm.allreduce_many_([prog.counts, prog.sums])
-                ml.kmeans_update(prog.counts, prog.sums, prog.mu)
-            elif family == "logreg":
-                if comm is not None:
-                    comm.allreduce_(prog.grad)
-                ml.axpy_inplace(prog.theta, prog.grad, prog.alpha)
+            if family in ("kmeans", "logreg"):
+                rest()
             else:
                 if comm is not None:
                     comm.allreduce_(counts)
@@ -412,6 +419,8 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             "dtype": "f64" if family != "groupby" else "int64",
             "data": "synthetic (reference Rng LCG, seed 1, generated on device, bit-identical to host)",
             "config": {"workload": args.config, **p, "parallelism": f"sample-sharded dp{world}",
+                       "exchange": None if world == 1 else ("peer-memory fused allreduce+update" if args.comm == "peer"
+                                                            else "NCCL allReduce + update kernel"),
                        "l2": "inputs larger than L2 (no flush needed)" if bytes_launch > 256e6 else
                              "inputs L2-resident (launch-bound config)",
                        "method": {0: "auto", 1: "direct", 2: "screened"}[args.method],
@@ -539,6 +548,9 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--method", type=int, default=0, help="k-means: 0 auto, 1 direct fp64, 2 screened")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--comm", default="peer", choices=["peer", "nccl"],
+                    help="N>1 exchange: the fused peer-memory allreduce+update kernel (csrc/peer.cu, "
+                         "ascending-rank fold), or NCCL allReduce + a separate update kernel")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     family, p, metric, unit = CONFIGS[args.config]

@@ -159,6 +159,24 @@ int dlx_comm_allreduce_sum(dlx_comm_t comm, void* d_buf, int64_t count, int dtyp
 int dlx_comm_allreduce_sum_group(dlx_comm_t comm, void* const* d_bufs, const int64_t* counts,
                                  const int* dtypes, int nbufs, dlx_stream_t stream);
 
+/* ---- multi-GPU, peer memory: one-shot allreduce of a partial record fused with its update
+ *      (peer.cu).  Each rank allocates an exchange buffer (dlx_peer_alloc, exported as a CUDA
+ *      IPC handle), opens every peer's handle (dlx_peer_open) and passes all nranks buffer
+ *      pointers (its own at index rank) to dlx_peer_allreduce.  The record is `items` items of
+ *      `ni` int64 values (d_counts, items x ni) and `nf` fp64 values (d_sums, items x nf); every
+ *      rank folds the per-rank records in ascending rank order (bit-identical on all ranks) and
+ *      overwrites its local record with the sum.  epilogue: 0 none; 1 k-means update
+ *      d_out[c*nf+j] = sums[c][j] / (double)counts[c] (ni == 1); 2 BGD step
+ *      d_out[i] = d_out[i] - alpha * sums[i].  All ranks must issue the same sequence of calls. */
+#define DLX_PEER_HANDLE_BYTES 64
+int dlx_peer_alloc(int64_t bytes, void** d_ptr, uint8_t* h_handle /* DLX_PEER_HANDLE_BYTES */);
+int dlx_peer_open(const uint8_t* h_handle, void** d_ptr);
+int dlx_peer_close(void* d_ptr);
+int dlx_peer_free(void* d_ptr);
+int dlx_peer_allreduce(void* const* h_bufs, int nranks, int rank, int64_t cap_bytes, int64_t items,
+                       int ni, int nf, int64_t* d_counts, double* d_sums, int epilogue,
+                       double* d_out, double alpha, dlx_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,12 @@ _SIGS = {
     "dlx_comm_allreduce_sum": (_int, [_vp, _vp, _i64, _int, _vp]),
     "dlx_comm_allreduce_sum_group": (_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_i64),
                                             ctypes.POINTER(_int), _int, _vp]),
+    "dlx_peer_alloc": (_int, [_i64, ctypes.POINTER(_vp), ctypes.c_char_p]),
+    "dlx_peer_open": (_int, [ctypes.c_char_p, ctypes.POINTER(_vp)]),
+    "dlx_peer_close": (_int, [_vp]),
+    "dlx_peer_free": (_int, [_vp]),
+    "dlx_peer_allreduce": (_int, [ctypes.POINTER(_vp), _int, _int, _i64, _i64, _int, _int, _vp, _vp,
+                                  _int, _vp, _dbl, _vp]),
 }
 
 # Every symbol include/dlx.h declares (checked by tests/test_abi.py).

@@ -75,3 +75,86 @@ class Comm:
         if self.world > 1 and self._h:
             check(_lib.load().dlx_comm_destroy(self._h))
             self._h = ctypes.c_void_p()
+
+
+class PeerComm:
+    """Peer-memory collective (csrc/peer.cu): the partial record is summed across ranks by one
+    kernel that reads every peer's exchange buffer directly (NVLink loads over NVSwitch; CUDA
+    IPC within one device), folds the ranks in ascending order (bit-identical on every rank,
+    SPEC.md:648's ascending-chunk combine lifted to ranks) and applies the update that consumes
+    the sum in the same launch.  The exchange buffers' IPC handles travel once through
+    ``torch.distributed`` (any backend: plumbing only).  Same interface as :class:`Comm`, plus
+    the fused ``kmeans_update_`` / ``bgd_step_``."""
+
+    HANDLE_BYTES = 64
+
+    def __init__(self, rank: int, world: int, cap_bytes: int = 8 << 20, group=None):
+        L = _lib.load()
+        self.rank, self.world, self.cap = rank, world, int(cap_bytes)
+        self._own = ctypes.c_void_p()
+        h = ctypes.create_string_buffer(self.HANDLE_BYTES)
+        check(L.dlx_peer_alloc(self.cap, ctypes.byref(self._own), h))
+        handles = [h.raw]
+        if world > 1:
+            import torch.distributed as dist
+            handles = [None] * world
+            dist.all_gather_object(handles, h.raw, group=group)
+        self._opened = []
+        ptrs = []
+        for q in range(world):
+            if q == rank:
+                ptrs.append(self._own.value)
+                continue
+            p = ctypes.c_void_p()
+            check(L.dlx_peer_open(handles[q], ctypes.byref(p)))
+            self._opened.append(p)
+            ptrs.append(p.value)
+        self._bufs = (ctypes.c_void_p * world)(*ptrs)
+
+    @classmethod
+    def from_torch_distributed(cls, cap_bytes: int = 8 << 20) -> "PeerComm":
+        import torch.distributed as dist
+        return cls(dist.get_rank(), dist.get_world_size(), cap_bytes)
+
+    def _run(self, items, ni, nf, counts, sums, epilogue=0, out=None, alpha=0.0):
+        ptr = lambda t: ctypes.c_void_p(t.data_ptr() if t is not None else None)  # noqa: E731
+        check(_lib.load().dlx_peer_allreduce(
+            self._bufs, self.world, self.rank, self.cap, int(items), int(ni), int(nf),
+            ptr(counts), ptr(sums), int(epilogue), ptr(out), float(alpha),
+            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+
+    def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
+        assert t.is_contiguous() and t.dtype in (torch.float64, torch.int64)
+        if t.dtype == torch.int64:
+            self._run(t.numel(), 1, 0, t, None)
+        else:
+            self._run(t.numel(), 0, 1, None, t)
+        return t
+
+    def allreduce_many_(self, tensors) -> None:
+        for t in tensors:
+            self.allreduce_(t)
+
+    def allreduce_int(self, v: int) -> int:
+        t = torch.tensor([v], dtype=torch.int64, device="cuda")
+        self.allreduce_(t)
+        return int(t.item())
+
+    def kmeans_update_(self, counts: torch.Tensor, sums: torch.Tensor, mu: torch.Tensor) -> None:
+        """counts (k,) int64 and sums (k, d) fp64 summed across ranks in place, then
+        mu = sums / toDouble(counts) (kmeans_update's semantics), in one launch."""
+        k, d = sums.shape
+        self._run(k, 1, d, counts, sums, epilogue=1, out=mu)
+
+    def bgd_step_(self, grad: torch.Tensor, theta: torch.Tensor, alpha: float) -> None:
+        """grad summed across ranks in place, then theta -= alpha * grad (axpy_inplace)."""
+        self._run(grad.numel(), 0, 1, None, grad, epilogue=2, out=theta, alpha=alpha)
+
+    def close(self):
+        L = _lib.load()
+        for p in self._opened:
+            check(L.dlx_peer_close(p))
+        self._opened = []
+        if self._own:
+            check(L.dlx_peer_free(self._own))
+            self._own = ctypes.c_void_p()

@@ -36,6 +36,9 @@ class KMeansProgram:
     def _body(self):
         ml.kmeans_step(self.x, self.mu, self.assign, self.counts, self.sums, method=self.method,
                        want_assign=self.assign is not None)
+        if self.comm is not None and hasattr(self.comm, "kmeans_update_"):
+            self.comm.kmeans_update_(self.counts, self.sums, self.mu)   # fused allreduce + update
+            return
         if self.comm is not None:
             self.comm.allreduce_many_([self.counts, self.sums])
         ml.kmeans_update(self.counts, self.sums, self.mu)
@@ -79,6 +82,9 @@ class LogRegProgram:
 
     def _body(self):
         ml.logreg_grad(self.x, self.y, self.theta, self.grad)
+        if self.comm is not None and hasattr(self.comm, "bgd_step_"):
+            self.comm.bgd_step_(self.grad, self.theta, self.alpha)   # fused allreduce + step
+            return
         if self.comm is not None:
             self.comm.allreduce_(self.grad)
         ml.axpy_inplace(self.theta, self.grad, self.alpha)
@@ -102,3 +108,8 @@ class LogRegProgram:
             self.graph.replay()
         else:
             self._body()
+
+    def run(self, iters: int):
+        for _ in range(iters):
+            self.step()
+        return self
