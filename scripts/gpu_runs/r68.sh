@@ -1,0 +1,8 @@
+#!/bin/bash
+# ncu full capture of GDA pass 2 (DMMA) at C3
+OUT=gpurun_out/r68; mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gda_pass2 -s 2 -c 1 -o $OUT/prof_gda \
+  python bench.py --config c3 --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file $OUT/launches_c3.csv \
+  python bench.py --config c3 --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu2.log 2>&1

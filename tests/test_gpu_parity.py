@@ -303,7 +303,7 @@ def test_c3_gda(ml, golden):
     np.testing.assert_allclose(S, Sr, rtol=RTOL, atol=1e-9 * np.abs(Sr).max())
 
 
-@pytest.mark.parametrize("n,d", [(1, 2), (999, 16), (5000, 30), (4097, 100), (2000, 128)])
+@pytest.mark.parametrize("n,d", [(1, 2), (999, 16), (5000, 30), (4097, 100), (2000, 128), (300_001, 64), (37_893, 48), (128 * 148 * 2 + 5, 64)])
 def test_gda_shapes(ml, n, d):
     x = dev_units(ml, n, d, seed=8)
     y = ml.rng_ints(n, 2, seed=8, first_draw=n * d)
