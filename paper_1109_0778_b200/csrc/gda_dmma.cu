@@ -12,9 +12,10 @@
 // Data movement: one persistent CTA per SM, warp-specialised.  Each 64-sample tile's raw rows
 // (64 x d fp64, contiguous in the row-major matrix) and labels arrive by 1-D bulk TMA copies
 // into a three-slot ring, issued three tiles ahead, so HBM latency never stalls a warp (the
-// previous version's long-scoreboard stalls).  Four centring warps turn a raw slot into a
+// previous version's long-scoreboard stalls).  Eight centring warps turn a raw slot into a
 // padded operand tile D[b] = x - mu_y (row stride 68 doubles: the fragment loads of four
 // consecutive rows fall in distinct banks; two D buffers, mbarrier full/empty handshakes),
+// (eight centring warps: four left the tensor-core warps waiting on full D buffers, profiles r73-r74)
 // while twelve tensor-core warps own 3 lower blocks each (36 = 12 x 3 for d = 64) and run the
 // DMMA chains on the other D buffer, so centring overlaps the tensor-core phase.
 #include <algorithm>
@@ -27,14 +28,20 @@ namespace dlx {
 using namespace sm100;
 
 constexpr int kGdMmaWarps = 12;                     // tensor-core warps: 3 lower blocks each
-constexpr int kGdCtrWarps = 4;                      // centring warps (one per SM sub-partition)
+#ifndef DLX_GDA_CTR_WARPS
+#define DLX_GDA_CTR_WARPS 8
+#endif
+#ifndef DLX_GDA_DBUFS
+#define DLX_GDA_DBUFS 2
+#endif
+constexpr int kGdCtrWarps = DLX_GDA_CTR_WARPS;      // centring warps (two per SM sub-partition)
 constexpr int kGdThreads = (kGdMmaWarps + kGdCtrWarps) * 32;
 constexpr int kGdCtrThreads = kGdCtrWarps * 32;
 constexpr int kGdTile = 64;           // samples per tile
 constexpr int kGdStride = 64 + 4;     // padded operand row stride (doubles)
 constexpr int kGdBlocksPerWarp = 3;   // 36 lower blocks of a 64x64 S over 12 warps
 constexpr int kGdSlots = 3;           // raw tile ring (bulk copies in flight)
-constexpr int kGdDBufs = 2;           // centred operand tiles
+constexpr int kGdDBufs = DLX_GDA_DBUFS;   // centred operand tiles
 constexpr size_t kGdRawBytes = static_cast<size_t>(kGdTile) * 64 * 8;
 constexpr size_t kGdDBytes = static_cast<size_t>(kGdTile) * kGdStride * 8;
 constexpr size_t kGdOffY = kGdSlots * kGdRawBytes;
