@@ -14,10 +14,10 @@
 // into a three-slot ring, issued three tiles ahead, so HBM latency never stalls a warp (the
 // previous version's long-scoreboard stalls).  Eight centring warps turn a raw slot into a
 // padded operand tile D[b] = x - mu_y (row stride 68 doubles: the fragment loads of four
-// consecutive rows fall in distinct banks; two D buffers, mbarrier full/empty handshakes),
-// (eight centring warps: four left the tensor-core warps waiting on full D buffers, profiles r73-r74)
+// consecutive rows fall in distinct banks; two D buffers, mbarrier full/empty handshakes)
 // while twelve tensor-core warps own 3 lower blocks each (36 = 12 x 3 for d = 64) and run the
-// DMMA chains on the other D buffer, so centring overlaps the tensor-core phase.
+// DMMA chains on the other D buffer, so centring overlaps the tensor-core phase.  (With four
+// centring warps the tensor-core warps sat on empty D buffers 20% of the time, profile r73.)
 #include <algorithm>
 
 #include "common.cuh"
