@@ -42,6 +42,13 @@ CONFIGS = {
 # logreg sample 8d + 8; GDA sample 2 * (8d + 8) (two passes); GroupBy key 8.
 
 
+# fp64 tensor-core (DMMA) peak: not in MEASURED_PEAKS.json (bf16 only) and not in the profiling
+# guide, so measured here: scripts/mb/dmma.cu, independent mma.sync f64 chains on every SM,
+# best shape 36.9 TFLOP/s (profiles/r75/dmma.txt)
+DMMA_PEAK_TFLOPS = 36.9
+DMMA_PEAK_KIND = "measured microbench (scripts/mb/dmma.cu, profiles/r75/dmma.txt)"
+
+
 def algorithmic_bytes(family, p, n_local):
     if family == "kmeans":
         return n_local * (p["d"] * 8 + 4)
@@ -352,6 +359,7 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
     torch.cuda.synchronize()
     barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     L = _lib.load()
@@ -376,7 +384,9 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             if comm is not None:
                 comm.allreduce_many_([n1, s0, s1])
             mu0, mu1 = ml.gda_means(n1, s0, s1, n)
-            S = ml.gda_pass2(x, y, mu0, mu1)
+            ev2[s][0].record(stream)
+            S = ml.gda_pass2(x, y, mu0, mu1)   # dominant kernel: the DMMA scatter
+            ev2[s][1].record(stream)
             if comm is not None:
                 comm.allreduce_(S)
     t_end.record(stream)
@@ -386,10 +396,11 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
     clocks = sampler.stop()
     total_ms = t_start.elapsed_time(t_end)
     kern_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    pass2_ms = sum(a.elapsed_time(b) for a, b in ev2) / args.steps if family == "gda" else 0.0
     if dist is not None:
-        t = torch.tensor([total_ms, kern_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([total_ms, kern_ms, pass2_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, kern_ms = float(t[0]), float(t[1])
+        total_ms, kern_ms, pass2_ms = float(t[0]), float(t[1]), float(t[2])
     ms_per_step = total_ms / args.steps
     value = 1000.0 / ms_per_step
 
@@ -433,6 +444,18 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             "gpu_launches": launches,
             "clocks": clocks,
         }
+        if family == "gda":
+            # dominant kernel = pass 2, the scatter on the fp64 tensor cores: executed DMMA flops
+            # (lower-triangle 8x8 blocks, 2*8*8 flop per sample per block) over its event time,
+            # against the measured DMMA peak; pass 1 (HBM-bound) stays as a secondary line
+            nb = (d + 7) // 8
+            flops = n_local * 2.0 * 64 * nb * (nb + 1) // 2
+            result["roofline_pass1"] = result["roofline"]
+            result["roofline"] = {"bound": "tensor", "achieved": flops / (pass2_ms * 1e-3) / 1e12,
+                                  "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                                  "frac": flops / (pass2_ms * 1e-3) / 1e12 / DMMA_PEAK_TFLOPS,
+                                  "traffic": None, "peak_kind": DMMA_PEAK_KIND, "kernel_ms": pass2_ms,
+                                  "algorithmic_flops_per_launch": flops}
         if world == 1 and not args.no_cpu_baseline:
             try:
                 result["cpu_baseline"] = (cpu_baseline_kmeans(p) if family == "kmeans"
