@@ -50,6 +50,12 @@ constexpr size_t kGdOffMu = kGdOffD + kGdDBufs * kGdDBytes;
 constexpr size_t kGdOffBar = kGdOffMu + 2 * 64 * 8;
 constexpr size_t kGdSmem = kGdOffBar + (kGdSlots + 2 * kGdDBufs) * 8;
 
+// d = 64: the 36 lower 8x8 blocks as 12 triples {si, o0, o1, o2} = blocks (si, o_u) sharing the
+// index si (each unordered pair {a, b} with a >= b appears once)
+__constant__ int kGdTriples[kGdMmaWarps][4] = {
+    {0, 0, 2, 3}, {0, 4, 5, 7}, {1, 0, 1, 2}, {1, 4, 5, 6}, {2, 2, 3, 4}, {2, 5, 6, 7},
+    {3, 1, 3, 4}, {3, 5, 6, 7}, {4, 4, 5, 6}, {5, 5, 6, 7}, {6, 0, 6, 7}, {7, 1, 4, 7}};
+
 __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(c[0]), "+d"(c[1])
@@ -168,48 +174,68 @@ gda_pass2_dmma_kernel(const double* __restrict__ x, const long long* __restrict_
     return;
   }
 
-  // ---- tensor-core warps: blocks t = warp + 12u of the lower triangle, decoded to (ba >= bb)
+  // ---- tensor-core warps ----------------------------------------------------------------
+  // d = 64: warp w owns blocks (si, o0), (si, o1), (si, o2) of kGdTriples[w] — every lower 8x8
+  // block exactly once, three per warp sharing one index, so a k-step loads 4 fragments for 3
+  // DMMAs (A and B fragments of an index are the same register: D[k0+kq][8*idx + g]).  Other d:
+  // blocks t = warp + 12u of the lower triangle, 2 fragments per DMMA.
   const int nb = (d + 7) / 8;
   const int nblocks = nb * (nb + 1) / 2;
+  const bool shared = nb == 8;
   int ba[kGdBlocksPerWarp], bb[kGdBlocksPerWarp];
   double acc[kGdBlocksPerWarp][2][2];   // [block][k-step parity][C pair]: 6 independent DMMA chains
 #pragma unroll
   for (int u = 0; u < kGdBlocksPerWarp; ++u) {
-    int t = warp + kGdMmaWarps * u;
-    int a = 0;
-    while (t >= a + 1) { t -= a + 1; ++a; }
-    ba[u] = a;
-    bb[u] = t;
+    if (shared) {
+      ba[u] = kGdTriples[warp][0];
+      bb[u] = kGdTriples[warp][1 + u];
+    } else {
+      int t = warp + kGdMmaWarps * u;
+      int a = 0;
+      while (t >= a + 1) { t -= a + 1; ++a; }
+      ba[u] = a;
+      bb[u] = t;
+    }
     acc[u][0][0] = acc[u][0][1] = acc[u][1][0] = acc[u][1][1] = 0.0;
   }
+  const bool own[kGdBlocksPerWarp] = {shared || warp < nblocks, shared || warp + kGdMmaWarps < nblocks,
+                                      shared || warp + 2 * kGdMmaWarps < nblocks};
   const int g = lane >> 2, kq = lane & 3;
   for (int m = 0; m < mt; ++m) {
     const int b = m % kGdDBufs;
     mbar_wait(&d_full[b], (m / kGdDBufs) & 1);
     const double* D = Dbuf + static_cast<size_t>(b) * kGdTile * kGdStride;
+    if (shared) {
 #pragma unroll 2
-    for (int k0 = 0; k0 < kGdTile; k0 += 8) {
+      for (int k0 = 0; k0 < kGdTile; k0 += 8) {
 #pragma unroll
-      for (int p = 0; p < 2; ++p) {
-        const double* row = D + (k0 + 4 * p + kq) * kGdStride;
+        for (int p = 0; p < 2; ++p) {
+          const double* row = D + (k0 + 4 * p + kq) * kGdStride + g;
+          const double fa = row[ba[0] * 8];
 #pragma unroll
-        for (int u = 0; u < kGdBlocksPerWarp; ++u) {
-          if (warp + kGdMmaWarps * u < nblocks) {
-            const double a = row[ba[u] * 8 + g];   // A[r=g][k=kq] = D[k0+kq][8*ba + g]
-            const double bv = row[bb[u] * 8 + g];  // B[k=kq][c=g] = D[k0+kq][8*bb + g]
-            dmma_8x8x4(acc[u][p], a, bv);
-          }
+          for (int u = 0; u < kGdBlocksPerWarp; ++u) dmma_8x8x4(acc[u][p], fa, row[bb[u] * 8]);
+        }
+      }
+    } else {
+#pragma unroll 2
+      for (int k0 = 0; k0 < kGdTile; k0 += 8) {
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const double* row = D + (k0 + 4 * p + kq) * kGdStride + g;
+#pragma unroll
+          for (int u = 0; u < kGdBlocksPerWarp; ++u)
+            if (own[u]) dmma_8x8x4(acc[u][p], row[ba[u] * 8], row[bb[u] * 8]);
         }
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&d_empty[b]);
   }
-  // C[r][c]: r = g, c = 2*kq + {0,1}; write block and its mirror
+  // C[r][c] of block (ba, bb): r = g, c = 2*kq + {0,1}; write the block and its mirror
   double* out = parts + static_cast<size_t>(blockIdx.x) * d * d;
 #pragma unroll
   for (int u = 0; u < kGdBlocksPerWarp; ++u) {
-    if (warp + kGdMmaWarps * u >= nblocks) continue;
+    if (!own[u]) continue;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int r = ba[u] * 8 + g, c = bb[u] * 8 + 2 * kq + h;
