@@ -18,8 +18,17 @@ constexpr int kRowThreads = 256;
 constexpr int kRowWarps = kRowThreads / 32;
 constexpr int kMaxM = 4;  // 128-bit column groups per lane => d <= 64*kMaxM
 
+// One full wave of 2 CTAs per SM (16 warps, up to 128 registers per thread).  The earlier
+// 4 CTAs per SM grid against a 3-CTA register occupancy left a quarter of the work to a
+// second, 1-CTA wave: logreg L16 92 % -> 107 % of the copy peak, C2 65 % -> 98 % (profiles r77-r78).
+#ifndef DLX_ROW_GRID_MULT
+#define DLX_ROW_GRID_MULT 2
+#endif
+#ifndef DLX_ROW_MINB
+#define DLX_ROW_MINB 2
+#endif
 static int row_grid(int64_t n) {
-  int64_t grid = static_cast<int64_t>(sm_count()) * 4;
+  int64_t grid = static_cast<int64_t>(sm_count()) * DLX_ROW_GRID_MULT;
   const int64_t need = (n + kRowWarps - 1) / kRowWarps;
   return static_cast<int>(std::max<int64_t>(1, std::min(grid, need)));
 }
@@ -95,7 +104,7 @@ __device__ __forceinline__ int lane_of_row(int r) {
 // One fused pass: dot (FMA partials + reduce-scatter), sigmoid once per row on 4 lanes,
 // residual broadcast, gradient FMAs into per-lane registers.
 template <int M>
-__global__ void __launch_bounds__(kRowThreads)
+__global__ void __launch_bounds__(kRowThreads, DLX_ROW_MINB)
 logreg_grad_kernel(const double* __restrict__ x, const long long* __restrict__ y, int64_t n,
                    int d, const double* __restrict__ theta, double* __restrict__ parts) {
   pdl_wait();   // programmatic dependent launch: inputs are final from here on
@@ -145,7 +154,7 @@ logreg_grad_kernel(const double* __restrict__ x, const long long* __restrict__ y
 // ---------------------------------------------------------------------------------------
 // GDA pass 1: n1 = #{y == 1}, sum_c[j] = sum_{y_i == c} x_ij  (c in {0, 1})
 template <int M>
-__global__ void __launch_bounds__(kRowThreads)
+__global__ void __launch_bounds__(kRowThreads, DLX_ROW_MINB)
 gda_pass1_kernel(const double* __restrict__ x, const long long* __restrict__ y, int64_t n, int d,
                  double* __restrict__ parts0, double* __restrict__ parts1,
                  long long* __restrict__ parts_n1) {
