@@ -454,7 +454,8 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             result["roofline"] = {"bound": "tensor", "achieved": flops / (pass2_ms * 1e-3) / 1e12,
                                   "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                                   "frac": flops / (pass2_ms * 1e-3) / 1e12 / DMMA_PEAK_TFLOPS,
-                                  "traffic": None, "peak_kind": DMMA_PEAK_KIND, "kernel_ms": pass2_ms,
+                                  "traffic": ncu_traffic(args.config), "peak_kind": DMMA_PEAK_KIND,
+                                  "kernel_ms": pass2_ms,
                                   "algorithmic_flops_per_launch": flops}
         if world == 1 and not args.no_cpu_baseline:
             try:
