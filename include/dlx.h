@@ -122,6 +122,17 @@ int dlx_gda_pass1(const double* d_x, const int64_t* d_y, int64_t n, int32_t d, i
 int dlx_gda_means(const int64_t* d_n1, const double* d_sum0, const double* d_sum1,
                   int64_t n_total, int32_t d, double* d_mu0, double* d_mu1, dlx_stream_t stream);
 /* pass 2 (d*d reduces): S[a*d+b] = sum_i (x_ia - mu_{y_i,a}) (x_ib - mu_{y_i,b}) */
+/* Single-pass GDA fit (d <= 64): n1, mu0, mu1 and S from ONE read of x.  The scatter is
+ * accumulated around a shift (the class means of the first <= 64 rows) and corrected by the
+ * rank-1 terms sd_c sd_c^T / n_c; when the correction cancels more than 99 % of a diagonal
+ * entry, pass 2 on the exact means runs instead (decided on the device, no host sync).
+ * Results match dlx_gda_pass1 + dlx_gda_means + dlx_gda_pass2 to rtol 1e-9. */
+size_t dlx_gda_fit_workspace_bytes(int64_t n, int32_t d);
+int dlx_gda_fit(const double* d_x, const int64_t* d_y, int64_t n, int32_t d, int64_t* d_n1,
+                double* d_mu0, double* d_mu1, double* d_scatter, void* d_workspace,
+                size_t workspace_bytes, dlx_stream_t stream);
+/* 1 if the last dlx_gda_fit on this workspace took the exact-means fallback (synchronous). */
+int dlx_gda_fit_last_fallback(const void* d_workspace, int64_t n, int32_t d, int* h_fallback);
 int dlx_gda_pass2(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
                   const double* d_mu0, const double* d_mu1, double* d_scatter, void* d_workspace,
                   size_t workspace_bytes, dlx_stream_t stream);

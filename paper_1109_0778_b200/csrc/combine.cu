@@ -40,9 +40,10 @@ __device__ __forceinline__ void combine_columns(const Tin* __restrict__ parts, i
 template <class Tin, class Tout>
 __global__ void __launch_bounds__(kCombWarps * 32)
 combine_partials_kernel(const Tin* __restrict__ parts, int nparts, long long width,
-                        Tout* __restrict__ out) {
+                        Tout* __restrict__ out, const int* __restrict__ skip) {
   pdl_wait();   // programmatic dependent launch: inputs are final from here on
   pdl_trigger();
+  if (skip != nullptr && *skip) return;   // a device-side decision (GDA fit fallback)
   combine_columns<Tin, Tout>(parts, nparts, width, out, blockIdx.x);
 }
 
@@ -61,17 +62,21 @@ combine_pair_kernel(const double* __restrict__ pf, long long wf, double* __restr
 
 template <class Tin, class Tout>
 static int launch_combine(const Tin* parts, int nparts, long long width, Tout* out,
-                          cudaStream_t stream) {
+                          cudaStream_t stream, const int* skip = nullptr) {
   if (width <= 0) return DLX_OK;
   const long long blocks = (width + 31) / 32;
-  DLX_CUDA(launch_pdl(combine_partials_kernel<Tin, Tout>, dim3(static_cast<unsigned>(blocks)), dim3(kCombWarps * 32), 0, stream, 
-      parts, nparts, width, out));
+  DLX_CUDA(launch_pdl(combine_partials_kernel<Tin, Tout>, dim3(static_cast<unsigned>(blocks)), dim3(kCombWarps * 32), 0, stream,
+      parts, nparts, width, out, skip));
   DLX_LAUNCHED("combine_partials_kernel");
   return DLX_OK;
 }
 
 int combine_f64(const double* parts, int nparts, long long width, double* out, cudaStream_t s) {
   return launch_combine<double, double>(parts, nparts, width, out, s);
+}
+int combine_f64_unless(const double* parts, int nparts, long long width, double* out,
+                       const int* d_skip, cudaStream_t s) {
+  return launch_combine<double, double>(parts, nparts, width, out, s, d_skip);
 }
 int combine_i64(const long long* parts, int nparts, long long width, long long* out,
                 cudaStream_t s) {

@@ -55,6 +55,9 @@ int combine_i64(const long long* parts, int nparts, long long width, long long* 
 int combine_f64_i64(const double* pf, long long wf, double* of, const long long* pi, long long wi,
                     long long* oi, int nparts, cudaStream_t s);
 int combine_u32_i64(const unsigned* parts, int nparts, long long width, long long* out, cudaStream_t s);
+// combine_f64 that does nothing when the device flag *d_skip is set when it runs
+int combine_f64_unless(const double* parts, int nparts, long long width, double* out,
+                       const int* d_skip, cudaStream_t s);
 
 // Programmatic dependent launch (PDL): a kernel launched with launch_pdl may start while the
 // previous kernel on the stream is still running; it must call pdl_wait() before touching

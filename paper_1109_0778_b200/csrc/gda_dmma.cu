@@ -12,12 +12,13 @@
 // Data movement: one persistent CTA per SM, warp-specialised.  Each 64-sample tile's raw rows
 // (64 x d fp64, contiguous in the row-major matrix) and labels arrive by 1-D bulk TMA copies
 // into a three-slot ring, issued three tiles ahead, so HBM latency never stalls a warp (the
-// previous version's long-scoreboard stalls).  Eight centring warps turn a raw slot into a
+// previous version's long-scoreboard stalls).  Twelve centring warps turn a raw slot into a
 // padded operand tile D[b] = x - mu_y (row stride 68 doubles: the fragment loads of four
 // consecutive rows fall in distinct banks; two D buffers, mbarrier full/empty handshakes)
 // while twelve tensor-core warps own 3 lower blocks each (36 = 12 x 3 for d = 64) and run the
 // DMMA chains on the other D buffer, so centring overlaps the tensor-core phase.  (With four
-// centring warps the tensor-core warps sat on empty D buffers 20% of the time, profile r73.)
+// centring warps the tensor-core warps sat on empty D buffers 20% of the time, profile r73;
+// eight suffice for pass 2 alone, twelve keep up with the single-pass fit's class sums, r81.)
 #include <algorithm>
 
 #include "common.cuh"
@@ -29,12 +30,12 @@ using namespace sm100;
 
 constexpr int kGdMmaWarps = 12;                     // tensor-core warps: 3 lower blocks each
 #ifndef DLX_GDA_CTR_WARPS
-#define DLX_GDA_CTR_WARPS 8
+#define DLX_GDA_CTR_WARPS 12
 #endif
 #ifndef DLX_GDA_DBUFS
 #define DLX_GDA_DBUFS 2
 #endif
-constexpr int kGdCtrWarps = DLX_GDA_CTR_WARPS;      // centring warps (two per SM sub-partition)
+constexpr int kGdCtrWarps = DLX_GDA_CTR_WARPS;      // centring warps (three per SM sub-partition)
 constexpr int kGdThreads = (kGdMmaWarps + kGdCtrWarps) * 32;
 constexpr int kGdCtrThreads = kGdCtrWarps * 32;
 constexpr int kGdTile = 64;           // samples per tile
@@ -62,10 +63,19 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// kFused = false: pass 2 proper, centring on the class means mu0 / mu1 (skipped entirely when
+// *skip is set: the single-pass fit below already produced a certified S).
+// kFused = true: the single-pass fit.  Centring is on a shift c_y (the class means of the
+// first <= 64 rows, identical in every CTA), and the centring warps also accumulate the
+// shifted class sums sum_{y_i = c}(x_i - c_c) and n1, so one read of x yields
+// S' = sum (x - c_y)(x - c_y)^T, mu_c = c_c + sd_c / n_c and S = S' - sum_c sd_c sd_c^T / n_c.
+template <bool kFused>
 __global__ void __launch_bounds__(kGdThreads, 1)
 gda_pass2_dmma_kernel(const double* __restrict__ x, const long long* __restrict__ y, int64_t n,
                       int d, const double* __restrict__ mu0, const double* __restrict__ mu1,
-                      double* __restrict__ parts) {
+                      double* __restrict__ parts, const int* __restrict__ skip,
+                      double* __restrict__ parts_sd, long long* __restrict__ parts_n1,
+                      double* __restrict__ shift_out) {
   extern __shared__ __align__(1024) unsigned char smem[];
   double* const raw = reinterpret_cast<double*>(smem);
   long long* const ys = reinterpret_cast<long long*>(smem + kGdOffY);
@@ -105,17 +115,65 @@ gda_pass2_dmma_kernel(const double* __restrict__ x, const long long* __restrict_
   // even be the kernel that wrote x), so every global read comes after the wait
   pdl_wait();
   pdl_trigger();
-  for (int j = tid; j < 128; j += kGdThreads) {
-    const int c = j >> 6, jj = j & 63;
-    mu_s[j] = jj < d ? (c ? mu1[jj] : mu0[jj]) : 0.0;
+  if (!kFused && skip != nullptr && *skip) return;   // uniform over the grid
+  if (!kFused) {
+    for (int j = tid; j < 128; j += kGdThreads) {
+      const int c = j >> 6, jj = j & 63;
+      mu_s[j] = jj < d ? (c ? mu1[jj] : mu0[jj]) : 0.0;
+    }
   }
   __syncthreads();
 
   if (warp >= kGdMmaWarps) {
-    // ---- centring warps: raw slot -> D[b] = x - mu_y (zero outside n / d) -----------------
+    // ---- centring warps: raw slot -> D[b] = x - mu_y (or x - c_y), zero outside n / d ------
+    // thread = column pair (2cp, 2cp+1) x row phase rp: fixed columns, so the centre values
+    // and the fused class sums live in registers
     const int ct = tid - kIssuer;
+    const int cp = ct & 31, rp = ct >> 5, j0 = 2 * cp;
     if (ct == 0)
       for (int m = 0; m < kGdSlots && m < mt; ++m) issue(m);
+    if (kFused) {
+      // shift c_c = mean of the class-c rows among the first R <= 64 rows (all rows' mean for
+      // a class absent there, 0 for n = 0); every CTA computes it in the same order
+      const int R = static_cast<int>(std::min<int64_t>(n, 64));
+      double2 q0 = make_double2(0.0, 0.0), q1 = q0;
+      int k1 = 0;
+      for (int r = rp; r < R; r += kGdCtrWarps) {
+        const double vx = j0 < d ? x[static_cast<int64_t>(r) * d + j0] : 0.0;
+        const double vy = j0 + 1 < d ? x[static_cast<int64_t>(r) * d + j0 + 1] : 0.0;
+        const bool one = y[r] == 1;
+        if (one) { q1.x += vx; q1.y += vy; ++k1; } else { q0.x += vx; q0.y += vy; }
+      }
+      double* red = Dbuf;   // free until the first tile is centred
+      int* kred = reinterpret_cast<int*>(Dbuf + kGdCtrWarps * 128);
+      *reinterpret_cast<double2*>(red + rp * 128 + j0) = q0;
+      *reinterpret_cast<double2*>(red + rp * 128 + 64 + j0) = q1;
+      if (cp == 0) kred[rp] = k1;
+      named_bar(1, kGdCtrThreads);
+      const int c = (ct >> 6) & 1, j = ct & 63;   // threads 0..127: (class, column)
+      double sh = 0.0;
+      if (ct < 128) {
+        double t = 0.0, ta = 0.0;
+        int kc = 0;
+        for (int w = 0; w < kGdCtrWarps; ++w) {
+          t += red[w * 128 + c * 64 + j];
+          ta += red[w * 128 + j] + red[w * 128 + 64 + j];
+          kc += kred[w];
+        }
+        const int k_c = c ? kc : R - kc;
+        sh = k_c > 0 ? t / k_c : (R > 0 ? ta / R : 0.0);
+      }
+      named_bar(1, kGdCtrThreads);   // every read of red done before D is reused
+      if (ct < 128) {
+        mu_s[c * 64 + j] = j < d ? sh : 0.0;
+        if (blockIdx.x == 0) shift_out[c * 64 + j] = j < d ? sh : 0.0;
+      }
+      named_bar(1, kGdCtrThreads);
+    }
+    const double2 m0 = *reinterpret_cast<const double2*>(mu_s + j0);
+    const double2 m1 = *reinterpret_cast<const double2*>(mu_s + 64 + j0);
+    double2 a0 = make_double2(0.0, 0.0), a1 = a0;   // fused: shifted class sums of my columns
+    long long c1 = 0;                                // fused: class-1 rows (cp == 0 threads)
     for (int m = 0; m < mt; ++m) {
       const int s = m % kGdSlots, b = m % kGdDBufs;
       const int64_t i0 = tile_of(m) * kGdTile;
@@ -127,39 +185,37 @@ gda_pass2_dmma_kernel(const double* __restrict__ x, const long long* __restrict_
       const long long* yv = ys + s * kGdTile;
       double* D = Dbuf + static_cast<size_t>(b) * kGdTile * kGdStride;
       if (from_smem && d == 64) {
-        // fast path: thread = column pair (2cp, 2cp+1) x row phase; mu pair in registers, one
-        // label broadcast per warp-row, 16-byte loads and stores
-        const int cp = ct & 31, rp = ct >> 5;
-        const double2 m0 = *reinterpret_cast<const double2*>(mu_s + 2 * cp);
-        const double2 m1 = *reinterpret_cast<const double2*>(mu_s + 64 + 2 * cp);
+        // fast path: one label broadcast per warp-row, 16-byte loads and stores
 #pragma unroll 4
         for (int r = rp; r < kGdTile; r += kGdCtrWarps) {
-          const double2 xv = *reinterpret_cast<const double2*>(rs + r * 64 + 2 * cp);
+          const double2 xv = *reinterpret_cast<const double2*>(rs + r * 64 + j0);
           const bool one = yv[r] == 1;
           double2 o;
           o.x = xv.x - (one ? m1.x : m0.x);
           o.y = xv.y - (one ? m1.y : m0.y);
-          *reinterpret_cast<double2*>(D + r * kGdStride + 2 * cp) = o;
-        }
-      } else
-#pragma unroll 2
-      for (int e0 = ct; e0 < kGdTile * 64; e0 += 4 * kGdCtrThreads) {
-        double v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int e = e0 + u * kGdCtrThreads;
-          const int r = e >> 6, j = e & 63;
-          v[u] = 0.0;
-          if (r < rows && j < d) {
-            const double xv = from_smem ? rs[r * d + j] : __ldg(x + (i0 + r) * d + j);
-            const long long lab = from_smem ? yv[r] : __ldg(y + i0 + r);
-            v[u] = xv - mu_s[(lab == 1 ? 64 : 0) + j];
+          *reinterpret_cast<double2*>(D + r * kGdStride + j0) = o;
+          if (kFused) {
+            a1.x += one ? o.x : 0.0; a1.y += one ? o.y : 0.0;
+            a0.x += one ? 0.0 : o.x; a0.y += one ? 0.0 : o.y;
+            c1 += one;
           }
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int e = e0 + u * kGdCtrThreads;
-          D[(e >> 6) * kGdStride + (e & 63)] = v[u];
+      } else {
+        for (int r = rp; r < kGdTile; r += kGdCtrWarps) {
+          double2 o = make_double2(0.0, 0.0);
+          if (r < rows) {
+            const int64_t gi = i0 + r;
+            const long long lab = from_smem ? yv[r] : __ldg(y + gi);
+            const bool one = lab == 1;
+            if (j0 < d) o.x = (from_smem ? rs[r * d + j0] : __ldg(x + gi * d + j0)) - (one ? m1.x : m0.x);
+            if (j0 + 1 < d) o.y = (from_smem ? rs[r * d + j0 + 1] : __ldg(x + gi * d + j0 + 1)) - (one ? m1.y : m0.y);
+            if (kFused) {
+              a1.x += one ? o.x : 0.0; a1.y += one ? o.y : 0.0;
+              a0.x += one ? 0.0 : o.x; a0.y += one ? 0.0 : o.y;
+              c1 += one;
+            }
+          }
+          *reinterpret_cast<double2*>(D + r * kGdStride + j0) = o;
         }
       }
       named_bar(1, kGdCtrThreads);   // D[b] written, raw slot s read by every centring thread
@@ -169,6 +225,27 @@ gda_pass2_dmma_kernel(const double* __restrict__ x, const long long* __restrict_
           fence_proxy_async_smem();   // generic-proxy reads of slot s before the async refill
           issue(m + kGdSlots);
         }
+      }
+    }
+    if (kFused) {
+      // per-CTA partial record: sd_c[j] (ascending row-phase fold) and n1; raw slot 0 is free
+      // (every tile has been consumed and no copy is outstanding)
+      double* red = raw;
+      long long* kred = reinterpret_cast<long long*>(raw + kGdCtrWarps * 128);
+      *reinterpret_cast<double2*>(red + rp * 128 + j0) = a0;
+      *reinterpret_cast<double2*>(red + rp * 128 + 64 + j0) = a1;
+      if (cp == 0) kred[rp] = c1;
+      named_bar(1, kGdCtrThreads);
+      if (ct < 128) {
+        const int c = ct >> 6, j = ct & 63;
+        double t = 0.0;
+        for (int w = 0; w < kGdCtrWarps; ++w) t += red[w * 128 + c * 64 + j];
+        if (j < d) parts_sd[static_cast<size_t>(blockIdx.x) * 2 * d + c * d + j] = t;
+      }
+      if (ct == 0) {
+        long long k = 0;
+        for (int w = 0; w < kGdCtrWarps; ++w) k += kred[w];
+        parts_n1[blockIdx.x] = k;
       }
     }
     return;
@@ -260,11 +337,135 @@ int gda_pass2_dmma(const double* x, const long long* y, int64_t n, int d, const 
   const int grid = gda_pass2_dmma_grid(n);
   DLX_REQUIRE(parts && parts_bytes >= static_cast<size_t>(grid) * d * d * sizeof(double),
               DLX_ERR_ARG, "gda: workspace too small");
-  DLX_CUDA(cudaFuncSetAttribute(gda_pass2_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  DLX_CUDA(cudaFuncSetAttribute(gda_pass2_dmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(kGdSmem)));
-  DLX_CUDA(launch_pdl(gda_pass2_dmma_kernel, dim3(grid), dim3(kGdThreads), kGdSmem, stream, x, y, n, d, mu0, mu1, parts));
+  DLX_CUDA(launch_pdl(gda_pass2_dmma_kernel<false>, dim3(grid), dim3(kGdThreads), kGdSmem, stream, x, y, n,
+                      d, mu0, mu1, parts, static_cast<const int*>(nullptr), static_cast<double*>(nullptr),
+                      static_cast<long long*>(nullptr), static_cast<double*>(nullptr)));
   DLX_LAUNCHED("gda_pass2_dmma_kernel");
   return combine_f64(parts, grid, static_cast<long long>(d) * d, out, stream);
 }
 
+// Single-pass fit, last step: mu_c = c_c + sd_c / n_c and S = S' - sum_c sd_c sd_c^T / n_c.
+// Certified: the rank-1 corrections may cancel at most 99 % of any diagonal entry of S'
+// (relative rounding amplification <= 100); otherwise *ok = 0 and the caller's pass 2 on the
+// exact means runs (gda_pass2_dmma_kernel<false> / combine gated on *ok).
+__global__ void __launch_bounds__(1024)
+gda_fit_finalize_kernel(const double* __restrict__ Sp, const double* __restrict__ sd,
+                        const long long* __restrict__ n1p, int64_t n, int d,
+                        const double* __restrict__ shift, long long* __restrict__ n1_out,
+                        double* __restrict__ mu0, double* __restrict__ mu1, double* __restrict__ S,
+                        int* __restrict__ ok) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ int bad;
+  const long long n1 = *n1p, n0 = n - n1;
+  const double dn0 = static_cast<double>(n0), dn1 = static_cast<double>(n1);
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  auto corr = [&](int a, int b) {
+    double c = 0.0;
+    if (n0 > 0) c += sd[a] * sd[b] / dn0;
+    if (n1 > 0) c += sd[d + a] * sd[d + b] / dn1;
+    return c;
+  };
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    mu0[j] = shift[j] + sd[j] / dn0;            // an empty class: 0 / 0 -> NaN, as the reference
+    mu1[j] = shift[64 + j] + sd[d + j] / dn1;
+    const double cj = corr(j, j), sj = Sp[j * d + j];
+    if (!(cj <= 0.99 * sj)) bad = 1;            // also catches NaN / inf
+  }
+  for (int e = threadIdx.x; e < d * d; e += blockDim.x) S[e] = Sp[e] - corr(e / d, e % d);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *ok = !bad;
+    *n1_out = n1;
+  }
+}
+
+size_t gda_fit_workspace_bytes(int64_t n, int d) {
+  const int grid = gda_pass2_dmma_grid(n);
+  Carve c(nullptr);
+  c.take<double>(static_cast<size_t>(grid) * d * d);
+  c.take<double>(static_cast<size_t>(grid) * 2 * d);
+  c.take<long long>(grid);
+  c.take<double>(static_cast<size_t>(d) * d);
+  c.take<double>(2 * static_cast<size_t>(d));
+  c.take<long long>(1);
+  c.take<double>(128);
+  c.take<int>(1);
+  return c.used + 256;
+}
+
+int gda_fit(const double* x, const long long* y, int64_t n, int d, long long* n1_out, double* mu0,
+            double* mu1, double* S, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  DLX_REQUIRE(n >= 0 && d > 0, DLX_ERR_ARG, "gda fit: bad shape");
+  DLX_REQUIRE(d <= 64, DLX_ERR_GENERATION, "GenerationFailed: single-pass GDA fit needs d <= 64");
+  const int grid = gda_pass2_dmma_grid(n);
+  Carve c(ws);
+  double* parts = c.take<double>(static_cast<size_t>(grid) * d * d);
+  double* parts_sd = c.take<double>(static_cast<size_t>(grid) * 2 * d);
+  long long* parts_n1 = c.take<long long>(grid);
+  double* Sp = c.take<double>(static_cast<size_t>(d) * d);
+  double* sd = c.take<double>(2 * static_cast<size_t>(d));
+  long long* n1 = c.take<long long>(1);
+  double* shift = c.take<double>(128);
+  int* ok = c.take<int>(1);
+  DLX_REQUIRE(ws && c.used <= ws_bytes, DLX_ERR_ARG, "gda fit: workspace too small");
+  DLX_CUDA(cudaFuncSetAttribute(gda_pass2_dmma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kGdSmem)));
+  DLX_CUDA(cudaFuncSetAttribute(gda_pass2_dmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kGdSmem)));
+  DLX_CUDA(launch_pdl(gda_pass2_dmma_kernel<true>, dim3(grid), dim3(kGdThreads), kGdSmem, stream, x, y, n, d,
+                      static_cast<const double*>(nullptr), static_cast<const double*>(nullptr), parts,
+                      static_cast<const int*>(nullptr), parts_sd, parts_n1, shift));
+  DLX_LAUNCHED("gda_pass2_dmma_kernel");
+  int rc = combine_f64(parts, grid, static_cast<long long>(d) * d, Sp, stream);
+  if (rc == DLX_OK) rc = combine_f64_i64(parts_sd, 2LL * d, sd, parts_n1, 1, n1, grid, stream);
+  if (rc != DLX_OK) return rc;
+  DLX_CUDA(launch_pdl(gda_fit_finalize_kernel, dim3(1), dim3(1024), 0, stream, static_cast<const double*>(Sp),
+                      static_cast<const double*>(sd), static_cast<const long long*>(n1), n, d,
+                      static_cast<const double*>(shift), n1_out, mu0, mu1, S, ok));
+  DLX_LAUNCHED("gda_fit_finalize_kernel");
+  // fallback, decided on the device: pass 2 on the exact means when the shift was too far off
+  DLX_CUDA(launch_pdl(gda_pass2_dmma_kernel<false>, dim3(grid), dim3(kGdThreads), kGdSmem, stream, x, y, n, d,
+                      static_cast<const double*>(mu0), static_cast<const double*>(mu1), parts,
+                      static_cast<const int*>(ok), static_cast<double*>(nullptr),
+                      static_cast<long long*>(nullptr), static_cast<double*>(nullptr)));
+  DLX_LAUNCHED("gda_pass2_dmma_kernel");
+  return combine_f64_unless(parts, grid, static_cast<long long>(d) * d, S, ok, stream);
+}
+
 }  // namespace dlx
+
+extern "C" {
+
+size_t dlx_gda_fit_workspace_bytes(int64_t n, int32_t d) { return dlx::gda_fit_workspace_bytes(n, d); }
+
+int dlx_gda_fit(const double* d_x, const int64_t* d_y, int64_t n, int32_t d, int64_t* d_n1,
+                double* d_mu0, double* d_mu1, double* d_scatter, void* d_workspace,
+                size_t workspace_bytes, dlx_stream_t stream) {
+  return dlx::gda_fit(d_x, reinterpret_cast<const long long*>(d_y), n, d, reinterpret_cast<long long*>(d_n1),
+                      d_mu0, d_mu1, d_scatter, d_workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int dlx_gda_fit_last_fallback(const void* d_workspace, int64_t n, int32_t d, int* h_fallback) {
+  // the certification flag of the last dlx_gda_fit on this workspace (synchronous read)
+  DLX_REQUIRE(d_workspace && h_fallback, DLX_ERR_ARG, "gda fit: bad args");
+  dlx::Carve c(const_cast<void*>(d_workspace));
+  const int grid = dlx::gda_pass2_dmma_grid(n);
+  c.take<double>(static_cast<size_t>(grid) * d * d);
+  c.take<double>(static_cast<size_t>(grid) * 2 * d);
+  c.take<long long>(grid);
+  c.take<double>(static_cast<size_t>(d) * d);
+  c.take<double>(2 * static_cast<size_t>(d));
+  c.take<long long>(1);
+  c.take<double>(128);
+  int* ok = c.take<int>(1);
+  int h = 0;
+  DLX_CUDA(cudaMemcpy(&h, ok, sizeof(int), cudaMemcpyDeviceToHost));
+  *h_fallback = !h;
+  return DLX_OK;
+}
+
+}  // extern "C"

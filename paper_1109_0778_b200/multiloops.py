@@ -217,9 +217,36 @@ def gda_pass2(x: torch.Tensor, y: torch.Tensor, mu0: torch.Tensor, mu1: torch.Te
     return out
 
 
+def gda_fit(x: torch.Tensor, y: torch.Tensor):
+    """Single-pass fit (d <= 64, csrc/gda_dmma.cu): n1, mu0, mu1, S from one read of x."""
+    L = _lib.load()
+    n, d = x.shape
+    n1 = torch.empty(1, dtype=_I64, device=x.device)
+    mu0 = torch.empty(d, dtype=_F64, device=x.device)
+    mu1 = torch.empty(d, dtype=_F64, device=x.device)
+    S = torch.empty((d, d), dtype=_F64, device=x.device)
+    ws, wsb = _WS.get(L.dlx_gda_fit_workspace_bytes(n, d), x.device)
+    check(L.dlx_gda_fit(_ptr(x), _ptr(y), n, d, _ptr(n1), _ptr(mu0), _ptr(mu1), _ptr(S), ws, wsb, _stream()))
+    return n1, mu0, mu1, S
+
+
+def gda_fit_last_fallback(x: torch.Tensor) -> bool:
+    """Whether the last gda_fit on x's shape took the exact-means fallback (synchronises)."""
+    L = _lib.load()
+    n, d = x.shape
+    ws, _ = _WS.get(L.dlx_gda_fit_workspace_bytes(n, d), x.device)
+    flag = ctypes.c_int(0)
+    check(L.dlx_gda_fit_last_fallback(ws, n, d, ctypes.byref(flag)))
+    return bool(flag.value)
+
+
 def gda(x: torch.Tensor, y: torch.Tensor, comm=None):
-    """phi-numerator n1, mu0, mu1 and the unnormalised scatter S."""
-    n_local = x.shape[0]
+    """phi-numerator n1, mu0, mu1 and the unnormalised scatter S.  One
+    device-local fit reads x once (gda_fit); sharded fits run the two reference passes with
+    the class sums and the scatter summed across ranks in between."""
+    n_local, d = x.shape
+    if comm is None and d <= 64:
+        return gda_fit(x, y)
     n1, s0, s1 = gda_pass1(x, y)
     n_total = n_local
     if comm is not None:

@@ -320,6 +320,67 @@ def test_gda_shapes(ml, n, d):
         np.testing.assert_allclose(S.cpu().numpy(), Sr, rtol=RTOL, atol=1e-9 * max(1.0, np.abs(Sr).max()))
 
 
+def _gda_two_pass(ml, x, y):
+    n1, s0, s1 = ml.gda_pass1(x, y)
+    mu0, mu1 = ml.gda_means(n1, s0, s1, x.shape[0])
+    return n1, mu0, mu1, ml.gda_pass2(x, y, mu0, mu1)
+
+
+@pytest.mark.parametrize("n,d", [(1, 64), (63, 64), (64, 64), (65, 64), (10_000, 64), (1_048_576, 64), (5_001, 17), (40_000, 32)])
+def test_gda_fit_matches_two_pass(ml, n, d):
+    """The single-pass fit (shifted scatter + rank-1 correction) against the reference's two
+    passes on the same device, and its certification flag stays clear on iid data."""
+    x = dev_units(ml, n, d, seed=9)
+    y = ml.rng_ints(n, 2, seed=9, first_draw=n * d)
+    f = ml.gda_fit(x, y)
+    assert not ml.gda_fit_last_fallback(x) or n < 2
+    if d % 2:   # the two-pass row kernels need even d; the fit does not: check it on the oracle
+        xh, yh = x.cpu().numpy(), y.cpu().numpy()
+        n1r, s0, s1 = O.gda_pass1(xh, yh)
+        m0, m1 = s0 / float(n - n1r), s1 / float(n1r)
+        t = (torch.tensor([n1r]), torch.from_numpy(m0), torch.from_numpy(m1),
+             torch.from_numpy(O.gda_pass2(xh, yh, m0, m1)))
+    else:
+        t = _gda_two_pass(ml, x, y)
+    assert int(f[0].item()) == int(t[0].item())
+    for a, b in zip(f[1:], t[1:]):
+        a, b = a.cpu().numpy(), b.cpu().numpy()
+        np.testing.assert_allclose(a, b, rtol=RTOL, atol=1e-9 * max(1.0, np.nanmax(np.abs(b))) if np.isfinite(b).any() else 0)
+
+
+@pytest.mark.parametrize("kind", ["sorted_offset", "one_class_first", "single_class", "huge_mean"])
+def test_gda_fit_fallback(ml, kind):
+    """Inputs whose first rows misrepresent the class means: the rank-1 correction would cancel
+    the shifted scatter, the device-side certification rejects it and pass 2 on the exact
+    means runs; results equal the two-pass path either way."""
+    n, d = 20_000, 64
+    x = dev_units(ml, n, d, seed=10)
+    y = ml.rng_ints(n, 2, seed=10, first_draw=n * d)
+    if kind == "sorted_offset":        # first 64 rows near 0, the rest near 1e4
+        x[64:] += 1.0e4
+    elif kind == "one_class_first":    # first 64 rows all class 1, far from the class-0 mean
+        y[:64] = 1
+        x[:64] -= 5.0e3
+    elif kind == "single_class":       # class 0 empty: mu0 is NaN, S from class 1 only
+        y[:] = 1
+    else:                              # mean 1e6, unit spread: the shift handles it
+        x += 1.0e6
+    f = ml.gda_fit(x, y)
+    fb = ml.gda_fit_last_fallback(x)
+    if kind in ("sorted_offset", "one_class_first"):
+        assert fb
+    if kind == "huge_mean":
+        assert not fb
+    t = _gda_two_pass(ml, x, y)
+    assert int(f[0].item()) == int(t[0].item())
+    for a, b in zip(f[1:], t[1:]):
+        a, b = a.cpu().numpy(), b.cpu().numpy()
+        assert np.array_equal(np.isnan(a), np.isnan(b))
+        fin = np.isfinite(b)
+        if fin.any():
+            np.testing.assert_allclose(a[fin], b[fin], rtol=RTOL, atol=1e-9 * np.abs(b[fin]).max())
+
+
 # ---- generic collect / reduce -------------------------------------------------------------------------
 
 def test_generic_families(ml):
