@@ -36,6 +36,9 @@ CONFIGS = {
     "l16": ("logreg", dict(n=16_777_216, d=64), "logistic-regression BGD iters/sec (N=16M,d=64)", "it/s"),
     "c3": ("gda", dict(n=1_048_576, d=64), "GDA fits/sec (N=1M,d=64)", "fits/s"),
     "c5": ("groupby", dict(n=1_000_000_000, K=64), "GroupBy bucket-count passes/sec (1e9 keys, K=64)", "passes/s"),
+    # SURVEY §8 a7 leaves K open and proposes a sweep: 4,096 and 65,536 buckets
+    "c5k4096": ("groupby", dict(n=1_000_000_000, K=4096), "GroupBy bucket-count passes/sec (1e9 keys, K=4096)", "passes/s"),
+    "c5k65536": ("groupby", dict(n=1_000_000_000, K=65536), "GroupBy bucket-count passes/sec (1e9 keys, K=65536)", "passes/s"),
 }
 
 # algorithmic bytes per unit: k-means sample d*8 + 4 (int32 assignment write);

@@ -230,7 +230,7 @@ def test_c4_first_two_iterations(ml, golden, oracle_hashes, method):
 # ---- GroupBy ------------------------------------------------------------------------------------
 
 @pytest.mark.parametrize("n,K", [(1, 64), (1001, 64), (1_000_003, 64), (1_000_000, 4096), (999_999, 65536),
-                                 (500_000, 200_000), (100, 1)])
+                                 (77_777, 30_001), (1, 65536), (500_000, 200_000), (100, 1)])
 def test_groupby(ml, n, K):
     keys = ml.rng_ints(n, K, seed=K)
     assert np.array_equal(ml.groupby_count(keys, K).cpu().numpy(), O.groupby_count(keys.cpu().numpy(), K))
@@ -240,6 +240,17 @@ def test_groupby_out_of_range(ml):
     keys = torch.tensor([0, 1, 1, -1, 5, 4, 2, 1 << 40, 3], dtype=torch.int64, device="cuda")
     assert ml.groupby_count(keys, 5).cpu().tolist() == [1, 2, 1, 1, 1]
     assert ml.groupby_count(keys, 300_000).cpu().numpy()[:6].tolist() == [1, 2, 1, 1, 1, 1]
+    assert ml.groupby_count(keys, 50_001).cpu().numpy()[:6].tolist() == [1, 2, 1, 1, 1, 1]   # cluster path
+
+
+@pytest.mark.parametrize("key", [0, 40_000, 65_535])
+def test_groupby_cluster_one_hot_bucket(ml, key):
+    """Every key in one bucket (local or partner-SM half of the two-CTA histogram): maximal
+    contention on a single distributed-shared-memory counter."""
+    n = 3_000_001
+    keys = torch.full((n,), key, dtype=torch.int64, device="cuda")
+    c = ml.groupby_count(keys, 65536).cpu().numpy()
+    assert c[key] == n and c.sum() == n
 
 
 @pytest.mark.parametrize("K", ["64", "4096", "65536"])
