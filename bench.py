@@ -39,6 +39,8 @@ CONFIGS = {
     # SURVEY §8 a7 leaves K open and proposes a sweep: 4,096 and 65,536 buckets
     "c5k4096": ("groupby", dict(n=1_000_000_000, K=4096), "GroupBy bucket-count passes/sec (1e9 keys, K=4096)", "passes/s"),
     "c5k65536": ("groupby", dict(n=1_000_000_000, K=65536), "GroupBy bucket-count passes/sec (1e9 keys, K=65536)", "passes/s"),
+    "c5k131072": ("groupby", dict(n=1_000_000_000, K=131072), "GroupBy bucket-count passes/sec (1e9 keys, K=131072)", "passes/s"),
+    "c5k262144": ("groupby", dict(n=1_000_000_000, K=262144), "GroupBy bucket-count passes/sec (1e9 keys, K=262144)", "passes/s"),
 }
 
 # algorithmic bytes per unit: k-means sample d*8 + 4 (int32 assignment write);

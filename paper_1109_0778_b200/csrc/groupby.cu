@@ -19,11 +19,15 @@ constexpr int kGbThreads = 512;
 constexpr size_t kGbSmemBudget = 96 * 1024;
 constexpr int kGbPairThreads = 1024;               // two-CTA cluster path (groupby_pair_kernel)
 
-constexpr size_t kGbPairSmemBudget = 200 * 1024;   // half histogram per CTA
+constexpr size_t kGbPairSmemBudget = 200 * 1024;   // histogram slice per CTA
+#ifndef DLX_GB_MAX_CLUSTER
+#define DLX_GB_MAX_CLUSTER 4
+#endif
 
 struct GroupbyPlan {
   bool shared;   // shared-memory privatised path
-  bool pair;     // two-CTA cluster, one histogram across both shared memories
+  bool pair;     // CTA cluster, one histogram sliced across the cluster's shared memories
+  int csize;     // cluster size (2, 4, 8)
   int copies;    // sub-histograms per CTA
   int grid;
   size_t smem;
@@ -46,12 +50,15 @@ static GroupbyPlan groupby_plan(int64_t n, int64_t nb) {
     p.copies = 0;
     p.smem = 0;
     per_sm = 4;
-    const size_t half = static_cast<size_t>((nb + 1) / 2) * sizeof(unsigned);
-    if (half <= kGbPairSmemBudget) {
-      p.pair = true;
-      p.smem = half;
-      p.grid = (sm_count() / 2) * 2;   // one CTA per SM, whole clusters
-      return p;
+    for (int c = 2; c <= DLX_GB_MAX_CLUSTER; c *= 2) {
+      const size_t slice = static_cast<size_t>((nb + c - 1) / c) * sizeof(unsigned);
+      if (slice <= kGbPairSmemBudget) {
+        p.pair = true;
+        p.csize = c;
+        p.smem = slice;
+        p.grid = (sm_count() / c) * c;   // one CTA per SM, whole clusters
+        return p;
+      }
     }
   }
   int64_t grid = static_cast<int64_t>(sm_count()) * per_sm;
@@ -115,26 +122,31 @@ groupby_smem_kernel(const long long* __restrict__ keys, int64_t n, long long nb,
 // foreign half incremented remotely through distributed shared memory: 1.61 ms vs 5.42 ms at
 // 1e9 keys, K = 65,536 (remote DSMEM atomics are the bottleneck); the global-atomics path
 // this replaces took 6.54 ms.
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGbPairThreads, 1)
+// Cluster size kC = 2 or 4 (DLX_GB_MAX_CLUSTER; 8 is built but loses to global atomics, r89):
+// each CTA holds a 1/kC slice of the histogram and every key of the cluster's stream is read
+// by kC SMs (L2 hits after the first), so the L2->SM stream grows with kC.
+template <int kC>
+__global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kGbPairThreads, 1)
 groupby_pair_kernel(const long long* __restrict__ keys, int64_t n, long long nb,
                     unsigned* __restrict__ partials) {
   namespace cg = cooperative_groups;
   extern __shared__ unsigned hist[];
-  const long long half = (nb + 1) / 2;
+  const long long per = (nb + kC - 1) / kC;
   const unsigned rank = cg::this_cluster().block_rank();
-  for (long long e = threadIdx.x; e < half; e += kGbPairThreads) hist[e] = 0;
+  for (long long e = threadIdx.x; e < per; e += kGbPairThreads) hist[e] = 0;
   __syncthreads();
   pdl_wait();  // programmatic dependent launch: keys are final from here on
   pdl_trigger();
-  const unsigned long long lo_k = rank ? half : 0, w_k = rank ? nb - half : half;
+  const long long lo = std::min<long long>(nb, rank * per), w = std::min<long long>(per, nb - lo);
+  const unsigned long long lo_k = static_cast<unsigned long long>(lo), w_k = static_cast<unsigned long long>(w);
   auto count = [&](long long key) {
     const unsigned long long rel = static_cast<unsigned long long>(key) - lo_k;   // < 0 wraps
     if (rel < w_k) atomicAdd(hist + rel, 1u);
   };
   const int64_t npairs = n >> 1;
   const longlong2* kp = reinterpret_cast<const longlong2*>(keys);
-  const int64_t T = static_cast<int64_t>(gridDim.x >> 1) * kGbPairThreads;
-  int64_t q = static_cast<int64_t>(blockIdx.x >> 1) * kGbPairThreads + threadIdx.x;
+  const int64_t T = static_cast<int64_t>(gridDim.x / kC) * kGbPairThreads;
+  int64_t q = static_cast<int64_t>(blockIdx.x / kC) * kGbPairThreads + threadIdx.x;
   for (; q + 3 * T < npairs; q += 4 * T) {
     longlong2 v0 = __ldg(kp + q), v1 = __ldg(kp + q + T), v2 = __ldg(kp + q + 2 * T),
               v3 = __ldg(kp + q + 3 * T);
@@ -146,10 +158,9 @@ groupby_pair_kernel(const long long* __restrict__ keys, int64_t n, long long nb,
     count(v.x);
     count(v.y);
   }
-  if ((n & 1) && (blockIdx.x >> 1) == 0 && threadIdx.x == 0) count(keys[n - 1]);   // both halves look
+  if ((n & 1) && blockIdx.x / kC == 0 && threadIdx.x == 0) count(keys[n - 1]);   // every slice looks
   __syncthreads();
-  const long long lo = rank * half, w = std::min<long long>(half, nb - lo);
-  unsigned* out = partials + static_cast<size_t>(blockIdx.x >> 1) * nb + lo;
+  unsigned* out = partials + static_cast<size_t>(blockIdx.x / kC) * nb + lo;
   for (long long b = threadIdx.x; b < w; b += kGbPairThreads) out[b] = hist[b];
 }
 
@@ -184,7 +195,7 @@ extern "C" {
 
 size_t dlx_groupby_workspace_bytes(int64_t n, int64_t nbuckets) {
   GroupbyPlan p = groupby_plan(n, nbuckets);
-  if (p.pair) return static_cast<size_t>(p.grid / 2) * nbuckets * sizeof(unsigned) + 256;
+  if (p.pair) return static_cast<size_t>(p.grid / p.csize) * nbuckets * sizeof(unsigned) + 256;
   if (!p.shared) return 256;
   return static_cast<size_t>(p.grid) * nbuckets * sizeof(unsigned) + 256;
 }
@@ -197,14 +208,14 @@ int dlx_groupby_count(const int64_t* d_keys, int64_t n, int64_t nbuckets, int64_
               "groupby: keys must be 16-byte aligned");
   GroupbyPlan p = groupby_plan(n, nbuckets);
   if (p.pair) {
-    const int clusters = p.grid / 2;
+    const int clusters = p.grid / p.csize;
     const size_t need = static_cast<size_t>(clusters) * nbuckets * sizeof(unsigned);
     DLX_REQUIRE(d_workspace && workspace_bytes >= need, DLX_ERR_ARG,
                 "groupby: workspace too small (%zu < %zu)", workspace_bytes, need);
     unsigned* partials = static_cast<unsigned*>(d_workspace);
-    DLX_CUDA(cudaFuncSetAttribute(groupby_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(p.smem)));
-    DLX_CUDA(launch_pdl(groupby_pair_kernel, dim3(p.grid), dim3(kGbPairThreads), p.smem, stream,
+    auto kern = p.csize == 2 ? groupby_pair_kernel<2> : p.csize == 4 ? groupby_pair_kernel<4> : groupby_pair_kernel<8>;
+    DLX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem)));
+    DLX_CUDA(launch_pdl(kern, dim3(p.grid), dim3(kGbPairThreads), p.smem, stream,
                         reinterpret_cast<const long long*>(d_keys), n, nbuckets, partials));
     DLX_LAUNCHED("groupby_pair_kernel");
     return combine_u32_i64(partials, clusters, nbuckets, reinterpret_cast<long long*>(d_counts), stream);

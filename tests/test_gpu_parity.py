@@ -230,7 +230,8 @@ def test_c4_first_two_iterations(ml, golden, oracle_hashes, method):
 # ---- GroupBy ------------------------------------------------------------------------------------
 
 @pytest.mark.parametrize("n,K", [(1, 64), (1001, 64), (1_000_003, 64), (1_000_000, 4096), (999_999, 65536),
-                                 (77_777, 30_001), (1, 65536), (500_000, 200_000), (100, 1)])
+                                 (77_777, 30_001), (1, 65536), (500_000, 200_000), (400_001, 300_001),
+                                 (300_000, 500_000), (100, 1)])
 def test_groupby(ml, n, K):
     keys = ml.rng_ints(n, K, seed=K)
     assert np.array_equal(ml.groupby_count(keys, K).cpu().numpy(), O.groupby_count(keys.cpu().numpy(), K))
