@@ -89,9 +89,9 @@ int sm_count();
 struct Carve {
   char* base;
   size_t used = 0;
-  explicit Carve(void* p) : base(static_cast<char*>(p)) {}
+  __host__ __device__ explicit Carve(void* p) : base(static_cast<char*>(p)) {}
   template <class T>
-  T* take(size_t count) {
+  __host__ __device__ T* take(size_t count) {
     used = (used + 255) & ~size_t(255);
     T* p = reinterpret_cast<T*>(base ? base + used : nullptr);
     used += count * sizeof(T);

@@ -186,6 +186,168 @@ kmeans_direct_kernel(const double* __restrict__ x, int64_t n, int d, int k,
   for (int c = tid; c < k; c += kThreads) pc[c] = counts_s[c];
 }
 
+// ---------------------------------------------------------------------------------------
+// Small-problem direct kernel (d <= 64, k <= 64): the reference chain computed exactly, one
+// sample per thread, for shapes where the screen's fixed per-launch cost (TMEM setup, plane
+// prologue, pipeline ramp, flush) or its per-row streaming cost exceeds the fp64 work —
+// C1 (65,536 x 16, k = 8) and any k*d <= 512.  128-sample tiles; the bucket-reduce is a
+// stable counting sort of the tile by assignment (per-warp __match_any ranks) followed by a
+// segmented fold: the cell (c, j) owner adds the tile's class-c samples in ascending sample
+// order, so the CTA's record is deterministic without fp64 atomics.
+constexpr int kSmThreads = 128;
+
+struct SmallPlan {
+  int xstride;   // odd padded row stride of the staged tile
+  size_t smem;
+  int grid;
+};
+
+static bool small_plan(int64_t n, int d, int k, SmallPlan* p) {
+  if (d > 64 || k > 64) return false;
+  p->xstride = d | 1;
+  Carve c(nullptr);
+  c.take<double>(static_cast<size_t>(k) * d);                       // mu
+  c.take<double>(static_cast<size_t>(k) * d);                       // sums
+  c.take<double>(static_cast<size_t>(kSmThreads) * p->xstride);     // x tile
+  c.take<long long>(64);                                            // CTA counts
+  c.take<int>(kSmThreads);                                          // tile assignments
+  c.take<int>(kSmThreads);                                          // sorted order
+  c.take<int>(64);                                                  // tile counts
+  c.take<int>(64);                                                  // tile offsets
+  c.take<int>(4 * 64);                                              // per-warp counts
+  p->smem = c.used + 256;
+  const int per_sm = std::max(1, std::min(8, static_cast<int>((227 * 1024) / (p->smem + 1024))));
+  const int64_t tiles = (n + kSmThreads - 1) / kSmThreads;
+  p->grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, static_cast<int64_t>(sm_count()) * per_sm)));
+  return true;
+}
+
+__global__ void __launch_bounds__(kSmThreads)
+kmeans_small_kernel(const double* __restrict__ x, int64_t n, int d, int k,
+                    const double* __restrict__ mu, int32_t* __restrict__ assign,
+                    long long* __restrict__ part_counts, double* __restrict__ part_sums, int xstride) {
+  extern __shared__ __align__(16) unsigned char small_smem[];
+  Carve cv(small_smem);
+  double* mu_s = cv.take<double>(static_cast<size_t>(k) * d);
+  double* sums_s = cv.take<double>(static_cast<size_t>(k) * d);
+  double* xs = cv.take<double>(static_cast<size_t>(kSmThreads) * xstride);
+  long long* counts_s = cv.take<long long>(64);
+  int* asg_s = cv.take<int>(kSmThreads);
+  int* order_s = cv.take<int>(kSmThreads);
+  int* cnt_s = cv.take<int>(64);
+  int* off_s = cv.take<int>(64);
+  int* wcnt_s = cv.take<int>(4 * 64);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kd = k * d;
+  pdl_wait();   // mu comes from the previous iteration's update
+  pdl_trigger();
+  for (int e = tid; e < kd; e += kSmThreads) {
+    mu_s[e] = mu[e];
+    sums_s[e] = 0.0;
+  }
+  if (tid < 64) counts_s[tid] = 0;
+  const int tpc = kSmThreads / d;            // fold threads per column
+  const int fj = tid % d, fr = tid / d;      // fold cell column and centroid phase
+  const int64_t ntiles = (n + kSmThreads - 1) / kSmThreads;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t i0 = t * kSmThreads;
+    const int rows = static_cast<int>(n - i0 < kSmThreads ? n - i0 : kSmThreads);
+    __syncthreads();   // previous tile folded (and the init above is complete)
+    const double* xt = x + i0 * d;
+    for (int e = tid; e < rows * d; e += kSmThreads) {
+      const int r = e / d;
+      xs[r * xstride + (e - r * d)] = __ldg(xt + e);
+    }
+    if (tid < 64) cnt_s[tid] = 0;
+    for (int e = tid; e < 4 * 64; e += kSmThreads) wcnt_s[e] = 0;
+    __syncthreads();
+    // the reference chain: per centroid a sequential j-order sum of rounded squares (no FMA),
+    // then `if (dist < best)` over ascending c from (1e300, 0)
+    int a = -1;
+    if (tid < rows) {
+      const double* xr = xs + tid * xstride;
+      double best = 1e300;
+      int bi = 0;
+      for (int c0 = 0; c0 < k; c0 += 8) {
+        double acc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+        if (c0 + 8 <= k) {
+          for (int j = 0; j < d; ++j) {
+            const double xv = xr[j];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const double diff = __dsub_rn(xv, mu_s[(c0 + u) * d + j]);
+              acc[u] = __dadd_rn(acc[u], __dmul_rn(diff, diff));
+            }
+          }
+        } else {
+          for (int j = 0; j < d; ++j) {
+            const double xv = xr[j];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (c0 + u < k) {
+                const double diff = __dsub_rn(xv, mu_s[(c0 + u) * d + j]);
+                acc[u] = __dadd_rn(acc[u], __dmul_rn(diff, diff));
+              }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (c0 + u < k && acc[u] < best) {
+            best = acc[u];
+            bi = c0 + u;
+          }
+      }
+      a = bi;
+      asg_s[tid] = a;
+      if (assign) assign[i0 + tid] = a;
+    }
+    // stable counting sort of the tile by assignment: rank within the warp from __match_any,
+    // plus the same-centroid counts of the lower warps
+    const unsigned same = __match_any_sync(0xffffffffu, a);
+    const int wrank = __popc(same & ((1u << lane) - 1u));
+    if (a >= 0 && wrank == 0) wcnt_s[warp * 64 + a] = __popc(same);
+    __syncthreads();
+    if (tid < k) {
+      int tot = 0;
+      for (int w = 0; w < 4; ++w) tot += wcnt_s[w * 64 + tid];
+      cnt_s[tid] = tot;
+      counts_s[tid] += tot;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int off = 0;
+      for (int c = 0; c < k; ++c) {
+        off_s[c] = off;
+        off += cnt_s[c];
+      }
+    }
+    __syncthreads();
+    if (a >= 0) {
+      int r = wrank;
+      for (int w = 0; w < warp; ++w) r += wcnt_s[w * 64 + a];
+      order_s[off_s[a] + r] = tid;
+    }
+    __syncthreads();
+    // segmented fold: cell (c, j) gets its tile samples in ascending order from one owner
+    if (fr < tpc) {
+      for (int c = fr; c < k; c += tpc) {
+        const int lo = off_s[c], hi = lo + cnt_s[c];
+        if (lo == hi) continue;
+        double acc = sums_s[c * d + fj];
+        for (int q = lo; q < hi; ++q) acc += xs[order_s[q] * xstride + fj];
+        sums_s[c * d + fj] = acc;
+      }
+    }
+  }
+  __syncthreads();
+  double* ps = part_sums + static_cast<size_t>(blockIdx.x) * kd;
+  for (int e = tid; e < kd; e += kSmThreads) ps[e] = sums_s[e];
+  long long* pc = part_counts + static_cast<size_t>(blockIdx.x) * k;
+  for (int c = tid; c < k; c += kSmThreads) pc[c] = counts_s[c];
+}
+
 __global__ void kmeans_update_kernel(const long long* __restrict__ counts,
                                      const double* __restrict__ sums, int k, int d,
                                      double* __restrict__ mu) {
@@ -213,11 +375,43 @@ size_t kmeans_screened_workspace_bytes(int64_t n, int d, int k);
 
 static size_t direct_workspace_bytes(int64_t n, int d, int k) {
   KmeansPlan p;
-  if (!make_plan(n, d, k, &p)) return 0;
+  int grid = 0;
+  if (make_plan(n, d, k, &p)) grid = p.grid;
+  SmallPlan sp;
+  if (small_plan(n, d, k, &sp)) grid = std::max(grid, sp.grid);
+  if (grid == 0) return 0;
   Carve c(nullptr);
-  c.take<long long>(static_cast<size_t>(p.grid) * k);
-  c.take<double>(static_cast<size_t>(p.grid) * k * d);
+  c.take<long long>(static_cast<size_t>(grid) * k);
+  c.take<double>(static_cast<size_t>(grid) * k * d);
   return c.used + 256;
+}
+
+// AUTO's choice of the small direct kernel: a cheap fp64 chain (k*d <= 256 terms per sample).
+// Measured (scripts/kmeans_crossover.py, r90): d=16, k=8 it beats the screen at every N
+// (65,536: 27.9 vs 26.9 us eager; 1M: 71 vs 123 us; 4M: 0.25 vs 0.43 ms); at k*d = 512 or
+// 1,024 the latency-bound fp64 chains lose from N ~ 262K on (d=64, k=8, 4M: 1.77 vs 0.46 ms).
+static bool prefer_small(int64_t n, int d, int k) {
+  SmallPlan sp;
+  if (!small_plan(n, d, k, &sp)) return false;
+  return static_cast<int64_t>(k) * d <= 256;
+}
+
+static int kmeans_small_step(const double* x, int64_t n, int d, int k, const double* mu,
+                             int32_t* assign, long long* counts, double* sums, void* ws,
+                             size_t ws_bytes, cudaStream_t stream) {
+  SmallPlan p;
+  DLX_REQUIRE(small_plan(n, d, k, &p), DLX_ERR_GENERATION, "GenerationFailed: small k-means plan");
+  Carve c(ws);
+  long long* pc = c.take<long long>(static_cast<size_t>(p.grid) * k);
+  double* psum = c.take<double>(static_cast<size_t>(p.grid) * k * d);
+  DLX_REQUIRE(c.used <= ws_bytes, DLX_ERR_ARG, "k-means workspace too small (%zu < %zu)",
+              ws_bytes, c.used);
+  DLX_CUDA(cudaFuncSetAttribute(kmeans_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(p.smem)));
+  DLX_CUDA(launch_pdl(kmeans_small_kernel, dim3(p.grid), dim3(kSmThreads), p.smem, stream, x, n, d, k, mu,
+                      assign, pc, psum, p.xstride));
+  DLX_LAUNCHED("kmeans_small_kernel");
+  return kmeans_finalize(pc, psum, p.grid, k, d, counts, sums, stream);
 }
 
 static int kmeans_direct_step(const double* x, int64_t n, int d, int k, const double* mu,
@@ -262,11 +456,18 @@ int dlx_kmeans_step(const double* d_x, int64_t n, int32_t d, int32_t k, const do
     DLX_CUDA(cudaMemsetAsync(d_sums, 0, sizeof(double) * k * d, stream));
     return DLX_OK;
   }
+  if (method == DLX_KMEANS_AUTO && prefer_small(n, d, k))
+    return kmeans_small_step(d_x, n, d, k, d_mu, d_assign, counts, d_sums, d_workspace,
+                             workspace_bytes, stream);
   if (method == DLX_KMEANS_SCREENED || method == DLX_KMEANS_AUTO) {
     int rc = kmeans_screened_step(d_x, n, d, k, d_mu, d_assign, counts, d_sums, d_workspace,
                                   workspace_bytes, stream, false);
     if (rc != DLX_ERR_GENERATION || method == DLX_KMEANS_SCREENED) return rc;
   }
+  SmallPlan sp;
+  if (small_plan(n, d, k, &sp))
+    return kmeans_small_step(d_x, n, d, k, d_mu, d_assign, counts, d_sums, d_workspace,
+                             workspace_bytes, stream);
   return kmeans_direct_step(d_x, n, d, k, d_mu, d_assign, counts, d_sums, d_workspace,
                             workspace_bytes, stream);
 }

@@ -84,7 +84,8 @@ def test_kmeans_graph_equals_eager(ml):
 
 
 @pytest.mark.parametrize("n,d,k", [(1, 16, 8), (37, 5, 3), (1000, 64, 64), (5000, 33, 17), (3000, 130, 10),
-                                   (2048, 16, 1), (4099, 64, 64), (10_000, 2, 70), (777, 96, 24)])
+                                   (2048, 16, 1), (4099, 64, 64), (10_000, 2, 70), (777, 96, 24),
+                                   (1_000_003, 16, 8), (300_001, 64, 8), (200_000, 7, 64)])
 @pytest.mark.parametrize("method", [0, 1])
 def test_kmeans_shapes(ml, n, d, k, method):
     x = dev_units(ml, n, d, seed=n + d + k)
