@@ -21,7 +21,7 @@ for w in $WHAT; do
          timeout 1200 ncu --set full --clock-control none --import-source on -k regex:kmeans_screened -s 3 -c 1 -o $OUT/prof_kmeans \
            python bench.py --config c4 --steps 4 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_kmeans.log 2>&1 ;;
     tests) timeout 1800 python -m pytest tests -m gpu -q -rf --durations=15 > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log ;;
-    bench) for c in c4 c1 c2 l16 c3 c5; do
+    bench) for c in c4 c1 c2 l16 c3 c5 c5k65536 c4shard8; do
              timeout 600 python bench.py --config $c --steps 10 --warmup 3 > $OUT/bench_$c.json 2> $OUT/bench_$c.err
            done ;;
     benchref) timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_ref_c4.json 2> $OUT/bench_ref_c4.err ;;
@@ -30,7 +30,7 @@ for w in $WHAT; do
          timeout 1200 ncu --set full --clock-control none --import-source on -k regex:kmeans_screened -s 3 -c 1 -o $OUT/prof_kmeans \
            python bench.py --config c4 --steps 4 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_kmeans.log 2>&1
          for c in c5 l16 c3; do
-           timeout 900 ncu --set full --clock-control none --import-source on -k regex:"groupby_smem|logreg_grad|gda_pass2" -s 3 -c 1 -o $OUT/prof_$c \
+           timeout 900 ncu --set full --clock-control none --import-source on -k regex:"groupby_smem|logreg_grad|gda_pass2" -s 4 -c 1 -o $OUT/prof_$c \
              python bench.py --config $c --steps 4 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_$c.log 2>&1
          done ;;
   esac
