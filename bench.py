@@ -330,20 +330,12 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
         holder = {}
 
         def kernel_fn():
-            if comm is None:
-                holder["r"] = ml.gda_fit(x, y)   # one read of x (csrc/gda_dmma.cu)
-            else:
-                holder["r"] = ml.gda_pass1(x, y)
+            # one read of x (csrc/gda_dmma.cu single-pass fit); sharded: the ranks' fits pooled
+            # through the exchange (gda_combine_ranks_kernel)
+            holder["r"] = ml.gda(x, y, comm)
 
         def step():
             kernel_fn()
-            if comm is None:
-                return
-            n1, s0, s1 = holder["r"]
-            comm.allreduce_many_([n1, s0, s1])
-            mu0, mu1 = ml.gda_means(n1, s0, s1, n)
-            S = ml.gda_pass2(x, y, mu0, mu1)
-            comm.allreduce_(S)
     else:
         K = p["K"]
         keys = ml.rng_ints(n_local, K, seed=1, first_draw=lo, device=dev)
@@ -381,7 +373,7 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             if comm is not None:
                 comm.allreduce_(counts)
     if comm is None or isinstance(comm, PeerComm):
-        if family in ("kmeans", "logreg", "groupby") or (family == "gda" and comm is None):
+        if family in ("kmeans", "logreg", "groupby", "gda"):
             def cap(fn):
                 side = torch.cuda.Stream()
                 side.wait_stream(torch.cuda.current_stream())
@@ -408,21 +400,11 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             run_kernel()
             ev[s][1].record(stream)
             run_rest()   # remainder of the step (allreduce + update)
-        elif comm is None:
+        else:
             ev2[s][0].record(stream)
             run_kernel()   # the single-pass fit: DMMA scatter + class sums, combines, finalize
             ev2[s][1].record(stream)
             ev[s][1].record(stream)
-        else:
-            kernel_fn()
-            ev[s][1].record(stream)
-            n1, s0, s1 = holder["r"]
-            comm.allreduce_many_([n1, s0, s1])
-            mu0, mu1 = ml.gda_means(n1, s0, s1, n)
-            ev2[s][0].record(stream)
-            S = ml.gda_pass2(x, y, mu0, mu1)   # dominant kernel: the DMMA scatter
-            ev2[s][1].record(stream)
-            comm.allreduce_(S)
     t_end.record(stream)
     # this library's kernels in the timed region: counted at launch, or per captured graph
     # (the launches recorded while capturing) times its replays
@@ -491,8 +473,9 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             hb = algorithmic_bytes(family, p, n_local) / (pass2_ms * 1e-3) / 1e9
             result["roofline_hbm"] = {"bound": "hbm", "achieved": hb, "peak": peak, "unit": "GB/s",
                                       "frac": hb / peak, "kernel_ms": pass2_ms}
-            result["config"]["gda_path"] = "single-pass fit" if comm is None else "two passes + allreduce"
-            result["config"]["gda_fit_fallback"] = (ml.gda_fit_last_fallback(x) if comm is None else None)
+            result["config"]["gda_path"] = ("single-pass fit" if comm is None else
+                                            "single-pass fit per rank, pooled through the exchange")
+            result["config"]["gda_fit_fallback"] = ml.gda_fit_last_fallback(x)
             result["roofline"] = {"bound": "tensor", "achieved": flops / (pass2_ms * 1e-3) / 1e12,
                                   "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                                   "frac": flops / (pass2_ms * 1e-3) / 1e12 / DMMA_PEAK_TFLOPS,

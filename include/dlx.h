@@ -131,6 +131,12 @@ size_t dlx_gda_fit_workspace_bytes(int64_t n, int32_t d);
 int dlx_gda_fit(const double* d_x, const int64_t* d_y, int64_t n, int32_t d, int64_t* d_n1,
                 double* d_mu0, double* d_mu1, double* d_scatter, void* d_workspace,
                 size_t workspace_bytes, dlx_stream_t stream);
+/* Sharded fit: combine the ranks' dlx_gda_fit results.  d_table = world rows of
+ * (n0, n1, mu0[d], mu1[d]) as fp64, summed across ranks (rank r fills row r, zeros elsewhere);
+ * d_scatter = the sum of the ranks' S on input, the global S on output (pooled-scatter
+ * identity, between-rank term from mean differences); writes the global n1, mu0, mu1. */
+int dlx_gda_combine_ranks(const double* d_table, int32_t world, int32_t d, double* d_scatter,
+                          int64_t* d_n1, double* d_mu0, double* d_mu1, dlx_stream_t stream);
 /* 1 if the last dlx_gda_fit on this workspace took the exact-means fallback (synchronous). */
 int dlx_gda_fit_last_fallback(const void* d_workspace, int64_t n, int32_t d, int* h_fallback);
 int dlx_gda_pass2(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,

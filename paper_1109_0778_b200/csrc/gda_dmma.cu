@@ -436,9 +436,68 @@ int gda_fit(const double* x, const long long* y, int64_t n, int d, long long* n1
   return combine_f64_unless(parts, grid, static_cast<long long>(d) * d, S, ok, stream);
 }
 
+// Sharded fit: rank r's single-pass fit gives n_rc, mu_rc and S_r (its scatter around its own
+// class means).  With every rank's (n_rc, mu_rc) summed into a table (rank r fills row r, the
+// other rows are zero, so the sum is exact) and the S_r summed, the global result follows from
+// the pooled-scatter identity  S = sum_r S_r + sum_r sum_c n_rc (mu_rc - mu_c)(mu_rc - mu_c)^T,
+// mu_c = sum_r n_rc mu_rc / n_c — the between-rank term computed directly from the differences
+// (no cancellation), ranks folded in ascending order.  Ranks without class-c rows are skipped.
+__global__ void __launch_bounds__(1024)
+gda_combine_ranks_kernel(const double* __restrict__ table, int world, int d, double* __restrict__ S,
+                         long long* __restrict__ n1_out, double* __restrict__ mu0, double* __restrict__ mu1) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ double mu_s[];   // [2][d] global class means
+  const int w = 2 + 2 * d;
+  double n[2] = {0.0, 0.0};
+  for (int r = 0; r < world; ++r) {
+    n[0] += table[r * w];
+    n[1] += table[r * w + 1];
+  }
+  for (int e = threadIdx.x; e < 2 * d; e += blockDim.x) {
+    const int c = e / d, j = e % d;
+    double acc = 0.0;
+    for (int r = 0; r < world; ++r) {
+      const double nr = table[r * w + c];
+      if (nr > 0.0) acc += nr * table[r * w + 2 + c * d + j];
+    }
+    const double m = acc / n[c];   // an empty class: 0 / 0 -> NaN, as the reference
+    mu_s[e] = m;
+    (c ? mu1 : mu0)[j] = m;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
+    const int a = e / d, b = e % d;
+    double acc = S[e];
+    for (int r = 0; r < world; ++r)
+      for (int c = 0; c < 2; ++c) {
+        const double nr = table[r * w + c];
+        if (nr > 0.0) {
+          const double* mr = table + r * w + 2 + c * d;
+          acc += nr * ((mr[a] - mu_s[c * d + a]) * (mr[b] - mu_s[c * d + b]));
+        }
+      }
+    S[e] = acc;
+  }
+  if (threadIdx.x == 0) *n1_out = static_cast<long long>(n[1]);
+}
+
 }  // namespace dlx
 
 extern "C" {
+
+int dlx_gda_combine_ranks(const double* d_table, int32_t world, int32_t d, double* d_scatter,
+                          int64_t* d_n1, double* d_mu0, double* d_mu1, dlx_stream_t stream) {
+  DLX_REQUIRE(d_table && d_scatter && d_n1 && d_mu0 && d_mu1 && world >= 1 && d > 0 && d <= 4096,
+              DLX_ERR_ARG, "gda combine ranks: bad args");
+  const size_t smem = 2 * static_cast<size_t>(d) * sizeof(double);
+  DLX_CUDA(dlx::launch_pdl(dlx::gda_combine_ranks_kernel, dim3(1), dim3(1024), smem, static_cast<cudaStream_t>(stream),
+                      d_table, static_cast<int>(world), static_cast<int>(d), d_scatter,
+                      reinterpret_cast<long long*>(d_n1), d_mu0, d_mu1));
+  DLX_LAUNCHED("gda_combine_ranks_kernel");
+  return DLX_OK;
+}
+
 
 size_t dlx_gda_fit_workspace_bytes(int64_t n, int32_t d) { return dlx::gda_fit_workspace_bytes(n, d); }
 

@@ -245,8 +245,24 @@ def gda(x: torch.Tensor, y: torch.Tensor, comm=None):
     device-local fit reads x once (gda_fit); sharded fits run the two reference passes with
     the class sums and the scatter summed across ranks in between."""
     n_local, d = x.shape
-    if comm is None and d <= 64:
-        return gda_fit(x, y)
+    if d <= 64:
+        n1, mu0, mu1, S = gda_fit(x, y)
+        if comm is None:
+            return n1, mu0, mu1, S
+        # sharded: pool the ranks' fits (csrc/gda_dmma.cu, gda_combine_ranks_kernel)
+        L = _lib.load()
+        w = 2 + 2 * d
+        table = torch.zeros((comm.world, w), dtype=_F64, device=x.device)
+        row = table[comm.rank]
+        row[0:1].copy_(n_local - n1)
+        row[1:2].copy_(n1)
+        row[2:2 + d].copy_(mu0)
+        row[2 + d:].copy_(mu1)
+        comm.allreduce_(table.view(-1))
+        comm.allreduce_(S)
+        check(L.dlx_gda_combine_ranks(_ptr(table), comm.world, d, _ptr(S), _ptr(n1), _ptr(mu0), _ptr(mu1),
+                                      _stream()))
+        return n1, mu0, mu1, S
     n1, s0, s1 = gda_pass1(x, y)
     n_total = n_local
     if comm is not None:

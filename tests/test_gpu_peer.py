@@ -30,6 +30,7 @@ def _free_port():
 N_KM, D_KM, K_KM, IT_KM = 50_000, 64, 16, 4
 N_LR, D_LR, IT_LR = 30_000, 64, 3
 N_GB, K_GB = 200_001, 4096
+N_GD, D_GD = 50_001, 64
 
 
 def _worker(rank, world, port, q):
@@ -80,6 +81,12 @@ def _work(rank, world, port, q):
         comm.allreduce_(cnt)
         out["groupby"] = cnt.cpu().numpy()
         out["n"] = comm.allreduce_int(hi - lo)
+        # GDA: each rank's single-pass fit pooled through the exchange (gda_combine_ranks_kernel)
+        lo, hi = shard_range(N_GD, rank, world)
+        xg = ml.rng_units((hi - lo) * D_GD, seed=4, first_draw=lo * D_GD).view(hi - lo, D_GD)
+        yg = ml.rng_ints(hi - lo, 2, seed=4, first_draw=N_GD * D_GD + lo)
+        n1, mu0, mu1, S = ml.gda(xg, yg, comm)
+        out["gda"] = (int(n1.item()), mu0.cpu().numpy(), mu1.cpu().numpy(), S.cpu().numpy())
         torch.cuda.synchronize()
     finally:
         comm.close()
@@ -130,6 +137,17 @@ def test_peer_allreduce_world2_one_device():
     assert np.array_equal(r0["groupby"], O.groupby_count(keys, K_GB))
     assert np.array_equal(r1["groupby"], r0["groupby"])
     assert r0["n"] == r1["n"] == N_GB
+    xg = O.rng_units(4, 0, N_GD * D_GD).reshape(N_GD, D_GD)
+    yg = O.rng_ints(4, N_GD * D_GD, N_GD, 2)
+    n1, s0, s1 = O.gda_pass1(xg, yg, workers=O.threads(), chunks=4 * O.threads())
+    m0, m1 = s0 / float(N_GD - n1), s1 / float(n1)
+    Sr = O.gda_pass2(xg, yg, m0, m1, workers=O.threads(), chunks=4 * O.threads())
+    for r in (r0, r1):
+        assert r["gda"][0] == n1
+        np.testing.assert_allclose(r["gda"][1], m0, rtol=1e-9)
+        np.testing.assert_allclose(r["gda"][2], m1, rtol=1e-9)
+        np.testing.assert_allclose(r["gda"][3], Sr, rtol=1e-9, atol=1e-9 * np.abs(Sr).max())
+    assert np.array_equal(r0["gda"][3].view(np.int64), r1["gda"][3].view(np.int64))
 
 
 def test_peer_world1_epilogues_match_unfused():
