@@ -75,6 +75,24 @@ def _worker(rank, world, port, q):
     S = torch.from_numpy(O.gda_pass2(xg, yg, mu0, mu1))
     dist.all_reduce(S)
     out["gda"] = (n1, mu0, mu1, S.numpy())
+    # ---- GDA, single pass per rank pooled (the sharded dlx path: gda_combine_ranks_kernel) -----
+    nl1, ls0, ls1 = O.gda_pass1(xg, yg)
+    nloc = hi - lo
+    lm0, lm1 = ls0 / float(nloc - nl1), ls1 / float(nl1)
+    S_r = torch.from_numpy(O.gda_pass2(xg, yg, lm0, lm1))          # scatter around the rank's means
+    table = torch.zeros((world, 2 + 2 * dg), dtype=torch.float64)
+    table[rank] = torch.from_numpy(np.concatenate([[float(nloc - nl1), float(nl1)], lm0, lm1]))
+    dist.all_reduce(table)
+    dist.all_reduce(S_r)
+    t = table.numpy()
+    nc = t[:, :2].sum(axis=0)
+    mus = [sum(t[r, c] * t[r, 2 + c * dg:2 + (c + 1) * dg] for r in range(world)) / nc[c] for c in range(2)]
+    Sp = S_r.numpy().copy()
+    for r in range(world):
+        for c in range(2):
+            dv = t[r, 2 + c * dg:2 + (c + 1) * dg] - mus[c]
+            Sp += t[r, c] * np.outer(dv, dv)
+    out["gda_pooled"] = (int(nc[1]), mus[0], mus[1], Sp)
     if rank == 0:
         q.put(out)
     dist.barrier()
@@ -123,3 +141,8 @@ def test_world2_gloo_matches_single_process():
     assert out["gda"][0] == n1
     np.testing.assert_allclose(out["gda"][1], mu0, rtol=1e-12)
     np.testing.assert_allclose(out["gda"][3], S, rtol=1e-11)
+    # pooled-scatter identity (the sharded single-pass path) against the same references
+    assert out["gda_pooled"][0] == n1
+    np.testing.assert_allclose(out["gda_pooled"][1], mu0, rtol=1e-12)
+    np.testing.assert_allclose(out["gda_pooled"][2], mu1, rtol=1e-12)
+    np.testing.assert_allclose(out["gda_pooled"][3], S, rtol=1e-11)
