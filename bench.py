@@ -259,6 +259,10 @@ def cpu_baseline_generic(family, p):
     return {"value": 1.0 / t, "unit": unit, "cores": threads, "kind": "port", "sample": smp}
 
 
+def _reduce_dev(dist, dev):
+    return "cpu" if dist.get_backend() == "gloo" else dev
+
+
 def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
     import torch
 
@@ -267,13 +271,23 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
     from paper_1109_0778_b200.comm import Comm, PeerComm, shard_range
     from paper_1109_0778_b200.programs import KMeansProgram, LogRegProgram
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # DLX_BENCH_SHARED_DEVICE=1 (code-path check only, never a measurement): several ranks on one
+    # GPU, gloo for the plumbing and the peer exchange (CUDA IPC works within a device; NCCL
+    # refuses duplicate devices)
+    shared = os.environ.get("DLX_BENCH_SHARED_DEVICE") == "1"
+    if shared and world > 1 and args.comm != "peer":
+        raise SystemExit("DLX_BENCH_SHARED_DEVICE needs --comm peer")
+    local_dev = local_rank % torch.cuda.device_count() if shared else local_rank
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     dist = None
     comm = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         comm = PeerComm.from_torch_distributed() if args.comm == "peer" else Comm.from_torch_distributed()
     _lib.load()
 
@@ -353,7 +367,7 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
     torch.cuda.synchronize()
     barrier()
 
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(local_dev)
     sampler.start()
     time.sleep(0.3)
     torch.cuda.synchronize()
@@ -416,7 +430,7 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
     kern_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
     pass2_ms = sum(a.elapsed_time(b) for a, b in ev2) / args.steps if family == "gda" else 0.0
     if dist is not None:
-        t = torch.tensor([total_ms, kern_ms, pass2_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([total_ms, kern_ms, pass2_ms], dtype=torch.float64, device=_reduce_dev(dist, dev))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, kern_ms, pass2_ms = float(t[0]), float(t[1]), float(t[2])
     ms_per_step = total_ms / args.steps
@@ -558,7 +572,7 @@ def e2e_kmeans(args, p, n_local, lo, comm, dist, dev, iters_per_job=10):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     if dist is not None:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms], dtype=torch.float64, device=_reduce_dev(dist, dev))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t[0])
     it_s = jobs * iters_per_job / (ms * 1e-3)
@@ -609,7 +623,7 @@ def e2e_logreg(args, p, n_local, lo, comm, dist, dev, iters_per_job=20):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     if dist is not None:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms], dtype=torch.float64, device=_reduce_dev(dist, dev))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t[0])
     return {"value": jobs * iters_per_job / (ms * 1e-3), "unit": "it/s",
