@@ -29,6 +29,7 @@
 #include <json.hpp>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -219,16 +220,30 @@ static bool g_debug = false;  // DLX_PROGRAM_DEBUG=1: why a specialised family d
     if (g_debug) fprintf(stderr, "[dlx program] %s: %s\n", __func__, why); \
     return false;                                                        \
   } while (0)
+// Device vector.  Small vectors (<= kMirrorBytes: centroids, counts, sums, parameters) keep a
+// host mirror so the host statements that read or update them element by element
+// (VectorApply / VectorUpdate — e.g. the k*d `mu(c*d+j) = sum / count` updates of a staged
+// k-means iteration) cost one transfer per vector instead of one synchronous copy per element:
+// the mirror is loaded on the first host read, host writes mark a dirty range, and every device
+// launch first flushes dirty ranges (one copy each) and afterwards invalidates the mirrors.
+constexpr size_t kMirrorBytes = 64 << 10;
+bool g_no_mirror = false;   // DLX_PROGRAM_NO_MIRROR=1: per-element transfers (A/B timing only)
 struct DevVec {
   void* p = nullptr;
   int64_t n = 0;
   Ty elem = Ty::Double;
+  std::vector<unsigned char> host;
+  bool host_valid = false;
+  int64_t dirty_lo = INT64_MAX, dirty_hi = -1;   // [lo, hi) newer on the host than on the device
   ~DevVec() {
     if (p) cudaFree(p);
   }
   size_t esize() const { return elem == Ty::Bool ? 1 : 8; }
+  bool mirrored() const { return !g_no_mirror && static_cast<size_t>(n) * esize() <= kMirrorBytes; }
 };
 using VecP = std::shared_ptr<DevVec>;
+// vectors created during one run (for flush / invalidate around device launches)
+thread_local std::vector<std::weak_ptr<DevVec>>* g_vecs = nullptr;
 struct Cell;
 using CellP = std::shared_ptr<Cell>;
 struct Val {
@@ -250,6 +265,7 @@ VecP new_vec(int64_t n, Ty elem, cudaStream_t st, bool zero) {
   auto v = std::make_shared<DevVec>();
   v->n = n;
   v->elem = elem;
+  if (g_vecs) g_vecs->push_back(v);
   if (g_dry) return v;
   ckc(cudaMalloc(&v->p, std::max<size_t>(16, static_cast<size_t>(n) * v->esize())), "cudaMalloc");
   if (zero) ckc(cudaMemsetAsync(v->p, 0, static_cast<size_t>(n) * v->esize(), st), "cudaMemset");
@@ -357,6 +373,9 @@ class Executor {
   uint64_t draws_ = 0;
   cudaStream_t st_;
   std::unordered_map<int, Val> env_;
+ public:
+  std::vector<std::weak_ptr<DevVec>> vecs_;   // every vector of this run (g_vecs points here)
+ private:
 
   // symbolic state of the loop being lowered
   int loop_index_ = -1;
@@ -422,9 +441,56 @@ class Executor {
     gen_fail("don't know how to evaluate " + op);
   }
 
+  // ---- host mirrors of small vectors ------------------------------------------------------
+  void load_mirror(const VecP& v) {
+    if (v->host_valid) return;
+    v->host.resize(static_cast<size_t>(v->n) * v->esize());
+    if (!v->host.empty())
+      ckc(cudaMemcpyAsync(v->host.data(), v->p, v->host.size(), cudaMemcpyDeviceToHost, st_), "d2h");
+    ckc(cudaStreamSynchronize(st_), "sync");
+    v->host_valid = true;
+  }
+  void flush_mirrors() {   // before a device launch: host updates -> device, one copy per vector
+    bool any = false;
+    for (auto& w : vecs_)
+      if (auto v = w.lock())
+        if (v->dirty_hi > v->dirty_lo) {
+          const size_t es = v->esize();
+          ckc(cudaMemcpyAsync(static_cast<unsigned char*>(v->p) + v->dirty_lo * es, v->host.data() + v->dirty_lo * es,
+                              static_cast<size_t>(v->dirty_hi - v->dirty_lo) * es, cudaMemcpyHostToDevice, st_),
+              "h2d");
+          v->dirty_lo = INT64_MAX;
+          v->dirty_hi = -1;
+          any = true;
+        }
+    if (any) ckc(cudaStreamSynchronize(st_), "sync");   // the mirrors may change right after
+  }
+  void invalidate_mirrors() {   // after a device launch: any vector may have been written
+    size_t live = 0;
+    for (auto& w : vecs_)
+      if (auto v = w.lock()) {
+        v->host_valid = false;
+        vecs_[live++] = w;
+      }
+    vecs_.resize(live);
+  }
+
   Val vec_get(const VecP& v, int64_t i) {
     if (i < 0 || i >= v->n) trap("TrapIndexOutOfBounds: index " + std::to_string(i));
     if (g_dry) return v->elem == Ty::Double ? Val{0.5} : v->elem == Ty::Bool ? Val{false} : Val{int64_t{1}};
+    if (v->mirrored()) {
+      load_mirror(v);
+      const unsigned char* h = v->host.data() + static_cast<size_t>(i) * v->esize();
+      if (v->elem == Ty::Double) {
+        double x;
+        std::memcpy(&x, h, 8);
+        return Val{x};
+      }
+      if (v->elem == Ty::Bool) return Val{*h != 0};
+      int64_t x;
+      std::memcpy(&x, h, 8);
+      return Val{x};
+    }
     ckc(cudaStreamSynchronize(st_), "sync");
     if (v->elem == Ty::Double) {
       double x;
@@ -444,6 +510,22 @@ class Executor {
   void vec_set(const VecP& v, int64_t i, const Val& x) {
     if (i < 0 || i >= v->n) trap("TrapIndexOutOfBounds: store index " + std::to_string(i));
     if (g_dry) return;
+    if (v->mirrored()) {
+      load_mirror(v);
+      unsigned char* h = v->host.data() + static_cast<size_t>(i) * v->esize();
+      if (v->elem == Ty::Double) {
+        const double d = x.d();
+        std::memcpy(h, &d, 8);
+      } else if (v->elem == Ty::Bool) {
+        *h = x.b() ? 1 : 0;
+      } else {
+        const int64_t q = x.i();
+        std::memcpy(h, &q, 8);
+      }
+      v->dirty_lo = std::min(v->dirty_lo, i);
+      v->dirty_hi = std::max(v->dirty_hi, i + 1);
+      return;
+    }
     if (v->elem == Ty::Double) {
       const double d = x.d();
       ckc(cudaMemcpyAsync(static_cast<double*>(v->p) + i, &d, 8, cudaMemcpyHostToDevice, st_), "h2d");
@@ -1190,6 +1272,13 @@ class Executor {
 
   // ---- one root ParallelLoop -------------------------------------------------------------------
   Val run_loop(const Stmt& s) {
+    if (!g_dry) flush_mirrors();
+    Val r = run_loop_impl(s);
+    if (!g_dry) invalidate_mirrors();
+    return r;
+  }
+
+  Val run_loop_impl(const Stmt& s) {
     const Loop& L = *s.loop;
     const int64_t n = atom(L.range).i();
     dry_n_ = n;
@@ -1234,10 +1323,36 @@ class Executor {
 
 }  // namespace
 
+// Parsed descriptors by content: a caller that runs the same staged program again (an
+// iteration driver, a benchmark, a server) skips the JSON parse, which dominates the host time
+// of large programs (a k = 8, d = 16 k-means iteration is ~1 MB of descriptor).
+std::shared_ptr<const Program> cached_program(const std::string& text) {
+  static std::mutex mu;
+  static std::unordered_map<std::string, std::shared_ptr<const Program>> cache;
+  static std::vector<std::string> order;   // FIFO eviction, a handful of programs
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(text);
+    if (it != cache.end()) return it->second;
+  }
+  auto p = std::make_shared<const Program>(parse_program(text));
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.emplace(text, p).second) {
+    order.push_back(text);
+    if (order.size() > 8) {
+      cache.erase(order.front());
+      order.erase(order.begin());
+    }
+  }
+  return p;
+}
+
 RunResult run_program(const std::string& program_json, uint64_t seed, int device) {
   g_dry = getenv("DLX_PROGRAM_DRYRUN") != nullptr;
   g_debug = getenv("DLX_PROGRAM_DEBUG") != nullptr;
-  Program p = parse_program(program_json);
+  g_no_mirror = getenv("DLX_PROGRAM_NO_MIRROR") != nullptr;
+  const std::shared_ptr<const Program> pp = cached_program(program_json);
+  const Program& p = *pp;
   cudaStream_t st = nullptr;
   if (!g_dry) {
     cudaError_t e = cudaSetDevice(device);
@@ -1248,6 +1363,10 @@ RunResult run_program(const std::string& program_json, uint64_t seed, int device
   RunResult r;
   try {
     Executor ex(p, seed, st);
+    struct VecRegistry {   // route new_vec registrations to this run's executor
+      explicit VecRegistry(std::vector<std::weak_ptr<DevVec>>* r) { g_vecs = r; }
+      ~VecRegistry() { g_vecs = nullptr; }
+    } reg(&ex.vecs_);
     Val v = ex.run();
     if (!g_dry) cudaStreamSynchronize(st);
     r.output = ex.output;
