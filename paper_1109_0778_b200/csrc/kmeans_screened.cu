@@ -592,6 +592,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     const int4* nm4 = reinterpret_cast<const int4*>(S.nm0);
     const uint32_t oh_row = (static_cast<uint32_t>(q) >> 3) * 512u + (q & 7) * 64u;
     const uint32_t oh_sw = (q & 7) >> 1;
+    int oh_prev0 = -1, oh_prev1 = -1;   // chunk of this row's bit in each one-hot buffer's previous tile
     for (int m = 0; m < mtiles; ++m) {
       const int64_t t = blockIdx.x + static_cast<int64_t>(m) * gridDim.x;
       const int b = m & 1;
@@ -666,6 +667,33 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       if (quarter == 0 && lane == 0) TRACE_EV(m, 15);
       {
         unsigned char* ohb = smem + kOffOH + b * kOHBuf + oh_row;
+#ifndef DLX_KMEANS_OH_FULL
+        // only the 16-byte chunk that holds this row's bit now, and the one that held it in this
+        // buffer's previous tile, change: after the first use of each buffer (all four chunks)
+        // a row costs at most two stores
+        const int nc = hot >= 0 ? (hot >> 4) : -1;
+        const int pc = m >= 2 ? (b ? oh_prev1 : oh_prev0) : -2;
+        if (b) oh_prev1 = nc;
+        else oh_prev0 = nc;
+        uint4 w = make_uint4(0u, 0u, 0u, 0u);
+        if (nc >= 0) {
+          const int rel = hot & 15;
+          const uint32_t bit = 1u << (8 * (rel & 3));
+          const int wi = rel >> 2;
+          w.x = wi == 0 ? bit : 0u;
+          w.y = wi == 1 ? bit : 0u;
+          w.z = wi == 2 ? bit : 0u;
+          w.w = wi == 3 ? bit : 0u;
+        }
+        if (pc == -2) {
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch)
+            *reinterpret_cast<uint4*>(ohb + ((ch ^ oh_sw) << 4)) = ch == nc ? w : make_uint4(0u, 0u, 0u, 0u);
+        } else {
+          if (pc >= 0 && pc != nc) *reinterpret_cast<uint4*>(ohb + ((pc ^ oh_sw) << 4)) = make_uint4(0u, 0u, 0u, 0u);
+          if (nc >= 0) *reinterpret_cast<uint4*>(ohb + ((nc ^ oh_sw) << 4)) = w;
+        }
+#else
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
           uint4 w = make_uint4(0u, 0u, 0u, 0u);
@@ -680,6 +708,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
           }
           *reinterpret_cast<uint4*>(ohb + ((ch ^ oh_sw) << 4)) = w;
         }
+#endif
       }
       fence_proxy_async_smem();
       __syncwarp();
