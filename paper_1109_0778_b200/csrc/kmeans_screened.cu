@@ -717,7 +717,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       // hand the decision to the tail warp
       if (m >= 2) mbar_wait(&S.dec_empty[b], ((m >> 1) - 1) & 1);
       S.dec_a[b][q] = hot;
-      S.dec_mask[b][q] = full;
+      if (hot == -1) S.dec_mask[b][q] = full;   // read by the tail for pending rows only
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.dec_full[b]);
     }
