@@ -91,6 +91,10 @@ constexpr int kConvRows = kTile / kNumC;
 constexpr int kPairs = kConvRows / 2;                      // row pairs per converter warp per tile
 constexpr int kBuf = kNumC == 8 ? kPairs : 4;             // rolling register buffer (pairs)
 constexpr int kNumA = 3;     // plane buffers in flight
+#ifndef DLX_KMEANS_L2_AHEAD
+#define DLX_KMEANS_L2_AHEAD 3
+#endif
+constexpr int kL2Ahead = DLX_KMEANS_L2_AHEAD;   // converters' L2 prefetch distance (tiles; 0 = off)
 // warpgroup 0: warp 0 screen MMAs, warp 1 fold MMAs, warp 2 tail (warp 3 idle); warpgroup 1:
 // epilogue; then the converter warpgroups.  Registers are rebalanced with setmaxnreg after the
 // prologue: warpgroup 0 drops to 32, the epilogue runs at 128, converters take the rest.
@@ -499,6 +503,15 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       const int b = m % kNumA;
       int64_t nxt_rows = 0;
       const double* nxt = base_of(m + 1 < mtiles ? m + 1 : m, nxt_rows);
+#if DLX_KMEANS_L2_AHEAD > 0
+      // this warp's rows of tile m + kL2Ahead (contiguous) into L2 ahead of the register loads
+      // (issued one tile ahead): those then wait on L2 rather than on HBM latency under load
+      if (lane == 0 && m + kL2Ahead < mtiles) {
+        const TileRows tp = tile_rows<kShift>(tile_of(m + kL2Ahead), n);
+        const int64_t r0 = tp.row0 + kConvRows * cw;
+        if (r0 + kConvRows <= n) bulk_prefetch_l2(x + r0 * D, static_cast<uint32_t>(kConvRows * D * 8));
+      }
+#endif
       if (cw == 0 && lane == 0) TRACE_EV(m, 2);
       if (m >= kNumA) mbar_wait(&S.a_empty[b], ((m / kNumA) - 1) & 1);
       if (cw == 0 && lane == 0) TRACE_EV(m, 3);
