@@ -347,7 +347,10 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsIssuer));
   if (warp == kWarpMma) {
     // ======================= screen MMA issuer =======================
-    if (lane == 0) {
+    // the whole warp runs the loop and waits (a converged warp sleeping in try_wait); lane 0
+    // issues.  A lane-0-only loop left 31 lanes diverged at the exit barrier, and the issuer's
+    // SMSP then ran its converters ~1K cycles per tile behind the idle-warp SMSP (trace r121-r123).
+    {
       // all operands unsigned: sample planes h'' = b7, l = b6, F = b5; centroid rows h'', l', G
       constexpr uint32_t ID_64 = idesc_i8(kTile, 64, 0, 0), ID_128 = idesc_i8(kTile, 128, 0, 0);
       constexpr uint32_t ID_192 = idesc_i8(kTile, 192, 0, 0);
@@ -360,6 +363,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         TRACE_EV(ns, 9);
         tc_fence_after();
         const uint32_t a0 = smem_addr(smem + kOffA + (ns % kNumA) * kABuf);
+        if (lane == 0) {
         for (int kk = 0; kk < nk; ++kk) {
           const uint64_t xh = sw128_kmajor_desc(a0 + 32 * kk);             // b7 = h''
           const uint64_t xl = sw128_kmajor_desc(a0 + 64 + 32 * kk);        // b6 = l
@@ -375,11 +379,13 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         }
         mma_commit(&S.t_full);
         TRACE_EV(ns, 0);
+        }
+        __syncwarp();
       }
     }
   } else if (warp == kWarpFold) {
     // ======================= fold MMA issuer =======================
-    if (lane == 0) {
+    {   // converged warp, lane 0 issues (as the screen issuer)
       constexpr uint32_t ID_fold = idesc_i8_major(kTile, 64, 0, 0, 1, 1);
       for (int nf = 0; nf < mtiles; ++nf) {
         mbar_wait(&S.oh_full[nf & 1], (nf >> 1) & 1);
@@ -387,6 +393,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         tc_fence_after();
         const uint32_t a0 = smem_addr(smem + kOffA + (nf % kNumA) * kABuf);
         const uint32_t oh = smem_addr(smem + kOffOH + (nf & 1) * kOHBuf);
+        if (lane == 0) {
 #pragma unroll
         for (int kk = 0; kk < kTile / 32; ++kk) {
           const uint64_t bdesc = sw64_kmajor_desc(oh + kk * 2048);   // MN-major [q][c], SW64
@@ -399,8 +406,11 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         mma_commit(&S.a_empty[nf % kNumA]);
         mma_commit(&S.oh_empty[nf & 1]);
         TRACE_EV(nf, 1);
+        }
+        __syncwarp();
       }
-      mma_commit(&S.fold_done);
+      if (lane == 0) mma_commit(&S.fold_done);
+      __syncwarp();
     }
   } else if (warp == kWarpTail) {
     // ======================= tail: assignments, counts, pending list =======================
