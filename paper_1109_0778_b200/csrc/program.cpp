@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <cstring>
 #include <json.hpp>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -228,15 +229,23 @@ static bool g_debug = false;  // DLX_PROGRAM_DEBUG=1: why a specialised family d
 // launch first flushes dirty ranges (one copy each) and afterwards invalidates the mirrors.
 constexpr size_t kMirrorBytes = 64 << 10;
 bool g_no_mirror = false;   // DLX_PROGRAM_NO_MIRROR=1: per-element transfers (A/B timing only)
+bool g_serial = false;      // DLX_PROGRAM_SERIAL=1: complete every loop before the next statement
+// The run's main stream (host statements, RNG fills, mirror flushes, frees) and the fence that
+// orders the main stream after every in-flight loop before device memory is freed or rewritten.
+thread_local cudaStream_t g_main_st = nullptr;
+thread_local std::function<void()>* g_fence = nullptr;
 struct DevVec {
   void* p = nullptr;
   int64_t n = 0;
   Ty elem = Ty::Double;
+  cudaStream_t fst = nullptr;   // stream the buffer is freed on (stream-ordered allocator)
   std::vector<unsigned char> host;
   bool host_valid = false;
   int64_t dirty_lo = INT64_MAX, dirty_hi = -1;   // [lo, hi) newer on the host than on the device
   ~DevVec() {
-    if (p) cudaFree(p);
+    if (!p) return;
+    if (g_fence) (*g_fence)();   // a loop still in flight may read this buffer
+    cudaFreeAsync(p, fst);
   }
   size_t esize() const { return elem == Ty::Bool ? 1 : 8; }
   bool mirrored() const { return !g_no_mirror && static_cast<size_t>(n) * esize() <= kMirrorBytes; }
@@ -267,7 +276,8 @@ VecP new_vec(int64_t n, Ty elem, cudaStream_t st, bool zero) {
   v->elem = elem;
   if (g_vecs) g_vecs->push_back(v);
   if (g_dry) return v;
-  ckc(cudaMalloc(&v->p, std::max<size_t>(16, static_cast<size_t>(n) * v->esize())), "cudaMalloc");
+  v->fst = g_main_st;
+  ckc(cudaMallocAsync(&v->p, std::max<size_t>(16, static_cast<size_t>(n) * v->esize()), st), "cudaMallocAsync");
   if (zero) ckc(cudaMemsetAsync(v->p, 0, static_cast<size_t>(n) * v->esize(), st), "cudaMemset");
   return v;
 }
@@ -357,22 +367,146 @@ std::optional<Affine> affine(const SEP& s) {
   return std::nullopt;
 }
 
+// ---- per-thread, per-device execution resources (kept across runs) ------------------------------
+// Loop streams: independent root loops (no data edge between them in the DEG, i.e. neither
+// reads a value the other binds) are launched on different streams and their completions are
+// deferred, so the kernels overlap each other and the host statements that follow
+// (scheduleDEG's concurrent independent kernels).  Results come back through a
+// pinned staging arena so the device->host copies stay asynchronous.
+constexpr int kLoopStreams = 4;
+struct PinnedArena {
+  std::vector<std::pair<unsigned char*, size_t>> blocks;   // the last block is the current one
+  size_t used = 0;
+  void* get(size_t bytes) {
+    bytes = (std::max<size_t>(bytes, 1) + 63) & ~size_t{63};
+    if (blocks.empty() || used + bytes > blocks.back().second) {
+      const size_t sz = std::max<size_t>(bytes, 1 << 20);
+      void* h = nullptr;
+      ckc(cudaMallocHost(&h, sz), "cudaMallocHost");
+      blocks.emplace_back(static_cast<unsigned char*>(h), sz);
+      used = 0;
+    }
+    void* r = blocks.back().first + used;
+    used += bytes;
+    return r;
+  }
+  template <class T>
+  T* get_n(size_t n) { return static_cast<T*>(get(n * sizeof(T))); }
+  void reset() {   // nothing in flight: keep one block, as large as the run needed
+    if (blocks.size() > 1) {
+      size_t total = 0;
+      for (auto& b : blocks) {
+        total += b.second;
+        cudaFreeHost(b.first);
+      }
+      blocks.clear();
+      void* h = nullptr;
+      if (cudaMallocHost(&h, total) == cudaSuccess) blocks.emplace_back(static_cast<unsigned char*>(h), total);
+    }
+    used = 0;
+  }
+};
+struct DeviceRes {
+  cudaStream_t loop[kLoopStreams] = {};
+  std::vector<cudaEvent_t> events;   // free list
+  PinnedArena pin;
+  bool init = false;
+};
+DeviceRes& device_res(int device) {
+  thread_local std::map<int, DeviceRes> res;   // never torn down (process-lifetime streams)
+  DeviceRes& r = res[device];
+  if (!r.init) {
+    for (auto& s : r.loop) ckc(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    cudaMemPool_t pool;   // keep freed blocks of the stream-ordered allocator for the next loops
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = 256ull << 20;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    r.init = true;
+  }
+  return r;
+}
+
 // ---- the executor -------------------------------------------------------------------------------
 class Executor {
  public:
-  Executor(const Program& p, uint64_t seed, cudaStream_t st) : P(p), seed_(seed), st_(st) {}
+  Executor(const Program& p, uint64_t seed, cudaStream_t st, DeviceRes* res)
+      : P(p), seed_(seed), st_(st), res_(res), lst_(st) {
+    fence_ = [this] { fence(); };
+  }
 
   std::string output;
   json report = json::array();
 
-  Val run() { return exec_block(P.root); }
+  Val run() {
+    Val v = exec_block(P.root);
+    join_all();
+    return v;
+  }
+  std::function<void()> fence_;   // g_fence points here during the run
 
  private:
   const Program& P;
   uint64_t seed_;
   uint64_t draws_ = 0;
   cudaStream_t st_;
+  DeviceRes* res_;
+  cudaStream_t lst_;   // stream of the loop being launched
+  int64_t launches_ = 0;
   std::unordered_map<int, Val> env_;
+
+  // ---- deferred loop completion (DEG overlap) -----------------------------------------------
+  struct Pending {
+    cudaEvent_t ev;                 // recorded on the loop's stream after its result copies
+    std::function<void()> finish;   // binds the loop's outputs (and raises its traps)
+  };
+  std::vector<Pending> pending_;   // launch (= program) order
+  cudaEvent_t get_event() {
+    if (res_->events.empty()) {
+      cudaEvent_t e;
+      ckc(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+      return e;
+    }
+    cudaEvent_t e = res_->events.back();
+    res_->events.pop_back();
+    return e;
+  }
+  // The loop just enqueued on lst_ binds `outs` when it completes.  Until then the symbols are
+  // unbound, so the first statement that reads one of them joins (a data edge of the DEG).
+  void defer(const std::vector<int>& outs, std::function<void()> fn) {
+    for (int o : outs) env_.erase(o);
+    cudaEvent_t ev = get_event();
+    ckc(cudaEventRecord(ev, lst_), "cudaEventRecord");
+    pending_.push_back(Pending{ev, std::move(fn)});
+    if (g_serial) join_all();
+  }
+  // Device-side ordering only: later main-stream work (frees, host->device rewrites of vectors
+  // a pending loop may read: the DEG's anti-dependences) waits for every loop in flight.
+  void fence() {
+    for (const Pending& p : pending_) cudaStreamWaitEvent(st_, p.ev, 0);
+  }
+  void join_all() {
+    if (pending_.empty()) return;
+    std::vector<Pending> pend;
+    pend.swap(pending_);
+    cudaError_t err = cudaSuccess;
+    for (const Pending& p : pend) {
+      cudaError_t e = cudaEventSynchronize(p.ev);
+      if (err == cudaSuccess) err = e;
+      res_->events.push_back(p.ev);
+    }
+    ckc(err, "loop completion");
+    for (Pending& p : pend) p.finish();   // program order: the first loop's trap wins
+    res_->pin.reset();
+  }
+  void* dalloc(size_t bytes) {
+    void* p = nullptr;
+    ckc(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), lst_), "cudaMallocAsync");
+    return p;
+  }
+  void dfree(void* p) {
+    if (p) cudaFreeAsync(p, lst_);
+  }
  public:
   std::vector<std::weak_ptr<DevVec>> vecs_;   // every vector of this run (g_vecs points here)
  private:
@@ -387,6 +521,10 @@ class Executor {
     switch (a.k) {
       case Atom::Sym: {
         auto it = env_.find(a.sym);
+        if (it == env_.end() && !pending_.empty()) {
+          join_all();
+          it = env_.find(a.sym);
+        }
         if (it == env_.end()) gen_fail("x" + std::to_string(a.sym) + " referenced before definition");
         return it->second;
       }
@@ -402,10 +540,15 @@ class Executor {
     const Block& bl = P.blocks.at(b);
     for (int s : bl.stmts) {
       const Stmt& st = P.stmts.at(s);
-      if (st.op == "ParallelLoop") {
-        run_loop(st);  // binds every live elem's `out` (elems[0].out is the statement's own sym)
-      } else {
-        env_[s] = exec_stmt(st);
+      try {
+        if (st.op == "ParallelLoop") {
+          run_loop(st);  // binds every live elem's `out` (elems[0].out is the statement's own sym)
+        } else {
+          env_[s] = exec_stmt(st);
+        }
+      } catch (...) {
+        join_all();   // a trap of an earlier loop still in flight takes precedence
+        throw;
       }
     }
     return atom(bl.result);
@@ -455,6 +598,7 @@ class Executor {
     for (auto& w : vecs_)
       if (auto v = w.lock())
         if (v->dirty_hi > v->dirty_lo) {
+          if (!any) fence();   // WAR: a loop in flight may still read the old contents
           const size_t es = v->esize();
           ckc(cudaMemcpyAsync(static_cast<unsigned char*>(v->p) + v->dirty_lo * es, v->host.data() + v->dirty_lo * es,
                               static_cast<size_t>(v->dirty_hi - v->dirty_lo) * es, cudaMemcpyHostToDevice, st_),
@@ -526,6 +670,7 @@ class Executor {
       v->dirty_hi = std::max(v->dirty_hi, i + 1);
       return;
     }
+    fence();
     if (v->elem == Ty::Double) {
       const double d = x.d();
       ckc(cudaMemcpyAsync(static_cast<double*>(v->p) + i, &d, 8, cudaMemcpyHostToDevice, st_), "h2d");
@@ -624,6 +769,10 @@ class Executor {
         auto it = sym_.find(a.sym);
         if (it != sym_.end()) return it->second;
         auto e = env_.find(a.sym);
+        if (e == env_.end() && !pending_.empty()) {
+          join_all();
+          e = env_.find(a.sym);
+        }
         if (e == env_.end()) gen_fail("loop body reads x" + std::to_string(a.sym) + " before definition");
         const Val& v = e->second;
         if (v.is_vec()) {
@@ -864,37 +1013,37 @@ class Executor {
     rep["k"] = k;
     rep["launch"] = "dlx_kmeans_step";
     if (g_dry) return dry_bind(els), true;
-    void* ws = nullptr;
     const size_t wsb = dlx_kmeans_workspace_bytes(n, d, k);
-    ckc(cudaMalloc(&ws, wsb), "cudaMalloc ws");
-    int32_t* a32 = nullptr;
-    int64_t* counts = nullptr;
-    double* sums = nullptr;
-    ckc(cudaMalloc(&a32, std::max<int64_t>(1, n) * 4), "cudaMalloc");
-    ckc(cudaMalloc(&counts, k * 8), "cudaMalloc");
-    ckc(cudaMalloc(&sums, static_cast<size_t>(k) * d * 8), "cudaMalloc");
+    void* ws = dalloc(wsb);
+    auto* a32 = static_cast<int32_t*>(dalloc(std::max<int64_t>(1, n) * 4));
+    auto* counts = static_cast<int64_t*>(dalloc(k * 8));
+    auto* sums = static_cast<double*>(dalloc(static_cast<size_t>(k) * d * 8));
     int rc = dlx_kmeans_step(static_cast<const double*>(ks.x->p), n, d, k, static_cast<const double*>(ks.mu->p),
-                             a32, counts, sums, ws, wsb, DLX_KMEANS_AUTO, st_);
-    VecP assign = new_vec(n, Ty::Int, st_, false);
-    if (rc == DLX_OK) rc = dlx_widen_i32_i64(a32, n, static_cast<int64_t*>(assign->p), st_);
-    std::vector<int64_t> hc(k);
-    std::vector<double> hs(static_cast<size_t>(k) * d);
+                             a32, counts, sums, ws, wsb, DLX_KMEANS_AUTO, lst_);
+    VecP assign = new_vec(n, Ty::Int, lst_, false);
+    if (rc == DLX_OK) rc = dlx_widen_i32_i64(a32, n, static_cast<int64_t*>(assign->p), lst_);
+    int64_t* hc = res_->pin.get_n<int64_t>(k);
+    double* hs = res_->pin.get_n<double>(static_cast<size_t>(k) * d);
     if (rc == DLX_OK) {
-      cudaMemcpyAsync(hc.data(), counts, k * 8, cudaMemcpyDeviceToHost, st_);
-      cudaMemcpyAsync(hs.data(), sums, hs.size() * 8, cudaMemcpyDeviceToHost, st_);
-      ckc(cudaStreamSynchronize(st_), "sync");
+      cudaMemcpyAsync(hc, counts, k * 8, cudaMemcpyDeviceToHost, lst_);
+      cudaMemcpyAsync(hs, sums, static_cast<size_t>(k) * d * 8, cudaMemcpyDeviceToHost, lst_);
     }
-    cudaFree(ws);
-    cudaFree(a32);
-    cudaFree(counts);
-    cudaFree(sums);
+    dfree(ws);
+    dfree(a32);
+    dfree(counts);
+    dfree(sums);
     ck(rc);
-    env_[els[ci].e->out] = Val{assign};
+    std::vector<int> outs;
+    std::vector<std::pair<int, int64_t>> bind;   // out sym -> index into counts (< 0: sums[~i])
     for (size_t q = 0; q < els.size(); ++q) {
+      outs.push_back(els[q].e->out);
       if (static_cast<int>(q) == ci) continue;
-      if (slots[q].kind == 0) env_[els[q].e->out] = Val{hc[slots[q].c]};
-      else env_[els[q].e->out] = Val{hs[slots[q].c * d + slots[q].j]};
+      bind.emplace_back(els[q].e->out, slots[q].kind == 0 ? slots[q].c : ~(slots[q].c * d + slots[q].j));
     }
+    defer(outs, [this, aout = els[ci].e->out, assign, hc, hs, bind = std::move(bind)] {
+      env_[aout] = Val{assign};
+      for (auto [o, ix] : bind) env_[o] = ix >= 0 ? Val{hc[ix]} : Val{hs[~ix]};
+    });
     rep["family"] = "kmeans";
     rep["n"] = n;
     rep["d"] = d;
@@ -933,21 +1082,20 @@ class Executor {
     rep["buckets"] = nb;
     rep["launch"] = "dlx_groupby_count";
     if (g_dry) return dry_bind(els), true;
-    void* ws = nullptr;
-    int64_t* counts = nullptr;
     const size_t wsb = dlx_groupby_workspace_bytes(n, nb);
-    ckc(cudaMalloc(&ws, wsb), "cudaMalloc");
-    ckc(cudaMalloc(&counts, nb * 8), "cudaMalloc");
-    int rc = dlx_groupby_count(static_cast<const int64_t*>(keys->p), n, nb, counts, ws, wsb, st_);
-    std::vector<int64_t> hc(nb);
-    if (rc == DLX_OK) {
-      cudaMemcpyAsync(hc.data(), counts, nb * 8, cudaMemcpyDeviceToHost, st_);
-      ckc(cudaStreamSynchronize(st_), "sync");
-    }
-    cudaFree(ws);
-    cudaFree(counts);
+    void* ws = dalloc(wsb);
+    auto* counts = static_cast<int64_t*>(dalloc(nb * 8));
+    int rc = dlx_groupby_count(static_cast<const int64_t*>(keys->p), n, nb, counts, ws, wsb, lst_);
+    int64_t* hc = res_->pin.get_n<int64_t>(nb);
+    if (rc == DLX_OK) cudaMemcpyAsync(hc, counts, nb * 8, cudaMemcpyDeviceToHost, lst_);
+    dfree(ws);
+    dfree(counts);
     ck(rc);
-    for (size_t q = 0; q < els.size(); ++q) env_[els[q].e->out] = Val{hc[bucket[q]]};
+    std::vector<int> outs;
+    for (size_t q = 0; q < els.size(); ++q) outs.push_back(els[q].e->out);
+    defer(outs, [this, outs, hc, bucket] {
+      for (size_t q = 0; q < outs.size(); ++q) env_[outs[q]] = Val{hc[bucket[q]]};
+    });
     rep["family"] = "groupby";
     rep["n"] = n;
     rep["buckets"] = nb;
@@ -1023,28 +1171,34 @@ class Executor {
     rep["d"] = d;
     rep["launch"] = "dlx_gda_pass2";
     if (g_dry) return dry_bind(els), true;
-    double *dm0 = nullptr, *dm1 = nullptr, *S = nullptr;
-    void* ws = nullptr;
     const size_t wsb = dlx_gda_workspace_bytes(n, static_cast<int32_t>(d));
-    ckc(cudaMalloc(&dm0, d * 8), "cudaMalloc");
-    ckc(cudaMalloc(&dm1, d * 8), "cudaMalloc");
-    ckc(cudaMalloc(&S, d * d * 8), "cudaMalloc");
-    ckc(cudaMalloc(&ws, wsb), "cudaMalloc");
-    cudaMemcpyAsync(dm0, mu0.data(), d * 8, cudaMemcpyHostToDevice, st_);
-    cudaMemcpyAsync(dm1, mu1.data(), d * 8, cudaMemcpyHostToDevice, st_);
+    auto* dm0 = static_cast<double*>(dalloc(d * 8));
+    auto* dm1 = static_cast<double*>(dalloc(d * 8));
+    auto* S = static_cast<double*>(dalloc(d * d * 8));
+    void* ws = dalloc(wsb);
+    double* hmu = res_->pin.get_n<double>(2 * d);   // pinned: the copies stay asynchronous
+    std::memcpy(hmu, mu0.data(), d * 8);
+    std::memcpy(hmu + d, mu1.data(), d * 8);
+    cudaMemcpyAsync(dm0, hmu, d * 8, cudaMemcpyHostToDevice, lst_);
+    cudaMemcpyAsync(dm1, hmu + d, d * 8, cudaMemcpyHostToDevice, lst_);
     int rc = dlx_gda_pass2(static_cast<const double*>(X->p), static_cast<const int64_t*>(Y->p), n,
-                           static_cast<int32_t>(d), dm0, dm1, S, ws, wsb, st_);
-    std::vector<double> hS(d * d);
-    if (rc == DLX_OK) {
-      cudaMemcpyAsync(hS.data(), S, hS.size() * 8, cudaMemcpyDeviceToHost, st_);
-      ckc(cudaStreamSynchronize(st_), "sync");
-    }
-    cudaFree(dm0);
-    cudaFree(dm1);
-    cudaFree(S);
-    cudaFree(ws);
+                           static_cast<int32_t>(d), dm0, dm1, S, ws, wsb, lst_);
+    double* hS = res_->pin.get_n<double>(d * d);
+    if (rc == DLX_OK) cudaMemcpyAsync(hS, S, d * d * 8, cudaMemcpyDeviceToHost, lst_);
+    dfree(dm0);
+    dfree(dm1);
+    dfree(S);
+    dfree(ws);
     ck(rc);
-    for (size_t q = 0; q < els.size(); ++q) env_[els[q].e->out] = Val{hS[cell[q].first * d + cell[q].second]};
+    std::vector<int> outs;
+    std::vector<int64_t> ix;
+    for (size_t q = 0; q < els.size(); ++q) {
+      outs.push_back(els[q].e->out);
+      ix.push_back(cell[q].first * d + cell[q].second);
+    }
+    defer(outs, [this, outs, ix = std::move(ix), hS] {
+      for (size_t q = 0; q < outs.size(); ++q) env_[outs[q]] = Val{hS[ix[q]]};
+    });
     rep["family"] = "gda_scatter";
     rep["n"] = n;
     rep["d"] = d;
@@ -1165,7 +1319,7 @@ class Executor {
         ve.kind = le.e->append ? DLX_VM_APPEND : DLX_VM_COLLECT;
         ve.ty = vm_ty(le.e->out_ty.elem);
         outs[q] = new_vec(n, le.e->out_ty.elem == Ty::Double ? Ty::Double : le.e->out_ty.elem == Ty::Bool ? Ty::Bool : Ty::Int,
-                          st_, true);
+                          lst_, true);
         ve.out = outs[q]->p;
       } else if (le.e->kind == "reduce") {
         ve.kind = DLX_VM_REDUCE;
@@ -1208,51 +1362,55 @@ class Executor {
     rep["instructions"] = static_cast<int>(B.code.size());
     rep["launch"] = "dlx_vm_run_loop";
     if (g_dry) return dry_bind(els), true;
-    dlx_vm_instr* dcode = nullptr;
-    int64_t* dres = nullptr;
-    int* dtrap = nullptr;
-    void* ws = nullptr;
     const size_t wsb = dlx_vm_workspace_bytes(n);
-    ckc(cudaMalloc(&dcode, std::max<size_t>(1, B.code.size()) * sizeof(dlx_vm_instr)), "cudaMalloc");
-    ckc(cudaMalloc(&dres, DLX_VM_MAX_ELEMS * 8), "cudaMalloc");
-    ckc(cudaMalloc(&dtrap, sizeof(int)), "cudaMalloc");
-    ckc(cudaMalloc(&ws, wsb), "cudaMalloc");
-    cudaMemcpyAsync(dcode, B.code.data(), B.code.size() * sizeof(dlx_vm_instr), cudaMemcpyHostToDevice, st_);
-    cudaMemsetAsync(dtrap, 0, sizeof(int), st_);
-    std::vector<int64_t> zeros(DLX_VM_MAX_ELEMS);
+    const size_t code_bytes = std::max<size_t>(1, B.code.size()) * sizeof(dlx_vm_instr);
+    auto* dcode = static_cast<dlx_vm_instr*>(dalloc(code_bytes));
+    auto* dres = static_cast<int64_t*>(dalloc((DLX_VM_MAX_ELEMS + 1) * 8));   // results, then the trap word
+    int* dtrap = reinterpret_cast<int*>(dres + DLX_VM_MAX_ELEMS);
+    void* ws = dalloc(wsb);
+    // staged through pinned memory so the copies (and the launch) do not block the host
+    auto* hin = res_->pin.get_n<unsigned char>(code_bytes + (DLX_VM_MAX_ELEMS + 1) * 8);
+    if (!B.code.empty()) std::memcpy(hin, B.code.data(), B.code.size() * sizeof(dlx_vm_instr));
+    auto* zeros = reinterpret_cast<int64_t*>(hin + ((code_bytes + 7) & ~size_t{7}));
+    std::memset(zeros, 0, (DLX_VM_MAX_ELEMS + 1) * 8);
     for (size_t q = 0; q < els.size(); ++q) zeros[q] = L.elem[q].zero;
-    cudaMemcpyAsync(dres, zeros.data(), zeros.size() * 8, cudaMemcpyHostToDevice, st_);
-    int rc = dlx_vm_run_loop(dcode, &L, dres, dtrap, ws, wsb, st_);
-    std::vector<int64_t> res(DLX_VM_MAX_ELEMS);
-    int htrap = 0;
-    if (rc == DLX_OK) {
-      cudaMemcpyAsync(res.data(), dres, res.size() * 8, cudaMemcpyDeviceToHost, st_);
-      cudaMemcpyAsync(&htrap, dtrap, sizeof(int), cudaMemcpyDeviceToHost, st_);
-      ckc(cudaStreamSynchronize(st_), "sync");
-    }
-    cudaFree(dcode);
-    cudaFree(dres);
-    cudaFree(dtrap);
-    cudaFree(ws);
+    cudaMemcpyAsync(dcode, hin, B.code.size() * sizeof(dlx_vm_instr), cudaMemcpyHostToDevice, lst_);
+    cudaMemcpyAsync(dres, zeros, (DLX_VM_MAX_ELEMS + 1) * 8, cudaMemcpyHostToDevice, lst_);
+    int rc = dlx_vm_run_loop(dcode, &L, dres, dtrap, ws, wsb, lst_);
+    int64_t* res = res_->pin.get_n<int64_t>(DLX_VM_MAX_ELEMS + 1);
+    if (rc == DLX_OK) cudaMemcpyAsync(res, dres, (DLX_VM_MAX_ELEMS + 1) * 8, cudaMemcpyDeviceToHost, lst_);
+    dfree(dcode);
+    dfree(dres);
+    dfree(ws);
     ck(rc);
-    if (htrap & 1) trap("TrapDivByZero: integer division by zero in a multiloop");
-    if (htrap & 2) trap("TrapIndexOutOfBounds: element load out of range in a multiloop");
-    if (htrap & 4) gen_fail("generic kernel met an unknown instruction");
-    for (size_t q = 0; q < els.size(); ++q) {
-      const Elem& e = *els[q].e;
-      if (e.kind == "collect") {
-        if (e.append) outs[q]->n = res[q];   // the builder's final length
-        env_[e.out] = Val{outs[q]};
-      } else if (e.out_ty.t == Ty::Double) {
-        double dv;
-        std::memcpy(&dv, &res[q], 8);
-        env_[e.out] = Val{dv};
-      } else if (e.out_ty.t == Ty::Bool) {
-        env_[e.out] = Val{res[q] != 0};
-      } else {
-        env_[e.out] = Val{res[q]};
-      }
+    std::vector<int> out_syms;
+    std::vector<const Elem*> es;
+    for (const LElem& le : els) {
+      out_syms.push_back(le.e->out);
+      es.push_back(le.e);
     }
+    defer(out_syms, [this, res, es = std::move(es), outs = std::move(outs)] {
+      int htrap;
+      std::memcpy(&htrap, res + DLX_VM_MAX_ELEMS, sizeof(int));
+      if (htrap & 1) trap("TrapDivByZero: integer division by zero in a multiloop");
+      if (htrap & 2) trap("TrapIndexOutOfBounds: element load out of range in a multiloop");
+      if (htrap & 4) gen_fail("generic kernel met an unknown instruction");
+      for (size_t q = 0; q < es.size(); ++q) {
+        const Elem& e = *es[q];
+        if (e.kind == "collect") {
+          if (e.append) outs[q]->n = res[q];   // the builder's final length
+          env_[e.out] = Val{outs[q]};
+        } else if (e.out_ty.t == Ty::Double) {
+          double dv;
+          std::memcpy(&dv, &res[q], 8);
+          env_[e.out] = Val{dv};
+        } else if (e.out_ty.t == Ty::Bool) {
+          env_[e.out] = Val{res[q] != 0};
+        } else {
+          env_[e.out] = Val{res[q]};
+        }
+      }
+    });
     rep["family"] = "generic";
     rep["n"] = n;
     rep["elems"] = static_cast<int>(els.size());
@@ -1272,9 +1430,22 @@ class Executor {
 
   // ---- one root ParallelLoop -------------------------------------------------------------------
   Val run_loop(const Stmt& s) {
-    if (!g_dry) flush_mirrors();
+    if (g_dry) return run_loop_impl(s);
+    flush_mirrors();
+    // next loop stream, ordered after everything the main stream has enqueued so far (RNG
+    // fills, literals, mirror flushes: the loop's inputs)
+    lst_ = res_->loop[launches_++ % kLoopStreams];
+    cudaEvent_t ev = get_event();
+    ckc(cudaEventRecord(ev, st_), "cudaEventRecord");
+    ckc(cudaStreamWaitEvent(lst_, ev, 0), "cudaStreamWaitEvent");
+    res_->events.push_back(ev);
+    const size_t inflight = pending_.size();
     Val r = run_loop_impl(s);
-    if (!g_dry) invalidate_mirrors();
+    if (!report.empty() && report.back().contains("launch")) {
+      report.back()["stream"] = static_cast<int>((launches_ - 1) % kLoopStreams);
+      report.back()["in_flight"] = static_cast<int>(inflight);   // loops it may overlap
+    }
+    invalidate_mirrors();
     return r;
   }
 
@@ -1351,6 +1522,7 @@ RunResult run_program(const std::string& program_json, uint64_t seed, int device
   g_dry = getenv("DLX_PROGRAM_DRYRUN") != nullptr;
   g_debug = getenv("DLX_PROGRAM_DEBUG") != nullptr;
   g_no_mirror = getenv("DLX_PROGRAM_NO_MIRROR") != nullptr;
+  g_serial = getenv("DLX_PROGRAM_SERIAL") != nullptr;
   const std::shared_ptr<const Program> pp = cached_program(program_json);
   const Program& p = *pp;
   cudaStream_t st = nullptr;
@@ -1362,11 +1534,18 @@ RunResult run_program(const std::string& program_json, uint64_t seed, int device
   }
   RunResult r;
   try {
-    Executor ex(p, seed, st);
-    struct VecRegistry {   // route new_vec registrations to this run's executor
-      explicit VecRegistry(std::vector<std::weak_ptr<DevVec>>* r) { g_vecs = r; }
-      ~VecRegistry() { g_vecs = nullptr; }
-    } reg(&ex.vecs_);
+    Executor ex(p, seed, st, g_dry ? nullptr : &device_res(device));
+    struct VecRegistry {   // route new_vec registrations / frees to this run's executor
+      VecRegistry(std::vector<std::weak_ptr<DevVec>>* r, std::function<void()>* f, cudaStream_t s) {
+        g_vecs = r;
+        g_fence = f;
+        g_main_st = s;
+      }
+      ~VecRegistry() {
+        g_vecs = nullptr;
+        g_fence = nullptr;
+      }
+    } reg(&ex.vecs_, g_dry ? nullptr : &ex.fence_, st);
     Val v = ex.run();
     if (!g_dry) cudaStreamSynchronize(st);
     r.output = ex.output;

@@ -191,3 +191,88 @@ def test_lowering_families_dry_run(name, monkeypatch):
     monkeypatch.setenv("DLX_PROGRAM_DRYRUN", "1")
     _, report = run_program(load(name)["program"], seed=1)
     assert [r["family"] for r in report] == EXPECTED_FAMILIES[name]
+
+
+def _offset_program(p, off):
+    """Renumber every symbol and block of a dlx-program/1 descriptor by `off`."""
+    def atom(a):
+        return dict(a, s=a["s"] + off) if "s" in a else a
+
+    stmts = {}
+    for k, st in p["stmts"].items():
+        st = dict(st, args=[atom(a) for a in st["args"]])
+        if "blocks" in st:
+            st["blocks"] = [b + off for b in st["blocks"]]
+        if "loop" in st:
+            lp = st["loop"]
+            lp = dict(lp, range=atom(lp["range"]), index=lp["index"] + off, body=lp["body"] + off)
+            lp["elems"] = [dict(e, out=e["out"] + off, elem=e["elem"] + off,
+                                cond=e["cond"] + off if e["cond"] >= 0 else -1,
+                                combine=e["combine"] + off if e["combine"] >= 0 else -1,
+                                rv_left=e.get("rv_left", -1) + off if e.get("rv_left", -1) >= 0 else -1,
+                                rv_right=e.get("rv_right", -1) + off if e.get("rv_right", -1) >= 0 else -1)
+                           for e in lp["elems"]]
+            st["loop"] = lp
+        stmts[str(int(k) + off)] = st
+    blocks = {str(int(k) + off): dict(b, stmts=[s + off for s in b["stmts"]], result=atom(b["result"]),
+                                      bound=[s + off for s in b.get("bound", [])])
+              for k, b in p["blocks"].items()}
+    return {"format": p["format"], "root": p["root"] + off, "stmts": stmts, "blocks": blocks}
+
+
+def _merge_independent(pa, pb, off=100000):
+    """One program running `pa` and a renumbered copy of `pb` side by side: each program's
+    statements before its first loop, then both first loops back to back (no data edge between
+    them in the DEG), then the rest of `pa`, then the rest of `pb`."""
+    pb = _offset_program(pb, off)
+    stmts = dict(pa["stmts"], **pb["stmts"])
+    blocks = dict(pa["blocks"], **pb["blocks"])
+    ra = pa["blocks"][str(pa["root"])]["stmts"]
+    rb = pb["blocks"][str(pb["root"])]["stmts"]
+
+    def split(root, st):
+        i = next(q for q, s in enumerate(root) if st[str(s)]["op"] == "ParallelLoop")
+        return root[:i], root[i], root[i + 1:]
+
+    a0, la, a1 = split(ra, stmts)
+    b0, lb, b1 = split(rb, stmts)
+    root = a0 + b0 + [la, lb] + a1 + b1
+    blocks[str(pa["root"])] = dict(blocks[str(pa["root"])], stmts=root)
+    del blocks[str(pb["root"])]
+    return {"format": pa["format"], "root": pa["root"], "stmts": stmts, "blocks": blocks}
+
+
+def test_merged_program_lowers_both_loops_dry_run(monkeypatch):
+    from paper_1109_0778_b200.program import run_program
+    monkeypatch.setenv("DLX_PROGRAM_DRYRUN", "1")
+    mv = load("mean_variance_n100000")["program"]
+    _, report = run_program(_merge_independent(mv, mv), seed=1)
+    assert [r["family"] for r in report] == ["generic", "generic"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("second", ["mean_variance_n100000", "groupby_n100000_k16", "kmeans_n65536_d16_k8_it1"])
+def test_independent_loops_overlap(second, monkeypatch):
+    """DEG overlap (scheduleDEG): two root loops with no data edge between
+    them run on different loop streams with the first still in flight when the second
+    launches; results equal the serialised execution (DLX_PROGRAM_SERIAL) bit for bit and the
+    first program's output equals its reference-staged fixture."""
+    from paper_1109_0778_b200.program import run_program
+    fa = load("mean_variance_n100000")
+    merged = _merge_independent(fa["program"], load(second)["program"])
+    text, report = run_program(merged, seed=1)
+    assert len(report) == 2
+    assert report[0]["in_flight"] == 0 and report[1]["in_flight"] == 1
+    assert report[0]["stream"] != report[1]["stream"]
+    monkeypatch.setenv("DLX_PROGRAM_SERIAL", "1")
+    text_s, report_s = run_program(merged, seed=1)
+    assert all(r["in_flight"] == 0 for r in report_s)
+    assert text == text_s
+    exp = lines(fa["expected"])
+    assert all(same_value(g, e) for g, e in zip(lines(text)[:len(exp)], exp))
+    if second == "mean_variance_n100000":   # the copy draws the next 100000 units
+        x = O.rng_units(1, 100000, 100000)
+        mean = x.sum() / 1e5
+        got = lines(text)[len(exp):]
+        assert same_value(got[0], repr(float(mean)))
+        assert same_value(got[1], repr(float((x * x).sum() / 1e5 - mean * mean)))
