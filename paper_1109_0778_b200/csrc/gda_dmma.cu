@@ -39,12 +39,17 @@ constexpr int kGdCtrWarps = DLX_GDA_CTR_WARPS;      // centring warps (three per
 constexpr int kGdThreads = (kGdMmaWarps + kGdCtrWarps) * 32;
 constexpr int kGdCtrThreads = kGdCtrWarps * 32;
 constexpr int kGdTile = 64;           // samples per tile
-constexpr int kGdStride = 64 + 4;     // padded operand row stride (doubles)
+// Operand tile layout: rows k and k + 4 of each 8-row group are interleaved per column, so one
+// 16-byte load gives a lane its fragments for both k-steps of the group (pair-row pr = 4 * group
+// + k % 4 holds [col][k / 4 % 2]); pair-row stride 132 doubles: the 8 lanes of a quarter-warp
+// (g in 2 values x kq in 4) hit 8 distinct 16-byte bank groups.
+constexpr int kGdPStride = 2 * 64 + 4;   // doubles per pair-row
+constexpr int kGdPairRows = 32;          // 64 samples = 32 pair-rows
 constexpr int kGdBlocksPerWarp = 3;   // 36 lower blocks of a 64x64 S over 12 warps
 constexpr int kGdSlots = 3;           // raw tile ring (bulk copies in flight)
 constexpr int kGdDBufs = DLX_GDA_DBUFS;   // centred operand tiles
 constexpr size_t kGdRawBytes = static_cast<size_t>(kGdTile) * 64 * 8;
-constexpr size_t kGdDBytes = static_cast<size_t>(kGdTile) * kGdStride * 8;
+constexpr size_t kGdDBytes = static_cast<size_t>(kGdPairRows) * kGdPStride * 8;
 constexpr size_t kGdOffY = kGdSlots * kGdRawBytes;
 constexpr size_t kGdOffD = kGdOffY + kGdSlots * kGdTile * 8;
 constexpr size_t kGdOffMu = kGdOffD + kGdDBufs * kGdDBytes;
@@ -170,10 +175,11 @@ gda_pass2_dmma_kernel(const double* __restrict__ x, const long long* __restrict_
       }
       named_bar(1, kGdCtrThreads);
     }
-    const double2 m0 = *reinterpret_cast<const double2*>(mu_s + j0);
-    const double2 m1 = *reinterpret_cast<const double2*>(mu_s + 64 + j0);
-    double2 a0 = make_double2(0.0, 0.0), a1 = a0;   // fused: shifted class sums of my columns
-    long long c1 = 0;                                // fused: class-1 rows (cp == 0 threads)
+    // main loop mapping: lane = columns (ja, jb) = (cp, cp + 32), warp rp = pair-rows rp + 12 u
+    const int ja = cp, jb = cp + 32;
+    const double m0a = mu_s[ja], m0b = mu_s[jb], m1a = mu_s[64 + ja], m1b = mu_s[64 + jb];
+    double a0a = 0.0, a0b = 0.0, a1a = 0.0, a1b = 0.0;   // fused: shifted class sums of my columns
+    long long c1 = 0;                                    // fused: class-1 rows (cp == 0 threads)
     for (int m = 0; m < mt; ++m) {
       const int s = m % kGdSlots, b = m % kGdDBufs;
       const int64_t i0 = tile_of(m) * kGdTile;
@@ -183,39 +189,52 @@ gda_pass2_dmma_kernel(const double* __restrict__ x, const long long* __restrict_
       if (m >= kGdDBufs) mbar_wait(&d_empty[b], ((m - kGdDBufs) / kGdDBufs) & 1);
       const double* rs = raw + static_cast<size_t>(s) * kGdTile * 64;
       const long long* yv = ys + s * kGdTile;
-      double* D = Dbuf + static_cast<size_t>(b) * kGdTile * kGdStride;
+      double* D = Dbuf + static_cast<size_t>(b) * kGdPairRows * kGdPStride;
       if (from_smem && d == 64) {
-        // fast path: one label broadcast per warp-row, 16-byte loads and stores
-#pragma unroll 4
-        for (int r = rp; r < kGdTile; r += kGdCtrWarps) {
-          const double2 xv = *reinterpret_cast<const double2*>(rs + r * 64 + j0);
-          const bool one = yv[r] == 1;
-          double2 o;
-          o.x = xv.x - (one ? m1.x : m0.x);
-          o.y = xv.y - (one ? m1.y : m0.y);
-          *reinterpret_cast<double2*>(D + r * kGdStride + j0) = o;
+        // fast path: conflict-free 8-byte loads of two rows, 16-byte stores of (row, row + 4)
+#pragma unroll 3
+        for (int pr = rp; pr < kGdPairRows; pr += kGdCtrWarps) {
+          const int r0 = (pr >> 2) * 8 + (pr & 3), r1 = r0 + 4;
+          const double xa0 = rs[r0 * 64 + ja], xa1 = rs[r1 * 64 + ja];
+          const double xb0 = rs[r0 * 64 + jb], xb1 = rs[r1 * 64 + jb];
+          const bool one0 = yv[r0] == 1, one1 = yv[r1] == 1;
+          double2 oa, ob;
+          oa.x = xa0 - (one0 ? m1a : m0a);
+          oa.y = xa1 - (one1 ? m1a : m0a);
+          ob.x = xb0 - (one0 ? m1b : m0b);
+          ob.y = xb1 - (one1 ? m1b : m0b);
+          *reinterpret_cast<double2*>(D + pr * kGdPStride + 2 * ja) = oa;
+          *reinterpret_cast<double2*>(D + pr * kGdPStride + 2 * jb) = ob;
           if (kFused) {
-            a1.x += one ? o.x : 0.0; a1.y += one ? o.y : 0.0;
-            a0.x += one ? 0.0 : o.x; a0.y += one ? 0.0 : o.y;
-            c1 += one;
+            a1a += one0 ? oa.x : 0.0; a1b += one0 ? ob.x : 0.0;
+            a0a += one0 ? 0.0 : oa.x; a0b += one0 ? 0.0 : ob.x;
+            a1a += one1 ? oa.y : 0.0; a1b += one1 ? ob.y : 0.0;
+            a0a += one1 ? 0.0 : oa.y; a0b += one1 ? 0.0 : ob.y;
+            c1 += one0 + one1;
           }
         }
       } else {
-        for (int r = rp; r < kGdTile; r += kGdCtrWarps) {
-          double2 o = make_double2(0.0, 0.0);
-          if (r < rows) {
-            const int64_t gi = i0 + r;
-            const long long lab = from_smem ? yv[r] : __ldg(y + gi);
-            const bool one = lab == 1;
-            if (j0 < d) o.x = (from_smem ? rs[r * d + j0] : __ldg(x + gi * d + j0)) - (one ? m1.x : m0.x);
-            if (j0 + 1 < d) o.y = (from_smem ? rs[r * d + j0 + 1] : __ldg(x + gi * d + j0 + 1)) - (one ? m1.y : m0.y);
-            if (kFused) {
-              a1.x += one ? o.x : 0.0; a1.y += one ? o.y : 0.0;
-              a0.x += one ? 0.0 : o.x; a0.y += one ? 0.0 : o.y;
-              c1 += one;
+        for (int pr = rp; pr < kGdPairRows; pr += kGdCtrWarps) {
+          const int r0 = (pr >> 2) * 8 + (pr & 3);
+          double va[2] = {0.0, 0.0}, vb[2] = {0.0, 0.0};
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = r0 + 4 * h;
+            if (r < rows) {
+              const int64_t gi = i0 + r;
+              const long long lab = from_smem ? yv[r] : __ldg(y + gi);
+              const bool one = lab == 1;
+              if (ja < d) va[h] = (from_smem ? rs[r * d + ja] : __ldg(x + gi * d + ja)) - (one ? m1a : m0a);
+              if (jb < d) vb[h] = (from_smem ? rs[r * d + jb] : __ldg(x + gi * d + jb)) - (one ? m1b : m0b);
+              if (kFused) {
+                a1a += one ? va[h] : 0.0; a1b += one ? vb[h] : 0.0;
+                a0a += one ? 0.0 : va[h]; a0b += one ? 0.0 : vb[h];
+                c1 += one;
+              }
             }
           }
-          *reinterpret_cast<double2*>(D + r * kGdStride + j0) = o;
+          *reinterpret_cast<double2*>(D + pr * kGdPStride + 2 * ja) = make_double2(va[0], va[1]);
+          *reinterpret_cast<double2*>(D + pr * kGdPStride + 2 * jb) = make_double2(vb[0], vb[1]);
         }
       }
       named_bar(1, kGdCtrThreads);   // D[b] written, raw slot s read by every centring thread
@@ -232,8 +251,10 @@ gda_pass2_dmma_kernel(const double* __restrict__ x, const long long* __restrict_
       // (every tile has been consumed and no copy is outstanding)
       double* red = raw;
       long long* kred = reinterpret_cast<long long*>(raw + kGdCtrWarps * 128);
-      *reinterpret_cast<double2*>(red + rp * 128 + j0) = a0;
-      *reinterpret_cast<double2*>(red + rp * 128 + 64 + j0) = a1;
+      red[rp * 128 + ja] = a0a;
+      red[rp * 128 + jb] = a0b;
+      red[rp * 128 + 64 + ja] = a1a;
+      red[rp * 128 + 64 + jb] = a1b;
       if (cp == 0) kred[rp] = c1;
       named_bar(1, kGdCtrThreads);
       if (ct < 128) {
@@ -281,28 +302,32 @@ gda_pass2_dmma_kernel(const double* __restrict__ x, const long long* __restrict_
   for (int m = 0; m < mt; ++m) {
     const int b = m % kGdDBufs;
     mbar_wait(&d_full[b], (m / kGdDBufs) & 1);
-    const double* D = Dbuf + static_cast<size_t>(b) * kGdTile * kGdStride;
+    const double* D = Dbuf + static_cast<size_t>(b) * kGdPairRows * kGdPStride;
     if (shared) {
 #pragma unroll 2
       for (int k0 = 0; k0 < kGdTile; k0 += 8) {
+        // one 16-byte load per index: .x = row k0 + kq, .y = row k0 + 4 + kq (column 8 idx + g)
+        const double* prow = D + ((k0 >> 3) * 4 + kq) * kGdPStride + 2 * g;
+        const double2 fa = *reinterpret_cast<const double2*>(prow + 16 * ba[0]);
 #pragma unroll
-        for (int p = 0; p < 2; ++p) {
-          const double* row = D + (k0 + 4 * p + kq) * kGdStride + g;
-          const double fa = row[ba[0] * 8];
-#pragma unroll
-          for (int u = 0; u < kGdBlocksPerWarp; ++u) dmma_8x8x4(acc[u][p], fa, row[bb[u] * 8]);
+        for (int u = 0; u < kGdBlocksPerWarp; ++u) {
+          const double2 fb = *reinterpret_cast<const double2*>(prow + 16 * bb[u]);
+          dmma_8x8x4(acc[u][0], fa.x, fb.x);
+          dmma_8x8x4(acc[u][1], fa.y, fb.y);
         }
       }
     } else {
 #pragma unroll 2
       for (int k0 = 0; k0 < kGdTile; k0 += 8) {
+        const double* prow = D + ((k0 >> 3) * 4 + kq) * kGdPStride + 2 * g;
 #pragma unroll
-        for (int p = 0; p < 2; ++p) {
-          const double* row = D + (k0 + 4 * p + kq) * kGdStride + g;
-#pragma unroll
-          for (int u = 0; u < kGdBlocksPerWarp; ++u)
-            if (own[u]) dmma_8x8x4(acc[u][p], row[ba[u] * 8], row[bb[u] * 8]);
-        }
+        for (int u = 0; u < kGdBlocksPerWarp; ++u)
+          if (own[u]) {
+            const double2 fa = *reinterpret_cast<const double2*>(prow + 16 * ba[u]);
+            const double2 fb = *reinterpret_cast<const double2*>(prow + 16 * bb[u]);
+            dmma_8x8x4(acc[u][0], fa.x, fb.x);
+            dmma_8x8x4(acc[u][1], fa.y, fb.y);
+          }
       }
     }
     __syncwarp();
