@@ -228,6 +228,7 @@ static bool g_debug = false;  // DLX_PROGRAM_DEBUG=1: why a specialised family d
 // the mirror is loaded on the first host read, host writes mark a dirty range, and every device
 // launch first flushes dirty ranges (one copy each) and afterwards invalidates the mirrors.
 constexpr size_t kMirrorBytes = 64 << 10;
+constexpr int64_t kPageElems = 8192;   // read-through page of a large vector (64 KiB of fp64)
 bool g_no_mirror = false;   // DLX_PROGRAM_NO_MIRROR=1: per-element transfers (A/B timing only)
 bool g_serial = false;      // DLX_PROGRAM_SERIAL=1: complete every loop before the next statement
 // The run's main stream (host statements, RNG fills, mirror flushes, frees) and the fence that
@@ -241,6 +242,12 @@ struct DevVec {
   cudaStream_t fst = nullptr;   // stream the buffer is freed on (stream-ordered allocator)
   std::vector<unsigned char> host;
   bool host_valid = false;
+  // large vectors: a read-through page of host copies around the last element read (host
+  // statements that read x(0), x(1), ... — the k-means centroid initialisation — cost one
+  // transfer per page instead of one synchronous copy per element)
+  std::vector<unsigned char> page;
+  int64_t page_lo = 0;
+  bool page_valid = false;
   int64_t dirty_lo = INT64_MAX, dirty_hi = -1;   // [lo, hi) newer on the host than on the device
   ~DevVec() {
     if (!p) return;
@@ -419,7 +426,10 @@ DeviceRes& device_res(int device) {
     for (auto& s : r.loop) ckc(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
     cudaMemPool_t pool;   // keep freed blocks of the stream-ordered allocator for the next loops
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t keep = 256ull << 20;
+      // DLX_POOL_KEEP_GB: bytes the pool keeps mapped across syncs (default 32 GB: remapping an
+      // 8 GiB input on every run cost 0.1-1 s per C4 program run, r131)
+      const char* kg = getenv("DLX_POOL_KEEP_GB");
+      uint64_t keep = kg ? static_cast<uint64_t>(atof(kg) * (1ull << 30)) : (32ull << 30);
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
     r.init = true;
@@ -495,9 +505,12 @@ class Executor {
       if (err == cudaSuccess) err = e;
       res_->events.push_back(p.ev);
     }
+    struct ArenaReset {   // the staged results are consumed (or abandoned on a trap)
+      PinnedArena& a;
+      ~ArenaReset() { a.reset(); }
+    } arena_reset{res_->pin};
     ckc(err, "loop completion");
     for (Pending& p : pend) p.finish();   // program order: the first loop's trap wins
-    res_->pin.reset();
   }
   void* dalloc(size_t bytes) {
     void* p = nullptr;
@@ -614,6 +627,7 @@ class Executor {
     for (auto& w : vecs_)
       if (auto v = w.lock()) {
         v->host_valid = false;
+        v->page_valid = false;
         vecs_[live++] = w;
       }
     vecs_.resize(live);
@@ -635,19 +649,31 @@ class Executor {
       std::memcpy(&x, h, 8);
       return Val{x};
     }
-    ckc(cudaStreamSynchronize(st_), "sync");
+    const size_t es = v->esize();
+    if (g_no_mirror) {   // A/B: one synchronous copy per element
+      v->page_valid = false;
+      v->page.resize(es);
+      ckc(cudaStreamSynchronize(st_), "sync");
+      ckc(cudaMemcpy(v->page.data(), static_cast<unsigned char*>(v->p) + i * es, es, cudaMemcpyDeviceToHost), "d2h");
+      v->page_lo = i;
+    } else if (!v->page_valid || i < v->page_lo || i >= v->page_lo + static_cast<int64_t>(v->page.size() / es)) {
+      const int64_t lo = i & ~(kPageElems - 1), hi = std::min(v->n, lo + kPageElems);
+      v->page.resize(static_cast<size_t>(hi - lo) * es);
+      ckc(cudaMemcpyAsync(v->page.data(), static_cast<unsigned char*>(v->p) + lo * es, v->page.size(),
+                          cudaMemcpyDeviceToHost, st_), "d2h");
+      ckc(cudaStreamSynchronize(st_), "sync");
+      v->page_lo = lo;
+      v->page_valid = true;
+    }
+    const unsigned char* h = v->page.data() + static_cast<size_t>(i - v->page_lo) * es;
     if (v->elem == Ty::Double) {
       double x;
-      ckc(cudaMemcpy(&x, static_cast<double*>(v->p) + i, 8, cudaMemcpyDeviceToHost), "d2h");
+      std::memcpy(&x, h, 8);
       return Val{x};
     }
-    if (v->elem == Ty::Bool) {
-      unsigned char x;
-      ckc(cudaMemcpy(&x, static_cast<unsigned char*>(v->p) + i, 1, cudaMemcpyDeviceToHost), "d2h");
-      return Val{x != 0};
-    }
+    if (v->elem == Ty::Bool) return Val{*h != 0};
     int64_t x;
-    ckc(cudaMemcpy(&x, static_cast<int64_t*>(v->p) + i, 8, cudaMemcpyDeviceToHost), "d2h");
+    std::memcpy(&x, h, 8);
     return Val{x};
   }
 
@@ -671,6 +697,7 @@ class Executor {
       return;
     }
     fence();
+    v->page_valid = false;   // the page may hold the old value
     if (v->elem == Ty::Double) {
       const double d = x.d();
       ckc(cudaMemcpyAsync(static_cast<double*>(v->p) + i, &d, 8, cudaMemcpyHostToDevice, st_), "h2d");

@@ -1,0 +1,152 @@
+"""Direct construction of "dlx-program/1" descriptors for the OptiML k-means iteration, in the
+shape the reference's own staging produces ("production callers may construct a
+LoopPayload-shaped descriptor directly — no staging/fusion at 4k-elem scale").
+
+The reference front-end stages one k-means iteration as ONE fused ParallelLoop (fuse_loops,
+proj/src/fusion.cpp:170-288): a collect whose elem is the staged_if argmin chain over k inner
+distance reduces (stage.cpp:73-104; loops.cpp:111-174), horizontally fused with the k counts
+and k*d sums, each a predicated reduce keyed on the collect's value (vertical fusion
+substitutes it), then host statements mu(c*d+j) = sum_cj / toDouble(count_c)
+(vectordsl.cpp:90-103).  At the headline shape (k = d = 64: 4,160 elems) the reference's
+fusion pass is quadratic, so this module emits the same loop payload
+(node.hpp:60-81: range, index, body, elems with elem / cond / combine blocks, zero,
+rv_left / rv_right) without it.  `tests/test_staged_programs.py` checks that the directly built
+program at the fixture shape produces exactly the reference-staged program's output.
+"""
+from __future__ import annotations
+
+import json
+
+
+class _Builder:
+    def __init__(self):
+        self.stmts: dict[str, dict] = {}
+        self.blocks: dict[str, dict] = {}
+        self.next_sym = 0
+        self.next_block = 1   # block 0 is the root
+
+    @staticmethod
+    def s(sym: int, ty: str) -> dict:
+        return {"s": sym, "t": ty}
+
+    @staticmethod
+    def i(v: int) -> dict:
+        return {"i": int(v), "t": "Int"}
+
+    @staticmethod
+    def d(v: float) -> dict:
+        return {"d": float(v), "t": "Double"}
+
+    def sym(self) -> int:
+        self.next_sym += 1
+        return self.next_sym - 1
+
+    def stmt(self, out: list, op: str, ty: str, args: list, **extra) -> int:
+        x = self.sym()
+        self.stmts[str(x)] = dict(op=op, ty=ty, args=args, **extra)
+        out.append(x)
+        return x
+
+    def block(self, stmts: list, result: dict, bound=()) -> int:
+        b = self.next_block
+        self.next_block += 1
+        self.blocks[str(b)] = {"stmts": stmts, "result": result, "bound": list(bound)}
+        return b
+
+    def reduce_elem(self, out: int, ty: str, elem: int, cond: int, zero: dict) -> dict:
+        l, r = self.sym(), self.sym()
+        body = []
+        p = self.stmt(body, "Plus", ty, [self.s(l, ty), self.s(r, ty)])
+        comb = self.block(body, self.s(p, ty), bound=[l, r])
+        return {"kind": "reduce", "live": True, "out": out, "out_ty": ty, "elem": elem, "cond": cond,
+                "combine": comb, "append": False, "zero": zero, "rv_left": l, "rv_right": r}
+
+
+def kmeans_program(n: int, d: int, k: int, iters: int = 1) -> dict:
+    """The staged program of integration/stage_programs.cpp::kmeans(n, d, k, iters): x =
+    randVector(n*d), mu = the first k rows of x, `iters` fused iterations (each prints the
+    assignment of row 0 and the k counts), then the k*d centroids are printed."""
+    B = _Builder()
+    root: list[int] = []
+    VD, VI = "Vector[Double]", "Vector[Int]"
+    x = B.stmt(root, "VectorRand", VD, [B.i(n * d)])
+    mu = B.stmt(root, "VectorNew", VD, [B.i(k * d)], aux_ty="Double")
+    for e in range(k * d):
+        a = B.stmt(root, "VectorApply", "Double", [B.s(x, VD), B.i(e)])
+        B.stmt(root, "VectorUpdate", "Unit", [B.s(mu, VD), B.i(e), B.s(a, "Double")])
+    for _ in range(iters):
+        i = B.sym()                       # the loop index
+        loop_sym = B.sym()                # the collect's out (= the ParallelLoop statement)
+        # collect elem: k distance reduces over j (one fused inner loop), then the argmin chain
+        eb: list[int] = []
+        j = B.sym()
+        douts = [B.sym() for _ in range(k)]
+        inner_elems = []
+        for c in range(k):
+            body: list[int] = []
+            row = B.stmt(body, "Times", "Int", [B.i(d), B.s(i, "Int")])
+            xi = B.stmt(body, "Plus", "Int", [B.s(row, "Int"), B.s(j, "Int")])
+            xv = B.stmt(body, "VectorApply", "Double", [B.s(x, VD), B.s(xi, "Int")])
+            mi = j if c == 0 else B.stmt(body, "Plus", "Int", [B.i(c * d), B.s(j, "Int")])
+            mv = B.stmt(body, "VectorApply", "Double", [B.s(mu, VD), B.s(mi, "Int")])
+            df = B.stmt(body, "Minus", "Double", [B.s(xv, "Double"), B.s(mv, "Double")])
+            sq = B.stmt(body, "Times", "Double", [B.s(df, "Double"), B.s(df, "Double")])
+            inner_elems.append(B.reduce_elem(douts[c], "Double", B.block(body, B.s(sq, "Double")), -1, B.d(0.0)))
+        inner_body = B.block([], {"u": 1, "t": "Unit"}, bound=[j])
+        B.stmts[str(douts[0])] = {"op": "ParallelLoop", "ty": "Double", "args": [],
+                                  "loop": {"range": B.i(d), "index": j, "body": inner_body, "elems": inner_elems}}
+        eb.append(douts[0])
+        best, idx = B.d(1e300), B.i(0)
+        for c in range(k):
+            lt = B.stmt(eb, "Lt", "Bool", [B.s(douts[c], "Double"), best])
+            if c + 1 < k:   # the last best is dead (the reference's DCE drops it)
+                nb = B.stmt(eb, "IfThenElse", "Double", [B.s(lt, "Bool")],
+                            blocks=[B.block([], B.s(douts[c], "Double")), B.block([], best)])
+            ni = B.stmt(eb, "IfThenElse", "Int", [B.s(lt, "Bool")],
+                        blocks=[B.block([], B.i(c)), B.block([], idx)])
+            if c + 1 < k:
+                best = B.s(nb, "Double")
+            idx = B.s(ni, "Int")
+        a_sym = idx["s"]
+        elems = [{"kind": "collect", "live": True, "out": loop_sym, "out_ty": VI, "elem": B.block(eb, idx),
+                  "cond": -1, "combine": -1, "append": False}]
+        counts, sums = [], []
+        for c in range(k):
+            def cond_block():
+                cb: list[int] = []
+                q = B.stmt(cb, "Eq", "Bool", [B.s(a_sym, "Int"), B.i(c)])
+                return B.block(cb, B.s(q, "Bool"))
+            cnt = B.sym()
+            counts.append(cnt)
+            elems.append(B.reduce_elem(cnt, "Int", B.block([], B.i(1)), cond_block(), B.i(0)))
+            for jj in range(d):
+                body = []
+                row = B.stmt(body, "Times", "Int", [B.i(d), B.s(i, "Int")])
+                xi = row if jj == 0 else B.stmt(body, "Plus", "Int", [B.s(row, "Int"), B.i(jj)])
+                xv = B.stmt(body, "VectorApply", "Double", [B.s(x, VD), B.s(xi, "Int")])
+                sm = B.sym()
+                sums.append(sm)
+                elems.append(B.reduce_elem(sm, "Double", B.block(body, B.s(xv, "Double")), cond_block(), B.d(0.0)))
+        body = B.block([], {"u": 1, "t": "Unit"}, bound=[i])
+        B.stmts[str(loop_sym)] = {"op": "ParallelLoop", "ty": VI, "args": [],
+                                  "loop": {"range": B.i(n), "index": i, "body": body, "elems": elems}}
+        root.append(loop_sym)
+        a0 = B.stmt(root, "VectorApply", "Int", [B.s(loop_sym, VI), B.i(0)])
+        B.stmt(root, "Print", "Unit", [B.s(a0, "Int")])
+        for c in range(k):
+            B.stmt(root, "Print", "Unit", [B.s(counts[c], "Int")])
+            cd = B.stmt(root, "ToDouble", "Double", [B.s(counts[c], "Int")])
+            for jj in range(d):
+                q = B.stmt(root, "Divide", "Double", [B.s(sums[c * d + jj], "Double"), B.s(cd, "Double")])
+                B.stmt(root, "VectorUpdate", "Unit", [B.s(mu, VD), B.i(c * d + jj), B.s(q, "Double")])
+    for e in range(k * d):
+        v = B.stmt(root, "VectorApply", "Double", [B.s(mu, VD), B.i(e)])
+        B.stmt(root, "Print", "Unit", [B.s(v, "Double")])
+    B.blocks["0"] = {"stmts": root, "result": {"u": 1, "t": "Unit"}, "bound": []}
+    return {"format": "dlx-program/1", "root": 0, "stmts": B.stmts, "blocks": B.blocks}
+
+
+if __name__ == "__main__":   # python -m paper_1109_0778_b200.descriptors N D K ITERS > out.json
+    import sys
+    n, d, k, it = (int(v) for v in sys.argv[1:5])
+    json.dump({"seed": 1, "program": kmeans_program(n, d, k, it)}, sys.stdout)

@@ -276,3 +276,32 @@ def test_independent_loops_overlap(second, monkeypatch):
         got = lines(text)[len(exp):]
         assert same_value(got[0], repr(float(mean)))
         assert same_value(got[1], repr(float((x * x).sum() / 1e5 - mean * mean)))
+
+
+@pytest.mark.parametrize("shape", [(4096, 16, 8, 2), (16_777_216, 64, 64, 1)])
+def test_direct_kmeans_descriptor_dry_run(shape, monkeypatch):
+    """CPU: the directly built k-means program (descriptors.kmeans_program: the reference's
+    fused-loop shape without its quadratic fusion pass) lowers every iteration to the k-means
+    family with all k(d+1)+1 elems live — at the fixture shape and at C4."""
+    from paper_1109_0778_b200.descriptors import kmeans_program
+    from paper_1109_0778_b200.program import run_program
+    monkeypatch.setenv("DLX_PROGRAM_DRYRUN", "1")
+    n, d, k, it = shape
+    _, report = run_program(kmeans_program(n, d, k, it), seed=1)
+    assert [r["family"] for r in report] == ["kmeans"] * it
+    assert all(r["live_elems"] == 1 + k * (d + 1) and r["k"] == k and r["d"] == d for r in report)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,shape", [("kmeans_n4096_d16_k8_it2", (4096, 16, 8, 2)),
+                                        ("kmeans_n65536_d16_k8_it1", (65536, 16, 8, 1))])
+def test_direct_kmeans_descriptor_matches_reference_staged(name, shape):
+    """The directly built program prints what the REFERENCE-staged program's MiniC prints
+    (assignment of row 0, counts, every centroid) on the B200 executor."""
+    from paper_1109_0778_b200.descriptors import kmeans_program
+    from paper_1109_0778_b200.program import run_program
+    text, report = run_program(kmeans_program(*shape), seed=1)
+    got, exp = lines(text), lines(load(name)["expected"])
+    assert len(got) == len(exp)
+    assert all(same_value(g, e) for g, e in zip(got, exp))
+    assert [r["family"] for r in report] == ["kmeans"] * shape[3]
