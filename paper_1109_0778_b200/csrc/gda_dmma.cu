@@ -206,10 +206,10 @@ gda_pass2_dmma_kernel(const double* __restrict__ x, const long long* __restrict_
           *reinterpret_cast<double2*>(D + pr * kGdPStride + 2 * ja) = oa;
           *reinterpret_cast<double2*>(D + pr * kGdPStride + 2 * jb) = ob;
           if (kFused) {
-            a1a += one0 ? oa.x : 0.0; a1b += one0 ? ob.x : 0.0;
-            a0a += one0 ? 0.0 : oa.x; a0b += one0 ? 0.0 : ob.x;
-            a1a += one1 ? oa.y : 0.0; a1b += one1 ? ob.y : 0.0;
-            a0a += one1 ? 0.0 : oa.y; a0b += one1 ? 0.0 : ob.y;
+            // the label is warp-uniform (one row per warp): branch, so each element costs one
+            // fp64 add for its class sum instead of two selects-and-adds
+            if (one0) { a1a += oa.x; a1b += ob.x; } else { a0a += oa.x; a0b += ob.x; }
+            if (one1) { a1a += oa.y; a1b += ob.y; } else { a0a += oa.y; a0b += ob.y; }
             c1 += one0 + one1;
           }
         }
