@@ -305,3 +305,57 @@ def test_direct_kmeans_descriptor_matches_reference_staged(name, shape):
     assert len(got) == len(exp)
     assert all(same_value(g, e) for g, e in zip(got, exp))
     assert [r["family"] for r in report] == ["kmeans"] * shape[3]
+
+
+def _two_trapping_loops():
+    """Two independent root loops that both trap on the device: the first divides by zero
+    (Int, at i = 5), the second loads past the end of a 10-element vector."""
+    from paper_1109_0778_b200.descriptors import _Builder
+    B = _Builder()
+    root = []
+    v = B.stmt(root, "VectorNew", "Vector[Double]", [B.i(10)], aux_ty="Double")
+    outs = []
+    for kind in ("div", "oob"):
+        i, out = B.sym(), B.sym()
+        body = []
+        if kind == "div":
+            m = B.stmt(body, "Minus", "Int", [B.s(i, "Int"), B.i(5)])
+            q = B.stmt(body, "Divide", "Int", [B.i(1), B.s(m, "Int")])
+            el = B.reduce_elem(out, "Int", B.block(body, B.s(q, "Int")), -1, B.i(0))
+        else:
+            ix = B.stmt(body, "Plus", "Int", [B.s(i, "Int"), B.i(1000)])
+            q = B.stmt(body, "VectorApply", "Double", [B.s(v, "Vector[Double]"), B.s(ix, "Int")])
+            el = B.reduce_elem(out, "Double", B.block(body, B.s(q, "Double")), -1, B.d(0.0))
+        B.stmts[str(out)] = {"op": "ParallelLoop", "ty": el["out_ty"], "args": [],
+                             "loop": {"range": B.i(100), "index": i, "body": B.block([], {"u": 1, "t": "Unit"}, bound=[i]),
+                                      "elems": [el]}}
+        root.append(out)
+        outs.append(out)
+    for o, ty in zip(outs, ("Int", "Double")):
+        B.stmt(root, "Print", "Unit", [B.s(o, ty)])
+    B.blocks["0"] = {"stmts": root, "result": {"u": 1, "t": "Unit"}, "bound": []}
+    return {"format": "dlx-program/1", "root": 0, "stmts": B.stmts, "blocks": B.blocks}
+
+
+def test_two_trapping_loops_dry_run(monkeypatch):
+    from paper_1109_0778_b200.program import run_program
+    monkeypatch.setenv("DLX_PROGRAM_DRYRUN", "1")
+    _, report = run_program(_two_trapping_loops(), seed=1)
+    assert [r["family"] for r in report] == ["generic", "generic"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("serial", [False, True])
+def test_trap_of_earlier_loop_wins(serial, monkeypatch):
+    """With both loops in flight, the earlier loop's trap (program order) is the one raised,
+    as in sequential execution (Int division by zero traps)."""
+    from paper_1109_0778_b200 import TrapError
+    from paper_1109_0778_b200.program import run_program
+    if serial:
+        monkeypatch.setenv("DLX_PROGRAM_SERIAL", "1")
+    with pytest.raises(TrapError, match="division by zero"):
+        run_program(_two_trapping_loops(), seed=1)
+    # the executor's per-device resources (loop streams, events, pinned staging) stay usable
+    fx = load("mean_variance_n100000")
+    text, _ = run_program(fx["program"], seed=1)
+    assert all(same_value(g, e) for g, e in zip(lines(text), lines(fx["expected"])))
