@@ -86,6 +86,13 @@ size_t dlx_kmeans_workspace_bytes(int64_t n, int32_t d, int32_t k);
 int dlx_kmeans_step(const double* d_x, int64_t n, int32_t d, int32_t k, const double* d_mu,
                     int32_t* d_assign, int64_t* d_counts, double* d_sums, void* d_workspace,
                     size_t workspace_bytes, int method, dlx_stream_t stream);
+/* One whole k-means iteration at one rank: dlx_kmeans_step, then d_mu updated in place with
+ * dlx_kmeans_update's arithmetic, the update fused into the step's combine launch (one launch
+ * fewer per iteration).  Results bit-identical to step + update.  Replaces the reference's
+ * staged iteration: fused loop + k*d `mu.update(c*d+j, sum/toDouble(count))` (vectordsl.cpp:90-103). */
+int dlx_kmeans_iteration(const double* d_x, int64_t n, int32_t d, int32_t k, double* d_mu,
+                         int32_t* d_assign, int64_t* d_counts, double* d_sums, void* d_workspace,
+                         size_t workspace_bytes, int method, dlx_stream_t stream);
 /* mu[c*d+j] = sums[c*d+j] / (double)counts[c]  (empty cluster -> 0/0 = NaN) */
 int dlx_kmeans_update(const int64_t* d_counts, const double* d_sums, int32_t k, int32_t d,
                       double* d_mu, dlx_stream_t stream);

@@ -69,6 +69,7 @@ _SIGS = {
     "dlx_kmeans_workspace_bytes": (_sz, [_i64, _i32, _i32]),
     "dlx_kmeans_step": (_int, [_vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _int, _vp]),
     "dlx_kmeans_update": (_int, [_vp, _vp, _i32, _i32, _vp, _vp]),
+    "dlx_kmeans_iteration": (_int, [_vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _int, _vp]),
     "dlx_kmeans_last_recheck_count": (_int, [_vp, _i64, _i32, _i32, ctypes.POINTER(_i64), _vp]),
     "dlx_groupby_workspace_bytes": (_sz, [_i64, _i64]),
     "dlx_groupby_count": (_int, [_vp, _i64, _i64, _vp, _vp, _sz, _vp]),

@@ -96,4 +96,47 @@ int combine_f64_i64(const double* pf, long long wf, double* of, const long long*
   return DLX_OK;
 }
 
+// k-means at one rank: the combine of (sums, counts) fused with the centroid update
+// mu[c*d+j] = sums[c*d+j] / (double)counts[c] (kmeans_update_kernel's arithmetic).  A sums
+// block also folds the counts of its columns' centroids (integer sums: the same value the
+// counts blocks write), so the update needs no second launch.
+__global__ void __launch_bounds__(kCombWarps * 32)
+combine_kmeans_update_kernel(const double* __restrict__ pf, double* __restrict__ of,
+                             const long long* __restrict__ pi, long long* __restrict__ oi, int k, int d,
+                             int nparts, double* __restrict__ mu) {
+  pdl_wait();   // the multiloop that wrote the partials has completed (it also read mu)
+  pdl_trigger();
+  const long long wf = static_cast<long long>(k) * d;
+  const long long bf = (wf + 31) / 32;
+  if (blockIdx.x >= bf) {
+    combine_columns<long long, long long>(pi, nparts, k, oi, blockIdx.x - bf);
+    return;
+  }
+  __shared__ long long cnt_s[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long e = static_cast<long long>(blockIdx.x) * 32 + lane;
+  const int c = e < wf ? static_cast<int>(e / d) : 0;
+  long long a = 0;   // count of my column's centroid, folded per warp then across warps
+  for (int p = warp; p < nparts; p += kCombWarps) a += pi[static_cast<size_t>(p) * k + c];
+  __shared__ long long cred[kCombWarps][33];
+  cred[warp][lane] = a;
+  combine_columns<double, double>(pf, nparts, wf, of, blockIdx.x);   // ends with __syncthreads + warp 0 write
+  if (warp == 0) {
+    long long t = 0;
+    for (int w = 0; w < kCombWarps; ++w) t += cred[w][lane];
+    cnt_s[lane] = t;
+  }
+  __syncthreads();
+  if (warp == 0 && e < wf) mu[e] = of[e] / static_cast<double>(cnt_s[lane]);  // IEEE: 0/0 -> NaN
+}
+
+int combine_kmeans_update(const double* pf, double* of, const long long* pi, long long* oi, int k, int d,
+                          int nparts, double* mu, cudaStream_t s) {
+  const long long blocks = (static_cast<long long>(k) * d + 31) / 32 + (k + 31) / 32;
+  DLX_CUDA(launch_pdl(combine_kmeans_update_kernel, dim3(static_cast<unsigned>(blocks)), dim3(kCombWarps * 32), 0,
+                      s, pf, of, pi, oi, k, d, nparts, mu));
+  DLX_LAUNCHED("combine_kmeans_update_kernel");
+  return DLX_OK;
+}
+
 }  // namespace dlx

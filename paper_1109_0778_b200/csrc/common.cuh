@@ -52,6 +52,8 @@ inline int cuda_fail(cudaError_t e, const char* what) {
 int combine_f64(const double* parts, int nparts, long long width, double* out, cudaStream_t s);
 int combine_i64(const long long* parts, int nparts, long long width, long long* out, cudaStream_t s);
 // an fp64 and an int64 record (same number of partials) in one launch
+int combine_kmeans_update(const double* pf, double* of, const long long* pi, long long* oi, int k, int d,
+                          int nparts, double* mu, cudaStream_t s);
 int combine_f64_i64(const double* pf, long long wf, double* of, const long long* pi, long long wi,
                     long long* oi, int nparts, cudaStream_t s);
 int combine_u32_i64(const unsigned* parts, int nparts, long long width, long long* out, cudaStream_t s);

@@ -360,8 +360,10 @@ __global__ void kmeans_update_kernel(const long long* __restrict__ counts,
   }
 }
 
+// mu_out != nullptr: the combine also applies the centroid update (one launch, N = 1 programs)
 int kmeans_finalize(const long long* part_counts, const double* part_sums, int parts, int k, int d,
-                    long long* counts, double* sums, cudaStream_t stream) {
+                    long long* counts, double* sums, cudaStream_t stream, double* mu_out) {
+  if (mu_out) return combine_kmeans_update(part_sums, sums, part_counts, counts, k, d, parts, mu_out, stream);
   return combine_f64_i64(part_sums, static_cast<long long>(k) * d, sums, part_counts, k, counts, parts,
                          stream);
 }
@@ -370,7 +372,7 @@ int kmeans_finalize(const long long* part_counts, const double* part_sums, int p
 // is outside its plan so AUTO can fall back to the direct kernel.
 int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double* mu,
                          int32_t* assign, long long* counts, double* sums, void* ws,
-                         size_t ws_bytes, cudaStream_t stream, bool probe_only);
+                         size_t ws_bytes, cudaStream_t stream, bool probe_only, double* mu_out);
 size_t kmeans_screened_workspace_bytes(int64_t n, int d, int k);
 
 static size_t direct_workspace_bytes(int64_t n, int d, int k) {
@@ -398,7 +400,7 @@ static bool prefer_small(int64_t n, int d, int k) {
 
 static int kmeans_small_step(const double* x, int64_t n, int d, int k, const double* mu,
                              int32_t* assign, long long* counts, double* sums, void* ws,
-                             size_t ws_bytes, cudaStream_t stream) {
+                             size_t ws_bytes, cudaStream_t stream, double* mu_out) {
   SmallPlan p;
   DLX_REQUIRE(small_plan(n, d, k, &p), DLX_ERR_GENERATION, "GenerationFailed: small k-means plan");
   Carve c(ws);
@@ -411,12 +413,12 @@ static int kmeans_small_step(const double* x, int64_t n, int d, int k, const dou
   DLX_CUDA(launch_pdl(kmeans_small_kernel, dim3(p.grid), dim3(kSmThreads), p.smem, stream, x, n, d, k, mu,
                       assign, pc, psum, p.xstride));
   DLX_LAUNCHED("kmeans_small_kernel");
-  return kmeans_finalize(pc, psum, p.grid, k, d, counts, sums, stream);
+  return kmeans_finalize(pc, psum, p.grid, k, d, counts, sums, stream, mu_out);
 }
 
 static int kmeans_direct_step(const double* x, int64_t n, int d, int k, const double* mu,
                               int32_t* assign, long long* counts, double* sums, void* ws,
-                              size_t ws_bytes, cudaStream_t stream) {
+                              size_t ws_bytes, cudaStream_t stream, double* mu_out) {
   KmeansPlan p;
   DLX_REQUIRE(make_plan(n, d, k, &p), DLX_ERR_GENERATION,
               "GenerationFailed: k-means k=%d d=%d exceeds the shared-memory plan", k, d);
@@ -430,7 +432,7 @@ static int kmeans_direct_step(const double* x, int64_t n, int d, int k, const do
                                 static_cast<int>(p.smem)));
   kmeans_direct_kernel<<<p.grid, kThreads, p.smem, stream>>>(x, n, d, k, mu, assign, pc, psum, p);
   DLX_LAUNCHED("kmeans_direct_kernel");
-  return kmeans_finalize(pc, psum, p.grid, k, d, counts, sums, stream);
+  return kmeans_finalize(pc, psum, p.grid, k, d, counts, sums, stream, mu_out);
 }
 
 }  // namespace dlx
@@ -443,9 +445,9 @@ size_t dlx_kmeans_workspace_bytes(int64_t n, int32_t d, int32_t k) {
   return std::max(direct_workspace_bytes(n, d, k), kmeans_screened_workspace_bytes(n, d, k));
 }
 
-int dlx_kmeans_step(const double* d_x, int64_t n, int32_t d, int32_t k, const double* d_mu,
-                    int32_t* d_assign, int64_t* d_counts, double* d_sums, void* d_workspace,
-                    size_t workspace_bytes, int method, dlx_stream_t stream) {
+static int kmeans_step_impl(const double* d_x, int64_t n, int32_t d, int32_t k, const double* d_mu,
+                            int32_t* d_assign, int64_t* d_counts, double* d_sums, void* d_workspace,
+                            size_t workspace_bytes, int method, dlx_stream_t stream, double* mu_out) {
   DLX_REQUIRE(n >= 0 && d > 0 && k > 0, DLX_ERR_ARG, "k-means: bad shape n=%lld d=%d k=%d",
               (long long)n, d, k);
   DLX_REQUIRE(d_mu && d_counts && d_sums && (d_x || n == 0), DLX_ERR_ARG,
@@ -454,22 +456,36 @@ int dlx_kmeans_step(const double* d_x, int64_t n, int32_t d, int32_t k, const do
   if (n == 0) {
     DLX_CUDA(cudaMemsetAsync(d_counts, 0, sizeof(int64_t) * k, stream));
     DLX_CUDA(cudaMemsetAsync(d_sums, 0, sizeof(double) * k * d, stream));
-    return DLX_OK;
+    return mu_out ? dlx_kmeans_update(d_counts, d_sums, k, d, mu_out, stream) : DLX_OK;
   }
   if (method == DLX_KMEANS_AUTO && prefer_small(n, d, k))
     return kmeans_small_step(d_x, n, d, k, d_mu, d_assign, counts, d_sums, d_workspace,
-                             workspace_bytes, stream);
+                             workspace_bytes, stream, mu_out);
   if (method == DLX_KMEANS_SCREENED || method == DLX_KMEANS_AUTO) {
     int rc = kmeans_screened_step(d_x, n, d, k, d_mu, d_assign, counts, d_sums, d_workspace,
-                                  workspace_bytes, stream, false);
+                                  workspace_bytes, stream, false, mu_out);
     if (rc != DLX_ERR_GENERATION || method == DLX_KMEANS_SCREENED) return rc;
   }
   SmallPlan sp;
   if (small_plan(n, d, k, &sp))
     return kmeans_small_step(d_x, n, d, k, d_mu, d_assign, counts, d_sums, d_workspace,
-                             workspace_bytes, stream);
+                             workspace_bytes, stream, mu_out);
   return kmeans_direct_step(d_x, n, d, k, d_mu, d_assign, counts, d_sums, d_workspace,
-                            workspace_bytes, stream);
+                            workspace_bytes, stream, mu_out);
+}
+
+int dlx_kmeans_step(const double* d_x, int64_t n, int32_t d, int32_t k, const double* d_mu,
+                    int32_t* d_assign, int64_t* d_counts, double* d_sums, void* d_workspace,
+                    size_t workspace_bytes, int method, dlx_stream_t stream) {
+  return kmeans_step_impl(d_x, n, d, k, d_mu, d_assign, d_counts, d_sums, d_workspace, workspace_bytes, method,
+                          stream, nullptr);
+}
+
+int dlx_kmeans_iteration(const double* d_x, int64_t n, int32_t d, int32_t k, double* d_mu,
+                         int32_t* d_assign, int64_t* d_counts, double* d_sums, void* d_workspace,
+                         size_t workspace_bytes, int method, dlx_stream_t stream) {
+  return kmeans_step_impl(d_x, n, d, k, d_mu, d_assign, d_counts, d_sums, d_workspace, workspace_bytes, method,
+                          stream, d_mu);
 }
 
 int dlx_kmeans_update(const int64_t* d_counts, const double* d_sums, int32_t k, int32_t d,

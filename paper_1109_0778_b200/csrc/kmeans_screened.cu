@@ -74,7 +74,7 @@
 namespace dlx {
 
 int kmeans_finalize(const long long* part_counts, const double* part_sums, int parts, int k, int d,
-                    long long* counts, double* sums, cudaStream_t stream);
+                    long long* counts, double* sums, cudaStream_t stream, double* mu_out);
 
 namespace sk {
 
@@ -1022,7 +1022,7 @@ size_t kmeans_screened_workspace_bytes(int64_t n, int d, int k) {
 
 int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double* mu,
                          int32_t* assign, long long* counts, double* sums, void* ws,
-                         size_t ws_bytes, cudaStream_t stream, bool probe_only) {
+                         size_t ws_bytes, cudaStream_t stream, bool probe_only, double* mu_out) {
   DLX_REQUIRE(d >= 2 && d <= sk::kMaxD && (d & 1) == 0 && k >= 1 && k <= sk::kMaxK,
               DLX_ERR_GENERATION,
               "GenerationFailed: screened k-means needs even d <= %d and k <= %d (got d=%d k=%d)",
@@ -1098,7 +1098,7 @@ int kmeans_screened_step(const double* x, int64_t n, int d, int k, const double*
     }
   }
   return kmeans_finalize(w.part_counts, w.part_sums, grid, k, d, counts, sums,
-                         stream);
+                         stream, mu_out);
 }
 
 // pending (re-checked) samples of the last screened step on this workspace

@@ -142,6 +142,25 @@ def kmeans_step(x: torch.Tensor, mu: torch.Tensor, assign: torch.Tensor | None =
     return (assign if want_assign else None), counts, sums
 
 
+def kmeans_iteration(x: torch.Tensor, mu: torch.Tensor, assign: torch.Tensor | None = None,
+                     counts: torch.Tensor | None = None, sums: torch.Tensor | None = None,
+                     method: int = _lib.KMEANS_AUTO, want_assign: bool = True):
+    """kmeans_step + kmeans_update in place on mu, the update fused into the combine launch
+    (dlx_kmeans_iteration): (assign int32 | None, counts, sums); mu holds the new centroids."""
+    L = _lib.load()
+    n, d = x.shape
+    k = mu.shape[0]
+    dev = x.device
+    if want_assign and assign is None:
+        assign = torch.empty(n, dtype=torch.int32, device=dev)
+    counts = counts if counts is not None else torch.empty(k, dtype=_I64, device=dev)
+    sums = sums if sums is not None else torch.empty((k, d), dtype=_F64, device=dev)
+    ws, wsb = _WS.get(L.dlx_kmeans_workspace_bytes(n, d, k), dev)
+    check(L.dlx_kmeans_iteration(_ptr(x), n, d, k, _ptr(mu), _ptr(assign) if want_assign else None,
+                                 _ptr(counts), _ptr(sums), ws, wsb, method, _stream()))
+    return (assign if want_assign else None), counts, sums
+
+
 def kmeans_update(counts: torch.Tensor, sums: torch.Tensor, mu: torch.Tensor | None = None) -> torch.Tensor:
     L = _lib.load()
     k, d = sums.shape

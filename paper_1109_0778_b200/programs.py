@@ -9,10 +9,15 @@ kernel stay device-resident and can be captured once into a CUDA graph and repla
 """
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import _lib
 from . import multiloops as ml
+
+# DLX_KMEANS_UNFUSED_UPDATE=1: separate update launch at one rank (A/B timing only)
+_UNFUSED = os.environ.get("DLX_KMEANS_UNFUSED_UPDATE") == "1"
 
 
 class KMeansProgram:
@@ -34,6 +39,10 @@ class KMeansProgram:
         self.graph = None
 
     def _body(self):
+        if self.comm is None and not _UNFUSED:   # one rank: the update rides on the step's combine launch
+            ml.kmeans_iteration(self.x, self.mu, self.assign, self.counts, self.sums, method=self.method,
+                                want_assign=self.assign is not None)
+            return
         ml.kmeans_step(self.x, self.mu, self.assign, self.counts, self.sums, method=self.method,
                        want_assign=self.assign is not None)
         if self.comm is not None and hasattr(self.comm, "kmeans_update_"):

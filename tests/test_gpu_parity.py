@@ -419,3 +419,20 @@ def test_generation_failed_is_loud(ml):
     y = ml.rng_ints(10, 2, seed=1)
     with pytest.raises(GenerationFailed):
         ml.logreg_grad(x, y, torch.zeros(129 * 4, dtype=torch.float64, device="cuda"))
+
+
+@pytest.mark.parametrize("n,d,k,method", [(0, 16, 8, 0), (4096, 16, 8, 0), (20_000, 64, 64, 0),
+                                          (300_001, 64, 64, 2), (5000, 30, 5, 1), (1003, 16, 8, 2)])
+def test_kmeans_iteration_fused_update(ml, n, d, k, method):
+    """dlx_kmeans_iteration (update fused into the combine launch) equals dlx_kmeans_step +
+    dlx_kmeans_update bit for bit on every path (small, screened, direct, empty input)."""
+    x = dev_units(ml, max(n, k), d, seed=11)[:n] if n else torch.empty((0, d), dtype=torch.float64, device="cuda")
+    mu0 = dev_units(ml, k, d, seed=12)
+    a, c, s = ml.kmeans_step(x, mu0, method=method)
+    mu_ref = ml.kmeans_update(c, s)
+    mu = mu0.clone()
+    a2, c2, s2 = ml.kmeans_iteration(x, mu, method=method)
+    assert torch.equal(c, c2) and torch.equal(s.view(torch.int64), s2.view(torch.int64))
+    assert torch.equal(mu.view(torch.int64), mu_ref.view(torch.int64))
+    if n:
+        assert torch.equal(a, a2)
