@@ -337,7 +337,6 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
         def step():
             kernel_fn()
             rest()
-            ml.axpy_inplace(prog.theta, prog.grad, prog.alpha)
     elif family == "gda":
         x = ml.rng_units(n_local * d, seed=1, first_draw=lo * d, device=dev).view(n_local, d)
         y = ml.rng_ints(n_local, 2, seed=1, first_draw=n * d + lo, device=dev)

@@ -119,6 +119,17 @@ int dlx_logreg_grad(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
 int dlx_axpy_inplace(double* d_theta, const double* d_grad, double alpha, int64_t n,
                      dlx_stream_t stream);
 
+/* ---- bucket row sums: the keyed multi-sum multiloop (GDA pass 1's shape: a count and d
+ *      column sums per bucket, each a reduce predicated on key(i) == b, loops.cpp:111-174) ---- */
+/* For t < nbuckets: d_counts[t] = #{i : keys[i] == h_buckets[t]},
+ * d_sums[t*d + j] = sum over those i of x[i*d + j].  x: n*d row-major fp64, keys: n int64.
+ * One read of x per 4 (d <= 64), 2 (d <= 128) or 1 (d <= 256) buckets; d > 256 raises
+ * DLX_ERR_GENERATION.  Deterministic (fixed-shape per-CTA partials, combine.cu). */
+size_t dlx_bucket_rowsum_workspace_bytes(int64_t n, int32_t d, int32_t nbuckets);
+int dlx_bucket_rowsum(const double* d_x, const int64_t* d_keys, int64_t n, int32_t d,
+                      const int64_t* h_buckets, int32_t nbuckets, int64_t* d_counts, double* d_sums,
+                      void* d_workspace, size_t workspace_bytes, dlx_stream_t stream);
+
 /* ---- GDA ----------------------------------------------------------------- */
 /* pass 1 (1 + 2d predicated reduces keyed on y): n1 = #{y==1}, sum0/sum1 per class. */
 size_t dlx_gda_workspace_bytes(int64_t n, int32_t d);

@@ -3,6 +3,7 @@
 // public headers only (proj/include/stagekit/*.hpp).
 #include "stagekit_dlx.hpp"
 
+#include <cmath>
 #include <json.hpp>
 #include <set>
 
@@ -15,6 +16,15 @@ using json = nlohmann::ordered_json;
 
 namespace {
 
+// Doubles as JSON numbers, except the non-finite ones the reference's constant folding can
+// produce (graph.cpp:211-216: 1.0/0.0 -> inf, 0.0/0.0 -> nan), which JSON cannot hold as
+// numbers: those go as the strings "inf", "-inf", "nan", "-nan" (sign bit kept).
+json double_json(double v) {
+  if (std::isfinite(v)) return json(v);
+  if (std::isnan(v)) return json(std::signbit(v) ? "-nan" : "nan");
+  return json(v > 0 ? "inf" : "-inf");
+}
+
 json expr_json(const Expr& e) {
   json j;
   if (e.is_sym()) {
@@ -22,7 +32,7 @@ json expr_json(const Expr& e) {
   } else if (e.lit.is_int()) {
     j["i"] = e.lit.i();
   } else if (e.lit.is_double()) {
-    j["d"] = e.lit.d();
+    j["d"] = double_json(e.lit.d());
   } else if (e.lit.is_bool()) {
     j["b"] = e.lit.b();
   } else if (e.lit.is_str()) {
@@ -71,7 +81,7 @@ struct Writer {
       for (const Lit& l : st.def.lits) {
         json jl;
         if (l.is_int()) jl["i"] = l.i();
-        else if (l.is_double()) jl["d"] = l.d();
+        else if (l.is_double()) jl["d"] = double_json(l.d());
         else if (l.is_bool()) jl["b"] = l.b();
         js["lits"].push_back(jl);
       }

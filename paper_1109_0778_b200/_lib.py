@@ -89,7 +89,13 @@ _SIGS = {
     "dlx_widen_i32_i64": (_int, [_vp, _i64, _vp, _vp]),
     "dlx_vm_workspace_bytes": (_sz, [_i64]),
     "dlx_vm_run_loop": (_int, [_vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "dlx_bucket_rowsum_workspace_bytes": (_sz, [_i64, _i32, _i32]),
+    "dlx_bucket_rowsum": (_int, [_vp, _vp, _i64, _i32, _vp, _i32, _vp, _vp, _vp, _sz, _vp]),
     "dlx_program_run": (_int, [ctypes.c_char_p, _u64, _int, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p)]),
+    "dlx_program_create": (_int, [ctypes.c_char_p, _sz, ctypes.POINTER(_vp)]),
+    "dlx_program_destroy": (_int, [_vp]),
+    "dlx_program_execute": (_int, [_vp, _vp, _vp]),
+    "dlx_run_result_free": (None, [_vp]),
     "dlx_string_free": (None, [_vp]),
     "dlx_comm_unique_id": (_int, [ctypes.c_char_p]),
     "dlx_comm_init": (_int, [ctypes.POINTER(_vp), ctypes.c_char_p, _int, _int]),
@@ -109,7 +115,7 @@ _SIGS = {
                                   _int, _vp, _dbl, _vp]),
 }
 
-# Every symbol include/dlx.h declares (checked by tests/test_abi.py).
+# Every symbol include/dlx*.h declares (checked by tests/test_abi.py).
 EXPORTED = tuple(_SIGS)
 
 
@@ -140,3 +146,22 @@ def check(rc: int) -> None:
     if rc == DLX_ERR_TRAP:
         raise TrapError(rc, msg)
     raise DlxError(rc, msg)
+
+
+# ---- dlx_program.h structs --------------------------------------------------------------------
+VAL_UNIT, VAL_INT, VAL_DOUBLE, VAL_BOOL, VAL_STR, VAL_VECTOR = range(6)
+EXEC_SERIAL, EXEC_DRYRUN, EXEC_NOCACHE = 1, 2, 4
+
+
+class ProgramInput(ctypes.Structure):
+    _fields_ = [("sym", _i32), ("elem", _i32), ("n", _i64), ("h_data", _vp), ("d_data", _vp)]
+
+
+class ExecOptions(ctypes.Structure):
+    _fields_ = [("seed", _u64), ("ndevices", _i32), ("devices", ctypes.POINTER(_i32)), ("ninputs", _i32),
+                ("inputs", ctypes.POINTER(ProgramInput)), ("flags", _i32)]
+
+
+class RunResult(ctypes.Structure):
+    _fields_ = [("text", _vp), ("report", _vp), ("kind", _i32), ("i", _i64), ("d", _dbl), ("s", _vp),
+                ("vec_elem", _i32), ("vec_len", _i64), ("vec_data", _vp)]

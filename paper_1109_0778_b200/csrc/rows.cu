@@ -152,50 +152,81 @@ logreg_grad_kernel(const double* __restrict__ x, const long long* __restrict__ y
 }
 
 // ---------------------------------------------------------------------------------------
-// GDA pass 1: n1 = #{y == 1}, sum_c[j] = sum_{y_i == c} x_ij  (c in {0, 1})
-template <int M>
+// Bucket row sums — the keyed multi-sum multiloop (GDA pass 1: 1 + 2d reduces predicated on
+// y(i) == c, loops.cpp:111-174): for the pass's KB bucket values b_t,
+//   counts[t] = #{i : key_i == b_t},   sums[t][j] = sum_{key_i == b_t} x_ij.
+// Same streaming skeleton as the gradient: a warp holds 8 rows, lane l columns {2l, 2l+1} + 64m;
+// the key of each row is broadcast from lane r, and every bucket's accumulator adds the element
+// only where the key matches (a select, not a 0/1 weight: 0 * inf would be NaN, and the
+// reference adds nothing for a filtered-out index, loops.hpp:22-24).
+struct Buckets {
+  long long b[8];
+};
+
+template <int M, int KB, bool VEC>
 __global__ void __launch_bounds__(kRowThreads, DLX_ROW_MINB)
-gda_pass1_kernel(const double* __restrict__ x, const long long* __restrict__ y, int64_t n, int d,
-                 double* __restrict__ parts0, double* __restrict__ parts1,
-                 long long* __restrict__ parts_n1) {
+bucket_rowsum_kernel(const double* __restrict__ x, const long long* __restrict__ key, int64_t n, int d,
+                     Buckets bk, int nb, double* __restrict__ parts, long long* __restrict__ parts_cnt) {
   pdl_wait();   // programmatic dependent launch: inputs are final from here on
   pdl_trigger();
   extern __shared__ double red_s[];
-  __shared__ long long n1_s[kRowWarps];
+  __shared__ long long cnt_s[kRowWarps][KB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double a0[M][2], a1[M][2];
+  double acc[KB][M][2];
+  unsigned cnt[KB];   // rows a warp visits: < 2^32
 #pragma unroll
-  for (int m = 0; m < M; ++m) a0[m][0] = a0[m][1] = a1[m][0] = a1[m][1] = 0.0;
-  long long n1 = 0;
+  for (int t = 0; t < KB; ++t) {
+    cnt[t] = 0;
+#pragma unroll
+    for (int m = 0; m < M; ++m) acc[t][m][0] = acc[t][m][1] = 0.0;
+  }
   const int64_t nblk = (n + kRows - 1) / kRows;
   const int64_t W = static_cast<int64_t>(gridDim.x) * kRowWarps;
   for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kRowWarps + warp; blk < nblk; blk += W) {
     const int64_t i0 = blk * kRows;
     double2 v[kRows][M];
-    load_rows<M>(x, i0, n, d, lane, v);
-    // lanes 0..7 fetch the 8 labels, then broadcast
-    const long long ylane = (lane < kRows && i0 + lane < n) ? __ldg(y + i0 + lane) : -1;
+    if (VEC) {
+      load_rows<M>(x, i0, n, d, lane, v);
+    } else {   // odd d: rows are not 16-byte aligned
+#pragma unroll
+      for (int r = 0; r < kRows; ++r)
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const int64_t i = i0 + r;
+          const int j = 64 * m + 2 * lane;
+          v[r][m].x = (i < n && j < d) ? __ldg(x + i * d + j) : 0.0;
+          v[r][m].y = (i < n && j + 1 < d) ? __ldg(x + i * d + j + 1) : 0.0;
+        }
+    }
+    const long long klane = (lane < kRows && i0 + lane < n) ? __ldg(key + i0 + lane) : 0;
+    const bool live = lane < kRows && i0 + lane < n;
 #pragma unroll
     for (int r = 0; r < kRows; ++r) {
-      const long long yv = __shfl_sync(0xffffffffu, ylane, r);
-      const double w1 = yv == 1 ? 1.0 : 0.0, w0 = yv == 0 ? 1.0 : 0.0;
-      n1 += (yv == 1);
+      const long long kv = __shfl_sync(0xffffffffu, klane, r);
+      const bool lv = __shfl_sync(0xffffffffu, live, r);
 #pragma unroll
-      for (int m = 0; m < M; ++m) {
-        a1[m][0] = fma(w1, v[r][m].x, a1[m][0]);
-        a1[m][1] = fma(w1, v[r][m].y, a1[m][1]);
-        a0[m][0] = fma(w0, v[r][m].x, a0[m][0]);
-        a0[m][1] = fma(w0, v[r][m].y, a0[m][1]);
+      for (int t = 0; t < KB; ++t) {
+        const bool hit = lv && kv == bk.b[t];
+        cnt[t] += hit;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          acc[t][m][0] = hit ? acc[t][m][0] + v[r][m].x : acc[t][m][0];
+          acc[t][m][1] = hit ? acc[t][m][1] + v[r][m].y : acc[t][m][1];
+        }
       }
     }
   }
-  if (lane == 0) n1_s[warp] = n1;  // every lane counted the same rows
-  cta_reduce_columns<M>(a0, d, red_s, parts0 + static_cast<size_t>(blockIdx.x) * d);
-  cta_reduce_columns<M>(a1, d, red_s, parts1 + static_cast<size_t>(blockIdx.x) * d);
-  if (threadIdx.x == 0) {
-    long long t = 0;
-    for (int w = 0; w < kRowWarps; ++w) t += n1_s[w];
-    parts_n1[blockIdx.x] = t;
+  if (lane == 0)   // every lane counted the same rows
+#pragma unroll
+    for (int t = 0; t < KB; ++t) cnt_s[warp][t] = cnt[t];
+  // partial record of this CTA: nb (<= KB, the pass's real buckets) rows of d sums, nb counts
+#pragma unroll
+  for (int t = 0; t < KB; ++t)
+    if (t < nb) cta_reduce_columns<M>(acc[t], d, red_s, parts + (static_cast<size_t>(blockIdx.x) * nb + t) * d);
+  if (threadIdx.x < nb) {
+    long long s = 0;
+    for (int w = 0; w < kRowWarps; ++w) s += cnt_s[w][threadIdx.x];
+    parts_cnt[static_cast<size_t>(blockIdx.x) * nb + threadIdx.x] = s;
   }
 }
 
@@ -338,36 +369,97 @@ int dlx_logreg_grad(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
 }
 
 size_t dlx_gda_workspace_bytes(int64_t n, int32_t d) {
-  const size_t p1 = static_cast<size_t>(row_grid(n)) * (2 * d * sizeof(double) + sizeof(long long)) + 1024;
+  const size_t p1 = dlx_bucket_rowsum_workspace_bytes(n, d, 2) + 2 * d * sizeof(double) + 1024;
   const size_t p2 = static_cast<size_t>(std::max(gda2_grid(n), gda_pass2_dmma_grid(n))) * d * d *
                         sizeof(double) + 256;
   return std::max(p1, p2);
 }
 
+}  // extern "C"
+
+namespace {
+// buckets per pass for a row of M column groups (registers: KB * M * 2 accumulators per lane)
+int buckets_per_pass(int M) { return M == 1 ? 4 : M == 2 ? 2 : 1; }
+
+template <int M, int KB>
+int launch_bucket_rowsum(bool vec, dim3 grid, size_t smem, cudaStream_t stream, const double* x,
+                         const long long* key, int64_t n, int d, const Buckets& bk, int nb, double* parts,
+                         long long* pc) {
+  if (vec)
+    DLX_CUDA(launch_pdl(bucket_rowsum_kernel<M, KB, true>, grid, dim3(kRowThreads), smem, stream, x, key, n, d, bk, nb, parts, pc));
+  else
+    DLX_CUDA(launch_pdl(bucket_rowsum_kernel<M, KB, false>, grid, dim3(kRowThreads), smem, stream, x, key, n, d, bk, nb, parts, pc));
+  DLX_LAUNCHED("bucket_rowsum_kernel");
+  return DLX_OK;
+}
+}  // namespace
+
+extern "C" {
+
+size_t dlx_bucket_rowsum_workspace_bytes(int64_t n, int32_t d, int32_t nbuckets) {
+  (void)nbuckets;
+  return static_cast<size_t>(row_grid(n)) * 4 * (static_cast<size_t>(std::max(d, 1)) * sizeof(double) + sizeof(long long)) + 1024;
+}
+
+int dlx_bucket_rowsum(const double* d_x, const int64_t* d_keys, int64_t n, int32_t d,
+                      const int64_t* h_buckets, int32_t nbuckets, int64_t* d_counts, double* d_sums,
+                      void* d_workspace, size_t workspace_bytes, dlx_stream_t stream) {
+  DLX_REQUIRE(n >= 0 && d > 0 && nbuckets >= 0 && (nbuckets == 0 || h_buckets), DLX_ERR_ARG, "bucket_rowsum: bad arguments");
+  DLX_REQUIRE(m_for(d) <= kMaxM, DLX_ERR_GENERATION,
+              "GenerationFailed: bucket row sums need d <= %d (got %d)", 64 * kMaxM, d);
+  const int M = m_for(d) == 3 ? 4 : m_for(d);
+  const int KB = (M == 1 && nbuckets <= 2) ? 2 : buckets_per_pass(M);   // GDA's two classes: KB = 2
+  const int grid = row_grid(n);
+  Carve c(d_workspace);
+  double* parts = c.take<double>(static_cast<size_t>(grid) * KB * d);
+  long long* pc = c.take<long long>(static_cast<size_t>(grid) * KB);
+  DLX_REQUIRE(d_workspace && c.used <= workspace_bytes, DLX_ERR_ARG, "bucket_rowsum: workspace too small");
+  const size_t smem = static_cast<size_t>(kRowWarps) * d * sizeof(double);
+  const long long* key = reinterpret_cast<const long long*>(d_keys);
+  const bool vec = d % 2 == 0;
+  for (int b0 = 0; b0 < nbuckets; b0 += KB) {   // one pass over x per KB buckets
+    Buckets bk;
+    const int nb = std::min(KB, nbuckets - b0);
+    for (int t = 0; t < 8; ++t) bk.b[t] = t < nb ? h_buckets[b0 + t] : (t > 0 ? bk.b[t - 1] : 0);
+    int rc;
+    switch (M) {
+      case 1: rc = KB == 2 ? launch_bucket_rowsum<1, 2>(vec, dim3(grid), smem, stream, d_x, key, n, d, bk, nb, parts, pc)
+                           : launch_bucket_rowsum<1, 4>(vec, dim3(grid), smem, stream, d_x, key, n, d, bk, nb, parts, pc); break;
+      case 2: rc = launch_bucket_rowsum<2, 2>(vec, dim3(grid), smem, stream, d_x, key, n, d, bk, nb, parts, pc); break;
+      default: rc = launch_bucket_rowsum<4, 1>(vec, dim3(grid), smem, stream, d_x, key, n, d, bk, nb, parts, pc); break;
+    }
+    if (rc != DLX_OK) return rc;
+    // padding buckets (t >= nb) repeat the last value and are not written
+    rc = combine_f64_i64(parts, static_cast<long long>(nb) * d, d_sums + static_cast<size_t>(b0) * d, pc, nb,
+                         reinterpret_cast<long long*>(d_counts) + b0, grid, stream);
+    if (rc != DLX_OK) return rc;
+    if (nb < KB) break;
+  }
+  return DLX_OK;
+}
+
 int dlx_gda_pass1(const double* d_x, const int64_t* d_y, int64_t n, int32_t d, int64_t* d_n1,
                   double* d_sum0, double* d_sum1, void* d_workspace, size_t workspace_bytes,
                   dlx_stream_t stream) {
+  // classes 0 and 1 as buckets: sums land contiguously (class 0 then class 1) in a scratch
+  // record carved after the row partials
   DLX_REQUIRE(n >= 0 && d > 0, DLX_ERR_ARG, "gda: bad shape");
   DLX_REQUIRE(d % 2 == 0 && m_for(d) <= kMaxM, DLX_ERR_GENERATION,
               "GenerationFailed: gda needs even d <= %d (got %d)", 64 * kMaxM, d);
-  const int grid = row_grid(n);
+  const size_t need = dlx_bucket_rowsum_workspace_bytes(n, d, 2);
   Carve c(d_workspace);
-  double* p0 = c.take<double>(static_cast<size_t>(grid) * d);
-  double* p1 = c.take<double>(static_cast<size_t>(grid) * d);
-  long long* pn = c.take<long long>(grid);
+  c.take<char>(need);
+  double* sums = c.take<double>(2 * static_cast<size_t>(d));
+  long long* cnt = c.take<long long>(2);
   DLX_REQUIRE(d_workspace && c.used <= workspace_bytes, DLX_ERR_ARG, "gda: workspace too small");
-  const size_t smem = static_cast<size_t>(kRowWarps) * d * sizeof(double);
-  const long long* y = reinterpret_cast<const long long*>(d_y);
-  switch (m_for(d)) {
-    case 1: DLX_CUDA(launch_pdl(gda_pass1_kernel<1>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, p0, p1, pn)); break;
-    case 2: DLX_CUDA(launch_pdl(gda_pass1_kernel<2>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, p0, p1, pn)); break;
-    case 3: DLX_CUDA(launch_pdl(gda_pass1_kernel<3>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, p0, p1, pn)); break;
-    default: DLX_CUDA(launch_pdl(gda_pass1_kernel<4>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, p0, p1, pn)); break;
-  }
-  DLX_LAUNCHED("gda_pass1_kernel");
-  int rc = combine_f64_i64(p0, d, d_sum0, pn, 1, reinterpret_cast<long long*>(d_n1), grid, stream);
-  if (rc == DLX_OK) rc = combine_f64(p1, grid, d, d_sum1, stream);
-  return rc;
+  const int64_t classes[2] = {0, 1};
+  int rc = dlx_bucket_rowsum(d_x, d_y, n, d, classes, 2, reinterpret_cast<int64_t*>(cnt), sums, d_workspace,
+                             need, stream);
+  if (rc != DLX_OK) return rc;
+  DLX_CUDA(cudaMemcpyAsync(d_sum0, sums, d * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+  DLX_CUDA(cudaMemcpyAsync(d_sum1, sums + d, d * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+  DLX_CUDA(cudaMemcpyAsync(d_n1, cnt + 1, sizeof(long long), cudaMemcpyDeviceToDevice, stream));
+  return DLX_OK;
 }
 
 int dlx_gda_means(const int64_t* d_n1, const double* d_sum0, const double* d_sum1,

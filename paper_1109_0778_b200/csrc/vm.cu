@@ -157,7 +157,11 @@ vm_loop_kernel(const dlx_vm_instr* __restrict__ code, dlx_vm_loop L, Reg* __rest
   Reg acc[DLX_VM_MAX_ELEMS];
   long long run[DLX_VM_MAX_ELEMS];   // append: next output slot of this CTA
   for (int e = 0; e < L.nelems; ++e) {
-    acc[e].i = L.elem[e].zero;
+    // start at the combine's identity (-0.0 / 0 / 1): the elem's `zero` is folded exactly once, by
+    // vm_final_kernel, as in `var acc = zero; for i: acc = combine(acc, elem)` (codegen.cpp:367-369)
+    const bool mul = L.elem[e].combine == DLX_VM_COMBINE_MUL;
+    if (L.elem[e].ty == DLX_VM_F64) acc[e].d = mul ? 1.0 : -0.0;   // -0.0 + x == x for every x
+    else acc[e].i = mul ? 1 : 0;
     run[e] = (chunk > 0 && L.elem[e].kind == DLX_VM_APPEND)
                  ? offsets[static_cast<size_t>(blockIdx.x) * DLX_VM_MAX_ELEMS + e] : 0;
   }
@@ -247,15 +251,16 @@ vm_loop_kernel(const dlx_vm_instr* __restrict__ code, dlx_vm_loop L, Reg* __rest
   }
 }
 
-// fold CTA partials in ascending order (the zero is already folded into every partial
-// except the first, so fold partial 0 then combine the rest)
+// fold the elem's zero, then the CTA partials in ascending order (each partial started at the
+// combine's identity, so the zero enters the result exactly once)
 __global__ void vm_final_kernel(const Reg* __restrict__ parts, int nparts, dlx_vm_loop L,
                                 long long* __restrict__ out) {
   const int e = threadIdx.x;
   if (e >= L.nelems || L.elem[e].kind != DLX_VM_REDUCE) return;
   const dlx_vm_elem& el = L.elem[e];
-  Reg v = parts[e];
-  for (int p = 1; p < nparts; ++p) {
+  Reg v;
+  v.i = el.zero;
+  for (int p = 0; p < nparts; ++p) {
     const Reg u = parts[static_cast<size_t>(p) * DLX_VM_MAX_ELEMS + e];
     if (el.ty == DLX_VM_F64) v.d = el.combine == DLX_VM_COMBINE_MUL ? __dmul_rn(v.d, u.d) : __dadd_rn(v.d, u.d);
     else v.i = el.combine == DLX_VM_COMBINE_MUL ? v.i * u.i : v.i + u.i;

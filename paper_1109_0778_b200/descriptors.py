@@ -16,6 +16,7 @@ program at the fixture shape produces exactly the reference-staged program's out
 from __future__ import annotations
 
 import json
+import math
 
 
 class _Builder:
@@ -35,7 +36,12 @@ class _Builder:
 
     @staticmethod
     def d(v: float) -> dict:
-        return {"d": float(v), "t": "Double"}
+        v = float(v)
+        if v != v:   # non-finite literals as strings (JSON numbers cannot hold them)
+            return {"d": "-nan" if math.copysign(1.0, v) < 0 else "nan", "t": "Double"}
+        if v in (math.inf, -math.inf):
+            return {"d": "inf" if v > 0 else "-inf", "t": "Double"}
+        return {"d": v, "t": "Double"}
 
     def sym(self) -> int:
         self.next_sym += 1
@@ -82,9 +88,11 @@ def kmeans_program(n: int, d: int, k: int, iters: int = 1) -> dict:
         j = B.sym()
         douts = [B.sym() for _ in range(k)]
         inner_elems = []
+        row = None
         for c in range(k):
             body: list[int] = []
-            row = B.stmt(body, "Times", "Int", [B.i(d), B.s(i, "Int")])
+            if row is None:   # i*d is CSE'd: defined in the first distance elem, reused by the rest
+                row = B.stmt(body, "Times", "Int", [B.i(d), B.s(i, "Int")])
             xi = B.stmt(body, "Plus", "Int", [B.s(row, "Int"), B.s(j, "Int")])
             xv = B.stmt(body, "VectorApply", "Double", [B.s(x, VD), B.s(xi, "Int")])
             mi = j if c == 0 else B.stmt(body, "Plus", "Int", [B.i(c * d), B.s(j, "Int")])
@@ -122,7 +130,7 @@ def kmeans_program(n: int, d: int, k: int, iters: int = 1) -> dict:
             for jj in range(d):
                 body = []
                 row = B.stmt(body, "Times", "Int", [B.i(d), B.s(i, "Int")])
-                xi = row if jj == 0 else B.stmt(body, "Plus", "Int", [B.s(row, "Int"), B.i(jj)])
+                xi = row if jj == 0 else B.stmt(body, "Plus", "Int", [B.i(jj), B.s(row, "Int")])
                 xv = B.stmt(body, "VectorApply", "Double", [B.s(x, VD), B.s(xi, "Int")])
                 sm = B.sym()
                 sums.append(sm)
@@ -142,6 +150,89 @@ def kmeans_program(n: int, d: int, k: int, iters: int = 1) -> dict:
     for e in range(k * d):
         v = B.stmt(root, "VectorApply", "Double", [B.s(mu, VD), B.i(e)])
         B.stmt(root, "Print", "Unit", [B.s(v, "Double")])
+    B.blocks["0"] = {"stmts": root, "result": {"u": 1, "t": "Unit"}, "bound": []}
+    return {"format": "dlx-program/1", "root": 0, "stmts": B.stmts, "blocks": B.blocks}
+
+
+def gda_program(n: int, d: int) -> dict:
+    """The staged program of integration/stage_programs.cpp::gda(n, d) in the shape the reference's
+    staging + fusion produce (tests/test_descriptors.py compares it statement by statement with
+    the reference-staged gda_n20000_d4 fixture): x = randVector(n*d), y = randIntVector(n, 2);
+    pass 1 = ONE fused loop of a count (y(i) == 1) and 2d column sums keyed on y(i) == 0 / 1
+    (loops.cpp:111-174); the means on the host; pass 2 = ONE fused loop of d*d reduces
+    (x(i*d+a) - mean_{y_i,a}) * (x(i*d+b) - mean_{y_i,b}) with IfThenElse mean selects; every
+    value printed."""
+    B = _Builder()
+    root: list[int] = []
+    VD, VI = "Vector[Double]", "Vector[Int]"
+    x = B.stmt(root, "VectorRand", VD, [B.i(n * d)])
+    y = B.stmt(root, "VectorRandInt", VI, [B.i(n), B.i(2)])
+
+    def key_cond(i, c):
+        cb: list[int] = []
+        yi = B.stmt(cb, "VectorApply", "Int", [B.s(y, VI), B.s(i, "Int")])
+        q = B.stmt(cb, "Eq", "Bool", [B.s(yi, "Int"), B.i(c)])
+        return B.block(cb, B.s(q, "Bool"))
+
+    # pass 1
+    i = B.sym()
+    n1 = B.sym()
+    elems = [B.reduce_elem(n1, "Int", B.block([], B.i(1)), key_cond(i, 1), B.i(0))]
+    s0, s1 = [], []
+    for j in range(d):
+        for c, outl in ((0, s0), (1, s1)):
+            body: list[int] = []
+            row = B.stmt(body, "Times", "Int", [B.i(d), B.s(i, "Int")])
+            ix = row if j == 0 else B.stmt(body, "Plus", "Int", [B.i(j), B.s(row, "Int")])
+            xv = B.stmt(body, "VectorApply", "Double", [B.s(x, VD), B.s(ix, "Int")])
+            o = B.sym()
+            outl.append(o)
+            elems.append(B.reduce_elem(o, "Double", B.block(body, B.s(xv, "Double")), key_cond(i, c), B.d(0.0)))
+    B.stmts[str(n1)] = {"op": "ParallelLoop", "ty": "Int", "args": [],
+                        "loop": {"range": B.i(n), "index": i, "body": B.block([], {"u": 1, "t": "Unit"}, bound=[i]),
+                                 "elems": elems}}
+    root.append(n1)
+    nn1 = B.stmt(root, "ToDouble", "Double", [B.s(n1, "Int")])
+    m0 = B.stmt(root, "Minus", "Int", [B.i(n), B.s(n1, "Int")])
+    nn0 = B.stmt(root, "ToDouble", "Double", [B.s(m0, "Int")])
+    mu0, mu1 = [], []
+    for j in range(d):
+        mu0.append(B.stmt(root, "Divide", "Double", [B.s(s0[j], "Double"), B.s(nn0, "Double")]))
+        mu1.append(B.stmt(root, "Divide", "Double", [B.s(s1[j], "Double"), B.s(nn1, "Double")]))
+    B.stmt(root, "Print", "Unit", [B.s(n1, "Int")])
+    for j in range(d):
+        B.stmt(root, "Print", "Unit", [B.s(mu0[j], "Double")])
+        B.stmt(root, "Print", "Unit", [B.s(mu1[j], "Double")])
+    # pass 2
+    i2 = B.sym()
+    outs, elems = [], []
+    for a in range(d):
+        for b in range(d):
+            body = []
+            yi = B.stmt(body, "VectorApply", "Int", [B.s(y, VI), B.s(i2, "Int")])
+            c1 = B.stmt(body, "Eq", "Bool", [B.s(yi, "Int"), B.i(1)])
+            ma = B.stmt(body, "IfThenElse", "Double", [B.s(c1, "Bool")],
+                        blocks=[B.block([], B.s(mu1[a], "Double")), B.block([], B.s(mu0[a], "Double"))])
+            mb = B.stmt(body, "IfThenElse", "Double", [B.s(c1, "Bool")],
+                        blocks=[B.block([], B.s(mu1[b], "Double")), B.block([], B.s(mu0[b], "Double"))])
+            row = B.stmt(body, "Times", "Int", [B.i(d), B.s(i2, "Int")])
+            ia = row if a == 0 else B.stmt(body, "Plus", "Int", [B.i(a), B.s(row, "Int")])
+            xa = B.stmt(body, "VectorApply", "Double", [B.s(x, VD), B.s(ia, "Int")])
+            da = B.stmt(body, "Minus", "Double", [B.s(xa, "Double"), B.s(ma, "Double")])
+            ib = ia if b == a else row if b == 0 else B.stmt(body, "Plus", "Int", [B.i(b), B.s(row, "Int")])
+            xb = B.stmt(body, "VectorApply", "Double", [B.s(x, VD), B.s(ib, "Int")])
+            db = B.stmt(body, "Minus", "Double", [B.s(xb, "Double"), B.s(mb, "Double")])
+            pr = B.stmt(body, "Times", "Double", [B.s(da, "Double"), B.s(db, "Double")])
+            o = B.sym()
+            outs.append(o)
+            elems.append(B.reduce_elem(o, "Double", B.block(body, B.s(pr, "Double")), -1, B.d(0.0)))
+    loop2 = outs[0]
+    B.stmts[str(loop2)] = {"op": "ParallelLoop", "ty": "Double", "args": [],
+                           "loop": {"range": B.i(n), "index": i2, "body": B.block([], {"u": 1, "t": "Unit"}, bound=[i2]),
+                                    "elems": elems}}
+    root.append(loop2)
+    for o in outs:
+        B.stmt(root, "Print", "Unit", [B.s(o, "Double")])
     B.blocks["0"] = {"stmts": root, "result": {"u": 1, "t": "Unit"}, "bound": []}
     return {"format": "dlx-program/1", "root": 0, "stmts": B.stmts, "blocks": B.blocks}
 

@@ -422,7 +422,8 @@ def test_generation_failed_is_loud(ml):
 
 
 @pytest.mark.parametrize("n,d,k,method", [(0, 16, 8, 0), (4096, 16, 8, 0), (20_000, 64, 64, 0),
-                                          (300_001, 64, 64, 2), (5000, 30, 5, 1), (1003, 16, 8, 2)])
+                                          (300_001, 64, 64, 2), (5000, 30, 5, 1), (3000, 66, 9, 1),
+                                          (2000, 16, 80, 1), (1003, 16, 8, 2)])
 def test_kmeans_iteration_fused_update(ml, n, d, k, method):
     """dlx_kmeans_iteration (update fused into the combine launch) equals dlx_kmeans_step +
     dlx_kmeans_update bit for bit on every path (small, screened, direct, empty input)."""

@@ -113,7 +113,7 @@ def test_staged_program_on_b200(path):
     if name.startswith("groupby"):
         assert fams == ["groupby"]
     if name.startswith("gda"):
-        assert "gda_scatter" in fams
+        assert fams == ["bucket_rows", "gda_scatter"]
 
 
 @pytest.mark.gpu
@@ -175,7 +175,7 @@ EXPECTED_FAMILIES = {
     "axpy_n100000": ["generic", "generic"],
     "count_gt_n100000": ["generic"],
     "find_count_n100000": ["generic", "generic"],
-    "gda_n20000_d4": ["generic", "gda_scatter"],
+    "gda_n20000_d4": ["bucket_rows", "gda_scatter"],
     "groupby_n100000_k16": ["groupby"],
     "kmeans_n4096_d16_k8_it2": ["kmeans", "kmeans"],
     "kmeans_n65536_d16_k8_it1": ["kmeans"],
