@@ -13,6 +13,7 @@
 // The result of a lowering (LoopPlan) is cached per loop statement in the program, so a
 // program executed again (or a While body) skips the symbolic evaluation.
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <tuple>
 
@@ -362,7 +363,7 @@ bool Executor::match_kmeans(const Stmt& s, int64_t n, std::vector<LElem>& els, L
   // exactly mu(c*d + j) = sum_cj / toDouble(count_c)
   p.upd_vec = -1;
   p.skip.clear();
-  p.unbound.clear();
+  p.sums_group_only = false;
   auto g = P.update_after.find(s.sym);
   if (g != P.update_after.end() && static_cast<int64_t>(g->second.entries.size()) == k * d) {
     std::vector<uint8_t> seen(k * d, 0);
@@ -380,8 +381,15 @@ bool Executor::match_kmeans(const Stmt& s, int64_t n, std::vector<LElem>& els, L
     if (ok) {
       p.upd_vec = g->second.vec_sym;
       p.skip = g->second.stmts;
-      for (const UpdateGroup::Entry& en : g->second.entries)
-        if (P.uses[en.sum_sym] == 1) p.unbound.push_back(en.sum_sym);   // read only by its divide
+      std::unordered_map<int, int> group_reads;   // sum -> reads by the group's divides
+      for (const UpdateGroup::Entry& en : g->second.entries) ++group_reads[en.sum_sym];
+      size_t only = 0;
+      for (LoopPlan::Out& o : p.outs) {
+        auto it = group_reads.find(o.sym);
+        o.group_only = it != group_reads.end() && P.uses[o.sym] == it->second;
+        only += o.group_only;
+      }
+      p.sums_group_only = only == static_cast<size_t>(k * d);
     } else if (g_run->debug) {
       fprintf(stderr, "[dlx program] update group after x%d does not cover mu(c*d+j) = sum/count\n", s.sym);
     }
@@ -849,13 +857,37 @@ void Executor::run_loop(const Stmt& s) {
   flush_mirrors();
   // next loop stream, ordered after everything the main stream has enqueued so far (RNG fills,
   // uploads, mirror flushes: the loop's inputs)
-  lst_ = res_->loop[launches_++ % kLoopStreams];
+  static const int nstreams = getenv("DLX_PROGRAM_STREAMS") ? std::max(1, std::min(kLoopStreams, atoi(getenv("DLX_PROGRAM_STREAMS")))) : kLoopStreams;
+  lst_ = res_->loop[launches_++ % nstreams];
   cudaEvent_t ev = get_event();
   ckc(cudaEventRecord(ev, st_), "cudaEventRecord");
   ckc(cudaStreamWaitEvent(lst_, ev, 0), "cudaStreamWaitEvent");
   res_->events.push_back(ev);
   const size_t inflight = pending_.size();
+  const auto t0 = std::chrono::steady_clock::now();
+  cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+  if (g_run->profile) {   // device time of the loop's launches (from its stream's start)
+    cudaEventCreate(&pe0);
+    cudaEventCreate(&pe1);
+    cudaEventRecord(pe0, lst_);
+  }
   launch(s, *plan, n, vecs, rep);
+  if (g_run->profile) {
+    cudaEventRecord(pe1, lst_);
+    fprintf(stderr, "[dlx profile] @%.2f ms x%d launch %.1f us (in flight %zu)\n", g_run->ms(), s.sym,
+            std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count(), inflight);
+    pending_.push_back(Pending{get_event(), [pe0, pe1, sym = s.sym, t0ev = prof_t0_] {
+                                 float ms = 0, a = 0, b = 0;
+                                 cudaEventElapsedTime(&ms, pe0, pe1);
+                                 cudaEventElapsedTime(&a, t0ev, pe0);
+                                 cudaEventElapsedTime(&b, t0ev, pe1);
+                                 fprintf(stderr, "[dlx profile] x%d device %.1f us [%.1f, %.1f] us from run start\n", sym,
+                                         ms * 1e3, a * 1e3, b * 1e3);
+                                 cudaEventDestroy(pe0);
+                                 cudaEventDestroy(pe1);
+                               }});
+    cudaEventRecord(pending_.back().ev, lst_);
+  }
   rep["stream"] = static_cast<int>((launches_ - 1) % kLoopStreams);
   rep["in_flight"] = static_cast<int>(inflight);   // loops it may overlap
   report.push_back(rep);
@@ -913,7 +945,7 @@ void Executor::launch_kmeans(const Stmt& s, LoopPlan& p, int64_t n, std::vector<
     fence_on(lst_);   // WAR: loops in flight may still read U
     if (U->wev) cudaStreamWaitEvent(lst_, U->wev, 0);
   }
-  const bool copy_sums = !U || p.unbound.size() < static_cast<size_t>(k) * d;
+  const bool copy_sums = !U || !p.sums_group_only;
   const size_t wsb = dlx_kmeans_workspace_bytes(n, d, k);
   void* ws = dalloc(wsb);
   VecP assign = new_vec(n, Ty::Int, lst_, false, /*i32=*/true);
@@ -940,20 +972,14 @@ void Executor::launch_kmeans(const Stmt& s, LoopPlan& p, int64_t n, std::vector<
   cudaEvent_t ev = complete_loop({}, nullptr);
   assign->wev = ev;
   for (const LoopPlan::Out& o : p.outs) {
-    if (o.src == 1) {
-      bind(o.sym, Val{assign});
-    } else if (!U || !copy_sums) {
-      if (!(U && std::find(p.unbound.begin(), p.unbound.end(), o.sym) != p.unbound.end()))
-        bind(o.sym, Val{make_lazy(hres + o.ix, o.ty, 8)});
-    } else {
-      bind(o.sym, Val{make_lazy(hres + o.ix, o.ty, 8)});
-    }
+    if (o.src == 1) bind(o.sym, Val{assign});
+    else if (!(U && o.group_only)) bind(o.sym, Val{make_lazy(hres + o.ix, o.ty, 8)});
   }
   if (U) {   // the group's k*d host statements ran on the device
     U->wev = ev;
     U->host_valid = false;
     U->page_valid = false;
-    for (int q : p.skip) skip_[q] = 1;
+    for (int q : p.skip) mark_skip(q);
   }
   rep["update"] = U ? "device" : p.upd_vec >= 0 ? "host" : "none";
 }

@@ -23,6 +23,7 @@
 #include "program_exec.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -106,11 +107,25 @@ std::string format_val(const Val& x) {
 }
 
 // ---- executor: construction, pending loops, lazies -------------------------------------------
+static std::shared_ptr<Scratch> take_scratch(const Program& p) {
+  {
+    std::lock_guard<std::mutex> lk(p.scratch_mu);
+    if (!p.scratch.empty()) {
+      auto s = std::static_pointer_cast<Scratch>(p.scratch.back());
+      p.scratch.pop_back();
+      return s;
+    }
+  }
+  auto s = std::make_shared<Scratch>();
+  s->env.resize(p.max_sym + 1);
+  s->bound.assign(p.max_sym + 1, 0);
+  s->skip.assign(p.max_sym + 1, 0);
+  return s;
+}
+
 Executor::Executor(const Program& p, const ExecOpts& o, cudaStream_t st, DeviceRes* res)
-    : P(p), opts_(o), st_(st), res_(res), lst_(st) {
-  env_.resize(P.max_sym + 1);
-  bound_.assign(P.max_sym + 1, 0);
-  skip_.assign(P.max_sym + 1, 0);
+    : P(p), opts_(o), st_(st), res_(res), lst_(st), sc_(take_scratch(p)), env_(sc_->env), bound_(sc_->bound),
+      skip_(sc_->skip) {
   fence_ = [this] { fence(); };
 }
 
@@ -119,9 +134,21 @@ Executor::~Executor() {
     join_all();
   } catch (...) {
   }
+  for (int s : sc_->touched) {   // release this run's values (device vectors are freed here)
+    env_[s] = Val{};
+    bound_[s] = 0;
+    skip_[s] = 0;
+  }
+  sc_->touched.clear();
+  std::lock_guard<std::mutex> lk(P.scratch_mu);
+  if (P.scratch.size() < 2) P.scratch.push_back(sc_);
 }
 
 Val Executor::run() {
+  if (g_run->profile && !g_run->dry) {
+    cudaEventCreate(&prof_t0_);
+    cudaEventRecord(prof_t0_, st_);
+  }
   Val v = exec_block(P.root);
   join_all();
   return v;
@@ -169,6 +196,16 @@ void Executor::fence_on(cudaStream_t s) {
 
 void Executor::join_all() {
   if (pending_.empty() && unresolved_.empty() && !main_async_) return;
+  const auto t0 = std::chrono::steady_clock::now();
+  struct Prof {
+    std::chrono::steady_clock::time_point t0;
+    size_t n;
+    ~Prof() {
+      if (g_run && g_run->profile)
+        fprintf(stderr, "[dlx profile] @%.2f ms join of %zu loops %.1f us\n", g_run->ms(), n,
+                std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+    }
+  } prof{t0, pending_.size()};
   std::vector<Pending> pend;
   pend.swap(pending_);
   cudaError_t err = cudaSuccess;
@@ -204,6 +241,8 @@ void Executor::join_all() {
   for (auto& w : vecs_)
     if (auto v = w.lock()) {
       v->wev = nullptr;   // every device write is complete
+      v->snap = nullptr;  // (the pinned staging is reset below)
+      v->snap_of = nullptr;
       vecs_[live++] = w;
     }
   vecs_.resize(live);
@@ -423,11 +462,14 @@ Val Executor::exec_block(int b) {
     }
     const Stmt& st = P.stmts[s];
     try {
+      if (!g_run->dry && !P.copy_runs.empty()) {
+        auto cr = P.copy_runs.find(s);
+        if (cr != P.copy_runs.end() && copy_run(cr->second)) continue;   // the run is now skipped
+      }
       if (st.op == Op::ParallelLoop) {
         run_loop(st);   // binds every live elem's `out` (elems[0].out is the statement's own sym)
       } else {
-        env_[s] = exec_stmt(st);
-        bound_[s] = 1;
+        bind(s, exec_stmt(st));
       }
     } catch (...) {
       join_all();   // a trap of an earlier loop still in flight takes precedence
@@ -435,6 +477,41 @@ Val Executor::exec_block(int b) {
     }
   }
   return atomv(bl.result);
+}
+
+// A CopyRun as device copies on the main stream (ordered after its producers and before the
+// next loop launch like any host write); false -> run its statements on the host (a trap, a
+// type mismatch, int32 storage: the host path reports exactly what the reference would).
+bool Executor::copy_run(const CopyRun& run) {
+  if (!bound_[run.x_sym] || !bound_[run.v_sym]) return false;
+  const Val& xv = env_[run.x_sym];
+  const Val& vv = env_[run.v_sym];
+  if (!xv.is_vec() || !vv.is_vec()) return false;
+  const VecP& X = xv.vec();
+  const VecP& V = vv.vec();
+  if (X == V || X->elem != V->elem || X->i32 || V->i32) return false;
+  for (auto [e1, e2] : run.pairs)
+    if (e1 < 0 || e1 >= X->n || e2 < 0 || e2 >= V->n) return false;
+  flush_mirrors();   // V's earlier host writes land first
+  fence();           // WAR: loops in flight may read V
+  if (X->wev) cudaStreamWaitEvent(st_, X->wev, 0);
+  if (V->wev) cudaStreamWaitEvent(st_, V->wev, 0);
+  const size_t es = X->esize();
+  size_t q = 0;
+  while (q < run.pairs.size()) {   // coalesce runs of consecutive (e1, e2)
+    size_t r = q + 1;
+    while (r < run.pairs.size() && run.pairs[r].first == run.pairs[r - 1].first + 1 &&
+           run.pairs[r].second == run.pairs[r - 1].second + 1)
+      ++r;
+    ckc(cudaMemcpyAsync(static_cast<unsigned char*>(V->p) + run.pairs[q].second * es,
+                        static_cast<const unsigned char*>(X->p) + run.pairs[q].first * es, (r - q) * es,
+                        cudaMemcpyDeviceToDevice, st_), "d2d copy run");
+    q = r;
+  }
+  V->host_valid = false;
+  V->page_valid = false;
+  for (size_t t = 1; t < run.stmts.size(); ++t) mark_skip(run.stmts[t]);
+  return true;
 }
 
 static int64_t wrap(uint64_t v) { return static_cast<int64_t>(v); }
@@ -579,7 +656,19 @@ Val Executor::exec_stmt(const Stmt& s) {
       const int64_t i = atom(s.args[1]).i();
       if (i < 0 || i >= v->n) trap("TrapIndexOutOfBounds: index " + std::to_string(i));
       if (v->wev && !g_run->dry && P.print_only[s.sym]) {
-        // a printed element of a vector a loop is still writing: read it asynchronously
+        // a printed element of a vector a loop is still writing: read it asynchronously (small
+        // vectors: one snapshot of the whole vector serves every such read until the next join)
+        if (v->mirrored()) {
+          if (!v->snap || v->snap_of != v->wev) {
+            cudaStreamWaitEvent(st_, v->wev, 0);
+            auto* stage = static_cast<unsigned char*>(res_->pin.get(std::max<size_t>(1, v->n * v->esize())));
+            ckc(cudaMemcpyAsync(stage, v->p, v->n * v->esize(), cudaMemcpyDeviceToHost, st_), "d2h");
+            v->snap = stage;
+            v->snap_of = v->wev;
+            main_async_ = true;
+          }
+          return Val{make_lazy(v->snap + i * v->esize(), v->elem, static_cast<int>(v->esize()))};
+        }
         cudaStreamWaitEvent(st_, v->wev, 0);
         auto* stage = res_->pin.get(8);
         ckc(cudaMemcpyAsync(stage, static_cast<unsigned char*>(v->p) + i * v->esize(), v->esize(), cudaMemcpyDeviceToHost,
@@ -654,6 +743,9 @@ RunOut execute(const Program& p, const ExecOpts& o) {
   ctx.debug = getenv("DLX_PROGRAM_DEBUG") != nullptr;
   ctx.serial = (o.flags & DLX_EXEC_SERIAL) || getenv("DLX_PROGRAM_SERIAL") != nullptr;
   ctx.nocache = (o.flags & DLX_EXEC_NOCACHE) != 0;
+  ctx.profile = getenv("DLX_PROGRAM_PROFILE") != nullptr;
+  ctx.t0 = std::chrono::steady_clock::now();
+  const auto t_run = std::chrono::steady_clock::now();
   if (o.ndevices > 1) gen_fail("multi-device execution needs the sharded executor (ndevices > 1)");
   const int device = (o.ndevices >= 1 && o.devices) ? o.devices[0] : 0;
   DeviceRes* res = nullptr;
@@ -675,6 +767,7 @@ RunOut execute(const Program& p, const ExecOpts& o) {
     Executor ex(p, o, st, ctx.dry ? &dry_res : res);
     ctx.fence = ctx.dry ? nullptr : &ex.fence_;
     Val v = ex.run();
+    if (ctx.profile) fprintf(stderr, "[dlx profile] @%.2f ms program done\n", ctx.ms());
     out.text = ex.output();
     out.report = ex.report.dump();
     v = ex.force(v);
@@ -691,8 +784,13 @@ RunOut execute(const Program& p, const ExecOpts& o) {
     }
     out.result = v;
     ex.join_all();
+    if (ctx.profile) fprintf(stderr, "[dlx profile] @%.2f ms results out\n", ctx.ms());
   }
+  if (ctx.profile) fprintf(stderr, "[dlx profile] @%.2f ms executor released\n", ctx.ms());
   if (!ctx.dry) ckc(cudaStreamSynchronize(st), "sync");
+  if (ctx.profile)
+    fprintf(stderr, "[dlx profile] run %.1f us\n",
+            std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_run).count());
   return out;
 }
 

@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <functional>
 #include <map>
 #include <memory>
@@ -34,8 +35,11 @@ struct RunCtx {
   bool debug = false;    // DLX_PROGRAM_DEBUG=1: why a specialised family did not match
   bool serial = false;   // complete every loop before the next statement
   bool nocache = false;
+  bool profile = false;  // DLX_PROGRAM_PROFILE=1: host time of launches, joins and the run
   cudaStream_t main = nullptr;
   std::function<void()>* fence = nullptr;
+  std::chrono::steady_clock::time_point t0;   // run start (profile timestamps)
+  double ms() const { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); }
 };
 extern thread_local RunCtx* g_run;
 
@@ -58,6 +62,10 @@ struct DevVec {
   int64_t page_lo = 0;
   bool page_valid = false;
   int64_t dirty_lo = INT64_MAX, dirty_hi = -1;   // [lo, hi) newer on the host than on the device
+  // small vectors a loop is still writing: one asynchronous copy of the whole vector into pinned
+  // staging serves every printed element read until the next join (device layout)
+  const unsigned char* snap = nullptr;
+  cudaEvent_t snap_of = nullptr;   // the write (wev) the snapshot follows
   ~DevVec();
   size_t esize() const { return elem == Ty::Bool ? 1 : i32 ? 4 : 8; }   // device element bytes
   size_t hsize() const { return elem == Ty::Bool ? 1 : 8; }            // host element bytes
@@ -149,13 +157,14 @@ struct LoopPlan {
     int src;        // 0: scalar slot ix of the staged result record; 1: the collect vector
     int64_t ix;
     Ty ty;
+    bool group_only = false;   // read only by the update group (not copied back when it is fused)
   };
   std::vector<Out> outs;
   int64_t nres = 0;                             // 64-bit slots in the staged result record
   // k-means: the update group run on the device
   int upd_vec = -1;                             // V's symbol (-1: none)
   std::vector<int> skip;                        // the group's host statements
-  std::vector<int> unbound;                     // outputs only the group reads (not copied back)
+  bool sums_group_only = false;                 // every sum is read only by the group
   // bucket counts / bucket rows: bucket values
   std::vector<int64_t> buckets;
   // GDA scatter: per column the class-mean sources (symbol, or -1 and a literal)
@@ -176,6 +185,14 @@ struct MatchCtx {   // what a lowering depends on (recorded into the LoopPlan)
   std::vector<int> deps;
   int slot(const SEP& vn);
   void bake(const SEP& s);
+};
+
+// A per-symbol environment (values, bound / skip flags), pooled in the Program across runs;
+// `touched` lists the symbols to clear when it goes back.
+struct Scratch {
+  std::vector<Val> env;
+  std::vector<uint8_t> bound, skip;
+  std::vector<int> touched;
 };
 
 // ---- the executor ----------------------------------------------------------------------------
@@ -199,14 +216,16 @@ class Executor {
   DeviceRes* res_;
   cudaStream_t lst_;   // stream of the loop being launched
   int64_t launches_ = 0;
-  std::vector<Val> env_;
-  std::vector<uint8_t> bound_;
-  std::vector<uint8_t> skip_;
+  std::shared_ptr<Scratch> sc_;
+  std::vector<Val>& env_;
+  std::vector<uint8_t>& bound_;
+  std::vector<uint8_t>& skip_;
   std::vector<std::weak_ptr<DevVec>> vecs_;   // every vector of this run
   std::vector<std::string> lines_;            // printed output
   std::vector<std::pair<size_t, LazyP>> prints_;   // lines waiting for a loop result
   std::vector<LazyP> unresolved_;
   bool main_async_ = false;                   // main-stream work reads pinned staging
+  cudaEvent_t prof_t0_ = nullptr;             // DLX_PROGRAM_PROFILE: run start on the main stream
 
   struct Pending {
     cudaEvent_t ev;                 // recorded on the loop's stream after its result copies
@@ -222,7 +241,12 @@ class Executor {
   LazyP make_lazy(const void* src, Ty ty, int esz);
   void bind(int sym, Val v) {
     env_[sym] = std::move(v);
+    if (!bound_[sym]) sc_->touched.push_back(sym);
     bound_[sym] = 1;
+  }
+  void mark_skip(int sym) {
+    skip_[sym] = 1;
+    sc_->touched.push_back(sym);
   }
 
   Val atomv(const Atom& a);                     // may be a Lazy
@@ -235,6 +259,7 @@ class Executor {
   Val vec_get(const VecP& v, int64_t i);
   void vec_set(const VecP& v, int64_t i, const Val& x);
   Val exec_block(int b);
+  bool copy_run(const CopyRun& run);
   Val exec_stmt(const Stmt& s);
   Val scalar(Op op, const Val& x, const Val& y);
 

@@ -138,6 +138,39 @@ struct Analyzer {
     }
   }
 
+  void find_copy_runs() {
+    for (size_t b = 0; b < P.blocks.size(); ++b) {
+      if (!P.has_block[b]) continue;
+      const std::vector<int>& ss = P.blocks[b].stmts;
+      size_t q = 0;
+      while (q + 1 < ss.size()) {
+        CopyRun run;
+        size_t r = q;
+        while (r + 1 < ss.size()) {
+          const Stmt& a = P.stmts[ss[r]];
+          const Stmt& u = P.stmts[ss[r + 1]];
+          const bool pair = a.op == Op::VectorApply && a.args.size() == 2 && a.args[0].k == Atom::Sym &&
+                            a.args[1].k == Atom::Int && u.op == Op::VectorUpdate && u.args.size() == 3 &&
+                            u.args[0].k == Atom::Sym && u.args[1].k == Atom::Int && u.args[2].k == Atom::Sym &&
+                            u.args[2].sym == a.sym && P.uses[a.sym] == 1 && a.args[0].sym != u.args[0].sym;
+          if (!pair || (run.x_sym >= 0 && (run.x_sym != a.args[0].sym || run.v_sym != u.args[0].sym))) break;
+          run.x_sym = a.args[0].sym;
+          run.v_sym = u.args[0].sym;
+          run.pairs.emplace_back(a.args[1].i, u.args[1].i);
+          run.stmts.push_back(a.sym);
+          run.stmts.push_back(u.sym);
+          r += 2;
+        }
+        if (run.pairs.size() >= 2) {
+          P.copy_runs[ss[q]] = std::move(run);
+          q = r;
+        } else {
+          ++q;
+        }
+      }
+    }
+  }
+
   void find_update_groups() {
     for (size_t b = 0; b < P.blocks.size(); ++b) {
       if (!P.has_block[b]) continue;
@@ -309,6 +342,7 @@ std::shared_ptr<Program> parse_program(const char* text, size_t len) {
   Analyzer an{p, {}};
   an.count_uses();
   an.find_update_groups();
+  an.find_copy_runs();
   return pp;
 }
 

@@ -99,6 +99,16 @@ struct UpdateGroup {
   std::vector<int> stmts;            // every ToDouble / Divide / VectorUpdate of the group
 };
 
+// A run of adjacent host statement pairs  a = VectorApply(X, e1);  VectorUpdate(V, e2, a)  (a read
+// nowhere else) — the k-means centroid initialisation `mu.update(e, x.at(e))` of the staged
+// programs.  Executed as device-to-device copies (contiguous segments coalesced) instead of
+// 2 * len host statements that would each wait for the device.
+struct CopyRun {
+  int x_sym = -1, v_sym = -1;
+  std::vector<std::pair<int64_t, int64_t>> pairs;   // (e1, e2) in program order
+  std::vector<int> stmts;                           // every statement of the run
+};
+
 struct LoopPlan;   // a cached lowering (program.cpp)
 
 struct Program {
@@ -111,9 +121,14 @@ struct Program {
   std::vector<int32_t> uses;         // references to each sym (args, results, ranges, zeros)
   std::vector<uint8_t> print_only;   // every use of the sym is a Print argument
   std::unordered_map<int, UpdateGroup> update_after;   // loop stmt sym -> its update group
+  std::unordered_map<int, CopyRun> copy_runs;          // first statement of the run -> run
   // lowering cache (loop stmt sym -> plan), filled by executions of this program
   mutable std::mutex plan_mu;
   mutable std::unordered_map<int, std::shared_ptr<LoopPlan>> plans;
+  // per-symbol environments of finished executions, reused by the next ones (sizing and
+  // clearing a max_sym-long environment per run is ~ms for a 10-iteration C4 program)
+  mutable std::mutex scratch_mu;
+  mutable std::vector<std::shared_ptr<void>> scratch;
 
   const Stmt& stmt(int s) const {
     if (s < 0 || s > max_sym || stmts[s].sym < 0) throw Fail(DLX_ERR_ARG, "malformed descriptor: no statement x" + std::to_string(s));
