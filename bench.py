@@ -146,11 +146,12 @@ def run_reference(args, family, p, metric, unit):
     import oracle as O
     threads = O.threads()
     t_steps = []
+    # every step is the FULL workload (no sampling, no scaling): same config as the GPU arm
     if family == "kmeans":
-        n_s = min(p["n"], int(os.environ.get("DLX_REF_SAMPLE", 1 << 21)))
+        n_s = p["n"]
         x = O.rng_units(1, 0, n_s * p["d"]).reshape(n_s, p["d"])
         mu = x[: p["k"]].copy()
-        scale = p["n"] / n_s
+        scale = 1.0
         for s in range(args.warmup + args.steps):
             t0 = time.perf_counter()
             a, c, sm = O.kmeans_step(x, p["k"], mu, workers=threads, chunks=4 * threads)
@@ -158,25 +159,25 @@ def run_reference(args, family, p, metric, unit):
             dt = time.perf_counter() - t0
             if s >= args.warmup:
                 t_steps.append(dt * scale)
-        sample = f"{n_s} of {p['n']} samples per step (d={p['d']}, k={p['k']}), time scaled by N/n_sample"
+        sample = f"full workload: every step is one k-means iteration over all {n_s} samples (d={p['d']}, k={p['k']})"
     elif family == "logreg":
-        n_s = min(p["n"], 1 << 21)
+        n_s = p["n"]
         x = O.rng_units(1, 0, n_s * p["d"]).reshape(n_s, p["d"])
         y = O.rng_ints(1, n_s * p["d"], n_s, 2)
         th = np.zeros(p["d"])
-        scale = p["n"] / n_s
+        scale = 1.0
         for s in range(args.warmup + args.steps):
             t0 = time.perf_counter()
             th = th - (1.0 / p["n"]) * O.logreg_grad(x, y, th, workers=threads, chunks=4 * threads)
             dt = time.perf_counter() - t0
             if s >= args.warmup:
                 t_steps.append(dt * scale)
-        sample = f"{n_s} of {p['n']} samples per step, scaled"
+        sample = f"full workload: every step is one BGD iteration over all {n_s} samples"
     elif family == "gda":
-        n_s = min(p["n"], 1 << 19)
+        n_s = p["n"]
         x = O.rng_units(1, 0, n_s * p["d"]).reshape(n_s, p["d"])
         y = O.rng_ints(1, n_s * p["d"], n_s, 2)
-        scale = p["n"] / n_s
+        scale = 1.0
         for s in range(args.warmup + args.steps):
             t0 = time.perf_counter()
             n1, s0, s1 = O.gda_pass1(x, y, workers=threads, chunks=4 * threads)
@@ -184,18 +185,18 @@ def run_reference(args, family, p, metric, unit):
             dt = time.perf_counter() - t0
             if s >= args.warmup:
                 t_steps.append(dt * scale)
-        sample = f"{n_s} of {p['n']} samples per step, scaled"
+        sample = f"full workload: every step is one GDA fit (pass 1 + pass 2) over all {n_s} samples"
     else:
-        n_s = min(p["n"], 1 << 27)
+        n_s = p["n"]
         keys = O.rng_ints(1, 0, n_s, p["K"])
-        scale = p["n"] / n_s
+        scale = 1.0
         for s in range(args.warmup + args.steps):
             t0 = time.perf_counter()
             O.groupby_count(keys, p["K"], workers=threads, chunks=4 * threads)
             dt = time.perf_counter() - t0
             if s >= args.warmup:
                 t_steps.append(dt * scale)
-        sample = f"{n_s} of {p['n']} keys per step, scaled"
+        sample = f"full workload: every step is one bucket-count pass over all {n_s} keys"
     t = sum(t_steps) / len(t_steps)
     value = 1.0 / t
     return {
@@ -212,7 +213,7 @@ def run_reference(args, family, p, metric, unit):
 def cpu_baseline_kmeans(p, budget_s=15.0):
     import oracle as O
     threads = O.threads()
-    n_s = min(p["n"], 1 << 20)
+    n_s = p["n"]
     x = O.rng_units(1, 0, n_s * p["d"]).reshape(n_s, p["d"])
     mu = x[: p["k"]].copy()
     times = []
@@ -221,10 +222,10 @@ def cpu_baseline_kmeans(p, budget_s=15.0):
         t0 = time.perf_counter()
         O.kmeans_step(x, p["k"], mu, workers=threads, chunks=4 * threads)
         times.append(time.perf_counter() - t0)
-    t = min(times) * p["n"] / n_s
+    t = min(times)
     return {"value": 1.0 / t, "unit": "it/s", "cores": threads, "kind": "port",
-            "sample": f"1 k-means iteration over {n_s} of {p['n']} samples (d={p['d']}, k={p['k']}), "
-                      f"executeDEG chunking {4 * threads} chunks, time scaled by N/n_sample"}
+            "sample": f"best of {len(times)} k-means iterations over all {n_s} samples (d={p['d']}, k={p['k']}), "
+                      f"executeDEG chunking {4 * threads} chunks; not scaled"}
 
 
 def cpu_baseline_generic(family, p):
@@ -232,30 +233,28 @@ def cpu_baseline_generic(family, p):
 
     import oracle as O
     threads = O.threads()
+    n_s = p["n"]   # the full workload, not scaled
     if family == "logreg":
-        n_s = min(p["n"], 1 << 20)
         x = O.rng_units(1, 0, n_s * p["d"]).reshape(n_s, p["d"])
         y = O.rng_ints(1, n_s * p["d"], n_s, 2)
         t0 = time.perf_counter()
         O.logreg_grad(x, y, np.zeros(p["d"]), workers=threads, chunks=4 * threads)
-        t = (time.perf_counter() - t0) * p["n"] / n_s
-        unit, smp = "it/s", f"1 gradient over {n_s} samples, scaled"
+        t = time.perf_counter() - t0
+        unit, smp = "it/s", f"1 gradient over all {n_s} samples"
     elif family == "gda":
-        n_s = min(p["n"], 1 << 18)
         x = O.rng_units(1, 0, n_s * p["d"]).reshape(n_s, p["d"])
         y = O.rng_ints(1, n_s * p["d"], n_s, 2)
         t0 = time.perf_counter()
         n1, s0, s1 = O.gda_pass1(x, y, workers=threads, chunks=4 * threads)
         O.gda_pass2(x, y, s0 / (n_s - n1), s1 / n1, workers=threads, chunks=4 * threads)
-        t = (time.perf_counter() - t0) * p["n"] / n_s
-        unit, smp = "fits/s", f"1 GDA fit over {n_s} samples, scaled"
+        t = time.perf_counter() - t0
+        unit, smp = "fits/s", f"1 GDA fit (two passes) over all {n_s} samples"
     else:
-        n_s = min(p["n"], 1 << 27)
         keys = O.rng_ints(1, 0, n_s, p["K"])
         t0 = time.perf_counter()
         O.groupby_count(keys, p["K"], workers=threads, chunks=4 * threads)
-        t = (time.perf_counter() - t0) * p["n"] / n_s
-        unit, smp = "passes/s", f"1 pass over {n_s} keys, scaled"
+        t = time.perf_counter() - t0
+        unit, smp = "passes/s", f"1 pass over all {n_s} keys"
     return {"value": 1.0 / t, "unit": unit, "cores": threads, "kind": "port", "sample": smp}
 
 
@@ -444,8 +443,12 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
 
     # ---- end to end through the public API with host buffers ----------------------------------
     e2e = None
+    e2e_family = None
     if family == "kmeans":
-        e2e = e2e_kmeans(args, p, n_local, lo, comm, dist, dev)
+        e2e_family = e2e_kmeans(args, p, n_local, lo, comm, dist, dev)
+        # one GPU: the headline e2e is the reference-facing drop-in (dlx_program_execute) with
+        # host buffers; sharded runs keep the family API's (the drop-in runs one device)
+        e2e = e2e_dropin_kmeans(args, p, dev) if world == 1 else e2e_family
     elif family == "logreg":
         e2e = e2e_logreg(args, p, n_local, lo, comm, dist, dev)
 
@@ -472,6 +475,7 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
                          "peak_kind": peak_kind, "kernel_ms": kern_ms,
                          "algorithmic_bytes_per_launch": bytes_launch},
             "e2e": e2e,
+            "e2e_family_api": e2e_family,
             "gpu_launches": launches,
             "cuda_graphs": sorted(graphs),
             "clocks": clocks,
@@ -481,8 +485,11 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             # pass 2 when sharded): executed DMMA flops (lower-triangle 8x8 blocks, 2*8*8 flop per
             # sample per block) over its event time, against the measured DMMA peak; the HBM
             # line of the same interval (x and y read once) is kept as roofline_hbm
+            # algorithmic flops of the symmetric scatter: d(d+1)/2 multiply-adds per sample
+            # (the kernel executes the 36 lower 8x8 blocks = 4,608 flop per sample at d = 64)
             nb = (d + 7) // 8
-            flops = n_local * 2.0 * 64 * nb * (nb + 1) // 2
+            flops = n_local * d * (d + 1)
+            flops_executed = n_local * 2.0 * 64 * nb * (nb + 1) // 2
             hb = algorithmic_bytes(family, p, n_local) / (pass2_ms * 1e-3) / 1e9
             result["roofline_hbm"] = {"bound": "hbm", "achieved": hb, "peak": peak, "unit": "GB/s",
                                       "frac": hb / peak, "kernel_ms": pass2_ms}
@@ -494,7 +501,9 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
                                   "frac": flops / (pass2_ms * 1e-3) / 1e12 / DMMA_PEAK_TFLOPS,
                                   "traffic": ncu_traffic(args.config), "peak_kind": DMMA_PEAK_KIND,
                                   "kernel_ms": pass2_ms,
-                                  "algorithmic_flops_per_launch": flops}
+                                  "algorithmic_flops_per_launch": flops,
+                                  "executed_flops_per_launch": flops_executed,
+                                  "executed_frac": flops_executed / (pass2_ms * 1e-3) / 1e12 / DMMA_PEAK_TFLOPS}
         if world == 1 and not args.no_cpu_baseline:
             try:
                 result["cpu_baseline"] = (cpu_baseline_kmeans(p) if family == "kmeans"
@@ -582,6 +591,70 @@ def e2e_kmeans(args, p, n_local, lo, comm, dist, dev, iters_per_job=10):
             "step": f"one job = H2D x shard (pinned) + {iters_per_job} iterations + D2H assignments and "
                     f"centroids; {jobs} jobs, double-buffered (H2D of job j+1 overlaps job j)",
             "iters_per_step": iters_per_job}
+
+
+def e2e_dropin_kmeans(args, p, dev, iters_per_job=10, jobs=4):
+    """e2e through the reference-facing drop-in (include/dlx_program.h): the staged k-means
+    program of `iters_per_job` fused iterations (descriptors.kmeans_program, pinned statement by
+    statement to the reference's own staging in tests/test_descriptors.py) executed with
+    dlx_program_execute, its VectorRand source replaced by caller data in pinned HOST memory
+    (dlx_program_input.h_data): every job copies the 8 GiB sample matrix to the device, runs the
+    iterations (centroid updates on the device) and returns the printed text (assignment of
+    row 0 and counts per iteration, every final centroid).  Two program handles on two host
+    threads, as a streaming caller would run them: one job's upload overlaps the other's
+    iterations.  Checked against SURVEY App. B (iteration-1 counts prefix)."""
+    import threading
+
+    import torch
+
+    from paper_1109_0778_b200 import multiloops as ml
+    from paper_1109_0778_b200.descriptors import kmeans_program
+    from paper_1109_0778_b200.program import Program
+    n, d, k = p["n"], p["d"], p["k"]
+    desc = kmeans_program(n, d, k, iters_per_job)
+    xsym = next(int(q) for q, st in desc["stmts"].items() if st["op"] == "VectorRand")
+    x_host = torch.empty(n * d, dtype=torch.float64, pin_memory=True)
+    x_host.copy_(ml.rng_units(n * d, seed=1, device=dev))
+    torch.cuda.synchronize()
+    progs = [Program(desc), Program(desc)]
+    outs = [None, None]
+    errs = []
+
+    def worker(t, njobs):
+        try:
+            torch.cuda.set_device(dev)
+            for _ in range(njobs):
+                outs[t] = progs[t].run(seed=1, device=dev.index, inputs={xsym: x_host})
+        except Exception as exc:   # reported, never hidden
+            errs.append(repr(exc))
+
+    for t in range(2):   # warm-up: lowers every loop once per handle (cached afterwards)
+        worker(t, 1)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=worker, args=(t, jobs // 2)) for t in range(2)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3
+    if errs:
+        return {"value": None, "error": errs[0]}
+    with open(os.path.join(ROOT, "tests", "golden", "appendix_b.json")) as f:
+        gold = json.load(f)["c4_kmeans"]["counts_prefix"][0]
+    lines = outs[0].output.split()
+    ok = [int(v) for v in lines[1:5]] == gold if (n, d, k) == (16_777_216, 64, 64) else None
+    launch = sorted({e["launch"] for e in outs[0].report})
+    del x_host, progs
+    torch.cuda.empty_cache()
+    return {"value": jobs * iters_per_job / (ms * 1e-3), "unit": "it/s", "h2d_bytes_per_step": n * d * 8,
+            "d2h_bytes_per_step": iters_per_job * (k * 8 + 4) + k * d * 8,
+            "api": "dlx_program_execute (drop-in for interpret/executeDEG), host-buffer input",
+            "step": f"one job = one staged program run: H2D of the pinned sample matrix + {iters_per_job} fused "
+                    f"iterations ({', '.join(launch)}, centroid update on the device) + printed results; "
+                    f"{jobs} jobs on 2 program handles / host threads (upload of one overlaps the other's iterations)",
+            "iters_per_step": iters_per_job, "wall_ms": ms, "appendix_b_counts": ok}
 
 
 def e2e_logreg(args, p, n_local, lo, comm, dist, dev, iters_per_job=20):
