@@ -115,6 +115,25 @@ size_t dlx_logreg_workspace_bytes(int64_t n, int32_t d);
 int dlx_logreg_grad(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
                     const double* d_theta, double* d_grad, void* d_workspace,
                     size_t workspace_bytes, dlx_stream_t stream);
+/* The staged logistic-regression loop (the collect form the reference fuses into
+ * one loop): h(i) = link(theta . x_i) (a collect, stored to d_h unless NULL) and
+ * grad_j = sum_i (h(i) - y_i) * x_ij.  The link is the loop body's own scalar expression of the
+ * dot t, compiled to dlx_link_code (registers r[0] = t, r[dst] = op(r[a], r[b]) / imm; IEEE
+ * round-to-nearest, no contraction): the reference op set has no exp, so staged programs carry
+ * e.g. softsign t / (1 + |t|), and the MathExp extension gives the sigmoid. */
+#define DLX_LINK_MAX_CODE 16
+#define DLX_LINK_MAX_REGS 8
+enum { DLX_LINK_CONST = 0, DLX_LINK_ADD, DLX_LINK_SUB, DLX_LINK_MUL, DLX_LINK_DIV, DLX_LINK_ABS,
+       DLX_LINK_EXP, DLX_LINK_SQRT };
+typedef struct {
+  int32_t n, out;
+  uint8_t op[DLX_LINK_MAX_CODE], dst[DLX_LINK_MAX_CODE], a[DLX_LINK_MAX_CODE], b[DLX_LINK_MAX_CODE];
+  double imm[DLX_LINK_MAX_CODE];
+} dlx_link_code;
+int dlx_rowdot_link_grad(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
+                         const double* d_theta, const dlx_link_code* h_link, double* d_h,
+                         double* d_grad, void* d_workspace, size_t workspace_bytes,
+                         dlx_stream_t stream);
 /* theta_j -= alpha * grad_j */
 int dlx_axpy_inplace(double* d_theta, const double* d_grad, double alpha, int64_t n,
                      dlx_stream_t stream);

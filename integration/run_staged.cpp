@@ -67,6 +67,63 @@ void stats(Stage& st, int64_t n) {
   for (int b = 0; b < 8; ++b) st.print(keys.count_where([&, b](DVal v) { return DInt(v) == st.lit(int64_t{b}); }));
 }
 
+// the C3 / C2 shapes at small size: GDA (pass 1 keyed sums + pass 2 scatter) and logistic
+// regression in the collect form with the softsign link (the reference has no exp)
+void gda(Stage& st, int64_t n, int d) {
+  DVec x = vec_rand(st, st.lit(n * d));
+  DVec y = vec_rand_int(st, st.lit(n), st.lit(int64_t{2}));
+  std::function<DBool(DInt)> is1 = [&](DInt i) { return y.at_i(i) == st.lit(int64_t{1}); };
+  std::function<DBool(DInt)> is0 = [&](DInt i) { return y.at_i(i) == st.lit(int64_t{0}); };
+  DInt n1(mk_reduce(st, st.lit(n), st.lit(int64_t{0}), [&](DInt) -> DVal { return st.lit(int64_t{1}); },
+                    [&](DVal l, DVal r) { return plus(st, l, r); }, &is1));
+  std::vector<DDouble> mu0, mu1;
+  DDouble nn1 = st.to_double(n1), nn0 = st.to_double(st.lit(n) - n1);
+  for (int j = 0; j < d; ++j) {
+    auto xj = [&, j](DInt i) -> DVal { return x.at(i * st.lit(int64_t{d}) + st.lit(int64_t{j})); };
+    mu0.push_back(DDouble(mk_reduce(st, st.lit(n), st.lit(0.0), xj, [&](DVal l, DVal r) { return plus(st, l, r); }, &is0)) / nn0);
+    mu1.push_back(DDouble(mk_reduce(st, st.lit(n), st.lit(0.0), xj, [&](DVal l, DVal r) { return plus(st, l, r); }, &is1)) / nn1);
+  }
+  st.print(n1);
+  for (int a = 0; a < d; ++a)
+    for (int b = 0; b < d; ++b)
+      st.print(DDouble(mk_reduce(
+          st, st.lit(n), st.lit(0.0),
+          [&, a, b](DInt i) -> DVal {
+            DBool c1 = y.at_i(i) == st.lit(int64_t{1});
+            DDouble ma = st.if_then_else<DDouble>(c1, [&] { return mu1[a]; }, [&] { return mu0[a]; });
+            DDouble mb = st.if_then_else<DDouble>(c1, [&] { return mu1[b]; }, [&] { return mu0[b]; });
+            return (x.at_d(i * st.lit(int64_t{d}) + st.lit(int64_t{a})) - ma) *
+                   (x.at_d(i * st.lit(int64_t{d}) + st.lit(int64_t{b})) - mb);
+          },
+          [&](DVal l, DVal r) { return plus(st, l, r); })));
+}
+
+void logreg(Stage& st, int64_t n, int d, int iters) {
+  DVec x = vec_rand(st, st.lit(n * d));
+  DVec y = vec_rand_int(st, st.lit(n), st.lit(int64_t{2}));
+  DVec th = vec_alloc(st, st.lit(int64_t{d}), SemType::f64());
+  for (int it = 0; it < iters; ++it) {
+    DVec h = mk_collect(st, st.lit(n), [&](DInt i) -> DVal {
+      DDouble dot(mk_reduce(st, st.lit(int64_t{d}), st.lit(0.0),
+                            [&](DInt j) -> DVal { return th.at_d(j) * x.at_d(i * st.lit(int64_t{d}) + j); },
+                            [&](DVal l, DVal r) { return plus(st, l, r); }));
+      return dot / (st.lit(1.0) + DDouble(st.abs(dot)));
+    });
+    st.print(h.at(st.lit(int64_t{0})));
+    std::vector<DDouble> g;
+    for (int j = 0; j < d; ++j)
+      g.push_back(DDouble(mk_reduce(
+          st, st.lit(n), st.lit(0.0),
+          [&, j](DInt i) -> DVal {
+            return (h.at_d(i) - st.to_double(y.at_i(i))) * x.at_d(i * st.lit(int64_t{d}) + st.lit(int64_t{j}));
+          },
+          [&](DVal l, DVal r) { return plus(st, l, r); })));
+    for (int j = 0; j < d; ++j)
+      th.update(st.lit(int64_t{j}), th.at_d(st.lit(int64_t{j})) - st.lit(1.0 / static_cast<double>(n)) * g[j]);
+  }
+  for (int j = 0; j < d; ++j) st.print(th.at(st.lit(int64_t{j})));
+}
+
 bool same(const std::string& a, const std::string& b) {
   if (a == b) return true;
   try {
@@ -86,7 +143,9 @@ int main() {
     std::function<void(Stage&)> body;
   };
   std::vector<Case> cases = {{"kmeans_n65536_d16_k8", [](Stage& st) { kmeans(st, 65536, 16, 8); }},
-                             {"stats_groupby_n1000000", [](Stage& st) { stats(st, 1000000); }}};
+                             {"stats_groupby_n1000000", [](Stage& st) { stats(st, 1000000); }},
+                             {"gda_n50000_d16", [](Stage& st) { gda(st, 50000, 16); }},
+                             {"logreg_n100000_d16_it3", [](Stage& st) { logreg(st, 100000, 16, 3); }}};
   int failures = 0;
   for (const Case& cs : cases) {
     Stage st;

@@ -141,6 +141,38 @@ void gda(Stage& st, int64_t n, int d) {
     }
 }
 
+// Logistic regression BGD in the collect form: h = link(theta . x_i) escapes
+// (printed), so fusion keeps one loop of 1 collect + d gradient reduces
+// (h(i) - y(i)) * x(i*d + j); then theta(j) -= alpha * g_j on the host.  The reference op set
+// has no exp (node.hpp:15-27), so the link is the softsign stand-in t / (1 + |t|) the survey
+// staged; the executor's logistic family evaluates whatever link expression the loop carries.
+void logreg(Stage& st, int64_t n, int d, int iters, double alpha) {
+  DVec x = vec_rand(st, st.lit(n * d));
+  DVec y = vec_rand_int(st, st.lit(n), st.lit(int64_t{2}));
+  DVec th = vec_alloc(st, st.lit(int64_t{d}), SemType::f64());
+  for (int it = 0; it < iters; ++it) {
+    DVec h = mk_collect(st, st.lit(n), [&](DInt i) -> DVal {
+      DDouble dot(mk_reduce(
+          st, st.lit(int64_t{d}), st.lit(0.0),
+          [&](DInt j) -> DVal { return th.at_d(j) * x.at_d(i * st.lit(int64_t{d}) + j); },
+          [&](DVal l, DVal r) { return plus(st, l, r); }));
+      return dot / (st.lit(1.0) + DDouble(st.abs(dot)));
+    });
+    st.print(h.at(st.lit(int64_t{0})));
+    std::vector<DDouble> g;
+    for (int j = 0; j < d; ++j)
+      g.push_back(DDouble(mk_reduce(
+          st, st.lit(n), st.lit(0.0),
+          [&, j](DInt i) -> DVal {
+            return (h.at_d(i) - st.to_double(y.at_i(i))) * x.at_d(i * st.lit(int64_t{d}) + st.lit(int64_t{j}));
+          },
+          [&](DVal l, DVal r) { return plus(st, l, r); })));
+    for (int j = 0; j < d; ++j)
+      th.update(st.lit(int64_t{j}), th.at_d(st.lit(int64_t{j})) - st.lit(alpha) * g[j]);
+  }
+  for (int j = 0; j < d; ++j) st.print(th.at(st.lit(int64_t{j})));
+}
+
 // mean_variance demo: mean and variance fuse into one loop.
 void mean_variance(Stage& st, int64_t n) {
   DVec x = vec_rand(st, st.lit(n));
@@ -194,6 +226,7 @@ int main(int argc, char** argv) {
       {"kmeans_n65536_d16_k8_it1", [](Stage& st) { kmeans(st, 65536, 16, 8, 1); }},
       {"groupby_n100000_k16", [](Stage& st) { groupby(st, 100000, 16); }},
       {"gda_n20000_d4", [](Stage& st) { gda(st, 20000, 4); }},
+      {"logreg_n20000_d8_it2", [](Stage& st) { logreg(st, 20000, 8, 2, 1.0 / 20000); }},
       {"mean_variance_n100000", [](Stage& st) { mean_variance(st, 100000); }},
       {"axpy_n100000", [](Stage& st) { axpy(st, 100000); }},
       {"count_gt_n100000", [](Stage& st) { count_gt(st, 100000); }},

@@ -76,6 +76,7 @@ _SIGS = {
     "dlx_logreg_workspace_bytes": (_sz, [_i64, _i32]),
     "dlx_logreg_grad": (_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _sz, _vp]),
     "dlx_axpy_inplace": (_int, [_vp, _vp, _dbl, _i64, _vp]),
+    "dlx_rowdot_link_grad": (_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "dlx_gda_workspace_bytes": (_sz, [_i64, _i32]),
     "dlx_gda_pass1": (_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "dlx_gda_means": (_int, [_vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp]),

@@ -365,7 +365,8 @@ bool Executor::match_kmeans(const Stmt& s, int64_t n, std::vector<LElem>& els, L
   p.skip.clear();
   p.sums_group_only = false;
   auto g = P.update_after.find(s.sym);
-  if (g != P.update_after.end() && static_cast<int64_t>(g->second.entries.size()) == k * d) {
+  if (g != P.update_after.end() && g->second.kind == UpdateGroup::Div &&
+      static_cast<int64_t>(g->second.entries.size()) == k * d) {
     std::vector<uint8_t> seen(k * d, 0);
     bool ok = true;
     for (const UpdateGroup::Entry& en : g->second.entries) {
@@ -580,6 +581,168 @@ bool Executor::match_gda2(int64_t n, std::vector<LElem>& els, LoopPlan& p, Match
   return true;
 }
 
+// ---- family: logistic regression (collect h = link(theta . x_i) + d residual-weighted sums) -----
+// The loop the reference fuses from the collect form: one collect whose value is a
+// scalar expression of a nested dot reduce D = sum_j theta(j) * x(i*d + j), and reduces
+// g_j = sum_i (h - toDouble(y(i))) * x(i*d + j) reading the collect's value h (vertical fusion).
+bool Executor::link_compile(const SEP& f, const SEP& dot, LoopPlan& p, std::unordered_map<const SE*, int>& reg) {
+  if (f == dot) return true;   // r[0]
+  if (reg.count(f.get())) return true;
+  auto emit = [&](uint8_t op, int a, int b, double imm) {
+    const int q = p.link.n;
+    const int r = static_cast<int>(reg.size()) + 1;
+    if (q >= DLX_LINK_MAX_CODE || r >= DLX_LINK_MAX_REGS) return false;
+    p.link.op[q] = op;
+    p.link.a[q] = static_cast<uint8_t>(a);
+    p.link.b[q] = static_cast<uint8_t>(b);
+    p.link.imm[q] = imm;
+    p.link.dst[q] = static_cast<uint8_t>(r);
+    p.link.n = q + 1;
+    reg[f.get()] = r;
+    return true;
+  };
+  auto r_of = [&](const SEP& x) { return x == dot ? 0 : reg.at(x.get()); };
+  switch (f->k) {
+    case SE::Const:
+      if (f->ty != Ty::Double) return false;
+      return emit(DLX_LINK_CONST, 0, 0, f->cd);
+    case SE::Host:
+      if (!f->host.is_dbl()) return false;
+      p.link_patches.emplace_back(p.link.n, f->sym);
+      return emit(DLX_LINK_CONST, 0, 0, f->host.d());
+    case SE::Bin: {
+      if (f->ty != Ty::Double || !link_compile(f->a[0], dot, p, reg) || !link_compile(f->a[1], dot, p, reg)) return false;
+      const uint8_t op = f->op == Op::Plus ? DLX_LINK_ADD : f->op == Op::Minus ? DLX_LINK_SUB
+                         : f->op == Op::Times ? DLX_LINK_MUL : f->op == Op::Divide ? DLX_LINK_DIV : 255;
+      if (op == 255) return false;
+      return emit(op, r_of(f->a[0]), r_of(f->a[1]), 0);
+    }
+    case SE::Un: {
+      if (f->ty != Ty::Double || !link_compile(f->a[0], dot, p, reg)) return false;
+      const uint8_t op = f->op == Op::MathAbs ? DLX_LINK_ABS : f->op == Op::MathExp ? DLX_LINK_EXP
+                         : f->op == Op::MathSqrt ? DLX_LINK_SQRT : 255;
+      if (op == 255) return false;
+      return emit(op, r_of(f->a[0]), 0, 0);
+    }
+    default: return false;
+  }
+}
+
+bool Executor::match_logistic(const Stmt& s, int64_t n, std::vector<LElem>& els, LoopPlan& p, MatchCtx& m) {
+  (void)n;
+  int ci = -1;
+  for (size_t q = 0; q < els.size(); ++q)
+    if (els[q].e->kind == Elem::Collect) {
+      if (ci >= 0) MISS("two collects");
+      ci = static_cast<int>(q);
+    }
+  if (ci < 0 || els[ci].cond || els[ci].e->append || els[ci].e->out_ty.elem != Ty::Double) MISS("no dense Double collect");
+  const SEP F = els[ci].value;
+  // the one nested reduce in F: the dot
+  SEP D;
+  std::vector<SEP> stack{F};
+  while (!stack.empty()) {
+    SEP x = stack.back();
+    stack.pop_back();
+    if (x->k == SE::Red) {
+      if (D && D != x) MISS("two nested reduces");
+      D = x;
+      continue;
+    }
+    if (x->k == SE::Load || x->k == SE::Idx || x->k == SE::Sel) MISS("link reads beyond the dot");
+    for (const SEP& c : x->a) stack.push_back(c);
+  }
+  if (!D || D->ty != Ty::Double || !is_plus_combine(D->a[1]) || !zero_is_pos0(D->zero)) MISS("no dot reduce");
+  const int64_t d = D->range;
+  const SEP& prod = D->a[0];
+  if (prod->k != SE::Bin || prod->op != Op::Times || prod->a[0]->k != SE::Load || prod->a[1]->k != SE::Load)
+    MISS("dot elem is not a product of two loads");
+  int xs = -1, ts = -1;
+  for (int side = 0; side < 2; ++side) {
+    const SEP& ld = prod->a[side];
+    Affine af;
+    if (!affine(ld->a[1], &af) || ld->a[0]->ty != Ty::Double) MISS("dot load");
+    if (af.a == d && af.b == 1 && af.c == 0 && af.inner == D->sym) xs = m.slot(ld->a[0]);
+    else if (af.a == 0 && af.b == 1 && af.c == 0 && af.inner == D->sym) ts = m.slot(ld->a[0]);
+  }
+  if (xs < 0 || ts < 0) MISS("dot is not theta(j) * x(i*d + j)");
+  p.link = dlx_link_code{};
+  p.link_patches.clear();
+  std::unordered_map<const SE*, int> reg;
+  if (!link_compile(F, D, p, reg)) MISS("link expression");
+  p.link.out = F == D ? 0 : reg.at(F.get());
+  // the gradient reduces
+  p.outs.clear();
+  p.outs.push_back({els[ci].e->out, 1, 0, Ty::Double});
+  int ys = -1;
+  std::vector<uint8_t> seen(d, 0);
+  for (size_t q = 0; q < els.size(); ++q) {
+    if (static_cast<int>(q) == ci) continue;
+    const LElem& le = els[q];
+    if (le.e->kind != Elem::Reduce || le.cond || !is_plus_combine(le.combine) || !zero_is_pos0(le.e->zero))
+      MISS("elem is not an unguarded + reduce from 0.0");
+    const SEP& v = le.value;
+    if (v->k != SE::Bin || v->op != Op::Times) MISS("gradient elem is not a product");
+    SEP R = v->a[0], L = v->a[1];
+    if (R->k == SE::Load) std::swap(R, L);
+    if (L->k != SE::Load || R->k != SE::Bin || R->op != Op::Minus || R->a[0] != F) MISS("not (h - y) * x");
+    const SEP& yd = R->a[1];
+    if (yd->k != SE::Un || yd->op != Op::ToDouble || yd->a[0]->k != SE::Load || yd->a[0]->a[0]->ty != Ty::Int)
+      MISS("label is not toDouble(y(i))");
+    Affine ay, ax;
+    if (!affine(yd->a[0]->a[1], &ay) || ay.a != 1 || ay.b != 0 || ay.c != 0) MISS("label index is not i");
+    const int y = m.slot(yd->a[0]->a[0]);
+    if (ys >= 0 && ys != y) MISS("two label vectors");
+    ys = y;
+    if (!affine(L->a[1], &ax) || m.slot(L->a[0]) != xs || ax.a != d || ax.b != 0 || ax.c < 0 || ax.c >= d)
+      MISS("gradient column is not x(i*d + j)");
+    if (seen[ax.c]) MISS("column twice");
+    seen[ax.c] = 1;
+    p.outs.push_back({le.e->out, 0, ax.c, Ty::Double});
+  }
+  if (ys < 0) MISS("no gradient");
+  p.x = xs;
+  p.mu = ts;
+  p.keys = ys;
+  p.d = d;
+  p.nres = d;
+  // theta(j) = theta(j) - alpha * g_j after the loop (UpdateGroup::Axpy): on the device
+  p.upd_vec = -1;
+  p.skip.clear();
+  p.sums_group_only = false;
+  auto g = P.update_after.find(s.sym);
+  if (g != P.update_after.end() && g->second.kind == UpdateGroup::Axpy &&
+      static_cast<int64_t>(g->second.entries.size()) == d) {
+    std::unordered_map<int, int64_t> col;   // gradient out -> column
+    for (const LoopPlan::Out& o : p.outs)
+      if (o.src == 0) col[o.sym] = o.ix;
+    std::vector<uint8_t> cov(d, 0);
+    bool ok = true;
+    for (const UpdateGroup::Entry& en : g->second.entries) {
+      auto c = col.find(en.sum_sym);
+      if (c == col.end() || c->second != en.e || cov[en.e]) ok = false;
+      else cov[en.e] = 1;
+    }
+    const Atom& al = g->second.alpha;
+    if (ok && (al.k == Atom::Double || al.k == Atom::Sym)) {
+      p.upd_vec = g->second.vec_sym;
+      p.skip = g->second.stmts;
+      p.alpha_sym = al.k == Atom::Sym ? al.sym : -1;
+      p.alpha_lit = al.d;
+      size_t only = 0;
+      for (LoopPlan::Out& o : p.outs) {
+        o.group_only = o.src == 0 && P.uses[o.sym] == 1;   // read only by its Times
+        only += o.group_only;
+      }
+      p.sums_group_only = only == static_cast<size_t>(d);
+    }
+  }
+  p.fam = LoopPlan::Logistic;
+  p.family = "logistic";
+  p.launch = p.upd_vec >= 0 ? "dlx_rowdot_link_grad + dlx_axpy_inplace" : "dlx_rowdot_link_grad";
+  return true;
+}
+
 // ---- generic multiloop kernel (bytecode) -------------------------------------------------------
 int Executor::vm_emit(LoopPlan& p, MatchCtx& m, std::unordered_map<const SE*, int>& reg, int& nreg, const SEP& s) {
   auto it = reg.find(s.get());
@@ -753,7 +916,7 @@ std::shared_ptr<LoopPlan> Executor::lower(const Stmt& s, int64_t n) {
     els.push_back(le);
   }
   auto p = std::make_shared<LoopPlan>();
-  const bool ok = match_kmeans(s, n, els, *p, m) || match_groupby(n, els, *p, m) ||
+  const bool ok = match_kmeans(s, n, els, *p, m) || match_logistic(s, n, els, *p, m) || match_groupby(n, els, *p, m) ||
                   match_bucket_rows(n, els, *p, m) || match_gda2(n, els, *p, m) || match_generic(n, els, *p, m);
   if (!ok) gen_fail("multiloop x" + std::to_string(s.sym) + " matches no kernel");
   p->vsyms = m.vsyms;
@@ -838,7 +1001,7 @@ void Executor::run_loop(const Stmt& s) {
   if (plan->fam == LoopPlan::Kmeans) rep["d"] = plan->d, rep["k"] = plan->k;
   if (plan->fam == LoopPlan::GroupBy) rep["buckets"] = plan->k;
   if (plan->fam == LoopPlan::BucketRows) rep["buckets"] = plan->k, rep["d"] = plan->d;
-  if (plan->fam == LoopPlan::GdaScatter) rep["d"] = plan->d;
+  if (plan->fam == LoopPlan::GdaScatter || plan->fam == LoopPlan::Logistic) rep["d"] = plan->d;
   if (plan->fam == LoopPlan::Generic) rep["elems"] = live, rep["instructions"] = static_cast<int>(plan->code.size());
   rep["launch"] = plan->launch;
   rep["cached"] = cached;
@@ -900,6 +1063,7 @@ void Executor::launch(const Stmt& s, LoopPlan& p, int64_t n, std::vector<VecP>& 
     case LoopPlan::GroupBy: launch_groupby(p, n, vecs); break;
     case LoopPlan::BucketRows: launch_bucket_rows(p, n, vecs); break;
     case LoopPlan::GdaScatter: launch_gda2(p, n, vecs); break;
+    case LoopPlan::Logistic: launch_logistic(p, n, vecs, rep); break;
     case LoopPlan::Generic: launch_generic(p, n, vecs); break;
   }
 }
@@ -1049,6 +1213,58 @@ void Executor::launch_gda2(LoopPlan& p, int64_t n, std::vector<VecP>& V) {
   ck(rc);
   complete_loop({}, nullptr);
   bind_scalars(p, hres);
+}
+
+void Executor::launch_logistic(LoopPlan& p, int64_t n, std::vector<VecP>& V, json& rep) {
+  const VecP& X = V[p.x];
+  const VecP& TH = V[p.mu];
+  const VecP& Y = V[p.keys];
+  const int32_t d = static_cast<int32_t>(p.d);
+  if (n * d > X->n || d > TH->n || n > Y->n) load_trap();
+  dlx_link_code link = p.link;
+  for (auto [q, sym] : p.link_patches) link.imm[q] = force(env_[sym]).d();
+  double alpha = p.alpha_lit;
+  VecP U;
+  if (p.upd_vec >= 0 && bound_[p.upd_vec] && env_[p.upd_vec].is_vec()) {
+    U = env_[p.upd_vec].vec();
+    if (U->elem != Ty::Double || U->n != d) U = nullptr;
+    if (U && p.alpha_sym >= 0) {
+      Val a = force(env_[p.alpha_sym]);
+      if (a.is_dbl()) alpha = a.d();
+      else U = nullptr;
+    }
+  }
+  wait_inputs(V);
+  if (U) {
+    fence_on(lst_);   // WAR: loops in flight may still read U
+    if (U->wev) cudaStreamWaitEvent(lst_, U->wev, 0);
+  }
+  const bool copy_grad = !U || !p.sums_group_only;
+  VecP h = new_vec(n, Ty::Double, lst_, false);
+  const size_t wsb = dlx_logreg_workspace_bytes(n, d);
+  void* ws = dalloc(wsb);
+  auto* grad = static_cast<double*>(dalloc(static_cast<size_t>(d) * 8));
+  int rc = dlx_rowdot_link_grad(static_cast<const double*>(X->p), static_cast<const int64_t*>(Y->p), n, d,
+                                static_cast<const double*>(TH->p), &link, static_cast<double*>(h->p), grad, ws, wsb, lst_);
+  if (rc == DLX_OK && U) rc = dlx_axpy_inplace(static_cast<double*>(U->p), grad, alpha, d, lst_);
+  int64_t* hres = res_->pin.get_n<int64_t>(d);
+  if (rc == DLX_OK && copy_grad) cudaMemcpyAsync(hres, grad, static_cast<size_t>(d) * 8, cudaMemcpyDeviceToHost, lst_);
+  dfree(ws);
+  dfree(grad);
+  ck(rc);
+  cudaEvent_t ev = complete_loop({}, nullptr);
+  h->wev = ev;
+  for (const LoopPlan::Out& o : p.outs) {
+    if (o.src == 1) bind(o.sym, Val{h});
+    else if (!(U && o.group_only)) bind(o.sym, Val{make_lazy(hres + o.ix, o.ty, 8)});
+  }
+  if (U) {
+    U->wev = ev;
+    U->host_valid = false;
+    U->page_valid = false;
+    for (int q : p.skip) mark_skip(q);
+  }
+  rep["update"] = U ? "device" : p.upd_vec >= 0 ? "host" : "none";
 }
 
 void Executor::launch_generic(LoopPlan& p, int64_t n, std::vector<VecP>& V) {

@@ -141,7 +141,7 @@ struct SE {
 // was matched against keep their element types and lengths and every baked host scalar its
 // value).
 struct LoopPlan {
-  enum Fam { Kmeans, GroupBy, BucketRows, GdaScatter, Generic } fam = Generic;
+  enum Fam { Kmeans, GroupBy, BucketRows, GdaScatter, Logistic, Generic } fam = Generic;
   std::string family, launch;
   // inputs: env symbols of the vectors the loop reads (slot order), their types and lengths
   std::vector<int> vsyms;
@@ -165,6 +165,12 @@ struct LoopPlan {
   int upd_vec = -1;                             // V's symbol (-1: none)
   std::vector<int> skip;                        // the group's host statements
   bool sums_group_only = false;                 // every sum is read only by the group
+  // logistic: the link expression of the dot (host scalars re-read per launch) and the axpy
+  // update group's alpha (a literal, or a host symbol)
+  dlx_link_code link{};
+  std::vector<std::pair<int, int>> link_patches;   // (instruction, host symbol)
+  int alpha_sym = -1;
+  double alpha_lit = 0;
   // bucket counts / bucket rows: bucket values
   std::vector<int64_t> buckets;
   // GDA scatter: per column the class-mean sources (symbol, or -1 and a literal)
@@ -296,6 +302,8 @@ class Executor {
   bool match_centred(const SEP& t, int64_t d, int* xs, int* ys, int64_t* col, int* s0, double* l0, int* s1, double* l1,
                      MatchCtx& m);
   bool match_gda2(int64_t n, std::vector<LElem>& els, LoopPlan& p, MatchCtx& m);
+  bool match_logistic(const Stmt& s, int64_t n, std::vector<LElem>& els, LoopPlan& p, MatchCtx& m);
+  bool link_compile(const SEP& f, const SEP& dot, LoopPlan& p, std::unordered_map<const SE*, int>& reg);
   bool match_generic(int64_t n, std::vector<LElem>& els, LoopPlan& p, MatchCtx& m);
   int vm_emit(LoopPlan& p, MatchCtx& m, std::unordered_map<const SE*, int>& reg, int& nreg, const SEP& s);
   // launches
@@ -303,6 +311,7 @@ class Executor {
   void launch_groupby(LoopPlan& p, int64_t n, std::vector<VecP>& V);
   void launch_bucket_rows(LoopPlan& p, int64_t n, std::vector<VecP>& V);
   void launch_gda2(LoopPlan& p, int64_t n, std::vector<VecP>& V);
+  void launch_logistic(LoopPlan& p, int64_t n, std::vector<VecP>& V, nlohmann::json& rep);
   void launch_generic(LoopPlan& p, int64_t n, std::vector<VecP>& V);
   void bind_scalars(const LoopPlan& p, const int64_t* hres);
   void* dalloc(size_t bytes);

@@ -5,6 +5,7 @@
 #include <charconv>
 #include <cmath>
 #include <json.hpp>
+#include <cstring>
 #include <limits>
 #include <unordered_set>
 
@@ -171,6 +172,9 @@ struct Analyzer {
     }
   }
 
+  // UpdateGroups after each loop L (see program_ir.hpp): per target V, the entries and every
+  // statement computing them; a group is kept when its temporaries are read only inside it,
+  // no other statement touches V before its last update, and (axpy) one alpha serves all.
   void find_update_groups() {
     for (size_t b = 0; b < P.blocks.size(); ++b) {
       if (!P.has_block[b]) continue;
@@ -182,77 +186,105 @@ struct Analyzer {
         for (const Elem& e : L.loop->elems)
           if (e.live && e.kind == Elem::Reduce) outs.insert(e.out);
         if (outs.empty()) continue;
-        std::unordered_map<int, int> cd_of;                    // ToDouble sym -> count sym
-        std::unordered_map<int, std::pair<int, int>> q_of;     // Divide sym -> (sum, count)
-        std::unordered_map<int, UpdateGroup> groups;           // V -> group
-        std::unordered_map<int, size_t> foreign_first;         // V -> first non-group reference
-        std::unordered_map<int, size_t> last_entry;
-        std::unordered_map<int, int> cd_uses;                  // ToDouble sym -> group uses
+        auto is_out = [&](const Atom& a) { return a.k == Atom::Sym && outs.count(a.sym); };
+        auto is_alpha = [&](const Atom& a) {   // a literal or a host scalar computed before the loop
+          return a.k == Atom::Double || (a.k == Atom::Sym && !outs.count(a.sym));
+        };
+        // candidate temporaries: sym -> defining statement's position
+        std::unordered_map<int, int> cd_of;                    // ToDouble(count) -> count
+        std::unordered_map<int, std::pair<int, int>> q_of;     // Divide(sum, cd) -> (sum, cd)
+        std::unordered_map<int, std::pair<int, Atom>> t_of;    // Times(alpha, g) -> (g, alpha)
+        std::unordered_map<int, std::pair<int, int64_t>> a_of; // VectorApply(V, j) -> (V, j)
+        std::unordered_map<int, std::pair<int, int>> m_of;     // Minus(a, t) -> (a, t)
+        struct Cand {
+          UpdateGroup g;
+          size_t last = 0;
+          bool mixed_alpha = false;
+          bool has_alpha = false;
+          Atom alpha;
+        };
+        std::unordered_map<int, Cand> cands[2];   // [Div, Axpy] by V
+        std::vector<int> pos_of_sym;               // position of each candidate statement
+        std::unordered_map<int, size_t> pos;
         for (size_t q = p + 1; q < ss.size(); ++q) {
           const Stmt& s = P.stmts[ss[q]];
-          if (s.op == Op::ToDouble && s.args.size() == 1 && s.args[0].k == Atom::Sym && outs.count(s.args[0].sym)) {
-            cd_of[s.sym] = s.args[0].sym;
-            continue;
+          pos[s.sym] = q;
+          const auto& A = s.args;
+          if (s.op == Op::ToDouble && A.size() == 1 && is_out(A[0])) cd_of[s.sym] = A[0].sym;
+          else if (s.op == Op::Divide && A.size() == 2 && is_out(A[0]) && A[1].k == Atom::Sym && cd_of.count(A[1].sym))
+            q_of[s.sym] = {A[0].sym, A[1].sym};
+          else if (s.op == Op::Times && A.size() == 2 && is_out(A[1]) && is_alpha(A[0])) t_of[s.sym] = {A[1].sym, A[0]};
+          else if (s.op == Op::Times && A.size() == 2 && is_out(A[0]) && is_alpha(A[1])) t_of[s.sym] = {A[0].sym, A[1]};
+          else if (s.op == Op::VectorApply && A.size() == 2 && A[0].k == Atom::Sym && A[1].k == Atom::Int)
+            a_of[s.sym] = {A[0].sym, A[1].i};
+          else if (s.op == Op::Minus && A.size() == 2 && A[0].k == Atom::Sym && A[1].k == Atom::Sym && a_of.count(A[0].sym) &&
+                   t_of.count(A[1].sym))
+            m_of[s.sym] = {A[0].sym, A[1].sym};
+          else if (s.op == Op::VectorUpdate && A.size() == 3 && A[0].k == Atom::Sym && A[1].k == Atom::Int && A[2].k == Atom::Sym) {
+            const int V = A[0].sym;
+            const int64_t e = A[1].i;
+            if (q_of.count(A[2].sym)) {   // V(e) = sum / toDouble(count)
+              const auto [sum, cd] = q_of[A[2].sym];
+              Cand& c = cands[UpdateGroup::Div][V];
+              c.g.kind = UpdateGroup::Div;
+              c.g.vec_sym = V;
+              c.g.entries.push_back({e, sum, cd_of[cd]});
+              c.g.stmts.insert(c.g.stmts.end(), {s.sym, A[2].sym});
+              c.last = q;
+            } else if (m_of.count(A[2].sym)) {   // V(e) = V(e) - alpha * g
+              const auto [a, t] = m_of[A[2].sym];
+              if (a_of[a].first != V || a_of[a].second != e) continue;
+              Cand& c = cands[UpdateGroup::Axpy][V];
+              c.g.kind = UpdateGroup::Axpy;
+              c.g.vec_sym = V;
+              c.g.entries.push_back({e, t_of[t].first, -1});
+              c.g.stmts.insert(c.g.stmts.end(), {s.sym, A[2].sym, a, t});
+              const Atom& al = t_of[t].second;
+              if (!c.has_alpha) {
+                c.alpha = al;
+                c.has_alpha = true;
+              } else if (al.k != c.alpha.k || (al.k == Atom::Sym ? al.sym != c.alpha.sym : std::memcmp(&al.d, &c.alpha.d, 8) != 0)) {
+                c.mixed_alpha = true;
+              }
+              c.last = q;
+            }
           }
-          if (s.op == Op::Divide && s.args.size() == 2 && s.args[0].k == Atom::Sym && s.args[1].k == Atom::Sym &&
-              outs.count(s.args[0].sym) && cd_of.count(s.args[1].sym)) {
-            q_of[s.sym] = {s.args[0].sym, cd_of[s.args[1].sym]};
-            ++cd_uses[s.args[1].sym];
-            continue;
-          }
-          if (s.op == Op::VectorUpdate && s.args.size() == 3 && s.args[0].k == Atom::Sym && s.args[1].k == Atom::Int &&
-              s.args[2].k == Atom::Sym && q_of.count(s.args[2].sym)) {
-            const int V = s.args[0].sym;
-            const auto sc = q_of[s.args[2].sym];
-            UpdateGroup& g = groups[V];
-            g.vec_sym = V;
-            g.entries.push_back({s.args[1].i, sc.first, sc.second});
-            last_entry[V] = q;
-            continue;
-          }
-          std::unordered_set<int> r;
-          refs_stmt(s, r, 0);
-          for (int v : r)
-            if (!foreign_first.count(v)) foreign_first[v] = q;
         }
-        // the best valid group: no foreign reference to V before its last update, and the
-        // ToDouble / Divide temporaries used only by the group
         UpdateGroup best;
-        for (auto& [V, g] : groups) {
-          auto ff = foreign_first.find(V);
-          if (ff != foreign_first.end() && ff->second < last_entry[V]) continue;
-          if (g.entries.size() <= best.entries.size()) continue;
-          best = g;
-        }
-        if (best.entries.empty()) continue;
-        // the group's statements: every ToDouble / Divide feeding its updates, and the updates
-        std::unordered_set<int> qs, cds;
-        bool ok = true;
-        for (size_t q = p + 1; q < ss.size() && ok; ++q) {
-          const Stmt& s = P.stmts[ss[q]];
-          if (s.op == Op::VectorUpdate && s.args.size() == 3 && s.args[0].k == Atom::Sym && s.args[0].sym == best.vec_sym &&
-              s.args[2].k == Atom::Sym && q_of.count(s.args[2].sym)) {
-            best.stmts.push_back(s.sym);
-            qs.insert(s.args[2].sym);
+        for (int kind = 0; kind < 2; ++kind)
+          for (auto& [V, c] : cands[kind]) {
+            if (c.mixed_alpha || c.g.entries.size() <= best.entries.size()) continue;
+            UpdateGroup g = c.g;
+            if (kind == UpdateGroup::Div) {   // the ToDouble temporaries join the group
+              std::unordered_set<int> cds;
+              for (int st : c.g.stmts)
+                if (q_of.count(st)) cds.insert(q_of[st].second);
+              g.stmts.insert(g.stmts.end(), cds.begin(), cds.end());
+            }
+            std::unordered_set<int> in(g.stmts.begin(), g.stmts.end());
+            // every temporary is read only by statements of the group
+            bool ok = true;
+            for (int st : g.stmts) {
+              const Stmt& S = P.stmts[st];
+              if (S.op == Op::VectorUpdate) continue;
+              int inside = 0;
+              for (int u : g.stmts)
+                for (const Atom& a : P.stmts[u].args)
+                  if (a.k == Atom::Sym && a.sym == st) ++inside;
+              if (P.uses[st] != inside) ok = false;
+            }
+            // nothing outside the group touches V before its last update
+            for (size_t q = p + 1; q <= c.last && ok; ++q) {
+              if (in.count(ss[q])) continue;
+              std::unordered_set<int> r;
+              refs_stmt(P.stmts[ss[q]], r, 0);
+              if (r.count(V)) ok = false;
+            }
+            if (!ok) continue;
+            if (kind == UpdateGroup::Axpy) g.alpha = c.alpha;
+            best = std::move(g);
           }
-        }
-        for (size_t q = p + 1; q < ss.size() && ok; ++q) {
-          const Stmt& s = P.stmts[ss[q]];
-          if (s.op == Op::Divide && qs.count(s.sym)) {
-            if (P.uses[s.sym] != 1) ok = false;
-            cds.insert(s.args[1].sym);
-            best.stmts.push_back(s.sym);
-          }
-        }
-        for (int cd : cds) {
-          // every use of cd must be one of this group's divides
-          int in_group = 0;
-          for (int qq : qs)
-            if (P.stmts[qq].args[1].sym == cd) ++in_group;
-          if (P.uses[cd] != in_group) ok = false;
-          best.stmts.push_back(cd);
-        }
-        if (ok) P.update_after[L.sym] = std::move(best);
+        if (!best.entries.empty()) P.update_after[L.sym] = std::move(best);
       }
     }
   }

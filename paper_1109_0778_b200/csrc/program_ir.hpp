@@ -92,11 +92,17 @@ struct Block {
 // Found statically; the lowering checks at match time that (e, sum, count) cover
 // e = c*d + j exactly, and then the statements run as one device update fused into the loop's
 // combine launch instead of k*d host statements.
+//
+// Second kind (logistic-regression BGD, the staged `theta.update(j, theta(j) - alpha * g_j)`):
+// t = Times(alpha, g);  a = VectorApply(V, e);  m = Minus(a, t);  VectorUpdate(V, e, m), one alpha
+// (a literal or a host scalar) for every entry — run as one axpy after the loop's combine.
 struct UpdateGroup {
+  enum Kind { Div = 0, Axpy = 1 } kind = Div;
   int vec_sym = -1;                  // V
-  struct Entry { int64_t e; int sum_sym, count_sym; };
+  struct Entry { int64_t e; int sum_sym, count_sym; };   // Axpy: sum_sym = g, count_sym = -1
   std::vector<Entry> entries;        // in program order
-  std::vector<int> stmts;            // every ToDouble / Divide / VectorUpdate of the group
+  std::vector<int> stmts;            // every statement of the group (temporaries and updates)
+  Atom alpha;                        // Axpy
 };
 
 // A run of adjacent host statement pairs  a = VectorApply(X, e1);  VectorUpdate(V, e2, a)  (a read

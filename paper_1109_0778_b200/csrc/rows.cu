@@ -100,13 +100,45 @@ __device__ __forceinline__ int lane_of_row(int r) {
 }
 
 // ---------------------------------------------------------------------------------------
-// logistic regression: g_j = sum_i (sigmoid(theta . x_i) - y_i) x_ij
-// One fused pass: dot (FMA partials + reduce-scatter), sigmoid once per row on 4 lanes,
-// residual broadcast, gradient FMAs into per-lane registers.
-template <int M>
+// logistic regression: g_j = sum_i (link(theta . x_i) - y_i) x_ij
+// One fused pass: dot (FMA partials + reduce-scatter), the link once per row on 4 lanes
+// (optionally stored: the staged program's collect h(i) = link(theta . x_i)), residual
+// broadcast, gradient FMAs into per-lane registers.  Link = the sigmoid of the family API, or a
+// link expression compiled by the executor from the loop body (LinkCode: the reference has no
+// exp, so staged programs carry their own link, e.g. softsign t / (1 + |t|)).
+struct SigmoidLink {
+  __device__ __forceinline__ double operator()(double z) const { return 1.0 / (1.0 + exp(-z)); }
+};
+struct CodeLink {
+  dlx_link_code c;
+  // registers: r[0] = t; every instruction writes r[dst]; IEEE round-to-nearest, no contraction
+  __device__ double operator()(double t) const {
+    double r[DLX_LINK_MAX_REGS];
+    r[0] = t;
+    for (int q = 0; q < c.n; ++q) {
+      const double a = r[c.a[q]], b = r[c.b[q]];
+      double v;
+      switch (c.op[q]) {
+        case DLX_LINK_CONST: v = c.imm[q]; break;
+        case DLX_LINK_ADD: v = __dadd_rn(a, b); break;
+        case DLX_LINK_SUB: v = __dsub_rn(a, b); break;
+        case DLX_LINK_MUL: v = __dmul_rn(a, b); break;
+        case DLX_LINK_DIV: v = __ddiv_rn(a, b); break;
+        case DLX_LINK_ABS: v = fabs(a); break;
+        case DLX_LINK_EXP: v = exp(a); break;
+        default: v = __dsqrt_rn(a); break;
+      }
+      r[c.dst[q]] = v;
+    }
+    return r[c.out];
+  }
+};
+
+template <int M, class Link, bool WRITE_H>
 __global__ void __launch_bounds__(kRowThreads, DLX_ROW_MINB)
 logreg_grad_kernel(const double* __restrict__ x, const long long* __restrict__ y, int64_t n,
-                   int d, const double* __restrict__ theta, double* __restrict__ parts) {
+                   int d, const double* __restrict__ theta, Link link, double* __restrict__ h_out,
+                   double* __restrict__ parts) {
   pdl_wait();   // programmatic dependent launch: inputs are final from here on
   pdl_trigger();
   extern __shared__ double red_s[];
@@ -137,7 +169,9 @@ logreg_grad_kernel(const double* __restrict__ x, const long long* __restrict__ y
       p[r] = a;
     }
     const double z = reduce_scatter8(p, lane);
-    const double res = iy < n ? 1.0 / (1.0 + exp(-z)) - yv : 0.0;
+    const double h = iy < n ? link(z) : 0.0;
+    if (WRITE_H && (lane & 3) == 0 && iy < n) h_out[iy] = h;
+    const double res = iy < n ? h - yv : 0.0;
 #pragma unroll
     for (int r = 0; r < kRows; ++r) {
       const double rr = __shfl_sync(0xffffffffu, res, lane_of_row(r));
@@ -358,12 +392,47 @@ int dlx_logreg_grad(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
   double* parts = static_cast<double*>(d_workspace);
   const size_t smem = static_cast<size_t>(kRowWarps) * d * sizeof(double);
   const long long* y = reinterpret_cast<const long long*>(d_y);
+  const SigmoidLink sig;
   switch (m_for(d)) {
-    case 1: DLX_CUDA(launch_pdl(logreg_grad_kernel<1>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, parts)); break;
-    case 2: DLX_CUDA(launch_pdl(logreg_grad_kernel<2>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, parts)); break;
-    case 3: DLX_CUDA(launch_pdl(logreg_grad_kernel<3>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, parts)); break;
-    default: DLX_CUDA(launch_pdl(logreg_grad_kernel<4>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, parts)); break;
+    case 1: DLX_CUDA(launch_pdl(logreg_grad_kernel<1, SigmoidLink, false>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, sig, nullptr, parts)); break;
+    case 2: DLX_CUDA(launch_pdl(logreg_grad_kernel<2, SigmoidLink, false>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, sig, nullptr, parts)); break;
+    case 3: DLX_CUDA(launch_pdl(logreg_grad_kernel<3, SigmoidLink, false>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, sig, nullptr, parts)); break;
+    default: DLX_CUDA(launch_pdl(logreg_grad_kernel<4, SigmoidLink, false>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, sig, nullptr, parts)); break;
   }
+  DLX_LAUNCHED("logreg_grad_kernel");
+  return combine_f64(parts, grid, d, d_grad, stream);
+}
+
+int dlx_rowdot_link_grad(const double* d_x, const int64_t* d_y, int64_t n, int32_t d, const double* d_theta,
+                         const dlx_link_code* h_link, double* d_h, double* d_grad, void* d_workspace,
+                         size_t workspace_bytes, dlx_stream_t stream) {
+  DLX_REQUIRE(n >= 0 && d > 0 && h_link, DLX_ERR_ARG, "rowdot_link_grad: bad arguments");
+  DLX_REQUIRE(h_link->n >= 0 && h_link->n <= DLX_LINK_MAX_CODE && h_link->out >= 0 && h_link->out < DLX_LINK_MAX_REGS,
+              DLX_ERR_ARG, "rowdot_link_grad: bad link code");
+  for (int q = 0; q < h_link->n; ++q)
+    DLX_REQUIRE(h_link->dst[q] < DLX_LINK_MAX_REGS && h_link->a[q] < DLX_LINK_MAX_REGS && h_link->b[q] < DLX_LINK_MAX_REGS &&
+                h_link->op[q] <= DLX_LINK_SQRT, DLX_ERR_ARG, "rowdot_link_grad: bad link instruction %d", q);
+  DLX_REQUIRE(d % 2 == 0 && m_for(d) <= kMaxM, DLX_ERR_GENERATION,
+              "GenerationFailed: the row-dot gradient needs even d <= %d (got %d)", 64 * kMaxM, d);
+  const int grid = row_grid(n);
+  const size_t need = static_cast<size_t>(grid) * d * sizeof(double);
+  DLX_REQUIRE(d_workspace && workspace_bytes >= need, DLX_ERR_ARG, "rowdot_link_grad: workspace too small");
+  double* parts = static_cast<double*>(d_workspace);
+  const size_t smem = static_cast<size_t>(kRowWarps) * d * sizeof(double);
+  const long long* y = reinterpret_cast<const long long*>(d_y);
+  const CodeLink link{*h_link};
+#define DLX_RDL(MM)                                                                                              \
+  (d_h ? launch_pdl(logreg_grad_kernel<MM, CodeLink, true>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, \
+                    d_theta, link, d_h, parts)                                                                   \
+       : launch_pdl(logreg_grad_kernel<MM, CodeLink, false>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, \
+                    d_theta, link, nullptr, parts))
+  switch (m_for(d)) {
+    case 1: DLX_CUDA(DLX_RDL(1)); break;
+    case 2: DLX_CUDA(DLX_RDL(2)); break;
+    case 3: DLX_CUDA(DLX_RDL(3)); break;
+    default: DLX_CUDA(DLX_RDL(4)); break;
+  }
+#undef DLX_RDL
   DLX_LAUNCHED("logreg_grad_kernel");
   return combine_f64(parts, grid, d, d_grad, stream);
 }

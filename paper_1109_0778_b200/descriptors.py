@@ -237,6 +237,111 @@ def gda_program(n: int, d: int) -> dict:
     return {"format": "dlx-program/1", "root": 0, "stmts": B.stmts, "blocks": B.blocks}
 
 
+def groupby_program(n: int, K: int) -> dict:
+    """The staged program of integration/stage_programs.cpp::groupby(n, K) (pinned statement by
+    statement to the reference-staged groupby_n100000_k16 fixture): keys = randIntVector(n, K),
+    ONE fused loop of K count reduces predicated on keys(i) == b (vectordsl.cpp:138-151), every
+    count printed."""
+    B = _Builder()
+    root: list[int] = []
+    VI = "Vector[Int]"
+    keys = B.stmt(root, "VectorRandInt", VI, [B.i(n), B.i(K)])
+    i = B.sym()
+    outs, elems = [], []
+    for b in range(K):
+        cb: list[int] = []
+        kv = B.stmt(cb, "VectorApply", "Int", [B.s(keys, VI), B.s(i, "Int")])
+        q = B.stmt(cb, "Eq", "Bool", [B.s(kv, "Int"), B.i(b)])
+        o = B.sym()
+        outs.append(o)
+        elems.append(B.reduce_elem(o, "Int", B.block([], B.i(1)), B.block(cb, B.s(q, "Bool")), B.i(0)))
+    B.stmts[str(outs[0])] = {"op": "ParallelLoop", "ty": "Int", "args": [],
+                             "loop": {"range": B.i(n), "index": i, "body": B.block([], {"u": 1, "t": "Unit"}, bound=[i]),
+                                      "elems": elems}}
+    root.append(outs[0])
+    for o in outs:
+        B.stmt(root, "Print", "Unit", [B.s(o, "Int")])
+    B.blocks["0"] = {"stmts": root, "result": {"u": 1, "t": "Unit"}, "bound": []}
+    return {"format": "dlx-program/1", "root": 0, "stmts": B.stmts, "blocks": B.blocks}
+
+
+def logreg_program(n: int, d: int, iters: int, alpha: float, link: str = "sigmoid") -> dict:
+    """The staged program of integration/stage_programs.cpp::logreg(n, d, iters, alpha) in the
+    shape the reference's staging + fusion produce (tests/test_descriptors.py compares the softsign
+    form statement by statement with the reference-staged logreg_n20000_d8_it2 fixture):
+    x = randVector(n*d), y = randIntVector(n, 2), theta = zeros(d); per iteration ONE fused loop of
+    a collect h(i) = link(theta . x_i) (printed: h escapes) and d gradient reduces
+    (h(i) - toDouble(y(i))) * x(i*d + j), then theta(j) = theta(j) - alpha * g_j on the host;
+    theta printed at the end.  link: "softsign" t / (1 + |t|) (the reference has no exp,
+    node.hpp:15-27) or "sigmoid" 1 / (1 + exp(0 - t)) (the MathExp extension)."""
+    B = _Builder()
+    root: list[int] = []
+    VD, VI = "Vector[Double]", "Vector[Int]"
+    x = B.stmt(root, "VectorRand", VD, [B.i(n * d)])
+    y = B.stmt(root, "VectorRandInt", VI, [B.i(n), B.i(2)])
+    th = B.stmt(root, "VectorNew", VD, [B.i(d)], aux_ty="Double")
+    for _ in range(iters):
+        i = B.sym()
+        h = B.sym()
+        # collect elem: the dot (one nested reduce over j), then the link
+        eb: list[int] = []
+        j = B.sym()
+        dot = B.sym()
+        body: list[int] = []
+        row = B.stmt(body, "Times", "Int", [B.i(d), B.s(i, "Int")])
+        xi = B.stmt(body, "Plus", "Int", [B.s(row, "Int"), B.s(j, "Int")])
+        xv = B.stmt(body, "VectorApply", "Double", [B.s(x, VD), B.s(xi, "Int")])
+        tv = B.stmt(body, "VectorApply", "Double", [B.s(th, VD), B.s(j, "Int")])
+        pr = B.stmt(body, "Times", "Double", [B.s(tv, "Double"), B.s(xv, "Double")])
+        inner = B.reduce_elem(dot, "Double", B.block(body, B.s(pr, "Double")), -1, B.d(0.0))
+        B.stmts[str(dot)] = {"op": "ParallelLoop", "ty": "Double", "args": [],
+                             "loop": {"range": B.i(d), "index": j, "body": B.block([], {"u": 1, "t": "Unit"}, bound=[j]),
+                                      "elems": [inner]}}
+        eb.append(dot)
+        if link == "softsign":
+            ab = B.stmt(eb, "MathAbs", "Double", [B.s(dot, "Double")])
+            den = B.stmt(eb, "Plus", "Double", [B.d(1.0), B.s(ab, "Double")])
+            hv = B.stmt(eb, "Divide", "Double", [B.s(dot, "Double"), B.s(den, "Double")])
+        elif link == "sigmoid":
+            neg = B.stmt(eb, "Minus", "Double", [B.d(0.0), B.s(dot, "Double")])
+            ex = B.stmt(eb, "MathExp", "Double", [B.s(neg, "Double")])
+            den = B.stmt(eb, "Plus", "Double", [B.d(1.0), B.s(ex, "Double")])
+            hv = B.stmt(eb, "Divide", "Double", [B.d(1.0), B.s(den, "Double")])
+        else:
+            raise ValueError(link)
+        elems = [{"kind": "collect", "live": True, "out": h, "out_ty": VD, "elem": B.block(eb, B.s(hv, "Double")),
+                  "cond": -1, "combine": -1, "append": False}]
+        grads = []
+        for jj in range(d):
+            body = []
+            row = B.stmt(body, "Times", "Int", [B.i(d), B.s(i, "Int")])
+            ix = row if jj == 0 else B.stmt(body, "Plus", "Int", [B.i(jj), B.s(row, "Int")])
+            xv = B.stmt(body, "VectorApply", "Double", [B.s(x, VD), B.s(ix, "Int")])
+            yv = B.stmt(body, "VectorApply", "Int", [B.s(y, VI), B.s(i, "Int")])
+            yd = B.stmt(body, "ToDouble", "Double", [B.s(yv, "Int")])
+            r = B.stmt(body, "Minus", "Double", [B.s(hv, "Double"), B.s(yd, "Double")])
+            pr = B.stmt(body, "Times", "Double", [B.s(r, "Double"), B.s(xv, "Double")])
+            g = B.sym()
+            grads.append(g)
+            elems.append(B.reduce_elem(g, "Double", B.block(body, B.s(pr, "Double")), -1, B.d(0.0)))
+        B.stmts[str(h)] = {"op": "ParallelLoop", "ty": VD, "args": [],
+                           "loop": {"range": B.i(n), "index": i, "body": B.block([], {"u": 1, "t": "Unit"}, bound=[i]),
+                                    "elems": elems}}
+        root.append(h)
+        h0 = B.stmt(root, "VectorApply", "Double", [B.s(h, VD), B.i(0)])
+        B.stmt(root, "Print", "Unit", [B.s(h0, "Double")])
+        for jj in range(d):
+            t = B.stmt(root, "Times", "Double", [B.d(alpha), B.s(grads[jj], "Double")])
+            a = B.stmt(root, "VectorApply", "Double", [B.s(th, VD), B.i(jj)])
+            m = B.stmt(root, "Minus", "Double", [B.s(a, "Double"), B.s(t, "Double")])
+            B.stmt(root, "VectorUpdate", "Unit", [B.s(th, VD), B.i(jj), B.s(m, "Double")])
+    for jj in range(d):
+        v = B.stmt(root, "VectorApply", "Double", [B.s(th, VD), B.i(jj)])
+        B.stmt(root, "Print", "Unit", [B.s(v, "Double")])
+    B.blocks["0"] = {"stmts": root, "result": {"u": 1, "t": "Unit"}, "bound": []}
+    return {"format": "dlx-program/1", "root": 0, "stmts": B.stmts, "blocks": B.blocks}
+
+
 if __name__ == "__main__":   # python -m paper_1109_0778_b200.descriptors N D K ITERS > out.json
     import sys
     n, d, k, it = (int(v) for v in sys.argv[1:5])

@@ -83,6 +83,29 @@ def test_gda_program_is_the_reference_staged_program():
     assert got == exp, first_diff(got, exp)
 
 
+def test_groupby_program_is_the_reference_staged_program():
+    got, exp = canon(D.groupby_program(100000, 16)), canon(load("groupby_n100000_k16"))
+    assert got == exp, first_diff(got, exp)
+
+
+def test_logreg_program_is_the_reference_staged_program():
+    got = canon(D.logreg_program(20000, 8, 2, 1.0 / 20000, link="softsign"))
+    exp = canon(load("logreg_n20000_d8_it2"))
+    assert got == exp, first_diff(got, exp)
+
+
+@pytest.mark.parametrize("link", ["softsign", "sigmoid"])
+def test_logreg_program_c2_lowers_to_logistic_with_device_update(link):
+    """C2 (N = 1M, d = 64, 20 BGD iterations) through the drop-in: every iteration's fused loop
+    (1 collect + 64 gradient reduces) lowers to the logistic family and its 64 host updates
+    theta(j) = theta(j) - alpha * g_j run on the device (UpdateGroup::Axpy)."""
+    from paper_1109_0778_b200.program import Program
+    n, d, it = 1 << 20, 64, 20
+    r = Program(D.logreg_program(n, d, it, 1.0 / n, link=link)).run(dry_run=True)
+    assert [e["family"] for e in r.report] == ["logistic"] * it
+    assert all(e["update"] == "device" and e["live_elems"] == 1 + d for e in r.report)
+
+
 @pytest.mark.parametrize("name,shape", [("kmeans_n4096_d16_k8_it2", (4096, 16, 8, 2)),
                                         ("kmeans_n65536_d16_k8_it1", (65536, 16, 8, 1))])
 def test_kmeans_program_is_the_reference_staged_program(name, shape):

@@ -118,6 +118,45 @@ def test_c4_kmeans_program_matches_family_api():
     del x
 
 
+def test_c2_logreg_twenty_iterations_through_the_dropin():
+    """BASELINE C2 (logistic regression BGD, N = 1M, d = 64, 20 iterations) as ONE staged program
+    of 20 fused loops (collect h = sigmoid(theta . x_i) + 64 gradient reduces, theta updated on
+    the device): theta after 20 iterations and h(0) of every iteration against the family API
+    (LogRegProgram, itself pinned to the oracle) at rtol 1e-9, and the first iteration's h(0)
+    against the oracle."""
+    import torch
+    from paper_1109_0778_b200 import multiloops as ml
+    from paper_1109_0778_b200.programs import LogRegProgram
+    from paper_1109_0778_b200.program import Program
+    n, d, it = 1 << 20, 64, 20
+    r = Program(D.logreg_program(n, d, it, 1.0 / n, link="sigmoid")).run(seed=1)
+    assert all(e["family"] == "logistic" and e["update"] == "device" for e in r.report)
+    out = [float(v) for v in lines(r.output)]
+    assert len(out) == it + d
+    dev = torch.device("cuda")
+    x = ml.rng_units(n * d, seed=1, device=dev).view(n, d)
+    y = ml.rng_ints(n, 2, seed=1, first_draw=n * d, device=dev)
+    prog = LogRegProgram(x, y, torch.zeros(d, dtype=torch.float64, device=dev), 1.0 / n)
+    for t in range(it):
+        h0 = 1.0 / (1.0 + math.exp(0.0 - float((prog.theta * x[0]).sum().item())))
+        assert close(out[t], h0, rtol=1e-12), t
+        prog.run(1)
+    np.testing.assert_allclose(out[it:], prog.theta.cpu().numpy(), rtol=1e-9, atol=1e-15)
+
+
+@pytest.mark.parametrize("K", [64, 4096])
+def test_c5_groupby_1e9_keys_through_the_dropin(golden, K):
+    """BASELINE C5 (1e9 keys) as the reference stages it (one loop of K count reduces keyed on
+    keys(i) == b) through the drop-in: bit-exact against App. B (first, last, min, max)."""
+    from paper_1109_0778_b200.program import Program
+    r = Program(D.groupby_program(1_000_000_000, K)).run(seed=1)
+    assert [e["family"] for e in r.report] == ["groupby"]
+    c = [int(v) for v in lines(r.output)]
+    g = golden["c5_groupby"]["by_k"][str(K)]
+    assert len(c) == K and sum(c) == 1_000_000_000
+    assert (c[0], c[-1], min(c), max(c)) == (g["first"], g["last"], g["min"], g["max"])
+
+
 def _collect_program(n):
     """x = randVector(n); y = collect(i -> 2.5 * x(i)); s = sum(y); print s; result y."""
     B = D._Builder()
@@ -184,3 +223,20 @@ def test_prints_of_pending_results_keep_program_order():
     assert max(e["in_flight"] for e in a.report) >= 1     # no host sync between iterations
     assert all(e["in_flight"] == 0 for e in b.report)
     assert not math.isnan(float(lines(a.output)[-1]))
+
+
+def test_reference_side_binding_run_staged():
+    """The C++ reference-side binding (integration/stagekit_dlx_run.cpp: run_on_b200, what a
+    stagekit `run` pipeline calls instead of interpret / executeDEG) end to end: programs staged
+    with the REFERENCE DSL, fused and scheduled by the reference's own passes, executed through
+    dlx_program_create / _execute and compared with the reference's emitted MiniC evaluated on
+    the CPU (oracle/_ref/run_staged, built from /root/reference by oracle/ref.mk where the
+    reference exists; it ships prebuilt to the GPU box)."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "run_staged")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/run_staged not built (no /root/reference where the repo was built)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("PASS") == 4 and "FAIL" not in r.stdout, r.stdout

@@ -43,6 +43,7 @@ def same_value(a: str, b: str, rtol=1e-9) -> bool:
 def test_fixtures_present():
     names = {os.path.basename(f)[:-5] for f in FIXTURES}
     for n in ("kmeans_n65536_d16_k8_it1", "kmeans_n4096_d16_k8_it2", "groupby_n100000_k16", "gda_n20000_d4",
+              "logreg_n20000_d8_it2",
               "mean_variance_n100000", "axpy_n100000", "count_gt_n100000", "find_count_n100000"):
         assert n in names
     for f in FIXTURES:
@@ -114,6 +115,8 @@ def test_staged_program_on_b200(path):
         assert fams == ["groupby"]
     if name.startswith("gda"):
         assert fams == ["bucket_rows", "gda_scatter"]
+    if name.startswith("logreg"):
+        assert fams == ["logistic", "logistic"] and all(r["update"] == "device" for r in report)
 
 
 @pytest.mark.gpu
@@ -179,6 +182,7 @@ EXPECTED_FAMILIES = {
     "groupby_n100000_k16": ["groupby"],
     "kmeans_n4096_d16_k8_it2": ["kmeans", "kmeans"],
     "kmeans_n65536_d16_k8_it1": ["kmeans"],
+    "logreg_n20000_d8_it2": ["logistic", "logistic"],
     "mean_variance_n100000": ["generic"],
 }
 
