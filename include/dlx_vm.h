@@ -29,8 +29,8 @@ extern "C" {
 enum dlx_vm_op {
   DLX_VM_CONST = 0, /* dst = imm (64-bit pattern) */
   DLX_VM_IDX,       /* dst = loop index */
-  DLX_VM_LOAD,      /* dst = vec[aux][reg a]  (bounds-checked: trap bit 2) */
-  DLX_VM_ADD_I, DLX_VM_SUB_I, DLX_VM_MUL_I, DLX_VM_DIV_I, /* int64, wraparound; /0 -> trap bit 1 */
+  DLX_VM_LOAD,      /* dst = vec[aux][reg a]  (bounds-checked: DLX_VM_TRAP_BOUNDS) */
+  DLX_VM_ADD_I, DLX_VM_SUB_I, DLX_VM_MUL_I, DLX_VM_DIV_I, /* int64, wraparound; /0 -> DLX_VM_TRAP_DIV0 */
   DLX_VM_ADD_D, DLX_VM_SUB_D, DLX_VM_MUL_D, DLX_VM_DIV_D, /* fp64, round-to-nearest, no FMA */
   DLX_VM_LT_I, DLX_VM_LT_D, DLX_VM_EQ_I, DLX_VM_EQ_D,
   DLX_VM_AND, DLX_VM_OR, DLX_VM_NOT,
@@ -73,9 +73,14 @@ typedef struct {
  * elems the per-CTA counts and offsets) */
 size_t dlx_vm_workspace_bytes(int64_t range);
 /* d_code: ncode instructions in device memory; d_results: DLX_VM_MAX_ELEMS 64-bit slots;
- * d_trap: device int, OR-ed with 1 (int division by zero), 2 (index out of bounds). */
+ * d_trap: one device uint64 the caller sets to UINT64_MAX; it ends as the minimum over trapped
+ * indices of (index << 2 | DLX_VM_TRAP_*), i.e. the first trap sequential execution meets
+ * (UINT64_MAX: none). */
+#define DLX_VM_TRAP_DIV0 1   /* Int division by zero (TrapDivByZero) */
+#define DLX_VM_TRAP_BOUNDS 2 /* element load out of range (TrapIndexOutOfBounds) */
+#define DLX_VM_TRAP_BADOP 3  /* unknown instruction (GenerationFailed) */
 int dlx_vm_run_loop(const dlx_vm_instr* d_code, const dlx_vm_loop* h_loop, int64_t* d_results,
-                    int* d_trap, void* d_workspace, size_t workspace_bytes, dlx_stream_t stream);
+                    uint64_t* d_trap, void* d_workspace, size_t workspace_bytes, dlx_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -1288,7 +1288,7 @@ void Executor::launch_generic(LoopPlan& p, int64_t n, std::vector<VecP>& V) {
   const size_t code_bytes = std::max<size_t>(1, p.code.size()) * sizeof(dlx_vm_instr);
   auto* dcode = static_cast<dlx_vm_instr*>(dalloc(code_bytes));
   auto* dres = static_cast<int64_t*>(dalloc((DLX_VM_MAX_ELEMS + 1) * 8));   // results, then the trap word
-  int* dtrap = reinterpret_cast<int*>(dres + DLX_VM_MAX_ELEMS);
+  auto* dtrap = reinterpret_cast<uint64_t*>(dres + DLX_VM_MAX_ELEMS);
   void* ws = dalloc(wsb);
   // staged through pinned memory so the copies (and the launch) do not block the host
   auto* hcode = res_->pin.get_n<dlx_vm_instr>(std::max<size_t>(1, p.code.size()));
@@ -1297,6 +1297,7 @@ void Executor::launch_generic(LoopPlan& p, int64_t n, std::vector<VecP>& V) {
   auto* zeros = res_->pin.get_n<int64_t>(DLX_VM_MAX_ELEMS + 1);
   std::memset(zeros, 0, (DLX_VM_MAX_ELEMS + 1) * 8);
   for (int q = 0; q < L.nelems; ++q) zeros[q] = L.elem[q].zero;
+  zeros[DLX_VM_MAX_ELEMS] = -1;   // the trap word: UINT64_MAX = no trap
   cudaMemcpyAsync(dcode, hcode, p.code.size() * sizeof(dlx_vm_instr), cudaMemcpyHostToDevice, lst_);
   cudaMemcpyAsync(dres, zeros, (DLX_VM_MAX_ELEMS + 1) * 8, cudaMemcpyHostToDevice, lst_);
   int rc = dlx_vm_run_loop(dcode, &L, dres, dtrap, ws, wsb, lst_);
@@ -1313,11 +1314,16 @@ void Executor::launch_generic(LoopPlan& p, int64_t n, std::vector<VecP>& V) {
   for (int q = 0; q < L.nelems; ++q) append[q] = L.elem[q].kind == DLX_VM_APPEND;
   // deferred binding: traps and appended lengths are known only when the loop completes
   complete_loop(out_syms, [this, res, po, outs, append] {
-    int htrap;
-    std::memcpy(&htrap, res + DLX_VM_MAX_ELEMS, sizeof(int));
-    if (htrap & 1) trap("TrapDivByZero: integer division by zero in a multiloop");
-    if (htrap & 2) trap("TrapIndexOutOfBounds: element load out of range in a multiloop");
-    if (htrap & 4) gen_fail("generic kernel met an unknown instruction");
+    uint64_t htrap;
+    std::memcpy(&htrap, res + DLX_VM_MAX_ELEMS, sizeof(htrap));
+    if (htrap != ~0ull) {   // the first trap in index order, as sequential execution meets it
+      const std::string at = " at index " + std::to_string(htrap >> 2);
+      switch (static_cast<int>(htrap & 3)) {
+        case DLX_VM_TRAP_DIV0: trap("TrapDivByZero: integer division by zero in a multiloop" + at);
+        case DLX_VM_TRAP_BOUNDS: trap("TrapIndexOutOfBounds: element load out of range in a multiloop" + at);
+        default: gen_fail("generic kernel met an unknown instruction");
+      }
+    }
     for (const LoopPlan::Out& o : po) {
       if (o.src == 1) {
         const VecP& v = outs[o.ix];

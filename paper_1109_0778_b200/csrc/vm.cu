@@ -8,7 +8,7 @@
 // Reduce slots fold per thread, then warp / CTA trees, then the deterministic combine of
 // per-CTA partials (combine.cu).  fp64 arithmetic uses explicit _rn intrinsics (no FMA
 // contraction) so collects are bit-identical to the reference; Int arithmetic wraps; Int
-// division by zero and out-of-range loads raise the trap flag (TrapError on the host).
+// division by zero and out-of-range loads record the first trap in index order (TrapError on the host).
 // Filter-collect (append) elems make the launch order-preserving: a count pass over contiguous
 // per-CTA index ranges, an exclusive scan of the per-CTA counts, then the main pass writes each
 // CTA's selected values at its offset with a block-wide ballot scan per 256-index step, so the
@@ -27,8 +27,18 @@ union Reg {
 
 constexpr int kVmThreads = 256;
 
-__device__ __forceinline__ void vm_exec(const dlx_vm_instr* __restrict__ code, int begin, int end,
-                                        Reg* r, long long idx, const dlx_vm_loop* L, int* trap) {
+// record a trap of index idx: the word keeps the minimum (idx << 2 | kind), i.e. the first trap
+// in index order, as sequential interpret stops at it (codegen.cpp:391-425: indices ascend, and
+// within an index the body and the elems run in program order)
+__device__ __forceinline__ void vm_trap(unsigned long long* trap, long long idx, int kind) {
+  atomicMin(trap, (static_cast<unsigned long long>(idx) << 2) | static_cast<unsigned long long>(kind));
+}
+
+// runs code[begin, end) for index idx; false once it trapped (the caller then abandons the index,
+// so no later statement or elem of it runs and no second trap of it is recorded)
+__device__ __forceinline__ bool vm_exec(const dlx_vm_instr* __restrict__ code, int begin, int end,
+                                        Reg* r, long long idx, const dlx_vm_loop* L,
+                                        unsigned long long* trap) {
   for (int pc = begin; pc < end; ++pc) {
     const dlx_vm_instr in = code[pc];
     Reg& d = r[in.dst];
@@ -39,8 +49,8 @@ __device__ __forceinline__ void vm_exec(const dlx_vm_instr* __restrict__ code, i
       case DLX_VM_LOAD: {
         const long long k = a.i;
         if (k < 0 || k >= L->vec_len[in.aux]) {
-          atomicOr(trap, 2);
-          d.i = 0;
+          vm_trap(trap, idx, DLX_VM_TRAP_BOUNDS);
+          return false;
         } else if (L->vec_kind[in.aux] == DLX_VM_F64) {
           d.d = static_cast<const double*>(L->vec[in.aux])[k];
         } else if (L->vec_kind[in.aux] == DLX_VM_I64) {
@@ -55,8 +65,8 @@ __device__ __forceinline__ void vm_exec(const dlx_vm_instr* __restrict__ code, i
       case DLX_VM_MUL_I: d.i = static_cast<long long>(static_cast<unsigned long long>(a.i) * static_cast<unsigned long long>(b.i)); break;
       case DLX_VM_DIV_I:
         if (b.i == 0) {
-          atomicOr(trap, 1);
-          d.i = 0;
+          vm_trap(trap, idx, DLX_VM_TRAP_DIV0);
+          return false;
         } else {
           d.i = (a.i == LLONG_MIN && b.i == -1) ? a.i : a.i / b.i;
         }
@@ -78,9 +88,10 @@ __device__ __forceinline__ void vm_exec(const dlx_vm_instr* __restrict__ code, i
       case DLX_VM_EXP: d.d = exp(a.d); break;
       case DLX_VM_TODBL: d.d = static_cast<double>(a.i); break;
       case DLX_VM_SEL: d = r[in.imm].i ? a : b; break;  // imm holds the condition register
-      default: atomicOr(trap, 4); break;
+      default: vm_trap(trap, idx, DLX_VM_TRAP_BADOP); return false;
     }
   }
+  return true;
 }
 
 __device__ __forceinline__ void vm_store(const dlx_vm_elem& el, long long at, Reg v) {
@@ -98,7 +109,7 @@ __device__ __forceinline__ void vm_chunk(long long range, long long chunk, long 
 // count pass: how many indices of this CTA's range each append elem selects
 __global__ void __launch_bounds__(kVmThreads)
 vm_count_kernel(const dlx_vm_instr* __restrict__ code, dlx_vm_loop L, long long chunk,
-                long long* __restrict__ counts, int* __restrict__ trap) {
+                long long* __restrict__ counts, unsigned long long* __restrict__ trap) {
   __shared__ dlx_vm_instr code_s[DLX_VM_MAX_CODE];
   __shared__ long long cnt_s[DLX_VM_MAX_ELEMS];
   for (int e = threadIdx.x; e < L.ncode; e += kVmThreads) code_s[e] = code[e];
@@ -110,13 +121,13 @@ vm_count_kernel(const dlx_vm_instr* __restrict__ code, dlx_vm_loop L, long long 
   int my[DLX_VM_MAX_ELEMS];
   for (int e = 0; e < L.nelems; ++e) my[e] = 0;
   for (long long i = lo + threadIdx.x; i < hi; i += kVmThreads) {
-    vm_exec(code_s, 0, L.body_end, r, i, &L, trap);
+    if (!vm_exec(code_s, 0, L.body_end, r, i, &L, trap)) continue;
     for (int e = 0; e < L.nelems; ++e) {
       const dlx_vm_elem& el = L.elem[e];
       if (el.kind != DLX_VM_APPEND) continue;
       bool take = true;
       if (el.cond_end > el.cond_begin) {
-        vm_exec(code_s, el.cond_begin, el.cond_end, r, i, &L, trap);
+        if (!vm_exec(code_s, el.cond_begin, el.cond_end, r, i, &L, trap)) break;
         take = r[el.cond_reg].i != 0;
       }
       my[e] += take;
@@ -148,7 +159,7 @@ __global__ void vm_scan_kernel(const long long* __restrict__ counts, int nblocks
 
 __global__ void __launch_bounds__(kVmThreads)
 vm_loop_kernel(const dlx_vm_instr* __restrict__ code, dlx_vm_loop L, Reg* __restrict__ parts,
-               int* __restrict__ trap, long long chunk, const long long* __restrict__ offsets) {
+               unsigned long long* __restrict__ trap, long long chunk, const long long* __restrict__ offsets) {
   __shared__ dlx_vm_instr code_s[DLX_VM_MAX_CODE];
   __shared__ Reg red_s[kVmThreads / 32][DLX_VM_MAX_ELEMS];
   __shared__ int wsum_s[kVmThreads / 32];
@@ -180,19 +191,22 @@ vm_loop_kernel(const dlx_vm_instr* __restrict__ code, dlx_vm_loop L, Reg* __rest
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (; i < stop; i += step) {
     const long long idx = i + threadIdx.x;
-    const bool live = idx < stop;
-    if (live) vm_exec(code_s, 0, L.body_end, r, idx, &L, trap);
+    bool live = idx < stop;
+    if (live) live = vm_exec(code_s, 0, L.body_end, r, idx, &L, trap);
     for (int e = 0; e < L.nelems; ++e) {
       const dlx_vm_elem& el = L.elem[e];
+      // a trapped index stays `live == false` for its remaining elems (the loop is abandoned
+      // on the host anyway; every thread still reaches the append scans below)
       bool take = live;
       if (live && el.cond_end > el.cond_begin) {
-        vm_exec(code_s, el.cond_begin, el.cond_end, r, idx, &L, trap);
-        take = r[el.cond_reg].i != 0;
+        live = vm_exec(code_s, el.cond_begin, el.cond_end, r, idx, &L, trap);
+        take = live && r[el.cond_reg].i != 0;
       }
       Reg v;
       v.i = 0;
       if (take) {
-        vm_exec(code_s, el.value_begin, el.value_end, r, idx, &L, trap);
+        live = vm_exec(code_s, el.value_begin, el.value_end, r, idx, &L, trap);
+        take = live;
         v = r[el.value_reg];
       }
       if (el.kind == DLX_VM_APPEND) {   // block-uniform branch: every thread reaches the scan
@@ -285,7 +299,7 @@ size_t dlx_vm_workspace_bytes(int64_t range) {
 }
 
 int dlx_vm_run_loop(const dlx_vm_instr* d_code, const dlx_vm_loop* h_loop, int64_t* d_results,
-                    int* d_trap, void* d_workspace, size_t workspace_bytes, dlx_stream_t stream) {
+                    uint64_t* d_trap, void* d_workspace, size_t workspace_bytes, dlx_stream_t stream) {
   DLX_REQUIRE(h_loop && d_code && d_trap && d_results, DLX_ERR_ARG, "vm: null argument");
   const dlx_vm_loop& L = *h_loop;
   DLX_REQUIRE(L.ncode <= DLX_VM_MAX_CODE && L.nelems <= DLX_VM_MAX_ELEMS && L.range >= 0,
@@ -305,13 +319,15 @@ int dlx_vm_run_loop(const dlx_vm_instr* d_code, const dlx_vm_loop* h_loop, int64
   long long chunk = 0;
   if (append) {
     chunk = (L.range + grid - 1) / grid;
-    vm_count_kernel<<<grid, kVmThreads, 0, stream>>>(d_code, L, chunk, counts, d_trap);
+    vm_count_kernel<<<grid, kVmThreads, 0, stream>>>(d_code, L, chunk, counts,
+                                                     reinterpret_cast<unsigned long long*>(d_trap));
     DLX_LAUNCHED("vm_count_kernel");
     vm_scan_kernel<<<1, DLX_VM_MAX_ELEMS, 0, stream>>>(counts, grid, L, offsets,
                                                        reinterpret_cast<long long*>(d_results));
     DLX_LAUNCHED("vm_scan_kernel");
   }
-  vm_loop_kernel<<<grid, kVmThreads, 0, stream>>>(d_code, L, parts, d_trap, chunk, offsets);
+  vm_loop_kernel<<<grid, kVmThreads, 0, stream>>>(d_code, L, parts, reinterpret_cast<unsigned long long*>(d_trap),
+                                                  chunk, offsets);
   DLX_LAUNCHED("vm_loop_kernel");
   vm_final_kernel<<<1, DLX_VM_MAX_ELEMS, 0, stream>>>(parts, grid, L, reinterpret_cast<long long*>(d_results));
   DLX_LAUNCHED("vm_final_kernel");

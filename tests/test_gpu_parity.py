@@ -228,6 +228,30 @@ def test_c4_first_two_iterations(ml, golden, oracle_hashes, method):
         mu = torch.from_numpy(O.kmeans_update(c_ref, s_ref)).cuda()
 
 
+def test_c4_free_running_ten_iterations(ml, golden):
+    """the GPU and the oracle each run C4's 10 iterations on their OWN centroids (no
+    re-seeding from the oracle); the number of assignments that differ per iteration is 0 and
+    the counts agree exactly, so the fp64 sum-order differences (rtol 1e-9) never flip a
+    nearest-centroid decision at this workload."""
+    g = golden["c4_kmeans"]
+    n, d, k = g["n"], g["d"], g["k"]
+    x = dev_units(ml, n, d)
+    xh = x.cpu().numpy()
+    mu_g = x[:k].clone()
+    mu_o = xh[:k].copy()
+    diffs = []
+    for it in range(10):
+        a, c, s = ml.kmeans_step(x, mu_g)
+        a_o, c_o, s_o = O.kmeans_step(xh, k, mu_o, workers=O.threads(), chunks=4 * O.threads())
+        diffs.append(int(np.count_nonzero(a.cpu().numpy().astype(np.int64) != a_o)))
+        assert c.cpu().numpy().tolist() == c_o.tolist(), (it, diffs)
+        np.testing.assert_allclose(s.cpu().numpy(), s_o, rtol=RTOL)
+        mu_g = ml.kmeans_update(c, s)
+        mu_o = O.kmeans_update(c_o, s_o)
+        np.testing.assert_allclose(mu_g.cpu().numpy(), mu_o, rtol=RTOL)
+    assert diffs == [0] * 10
+
+
 # ---- GroupBy ------------------------------------------------------------------------------------
 
 @pytest.mark.parametrize("n,K", [(1, 64), (1001, 64), (1_000_003, 64), (1_000_000, 4096), (999_999, 65536),

@@ -42,7 +42,8 @@ def same_value(a: str, b: str, rtol=1e-9) -> bool:
 
 def test_fixtures_present():
     names = {os.path.basename(f)[:-5] for f in FIXTURES}
-    for n in ("kmeans_n65536_d16_k8_it1", "kmeans_n4096_d16_k8_it2", "groupby_n100000_k16", "gda_n20000_d4",
+    for n in ("kmeans_n65536_d16_k8_it1", "kmeans_n4096_d16_k8_it2", "kmeans_n4096_d16_k8_it2_assign",
+              "groupby_n100000_k16", "gda_n20000_d4",
               "logreg_n20000_d8_it2",
               "mean_variance_n100000", "axpy_n100000", "count_gt_n100000", "find_count_n100000"):
         assert n in names
@@ -71,6 +72,24 @@ def test_staged_kmeans_matches_oracle_port():
         got.append(str(int(assign[0])))
         got += [str(int(c)) for c in counts]
     got += [O.format_double(v) for v in hist[-1][2].reshape(-1)]
+    assert exp == got
+
+
+def test_staged_kmeans_every_assignment_matches_oracle_port():
+    """The reference-staged program that prints the WHOLE assignment vector after each of its two
+    iterations (integration/stage_programs.cpp kmeans(..., all_assign)): the oracle's assignments
+    equal, element by element, what the reference's own emitted MiniC computes."""
+    fx = load("kmeans_n4096_d16_k8_it2_assign")
+    n, d, k = 4096, 16, 8
+    x, mu0 = O.kmeans_inputs(n, d, k)
+    hist = O.kmeans_run(x, k, 2, mu0)
+    exp = lines(fx["expected"])
+    got = []
+    for counts, _, _, _, assign in hist:
+        got += [str(int(a)) for a in assign]
+        got += [str(int(c)) for c in counts]
+    got += [O.format_double(v) for v in hist[-1][2].reshape(-1)]
+    assert len(exp) == 2 * (n + k) + k * d
     assert exp == got
 
 
@@ -346,6 +365,44 @@ def test_two_trapping_loops_dry_run(monkeypatch):
     monkeypatch.setenv("DLX_PROGRAM_DRYRUN", "1")
     _, report = run_program(_two_trapping_loops(), seed=1)
     assert [r["family"] for r in report] == ["generic", "generic"]
+
+
+def _one_loop_two_traps(off):
+    """One root loop over i < 100 with two reduce elems: the first divides by (i - 5) (Int),
+    the second loads v(i + off) from a 10-element vector (out of range from i = 10 - off)."""
+    from paper_1109_0778_b200.descriptors import _Builder
+    B = _Builder()
+    root = []
+    v = B.stmt(root, "VectorNew", "Vector[Double]", [B.i(10)], aux_ty="Double")
+    i, out = B.sym(), B.sym()
+    b1, b2 = [], []
+    m = B.stmt(b1, "Minus", "Int", [B.s(i, "Int"), B.i(5)])
+    q = B.stmt(b1, "Divide", "Int", [B.i(1), B.s(m, "Int")])
+    e1 = B.reduce_elem(out, "Int", B.block(b1, B.s(q, "Int")), -1, B.i(0))
+    ix = B.stmt(b2, "Plus", "Int", [B.s(i, "Int"), B.i(off)])
+    ld = B.stmt(b2, "VectorApply", "Double", [B.s(v, "Vector[Double]"), B.s(ix, "Int")])
+    e2 = B.reduce_elem(B.sym(), "Double", B.block(b2, B.s(ld, "Double")), -1, B.d(0.0))
+    B.stmts[str(out)] = {"op": "ParallelLoop", "ty": "Int", "args": [],
+                         "loop": {"range": B.i(100), "index": i, "body": B.block([], {"u": 1, "t": "Unit"}, bound=[i]),
+                                  "elems": [e1, e2]}}
+    root.append(out)
+    B.stmt(root, "Print", "Unit", [B.s(out, "Int")])
+    B.stmt(root, "Print", "Unit", [B.s(e2["out"], "Double")])
+    B.blocks["0"] = {"stmts": root, "result": {"u": 1, "t": "Unit"}, "bound": []}
+    return {"format": "dlx-program/1", "root": 0, "stmts": B.stmts, "blocks": B.blocks}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("off,expect", [(7, "TrapIndexOutOfBounds.*index 3"),    # i=3 loads v(10) first
+                                        (5, "TrapDivByZero.*index 5"),          # same index: elem 1 runs first
+                                        (4, "TrapDivByZero.*index 5")])         # i=5 divides before i=6 loads
+def test_first_trap_in_index_order(off, expect):
+    """The reported trap is the one sequential interpret meets first: lowest index, then program
+    order inside the index (codegen.cpp:391-425), whatever order the device threads trap in."""
+    from paper_1109_0778_b200 import TrapError
+    from paper_1109_0778_b200.program import run_program
+    with pytest.raises(TrapError, match=expect):
+        run_program(_one_loop_two_traps(off), seed=1)
 
 
 @pytest.mark.gpu
