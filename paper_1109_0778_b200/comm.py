@@ -22,11 +22,13 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
 
 
 class Comm:
-    def __init__(self, rank: int, world: int, uid: bytes | None = None):
+    def __init__(self, rank: int, world: int, uid: bytes | None = None, force_nccl: bool = False):
+        """force_nccl: build the NCCL communicator even at world 1 (tests of the NCCL path)."""
         L = _lib.load()
         self.rank, self.world = rank, world
         self._h = ctypes.c_void_p()
-        if world > 1:
+        self._nccl = world > 1 or force_nccl
+        if self._nccl:
             assert uid is not None and len(uid) == 128
             check(L.dlx_comm_init(ctypes.byref(self._h), uid, world, rank))
 
@@ -46,7 +48,7 @@ class Comm:
         return cls(rank, world, obj[0])
 
     def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
-        if self.world == 1:
+        if not self._nccl:
             return t
         dtype = {torch.float64: 0, torch.int64: 1}[t.dtype]
         check(_lib.load().dlx_comm_allreduce_sum(self._h, ctypes.c_void_p(t.data_ptr()), t.numel(), dtype,
@@ -55,7 +57,7 @@ class Comm:
 
     def allreduce_many_(self, tensors) -> None:
         """Sum several records in place across ranks with one fused NCCL launch."""
-        if self.world == 1 or not tensors:
+        if not self._nccl or not tensors:
             return
         n = len(tensors)
         bufs = (ctypes.c_void_p * n)(*[t.data_ptr() for t in tensors])
@@ -65,14 +67,14 @@ class Comm:
                                                        ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
 
     def allreduce_int(self, v: int) -> int:
-        if self.world == 1:
+        if not self._nccl:
             return v
         t = torch.tensor([v], dtype=torch.int64, device="cuda")
         self.allreduce_(t)
         return int(t.item())
 
     def close(self):
-        if self.world > 1 and self._h:
+        if self._nccl and self._h:
             check(_lib.load().dlx_comm_destroy(self._h))
             self._h = ctypes.c_void_p()
 

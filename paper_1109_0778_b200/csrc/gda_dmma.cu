@@ -19,7 +19,10 @@
 // DMMA chains on the other D buffer, so centring overlaps the tensor-core phase.  (With four
 // centring warps the tensor-core warps sat on empty D buffers 20% of the time, profile r73;
 // eight suffice for pass 2 alone, twelve keep up with the single-pass fit's class sums, r81.)
+#include <cuda.h>
+
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -350,6 +353,318 @@ gda_pass2_dmma_kernel(const double* __restrict__ x, const long long* __restrict_
   }
 }
 
+// ---- d = 64: the k-split fit (r215-r218) ---------------------------------------------------
+// The kernel above gives each tensor-core warp 3 of the 36 lower 8x8 blocks, so every warp
+// reloads and every centring warp re-stores the whole tile (4 LDS.128 per 6 DMMAs).  Here the
+// split is over samples instead: eight tensor-core warps (two per SM sub-partition, so one
+// warp's loads and centring overlap the other's DMMAs) each own ALL 36 lower blocks (72 fp64
+// accumulators per lane, 36 independent DMMA chains) for 8 of every 64-sample tile's rows, so
+// a k-step costs 4 LDS.128 of x for 36 DMMAs; the warps centre their fragments in registers
+// straight from the raw tile (no centred copy in shared memory) and, in the single-pass fit,
+// also accumulate the shifted class sums from those centred fragments (sum over all rows and
+// over class 1; class 0 = all - class 1), so no other warp touches the fp64 pipe the DMMAs use.
+// One producer warp refills the 5-slot ring.
+//
+// Tiles arrive by TMA tensor copies (cp.async.bulk.tensor.2d, 4 boxes of 64 rows x 16 columns
+// with the 128-byte swizzle: 16-byte chunk ch of row r sits at chunk ch ^ (r & 7) of the row's
+// 128-byte line; rows past n are zero-filled by the TMA).  Lane (g, kq) loads, in box p, the
+// chunk q(g) = (g >> 1) | ((g & 1) << 2) of sample row kq — i.e. physical columns
+// 16p + 2q(g) + {0, 1} — and uses them as the LOGICAL columns 8(2p) + g and 8(2p+1) + g, so the
+// accumulated S is S_phys under the column permutation P(8 idx + g) = 16 (idx >> 1) + 2 q(g) +
+// (idx & 1), undone when the blocks are written.  With the swizzle, a quarter-warp's four rows
+// x two chunks land in eight distinct 16-byte bank groups (no conflicts).  The eight warps'
+// partial S and class sums are folded in ascending warp order through shared memory.
+constexpr int kG64MmaWarps = 8;
+constexpr int kG64Threads = (kG64MmaWarps + 4) * 32;   // + a warpgroup: the producer and 3 idle warps
+// registers: 168 at launch; the tensor-core warpgroups take 240, the other drops to 24
+constexpr int kG64RegsMma = 240, kG64RegsAux = 24;
+static_assert(kG64MmaWarps * 32 * kG64RegsMma + 4 * 32 * kG64RegsAux <= 65536, "register budget");
+constexpr int kG64Slots = 5;
+constexpr size_t kG64BoxBytes = 64 * 128;                                  // 64 rows x 16 doubles
+constexpr size_t kG64RawBytes = 4 * kG64BoxBytes;
+constexpr size_t kG64OffY = kG64Slots * kG64RawBytes;
+constexpr size_t kG64OffMu = kG64OffY + kG64Slots * 64 * 8;
+constexpr int kG64Mu1 = 66;   // class-1 centre row: 16 bytes past a bank-aligned row, so lanes
+                               // reading class-0 and class-1 centres of one column never collide
+constexpr size_t kG64OffRed = kG64OffMu + 136 * 8;                        // shift fold
+constexpr size_t kG64OffBar = kG64OffRed + kG64MmaWarps * 128 * 8 + 128;
+constexpr size_t kG64Smem = kG64OffBar + 2 * kG64Slots * 8 + 1024;       // + base alignment slack
+constexpr uint32_t kG64TxBytes = static_cast<uint32_t>(kG64RawBytes) + 512u;
+static_assert(kG64MmaWarps * (36 * 32 * 2 + 2 * 64) * 8 <= kG64OffY, "S fold must fit in the raw ring");
+
+__host__ __device__ __forceinline__ int g64_q(int g) { return (g >> 1) | ((g & 1) << 2); }
+__device__ __forceinline__ int g64_phys(int logical) {   // logical column 8 idx + g -> physical
+  const int idx = logical >> 3, g = logical & 7;
+  return 16 * (idx >> 1) + 2 * g64_q(g) + (idx & 1);
+}
+
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_addr(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* smem_dst, const CUtensorMap* map, int c0, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.1d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];" ::"r"(
+          smem_addr(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(smem_addr(bar))
+      : "memory");
+}
+
+template <bool kFused>
+__global__ void __launch_bounds__(kG64Threads, 1)
+gda_fit64_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmy,
+                 const double* __restrict__ x, const long long* __restrict__ y, int64_t n,
+                 const double* __restrict__ mu0, const double* __restrict__ mu1,
+                 double* __restrict__ parts, const int* __restrict__ skip,
+                 double* __restrict__ parts_sd, long long* __restrict__ parts_n1,
+                 double* __restrict__ shift_out) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // the 128-byte swizzle needs 1024-byte aligned boxes; offsetting the shared array itself (not
+  // an integer-cast address) keeps every access below an LDS rather than a generic load
+  unsigned char* const smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
+  unsigned char* const raw = smem;
+  long long* const ys = reinterpret_cast<long long*>(smem + kG64OffY);
+  double* const mu_s = reinterpret_cast<double*>(smem + kG64OffMu);   // [mu0: 0..63 | mu1: 66..129]
+  double* const red = reinterpret_cast<double*>(smem + kG64OffRed);
+  uint64_t* const full = reinterpret_cast<uint64_t*>(smem + kG64OffBar);
+  uint64_t* const empty = full + kG64Slots;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t ntiles = (n + 63) / 64;
+  const int mt = static_cast<int>(ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0);
+  auto tile_of = [&](int m) { return static_cast<int64_t>(blockIdx.x) + static_cast<int64_t>(m) * gridDim.x; };
+  auto rows_of = [&](int m) { return static_cast<int>(std::min<int64_t>(64, n - tile_of(m) * 64)); };
+  auto issue = [&](int m) {   // tile m -> slot m % kG64Slots (4 swizzled boxes + the labels)
+    const int s = m % kG64Slots;
+    const int row0 = static_cast<int>(tile_of(m) * 64);
+    mbar_arrive_expect_tx(&full[s], kG64TxBytes);
+#pragma unroll
+    for (int p = 0; p < 4; ++p) tma_load_2d(raw + s * kG64RawBytes + p * kG64BoxBytes, &tmx, 16 * p, row0, &full[s]);
+    tma_load_1d(ys + s * 64, &tmy, row0, &full[s]);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < kG64Slots; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kG64MmaWarps);
+    }
+    fence_mbar_init();
+  }
+  pdl_wait();   // x / y / the means may come from the predecessor kernel
+  pdl_trigger();
+  if (!kFused && skip != nullptr && *skip) return;   // uniform over the grid
+  if (!kFused)
+    for (int j = tid; j < 128; j += kG64Threads) mu_s[j < 64 ? j : kG64Mu1 + j - 64] = j < 64 ? mu0[j] : mu1[j - 64];
+  __syncthreads();
+
+  if (warp >= kG64MmaWarps) {
+    // ---- producer warp: keeps the ring kG64Slots tiles ahead of the slowest reader -----------
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kG64RegsAux));
+    if (warp == kG64MmaWarps && lane == 0) {
+      for (int m = 0; m < mt; ++m) {
+        if (m >= kG64Slots) {
+          mbar_wait(&empty[m % kG64Slots], ((m - kG64Slots) / kG64Slots) & 1);
+          fence_proxy_async_smem();
+        }
+        issue(m);
+      }
+    }
+    __syncwarp();
+    __syncthreads();   // (A)
+    return;
+  }
+
+  if (kFused) {
+    // shift c_c = mean of the class-c rows among the first R <= 64 rows (all R rows' mean for a
+    // class absent there, 0 for n = 0); every CTA computes it in the same order.  Thread t:
+    // column pair t & 31 (t & 31, + 32), rows (t >> 5) + 8u.
+    const int R = static_cast<int>(std::min<int64_t>(n, 64));
+    const int cp = tid & 31, rp = tid >> 5;
+    double q0a = 0.0, q0b = 0.0, q1a = 0.0, q1b = 0.0;
+    int k1 = 0;
+    for (int r = rp; r < R; r += kG64MmaWarps) {
+      const double va = x[static_cast<int64_t>(r) * 64 + cp], vb = x[static_cast<int64_t>(r) * 64 + cp + 32];
+      if (y[r] == 1) { q1a += va; q1b += vb; ++k1; } else { q0a += va; q0b += vb; }
+    }
+    red[rp * 128 + cp] = q0a;
+    red[rp * 128 + cp + 32] = q0b;
+    red[rp * 128 + 64 + cp] = q1a;
+    red[rp * 128 + 64 + cp + 32] = q1b;
+    int* kred = reinterpret_cast<int*>(red + kG64MmaWarps * 128);
+    if (cp == 0) kred[rp] = k1;
+    named_bar(1, kG64MmaWarps * 32);
+    double sh = 0.0;
+    const int c = tid >> 6 & 1, j = tid & 63;   // threads 0..127: (class, column)
+    if (tid < 128) {
+      double t = 0.0, ta = 0.0;
+      int kc = 0;
+      for (int w = 0; w < kG64MmaWarps; ++w) {
+        t += red[w * 128 + c * 64 + j];
+        ta += red[w * 128 + j] + red[w * 128 + 64 + j];
+        kc += kred[w];
+      }
+      const int k_c = c ? kc : R - kc;
+      sh = k_c > 0 ? t / k_c : (R > 0 ? ta / R : 0.0);
+    }
+    named_bar(1, kG64MmaWarps * 32);   // every read of red done
+    if (tid < 128) {
+      mu_s[c * kG64Mu1 + j] = sh;
+      if (blockIdx.x == 0) shift_out[c * 64 + j] = sh;
+    }
+    named_bar(1, kG64MmaWarps * 32);
+  }
+
+  // ---- tensor-core warps: rows 8 warp + 4 st + kq of every tile, all 36 lower blocks --------
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kG64RegsMma));
+  const int g = lane >> 2, kq = lane & 3, qg = g64_q(g);
+  const double* mrow = mu_s + 2 * qg;   // + 64 c + 16 p: the centre pair of this lane's columns
+  double acc[36][2];
+#pragma unroll
+  for (int b = 0; b < 36; ++b) acc[b][0] = acc[b][1] = 0.0;
+  double sa[8], s1[8];   // fused: shifted sums of this lane's logical columns (all rows, class 1)
+#pragma unroll
+  for (int idx = 0; idx < 8; ++idx) sa[idx] = s1[idx] = 0.0;
+  int c1 = 0;
+  for (int m = 0; m < mt; ++m) {
+    const int s = m % kG64Slots, rows = rows_of(m);
+    mbar_wait(&full[s], (m / kG64Slots) & 1);
+    const unsigned char* rs = raw + s * kG64RawBytes;
+    const long long* yv = ys + s * 64;
+#pragma unroll
+    for (int st = 0; st < 2; ++st) {
+      const int r = 8 * warp + 4 * st + kq;
+      const bool valid = r < rows;   // rows past n: zero-filled by the TMA, excluded here
+      const bool one = yv[r] == 1;
+      const unsigned char* rowp = rs + r * 128 + ((qg ^ (r & 7)) << 4);
+      const double* mc = mrow + (one ? kG64Mu1 : 0);
+      double f[8];
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const double2 v = *reinterpret_cast<const double2*>(rowp + p * kG64BoxBytes);
+        const double2 mu = *reinterpret_cast<const double2*>(mc + 16 * p);
+        f[2 * p] = valid ? v.x - mu.x : 0.0;
+        f[2 * p + 1] = valid ? v.y - mu.y : 0.0;
+      }
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b <= a; ++b) dmma_8x8x4(acc[a * (a + 1) / 2 + b], f[a], f[b]);
+      if (kFused) {
+#pragma unroll
+        for (int idx = 0; idx < 8; ++idx) {
+          sa[idx] += f[idx];
+          s1[idx] += one ? f[idx] : 0.0;
+        }
+        c1 += (valid && one) ? 1 : 0;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  __syncthreads();   // (A) every tile consumed, no copy outstanding: the ring becomes the fold area
+  double* fold = reinterpret_cast<double*>(raw);
+#pragma unroll
+  for (int b = 0; b < 36; ++b)
+    *reinterpret_cast<double2*>(fold + ((warp * 36 + b) * 32 + lane) * 2) = make_double2(acc[b][0], acc[b][1]);
+  double* fsum = fold + kG64MmaWarps * 36 * 64;   // [warp][class][logical column]
+  if (kFused) {
+    // class sums: fold the 4 row lanes (kq) of each column in order, then one lane per column
+#pragma unroll
+    for (int idx = 0; idx < 8; ++idx) {
+      double va = sa[idx], v1 = s1[idx];
+      va += __shfl_xor_sync(0xffffffffu, va, 1);
+      v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+      va += __shfl_xor_sync(0xffffffffu, va, 2);
+      v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
+      if (kq == 0) {
+        fsum[(warp * 2 + 0) * 64 + 8 * idx + g] = va - v1;   // class 0 = all rows - class 1
+        fsum[(warp * 2 + 1) * 64 + 8 * idx + g] = v1;
+      }
+    }
+    int k = c1;   // every lane of a row counts it: the g == 0 lanes hold one count per row
+    k = g == 0 ? k : 0;
+    for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+    if (lane == 0) reinterpret_cast<long long*>(red)[warp] = k;
+  }
+  named_bar(2, kG64MmaWarps * 32);
+  double* out = parts + static_cast<size_t>(blockIdx.x) * 4096;
+  for (int e = tid; e < 36 * 32; e += kG64MmaWarps * 32) {
+    const int b = e >> 5, ln = e & 31;
+    double2 v = *reinterpret_cast<const double2*>(fold + (b * 32 + ln) * 2);
+#pragma unroll
+    for (int w = 1; w < kG64MmaWarps; ++w) {
+      const double2 u = *reinterpret_cast<const double2*>(fold + ((w * 36 + b) * 32 + ln) * 2);
+      v.x += u.x;
+      v.y += u.y;
+    }
+    int a = 0;
+    while ((a + 1) * (a + 2) / 2 <= b) ++a;
+    const int bb = b - a * (a + 1) / 2;
+    const int pr = g64_phys(8 * a + (ln >> 2));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int pc = g64_phys(8 * bb + 2 * (ln & 3) + h);
+      const double val = h ? v.y : v.x;
+      out[pr * 64 + pc] = val;
+      if (a != bb) out[pc * 64 + pr] = val;
+    }
+  }
+  if (kFused) {
+    if (tid < 128) {   // (class, logical column) -> physical column, warps in ascending order
+      const int c = tid >> 6, L = tid & 63;
+      double t = 0.0;
+      for (int w = 0; w < kG64MmaWarps; ++w) t += fsum[(w * 2 + c) * 64 + L];
+      parts_sd[static_cast<size_t>(blockIdx.x) * 128 + c * 64 + g64_phys(L)] = t;
+    }
+    if (tid == 0) {
+      long long k = 0;
+      for (int w = 0; w < kG64MmaWarps; ++w) k += reinterpret_cast<const long long*>(red)[w];
+      parts_n1[blockIdx.x] = k;
+    }
+  }
+}
+
+// TMA tensor maps of x (n x 64 fp64, boxes of 64 rows x 16 columns, 128-byte swizzle) and y
+// (n int64, boxes of 64), encoded per launch through the driver entry point (no libcuda link)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+static int g64_maps(const double* x, const long long* y, int64_t n, CUtensorMap* tmx, CUtensorMap* tmy) {
+  EncodeTiledFn enc = encode_tiled();
+  DLX_REQUIRE(enc != nullptr, DLX_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t nn = static_cast<cuuint64_t>(std::max<int64_t>(n, 1));
+  const cuuint64_t dx[2] = {64, nn}, sx[1] = {64 * 8};
+  const cuuint32_t bx[2] = {16, 64}, ex[2] = {1, 1};
+  CUresult r = enc(tmx, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(x), dx, sx, bx, ex,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DLX_REQUIRE(r == CUDA_SUCCESS, DLX_ERR_CUDA, "cuTensorMapEncodeTiled(x) failed");
+  const cuuint64_t dy[1] = {nn}, sy[1] = {8};
+  const cuuint32_t by[1] = {64}, ey[1] = {1};
+  r = enc(tmy, CU_TENSOR_MAP_DATA_TYPE_INT64, 1, const_cast<long long*>(y), dy, sy, by, ey,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DLX_REQUIRE(r == CUDA_SUCCESS, DLX_ERR_CUDA, "cuTensorMapEncodeTiled(y) failed");
+  return DLX_OK;
+}
+
+// the k-split d = 64 kernel takes the bulk-copy ring: 16-byte aligned x and y
+static bool gda_fit64_ok(const double* x, const long long* y, int d) {
+  return d == 64 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0;
+}
+
 int gda_pass2_dmma_grid(int64_t n) {
   const int64_t tiles = (n + kGdTile - 1) / kGdTile;
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, sm_count())));
@@ -362,6 +677,17 @@ int gda_pass2_dmma(const double* x, const long long* y, int64_t n, int d, const 
   const int grid = gda_pass2_dmma_grid(n);
   DLX_REQUIRE(parts && parts_bytes >= static_cast<size_t>(grid) * d * d * sizeof(double),
               DLX_ERR_ARG, "gda: workspace too small");
+  if (gda_fit64_ok(x, y, d) && n > 0) {
+    CUtensorMap tmx, tmy;
+    if (int rc = g64_maps(x, y, n, &tmx, &tmy)) return rc;
+    DLX_CUDA(cudaFuncSetAttribute(gda_fit64_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kG64Smem)));
+    DLX_CUDA(launch_pdl(gda_fit64_kernel<false>, dim3(grid), dim3(kG64Threads), kG64Smem, stream, tmx, tmy, x, y, n, mu0,
+                        mu1, parts, static_cast<const int*>(nullptr), static_cast<double*>(nullptr),
+                        static_cast<long long*>(nullptr), static_cast<double*>(nullptr)));
+    DLX_LAUNCHED("gda_fit64_kernel");
+    return combine_f64(parts, grid, static_cast<long long>(d) * d, out, stream);
+  }
   DLX_CUDA(cudaFuncSetAttribute(gda_pass2_dmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(kGdSmem)));
   DLX_CUDA(launch_pdl(gda_pass2_dmma_kernel<false>, dim3(grid), dim3(kGdThreads), kGdSmem, stream, x, y, n,
@@ -437,14 +763,28 @@ int gda_fit(const double* x, const long long* y, int64_t n, int d, long long* n1
   double* shift = c.take<double>(128);
   int* ok = c.take<int>(1);
   DLX_REQUIRE(ws && c.used <= ws_bytes, DLX_ERR_ARG, "gda fit: workspace too small");
-  DLX_CUDA(cudaFuncSetAttribute(gda_pass2_dmma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(kGdSmem)));
-  DLX_CUDA(cudaFuncSetAttribute(gda_pass2_dmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(kGdSmem)));
-  DLX_CUDA(launch_pdl(gda_pass2_dmma_kernel<true>, dim3(grid), dim3(kGdThreads), kGdSmem, stream, x, y, n, d,
-                      static_cast<const double*>(nullptr), static_cast<const double*>(nullptr), parts,
-                      static_cast<const int*>(nullptr), parts_sd, parts_n1, shift));
-  DLX_LAUNCHED("gda_pass2_dmma_kernel");
+  const bool k64 = gda_fit64_ok(x, y, d) && n > 0 && !std::getenv("DLX_GDA_ROWBLOCKS");
+  CUtensorMap tmx, tmy;
+  if (k64) {
+    if (int rc = g64_maps(x, y, n, &tmx, &tmy)) return rc;
+    DLX_CUDA(cudaFuncSetAttribute(gda_fit64_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kG64Smem)));
+    DLX_CUDA(cudaFuncSetAttribute(gda_fit64_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kG64Smem)));
+    DLX_CUDA(launch_pdl(gda_fit64_kernel<true>, dim3(grid), dim3(kG64Threads), kG64Smem, stream, tmx, tmy, x, y, n,
+                        static_cast<const double*>(nullptr), static_cast<const double*>(nullptr), parts,
+                        static_cast<const int*>(nullptr), parts_sd, parts_n1, shift));
+    DLX_LAUNCHED("gda_fit64_kernel");
+  } else {
+    DLX_CUDA(cudaFuncSetAttribute(gda_pass2_dmma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kGdSmem)));
+    DLX_CUDA(cudaFuncSetAttribute(gda_pass2_dmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kGdSmem)));
+    DLX_CUDA(launch_pdl(gda_pass2_dmma_kernel<true>, dim3(grid), dim3(kGdThreads), kGdSmem, stream, x, y, n, d,
+                        static_cast<const double*>(nullptr), static_cast<const double*>(nullptr), parts,
+                        static_cast<const int*>(nullptr), parts_sd, parts_n1, shift));
+    DLX_LAUNCHED("gda_pass2_dmma_kernel");
+  }
   int rc = combine_f64(parts, grid, static_cast<long long>(d) * d, Sp, stream);
   if (rc == DLX_OK) rc = combine_f64_i64(parts_sd, 2LL * d, sd, parts_n1, 1, n1, grid, stream);
   if (rc != DLX_OK) return rc;
@@ -453,11 +793,19 @@ int gda_fit(const double* x, const long long* y, int64_t n, int d, long long* n1
                       static_cast<const double*>(shift), n1_out, mu0, mu1, S, ok));
   DLX_LAUNCHED("gda_fit_finalize_kernel");
   // fallback, decided on the device: pass 2 on the exact means when the shift was too far off
-  DLX_CUDA(launch_pdl(gda_pass2_dmma_kernel<false>, dim3(grid), dim3(kGdThreads), kGdSmem, stream, x, y, n, d,
-                      static_cast<const double*>(mu0), static_cast<const double*>(mu1), parts,
-                      static_cast<const int*>(ok), static_cast<double*>(nullptr),
-                      static_cast<long long*>(nullptr), static_cast<double*>(nullptr)));
-  DLX_LAUNCHED("gda_pass2_dmma_kernel");
+  if (k64) {
+    DLX_CUDA(launch_pdl(gda_fit64_kernel<false>, dim3(grid), dim3(kG64Threads), kG64Smem, stream, tmx, tmy, x, y, n,
+                        static_cast<const double*>(mu0), static_cast<const double*>(mu1), parts,
+                        static_cast<const int*>(ok), static_cast<double*>(nullptr),
+                        static_cast<long long*>(nullptr), static_cast<double*>(nullptr)));
+    DLX_LAUNCHED("gda_fit64_kernel");
+  } else {
+    DLX_CUDA(launch_pdl(gda_pass2_dmma_kernel<false>, dim3(grid), dim3(kGdThreads), kGdSmem, stream, x, y, n, d,
+                        static_cast<const double*>(mu0), static_cast<const double*>(mu1), parts,
+                        static_cast<const int*>(ok), static_cast<double*>(nullptr),
+                        static_cast<long long*>(nullptr), static_cast<double*>(nullptr)));
+    DLX_LAUNCHED("gda_pass2_dmma_kernel");
+  }
   return combine_f64_unless(parts, grid, static_cast<long long>(d) * d, S, ok, stream);
 }
 

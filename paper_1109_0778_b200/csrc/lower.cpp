@@ -887,6 +887,13 @@ bool Executor::match_generic(int64_t n, std::vector<LElem>& els, LoopPlan& p, Ma
 }
 
 // ---- lowering, cache, launch -------------------------------------------------------------------
+// DLX_PROGRAM_VM=1: loops outside the specialised families run on the bytecode kernel (vm.cu)
+// instead of a kernel compiled from the loop body (lower_jit.cpp)
+static bool use_vm() {
+  static const bool v = getenv("DLX_PROGRAM_VM") && atoi(getenv("DLX_PROGRAM_VM")) != 0;
+  return v;
+}
+
 std::shared_ptr<LoopPlan> Executor::lower(const Stmt& s, int64_t n) {
   const Loop& L = *s.loop;
   MatchCtx m;
@@ -917,7 +924,8 @@ std::shared_ptr<LoopPlan> Executor::lower(const Stmt& s, int64_t n) {
   }
   auto p = std::make_shared<LoopPlan>();
   const bool ok = match_kmeans(s, n, els, *p, m) || match_logistic(s, n, els, *p, m) || match_groupby(n, els, *p, m) ||
-                  match_bucket_rows(n, els, *p, m) || match_gda2(n, els, *p, m) || match_generic(n, els, *p, m);
+                  match_bucket_rows(n, els, *p, m) || match_gda2(n, els, *p, m) ||
+                  (use_vm() ? match_generic(n, els, *p, m) : match_compiled(n, els, *p, m));
   if (!ok) gen_fail("multiloop x" + std::to_string(s.sym) + " matches no kernel");
   p->vsyms = m.vsyms;
   for (const VecP& v : m.vecs) {
@@ -1003,6 +1011,10 @@ void Executor::run_loop(const Stmt& s) {
   if (plan->fam == LoopPlan::BucketRows) rep["buckets"] = plan->k, rep["d"] = plan->d;
   if (plan->fam == LoopPlan::GdaScatter || plan->fam == LoopPlan::Logistic) rep["d"] = plan->d;
   if (plan->fam == LoopPlan::Generic) rep["elems"] = live, rep["instructions"] = static_cast<int>(plan->code.size());
+  if (plan->fam == LoopPlan::Compiled) {
+    rep["elems"] = live;
+    rep["source_bytes"] = static_cast<int64_t>(plan->jit_src.size());
+  }
   rep["launch"] = plan->launch;
   rep["cached"] = cached;
   if (g_run->dry) {
@@ -1065,6 +1077,7 @@ void Executor::launch(const Stmt& s, LoopPlan& p, int64_t n, std::vector<VecP>& 
     case LoopPlan::GdaScatter: launch_gda2(p, n, vecs); break;
     case LoopPlan::Logistic: launch_logistic(p, n, vecs, rep); break;
     case LoopPlan::Generic: launch_generic(p, n, vecs); break;
+    case LoopPlan::Compiled: launch_compiled(p, n, vecs); break;
   }
 }
 

@@ -19,6 +19,7 @@
 #include "../../include/dlx.h"
 #include "../../include/dlx_program.h"
 #include "../../include/dlx_vm.h"
+#include "jit.hpp"
 #include "program_ir.hpp"
 
 namespace dlx {
@@ -141,7 +142,7 @@ struct SE {
 // was matched against keep their element types and lengths and every baked host scalar its
 // value).
 struct LoopPlan {
-  enum Fam { Kmeans, GroupBy, BucketRows, GdaScatter, Logistic, Generic } fam = Generic;
+  enum Fam { Kmeans, GroupBy, BucketRows, GdaScatter, Logistic, Generic, Compiled } fam = Generic;
   std::string family, launch;
   // inputs: env symbols of the vectors the loop reads (slot order), their types and lengths
   std::vector<int> vsyms;
@@ -182,6 +183,13 @@ struct LoopPlan {
   dlx_vm_loop L{};
   std::vector<std::pair<int, int>> patches;     // (instruction, host symbol): constants re-read per launch
   std::vector<Ty> coll_ty;                      // per elem collect element type
+  // compiled (NVRTC) kernel of the loop body (lower_jit.cpp)
+  std::string jit_src;
+  std::vector<std::string> jit_names;
+  std::vector<uint8_t> jit_kind;                // per elem: 0 reduce, 1 collect, 2 append
+  std::vector<int> jit_host;                    // host scalars read per launch (env symbols)
+  int jit_nred = 0, jit_napp = 0, jit_words = 0;
+  std::shared_ptr<const JitModule> jit;         // compiled on first launch (process-wide cache)
 };
 
 struct MatchCtx {   // what a lowering depends on (recorded into the LoopPlan)
@@ -305,6 +313,7 @@ class Executor {
   bool match_logistic(const Stmt& s, int64_t n, std::vector<LElem>& els, LoopPlan& p, MatchCtx& m);
   bool link_compile(const SEP& f, const SEP& dot, LoopPlan& p, std::unordered_map<const SE*, int>& reg);
   bool match_generic(int64_t n, std::vector<LElem>& els, LoopPlan& p, MatchCtx& m);
+  bool match_compiled(int64_t n, std::vector<LElem>& els, LoopPlan& p, MatchCtx& m);
   int vm_emit(LoopPlan& p, MatchCtx& m, std::unordered_map<const SE*, int>& reg, int& nreg, const SEP& s);
   // launches
   void launch_kmeans(const Stmt& s, LoopPlan& p, int64_t n, std::vector<VecP>& V, nlohmann::json& rep);
@@ -313,6 +322,7 @@ class Executor {
   void launch_gda2(LoopPlan& p, int64_t n, std::vector<VecP>& V);
   void launch_logistic(LoopPlan& p, int64_t n, std::vector<VecP>& V, nlohmann::json& rep);
   void launch_generic(LoopPlan& p, int64_t n, std::vector<VecP>& V);
+  void launch_compiled(LoopPlan& p, int64_t n, std::vector<VecP>& V);
   void bind_scalars(const LoopPlan& p, const int64_t* hres);
   void* dalloc(size_t bytes);
   void dfree(void* p);

@@ -2,7 +2,8 @@
 records are summed by one kernel that reads every rank's exchange buffer and folds the ranks in
 ascending order, fused with the update that consumes the sum.
 
-The pool has one GPU per box, so the world-size-2 test runs two processes on the same device:
+The pool has one GPU per box, so the world-size 2 / 4 / 8 tests run that many processes on the
+same device (uneven shards: no size below divides by 4 or 8):
 the exchange buffers are shared through CUDA IPC exactly as across NVSwitch peers (there the
 loads travel over NVLink), and the flag protocol, slot alternation and epilogues are the same
 code.  Parity: counts / GroupBy bit-exact, fp64 sums rtol 1e-9 against the single-process
@@ -27,9 +28,9 @@ def _free_port():
     return p
 
 
-N_KM, D_KM, K_KM, IT_KM = 50_000, 64, 16, 4
-N_LR, D_LR, IT_LR = 30_000, 64, 3
-N_GB, K_GB = 200_001, 4096
+N_KM, D_KM, K_KM, IT_KM = 50_003, 64, 16, 4
+N_LR, D_LR, IT_LR = 30_001, 64, 3
+N_GB, K_GB = 200_001, 65_536   # a 512 KiB int64 record
 N_GD, D_GD = 50_001, 64
 
 
@@ -95,28 +96,33 @@ def _work(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_peer_allreduce_world2_one_device():
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_peer_allreduce_one_device(world):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = {}
-    while len(res) < 2:
-        r, out = q.get(timeout=300)
+    while len(res) < world:
+        r, out = q.get(timeout=600)
         assert "error" not in out, f"rank {r}: {out['error']}"
         res[r] = out
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    r0, r1 = res[0], res[1]
-    # every rank holds bit-identical results (ascending-rank fold on both)
-    for (c0, s0, m0), (c1, s1, m1) in zip(r0["kmeans"], r1["kmeans"]):
-        assert np.array_equal(c0, c1) and np.array_equal(s0.view(np.int64), s1.view(np.int64))
-        assert np.array_equal(m0.view(np.int64), m1.view(np.int64))
-    assert np.array_equal(r0["logreg"].view(np.int64), r1["logreg"].view(np.int64))
+    r0 = res[0]
+    # every rank holds bit-identical results (ascending-rank fold on each)
+    for r in range(1, world):
+        rr = res[r]
+        for (c0, s0, m0), (c1, s1, m1) in zip(r0["kmeans"], rr["kmeans"]):
+            assert np.array_equal(c0, c1) and np.array_equal(s0.view(np.int64), s1.view(np.int64))
+            assert np.array_equal(m0.view(np.int64), m1.view(np.int64))
+        assert np.array_equal(r0["logreg"].view(np.int64), rr["logreg"].view(np.int64))
+        assert np.array_equal(rr["groupby"], r0["groupby"])
+        assert np.array_equal(r0["gda"][3].view(np.int64), rr["gda"][3].view(np.int64))
     # against the single-process oracle
     x, _ = O.kmeans_inputs(N_KM, D_KM, K_KM)
     mu = x[:K_KM].copy()
@@ -135,19 +141,18 @@ def test_peer_allreduce_world2_one_device():
     np.testing.assert_allclose(r0["logreg"], th, rtol=1e-9, atol=1e-13)
     keys = O.rng_ints(3, 0, N_GB, K_GB)
     assert np.array_equal(r0["groupby"], O.groupby_count(keys, K_GB))
-    assert np.array_equal(r1["groupby"], r0["groupby"])
-    assert r0["n"] == r1["n"] == N_GB
+    assert all(res[r]["n"] == N_GB for r in range(world))
     xg = O.rng_units(4, 0, N_GD * D_GD).reshape(N_GD, D_GD)
     yg = O.rng_ints(4, N_GD * D_GD, N_GD, 2)
     n1, s0, s1 = O.gda_pass1(xg, yg, workers=O.threads(), chunks=4 * O.threads())
     m0, m1 = s0 / float(N_GD - n1), s1 / float(n1)
     Sr = O.gda_pass2(xg, yg, m0, m1, workers=O.threads(), chunks=4 * O.threads())
-    for r in (r0, r1):
-        assert r["gda"][0] == n1
-        np.testing.assert_allclose(r["gda"][1], m0, rtol=1e-9)
-        np.testing.assert_allclose(r["gda"][2], m1, rtol=1e-9)
-        np.testing.assert_allclose(r["gda"][3], Sr, rtol=1e-9, atol=1e-9 * np.abs(Sr).max())
-    assert np.array_equal(r0["gda"][3].view(np.int64), r1["gda"][3].view(np.int64))
+    for r in range(world):
+        g = res[r]["gda"]
+        assert g[0] == n1
+        np.testing.assert_allclose(g[1], m0, rtol=1e-9)
+        np.testing.assert_allclose(g[2], m1, rtol=1e-9)
+        np.testing.assert_allclose(g[3], Sr, rtol=1e-9, atol=1e-9 * np.abs(Sr).max())
 
 
 def test_peer_world1_epilogues_match_unfused():
@@ -178,3 +183,25 @@ def test_peer_world1_epilogues_match_unfused():
             comm.allreduce_(big)
     finally:
         comm.close()
+
+
+def test_nccl_communicator_world1():
+    """The NCCL path (csrc/comm.cu: dlx_comm_init / allreduce_sum / allreduce_sum_group /
+    destroy) with a real one-rank communicator: the collective is the identity, on the caller's
+    stream, for fp64 and int64 records, single and grouped (NCCL refuses two ranks on one GPU, so
+    world 1 is what one box can run)."""
+    from paper_1109_0778_b200.comm import Comm
+    uid = Comm.unique_id()
+    c = Comm(0, 1, uid, force_nccl=True)
+    try:
+        a = torch.rand(4096, dtype=torch.float64, device="cuda")
+        b = torch.arange(65_536, dtype=torch.int64, device="cuda") - 7
+        a0, b0 = a.clone(), b.clone()
+        c.allreduce_(a)
+        c.allreduce_(b)
+        c.allreduce_many_([a, b])
+        torch.cuda.synchronize()
+        assert torch.equal(a, a0) and torch.equal(b, b0)
+        assert c.allreduce_int(41) == 41
+    finally:
+        c.close()

@@ -179,7 +179,7 @@ def test_filter_collect_thresholds(thr):
     hits = _find_count_expected(100000, thr)
     got = lines(text)
     assert [int(v) for v in got] == [len(hits), len(hits), int(hits[0]), int(hits.sum())]
-    assert [r["family"] for r in report] == ["generic", "generic"]
+    assert [r["family"] for r in report] == ["compiled", "compiled"]
 
 
 @pytest.mark.gpu
@@ -194,15 +194,15 @@ def test_filter_collect_empty_traps_on_read():
 
 
 EXPECTED_FAMILIES = {
-    "axpy_n100000": ["generic", "generic"],
-    "count_gt_n100000": ["generic"],
-    "find_count_n100000": ["generic", "generic"],
+    "axpy_n100000": ["compiled", "compiled"],
+    "count_gt_n100000": ["compiled"],
+    "find_count_n100000": ["compiled", "compiled"],
     "gda_n20000_d4": ["bucket_rows", "gda_scatter"],
     "groupby_n100000_k16": ["groupby"],
     "kmeans_n4096_d16_k8_it2": ["kmeans", "kmeans"],
     "kmeans_n65536_d16_k8_it1": ["kmeans"],
     "logreg_n20000_d8_it2": ["logistic", "logistic"],
-    "mean_variance_n100000": ["generic"],
+    "mean_variance_n100000": ["compiled"],
 }
 
 
@@ -270,7 +270,7 @@ def test_merged_program_lowers_both_loops_dry_run(monkeypatch):
     monkeypatch.setenv("DLX_PROGRAM_DRYRUN", "1")
     mv = load("mean_variance_n100000")["program"]
     _, report = run_program(_merge_independent(mv, mv), seed=1)
-    assert [r["family"] for r in report] == ["generic", "generic"]
+    assert [r["family"] for r in report] == ["compiled", "compiled"]
 
 
 @pytest.mark.gpu
@@ -364,7 +364,7 @@ def test_two_trapping_loops_dry_run(monkeypatch):
     from paper_1109_0778_b200.program import run_program
     monkeypatch.setenv("DLX_PROGRAM_DRYRUN", "1")
     _, report = run_program(_two_trapping_loops(), seed=1)
-    assert [r["family"] for r in report] == ["generic", "generic"]
+    assert [r["family"] for r in report] == ["compiled", "compiled"]
 
 
 def _one_loop_two_traps(off):
