@@ -130,6 +130,10 @@ typedef struct {
   uint8_t op[DLX_LINK_MAX_CODE], dst[DLX_LINK_MAX_CODE], a[DLX_LINK_MAX_CODE], b[DLX_LINK_MAX_CODE];
   double imm[DLX_LINK_MAX_CODE];
 } dlx_link_code;
+/* how dlx_rowdot_link_grad evaluates a link code: 1 = the sigmoid 1 / (1 + exp(0 - t)), 2 = the
+ * softsign t / (1 + |t|) (fixed functions, bit-identical to interpreting the code), 0 = the
+ * interpreted code */
+int dlx_link_kind(const dlx_link_code* h_link);
 int dlx_rowdot_link_grad(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
                          const double* d_theta, const dlx_link_code* h_link, double* d_h,
                          double* d_grad, void* d_workspace, size_t workspace_bytes,

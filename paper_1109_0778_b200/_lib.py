@@ -8,7 +8,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdlx.so")
+# DLX_LIB_PATH: an alternative build of the same library (A/B experiments of compile-time variants)
+LIB_PATH = os.environ.get("DLX_LIB_PATH") or os.path.join(_HERE, "libdlx.so")
 
 DLX_OK = 0
 DLX_ERR_CUDA = 1
@@ -77,6 +78,7 @@ _SIGS = {
     "dlx_logreg_grad": (_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _sz, _vp]),
     "dlx_axpy_inplace": (_int, [_vp, _vp, _dbl, _i64, _vp]),
     "dlx_rowdot_link_grad": (_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "dlx_link_kind": (_int, [_vp]),
     "dlx_gda_workspace_bytes": (_sz, [_i64, _i32]),
     "dlx_gda_pass1": (_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "dlx_gda_means": (_int, [_vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp]),

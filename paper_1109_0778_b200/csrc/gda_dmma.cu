@@ -379,17 +379,25 @@ constexpr int kG64Threads = (kG64MmaWarps + 4) * 32;   // + a warpgroup: the pro
 // registers: 168 at launch; the tensor-core warpgroups take 240, the other drops to 24
 constexpr int kG64RegsMma = 240, kG64RegsAux = 24;
 static_assert(kG64MmaWarps * 32 * kG64RegsMma + 4 * 32 * kG64RegsAux <= 65536, "register budget");
-constexpr int kG64Slots = 5;
-constexpr size_t kG64BoxBytes = 64 * 128;                                  // 64 rows x 16 doubles
+#ifndef DLX_G64_ROWS
+#define DLX_G64_ROWS 128
+#endif
+constexpr int kG64Rows = DLX_G64_ROWS;                  // samples per tile (8 or 16 rows per warp)
+constexpr int kG64Steps = kG64Rows / (4 * kG64MmaWarps);   // k-steps per warp per tile
+#ifndef DLX_G64_SLOTS
+#define DLX_G64_SLOTS (kG64Rows == 64 ? 5 : 3)
+#endif
+constexpr int kG64Slots = DLX_G64_SLOTS;
+constexpr size_t kG64BoxBytes = kG64Rows * 128;                            // kG64Rows rows x 16 doubles
 constexpr size_t kG64RawBytes = 4 * kG64BoxBytes;
 constexpr size_t kG64OffY = kG64Slots * kG64RawBytes;
-constexpr size_t kG64OffMu = kG64OffY + kG64Slots * 64 * 8;
+constexpr size_t kG64OffMu = kG64OffY + kG64Slots * kG64Rows * 8;
 constexpr int kG64Mu1 = 66;   // class-1 centre row: 16 bytes past a bank-aligned row, so lanes
                                // reading class-0 and class-1 centres of one column never collide
 constexpr size_t kG64OffRed = kG64OffMu + 136 * 8;                        // shift fold
 constexpr size_t kG64OffBar = kG64OffRed + kG64MmaWarps * 128 * 8 + 128;
 constexpr size_t kG64Smem = kG64OffBar + 2 * kG64Slots * 8 + 1024;       // + base alignment slack
-constexpr uint32_t kG64TxBytes = static_cast<uint32_t>(kG64RawBytes) + 512u;
+constexpr uint32_t kG64TxBytes = static_cast<uint32_t>(kG64RawBytes + kG64Rows * 8);
 static_assert(kG64MmaWarps * (36 * 32 * 2 + 2 * 64) * 8 <= kG64OffY, "S fold must fit in the raw ring");
 
 __host__ __device__ __forceinline__ int g64_q(int g) { return (g >> 1) | ((g & 1) << 2); }
@@ -432,17 +440,17 @@ gda_fit64_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant_
   uint64_t* const full = reinterpret_cast<uint64_t*>(smem + kG64OffBar);
   uint64_t* const empty = full + kG64Slots;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t ntiles = (n + 63) / 64;
+  const int64_t ntiles = (n + kG64Rows - 1) / kG64Rows;
   const int mt = static_cast<int>(ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0);
   auto tile_of = [&](int m) { return static_cast<int64_t>(blockIdx.x) + static_cast<int64_t>(m) * gridDim.x; };
-  auto rows_of = [&](int m) { return static_cast<int>(std::min<int64_t>(64, n - tile_of(m) * 64)); };
+  auto rows_of = [&](int m) { return static_cast<int>(std::min<int64_t>(kG64Rows, n - tile_of(m) * kG64Rows)); };
   auto issue = [&](int m) {   // tile m -> slot m % kG64Slots (4 swizzled boxes + the labels)
     const int s = m % kG64Slots;
-    const int row0 = static_cast<int>(tile_of(m) * 64);
+    const int row0 = static_cast<int>(tile_of(m) * kG64Rows);
     mbar_arrive_expect_tx(&full[s], kG64TxBytes);
 #pragma unroll
     for (int p = 0; p < 4; ++p) tma_load_2d(raw + s * kG64RawBytes + p * kG64BoxBytes, &tmx, 16 * p, row0, &full[s]);
-    tma_load_1d(ys + s * 64, &tmy, row0, &full[s]);
+    tma_load_1d(ys + s * kG64Rows, &tmy, row0, &full[s]);
   };
   if (tid == 0) {
     for (int s = 0; s < kG64Slots; ++s) {
@@ -530,10 +538,10 @@ gda_fit64_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant_
     const int s = m % kG64Slots, rows = rows_of(m);
     mbar_wait(&full[s], (m / kG64Slots) & 1);
     const unsigned char* rs = raw + s * kG64RawBytes;
-    const long long* yv = ys + s * 64;
+    const long long* yv = ys + s * kG64Rows;
 #pragma unroll
-    for (int st = 0; st < 2; ++st) {
-      const int r = 8 * warp + 4 * st + kq;
+    for (int st = 0; st < kG64Steps; ++st) {
+      const int r = 4 * kG64Steps * warp + 4 * st + kq;
       const bool valid = r < rows;   // rows past n: zero-filled by the TMA, excluded here
       const bool one = yv[r] == 1;
       const unsigned char* rowp = rs + r * 128 + ((qg ^ (r & 7)) << 4);
@@ -646,13 +654,13 @@ static int g64_maps(const double* x, const long long* y, int64_t n, CUtensorMap*
   DLX_REQUIRE(enc != nullptr, DLX_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t nn = static_cast<cuuint64_t>(std::max<int64_t>(n, 1));
   const cuuint64_t dx[2] = {64, nn}, sx[1] = {64 * 8};
-  const cuuint32_t bx[2] = {16, 64}, ex[2] = {1, 1};
+  const cuuint32_t bx[2] = {16, static_cast<cuuint32_t>(kG64Rows)}, ex[2] = {1, 1};
   CUresult r = enc(tmx, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(x), dx, sx, bx, ex,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   DLX_REQUIRE(r == CUDA_SUCCESS, DLX_ERR_CUDA, "cuTensorMapEncodeTiled(x) failed");
   const cuuint64_t dy[1] = {nn}, sy[1] = {8};
-  const cuuint32_t by[1] = {64}, ey[1] = {1};
+  const cuuint32_t by[1] = {static_cast<cuuint32_t>(kG64Rows)}, ey[1] = {1};
   r = enc(tmy, CU_TENSOR_MAP_DATA_TYPE_INT64, 1, const_cast<long long*>(y), dy, sy, by, ey,
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -1010,6 +1010,10 @@ void Executor::run_loop(const Stmt& s) {
   if (plan->fam == LoopPlan::GroupBy) rep["buckets"] = plan->k;
   if (plan->fam == LoopPlan::BucketRows) rep["buckets"] = plan->k, rep["d"] = plan->d;
   if (plan->fam == LoopPlan::GdaScatter || plan->fam == LoopPlan::Logistic) rep["d"] = plan->d;
+  if (plan->fam == LoopPlan::Logistic) {
+    const int lk = dlx_link_kind(&plan->link);
+    rep["link"] = lk == 1 ? "sigmoid" : lk == 2 ? "softsign" : "code";
+  }
   if (plan->fam == LoopPlan::Generic) rep["elems"] = live, rep["instructions"] = static_cast<int>(plan->code.size());
   if (plan->fam == LoopPlan::Compiled) {
     rep["elems"] = live;
@@ -1070,6 +1074,17 @@ void Executor::run_loop(const Stmt& s) {
 }
 
 void Executor::launch(const Stmt& s, LoopPlan& p, int64_t n, std::vector<VecP>& vecs, json& rep) {
+  if (sharded(p)) {   // contiguous index shards over ExecOptions.devices (shard.cpp)
+    rep["shards"] = static_cast<int>(devs_.size());
+    switch (p.fam) {
+      case LoopPlan::Kmeans: launch_kmeans_sharded(p, n, vecs, rep); return;
+      case LoopPlan::GroupBy: launch_groupby_sharded(p, n, vecs); return;
+      case LoopPlan::BucketRows: launch_bucket_rows_sharded(p, n, vecs); return;
+      case LoopPlan::GdaScatter: launch_gda2_sharded(p, n, vecs); return;
+      case LoopPlan::Logistic: launch_logistic_sharded(p, n, vecs, rep); return;
+      default: break;
+    }
+  }
   switch (p.fam) {
     case LoopPlan::Kmeans: launch_kmeans(s, p, n, vecs, rep); break;
     case LoopPlan::GroupBy: launch_groupby(p, n, vecs); break;
@@ -1156,6 +1171,7 @@ void Executor::launch_kmeans(const Stmt& s, LoopPlan& p, int64_t n, std::vector<
     U->wev = ev;
     U->host_valid = false;
     U->page_valid = false;
+    U->touched();
     for (int q : p.skip) mark_skip(q);
   }
   rep["update"] = U ? "device" : p.upd_vec >= 0 ? "host" : "none";
@@ -1275,6 +1291,7 @@ void Executor::launch_logistic(LoopPlan& p, int64_t n, std::vector<VecP>& V, jso
     U->wev = ev;
     U->host_valid = false;
     U->page_valid = false;
+    U->touched();
     for (int q : p.skip) mark_skip(q);
   }
   rep["update"] = U ? "device" : p.upd_vec >= 0 ? "host" : "none";

@@ -45,6 +45,15 @@ void ck(int rc) {
 }
 
 DevVec::~DevVec() {
+  if (!wins.empty()) {   // shard windows: freed on their shard's stream (after its readers)
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (const Win& w : wins) {
+      cudaSetDevice(w.dev);
+      cudaFreeAsync(w.p, w.st);
+    }
+    cudaSetDevice(cur);
+  }
   if (!p || borrowed) return;
   if (g_run && g_run->fence) (*g_run->fence)();   // a loop still in flight may read this buffer
   cudaFreeAsync(p, fst);
@@ -127,6 +136,12 @@ Executor::Executor(const Program& p, const ExecOpts& o, cudaStream_t st, DeviceR
     : P(p), opts_(o), st_(st), res_(res), lst_(st), sc_(take_scratch(p)), env_(sc_->env), bound_(sc_->bound),
       skip_(sc_->skip) {
   fence_ = [this] { fence(); };
+  if (o.ndevices >= 1 && o.devices)
+    devs_.assign(o.devices, o.devices + o.ndevices);
+  else
+    devs_.push_back(0);
+  primary_ = devs_[0];
+  replicate_ = getenv("DLX_SHARD_REPLICATE") != nullptr && atoi(getenv("DLX_SHARD_REPLICATE")) != 0;
 }
 
 Executor::~Executor() {
@@ -140,6 +155,16 @@ Executor::~Executor() {
     skip_[s] = 0;
   }
   sc_->touched.clear();
+  if (!xevents_.empty()) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto [dev, e] : xevents_) {
+      cudaSetDevice(dev);
+      cudaEventSynchronize(e);
+      cudaEventDestroy(e);
+    }
+    cudaSetDevice(cur);
+  }
   std::lock_guard<std::mutex> lk(P.scratch_mu);
   if (P.scratch.size() < 2) P.scratch.push_back(sc_);
 }
@@ -317,6 +342,7 @@ void Executor::widen(const VecP& v, cudaStream_t s) {
   cudaFreeAsync(v->p, s);
   v->p = w;
   v->i32 = false;
+  v->touched();   // same values, new layout: shard windows are stale
   if (s != st_) {   // a loop stream rewrote the buffer: later readers order after it
     cudaEvent_t ev = get_event();
     ckc(cudaEventRecord(ev, s), "cudaEventRecord");
@@ -418,6 +444,7 @@ Val Executor::vec_get(const VecP& v, int64_t i) {
 void Executor::vec_set(const VecP& v, int64_t i, const Val& x) {
   if (i < 0 || i >= v->n) trap("TrapIndexOutOfBounds: store index " + std::to_string(i));
   if (g_run->dry) return;
+  v->touched();
   if (v->i32) {   // the host writes reference Ints: widen the device copy first
     fence();
     widen(v, st_);
@@ -510,6 +537,7 @@ bool Executor::copy_run(const CopyRun& run) {
   }
   V->host_valid = false;
   V->page_valid = false;
+  V->touched();
   for (size_t t = 1; t < run.stmts.size(); ++t) mark_skip(run.stmts[t]);
   return true;
 }
@@ -615,6 +643,11 @@ Val Executor::exec_stmt(const Stmt& s) {
         }
       } else {
         v = new_vec(n, et, st_, false);
+        v->gen = true;
+        v->gen_int = ints;
+        v->gen_seed = opts_.seed;
+        v->gen_first = draws_;
+        v->gen_bound = ints ? atom(s.args[1]).i() : 0;
         if (g_run->dry) {
         } else if (ints) {
           ck(dlx_rng_ints(static_cast<int64_t*>(v->p), n, atom(s.args[1]).i(), opts_.seed, draws_, st_));
@@ -746,8 +779,27 @@ RunOut execute(const Program& p, const ExecOpts& o) {
   ctx.profile = getenv("DLX_PROGRAM_PROFILE") != nullptr;
   ctx.t0 = std::chrono::steady_clock::now();
   const auto t_run = std::chrono::steady_clock::now();
-  if (o.ndevices > 1) gen_fail("multi-device execution needs the sharded executor (ndevices > 1)");
   const int device = (o.ndevices >= 1 && o.devices) ? o.devices[0] : 0;
+  if (o.ndevices > 1 && !ctx.dry) {   // sharded loops (shard.cpp): every device must exist
+    int count = 0;
+    ckc(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+    for (int g = 0; g < o.ndevices; ++g)
+      if (o.devices[g] < 0 || o.devices[g] >= count)
+        throw Fail(DLX_ERR_ARG, "ExecOptions.devices[" + std::to_string(g) + "] = " + std::to_string(o.devices[g]) +
+                                    " is not a device (" + std::to_string(count) + " visible)");
+    for (int g = 1; g < o.ndevices; ++g)   // peer access where the hardware offers it (NVLink)
+      if (o.devices[g] != device) {
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, device, o.devices[g]);
+        if (can) {
+          cudaSetDevice(device);
+          cudaDeviceEnablePeerAccess(o.devices[g], 0);
+          cudaSetDevice(o.devices[g]);
+          cudaDeviceEnablePeerAccess(device, 0);
+          cudaGetLastError();   // already enabled: not an error here
+        }
+      }
+  }
   DeviceRes* res = nullptr;
   cudaStream_t st = nullptr;
   if (!ctx.dry) {

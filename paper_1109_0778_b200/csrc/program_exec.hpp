@@ -67,6 +67,24 @@ struct DevVec {
   // staging serves every printed element read until the next join (device layout)
   const unsigned char* snap = nullptr;
   cudaEvent_t snap_of = nullptr;   // the write (wev) the snapshot follows
+  // a synthetic source (VectorRand / VectorRandInt, not written since): shard windows on other
+  // devices are drawn there by skip-ahead (shard.cpp)
+  bool gen = false, gen_int = false;
+  uint64_t gen_seed = 0, gen_first = 0;
+  int64_t gen_bound = 0;
+  uint64_t ver = 0;   // bumped by every write (host stores, copy runs, device update groups, widening)
+  struct Win {        // elements [lo, hi) on a shard's device (shard.cpp)
+    int shard = -1, dev = -1;
+    void* p = nullptr;
+    int64_t lo = 0, hi = 0;
+    uint64_t ver = 0;
+    cudaStream_t st = nullptr;
+  };
+  std::vector<Win> wins;
+  void touched() {
+    ++ver;
+    gen = false;
+  }
   ~DevVec();
   size_t esize() const { return elem == Ty::Bool ? 1 : i32 ? 4 : 8; }   // device element bytes
   size_t hsize() const { return elem == Ty::Bool ? 1 : 8; }            // host element bytes
@@ -221,10 +239,21 @@ class Executor {
   void widen(const VecP& v, cudaStream_t s);
   nlohmann::json report = nlohmann::json::array();
   std::function<void()> fence_;   // RunCtx::fence points here during the run
+  // one contiguous index shard of a sharded loop (shard.cpp)
+  struct Shard {
+    int g = 0, dev = 0;
+    int64_t lo = 0, hi = 0;
+    cudaStream_t st = nullptr;
+    bool local = true;   // on the primary device, reading the vectors in place
+  };
 
  private:
   const Program& P;
   ExecOpts opts_;
+  std::vector<int> devs_;     // ExecOptions.devices; devs_[0] is the primary (vectors live there)
+  int primary_ = 0;
+  bool replicate_ = false;    // DLX_SHARD_REPLICATE=1: shard windows even on the primary (tests)
+  std::vector<std::pair<int, cudaEvent_t>> xevents_;   // events created on shard devices
   uint64_t draws_ = 0;
   cudaStream_t st_;
   DeviceRes* res_;
@@ -323,6 +352,17 @@ class Executor {
   void launch_logistic(LoopPlan& p, int64_t n, std::vector<VecP>& V, nlohmann::json& rep);
   void launch_generic(LoopPlan& p, int64_t n, std::vector<VecP>& V);
   void launch_compiled(LoopPlan& p, int64_t n, std::vector<VecP>& V);
+  // sharded launches (shard.cpp)
+  bool sharded(const LoopPlan& p) const;
+  std::vector<Shard> shards(int64_t n);
+  cudaEvent_t dev_event(int dev);
+  const void* window(const VecP& v, const Shard& s, int64_t lo, int64_t hi);
+  void run_shards(std::vector<Shard>& sh, const std::function<void(Shard&)>& body);
+  void launch_kmeans_sharded(LoopPlan& p, int64_t n, std::vector<VecP>& V, nlohmann::json& rep);
+  void launch_groupby_sharded(LoopPlan& p, int64_t n, std::vector<VecP>& V);
+  void launch_bucket_rows_sharded(LoopPlan& p, int64_t n, std::vector<VecP>& V);
+  void launch_gda2_sharded(LoopPlan& p, int64_t n, std::vector<VecP>& V);
+  void launch_logistic_sharded(LoopPlan& p, int64_t n, std::vector<VecP>& V, nlohmann::json& rep);
   void bind_scalars(const LoopPlan& p, const int64_t* hres);
   void* dalloc(size_t bytes);
   void dfree(void* p);

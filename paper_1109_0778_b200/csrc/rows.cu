@@ -10,6 +10,9 @@
 // (gda_dmma.cu); the CUDA-core register-tile kernel below covers 64 < d <= 128.
 #include <algorithm>
 
+#include <cstdlib>
+#include <utility>
+
 #include "common.cuh"
 
 namespace dlx {
@@ -109,6 +112,39 @@ __device__ __forceinline__ int lane_of_row(int r) {
 struct SigmoidLink {
   __device__ __forceinline__ double operator()(double z) const { return 1.0 / (1.0 + exp(-z)); }
 };
+struct SoftsignLink {
+  __device__ __forceinline__ double operator()(double z) const { return z / (1.0 + fabs(z)); }
+};
+// The link code as an expression over t (r[0]): the canonical sigmoid 1 / (1 + exp(0 - t)) and
+// softsign t / (1 + |t|) that staged logistic-regression loops carry run as the fixed functors
+// above (the same IEEE operations in the same order, so bit-identical: 0 - t and -t differ only
+// in the sign of a zero, and exp(+0) = exp(-0)); any other code runs the interpreted CodeLink.
+enum LinkKind { kLinkCode = 0, kLinkSigmoid = 1, kLinkSoftsign = 2 };
+static bool link_const(const dlx_link_code& c, int q, double v) { return c.op[q] == DLX_LINK_CONST && c.imm[q] == v; }
+// the instruction that last wrote register r before instruction q (-1: the input t when r == 0)
+static int link_def(const dlx_link_code& c, int r, int q) {
+  for (int p = q - 1; p >= 0; --p)
+    if (c.dst[p] == r) return p;
+  return r == 0 ? -1 : -2;
+}
+static LinkKind link_kind(const dlx_link_code& c) {
+  const int top = link_def(c, c.out, c.n);
+  if (top < 0 || c.op[top] != DLX_LINK_DIV) return kLinkCode;
+  const int num = link_def(c, c.a[top], top), den = link_def(c, c.b[top], top);
+  if (den < 0 || c.op[den] != DLX_LINK_ADD) return kLinkCode;
+  int l = link_def(c, c.a[den], den), r = link_def(c, c.b[den], den);
+  if (l >= 0 && !link_const(c, l, 1.0)) std::swap(l, r);
+  if (l < 0 || !link_const(c, l, 1.0) || r < 0) return kLinkCode;
+  if (num >= 0 && link_const(c, num, 1.0) && c.op[r] == DLX_LINK_EXP) {       // 1 / (1 + exp(0 - t))
+    const int sub = link_def(c, c.a[r], r);
+    if (sub < 0 || c.op[sub] != DLX_LINK_SUB) return kLinkCode;
+    const int z = link_def(c, c.a[sub], sub), t = link_def(c, c.b[sub], sub);
+    return (z >= 0 && link_const(c, z, 0.0) && t == -1) ? kLinkSigmoid : kLinkCode;
+  }
+  if (num == -1 && c.op[r] == DLX_LINK_ABS && link_def(c, c.a[r], r) == -1) return kLinkSoftsign;   // t / (1 + |t|)
+  return kLinkCode;
+}
+
 struct CodeLink {
   dlx_link_code c;
   // registers: r[0] = t; every instruction writes r[dst]; IEEE round-to-nearest, no contraction
@@ -403,6 +439,8 @@ int dlx_logreg_grad(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
   return combine_f64(parts, grid, d, d_grad, stream);
 }
 
+int dlx_link_kind(const dlx_link_code* h_link) { return h_link ? static_cast<int>(link_kind(*h_link)) : -1; }
+
 int dlx_rowdot_link_grad(const double* d_x, const int64_t* d_y, int64_t n, int32_t d, const double* d_theta,
                          const dlx_link_code* h_link, double* d_h, double* d_grad, void* d_workspace,
                          size_t workspace_bytes, dlx_stream_t stream) {
@@ -420,12 +458,17 @@ int dlx_rowdot_link_grad(const double* d_x, const int64_t* d_y, int64_t n, int32
   double* parts = static_cast<double*>(d_workspace);
   const size_t smem = static_cast<size_t>(kRowWarps) * d * sizeof(double);
   const long long* y = reinterpret_cast<const long long*>(d_y);
-  const CodeLink link{*h_link};
-#define DLX_RDL(MM)                                                                                              \
-  (d_h ? launch_pdl(logreg_grad_kernel<MM, CodeLink, true>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, \
-                    d_theta, link, d_h, parts)                                                                   \
-       : launch_pdl(logreg_grad_kernel<MM, CodeLink, false>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, \
-                    d_theta, link, nullptr, parts))
+  const CodeLink code{*h_link};
+  const LinkKind kind = getenv("DLX_LINK_INTERPRET") ? kLinkCode : link_kind(*h_link);
+#define DLX_RDL_L(MM, L, LV)                                                                                        \
+  (d_h ? launch_pdl(logreg_grad_kernel<MM, L, true>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d,   \
+                    d_theta, LV, d_h, parts)                                                                      \
+       : launch_pdl(logreg_grad_kernel<MM, L, false>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d,  \
+                    d_theta, LV, nullptr, parts))
+#define DLX_RDL(MM)                                                                    \
+  (kind == kLinkSigmoid ? DLX_RDL_L(MM, SigmoidLink, SigmoidLink{})                    \
+   : kind == kLinkSoftsign ? DLX_RDL_L(MM, SoftsignLink, SoftsignLink{})               \
+                           : DLX_RDL_L(MM, CodeLink, code))
   switch (m_for(d)) {
     case 1: DLX_CUDA(DLX_RDL(1)); break;
     case 2: DLX_CUDA(DLX_RDL(2)); break;
@@ -433,6 +476,7 @@ int dlx_rowdot_link_grad(const double* d_x, const int64_t* d_y, int64_t n, int32
     default: DLX_CUDA(DLX_RDL(4)); break;
   }
 #undef DLX_RDL
+#undef DLX_RDL_L
   DLX_LAUNCHED("logreg_grad_kernel");
   return combine_f64(parts, grid, d, d_grad, stream);
 }

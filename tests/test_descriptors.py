@@ -167,3 +167,19 @@ def test_nonfinite_literals_round_trip():
     assert '"inf"' in json.dumps(prog) and '"nan"' in json.dumps(prog)
     r = Program(prog).run(dry_run=True)
     assert r.output.split() == ["inf", "-inf", "nan", "1.5"]
+
+
+@pytest.mark.parametrize("link", ["sigmoid", "softsign"])
+def test_logistic_link_runs_as_fixed_function(link, monkeypatch):
+    """The link compiled from the staged loop body (1 / (1 + exp(0 - t)), t / (1 + |t|)) is
+    recognised and evaluated by the fixed functor, not the per-row interpreter (csrc/rows.cu
+    link_kind); the reference-staged logreg fixture carries the softsign."""
+    import json
+    from paper_1109_0778_b200 import descriptors as D
+    from paper_1109_0778_b200.program import run_program
+    monkeypatch.setenv("DLX_PROGRAM_DRYRUN", "1")
+    _, rep = run_program(D.logreg_program(1000, 8, 2, 0.001, link=link), seed=1)
+    assert [r["link"] for r in rep] == [link, link]
+    if link == "softsign":
+        fx = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "staged", "logreg_n20000_d8_it2.json")))
+        assert [r["link"] for r in run_program(fx["program"], seed=1)[1]] == ["softsign", "softsign"]

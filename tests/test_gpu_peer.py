@@ -52,7 +52,7 @@ def _work(rank, world, port, q):
     from paper_1109_0778_b200 import multiloops as ml
     from paper_1109_0778_b200.comm import PeerComm, shard_range
     from paper_1109_0778_b200.programs import KMeansProgram, LogRegProgram
-    comm = PeerComm(rank, world, cap_bytes=1 << 20)
+    comm = PeerComm(rank, world, cap_bytes=2 << 20)   # two 1 MiB slots: the 512 KiB GroupBy record
     out = {}
     try:
         # k-means: eager first iteration, then CUDA-graph replays (the bench's form)
