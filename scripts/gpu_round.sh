@@ -30,7 +30,7 @@ for w in $WHAT; do
          timeout 1200 ncu --set full --clock-control none --import-source on -k regex:kmeans_screened -s 3 -c 1 -o $OUT/prof_kmeans \
            python bench.py --config c4 --steps 4 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_kmeans.log 2>&1
          for c in c5 l16 c3; do
-           timeout 900 ncu --set full --clock-control none --import-source on -k regex:"groupby_smem|logreg_grad|gda_pass2" -s 4 -c 1 -o $OUT/prof_$c \
+           timeout 900 ncu --set full --clock-control none --import-source on -k regex:"groupby_smem|logreg_grad|gda_fit64" -s 4 -c 1 -o $OUT/prof_$c \
              python bench.py --config $c --steps 4 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_$c.log 2>&1
          done ;;
   esac
