@@ -444,7 +444,9 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
     # ---- end to end through the public API with host buffers ----------------------------------
     e2e = None
     e2e_family = None
-    if family == "kmeans":
+    if args.no_e2e:
+        pass   # A/B runs of kernel variants: the device-timed value only
+    elif family == "kmeans":
         e2e_family = e2e_kmeans(args, p, n_local, lo, comm, dist, dev)
         # one GPU: the headline e2e is the reference-facing drop-in (dlx_program_execute) with
         # host buffers; sharded runs keep the family API's (the drop-in runs one device)
@@ -727,6 +729,7 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--method", type=int, default=0, help="k-means: 0 auto, 1 direct fp64, 2 screened")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the e2e legs (kernel A/B runs)")
     ap.add_argument("--comm", default="peer", choices=["peer", "nccl"],
                     help="N>1 exchange: the fused peer-memory allreduce+update kernel (csrc/peer.cu, "
                          "ascending-rank fold), or NCCL allReduce + a separate update kernel")

@@ -10,10 +10,12 @@
 // The GPU tests run "program" through dlx_program_run and compare with "expected".
 //
 //   oracle/_ref/stage_programs OUT_DIR [NAME]  (built by `make -C oracle -f ref.mk`)
-// With NAME only that program is staged; the headline-shape program
-// "kmeans_n16777216_d64_k64_it1" (C4, k*(d+1) = 4,160 reduces in one fused loop) is staged only
-// on request and without "expected" (the sequential MiniC evaluation of 16M x 64 x 64 would take
-// hours): its GPU run is checked against the oracle port instead (scripts/c4_staged.py).
+// With NAME only that program is staged; the headline-shape programs
+// "kmeans_n16777216_d64_k64_it1[_unfused]" (C4, k*(d+1) = 4,160 reduces) are staged only on
+// request and write only the descriptor (OUT/NAME.program.json; the sequential MiniC evaluation
+// of 16M x 64 x 64 would take hours): the fused one takes the reference's quadratic fuse_loops
+// (> 25 min), the unfused one ~6 s and is fused by the executor (csrc/fuse.cpp).
+// Programs named *_unfused skip fuse_loops and are serialised with "fusion": "executor".
 #include <chrono>
 #include <cstdio>
 #include <fstream>
@@ -234,11 +236,23 @@ int main(int argc, char** argv) {
       {"axpy_n100000", [](Stage& st) { axpy(st, 100000); }},
       {"count_gt_n100000", [](Stage& st) { count_gt(st, 100000); }},
       {"find_count_n100000", [](Stage& st) { find_count(st, 100000); }},
+      // unfused: the reference's fuse_loops is skipped and the executor fuses the root loops
+      // (csrc/fuse.cpp); "expected" is the unfused program's own MiniC output (it equals the
+      // fused program's)
+      {"kmeans_n4096_d16_k8_it2_unfused", [](Stage& st) { kmeans(st, 4096, 16, 8, 2); }},
+      {"groupby_n100000_k16_unfused", [](Stage& st) { groupby(st, 100000, 16); }},
+      {"gda_n20000_d4_unfused", [](Stage& st) { gda(st, 20000, 4); }},
+      {"logreg_n20000_d8_it2_unfused", [](Stage& st) { logreg(st, 20000, 8, 2, 1.0 / 20000); }},
+      {"mean_variance_n100000_unfused", [](Stage& st) { mean_variance(st, 100000); }},
+      {"find_count_n100000_unfused", [](Stage& st) { find_count(st, 100000); }},
   };
   const std::string only = argc > 2 ? argv[2] : "";
-  if (only == "kmeans_n16777216_d64_k64_it1")
+  if (only == "kmeans_n16777216_d64_k64_it1" || only == "kmeans_n16777216_d64_k64_it1_unfused")
     specs = {{only, [](Stage& st) { kmeans(st, 16777216, 64, 64, 1); }}};
   const bool eval = only.rfind("kmeans_n16777216", 0) != 0;
+  auto ends_with = [](const std::string& a, const std::string& b) {
+    return a.size() >= b.size() && a.compare(a.size() - b.size(), b.size(), b) == 0;
+  };
   for (const Spec& sp : specs) {
     if (!only.empty() && sp.name != only) continue;
     const auto t0 = std::chrono::steady_clock::now();
@@ -247,10 +261,23 @@ int main(int argc, char** argv) {
     sp.body(st);
     st.finish();
     auto g = st.take_graph();
-    FusionOutcome fo = fuse_loops(g, /*with_motion=*/false);
+    const bool unfused = ends_with(sp.name, "_unfused");
+    FusionOutcome fo;
+    if (unfused) fo.graph = g;
+    else fo = fuse_loops(g, /*with_motion=*/false);
     Schedule s = build_schedule(*fo.graph, ScheduleOptions{true, false});
-    CodegenResult cg = run_codegen(*fo.graph, s);
     const auto t1 = std::chrono::steady_clock::now();
+    const std::string program = unfused ? stagekit_dlx::to_dlx_program_unfused(*fo.graph, s)
+                                        : stagekit_dlx::to_dlx_program(*fo.graph, s);
+    const auto t1s = std::chrono::steady_clock::now();
+    if (!eval) {   // production shape: the descriptor alone (no MiniC: codegen renders 4,161 loops)
+      std::ofstream(out_dir + "/" + sp.name + ".program.json") << program << "\n";
+      std::printf("%-28s stage+schedule %.2fs  serialise %.2fs  %zu bytes\n", sp.name.c_str(),
+                  std::chrono::duration<double>(t1 - t0).count(),
+                  std::chrono::duration<double>(t1s - t1).count(), program.size());
+      continue;
+    }
+    CodegenResult cg = run_codegen(*fo.graph, s);
     oracle_minic::Evaluator ev(seed);
     oracle_minic::EvalResult r;
     if (eval) r = ev.run(cg.program);
@@ -263,8 +290,8 @@ int main(int argc, char** argv) {
     fx["seed"] = seed;
     fx["fused_pairs"] = fo.fused_pairs;
     fx["root_loops"] = loops;
-    fx["program"] = json::parse(stagekit_dlx::to_dlx_program(*fo.graph, s));
-    fx["deg"] = json::parse(cg.deg_json);
+    fx["program"] = json::parse(program);
+    fx["deg"] = unfused ? json(nullptr) : json::parse(cg.deg_json);
     if (sp.name.size() > 7 && sp.name.compare(sp.name.size() - 7, 7, "_assign") == 0) {
       // the DEG's ordered-effect anti-dependence lists grow quadratically with the 8,192 Print
       // statements (322 MB); the executor never reads it, so this fixture carries none

@@ -44,11 +44,16 @@ json expr_json(const Expr& e) {
   return j;
 }
 
+// statements and blocks are keyed by id in std::map-ordered objects: an ordered_json object
+// looks keys up linearly, which made serialising an unfused production-shape program (4,161
+// root loops) quadratic
+using keyed_json = nlohmann::json;
+
 struct Writer {
   const Graph& g;
   const Schedule& s;
-  json stmts = json::object();
-  json blocks = json::object();
+  keyed_json stmts = keyed_json::object();
+  keyed_json blocks = keyed_json::object();
   std::set<BlockId> seen;
 
   void block(BlockId b) {
@@ -63,7 +68,7 @@ struct Writer {
     }
     jb["result"] = expr_json(bd.result);
     jb["bound"] = bd.bound;
-    blocks[std::to_string(b)] = std::move(jb);
+    blocks[std::to_string(b)] = keyed_json::parse(jb.dump());
   }
 
   void stmt(int32_t idx) {
@@ -122,23 +127,28 @@ struct Writer {
       }
       js["loop"] = std::move(jl);
     }
-    stmts[std::to_string(st.sym)] = std::move(js);
+    stmts[std::to_string(st.sym)] = keyed_json::parse(js.dump());
   }
 };
 
 }  // namespace
 
-std::string to_dlx_program(const Graph& g, const Schedule& s) {
+std::string to_dlx_program(const Graph& g, const Schedule& s, bool with_deg, bool executor_fusion) {
   Writer w{g, s};
   w.block(g.root());
-  json j;
-  j["format"] = "dlx-program/1";
-  j["root"] = g.root();
-  j["stmts"] = std::move(w.stmts);
-  j["blocks"] = std::move(w.blocks);
-  // the DEG exactly as the reference builds it (codegen.cpp:497-588)
-  j["deg"] = json::parse(deg_to_json(build_kernels(g, s)));
-  return j.dump();
+  std::string out = "{\"format\":\"dlx-program/1\",\"root\":" + std::to_string(g.root());
+  // an unfused graph: the executor fuses the root loops itself (csrc/fuse.cpp)
+  if (executor_fusion) out += ",\"fusion\":\"executor\"";
+  out += ",\"stmts\":" + w.stmts.dump() + ",\"blocks\":" + w.blocks.dump();
+  // the DEG exactly as the reference builds it (codegen.cpp:497-588); the executor derives its
+  // own order and overlap from the statements, so an unfused production-shape program (whose
+  // ordered-effect anti-dependence lists grow quadratically) can leave it out
+  if (with_deg) out += ",\"deg\":" + json::parse(deg_to_json(build_kernels(g, s))).dump();
+  return out + "}";
+}
+
+std::string to_dlx_program_unfused(const Graph& g, const Schedule& s) {
+  return to_dlx_program(g, s, /*with_deg=*/false, /*executor_fusion=*/true);
 }
 
 }  // namespace stagekit_dlx

@@ -22,7 +22,17 @@
 namespace stagekit_dlx {
 
 // Serialise a scheduled graph (call with a schedule built with motion off).
-std::string to_dlx_program(const stagekit::Graph& g, const stagekit::Schedule& s);
+// with_deg = false leaves the DEG out (the executor does not need it; unfused production-shape
+// programs have quadratically many anti-dependence entries); executor_fusion marks a graph the
+// reference's fuse_loops has not run on, so the executor fuses its root loops (csrc/fuse.cpp).
+std::string to_dlx_program(const stagekit::Graph& g, const stagekit::Schedule& s, bool with_deg = true,
+                           bool executor_fusion = false);
+
+// The production-shape path: stage, build_schedule (motion off), and
+// serialise WITHOUT the reference's fuse_loops (quadratic: one clone of the whole graph and one
+// rebuilt schedule per fused pair, fusion.cpp:170-288) — the executor fuses the root loops in
+// one linear pass instead.  No DEG.
+std::string to_dlx_program_unfused(const stagekit::Graph& g, const stagekit::Schedule& s);
 
 // Execute on the B200 executor through the C ABI; mirrors interpret()'s result shape.
 // Throws stagekit::StagingError(GenerationFailed) for loops the executor cannot lower and

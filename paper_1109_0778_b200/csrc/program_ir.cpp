@@ -2,6 +2,8 @@
 // (see program_ir.hpp).  Runs once per program handle; executions reuse the result.
 #include "program_ir.hpp"
 
+#include "fuse.hpp"
+
 #include <charconv>
 #include <cmath>
 #include <json.hpp>
@@ -371,6 +373,9 @@ std::shared_ptr<Program> parse_program(const char* text, size_t len) {
     if (p.has_block[b])
       for (int s : p.blocks[b].stmts) p.stmt(s);
   p.block(p.root);
+  // an unfused graph (the adapter skipped the reference's fuse_loops): fuse here, before the
+  // analyses, so update groups and copy runs see the fused loops
+  if (j.value("fusion", "") == "executor") p.fused_pairs = fuse_loops_linear(p);
   Analyzer an{p, {}};
   an.count_uses();
   an.find_update_groups();

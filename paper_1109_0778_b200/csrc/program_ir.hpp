@@ -120,6 +120,7 @@ struct LoopPlan;   // a cached lowering (program.cpp)
 struct Program {
   int root = -1;
   int max_sym = -1;
+  int fused_pairs = 0;               // loop pairs fused by the executor ("fusion": "executor")
   std::vector<Stmt> stmts;           // indexed by sym; op == Unknown and sym == -1 for holes
   std::vector<Block> blocks;         // indexed by block id
   std::vector<uint8_t> has_block;

@@ -420,3 +420,76 @@ def test_trap_of_earlier_loop_wins(serial, monkeypatch):
     fx = load("mean_variance_n100000")
     text, _ = run_program(fx["program"], seed=1)
     assert all(same_value(g, e) for g, e in zip(lines(text), lines(fx["expected"])))
+
+
+# ---- the executor's own fusion pass (csrc/fuse.cpp) --------------------
+# Fixtures *_unfused are the same reference-staged programs with the reference's fuse_loops
+# skipped (integration/stage_programs.cpp): the executor fuses their root (and nested) loops.
+UNFUSED = sorted(os.path.basename(f)[:-len("_unfused.json")] for f in FIXTURES if f.endswith("_unfused.json"))
+C4_UNFUSED = os.path.join(HERE, "golden", "staged_c4", "kmeans_n16777216_d64_k64_it1_unfused.program.json.xz")
+
+
+def _strip(report):
+    return [{k: v for k, v in e.items() if k not in ("loop", "cached")} for e in report]
+
+
+def test_unfused_fixtures_present():
+    assert set(UNFUSED) >= {"kmeans_n4096_d16_k8_it2", "groupby_n100000_k16", "gda_n20000_d4",
+                            "logreg_n20000_d8_it2", "mean_variance_n100000", "find_count_n100000"}
+
+
+@pytest.mark.parametrize("name", UNFUSED)
+def test_executor_fusion_matches_reference_fusion_dry_run(name, monkeypatch):
+    """CPU: the unfused reference-staged program, fused by the executor, lowers loop for loop
+    like the program the reference's fuse_loops fused (families, live elems, shapes, update
+    placement); the unfused program's own MiniC output equals the fused one's."""
+    from paper_1109_0778_b200.program import run_program
+    monkeypatch.setenv("DLX_PROGRAM_DRYRUN", "1")
+    fused, unf = load(name), load(name + "_unfused")
+    assert unf["program"]["fusion"] == "executor" and unf["fused_pairs"] == 0
+    assert unf["root_loops"] > fused["root_loops"]
+    assert fused["expected"] == unf["expected"]
+    _, ra = run_program(fused["program"], seed=1)
+    _, rb = run_program(unf["program"], seed=1)
+    assert _strip(ra) == _strip(rb)
+
+
+def test_executor_fusion_c4_shape_dry_run(monkeypatch):
+    """CPU: the headline program (one k-means iteration at N=16M, d=k=64) staged through the
+    reference DSL WITHOUT the reference's fuse_loops (4,161 root loops; the reference's own
+    fusion of it did not finish in 25 min) fuses in the executor into the one k-means
+    multiloop with all 4,161 elems live, the centroid update on the device."""
+    import lzma
+    import time
+    from paper_1109_0778_b200.program import Program
+    monkeypatch.setenv("DLX_PROGRAM_DRYRUN", "1")
+    with lzma.open(C4_UNFUSED, "rt") as f:
+        text = f.read()
+    p = json.loads(text)
+    root = p["blocks"][str(p["root"])]["stmts"]
+    assert p["fusion"] == "executor"
+    assert sum(p["stmts"][str(s)]["op"] == "ParallelLoop" for s in root) == 4161
+    t0 = time.time()
+    r = Program(text).run(dry_run=True)
+    assert time.time() - t0 < 60
+    assert len(r.report) == 1
+    e = r.report[0]
+    assert (e["family"], e["live_elems"], e["n"], e["d"], e["k"], e["update"]) == \
+        ("kmeans", 4161, 16_777_216, 64, 64, "device")
+
+
+@pytest.mark.gpu
+def test_executor_fusion_c4_shape_on_b200():
+    """B200: the unfused C4 program fused by the executor prints exactly what the directly built
+    C4 descriptor (descriptors.kmeans_program, pinned to the reference-staged fixtures) prints:
+    the assignment of row 0, the 64 counts and all 4,096 updated centroids."""
+    import lzma
+    from paper_1109_0778_b200.descriptors import kmeans_program
+    from paper_1109_0778_b200.program import Program
+    with lzma.open(C4_UNFUSED, "rt") as f:
+        got = Program(f.read()).run(seed=1)
+    exp = Program(kmeans_program(16_777_216, 64, 64, 1)).run(seed=1)
+    assert [r["family"] for r in got.report] == ["kmeans"]
+    g, e = lines(got.output), lines(exp.output)
+    assert len(g) == len(e) == 1 + 64 + 64 * 64
+    assert g == e
