@@ -245,6 +245,8 @@ int main(int argc, char** argv) {
       {"logreg_n20000_d8_it2_unfused", [](Stage& st) { logreg(st, 20000, 8, 2, 1.0 / 20000); }},
       {"mean_variance_n100000_unfused", [](Stage& st) { mean_variance(st, 100000); }},
       {"find_count_n100000_unfused", [](Stage& st) { find_count(st, 100000); }},
+      {"axpy_n100000_unfused", [](Stage& st) { axpy(st, 100000); }},
+      {"count_gt_n100000_unfused", [](Stage& st) { count_gt(st, 100000); }},
   };
   const std::string only = argc > 2 ? argv[2] : "";
   if (only == "kmeans_n16777216_d64_k64_it1" || only == "kmeans_n16777216_d64_k64_it1_unfused")

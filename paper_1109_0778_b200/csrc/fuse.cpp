@@ -7,16 +7,21 @@
 // range VectorLength(c) for a dense collect output c of A (vertical, fusion.cpp:204-210); L's
 // reads of A's collect outputs at L's own index become the producing elem's value
 // (contraction), L's index becomes A's, L's body-scope statements join A's and L's elems are
-// appended to A's, in order.  How it does it is different: the reference clones the whole graph
-// and rebuilds the whole schedule for every fused pair and restarts its scan (quadratic: one
+// appended to A's, in order.  One deliberate difference: a vertical pair A -> VectorLength(c) ->
+// L fuses here, while the reference's cycle check rejects it — the VectorLength statement is
+// an intermediate on a path from A to L (fusion.cpp:229, PairScan::path_avoiding_direct), so its
+// vertical rule (fusion.cpp:204-210) can never fire; here the length of a dense collect of A
+// is A's range and L's range is re-pointed at it.  How it does it is different: the reference
+// clones the whole graph and rebuilds the whole schedule for every fused pair and restarts its
+// scan (quadratic: one
 // k-means iteration at k = d = 64, 4,160 reduces, did not finish in 25 min), while this pass
 // walks each statement list once, keeping per earlier loop the symbols defined and the vectors
 // written since it (linear in the program, up to the number of open candidates).
 //
 // Legality (checked per pair, conservatively):
 //   * neither loop has a Foreach elem (effectful disjoint writes) and L's blocks hold no ordered
-//     effect (Print, VectorUpdate, VarWrite) and no random source (the draw order is program
-//     order);
+//     effect (Print, VectorUpdate, VarWrite), no allocation of mutable storage and no random
+//     source (the draw order is program order);
 //   * L reads no symbol defined by a statement between A and L (L moves up to A) and no vector
 //     or variable written between them;
 //   * L reads A's outputs only as VectorApply(c, i_L) for a dense (non-append) collect output c
@@ -90,6 +95,8 @@ struct Fuser {
       }
       if (st.op == Op::Print) S.effects = true;
       if (st.op == Op::VectorRand || st.op == Op::VectorRandInt) S.random = true;
+      // a loop allocating mutable storage is not fusable (fusion.cpp: fusable_loop)
+      if (st.op == Op::VectorNew || st.op == Op::VarAlloc) S.effects = true;
       for (int b : st.blocks)
         if (valid_block(b)) atom(P.blocks[b].result);
       if (st.loop) {
@@ -175,7 +182,7 @@ struct Fuser {
       if (it == len_of.end()) return false;
       bool ok = false;
       for (const Elem& e : la.elems)
-        if (e.kind == Elem::Collect && !e.append && e.out == it->second) ok = true;
+        if (e.kind == Elem::Collect && !e.append && e.cond < 0 && e.out == it->second) ok = true;
       if (!ok) return false;
       vertical = true;
     }
@@ -184,7 +191,9 @@ struct Fuser {
     std::unordered_set<int> a_outs;
     for (const Elem& e : la.elems) {
       a_outs.insert(e.out);
-      if (e.kind == Elem::Collect && !e.append && valid_block(e.elem)) collect_val[e.out] = P.blocks[e.elem].result;
+      // dense unconditional collects only (fusion.cpp: dense_collect_outs)
+      if (e.kind == Elem::Collect && !e.append && e.cond < 0 && valid_block(e.elem))
+        collect_val[e.out] = P.blocks[e.elem].result;
     }
     // L's reads: nothing defined or written since A (except a vertical range's length symbol)
     for (int r : SL.reads) {
