@@ -34,6 +34,19 @@
 // sample to the exact chain over every centroid.  NaN / inf centroids never win the chain
 // and are excluded from the screen.
 //
+// Three accumulators (the default, DLX_KMEANS_SCREEN_ACC=3).  The TMEM read-out of the screen
+// accumulators (128 lanes x 4 B per column) is the epilogue's floor per tile, so W2 is not
+// accumulated: 0 <= W2_c <= 255 sum_j (l'_cj + G_cj) =: 2^16 beta_c, and with
+// Q3 = 256 HH + CR + (W1>>8) the score T3_c = nm_c - 2 Q3_c brackets the distance within
+// [T3_c - 4.5 - 2 beta_c - 2e, T3_c + 1 + 2e]: window W3 = W + 2 ceil(max_c beta_c).  Rows with
+// several W3-survivors (~0.2 % on uniform data, against ~0.07 % for W) are refined in the
+// epilogue before they count as pending: their W2_c for the survivors only is summed exactly
+// from the sample's b6 / b5 planes (still in the plane buffer) and the centroid planes with
+// dp4a, T4_c = T3_c - 2 (W2_c >> 16) is the four-accumulator score, and the survivors are
+// re-screened with W (sound: every centroid outside the W3-survivors already lost).  So the
+// pending rows are exactly those of the four-accumulator screen, and a quarter of the TMEM
+// read-out (and its W2 arithmetic) is gone from every row.
+//
 // Bucket-reduce.  The eight planes of a 128-sample tile are stored as four SW128 buffers of
 // 128-byte rows [b7|b6], [b5|b4], [b3|b2], [b1|b0] (row = sample).  Read K-major they are the
 // screen's A operand; read MN-major (M = plane x column, K = sample) the SAME bytes are the A
@@ -95,6 +108,15 @@ constexpr int kNumA = 3;     // plane buffers in flight
 #define DLX_KMEANS_L2_AHEAD 3
 #endif
 constexpr int kL2Ahead = DLX_KMEANS_L2_AHEAD;   // converters' L2 prefetch distance (tiles; 0 = off)
+#ifndef DLX_KMEANS_SCREEN_ACC
+#define DLX_KMEANS_SCREEN_ACC 3
+#endif
+constexpr int kAcc = DLX_KMEANS_SCREEN_ACC;   // screen accumulators: 3 (HH, CR, W1; W2 refined) or 4
+static_assert(kAcc == 3 || kAcc == 4, "screen accumulators");
+#ifndef DLX_KMEANS_REFINE
+#define DLX_KMEANS_REFINE 0
+#endif
+constexpr bool kRefine = DLX_KMEANS_REFINE;   // 3 accumulators: refine W3-survivors in the epilogue
 // warpgroup 0: warp 0 screen MMAs, warp 1 fold MMAs, warp 2 tail (warp 3 idle); warpgroup 1:
 // epilogue; then the converter warpgroups.  Registers are rebalanced with setmaxnreg after the
 // prologue: warpgroup 0 drops to 32, the epilogue runs at 128, converters take the rest.
@@ -126,7 +148,7 @@ struct Misc {
   uint64_t t_full, t_empty, fold_done;
   unsigned long long valid;
   uint32_t tmem_base;
-  int em, yabs, disabled, window;
+  int em, yabs, disabled, window, window4, bsum_max;   // window4: W; window: W (4 acc) or W3
   uint32_t mu_maxhi;
   alignas(16) int nm0[kMaxK];             // floor(|mu_c|^2 / U) + sum_j M_cj
   double nmf[kMaxK];
@@ -255,6 +277,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     S.valid = 0;
     S.yabs = 0;
     S.mu_maxhi = 0;
+    S.bsum_max = 0;
     fence_mbar_init();
   }
   if (tid < kMaxK) S.cnt[tid] = 0;
@@ -307,7 +330,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     const unsigned long long valid = S.valid;
     for (int c = warp; c < kMaxK; c += kThreads / 32) {
       const bool cv = (valid >> c) & 1;
-      int sa = 0, ssum = 0;
+      int sa = 0, ssum = 0, sb = 0;
       for (int j = lane; j < kMaxD; j += 32) {
         // h'' = (Y >> 16) + 128 in [64, 192] (unsigned; the offset adds a per-sample constant to
         // every centroid's score); invalid centroids and columns past d are all-zero rows
@@ -318,11 +341,16 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         Bm[sw64_offset(128 + c, j)] = static_cast<unsigned char>(Y);
         sa += abs(Y);
         ssum += Y;
+        sb += ((Y >> 8) & 255) + (Y & 255);   // l'_cj + G_cj (zero for dead rows)
       }
       sa = __reduce_add_sync(0xffffffffu, sa);
       ssum = __reduce_add_sync(0xffffffffu, ssum);
+      sb = __reduce_add_sync(0xffffffffu, sb);
       if (lane == 0) {
-        if (cv) atomicMax(&S.yabs, sa);
+        if (cv) {
+          atomicMax(&S.yabs, sa);
+          atomicMax(&S.bsum_max, sb);
+        }
         // per-launch score constants (the sample exponent is fixed at e_t = e_m + 1)
         S.nm0[c] = (S.disabled || !cv) ? kInvalidNm
                                        : __double2int_rd(S.nmf[c] * ldexp(1.0, 19 - 2 * S.em)) + ssum;
@@ -333,7 +361,9 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
   if (tid == 0) {
     // W = 10 + ceil(4e), e = ((d*2^22 + max_c sum|M|)/2 + d/4) / 2^24  (+1 margin covers 2^-40 terms)
     const long long num = (static_cast<long long>(d) << 22) + S.yabs;
-    S.window = 10 + static_cast<int>((2 * num + d + (1ll << 24) - 1) >> 24);
+    S.window4 = 10 + static_cast<int>((2 * num + d + (1ll << 24) - 1) >> 24);
+    // W3 = W + 2 ceil(beta_max), beta_c = 255 sum_j (l'_cj + G_cj) / 2^16 (W2 not accumulated)
+    S.window = S.window4 + (kAcc == 3 ? 2 * static_cast<int>((255ll * S.bsum_max + 65535) >> 16) : 0);
   }
   fence_proxy_async_smem();
   if (warp == kWarpMma) tmem_alloc<kTmemCols>(&S.tmem_base);
@@ -371,11 +401,17 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
           const uint64_t m0 = sw64_kmajor_desc(bm + 32 * kk);              // rows h'', l', G
           const uint64_t m1 = sw64_kmajor_desc(bm + 64 * 64 + 32 * kk);    // rows l', G
           const uint32_t acc = kk > 0;
-          // TMEM columns: HH 0-63, CR 64-127, W1 128-191, W2 192-255
+          // TMEM columns: HH 0-63, CR 64-127, W1 128-191 (, W2 192-255)
           mma_i8(tmem + 0, xh, m0, ID_64, acc);      // HH  = h'' h''
-          mma_i8(tmem + 64, xl, m0, ID_192, acc);    // CR += l h'',  W1 += l l',  W2 += l G
-          mma_i8(tmem + 64, xh, m1, ID_128, 1);      // CR += h'' l', W1 += h'' G
-          mma_i8(tmem + 128, xf, m0, ID_128, 1);     // W1 += F h'',  W2 += F l'
+          if constexpr (kAcc == 4) {
+            mma_i8(tmem + 64, xl, m0, ID_192, acc);  // CR += l h'',  W1 += l l',  W2 += l G
+            mma_i8(tmem + 64, xh, m1, ID_128, 1);    // CR += h'' l', W1 += h'' G
+            mma_i8(tmem + 128, xf, m0, ID_128, 1);   // W1 += F h'',  W2 += F l'
+          } else {
+            mma_i8(tmem + 64, xl, m0, ID_128, acc);  // CR += l h'',  W1 += l l'
+            mma_i8(tmem + 64, xh, m1, ID_128, 1);    // CR += h'' l', W1 += h'' G
+            mma_i8(tmem + 128, xf, m0, ID_64, 1);    // W1 += F h''
+          }
         }
         mma_commit(&S.t_full);
         TRACE_EV(ns, 0);
@@ -611,7 +647,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     const unsigned long long kmask = k == 64 ? ~0ull : ((1ull << k) - 1);
     const unsigned long long vmask = S.valid;   // finite centroids (the others never survive)
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-    const int window = S.window;
+    const int window = S.window, window4 = S.window4;
     const int4* nm4 = reinterpret_cast<const int4*>(S.nm0);
     const uint32_t oh_row = (static_cast<uint32_t>(q) >> 3) * 512u + (q & 7) * 64u;
     const uint32_t oh_sw = (q & 7) >> 1;
@@ -633,14 +669,14 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
         tmem_ld8(tmem + lane_base + col, hh);
         tmem_ld8(tmem + lane_base + col + 64, cr);
         tmem_ld8(tmem + lane_base + col + 128, w1);
-        tmem_ld8(tmem + lane_base + col + 192, w2);
+        if constexpr (kAcc == 4) tmem_ld8(tmem + lane_base + col + 192, w2);
         const int4 n0 = nm4[2 * ch], n1 = nm4[2 * ch + 1];
         const int nm[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
         tmem_ld_wait();
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           // invalid centroids: zero B rows (Q = 0) and nm = kInvalidNm
-          const int Q = hh[u] * 256 + cr[u] + (w1[u] >> 8) + (w2[u] >> 16);
+          const int Q = hh[u] * 256 + cr[u] + (w1[u] >> 8) + (kAcc == 4 ? (w2[u] >> 16) : 0);
           const int v = nm[u] - 2 * Q;
           tv[8 * ch + u] = v;
           lmin = min(lmin, v);
@@ -673,6 +709,46 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
 #pragma unroll
           for (int u = 32; u < 64; ++u) nhi = __funnelshift_l(static_cast<unsigned>(tv[u] - thr1), nhi, 1);
           full = ((static_cast<unsigned long long>(__brev(nhi)) << 32) | __brev(nlo)) & vmask;
+          if (kAcc == 3 && kRefine && (full & (full - 1)) != 0 && flag == 0) {
+            // refine the W3-survivors with their exact W2 (rare: ~0.2 % of the rows)
+            const unsigned char* Ab = smem + kOffA + b3 * kABuf;
+            uint4 lq[4], fq[4];   // the row's b6 (l) and b5 (F) planes, 16 columns per chunk
+#pragma unroll
+            for (int c16 = 0; c16 < 4; ++c16) {
+              lq[c16] = *reinterpret_cast<const uint4*>(Ab + sw128_offset(q, 64 + 16 * c16));
+              fq[c16] = *reinterpret_cast<const uint4*>(Ab + kPlane2 + sw128_offset(q, 16 * c16));
+            }
+            int tl[kMaxK];
+#pragma unroll
+            for (int u = 0; u < kMaxK; ++u) tl[u] = tv[u];
+            int t4min = INT_MAX;
+            for (unsigned long long f = full; f; f &= f - 1) {
+              const int c = __ffsll(static_cast<long long>(f)) - 1;
+              unsigned w2 = 0;
+#pragma unroll
+              for (int c16 = 0; c16 < 4; ++c16) {
+                const uint4 G = *reinterpret_cast<const uint4*>(Bm + sw64_offset(128 + c, 16 * c16));
+                const uint4 L = *reinterpret_cast<const uint4*>(Bm + sw64_offset(64 + c, 16 * c16));
+                w2 = __dp4a(lq[c16].x, G.x, w2);
+                w2 = __dp4a(lq[c16].y, G.y, w2);
+                w2 = __dp4a(lq[c16].z, G.z, w2);
+                w2 = __dp4a(lq[c16].w, G.w, w2);
+                w2 = __dp4a(fq[c16].x, L.x, w2);
+                w2 = __dp4a(fq[c16].y, L.y, w2);
+                w2 = __dp4a(fq[c16].z, L.z, w2);
+                w2 = __dp4a(fq[c16].w, L.w, w2);
+              }
+              const int t4 = tl[c] - 2 * static_cast<int>(w2 >> 16);   // the 4-accumulator score
+              tl[c] = t4;
+              t4min = min(t4min, t4);
+            }
+            unsigned long long g = 0;
+            for (unsigned long long f = full; f; f &= f - 1) {
+              const int c = __ffsll(static_cast<long long>(f)) - 1;
+              if (tl[c] <= t4min + window4) g |= 1ull << c;
+            }
+            full = g;
+          }
           if ((full & (full - 1)) == 0) {
             a = __ffsll(static_cast<long long>(full)) - 1;
           } else {
