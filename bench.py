@@ -34,6 +34,10 @@ CONFIGS = {
                  "k-means iters/sec (N=2M shard of C4 at 8 GPUs, d=64, k=64)", "it/s"),
     "c2": ("logreg", dict(n=1_048_576, d=64), "logistic-regression BGD iters/sec (N=1M,d=64)", "it/s"),
     "l16": ("logreg", dict(n=16_777_216, d=64), "logistic-regression BGD iters/sec (N=16M,d=64)", "it/s"),
+    # the fp32-storage opt-in (x rounded to float, fp64 arithmetic): an extension,
+    # the reference has no fp32 type
+    "l16f32": ("logreg", dict(n=16_777_216, d=64, storage="f32"),
+               "logistic-regression BGD iters/sec (N=16M,d=64, fp32 storage of x)", "it/s"),
     "c3": ("gda", dict(n=1_048_576, d=64), "GDA fits/sec (N=1M,d=64)", "fits/s"),
     "c5": ("groupby", dict(n=1_000_000_000, K=64), "GroupBy bucket-count passes/sec (1e9 keys, K=64)", "passes/s"),
     # SURVEY §8 a7 leaves K open and proposes a sweep: 4,096 and 65,536 buckets
@@ -58,7 +62,7 @@ def algorithmic_bytes(family, p, n_local):
     if family == "kmeans":
         return n_local * (p["d"] * 8 + 4)
     if family == "logreg":
-        return n_local * (p["d"] * 8 + 8)
+        return n_local * (p["d"] * (4 if p.get("storage") == "f32" else 8) + 8)
     if family == "gda":
         return n_local * (p["d"] * 8 + 8)  # per pass (dominant kernel = one pass)
     if family == "groupby":
@@ -321,6 +325,8 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             rest()
     elif family == "logreg":
         x = ml.rng_units(n_local * d, seed=1, first_draw=lo * d, device=dev).view(n_local, d)
+        if p.get("storage") == "f32":
+            x = x.float()   # the fp32-storage opt-in: rounded once, promoted exactly in the kernel
         y = ml.rng_ints(n_local, 2, seed=1, first_draw=n * d + lo, device=dev)
         prog = LogRegProgram(x, y, torch.zeros(d, dtype=torch.float64, device=dev), 1.0 / n, comm=comm)
         kernel_fn = lambda: ml.logreg_grad(x, y, prog.theta, prog.grad)  # noqa: E731
@@ -679,6 +685,8 @@ def e2e_logreg(args, p, n_local, lo, comm, dist, dev, iters_per_job=20):
     from paper_1109_0778_b200.programs import LogRegProgram
     d, n = p["d"], p["n"]
     x0 = ml.rng_units(n_local * d, seed=1, first_draw=lo * d, device=dev).view(n_local, d)
+    if p.get("storage") == "f32":
+        x0 = x0.float()
     y0 = ml.rng_ints(n_local, 2, seed=1, first_draw=n * d + lo, device=dev)
     x_host = torch.empty_like(x0, device="cpu").pin_memory()
     y_host = torch.empty_like(y0, device="cpu").pin_memory()
@@ -714,7 +722,7 @@ def e2e_logreg(args, p, n_local, lo, comm, dist, dev, iters_per_job=20):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t[0])
     return {"value": jobs * iters_per_job / (ms * 1e-3), "unit": "it/s",
-            "h2d_bytes_per_step": n_local * (d * 8 + 8), "d2h_bytes_per_step": d * 8,
+            "h2d_bytes_per_step": n_local * (d * x0.element_size() + 8), "d2h_bytes_per_step": d * 8,
             "step": f"one job = H2D x,y shard (pinned) + {iters_per_job} BGD iterations + D2H theta; "
                     f"{jobs} jobs, double-buffered (H2D of job j+1 overlaps job j)",
             "iters_per_step": iters_per_job}

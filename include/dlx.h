@@ -115,6 +115,13 @@ size_t dlx_logreg_workspace_bytes(int64_t n, int32_t d);
 int dlx_logreg_grad(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
                     const double* d_theta, double* d_grad, void* d_workspace,
                     size_t workspace_bytes, dlx_stream_t stream);
+/* fp32 storage opt-in (the reference Ty has no fp32, types.hpp:11-20): x held
+ * as float (half the bytes of the HBM-bound stream), every element promoted exactly to double,
+ * the arithmetic that of dlx_logreg_grad — so the gradient is bit-identical to dlx_logreg_grad
+ * on the promoted matrix.  Same workspace as dlx_logreg_grad. */
+int dlx_logreg_grad_f32(const float* d_x, const int64_t* d_y, int64_t n, int32_t d,
+                        const double* d_theta, double* d_grad, void* d_workspace,
+                        size_t workspace_bytes, dlx_stream_t stream);
 /* The staged logistic-regression loop (the collect form the reference fuses into
  * one loop): h(i) = link(theta . x_i) (a collect, stored to d_h unless NULL) and
  * grad_j = sum_i (h(i) - y_i) * x_ij.  The link is the loop body's own scalar expression of the

@@ -76,6 +76,7 @@ _SIGS = {
     "dlx_groupby_count": (_int, [_vp, _i64, _i64, _vp, _vp, _sz, _vp]),
     "dlx_logreg_workspace_bytes": (_sz, [_i64, _i32]),
     "dlx_logreg_grad": (_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _sz, _vp]),
+    "dlx_logreg_grad_f32": (_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _sz, _vp]),
     "dlx_axpy_inplace": (_int, [_vp, _vp, _dbl, _i64, _vp]),
     "dlx_rowdot_link_grad": (_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "dlx_link_kind": (_int, [_vp]),

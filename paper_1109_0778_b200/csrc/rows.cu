@@ -57,6 +57,45 @@ __device__ void cta_reduce_columns(double (&acc)[M][2], int d, double* red_s, do
 
 // 8 rows in flight per warp: lane l holds columns {2l, 2l+1} + 64m of rows r0..r0+7.
 constexpr int kRows = 8;
+#ifndef DLX_F32_GROUPS
+#define DLX_F32_GROUPS 2   // fp32 storage, d <= 64: blocks of 8 rows in flight per warp step
+#endif
+
+// fp32 storage (the opt-in mode): two floats per lane, kept packed in registers
+// (so a warp keeps twice the rows in flight for the same registers) and promoted exactly to fp64
+// at use
+__device__ __forceinline__ float2 ld_stream_f32x2(const float* p) {
+  float2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p));
+  return r;
+}
+template <int M>
+__device__ __forceinline__ void load_rows(const float* __restrict__ x, int64_t i0, int64_t n, int d,
+                                          int lane, float2 (&v)[kRows][M]) {
+#pragma unroll
+  for (int r = 0; r < kRows; ++r) {
+    const int64_t i = i0 + r;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const int j = 64 * m + 2 * lane;
+      v[r][m] = (i < n && j < d) ? ld_stream_f32x2(x + i * d + j) : make_float2(0.f, 0.f);
+    }
+  }
+}
+__device__ __forceinline__ double2 to_d2(double2 v) { return v; }
+// float -> double, exact: for normal floats the double's words are built with integer ops
+// (exponent rebias +896, mantissa << 29) instead of F2F.F64.F32, whose throughput bounded the
+// fp32 kernel; zero, subnormal, inf and NaN take the conversion instruction
+__device__ __forceinline__ double f2d_exact(float f) {
+  const uint32_t u = __float_as_uint(f), em = u & 0x7fffffffu;
+  if (em - 0x00800000u < 0x7f000000u)   // 0 < exponent < 255
+    return __hiloint2double(static_cast<int>((u & 0x80000000u) | ((em >> 3) + 0x38000000u)), static_cast<int>(em << 29));
+  return static_cast<double>(f);
+}
+__device__ __forceinline__ double2 to_d2(float2 v) { return make_double2(f2d_exact(v.x), f2d_exact(v.y)); }
+template <class T> struct Vec2;
+template <> struct Vec2<double> { using type = double2; };
+template <> struct Vec2<float> { using type = float2; };
 
 template <int M>
 __device__ __forceinline__ void load_rows(const double* __restrict__ x, int64_t i0, int64_t n, int d,
@@ -170,9 +209,9 @@ struct CodeLink {
   }
 };
 
-template <int M, class Link, bool WRITE_H>
+template <int M, class Link, bool WRITE_H, class T = double>   // T: fp64 or fp32 storage of x
 __global__ void __launch_bounds__(kRowThreads, DLX_ROW_MINB)
-logreg_grad_kernel(const double* __restrict__ x, const long long* __restrict__ y, int64_t n,
+logreg_grad_kernel(const T* __restrict__ x, const long long* __restrict__ y, int64_t n,
                    int d, const double* __restrict__ theta, Link link, double* __restrict__ h_out,
                    double* __restrict__ parts) {
   pdl_wait();   // programmatic dependent launch: inputs are final from here on
@@ -187,34 +226,49 @@ logreg_grad_kernel(const double* __restrict__ x, const long long* __restrict__ y
     th[m][1] = j + 1 < d ? theta[j + 1] : 0.0;
     acc[m][0] = acc[m][1] = 0.0;
   }
+  // G blocks of 8 rows per warp step: fp32 storage keeps 16 rows (packed) in flight, the same
+  // registers and bytes in flight as 8 fp64 rows (d <= 64; wider rows keep 8).  A warp's blocks
+  // are w, w + W, w + 2W, ... either way, so the accumulation order (and every bit of the
+  // result) is that of the fp64 kernel on the promoted matrix.
+  constexpr int G = (sizeof(T) == 4 && M == 1) ? DLX_F32_GROUPS : 1;
   const int64_t nblk = (n + kRows - 1) / kRows;
   const int64_t W = static_cast<int64_t>(gridDim.x) * kRowWarps;
   const int my_row = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-  for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kRowWarps + warp; blk < nblk; blk += W) {
-    const int64_t i0 = blk * kRows;
-    double2 v[kRows][M];
-    load_rows<M>(x, i0, n, d, lane, v);
-    const int64_t iy = i0 + my_row;
-    const double yv = iy < n ? static_cast<double>(__ldg(y + iy)) : 0.0;
-    double p[kRows];
+  for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kRowWarps + warp; blk < nblk; blk += G * W) {
+    typename Vec2<T>::type v[G][kRows][M];
 #pragma unroll
-    for (int r = 0; r < kRows; ++r) {
-      double a = 0.0;
+    for (int g = 0; g < G; ++g) load_rows<M>(x, (blk + g * W) * kRows, n, d, lane, v[g]);
 #pragma unroll
-      for (int m = 0; m < M; ++m) a = fma(th[m][0], v[r][m].x, fma(th[m][1], v[r][m].y, a));
-      p[r] = a;
-    }
-    const double z = reduce_scatter8(p, lane);
-    const double h = iy < n ? link(z) : 0.0;
-    if (WRITE_H && (lane & 3) == 0 && iy < n) h_out[iy] = h;
-    const double res = iy < n ? h - yv : 0.0;
+    for (int g = 0; g < G; ++g) {
+      if (g > 0 && blk + g * W >= nblk) break;   // warp-uniform
+      const int64_t i0 = (blk + g * W) * kRows;
+      const int64_t iy = i0 + my_row;
+      const double yv = iy < n ? static_cast<double>(__ldg(y + iy)) : 0.0;
+      double2 e[kRows][M];   // promoted once (fp32 storage), used by the dot and the gradient
 #pragma unroll
-    for (int r = 0; r < kRows; ++r) {
-      const double rr = __shfl_sync(0xffffffffu, res, lane_of_row(r));
+      for (int r = 0; r < kRows; ++r)
 #pragma unroll
-      for (int m = 0; m < M; ++m) {
-        acc[m][0] = fma(rr, v[r][m].x, acc[m][0]);
-        acc[m][1] = fma(rr, v[r][m].y, acc[m][1]);
+        for (int m = 0; m < M; ++m) e[r][m] = to_d2(v[g][r][m]);
+      double p[kRows];
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) {
+        double a = 0.0;
+#pragma unroll
+        for (int m = 0; m < M; ++m) a = fma(th[m][0], e[r][m].x, fma(th[m][1], e[r][m].y, a));
+        p[r] = a;
+      }
+      const double z = reduce_scatter8(p, lane);
+      const double h = iy < n ? link(z) : 0.0;
+      if (WRITE_H && (lane & 3) == 0 && iy < n) h_out[iy] = h;
+      const double res = iy < n ? h - yv : 0.0;
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) {
+        const double rr = __shfl_sync(0xffffffffu, res, lane_of_row(r));
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          acc[m][0] = fma(rr, e[r][m].x, acc[m][0]);
+          acc[m][1] = fma(rr, e[r][m].y, acc[m][1]);
+        }
       }
     }
   }
@@ -416,9 +470,11 @@ size_t dlx_logreg_workspace_bytes(int64_t n, int32_t d) {
   return static_cast<size_t>(row_grid(n)) * d * sizeof(double) + 256;
 }
 
-int dlx_logreg_grad(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
-                    const double* d_theta, double* d_grad, void* d_workspace,
-                    size_t workspace_bytes, dlx_stream_t stream) {
+}  // extern "C"
+
+template <class T>
+static int logreg_grad_impl(const T* d_x, const int64_t* d_y, int64_t n, int32_t d, const double* d_theta,
+                            double* d_grad, void* d_workspace, size_t workspace_bytes, dlx_stream_t stream) {
   DLX_REQUIRE(n >= 0 && d > 0, DLX_ERR_ARG, "logreg: bad shape");
   DLX_REQUIRE(d % 2 == 0 && m_for(d) <= kMaxM, DLX_ERR_GENERATION,
               "GenerationFailed: logreg needs even d <= %d (got %d)", 64 * kMaxM, d);
@@ -430,13 +486,27 @@ int dlx_logreg_grad(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
   const long long* y = reinterpret_cast<const long long*>(d_y);
   const SigmoidLink sig;
   switch (m_for(d)) {
-    case 1: DLX_CUDA(launch_pdl(logreg_grad_kernel<1, SigmoidLink, false>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, sig, nullptr, parts)); break;
-    case 2: DLX_CUDA(launch_pdl(logreg_grad_kernel<2, SigmoidLink, false>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, sig, nullptr, parts)); break;
-    case 3: DLX_CUDA(launch_pdl(logreg_grad_kernel<3, SigmoidLink, false>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, sig, nullptr, parts)); break;
-    default: DLX_CUDA(launch_pdl(logreg_grad_kernel<4, SigmoidLink, false>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, sig, nullptr, parts)); break;
+    case 1: DLX_CUDA(launch_pdl(logreg_grad_kernel<1, SigmoidLink, false, T>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, sig, nullptr, parts)); break;
+    case 2: DLX_CUDA(launch_pdl(logreg_grad_kernel<2, SigmoidLink, false, T>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, sig, nullptr, parts)); break;
+    case 3: DLX_CUDA(launch_pdl(logreg_grad_kernel<3, SigmoidLink, false, T>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, sig, nullptr, parts)); break;
+    default: DLX_CUDA(launch_pdl(logreg_grad_kernel<4, SigmoidLink, false, T>, dim3(grid), dim3(kRowThreads), smem, stream, d_x, y, n, d, d_theta, sig, nullptr, parts)); break;
   }
   DLX_LAUNCHED("logreg_grad_kernel");
   return combine_f64(parts, grid, d, d_grad, stream);
+}
+
+extern "C" {
+
+int dlx_logreg_grad(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
+                    const double* d_theta, double* d_grad, void* d_workspace,
+                    size_t workspace_bytes, dlx_stream_t stream) {
+  return logreg_grad_impl(d_x, d_y, n, d, d_theta, d_grad, d_workspace, workspace_bytes, stream);
+}
+
+int dlx_logreg_grad_f32(const float* d_x, const int64_t* d_y, int64_t n, int32_t d,
+                        const double* d_theta, double* d_grad, void* d_workspace,
+                        size_t workspace_bytes, dlx_stream_t stream) {
+  return logreg_grad_impl(d_x, d_y, n, d, d_theta, d_grad, d_workspace, workspace_bytes, stream);
 }
 
 int dlx_link_kind(const dlx_link_code* h_link) { return h_link ? static_cast<int>(link_kind(*h_link)) : -1; }

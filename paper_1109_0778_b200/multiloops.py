@@ -195,7 +195,9 @@ def logreg_grad(x: torch.Tensor, y: torch.Tensor, theta: torch.Tensor, out=None)
     n, d = x.shape
     out = out if out is not None else torch.empty(d, dtype=_F64, device=x.device)
     ws, wsb = _WS.get(L.dlx_logreg_workspace_bytes(n, d), x.device)
-    check(L.dlx_logreg_grad(_ptr(x), _ptr(y), n, d, _ptr(theta), _ptr(out), ws, wsb, _stream()))
+    # float32 x: the fp32-storage opt-in (exact promotion, fp64 arithmetic, rows.cu)
+    fn = L.dlx_logreg_grad_f32 if x.dtype == torch.float32 else L.dlx_logreg_grad
+    check(fn(_ptr(x), _ptr(y), n, d, _ptr(theta), _ptr(out), ws, wsb, _stream()))
     return out
 
 

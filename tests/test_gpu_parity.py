@@ -302,6 +302,41 @@ def test_logreg_grad(ml, n, d):
     np.testing.assert_allclose(g, ref, rtol=RTOL, atol=1e-9 * np.abs(ref).max())
 
 
+@pytest.mark.parametrize("n,d", [(1, 64), (1000, 64), (1_048_576, 64), (3001, 2), (5000, 130), (4096, 256)])
+def test_logreg_grad_f32_storage(ml, n, d):
+    """The fp32-storage opt-in (dlx_logreg_grad_f32): x held as float, promoted exactly; the
+    gradient is bit-identical to the fp64 kernel on the promoted matrix and matches the oracle
+    on it (rtol 1e-9)."""
+    x32 = dev_units(ml, n, d, seed=5).float()
+    xp = x32.double()
+    y = ml.rng_ints(n, 2, seed=5, first_draw=n * d)
+    th = torch.linspace(-0.3, 0.3, d, dtype=torch.float64, device="cuda")
+    g32 = ml.logreg_grad(x32, y, th)
+    g64 = ml.logreg_grad(xp, y, th)
+    assert torch.equal(g32, g64)
+    ref = O.logreg_grad(xp.cpu().numpy(), y.cpu().numpy(), th.cpu().numpy(), workers=O.threads(), chunks=4 * O.threads())
+    np.testing.assert_allclose(g32.cpu().numpy(), ref, rtol=RTOL, atol=1e-9 * np.abs(ref).max())
+    # against the reference on the ORIGINAL fp64 inputs: north_star's fp32 tolerance, 1e-5
+    x64 = dev_units(ml, n, d, seed=5)
+    ref64 = O.logreg_grad(x64.cpu().numpy(), y.cpu().numpy(), th.cpu().numpy(), workers=O.threads(), chunks=4 * O.threads())
+    np.testing.assert_allclose(g32.cpu().numpy(), ref64, rtol=1e-5, atol=1e-5 * np.abs(ref64).max())
+
+
+def test_logreg_bgd_f32_storage_program(ml):
+    """BGD through LogRegProgram (CUDA-graph iterations) on fp32-stored x equals the fp64 program
+    on the promoted matrix bit for bit."""
+    from paper_1109_0778_b200.programs import LogRegProgram
+    n, d, iters = 1_048_576, 64, 5
+    x32 = dev_units(ml, n, d).float()
+    y = ml.rng_ints(n, 2, seed=1, first_draw=n * d)
+    a = LogRegProgram(x32, y, torch.zeros(d, dtype=torch.float64, device="cuda"), 1.0 / n).capture()
+    b = LogRegProgram(x32.double(), y, torch.zeros(d, dtype=torch.float64, device="cuda"), 1.0 / n).capture()
+    for _ in range(iters):
+        a.step()
+        b.step()
+    assert torch.equal(a.theta, b.theta)
+
+
 def test_c2_logreg_bgd_20_iterations(ml):
     from paper_1109_0778_b200.programs import LogRegProgram
     n, d, iters = 1_048_576, 64, 20
