@@ -60,6 +60,72 @@ combine_pair_kernel(const double* __restrict__ pf, long long wf, double* __restr
   else combine_columns<long long, long long>(pi, nparts, wi, oi, blockIdx.x - bf);
 }
 
+// The single-pass GDA fit's combine and finalize in one launch (gda_dmma.cu): the first blocks
+// fold the CTAs' S' records, the next the shifted class sums, one block the class-1 counts —
+// each as combine_columns does — and the last block to finish (a completion counter that the
+// fit kernel zeroed and this block resets, so graph replays start from zero) computes
+// mu_c = shift_c + sd_c / n_c, S = S' - sum_c sd_c sd_c^T / n_c and the certification flag
+// (every diagonal correction <= 0.99 of S'_jj; also false for NaN / inf): the arithmetic of
+// the former separate finalize kernel, with its inputs read from L2 (written by other blocks).
+// (Folding the class sums redundantly in every block so each finalizes its own S columns
+// measured slower: 18 vs 12 us, r315.)
+__global__ void __launch_bounds__(kCombWarps * 32)
+gda_fit_combine_kernel(const double* __restrict__ parts, const double* __restrict__ parts_sd,
+                       const long long* __restrict__ parts_n1, int nparts, int d, double* __restrict__ Sp,
+                       double* __restrict__ sd, long long* __restrict__ n1p, int64_t n,
+                       const double* __restrict__ shift, unsigned* __restrict__ counter,
+                       long long* __restrict__ n1_out, double* __restrict__ mu0, double* __restrict__ mu1,
+                       double* __restrict__ S, int* __restrict__ ok) {
+  pdl_wait();
+  pdl_trigger();
+  const long long wS = static_cast<long long>(d) * d, bS = (wS + 31) / 32, bsd = (2LL * d + 31) / 32;
+  if (blockIdx.x < bS) combine_columns<double, double>(parts, nparts, wS, Sp, blockIdx.x);
+  else if (blockIdx.x < bS + bsd) combine_columns<double, double>(parts_sd, nparts, 2LL * d, sd, blockIdx.x - bS);
+  else combine_columns<long long, long long>(parts_n1, nparts, 1, n1p, 0);
+  __shared__ int last, bad;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    bad = 0;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const long long n1 = __ldcg(n1p), n0 = n - n1;
+  const double dn0 = static_cast<double>(n0), dn1 = static_cast<double>(n1);
+  auto corr = [&](int a, int b) {
+    double c = 0.0;
+    if (n0 > 0) c += __ldcg(sd + a) * __ldcg(sd + b) / dn0;
+    if (n1 > 0) c += __ldcg(sd + d + a) * __ldcg(sd + d + b) / dn1;
+    return c;
+  };
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    mu0[j] = __ldcg(shift + j) + __ldcg(sd + j) / dn0;        // an empty class: 0 / 0 -> NaN, as the reference
+    mu1[j] = __ldcg(shift + 64 + j) + __ldcg(sd + d + j) / dn1;
+    const double cj = corr(j, j), sj = __ldcg(Sp + j * d + j);
+    if (!(cj <= 0.99 * sj)) bad = 1;
+  }
+  for (long long e = threadIdx.x; e < wS; e += blockDim.x)
+    S[e] = __ldcg(Sp + e) - corr(static_cast<int>(e / d), static_cast<int>(e % d));
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *ok = !bad;
+    *n1_out = n1;
+    *counter = 0u;
+  }
+}
+
+int gda_fit_combine(const double* parts, const double* parts_sd, const long long* parts_n1, int nparts, int d,
+                    double* Sp, double* sd, long long* n1p, int64_t n, const double* shift, unsigned* counter,
+                    long long* n1_out, double* mu0, double* mu1, double* S, int* ok, cudaStream_t s) {
+  const long long blocks = (static_cast<long long>(d) * d + 31) / 32 + (2LL * d + 31) / 32 + 1;
+  DLX_CUDA(launch_pdl(gda_fit_combine_kernel, dim3(static_cast<unsigned>(blocks)), dim3(kCombWarps * 32), 0, s,
+                      parts, parts_sd, parts_n1, nparts, d, Sp, sd, n1p, n, shift, counter, n1_out, mu0, mu1, S, ok));
+  DLX_LAUNCHED("gda_fit_combine_kernel");
+  return DLX_OK;
+}
+
 template <class Tin, class Tout>
 static int launch_combine(const Tin* parts, int nparts, long long width, Tout* out,
                           cudaStream_t stream, const int* skip = nullptr) {

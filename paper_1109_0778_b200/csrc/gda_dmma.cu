@@ -175,6 +175,7 @@ gda_pass2_dmma_kernel(const double* __restrict__ x, const long long* __restrict_
       if (ct < 128) {
         mu_s[c * 64 + j] = j < d ? sh : 0.0;
         if (blockIdx.x == 0) shift_out[c * 64 + j] = j < d ? sh : 0.0;
+        if (blockIdx.x == 0 && ct == 0) reinterpret_cast<unsigned*>(shift_out + 128)[0] = 0u;   // combine counter
       }
       named_bar(1, kGdCtrThreads);
     }
@@ -519,6 +520,7 @@ gda_fit64_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant_
     if (tid < 128) {
       mu_s[c * kG64Mu1 + j] = sh;
       if (blockIdx.x == 0) shift_out[c * 64 + j] = sh;
+      if (blockIdx.x == 0 && tid == 0) reinterpret_cast<unsigned*>(shift_out + 128)[0] = 0u;   // combine counter
     }
     named_bar(1, kG64MmaWarps * 32);
   }
@@ -706,42 +708,10 @@ int gda_pass2_dmma(const double* x, const long long* y, int64_t n, int d, const 
   return combine_f64(parts, grid, static_cast<long long>(d) * d, out, stream);
 }
 
-// Single-pass fit, last step: mu_c = c_c + sd_c / n_c and S = S' - sum_c sd_c sd_c^T / n_c.
-// Certified: the rank-1 corrections may cancel at most 99 % of any diagonal entry of S'
-// (relative rounding amplification <= 100); otherwise *ok = 0 and the caller's pass 2 on the
-// exact means runs (gda_pass2_dmma_kernel<false> / combine gated on *ok).
-__global__ void __launch_bounds__(1024)
-gda_fit_finalize_kernel(const double* __restrict__ Sp, const double* __restrict__ sd,
-                        const long long* __restrict__ n1p, int64_t n, int d,
-                        const double* __restrict__ shift, long long* __restrict__ n1_out,
-                        double* __restrict__ mu0, double* __restrict__ mu1, double* __restrict__ S,
-                        int* __restrict__ ok) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ int bad;
-  const long long n1 = *n1p, n0 = n - n1;
-  const double dn0 = static_cast<double>(n0), dn1 = static_cast<double>(n1);
-  if (threadIdx.x == 0) bad = 0;
-  __syncthreads();
-  auto corr = [&](int a, int b) {
-    double c = 0.0;
-    if (n0 > 0) c += sd[a] * sd[b] / dn0;
-    if (n1 > 0) c += sd[d + a] * sd[d + b] / dn1;
-    return c;
-  };
-  for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    mu0[j] = shift[j] + sd[j] / dn0;            // an empty class: 0 / 0 -> NaN, as the reference
-    mu1[j] = shift[64 + j] + sd[d + j] / dn1;
-    const double cj = corr(j, j), sj = Sp[j * d + j];
-    if (!(cj <= 0.99 * sj)) bad = 1;            // also catches NaN / inf
-  }
-  for (int e = threadIdx.x; e < d * d; e += blockDim.x) S[e] = Sp[e] - corr(e / d, e % d);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    *ok = !bad;
-    *n1_out = n1;
-  }
-}
+// Single-pass fit, last step (gda_fit_combine, combine.cu): mu_c = c_c + sd_c / n_c and
+// S = S' - sum_c sd_c sd_c^T / n_c.  Certified: the rank-1 corrections may cancel at most 99 % of
+// any diagonal entry of S' (relative rounding amplification <= 100); otherwise *ok = 0 and the
+// caller's pass 2 on the exact means runs (gda_pass2_dmma_kernel<false> / combine gated on *ok).
 
 size_t gda_fit_workspace_bytes(int64_t n, int d) {
   const int grid = gda_pass2_dmma_grid(n);
@@ -752,10 +722,14 @@ size_t gda_fit_workspace_bytes(int64_t n, int d) {
   c.take<double>(static_cast<size_t>(d) * d);
   c.take<double>(2 * static_cast<size_t>(d));
   c.take<long long>(1);
-  c.take<double>(128);
+  c.take<double>(129);
   c.take<int>(1);
   return c.used + 256;
 }
+
+int gda_fit_combine(const double* parts, const double* parts_sd, const long long* parts_n1, int nparts, int d,
+                    double* Sp, double* sd, long long* n1p, int64_t n, const double* shift, unsigned* counter,
+                    long long* n1_out, double* mu0, double* mu1, double* S, int* ok, cudaStream_t s);
 
 int gda_fit(const double* x, const long long* y, int64_t n, int d, long long* n1_out, double* mu0,
             double* mu1, double* S, void* ws, size_t ws_bytes, cudaStream_t stream) {
@@ -769,7 +743,7 @@ int gda_fit(const double* x, const long long* y, int64_t n, int d, long long* n1
   double* Sp = c.take<double>(static_cast<size_t>(d) * d);
   double* sd = c.take<double>(2 * static_cast<size_t>(d));
   long long* n1 = c.take<long long>(1);
-  double* shift = c.take<double>(128);
+  double* shift = c.take<double>(129);   // + the combine's completion counter
   int* ok = c.take<int>(1);
   DLX_REQUIRE(ws && c.used <= ws_bytes, DLX_ERR_ARG, "gda fit: workspace too small");
   const bool k64 = gda_fit64_ok(x, y, d) && n > 0 && !std::getenv("DLX_GDA_ROWBLOCKS");
@@ -794,13 +768,11 @@ int gda_fit(const double* x, const long long* y, int64_t n, int d, long long* n1
                         static_cast<const int*>(nullptr), parts_sd, parts_n1, shift));
     DLX_LAUNCHED("gda_pass2_dmma_kernel");
   }
-  int rc = combine_f64(parts, grid, static_cast<long long>(d) * d, Sp, stream);
-  if (rc == DLX_OK) rc = combine_f64_i64(parts_sd, 2LL * d, sd, parts_n1, 1, n1, grid, stream);
-  if (rc != DLX_OK) return rc;
-  DLX_CUDA(launch_pdl(gda_fit_finalize_kernel, dim3(1), dim3(1024), 0, stream, static_cast<const double*>(Sp),
-                      static_cast<const double*>(sd), static_cast<const long long*>(n1), n, d,
-                      static_cast<const double*>(shift), n1_out, mu0, mu1, S, ok));
-  DLX_LAUNCHED("gda_fit_finalize_kernel");
+  // combine + finalize in one launch (combine.cu); shift[128] is its completion counter, zeroed
+  // by the fit kernel's block 0
+  if (int rc = gda_fit_combine(parts, parts_sd, parts_n1, grid, d, Sp, sd, n1, n, shift,
+                               reinterpret_cast<unsigned*>(shift + 128), n1_out, mu0, mu1, S, ok, stream))
+    return rc;
   // fallback, decided on the device: pass 2 on the exact means when the shift was too far off
   if (k64) {
     DLX_CUDA(launch_pdl(gda_fit64_kernel<false>, dim3(grid), dim3(kG64Threads), kG64Smem, stream, tmx, tmy, x, y, n,
@@ -901,7 +873,7 @@ int dlx_gda_fit_last_fallback(const void* d_workspace, int64_t n, int32_t d, int
   c.take<double>(static_cast<size_t>(d) * d);
   c.take<double>(2 * static_cast<size_t>(d));
   c.take<long long>(1);
-  c.take<double>(128);
+  c.take<double>(129);
   int* ok = c.take<int>(1);
   int h = 0;
   DLX_CUDA(cudaMemcpy(&h, ok, sizeof(int), cudaMemcpyDeviceToHost));
