@@ -215,6 +215,26 @@ void find_count(Stage& st, int64_t n) {
   st.print(hits.sum());
 }
 
+// Fusion-legality probes (the executor's fusion pass must refuse these pairs, as the
+// reference's fuse_loops does): a sum over a mutable vector, an update of it, and the same sum
+// again (the second loop reads a vector written between the two); a sum, a map that subtracts
+// it (reads the first loop's reduce result) and the map's sum; a map over x and a sum over a
+// vector of another length (different ranges).
+void fusion_blockers(Stage& st, int64_t n) {
+  DVec m = vec_alloc(st, st.lit(int64_t{8}), SemType::f64());
+  for (int e = 0; e < 8; ++e) m.update(st.lit(int64_t{e}), st.lit(0.5 * e));
+  st.print(m.sum());
+  m.update(st.lit(int64_t{3}), st.lit(100.0));
+  st.print(m.sum());
+  DVec x = vec_rand(st, st.lit(n));
+  DDouble s(x.sum());
+  DVec y = x.map([&](DVal v) -> DVal { return DDouble(v) - s; });
+  st.print(y.sum());
+  DVec z = vec_rand(st, st.lit(n / 2));
+  st.print(z.sum());
+  st.print(y.at(st.lit(int64_t{1})));
+}
+
 struct Spec {
   std::string name;
   std::function<void(Stage&)> body;
@@ -247,6 +267,8 @@ int main(int argc, char** argv) {
       {"find_count_n100000_unfused", [](Stage& st) { find_count(st, 100000); }},
       {"axpy_n100000_unfused", [](Stage& st) { axpy(st, 100000); }},
       {"count_gt_n100000_unfused", [](Stage& st) { count_gt(st, 100000); }},
+      {"fusion_blockers_n10000", [](Stage& st) { fusion_blockers(st, 10000); }},
+      {"fusion_blockers_n10000_unfused", [](Stage& st) { fusion_blockers(st, 10000); }},
   };
   const std::string only = argc > 2 ? argv[2] : "";
   if (only == "kmeans_n16777216_d64_k64_it1" || only == "kmeans_n16777216_d64_k64_it1_unfused")

@@ -23,6 +23,10 @@
 #include "program_exec.hpp"
 
 #include <algorithm>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -260,7 +264,7 @@ void Executor::join_all() {
     l->src = nullptr;
   }
   unresolved_.clear();
-  for (auto& [line, l] : prints_) lines_[line] = format_val(lazy_val(*l));
+  format_prints();
   prints_.clear();
   size_t live = 0;
   for (auto& w : vecs_)
@@ -271,6 +275,80 @@ void Executor::join_all() {
       vecs_[live++] = w;
     }
   vecs_.resize(live);
+}
+
+// A small persistent pool for host-side work that is embarrassingly parallel: the formatting
+// of a loop's printed results (a GDA fit prints d^2 + 2d + 1 values, the C4 program k d
+// centroids; std::to_chars is ~80 ns a value, which made the join of such a program the
+// largest host cost of its run).
+namespace {
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool p;
+    return p;
+  }
+  // fn(i) for i in [0, n), in chunks, on the pool's workers and the calling thread
+  void parallel_for(size_t n, const std::function<void(size_t, size_t)>& fn) {
+    const size_t parts = std::min<size_t>(workers_.size() + 1, (n + 255) / 256);
+    if (parts <= 1) {
+      fn(0, n);
+      return;
+    }
+    std::unique_lock<std::mutex> call(call_mu_);   // one parallel_for at a time
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = &fn;
+      n_ = n;
+      parts_ = parts;
+      next_ = 1;
+      done_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn(0, n / parts);   // part 0 on the caller
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return done_ == parts_ - 1; });
+    fn_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const unsigned nw = std::min(7u, hw > 1 ? hw - 1 : 0u);
+    for (unsigned w = 0; w < nw; ++w) workers_.emplace_back([this] { loop(); });
+    for (auto& t : workers_) t.detach();
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return gen_ != seen && fn_ != nullptr && next_ < parts_; });
+      seen = gen_;
+      while (fn_ != nullptr && next_ < parts_) {
+        const size_t part = next_++;
+        const auto* fn = fn_;
+        const size_t lo = n_ * part / parts_, hi = n_ * (part + 1) / parts_;
+        lk.unlock();
+        (*fn)(lo, hi);
+        lk.lock();
+        if (++done_ == parts_ - 1) done_cv_.notify_one();
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, call_mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(size_t, size_t)>* fn_ = nullptr;
+  size_t n_ = 0, parts_ = 0, next_ = 0, done_ = 0;
+  uint64_t gen_ = 0;
+};
+}  // namespace
+
+void Executor::format_prints() {
+  HostPool::get().parallel_for(prints_.size(), [&](size_t lo, size_t hi) {
+    for (size_t q = lo; q < hi; ++q) lines_[prints_[q].first] = format_val(lazy_val(*prints_[q].second));
+  });
 }
 
 Val Executor::lazy_val(const Lazy& l) {

@@ -281,6 +281,7 @@ class Executor {
   void fence();
   void fence_on(cudaStream_t s);
   static Val lazy_val(const Lazy& l);
+  void format_prints();   // the deferred prints of joined loops (parallel on a host pool)
   LazyP make_lazy(const void* src, Ty ty, int esz);
   void bind(int sym, Val v) {
     env_[sym] = std::move(v);

@@ -436,7 +436,7 @@ def _strip(report):
 def test_unfused_fixtures_present():
     assert set(UNFUSED) >= {"kmeans_n4096_d16_k8_it2", "groupby_n100000_k16", "gda_n20000_d4",
                             "logreg_n20000_d8_it2", "mean_variance_n100000", "find_count_n100000",
-                            "axpy_n100000", "count_gt_n100000"}
+                            "axpy_n100000", "count_gt_n100000", "fusion_blockers_n10000"}
 
 
 @pytest.mark.parametrize("name", UNFUSED)
@@ -452,6 +452,13 @@ def test_executor_fusion_matches_reference_fusion_dry_run(name, monkeypatch):
     assert fused["expected"] == unf["expected"]
     _, ra = run_program(fused["program"], seed=1)
     _, rb = run_program(unf["program"], seed=1)
+    if name == "fusion_blockers_n10000":
+        # the pairs the fusion must refuse stay apart: the two sums of m around its update, x's
+        # sum and the map that reads it, loops of different ranges; the map and its own sum
+        # (range VectorLength of the map) fuse vertically, which the reference never does
+        assert [(e["n"], e["live_elems"]) for e in ra] == [(8, 1), (8, 1), (10000, 1), (10000, 1), (10000, 1), (5000, 1)]
+        assert [(e["n"], e["live_elems"]) for e in rb] == [(8, 1), (8, 1), (10000, 1), (10000, 2), (5000, 1)]
+        return
     if name == "axpy_n100000":
         # vertical fusion through VectorLength: z = zip_with(x, y) and z.sum() (range
         # VectorLength(z)) become ONE loop here; the reference's cycle check never lets its
