@@ -285,8 +285,10 @@ namespace {
 class HostPool {
  public:
   static HostPool& get() {
-    static HostPool p;
-    return p;
+    // never destroyed: its workers stay blocked on the condition variable until the process
+    // ends, and destroying a condition variable with waiters blocks (exit would hang)
+    static HostPool* p = new HostPool;
+    return *p;
   }
   // fn(i) for i in [0, n), in chunks, on the pool's workers and the calling thread
   void parallel_for(size_t n, const std::function<void(size_t, size_t)>& fn) {
@@ -364,7 +366,13 @@ Val Executor::lazy_val(const Lazy& l) {
 }
 
 LazyP Executor::make_lazy(const void* src, Ty ty, int esz) {
-  auto l = std::make_shared<Lazy>();
+  // lazies come in chunks (a GDA scatter binds d^2 of them per launch): one allocation per 1,024,
+  // each handle an aliasing pointer into its chunk
+  if (!lazy_chunk_ || lazy_used_ == lazy_chunk_->size()) {
+    lazy_chunk_ = std::make_shared<std::vector<Lazy>>(1024);
+    lazy_used_ = 0;
+  }
+  LazyP l(lazy_chunk_, &(*lazy_chunk_)[lazy_used_++]);
   l->src = static_cast<const unsigned char*>(src);
   l->ty = ty;
   l->esz = esz;

@@ -267,6 +267,8 @@ class Executor {
   std::vector<std::string> lines_;            // printed output
   std::vector<std::pair<size_t, LazyP>> prints_;   // lines waiting for a loop result
   std::vector<LazyP> unresolved_;
+  std::shared_ptr<std::vector<Lazy>> lazy_chunk_;   // make_lazy's current allocation chunk
+  size_t lazy_used_ = 0;
   bool main_async_ = false;                   // main-stream work reads pinned staging
   cudaEvent_t prof_t0_ = nullptr;             // DLX_PROGRAM_PROFILE: run start on the main stream
 
