@@ -1,6 +1,7 @@
-# early L2 prefetch of the first tiles before the PDL wait: A/B vs the committed kernel; N=2 code path on one GPU
-OUT=gpurun_out/r320; mkdir -p $OUT
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -rf -x --timeout 300 -k "kmeans or screened or c4" > $OUT/pytest_kmeans.log 2>&1; echo "rc=$?" >> $OUT/pytest_kmeans.log
+# d = 64 converters with 8 columns per lane (8-byte plane stores) vs the committed kernel; smoke
+OUT=gpurun_out/r323; mkdir -p $OUT
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_program.py -m gpu -q -rf -x --timeout 300 -k "kmeans or screened or c4 or c1" > $OUT/pytest_kmeans.log 2>&1; echo "rc=$?" >> $OUT/pytest_kmeans.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
 for i in 1 2 3; do
 for v in acc3 new; do
   if [ $v = new ]; then L=""; else L=paper_1109_0778_b200/build_$v/libdlx.so; fi
@@ -9,5 +10,4 @@ for v in acc3 new; do
   done
 done
 done
-DLX_BENCH_SHARED_DEVICE=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29611 bench.py --gpus 2 --steps 5 --warmup 3 > $OUT/bench_n2_shared.json 2> $OUT/bench_n2_shared.err; echo "rc=$?" >> $OUT/bench_n2_shared.err
 echo done > $OUT/DONE
