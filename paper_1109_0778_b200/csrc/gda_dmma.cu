@@ -429,7 +429,9 @@ gda_fit64_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant_
                  const double* __restrict__ mu0, const double* __restrict__ mu1,
                  double* __restrict__ parts, const int* __restrict__ skip,
                  double* __restrict__ parts_sd, long long* __restrict__ parts_n1,
-                 double* __restrict__ shift_out) {
+                 double* __restrict__ shift_out, double* __restrict__ S_out, unsigned* __restrict__ counter) {
+  // S_out (pass 2 on given means, !kFused): the last CTA to finish folds the CTAs' records into
+  // S_out itself (ascending CTA order) — the fit's fallback then needs no combine launch
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // the 128-byte swizzle needs 1024-byte aligned boxes; offsetting the shared array itself (not
   // an integer-cast address) keeps every access below an LDS rather than a generic load
@@ -634,6 +636,22 @@ gda_fit64_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant_
       parts_n1[blockIdx.x] = k;
     }
   }
+  if (!kFused && S_out != nullptr) {
+    __shared__ int last;
+    __threadfence();
+    named_bar(2, kG64MmaWarps * 32);
+    if (tid == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    named_bar(2, kG64MmaWarps * 32);
+    if (last) {
+      __threadfence();
+      for (int e = tid; e < 4096; e += kG64MmaWarps * 32) {
+        double v = 0.0;
+        for (unsigned p = 0; p < gridDim.x; ++p) v += __ldcg(parts + static_cast<size_t>(p) * 4096 + e);
+        S_out[e] = v;
+      }
+      if (tid == 0) *counter = 0u;
+    }
+  }
 }
 
 // TMA tensor maps of x (n x 64 fp64, boxes of 64 rows x 16 columns, 128-byte swizzle) and y
@@ -695,7 +713,8 @@ int gda_pass2_dmma(const double* x, const long long* y, int64_t n, int d, const 
                                   static_cast<int>(kG64Smem)));
     DLX_CUDA(launch_pdl(gda_fit64_kernel<false>, dim3(grid), dim3(kG64Threads), kG64Smem, stream, tmx, tmy, x, y, n, mu0,
                         mu1, parts, static_cast<const int*>(nullptr), static_cast<double*>(nullptr),
-                        static_cast<long long*>(nullptr), static_cast<double*>(nullptr)));
+                        static_cast<long long*>(nullptr), static_cast<double*>(nullptr), static_cast<double*>(nullptr),
+                        static_cast<unsigned*>(nullptr)));
     DLX_LAUNCHED("gda_fit64_kernel");
     return combine_f64(parts, grid, static_cast<long long>(d) * d, out, stream);
   }
@@ -756,7 +775,8 @@ int gda_fit(const double* x, const long long* y, int64_t n, int d, long long* n1
                                   static_cast<int>(kG64Smem)));
     DLX_CUDA(launch_pdl(gda_fit64_kernel<true>, dim3(grid), dim3(kG64Threads), kG64Smem, stream, tmx, tmy, x, y, n,
                         static_cast<const double*>(nullptr), static_cast<const double*>(nullptr), parts,
-                        static_cast<const int*>(nullptr), parts_sd, parts_n1, shift));
+                        static_cast<const int*>(nullptr), parts_sd, parts_n1, shift, static_cast<double*>(nullptr),
+                        static_cast<unsigned*>(nullptr)));
     DLX_LAUNCHED("gda_fit64_kernel");
   } else {
     DLX_CUDA(cudaFuncSetAttribute(gda_pass2_dmma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -774,12 +794,14 @@ int gda_fit(const double* x, const long long* y, int64_t n, int d, long long* n1
                                reinterpret_cast<unsigned*>(shift + 128), n1_out, mu0, mu1, S, ok, stream))
     return rc;
   // fallback, decided on the device: pass 2 on the exact means when the shift was too far off
-  if (k64) {
+  if (k64) {   // folds its own records into S when it runs (no combine launch)
     DLX_CUDA(launch_pdl(gda_fit64_kernel<false>, dim3(grid), dim3(kG64Threads), kG64Smem, stream, tmx, tmy, x, y, n,
                         static_cast<const double*>(mu0), static_cast<const double*>(mu1), parts,
                         static_cast<const int*>(ok), static_cast<double*>(nullptr),
-                        static_cast<long long*>(nullptr), static_cast<double*>(nullptr)));
+                        static_cast<long long*>(nullptr), static_cast<double*>(nullptr), S,
+                        reinterpret_cast<unsigned*>(shift + 128)));
     DLX_LAUNCHED("gda_fit64_kernel");
+    return DLX_OK;
   } else {
     DLX_CUDA(launch_pdl(gda_pass2_dmma_kernel<false>, dim3(grid), dim3(kGdThreads), kGdSmem, stream, x, y, n, d,
                         static_cast<const double*>(mu0), static_cast<const double*>(mu1), parts,

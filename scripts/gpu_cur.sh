@@ -1,13 +1,9 @@
-# d = 64 converters with 8 columns per lane (8-byte plane stores) vs the committed kernel; smoke
-OUT=gpurun_out/r323; mkdir -p $OUT
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_program.py -m gpu -q -rf -x --timeout 300 -k "kmeans or screened or c4 or c1" > $OUT/pytest_kmeans.log 2>&1; echo "rc=$?" >> $OUT/pytest_kmeans.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
-for i in 1 2 3; do
-for v in acc3 new; do
-  if [ $v = new ]; then L=""; else L=paper_1109_0778_b200/build_$v/libdlx.so; fi
-  for c in c4 c4shard8; do
-    DLX_LIB_PATH=$L timeout 300 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/bench_${c}_${v}_$i.json 2>> $OUT/bench.err
-  done
+# GDA fit fallback folds its own records (no combine launch when certified): tests, C3 bench, launch list
+OUT=gpurun_out/r324; mkdir -p $OUT
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_peer.py tests/test_gpu_program.py tests/test_gpu_sharded.py -m gpu -q -rf -x --timeout 300 -k "gda or c3" > $OUT/pytest_gda.log 2>&1; echo "rc=$?" >> $OUT/pytest_gda.log
+for i in 1 2; do
+  timeout 300 python bench.py --config c3 --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/bench_c3_$i.json 2>> $OUT/bench.err
 done
-done
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 30 --csv --log-file $OUT/launches_c3.csv \
+  python bench.py --config c3 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_launch_c3.log 2>&1
 echo done > $OUT/DONE
