@@ -348,6 +348,14 @@ class HostPool {
 }  // namespace
 
 void Executor::format_prints() {
+  static const bool serial = [] {
+    const char* e = getenv("DLX_HOST_POOL");
+    return e && e[0] == '0';
+  }();
+  if (serial) {
+    for (auto& [line, l] : prints_) lines_[line] = format_val(lazy_val(*l));
+    return;
+  }
   HostPool::get().parallel_for(prints_.size(), [&](size_t lo, size_t hi) {
     for (size_t q = lo; q < hi; ++q) lines_[prints_[q].first] = format_val(lazy_val(*prints_[q].second));
   });
@@ -366,13 +374,8 @@ Val Executor::lazy_val(const Lazy& l) {
 }
 
 LazyP Executor::make_lazy(const void* src, Ty ty, int esz) {
-  // lazies come in chunks (a GDA scatter binds d^2 of them per launch): one allocation per 1,024,
-  // each handle an aliasing pointer into its chunk
-  if (!lazy_chunk_ || lazy_used_ == lazy_chunk_->size()) {
-    lazy_chunk_ = std::make_shared<std::vector<Lazy>>(1024);
-    lazy_used_ = 0;
-  }
-  LazyP l(lazy_chunk_, &(*lazy_chunk_)[lazy_used_++]);
+  // a GDA scatter binds d^2 of these per launch: a deque slot each, no allocation or refcount
+  Lazy* l = &lazies_.emplace_back();
   l->src = static_cast<const unsigned char*>(src);
   l->ty = ty;
   l->esz = esz;

@@ -9,6 +9,7 @@
 #include <chrono>
 #include <functional>
 #include <map>
+#include <deque>
 #include <memory>
 #include <string>
 #include <variant>
@@ -101,7 +102,7 @@ struct Lazy {
   int esz = 8;
   bool ready = false;
 };
-using LazyP = std::shared_ptr<Lazy>;
+using LazyP = Lazy*;   // owned by the run's Executor (lazies_), which outlives every Val of the run
 
 struct Cell;
 using CellP = std::shared_ptr<Cell>;
@@ -267,8 +268,7 @@ class Executor {
   std::vector<std::string> lines_;            // printed output
   std::vector<std::pair<size_t, LazyP>> prints_;   // lines waiting for a loop result
   std::vector<LazyP> unresolved_;
-  std::shared_ptr<std::vector<Lazy>> lazy_chunk_;   // make_lazy's current allocation chunk
-  size_t lazy_used_ = 0;
+  std::deque<Lazy> lazies_;   // every lazy of this run (stable addresses; no refcounting per bind)
   bool main_async_ = false;                   // main-stream work reads pinned staging
   cudaEvent_t prof_t0_ = nullptr;             // DLX_PROGRAM_PROFILE: run start on the main stream
 

@@ -1,9 +1,10 @@
-# GDA combine: the finalize reads the class sums from shared memory; tests, C3 bench, launch list
-OUT=gpurun_out/r325; mkdir -p $OUT
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_peer.py tests/test_gpu_program.py tests/test_gpu_sharded.py -m gpu -q -rf -x --timeout 300 -k "gda or c3" > $OUT/pytest_gda.log 2>&1; echo "rc=$?" >> $OUT/pytest_gda.log
+# drop-in e2e regression hunt: host print pool on / off, raw-pointer lazies; C4 e2e and program times
+OUT=gpurun_out/r327; mkdir -p $OUT
 for i in 1 2; do
-  timeout 300 python bench.py --config c3 --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/bench_c3_$i.json 2>> $OUT/bench.err
+  timeout 600 python bench.py --config c4 --steps 10 --warmup 3 --no-cpu-baseline > $OUT/bench_c4_pool_$i.json 2> $OUT/bench_c4_pool_$i.err
+  DLX_HOST_POOL=0 timeout 600 python bench.py --config c4 --steps 10 --warmup 3 --no-cpu-baseline > $OUT/bench_c4_nopool_$i.json 2> $OUT/bench_c4_nopool_$i.err
 done
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 30 --csv --log-file $OUT/launches_c3.csv \
-  python bench.py --config c3 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_launch_c3.log 2>&1
+timeout 300 python scripts/program_times.py c3 c4 > $OUT/program_times_pool.jsonl 2> $OUT/program_times.err
+DLX_HOST_POOL=0 timeout 300 python scripts/program_times.py c3 c4 > $OUT/program_times_nopool.jsonl 2>> $OUT/program_times.err
+timeout 300 python scripts/diag/e2e_dropin_profile.py 16777216 64 64 > $OUT/e2e_c4.json 2> $OUT/e2e_c4_profile.txt
 echo done > $OUT/DONE
