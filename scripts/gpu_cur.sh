@@ -1,10 +1,13 @@
-# drop-in e2e regression hunt: host print pool on / off, raw-pointer lazies; C4 e2e and program times
-OUT=gpurun_out/r327; mkdir -p $OUT
+# k-means L2 prefetch distance re-tune after the three-accumulator screen (0 / 2 / 3 / 4 tiles); the
+# two-thread print-formatting test
+OUT=gpurun_out/r329; mkdir -p $OUT
+timeout 600 python -m pytest tests/test_gpu_program.py -m gpu -q -rf --timeout 300 -k "parallel_print" > $OUT/pytest_pool.log 2>&1; echo "rc=$?" >> $OUT/pytest_pool.log
 for i in 1 2; do
-  timeout 600 python bench.py --config c4 --steps 10 --warmup 3 --no-cpu-baseline > $OUT/bench_c4_pool_$i.json 2> $OUT/bench_c4_pool_$i.err
-  DLX_HOST_POOL=0 timeout 600 python bench.py --config c4 --steps 10 --warmup 3 --no-cpu-baseline > $OUT/bench_c4_nopool_$i.json 2> $OUT/bench_c4_nopool_$i.err
+for v in cur l2a2 l2a4 l2a0; do
+  if [ $v = cur ]; then L=""; else L=paper_1109_0778_b200/build_$v/libdlx.so; fi
+  for c in c4 c4shard8; do
+    DLX_LIB_PATH=$L timeout 300 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/bench_${c}_${v}_$i.json 2>> $OUT/bench.err
+  done
 done
-timeout 300 python scripts/program_times.py c3 c4 > $OUT/program_times_pool.jsonl 2> $OUT/program_times.err
-DLX_HOST_POOL=0 timeout 300 python scripts/program_times.py c3 c4 > $OUT/program_times_nopool.jsonl 2>> $OUT/program_times.err
-timeout 300 python scripts/diag/e2e_dropin_profile.py 16777216 64 64 > $OUT/e2e_c4.json 2> $OUT/e2e_c4_profile.txt
+done
 echo done > $OUT/DONE

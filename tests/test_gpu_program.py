@@ -240,3 +240,39 @@ def test_reference_side_binding_run_staged():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("PASS") == 4 and "FAIL" not in r.stdout, r.stdout
+
+
+def test_parallel_print_formatting_two_threads():
+    """Programs whose joined loops print > 256 values format them on the host pool
+    (program.cpp: HostPool); two handles on two host threads (the e2e bench's pattern) give the
+    serial formatting's text exactly, every run."""
+    import os
+    import subprocess
+    import sys
+    import threading
+    from paper_1109_0778_b200.descriptors import gda_program
+    from paper_1109_0778_b200.program import Program
+    desc = gda_program(20000, 24)   # 24^2 + 2 * 24 + 1 = 625 printed values after the joins
+    ref = Program(desc).run(seed=3).output
+    progs = [Program(desc), Program(desc)]
+    outs = [[], []]
+
+    def work(t):
+        for _ in range(4):
+            outs[t].append(progs[t].run(seed=3).output)
+
+    ths = [threading.Thread(target=work, args=(t,)) for t in range(2)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    assert all(o == ref for o in outs[0] + outs[1])
+    # the serial path (DLX_HOST_POOL=0) prints the same text, and a process using the pool exits
+    code = ("import sys; sys.path.insert(0, %r); from paper_1109_0778_b200.descriptors import gda_program; "
+            "from paper_1109_0778_b200.program import Program; print(Program(gda_program(20000, 24)).run(seed=3).output, end='')"
+            % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    for env_pool in ("0", "1"):
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                           env=dict(os.environ, DLX_HOST_POOL=env_pool))
+        assert r.returncode == 0, r.stderr[-2000:]
+        assert r.stdout == ref
