@@ -508,3 +508,52 @@ def test_executor_fusion_c4_shape_on_b200():
     g, e = lines(got.output), lines(exp.output)
     assert len(g) == len(e) == 1 + 64 + 64 * 64
     assert g == e
+
+
+# ---- the headline shape (d = k = 64) staged by the reference, unfused, at N = 4,096 -------------
+HEADLINE_UNFUSED = os.path.join(HERE, "golden", "staged_c4", "kmeans_n4096_d64_k64_it2_unfused.json.xz")
+
+
+def _load_xz(path):
+    import lzma
+    with lzma.open(path, "rt") as f:
+        return json.load(f)
+
+
+def test_headline_shape_unfused_fixture_matches_oracle_port():
+    """Two k-means iterations at d = k = 64 staged through the reference DSL (8,322 root loops; the
+    reference's fuse_loops cannot fuse this shape in reasonable time) and evaluated as the
+    reference's own MiniC: the oracle port prints exactly the same text."""
+    fx = _load_xz(HEADLINE_UNFUSED)
+    assert fx["program"]["fusion"] == "executor" and fx["root_loops"] == 8322
+    x, mu0 = O.kmeans_inputs(4096, 64, 64)
+    hist = O.kmeans_run(x, 64, 2, mu0)
+    got = []
+    for counts, _, _, _, assign in hist:
+        got.append(str(int(assign[0])))
+        got += [str(int(c)) for c in counts]
+    got += [O.format_double(v) for v in hist[-1][2].reshape(-1)]
+    assert lines(fx["expected"]) == got
+
+
+def test_headline_shape_unfused_dry_run(monkeypatch):
+    """CPU: the executor fuses the 8,322 root loops into the two k-means multiloops (4,161 live
+    elems each, centroid update on the device)."""
+    from paper_1109_0778_b200.program import Program
+    monkeypatch.setenv("DLX_PROGRAM_DRYRUN", "1")
+    r = Program(_load_xz(HEADLINE_UNFUSED)["program"]).run(dry_run=True)
+    assert [(e["family"], e["live_elems"], e["d"], e["k"], e["update"]) for e in r.report] == \
+        [("kmeans", 4161, 64, 64, "device")] * 2
+
+
+@pytest.mark.gpu
+def test_headline_shape_unfused_on_b200():
+    """B200: the unfused headline-shape program, fused by the executor and run on the tcgen05
+    screened kernel, prints the reference MiniC's output (ints exact, doubles rtol 1e-9)."""
+    from paper_1109_0778_b200.program import Program
+    fx = _load_xz(HEADLINE_UNFUSED)
+    r = Program(fx["program"]).run(seed=fx["seed"])
+    got, exp = lines(r.output), lines(fx["expected"])
+    assert len(got) == len(exp) == 2 * 65 + 64 * 64
+    bad = [(i, g, e) for i, (g, e) in enumerate(zip(got, exp)) if not same_value(g, e)]
+    assert not bad, bad[:5]
