@@ -27,6 +27,8 @@
 #include <functional>
 #include <mutex>
 #include <thread>
+
+#include <unistd.h>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -292,7 +294,8 @@ class HostPool {
   }
   // fn(i) for i in [0, n), in chunks, on the pool's workers and the calling thread
   void parallel_for(size_t n, const std::function<void(size_t, size_t)>& fn) {
-    const size_t parts = std::min<size_t>(workers_.size() + 1, (n + 255) / 256);
+    // a forked child inherits the pool object but not its threads: run serially there
+    const size_t parts = getpid() == pid_ ? std::min<size_t>(workers_.size() + 1, (n + 255) / 256) : 1;
     if (parts <= 1) {
       fn(0, n);
       return;
@@ -315,7 +318,7 @@ class HostPool {
   }
 
  private:
-  HostPool() {
+  HostPool() : pid_(getpid()) {
     const unsigned hw = std::thread::hardware_concurrency();
     const unsigned nw = std::min(7u, hw > 1 ? hw - 1 : 0u);
     for (unsigned w = 0; w < nw; ++w) workers_.emplace_back([this] { loop(); });
@@ -338,6 +341,7 @@ class HostPool {
       }
     }
   }
+  pid_t pid_;
   std::vector<std::thread> workers_;
   std::mutex mu_, call_mu_;
   std::condition_variable cv_, done_cv_;
