@@ -268,6 +268,10 @@ int main(int argc, char** argv) {
       {"axpy_n100000_unfused", [](Stage& st) { axpy(st, 100000); }},
       {"count_gt_n100000_unfused", [](Stage& st) { count_gt(st, 100000); }},
       {"fusion_blockers_n10000", [](Stage& st) { fusion_blockers(st, 10000); }},
+      {"gda_n20000_d16", [](Stage& st) { gda(st, 20000, 16); }},
+      {"gda_n20000_d16_unfused", [](Stage& st) { gda(st, 20000, 16); }},
+      {"logreg_n20000_d16_it3", [](Stage& st) { logreg(st, 20000, 16, 3, 1.0 / 20000); }},
+      {"logreg_n20000_d16_it3_unfused", [](Stage& st) { logreg(st, 20000, 16, 3, 1.0 / 20000); }},
       // the headline shape (d = k = 64) at a small N: the reference's fuse_loops cannot fuse it
       // in reasonable time, so only the unfused program exists; its MiniC output is evaluated
       {"kmeans_n4096_d64_k64_it2_unfused", [](Stage& st) { kmeans(st, 4096, 64, 64, 2); }},

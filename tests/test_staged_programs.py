@@ -135,7 +135,7 @@ def test_staged_program_on_b200(path):
     if name.startswith("gda"):
         assert fams == ["bucket_rows", "gda_scatter"]
     if name.startswith("logreg"):
-        assert fams == ["logistic", "logistic"] and all(r["update"] == "device" for r in report)
+        assert fams and set(fams) == {"logistic"} and all(r["update"] == "device" for r in report)
 
 
 @pytest.mark.gpu
