@@ -1,4 +1,5 @@
-# final full validation: every GPU test, smoke, default bench line
-bash scripts/gpu_round.sh r332 smoke tests
-OUT=gpurun_out/r332
-timeout 600 python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err
+# C3 / C1 drop-in host timelines after the host-cost trims
+OUT=gpurun_out/r333; mkdir -p $OUT
+DLX_PROGRAM_PROFILE=1 timeout 300 python scripts/diag/program_profile.py c3 > $OUT/c3_profile.txt 2>&1
+DLX_PROGRAM_PROFILE=1 timeout 300 python scripts/diag/program_profile.py c1 > $OUT/c1_profile.txt 2>&1
+echo done > $OUT/DONE
