@@ -311,8 +311,13 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
         prog = KMeansProgram(x, k, mu0, comm=comm, method=args.method)
         kernel_fn = lambda: ml.kmeans_step(x, prog.mu, prog.assign, prog.counts, prog.sums,  # noqa: E731
                                            method=args.method)
+        if comm is None:   # one rank: the update fused into the combine launch (dlx_kmeans_iteration)
+            kernel_fn = lambda: ml.kmeans_iteration(x, prog.mu, prog.assign, prog.counts,  # noqa: E731
+                                                    prog.sums, method=args.method)
 
         def rest():   # allreduce + update (one fused launch with --comm peer)
+            if comm is None:
+                return
             if isinstance(comm, PeerComm):
                 comm.kmeans_update_(prog.counts, prog.sums, prog.mu)
                 return
@@ -404,11 +409,13 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
                     fn()
                 return g, int(L.dlx_launch_count()) - c0
             graphs["kernel"] = cap(kernel_fn)
-            if family != "gda":
+            if family != "gda" and not (family == "kmeans" and comm is None):
                 graphs["rest"] = cap(rest)
             torch.cuda.synchronize()
     run_kernel = (graphs["kernel"][0].replay if "kernel" in graphs else kernel_fn)
     run_rest = (graphs["rest"][0].replay if "rest" in graphs else (rest if family != "gda" else None))
+    if family == "kmeans" and comm is None:
+        run_rest = rest   # nothing left: the update ran inside the kernel graph's combine
     launches0 = int(L.dlx_launch_count())
     t_start.record(stream)
     for s in range(args.steps):
@@ -474,6 +481,8 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             "config": {"workload": args.config, **p, "parallelism": f"sample-sharded dp{world}",
                        "exchange": None if world == 1 else ("peer-memory fused allreduce+update" if args.comm == "peer"
                                                             else "NCCL allReduce + update kernel"),
+                       **({"update": "fused into the combine launch (dlx_kmeans_iteration)" if world == 1
+                           else "after the exchange"} if family == "kmeans" else {}),
                        "l2": "inputs larger than L2 (no flush needed)" if bytes_launch > 256e6 else
                              "inputs L2-resident (launch-bound config)",
                        "method": {0: "auto", 1: "direct", 2: "screened"}[args.method],
