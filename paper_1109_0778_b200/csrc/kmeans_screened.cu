@@ -113,10 +113,6 @@ constexpr int kL2Ahead = DLX_KMEANS_L2_AHEAD;   // converters' L2 prefetch dista
 #endif
 constexpr int kAcc = DLX_KMEANS_SCREEN_ACC;   // screen accumulators: 3 (HH, CR, W1; W2 refined) or 4
 static_assert(kAcc == 3 || kAcc == 4, "screen accumulators");
-#ifndef DLX_KMEANS_REFINE
-#define DLX_KMEANS_REFINE 0
-#endif
-constexpr bool kRefine = DLX_KMEANS_REFINE;   // 3 accumulators: refine W3-survivors in the epilogue
 // warpgroup 0: warp 0 screen MMAs, warp 1 fold MMAs, warp 2 tail (warp 3 idle); warpgroup 1:
 // epilogue; then the converter warpgroups.  Registers are rebalanced with setmaxnreg after the
 // prologue: warpgroup 0 drops to 32, the epilogue runs at 128, converters take the rest.
@@ -647,7 +643,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     const unsigned long long kmask = k == 64 ? ~0ull : ((1ull << k) - 1);
     const unsigned long long vmask = S.valid;   // finite centroids (the others never survive)
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-    const int window = S.window, window4 = S.window4;
+    const int window = S.window;
     const int4* nm4 = reinterpret_cast<const int4*>(S.nm0);
     const uint32_t oh_row = (static_cast<uint32_t>(q) >> 3) * 512u + (q & 7) * 64u;
     const uint32_t oh_sw = (q & 7) >> 1;
@@ -709,46 +705,6 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
 #pragma unroll
           for (int u = 32; u < 64; ++u) nhi = __funnelshift_l(static_cast<unsigned>(tv[u] - thr1), nhi, 1);
           full = ((static_cast<unsigned long long>(__brev(nhi)) << 32) | __brev(nlo)) & vmask;
-          if (kAcc == 3 && kRefine && (full & (full - 1)) != 0 && flag == 0) {
-            // refine the W3-survivors with their exact W2 (rare: ~0.2 % of the rows)
-            const unsigned char* Ab = smem + kOffA + b3 * kABuf;
-            uint4 lq[4], fq[4];   // the row's b6 (l) and b5 (F) planes, 16 columns per chunk
-#pragma unroll
-            for (int c16 = 0; c16 < 4; ++c16) {
-              lq[c16] = *reinterpret_cast<const uint4*>(Ab + sw128_offset(q, 64 + 16 * c16));
-              fq[c16] = *reinterpret_cast<const uint4*>(Ab + kPlane2 + sw128_offset(q, 16 * c16));
-            }
-            int tl[kMaxK];
-#pragma unroll
-            for (int u = 0; u < kMaxK; ++u) tl[u] = tv[u];
-            int t4min = INT_MAX;
-            for (unsigned long long f = full; f; f &= f - 1) {
-              const int c = __ffsll(static_cast<long long>(f)) - 1;
-              unsigned w2 = 0;
-#pragma unroll
-              for (int c16 = 0; c16 < 4; ++c16) {
-                const uint4 G = *reinterpret_cast<const uint4*>(Bm + sw64_offset(128 + c, 16 * c16));
-                const uint4 L = *reinterpret_cast<const uint4*>(Bm + sw64_offset(64 + c, 16 * c16));
-                w2 = __dp4a(lq[c16].x, G.x, w2);
-                w2 = __dp4a(lq[c16].y, G.y, w2);
-                w2 = __dp4a(lq[c16].z, G.z, w2);
-                w2 = __dp4a(lq[c16].w, G.w, w2);
-                w2 = __dp4a(fq[c16].x, L.x, w2);
-                w2 = __dp4a(fq[c16].y, L.y, w2);
-                w2 = __dp4a(fq[c16].z, L.z, w2);
-                w2 = __dp4a(fq[c16].w, L.w, w2);
-              }
-              const int t4 = tl[c] - 2 * static_cast<int>(w2 >> 16);   // the 4-accumulator score
-              tl[c] = t4;
-              t4min = min(t4min, t4);
-            }
-            unsigned long long g = 0;
-            for (unsigned long long f = full; f; f &= f - 1) {
-              const int c = __ffsll(static_cast<long long>(f)) - 1;
-              if (tl[c] <= t4min + window4) g |= 1ull << c;
-            }
-            full = g;
-          }
           if ((full & (full - 1)) == 0) {
             a = __ffsll(static_cast<long long>(full)) - 1;
           } else {

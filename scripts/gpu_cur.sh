@@ -1,8 +1,6 @@
-# A/B: small-kernel staging (one round of 16 loads vs the previous loop), C1 bench alternating
-OUT=gpurun_out/r338; mkdir -p $OUT
+# C1 warm-cache profile of the small kernel + combine (ncu --cache-control none)
+OUT=gpurun_out/r340; mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
-for i in 1 2 3; do
-  timeout 300 python bench.py --config c1 --steps 50 --warmup 5 --no-cpu-baseline --no-e2e > $OUT/c1_new_$i.json 2>&1
-  DLX_LIB_PATH=$PWD/build_old/libdlx.so timeout 300 python bench.py --config c1 --steps 50 --warmup 5 --no-cpu-baseline --no-e2e > $OUT/c1_old_$i.json 2>&1
-done
+timeout 300 ncu --metrics gpu__time_duration.sum --cache-control none --clock-control none -c 20 --csv --log-file $OUT/launches_c1_warm.csv python bench.py --config c1 --steps 4 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_l.log 2>&1
+timeout 300 ncu --set full --cache-control none --clock-control none --import-source on -k regex:"kmeans_small|combine_kmeans" -s 6 -c 2 -o $OUT/prof_c1_warm python bench.py --config c1 --steps 4 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_f.log 2>&1
 echo done > $OUT/DONE
