@@ -89,13 +89,28 @@ gda_fit_combine_kernel(const double* __restrict__ parts, const double* __restric
                        double* __restrict__ sd, long long* __restrict__ n1p, int64_t n,
                        const double* __restrict__ shift, unsigned* __restrict__ counter,
                        long long* __restrict__ n1_out, double* __restrict__ mu0, double* __restrict__ mu1,
-                       double* __restrict__ S, int* __restrict__ ok) {
+                       double* __restrict__ S, int* __restrict__ ok, const double* __restrict__ parts_q,
+                       double* __restrict__ qmax) {
   pdl_wait();
   pdl_trigger();
   const long long wS = static_cast<long long>(d) * d, bS = (wS + 31) / 32, bsd = (2LL * d + 31) / 32;
   if (blockIdx.x < bS) combine_columns<double, double>(parts, nparts, wS, Sp, blockIdx.x);
   else if (blockIdx.x < bS + bsd) combine_columns<double, double>(parts_sd, nparts, 2LL * d, sd, blockIdx.x - bS);
-  else combine_columns<long long, long long>(parts_n1, nparts, 1, n1p, 0);
+  else if (blockIdx.x == bS + bsd) combine_columns<long long, long long>(parts_n1, nparts, 1, n1p, 0);
+  else {   // the int8 fit's quanta: max over the CTAs per column (inf marks an out-of-range CTA)
+    __shared__ double qred[kCombWarps][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int j = static_cast<int>(blockIdx.x - bS - bsd - 1) * 32 + lane;
+    double q = 0.0;
+    if (j < d)
+      for (int p = warp; p < nparts; p += kCombWarps) q = fmax(q, parts_q[static_cast<size_t>(p) * d + j]);
+    qred[warp][lane] = q;
+    __syncthreads();
+    if (warp == 0 && j < d) {
+      for (int w = 1; w < kCombWarps; ++w) q = fmax(q, qred[w][lane]);
+      qmax[j] = q;
+    }
+  }
   __shared__ int last, bad;
   __threadfence();
   __syncthreads();
@@ -122,6 +137,11 @@ gda_fit_combine_kernel(const double* __restrict__ parts, const double* __restric
     mu1[j] = __ldcg(shift + 64 + j) + sd_s[d + j] / dn1;
     const double cj = corr(j, j), sj = __ldcg(Sp + j * d + j);
     if (!(cj <= 0.99 * sj)) bad = 1;
+    // int8 fit: every CTA's quantum <= 2^-30 of the column's RMS deviation about the shift
+    if (parts_q != nullptr) {
+      const double q = __ldcg(qmax + j) * 1073741824.0;
+      if (!(q * q * static_cast<double>(n) <= sj)) bad = 1;
+    }
   }
   for (long long e = threadIdx.x; e < wS; e += blockDim.x)
     S[e] = __ldcg(Sp + e) - corr(static_cast<int>(e / d), static_cast<int>(e % d));
@@ -135,10 +155,13 @@ gda_fit_combine_kernel(const double* __restrict__ parts, const double* __restric
 
 int gda_fit_combine(const double* parts, const double* parts_sd, const long long* parts_n1, int nparts, int d,
                     double* Sp, double* sd, long long* n1p, int64_t n, const double* shift, unsigned* counter,
-                    long long* n1_out, double* mu0, double* mu1, double* S, int* ok, cudaStream_t s) {
-  const long long blocks = (static_cast<long long>(d) * d + 31) / 32 + (2LL * d + 31) / 32 + 1;
+                    long long* n1_out, double* mu0, double* mu1, double* S, int* ok, cudaStream_t s,
+                    const double* parts_q, double* qmax) {
+  const long long blocks = (static_cast<long long>(d) * d + 31) / 32 + (2LL * d + 31) / 32 + 1 +
+                           (parts_q != nullptr ? (d + 31) / 32 : 0);
   DLX_CUDA(launch_pdl(gda_fit_combine_kernel, dim3(static_cast<unsigned>(blocks)), dim3(kCombWarps * 32), 0, s,
-                      parts, parts_sd, parts_n1, nparts, d, Sp, sd, n1p, n, shift, counter, n1_out, mu0, mu1, S, ok));
+                      parts, parts_sd, parts_n1, nparts, d, Sp, sd, n1p, n, shift, counter, n1_out, mu0, mu1, S, ok,
+                      parts_q, qmax));
   DLX_LAUNCHED("gda_fit_combine_kernel");
   return DLX_OK;
 }

@@ -727,6 +727,349 @@ int gda_pass2_dmma(const double* x, const long long* y, int64_t n, int d, const 
   return combine_f64(parts, grid, static_cast<long long>(d) * d, out, stream);
 }
 
+// ---- the d = 64 single-pass fit on the int8 tensor cores (gda_fit_i8_kernel) ------------------
+// S' = sum_i f_i f_i^T with f = fl(x - c_y) (the shift-centred rows, as the DMMA kernel forms them)
+// computed as an EXACT integer product: every CTA quantises f per column to the fixed point
+// Z_j = rne(f_j * 2^s_j) (|Z| < 2^46, s_j from the CTA's first tile: max |f_j| * 2^s_j < 2^42)
+// and splits Z into six balanced base-256 digits e_0..e_5 (each in [-128, 127]); with digit
+// significance t = 5 - i, the digit products F_a^T F_b with t_a + t_b <= 5 (the dropped ones are
+// below 2^-36 of the leading term) are four tcgen05 kind::i8 MMAs per 32-row step over digit
+// pair groups G0 = {e5, e4}, G1 = {e3, e2}, G2 = {e1, e0}: (G0,G0), (G0,G1), (G0,G2), (G1,G1),
+// each M = 128 (two digits x 64 columns) x N = 128, int32 accumulators resident in all 512 TMEM
+// columns for the whole launch (a product <= 2^14 per row: exact for <= 2^17 rows per CTA).
+// The off-diagonal group products enter S' with their transposes.  The class sums stay fp64
+// sums of the same f (the means need them exactly as the DMMA path forms them).  Certification
+// (gda_fit_combine): every CTA's quantum 2^-s_j must be <= 2^-30 of column j's RMS deviation,
+// and a value outside the CTA's range (|f| >= 2^(46 - s_j), inf, NaN) sets the quantum to inf —
+// either way *ok = 0 and the exact DMMA pass 2 on the means runs instead.
+// 12 converter warps + the issuer: at most 4 warps per SM sub-partition, 128 registers each
+constexpr int kI8Conv = 12;                           // converter warps (then the epilogue)
+constexpr int kI8Threads = (kI8Conv + 1) * 32;        // + the MMA issuer warp
+constexpr int kI8Rows = 96;                           // rows per tile: 4 passes of 24 (3 K-steps)
+constexpr int kI8Stages = 4;                          // digit-plane buffers in flight
+constexpr uint32_t kI8Group = kI8Rows * 128;          // one digit-pair group: 96 rows x 128 B
+constexpr uint32_t kI8Stage = 3 * kI8Group;           // three groups per tile
+constexpr size_t kI8OffMu = kI8Stages * kI8Stage;     // [c0: 0..63 | c1: 64..127] shift
+constexpr size_t kI8OffScale = kI8OffMu + 128 * 8;    // 2^s_j, then thresholds 2^(46-s_j)
+constexpr size_t kI8OffRed = kI8OffScale + 128 * 8;   // reductions: 512 x 8 doubles
+constexpr size_t kI8OffBar = kI8OffRed + kI8Conv * 32 * 8 * 8;
+constexpr size_t kI8Smem = kI8OffBar + (2 * kI8Stages + 2) * 8 + 16 + 1024;
+#ifndef DLX_I8_L2_AHEAD
+#define DLX_I8_L2_AHEAD 3
+#endif
+constexpr int kI8L2Ahead = DLX_I8_L2_AHEAD;            // converters' L2 bulk prefetch distance (tiles)
+static_assert(kI8Conv * 4096 == kI8Rows * 512, "one 4 KB prefetch per converter warp covers a tile");
+constexpr int kI8MaxTiles = (1 << 17) / kI8Rows;      // 2^17 rows per CTA (int32 exactness)
+static_assert(2 * 128 * 129 * 4 <= kI8OffMu, "TMEM staging must fit in the plane buffers");
+static_assert(kI8Smem <= 232448, "shared memory");
+
+
+__global__ void __launch_bounds__(kI8Threads, 1)
+gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y, int64_t n,
+                  double* __restrict__ parts, double* __restrict__ parts_sd, long long* __restrict__ parts_n1,
+                  double* __restrict__ parts_q, double* __restrict__ shift_out) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* const smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
+  double* const mu_s = reinterpret_cast<double*>(smem + kI8OffMu);
+  double* const sc_s = reinterpret_cast<double*>(smem + kI8OffScale);   // [0,64): 2^s, [64,128): bound
+  double* const red = reinterpret_cast<double*>(smem + kI8OffRed);
+  uint64_t* const pfull = reinterpret_cast<uint64_t*>(smem + kI8OffBar);
+  uint64_t* const pempty = pfull + kI8Stages;
+  uint64_t* const done = pempty + kI8Stages;
+  uint32_t* const tmem_slot = reinterpret_cast<uint32_t*>(done + 2);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t ntiles = (n + kI8Rows - 1) / kI8Rows;
+  const int mt = static_cast<int>(ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0);
+  if (tid == 0) {
+    for (int s = 0; s < kI8Stages; ++s) {
+      mbar_init(&pfull[s], kI8Conv);
+      mbar_init(&pempty[s], 1);
+    }
+    mbar_init(done, 1);
+    fence_mbar_init();
+    tmem_slot[1] = 0;   // range flag
+  }
+  if (warp == kI8Conv) tmem_alloc<512>(tmem_slot);
+  pdl_wait();   // x / y may come from the predecessor kernel
+  pdl_trigger();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kI8Conv) {
+    // ---- MMA issuer: four group products per 32-row step, converged warp, lane 0 issues ----
+    constexpr uint32_t ID = idesc_i8_major(128, 128, 1, 1, 1, 1);
+    for (int m = 0; m < mt; ++m) {
+      const int s = m % kI8Stages;
+      mbar_wait(&pfull[s], (m / kI8Stages) & 1);
+      tc_fence_after();
+      const uint32_t b0 = smem_addr(smem + s * kI8Stage);
+      if (lane == 0) {
+#pragma unroll
+        for (int kk = 0; kk < kI8Rows / 32; ++kk) {
+          const uint64_t g0 = sw128_kmajor_desc(b0 + kk * 4096);
+          const uint64_t g1 = sw128_kmajor_desc(b0 + kI8Group + kk * 4096);
+          const uint64_t g2 = sw128_kmajor_desc(b0 + 2 * kI8Group + kk * 4096);
+          const uint32_t acc = (m > 0 || kk > 0) ? 1u : 0u;
+          mma_i8(tmem + 0, g0, g0, ID, acc);
+          mma_i8(tmem + 128, g0, g1, ID, acc);
+          mma_i8(tmem + 256, g0, g2, ID, acc);
+          mma_i8(tmem + 384, g1, g1, ID, acc);
+        }
+        mma_commit(&pempty[s]);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) mma_commit(done);
+    __syncwarp();
+  } else {
+    // ---- converters: warp w, lane l: columns 4c..4c+3 (c = l & 15) of rows {r, r + 4} of an
+    // 8-row swizzle atom (disjoint bank halves), 4 row passes of 24 rows per tile ----
+    const int c = lane & 15, hsel = lane >> 4;
+    const int rbase = (warp >> 2) * 8 + (warp & 3) + 4 * hsel;   // + 24 pass
+    // shift c_y: class means of the first R <= 64 rows (every CTA, same order)
+    {
+      const int R = static_cast<int>(std::min<int64_t>(n, 64));
+      const int cp = tid & 31, rp = tid >> 5;
+      double q0a = 0.0, q0b = 0.0, q1a = 0.0, q1b = 0.0;
+      int k1 = 0;
+      for (int r = rp; r < R; r += kI8Conv) {
+        const double va = x[static_cast<int64_t>(r) * 64 + cp], vb = x[static_cast<int64_t>(r) * 64 + cp + 32];
+        if (y[r] == 1) { q1a += va; q1b += vb; ++k1; } else { q0a += va; q0b += vb; }
+      }
+      red[rp * 128 + cp] = q0a;
+      red[rp * 128 + cp + 32] = q0b;
+      red[rp * 128 + 64 + cp] = q1a;
+      red[rp * 128 + 64 + cp + 32] = q1b;
+      int* kred = reinterpret_cast<int*>(red + kI8Conv * 128);
+      if (cp == 0) kred[rp] = k1;
+      named_bar(1, kI8Conv * 32);
+      if (tid < 128) {
+        const int cl = tid >> 6, j = tid & 63;
+        double t = 0.0, ta = 0.0;
+        int kc = 0;
+        for (int w = 0; w < kI8Conv; ++w) {
+          t += red[w * 128 + cl * 64 + j];
+          ta += red[w * 128 + j] + red[w * 128 + 64 + j];
+          kc += kred[w];
+        }
+        const int k_c = cl ? kc : R - kc;
+        const double sh = k_c > 0 ? t / k_c : (R > 0 ? ta / R : 0.0);
+        mu_s[cl * 64 + j] = sh;
+        if (blockIdx.x == 0) shift_out[cl * 64 + j] = sh;
+        if (blockIdx.x == 0 && tid == 0) reinterpret_cast<unsigned*>(shift_out + 128)[0] = 0u;   // combine counter
+      }
+      named_bar(1, kI8Conv * 32);
+    }
+    auto tile_row0 = [&](int m) { return (static_cast<int64_t>(blockIdx.x) + static_cast<int64_t>(m) * gridDim.x) * kI8Rows; };
+    // a rolling register lookahead: pass p of tile m + 1 is loaded as soon as pass p of tile m
+    // is converted
+    double4 cur[4];
+    long long ycur[4];
+    // unconditional loads (a row past the CTA's range reads row n - 1 and is excluded by its
+    // index): one definition per register, so the lookahead needs no copies at the loop edge
+    auto load = [&](int m, int p) {
+      const int64_t r = std::min(tile_row0(m) + 24 * p + rbase, n - 1);
+      const double2* src = reinterpret_cast<const double2*>(x + r * 64 + 4 * c);
+      const double2 a = __ldcs(src), b = __ldcs(src + 1);
+      cur[p] = make_double4(a.x, a.y, b.x, b.y);
+      ycur[p] = __ldg(y + r);
+    };
+#pragma unroll
+    for (int p = 0; p < 4; ++p) load(0, p);
+    // per-CTA scales from the first tile: max |f_j| over its rows
+    {
+      double mx[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        if (mt == 0 || tile_row0(0) + 24 * p + rbase >= n) continue;
+        const double* cc = mu_s + (ycur[p] == 1 ? 64 : 0) + 4 * c;
+        mx[0] = fmax(mx[0], fabs(cur[p].x - cc[0]));
+        mx[1] = fmax(mx[1], fabs(cur[p].y - cc[1]));
+        mx[2] = fmax(mx[2], fabs(cur[p].z - cc[2]));
+        mx[3] = fmax(mx[3], fabs(cur[p].w - cc[3]));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        mx[u] = fmax(mx[u], __shfl_xor_sync(0xffffffffu, mx[u], 16));
+        if (hsel == 0) red[warp * 64 + 4 * c + u] = mx[u];
+      }
+      named_bar(1, kI8Conv * 32);
+      if (tid < 64) {
+        double m = 0.0;
+        for (int w = 0; w < kI8Conv; ++w) m = fmax(m, red[w * 64 + tid]);   // NaN-free max (fmax)
+        int s = 1000;   // an all-zero column: any nonzero value later is out of range
+        if (m > 0.0 && m <= 1.0e300) s = 41 - ilogb(m);
+        s = max(-1000, min(1000, s));
+        sc_s[tid] = ldexp(1.0, s);
+        sc_s[64 + tid] = ldexp(1.0, 46 - s);
+        red[kI8Conv * 64 + tid] = ldexp(1.0, -s);   // the quantum, recorded below
+      }
+      named_bar(1, kI8Conv * 32);
+    }
+    auto prefetch = [&](int m) {   // this warp's 4 KB of tile m into L2
+      const int64_t b0 = tile_row0(m) * 512 + warp * 4096, b1 = n * 512;
+      if (lane == 0 && m < mt && b0 < b1)
+        bulk_prefetch_l2(reinterpret_cast<const unsigned char*>(x) + b0, static_cast<uint32_t>(std::min<int64_t>(4096, b1 - b0)));
+    };
+    for (int a = 1; a < kI8L2Ahead; ++a) prefetch(a);
+    // per-thread constants in registers (the plane stores would otherwise order every reload)
+    double scl[4], c0r[4], c1r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      scl[u] = sc_s[4 * c + u];
+      c0r[u] = mu_s[4 * c + u];
+      c1r[u] = mu_s[64 + 4 * c + u];
+    }
+    bool bad = false;
+    double sa[4] = {0.0, 0.0, 0.0, 0.0}, s1[4] = {0.0, 0.0, 0.0, 0.0};
+    int c1 = 0;
+    constexpr double kMagic = 6755399441055744.0 + 141289400074368.0;   // 1.5 * 2^52 + B, B = 0x808080808080
+    for (int m = 0; m < mt; ++m) {
+      const int s = m % kI8Stages;
+      if (kI8L2Ahead > 0) prefetch(m + kI8L2Ahead);
+      if (m >= kI8Stages) mbar_wait(&pempty[s], ((m - kI8Stages) / kI8Stages) & 1);
+      unsigned char* const gb = smem + s * kI8Stage;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const int r = 24 * p + rbase;
+        const bool valid = tile_row0(m) + 24 * p + rbase < n, one = ycur[p] == 1;
+        const double xv[4] = {cur[p].x, cur[p].y, cur[p].z, cur[p].w};
+        double cc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cc[u] = one ? c1r[u] : c0r[u];
+        load(m + 1, p);   // the values are in registers now: refill for the next tile
+        // Z + B with B = sum_i 128 * 2^(8i) has plain bytes u_i (no carries): e_i = u_i - 128, i.e.
+        // the byte u_i with its top bit flipped.  One FMA puts Z + B in the low 48 bits.
+        uint32_t lo[4], hi[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double f = valid ? xv[u] - cc[u] : 0.0;
+          if (valid) {
+            sa[u] += f;
+            s1[u] += one ? f : 0.0;
+          }
+          const long long bits = __double_as_longlong(fma(f, scl[u], kMagic));
+          lo[u] = static_cast<uint32_t>(bits);
+          hi[u] = static_cast<uint32_t>(bits >> 32);
+          // in range iff 0 <= Z + B < 2^48, i.e. the top 16 bits are the magic's (also false for
+          // inf / NaN and for |f 2^s| >= 2^51)
+          bad |= (hi[u] >> 16) != 0x4338u;
+        }
+        // 4 x 6 byte transpose: word i holds digit i of the 4 columns (column u in byte u)
+        const uint32_t t01l = __byte_perm(lo[0], lo[1], 0x5140), t01h = __byte_perm(lo[0], lo[1], 0x7362);
+        const uint32_t t23l = __byte_perm(lo[2], lo[3], 0x5140), t23h = __byte_perm(lo[2], lo[3], 0x7362);
+        const uint32_t h01 = __byte_perm(hi[0], hi[1], 0x5140), h23 = __byte_perm(hi[2], hi[3], 0x5140);
+        uint32_t w[6];
+        w[0] = __byte_perm(t01l, t23l, 0x5410) ^ 0x80808080u;
+        w[1] = __byte_perm(t01l, t23l, 0x7632) ^ 0x80808080u;
+        w[2] = __byte_perm(t01h, t23h, 0x5410) ^ 0x80808080u;
+        w[3] = __byte_perm(t01h, t23h, 0x7632) ^ 0x80808080u;
+        w[4] = __byte_perm(h01, h23, 0x5410) ^ 0x80808080u;
+        w[5] = __byte_perm(h01, h23, 0x7632) ^ 0x80808080u;
+        c1 += (valid && one) ? 1 : 0;
+        // group g holds (e_{5-2g} at bytes 0..63, e_{4-2g} at bytes 64..127)
+#pragma unroll
+        for (int g = 0; g < 3; ++g) {
+          *reinterpret_cast<uint32_t*>(gb + g * kI8Group + sw128_offset(r, 4 * c)) = w[5 - 2 * g];
+          *reinterpret_cast<uint32_t*>(gb + g * kI8Group + sw128_offset(r, 64 + 4 * c)) = w[4 - 2 * g];
+        }
+      }
+      fence_proxy_async_smem();   // generic-proxy stores -> visible to the tensor cores
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pfull[s]);
+    }
+    // ---- class sums, counts, range flag: fixed-order folds through shared memory ----
+    int* const flag_s = reinterpret_cast<int*>(tmem_slot + 1);
+    if (bad) atomicOr(flag_s, 1);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      red[(warp * 2 + hsel) * 128 + 4 * c + u] = sa[u] - s1[u];   // class 0 = all rows - class 1
+      red[(warp * 2 + hsel) * 128 + 64 + 4 * c + u] = s1[u];
+    }
+    int k1 = c == 0 ? c1 : 0;   // each row is counted by its 16 column lanes: keep one
+    for (int o = 16; o > 0; o >>= 1) k1 += __shfl_xor_sync(0xffffffffu, k1, o);
+    int* const kred = reinterpret_cast<int*>(mu_s);   // the shift is no longer read
+    named_bar(1, kI8Conv * 32);
+    if (lane == 0) kred[warp] = k1;
+    if (tid < 128) {
+      double t = 0.0;
+      for (int q = 0; q < 2 * kI8Conv; ++q) t += red[q * 128 + tid];
+      parts_sd[static_cast<size_t>(blockIdx.x) * 128 + tid] = t;
+    }
+    named_bar(1, kI8Conv * 32);
+    if (tid == 0) {
+      long long kk = 0;
+      for (int w = 0; w < kI8Conv; ++w) kk += kred[w];
+      parts_n1[blockIdx.x] = kk;
+    }
+    if (tid < 64)   // the CTA's quantum per column; inf when a value fell outside its range
+      parts_q[static_cast<size_t>(blockIdx.x) * 64 + tid] =
+          *flag_s ? __longlong_as_double(0x7ff0000000000000ll) : 1.0 / sc_s[tid];
+    // ---- S' from the four group products: TMEM -> padded staging -> fixed-order cell sums ----
+    mbar_wait(done, 0);
+    tc_fence_after();
+    if (mt == 0) {   // no tile: the accumulators were never written
+      for (int e = tid; e < 4096; e += kI8Conv * 32) parts[static_cast<size_t>(blockIdx.x) * 4096 + e] = 0.0;
+    } else {
+    int* const stage = reinterpret_cast<int*>(smem);   // [2][128][129] int32 (the plane buffers)
+    const int qd = warp & 3, cc = warp >> 2;   // lane quarter (warp rank in its warpgroup), chunk
+    constexpr int kJ = kI8Conv * 32 / 64;      // rows j per pass: cells (j0 + kJ v, k)
+    constexpr int kV = (64 + kJ - 1) / kJ;
+    double acc[kV];
+#pragma unroll
+    for (int v = 0; v < kV; ++v) acc[v] = 0.0;
+    const int k = tid & 63, j0 = tid >> 6;
+#pragma unroll 1
+    for (int R = 0; R < 2; ++R) {
+      for (int ch = cc; ch < 4; ch += kI8Conv / 4) {   // 64-column chunks of this round
+        const int gi = ch >> 1, n0 = (ch & 1) * 64;
+        int* const row = stage + (gi * 128 + 32 * qd + lane) * 129 + n0;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          int32_t v[16];
+          tmem_ld16(tmem + (static_cast<uint32_t>(32 * qd) << 16) + R * 256 + ch * 64 + 16 * h, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) row[16 * h + i] = v[i];
+        }
+      }
+      named_bar(1, kI8Conv * 32);
+#pragma unroll
+      for (int gi = 0; gi < 2; ++gi) {
+        const int P = 2 * R + gi;
+        const int pp = P == 3 ? 1 : 0, qq = P == 3 ? 1 : P;   // (0,0) (0,1) (0,2) (1,1)
+        const int* const D = stage + gi * 128 * 129;
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const double wgt = ldexp(1.0, 8 * ((5 - (2 * pp + a)) + (5 - (2 * qq + b))));
+#pragma unroll
+            for (int v = 0; v < kV; ++v) {
+              const int j = min(j0 + kJ * v, 63);
+              acc[v] += wgt * static_cast<double>(D[(a * 64 + j) * 129 + b * 64 + k]);
+              if (pp != qq) acc[v] += wgt * static_cast<double>(D[(a * 64 + k) * 129 + b * 64 + j]);
+            }
+          }
+      }
+      named_bar(1, kI8Conv * 32);
+    }
+    double* const out = parts + static_cast<size_t>(blockIdx.x) * 4096;
+    const int sk = ilogb(sc_s[k]);
+#pragma unroll
+    for (int v = 0; v < kV; ++v) {
+      const int j = j0 + kJ * v;
+      if (j < 64) out[j * 64 + k] = scalbn(acc[v], -(ilogb(sc_s[j]) + sk));
+    }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kI8Conv) tmem_dealloc<512>(tmem);
+}
+
 // Single-pass fit, last step (gda_fit_combine, combine.cu): mu_c = c_c + sd_c / n_c and
 // S = S' - sum_c sd_c sd_c^T / n_c.  Certified: the rank-1 corrections may cancel at most 99 % of
 // any diagonal entry of S' (relative rounding amplification <= 100); otherwise *ok = 0 and the
@@ -743,12 +1086,24 @@ size_t gda_fit_workspace_bytes(int64_t n, int d) {
   c.take<long long>(1);
   c.take<double>(129);
   c.take<int>(1);
+  c.take<double>(static_cast<size_t>(grid) * 64);   // int8 fit: the CTAs' quanta
+  c.take<double>(64);
   return c.used + 256;
 }
 
 int gda_fit_combine(const double* parts, const double* parts_sd, const long long* parts_n1, int nparts, int d,
                     double* Sp, double* sd, long long* n1p, int64_t n, const double* shift, unsigned* counter,
-                    long long* n1_out, double* mu0, double* mu1, double* S, int* ok, cudaStream_t s);
+                    long long* n1_out, double* mu0, double* mu1, double* S, int* ok, cudaStream_t s,
+                    const double* parts_q = nullptr, double* qmax = nullptr);
+
+// the int8 fit (DLX_GDA_I8=0 keeps the DMMA fit): d = 64, aligned rows, <= 2^17 rows per CTA
+static bool gda_i8_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DLX_GDA_I8");
+    return e != nullptr && e[0] == '1';
+  }();
+  return on;
+}
 
 int gda_fit(const double* x, const long long* y, int64_t n, int d, long long* n1_out, double* mu0,
             double* mu1, double* S, void* ws, size_t ws_bytes, cudaStream_t stream) {
@@ -764,10 +1119,23 @@ int gda_fit(const double* x, const long long* y, int64_t n, int d, long long* n1
   long long* n1 = c.take<long long>(1);
   double* shift = c.take<double>(129);   // + the combine's completion counter
   int* ok = c.take<int>(1);
+  double* parts_q = c.take<double>(static_cast<size_t>(grid) * 64);
+  double* qmax = c.take<double>(64);
   DLX_REQUIRE(ws && c.used <= ws_bytes, DLX_ERR_ARG, "gda fit: workspace too small");
   const bool k64 = gda_fit64_ok(x, y, d) && n > 0 && !std::getenv("DLX_GDA_ROWBLOCKS");
+  const int64_t i8_tiles = (n + kI8Rows - 1) / kI8Rows;
+  const bool i8 = k64 && gda_i8_enabled() && (i8_tiles + grid - 1) / grid <= kI8MaxTiles;
   CUtensorMap tmx, tmy;
-  if (k64) {
+  if (i8) {
+    if (int rc = g64_maps(x, y, n, &tmx, &tmy)) return rc;   // for the fallback pass
+    DLX_CUDA(cudaFuncSetAttribute(gda_fit_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kI8Smem)));
+    DLX_CUDA(cudaFuncSetAttribute(gda_fit64_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kG64Smem)));
+    DLX_CUDA(launch_pdl(gda_fit_i8_kernel, dim3(grid), dim3(kI8Threads), kI8Smem, stream, x, y, n, parts,
+                        parts_sd, parts_n1, parts_q, shift));
+    DLX_LAUNCHED("gda_fit_i8_kernel");
+  } else if (k64) {
     if (int rc = g64_maps(x, y, n, &tmx, &tmy)) return rc;
     DLX_CUDA(cudaFuncSetAttribute(gda_fit64_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kG64Smem)));
@@ -791,7 +1159,8 @@ int gda_fit(const double* x, const long long* y, int64_t n, int d, long long* n1
   // combine + finalize in one launch (combine.cu); shift[128] is its completion counter, zeroed
   // by the fit kernel's block 0
   if (int rc = gda_fit_combine(parts, parts_sd, parts_n1, grid, d, Sp, sd, n1, n, shift,
-                               reinterpret_cast<unsigned*>(shift + 128), n1_out, mu0, mu1, S, ok, stream))
+                               reinterpret_cast<unsigned*>(shift + 128), n1_out, mu0, mu1, S, ok, stream,
+                               i8 ? parts_q : nullptr, qmax))
     return rc;
   // fallback, decided on the device: pass 2 on the exact means when the shift was too far off
   if (k64) {   // folds its own records into S when it runs (no combine launch)

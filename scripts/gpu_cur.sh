@@ -1,6 +1,10 @@
-# C1 warm-cache profile of the small kernel + combine (ncu --cache-control none)
-OUT=gpurun_out/r340; mkdir -p $OUT
+# int8 GDA fit: unconditional lookahead loads; parity + C3 A/B + profile
+OUT=gpurun_out/r347; mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
-timeout 300 ncu --metrics gpu__time_duration.sum --cache-control none --clock-control none -c 20 --csv --log-file $OUT/launches_c1_warm.csv python bench.py --config c1 --steps 4 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_l.log 2>&1
-timeout 300 ncu --set full --cache-control none --clock-control none --import-source on -k regex:"kmeans_small|combine_kmeans" -s 6 -c 2 -o $OUT/prof_c1_warm python bench.py --config c1 --steps 4 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_f.log 2>&1
+DLX_GDA_I8=1 timeout 300 python -m pytest tests -m gpu -q -x -k "gda or c3" --timeout 100 > $OUT/pytest_gda_i8.log 2>&1; echo "rc=$?" >> $OUT/pytest_gda_i8.log
+for i in 1 2; do
+  DLX_GDA_I8=1 timeout 120 python bench.py --config c3 --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/c3_i8_$i.json 2>&1
+  timeout 120 python bench.py --config c3 --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/c3_def_$i.json 2>&1
+done
+DLX_GDA_I8=1 timeout 400 ncu --set full --clock-control none --import-source on -k regex:gda_fit_i8 -s 3 -c 1 -o $OUT/prof_c3_i8 python bench.py --config c3 --steps 4 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_f.log 2>&1
 echo done > $OUT/DONE
