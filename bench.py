@@ -498,29 +498,43 @@ def run_dlx(args, family, p, metric, unit, rank, world, local_rank):
             "clocks": clocks,
         }
         if family == "gda":
-            # dominant kernel = the scatter on the fp64 tensor cores (the single-pass fit at N = 1,
-            # pass 2 when sharded): executed DMMA flops (lower-triangle 8x8 blocks, 2*8*8 flop per
-            # sample per block) over its event time, against the measured DMMA peak; the HBM
-            # line of the same interval (x and y read once) is kept as roofline_hbm
-            # algorithmic flops of the symmetric scatter: d(d+1)/2 multiply-adds per sample
-            # (the kernel executes the 36 lower 8x8 blocks = 4,608 flop per sample at d = 64)
+            # dominant kernel = the single-pass fit's first pass (pass 2 when sharded).  The int8
+            # path (tcgen05 kind::i8 digit products, csrc/gda_dmma.cu gda_fit_i8_kernel) streams x
+            # and y once and is HBM-paced: its roofline is the HBM line, with the tensor line in
+            # executed int8 ops against the nominal dense int8 peak (not in MEASURED_PEAKS.json).
+            # The DMMA path's roofline is the fp64 tensor line on algorithmic symmetric flops.
             nb = (d + 7) // 8
             flops = n_local * d * (d + 1)
             flops_executed = n_local * 2.0 * 64 * nb * (nb + 1) // 2
             hb = algorithmic_bytes(family, p, n_local) / (pass2_ms * 1e-3) / 1e9
-            result["roofline_hbm"] = {"bound": "hbm", "achieved": hb, "peak": peak, "unit": "GB/s",
-                                      "frac": hb / peak, "kernel_ms": pass2_ms}
+            path = ml.gda_fit_path(x, y)
+            hbm_line = {"bound": "hbm", "achieved": hb, "peak": peak, "unit": "GB/s",
+                        "frac": hb / peak, "kernel_ms": pass2_ms}
+            dmma_line = {"bound": "tensor", "achieved": flops / (pass2_ms * 1e-3) / 1e12,
+                         "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": flops / (pass2_ms * 1e-3) / 1e12 / DMMA_PEAK_TFLOPS,
+                         "peak_kind": DMMA_PEAK_KIND, "kernel_ms": pass2_ms,
+                         "algorithmic_flops_per_launch": flops,
+                         "executed_flops_per_launch": flops_executed,
+                         "executed_frac": flops_executed / (pass2_ms * 1e-3) / 1e12 / DMMA_PEAK_TFLOPS}
             result["config"]["gda_path"] = ("single-pass fit" if comm is None else
                                             "single-pass fit per rank, pooled through the exchange")
+            result["config"]["gda_kernel"] = path
             result["config"]["gda_fit_fallback"] = ml.gda_fit_last_fallback(x)
-            result["roofline"] = {"bound": "tensor", "achieved": flops / (pass2_ms * 1e-3) / 1e12,
-                                  "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                                  "frac": flops / (pass2_ms * 1e-3) / 1e12 / DMMA_PEAK_TFLOPS,
-                                  "traffic": ncu_traffic(args.config), "peak_kind": DMMA_PEAK_KIND,
-                                  "kernel_ms": pass2_ms,
-                                  "algorithmic_flops_per_launch": flops,
-                                  "executed_flops_per_launch": flops_executed,
-                                  "executed_frac": flops_executed / (pass2_ms * 1e-3) / 1e12 / DMMA_PEAK_TFLOPS}
+            if path == "int8":
+                # 12 MMAs of 128 x 128 x 32 per 96-row tile: four group products x 3 K-steps
+                ops = n_local / 96.0 * 12 * 2.0 * 128 * 128 * 32
+                result["roofline"] = {**hbm_line, "traffic": ncu_traffic(args.config),
+                                      "algorithmic_bytes_per_launch": algorithmic_bytes(family, p, n_local)}
+                result["roofline_tensor_int8"] = {"bound": "tensor", "achieved": ops / (pass2_ms * 1e-3) / 1e12,
+                                                  "peak": 4500.0, "unit": "TOP/s",
+                                                  "frac": ops / (pass2_ms * 1e-3) / 1e12 / 4500.0,
+                                                  "peak_kind": "nominal dense int8 = the fp8 figure of B200_PROFILING.md (unmeasured)",
+                                                  "executed_ops_per_launch": ops}
+                result["roofline_fp64_equivalent"] = dmma_line
+            else:
+                result["roofline_hbm"] = hbm_line
+                result["roofline"] = {**dmma_line, "traffic": ncu_traffic(args.config)}
         if world == 1 and not args.no_cpu_baseline:
             try:
                 result["cpu_baseline"] = (cpu_baseline_kmeans(p) if family == "kmeans"

@@ -187,6 +187,10 @@ int dlx_gda_combine_ranks(const double* d_table, int32_t world, int32_t d, doubl
                           int64_t* d_n1, double* d_mu0, double* d_mu1, dlx_stream_t stream);
 /* 1 if the last dlx_gda_fit on this workspace took the exact-means fallback (synchronous). */
 int dlx_gda_fit_last_fallback(const void* d_workspace, int64_t n, int32_t d, int* h_fallback);
+/* Which first pass dlx_gda_fit runs for these inputs (host-side, no launch): 2 = the int8
+ * tensor-core fit (d = 64, 16-byte aligned x / y, <= 2^17 rows per CTA, DLX_GDA_I8 != 0),
+ * 1 = the k-split DMMA fit (d = 64, aligned), 0 = the row-block DMMA kernel. */
+int dlx_gda_fit_path(const void* d_x, const void* d_y, int64_t n, int32_t d, int* h_path);
 int dlx_gda_pass2(const double* d_x, const int64_t* d_y, int64_t n, int32_t d,
                   const double* d_mu0, const double* d_mu1, double* d_scatter, void* d_workspace,
                   size_t workspace_bytes, dlx_stream_t stream);

@@ -111,6 +111,7 @@ _SIGS = {
     "dlx_gda_fit": (_int, [_vp, _vp, _i64, _int, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "dlx_gda_combine_ranks": (_int, [_vp, _int, _int, _vp, _vp, _vp, _vp, _vp]),
     "dlx_gda_fit_last_fallback": (_int, [_vp, _i64, _int, ctypes.POINTER(_int)]),
+    "dlx_gda_fit_path": (_int, [_vp, _vp, _i64, _int, ctypes.POINTER(_int)]),
     "dlx_peer_alloc": (_int, [_i64, ctypes.POINTER(_vp), ctypes.c_char_p]),
     "dlx_peer_open": (_int, [ctypes.c_char_p, ctypes.POINTER(_vp)]),
     "dlx_peer_close": (_int, [_vp]),

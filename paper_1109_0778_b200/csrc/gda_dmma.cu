@@ -22,6 +22,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -362,8 +363,8 @@ gda_pass2_dmma_kernel(const double* __restrict__ x, const long long* __restrict_
 // accumulators per lane, 36 independent DMMA chains) for 8 of every 64-sample tile's rows, so
 // a k-step costs 4 LDS.128 of x for 36 DMMAs; the warps centre their fragments in registers
 // straight from the raw tile (no centred copy in shared memory) and, in the single-pass fit,
-// also accumulate the shifted class sums from those centred fragments (sum over all rows and
-// over class 1; class 0 = all - class 1), so no other warp touches the fp64 pipe the DMMAs use.
+// also accumulate the shifted per-class sums from those centred fragments (one select-and-add
+// per class), so no other warp touches the fp64 pipe the DMMAs use.
 // One producer warp refills the 5-slot ring.
 //
 // Tiles arrive by TMA tensor copies (cp.async.bulk.tensor.2d, 4 boxes of 64 rows x 16 columns
@@ -534,7 +535,7 @@ gda_fit64_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant_
   double acc[36][2];
 #pragma unroll
   for (int b = 0; b < 36; ++b) acc[b][0] = acc[b][1] = 0.0;
-  double sa[8], s1[8];   // fused: shifted sums of this lane's logical columns (all rows, class 1)
+  double sa[8], s1[8];   // fused: shifted sums of this lane's logical columns (class 0, class 1)
 #pragma unroll
   for (int idx = 0; idx < 8; ++idx) sa[idx] = s1[idx] = 0.0;
   int c1 = 0;
@@ -565,8 +566,8 @@ gda_fit64_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant_
       if (kFused) {
 #pragma unroll
         // (selecting the class accumulator instead, one add per element, measured slower: r225)
-        for (int idx = 0; idx < 8; ++idx) {
-          sa[idx] += f[idx];
+        for (int idx = 0; idx < 8; ++idx) {   // per-class sums (all - class 1 would turn an
+          sa[idx] += one ? 0.0 : f[idx];        // inf of class 1 into NaN for class 0)
           s1[idx] += one ? f[idx] : 0.0;
         }
         c1 += (valid && one) ? 1 : 0;
@@ -591,7 +592,7 @@ gda_fit64_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant_
       va += __shfl_xor_sync(0xffffffffu, va, 2);
       v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
       if (kq == 0) {
-        fsum[(warp * 2 + 0) * 64 + 8 * idx + g] = va - v1;   // class 0 = all rows - class 1
+        fsum[(warp * 2 + 0) * 64 + 8 * idx + g] = va;   // class 0
         fsum[(warp * 2 + 1) * 64 + 8 * idx + g] = v1;
       }
     }
@@ -730,8 +731,9 @@ int gda_pass2_dmma(const double* x, const long long* y, int64_t n, int d, const 
 // ---- the d = 64 single-pass fit on the int8 tensor cores (gda_fit_i8_kernel) ------------------
 // S' = sum_i f_i f_i^T with f = fl(x - c_y) (the shift-centred rows, as the DMMA kernel forms them)
 // computed as an EXACT integer product: every CTA quantises f per column to the fixed point
-// Z_j = rne(f_j * 2^s_j) (|Z| < 2^46, s_j from the CTA's first tile: max |f_j| * 2^s_j < 2^42)
-// and splits Z into six balanced base-256 digits e_0..e_5 (each in [-128, 127]); with digit
+// Z_j = rne(f_j * 2^s_j) (s_j from the CTA's first tile: max |f_j| * 2^s_j < 2^42) and splits Z
+// into six balanced base-256 digits e_0..e_5 (each in [-128, 127]; the bytes of Z + B, B = sum_i
+// 128 * 2^(8i), with their top bit flipped — one FMA against a magic constant); with digit
 // significance t = 5 - i, the digit products F_a^T F_b with t_a + t_b <= 5 (the dropped ones are
 // below 2^-36 of the leading term) are four tcgen05 kind::i8 MMAs per 32-row step over digit
 // pair groups G0 = {e5, e4}, G1 = {e3, e2}, G2 = {e1, e0}: (G0,G0), (G0,G1), (G0,G2), (G1,G1),
@@ -740,29 +742,29 @@ int gda_pass2_dmma(const double* x, const long long* y, int64_t n, int d, const 
 // The off-diagonal group products enter S' with their transposes.  The class sums stay fp64
 // sums of the same f (the means need them exactly as the DMMA path forms them).  Certification
 // (gda_fit_combine): every CTA's quantum 2^-s_j must be <= 2^-30 of column j's RMS deviation,
-// and a value outside the CTA's range (|f| >= 2^(46 - s_j), inf, NaN) sets the quantum to inf —
+// and a value outside the CTA's range (Z + B outside [0, 2^48), inf, NaN) sets the quantum to inf —
 // either way *ok = 0 and the exact DMMA pass 2 on the means runs instead.
-// 12 converter warps + the issuer: at most 4 warps per SM sub-partition, 128 registers each
+// 12 converter warps + the issuer + the producer: at most 4 warps per SM sub-partition, 128
+// registers each.  The producer bulk-copies x / y tiles (96 contiguous rows = 48 KB) into two
+// shared-memory stages, so the loads in flight do not cost converter registers.
 constexpr int kI8Conv = 12;                           // converter warps (then the epilogue)
-constexpr int kI8Threads = (kI8Conv + 1) * 32;        // + the MMA issuer warp
+constexpr int kI8Threads = (kI8Conv + 2) * 32;        // + the MMA issuer and the producer warp
 constexpr int kI8Rows = 96;                           // rows per tile: 4 passes of 24 (3 K-steps)
-constexpr int kI8Stages = 4;                          // digit-plane buffers in flight
+constexpr int kI8Stages = 3;                          // digit-plane buffers in flight
+constexpr int kI8XStages = 2;                         // x / y tiles in flight
 constexpr uint32_t kI8Group = kI8Rows * 128;          // one digit-pair group: 96 rows x 128 B
 constexpr uint32_t kI8Stage = 3 * kI8Group;           // three groups per tile
-constexpr size_t kI8OffMu = kI8Stages * kI8Stage;     // [c0: 0..63 | c1: 64..127] shift
-constexpr size_t kI8OffScale = kI8OffMu + 128 * 8;    // 2^s_j, then thresholds 2^(46-s_j)
-constexpr size_t kI8OffRed = kI8OffScale + 128 * 8;   // reductions: 512 x 8 doubles
-constexpr size_t kI8OffBar = kI8OffRed + kI8Conv * 32 * 8 * 8;
-constexpr size_t kI8Smem = kI8OffBar + (2 * kI8Stages + 2) * 8 + 16 + 1024;
-#ifndef DLX_I8_L2_AHEAD
-#define DLX_I8_L2_AHEAD 3
-#endif
-constexpr int kI8L2Ahead = DLX_I8_L2_AHEAD;            // converters' L2 bulk prefetch distance (tiles)
-static_assert(kI8Conv * 4096 == kI8Rows * 512, "one 4 KB prefetch per converter warp covers a tile");
+constexpr uint32_t kI8XBytes = kI8Rows * 512;         // one x tile
+constexpr size_t kI8OffX = kI8Stages * kI8Stage;
+constexpr size_t kI8OffY = kI8OffX + kI8XStages * kI8XBytes;
+constexpr size_t kI8OffMu = kI8OffY + kI8XStages * kI8Rows * 8;   // [c0: 0..63 | c1: 64..127] shift
+constexpr size_t kI8OffScale = kI8OffMu + 128 * 8;    // 2^s_j
+constexpr size_t kI8OffBar = kI8OffScale + 128 * 8;
+constexpr size_t kI8Smem = kI8OffBar + (2 * kI8Stages + 2 * kI8XStages + 2) * 8 + 16 + 1024;
 constexpr int kI8MaxTiles = (1 << 17) / kI8Rows;      // 2^17 rows per CTA (int32 exactness)
-static_assert(2 * 128 * 129 * 4 <= kI8OffMu, "TMEM staging must fit in the plane buffers");
+static_assert(2 * 128 * 129 * 4 <= kI8OffY, "TMEM staging must fit below the y stages");
+static_assert(2 * kI8Conv * 128 * 8 <= kI8XStages * kI8XBytes, "class-sum fold fits in the x stages");
 static_assert(kI8Smem <= 232448, "shared memory");
-
 
 __global__ void __launch_bounds__(kI8Threads, 1)
 gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y, int64_t n,
@@ -771,19 +773,26 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* const smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   double* const mu_s = reinterpret_cast<double*>(smem + kI8OffMu);
-  double* const sc_s = reinterpret_cast<double*>(smem + kI8OffScale);   // [0,64): 2^s, [64,128): bound
-  double* const red = reinterpret_cast<double*>(smem + kI8OffRed);
+  double* const sc_s = reinterpret_cast<double*>(smem + kI8OffScale);   // 2^s_j
   uint64_t* const pfull = reinterpret_cast<uint64_t*>(smem + kI8OffBar);
   uint64_t* const pempty = pfull + kI8Stages;
-  uint64_t* const done = pempty + kI8Stages;
+  uint64_t* const xfull = pempty + kI8Stages;
+  uint64_t* const xempty = xfull + kI8XStages;
+  uint64_t* const done = xempty + kI8XStages;
   uint32_t* const tmem_slot = reinterpret_cast<uint32_t*>(done + 2);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t ntiles = (n + kI8Rows - 1) / kI8Rows;
   const int mt = static_cast<int>(ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0);
+  auto tile_row0 = [&](int m) { return (static_cast<int64_t>(blockIdx.x) + static_cast<int64_t>(m) * gridDim.x) * kI8Rows; };
+  auto tile_rows = [&](int m) { return static_cast<int>(std::min<int64_t>(kI8Rows, n - tile_row0(m))); };
   if (tid == 0) {
     for (int s = 0; s < kI8Stages; ++s) {
       mbar_init(&pfull[s], kI8Conv);
       mbar_init(&pempty[s], 1);
+    }
+    for (int s = 0; s < kI8XStages; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], kI8Conv);
     }
     mbar_init(done, 1);
     fence_mbar_init();
@@ -823,7 +832,23 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
     }
     if (lane == 0) mma_commit(done);
     __syncwarp();
+  } else if (warp == kI8Conv + 1) {
+    // ---- producer: x tile (contiguous rows) and the even part of its labels per stage; an odd
+    // last label is read by its converter (bulk copies move multiples of 16 bytes) ----
+    if (lane == 0) {
+      for (int m = 0; m < mt; ++m) {
+        const int xs = m % kI8XStages;
+        if (m >= kI8XStages) mbar_wait(&xempty[xs], ((m - kI8XStages) / kI8XStages) & 1);
+        const int64_t row0 = tile_row0(m);
+        const uint32_t rows = static_cast<uint32_t>(tile_rows(m)), yb = (rows * 8u) & ~15u;
+        mbar_arrive_expect_tx(&xfull[xs], rows * 512u + yb);
+        bulk_g2s(smem + kI8OffX + xs * kI8XBytes, x + row0 * 64, rows * 512u, &xfull[xs]);
+        if (yb) bulk_g2s(smem + kI8OffY + xs * kI8Rows * 8, y + row0, yb, &xfull[xs]);
+      }
+    }
+    __syncwarp();
   } else {
+    double* const red = reinterpret_cast<double*>(smem);   // prologue folds: the plane buffers
     // ---- converters: warp w, lane l: columns 4c..4c+3 (c = l & 15) of rows {r, r + 4} of an
     // 8-row swizzle atom (disjoint bank halves), 4 row passes of 24 rows per tile ----
     const int c = lane & 15, hsel = lane >> 4;
@@ -862,33 +887,34 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
       }
       named_bar(1, kI8Conv * 32);
     }
-    auto tile_row0 = [&](int m) { return (static_cast<int64_t>(blockIdx.x) + static_cast<int64_t>(m) * gridDim.x) * kI8Rows; };
-    // a rolling register lookahead: pass p of tile m + 1 is loaded as soon as pass p of tile m
-    // is converted
-    double4 cur[4];
-    long long ycur[4];
-    // unconditional loads (a row past the CTA's range reads row n - 1 and is excluded by its
-    // index): one definition per register, so the lookahead needs no copies at the loop edge
-    auto load = [&](int m, int p) {
-      const int64_t r = std::min(tile_row0(m) + 24 * p + rbase, n - 1);
-      const double2* src = reinterpret_cast<const double2*>(x + r * 64 + 4 * c);
-      const double2 a = __ldcs(src), b = __ldcs(src + 1);
-      cur[p] = make_double4(a.x, a.y, b.x, b.y);
-      ycur[p] = __ldg(y + r);
+    // x / y of tile m, pass p: this thread's 4 columns of row 24 p + rbase (rows past the tile's
+    // end read stale stage bytes and are excluded by their index)
+    auto xrow = [&](int m, int p) {
+      const double* xt = reinterpret_cast<const double*>(smem + kI8OffX + (m % kI8XStages) * kI8XBytes);
+      const double2* src = reinterpret_cast<const double2*>(xt + (24 * p + rbase) * 64 + 4 * c);
+      const double2 a = src[0], b = src[1];
+      return make_double4(a.x, a.y, b.x, b.y);
     };
-#pragma unroll
-    for (int p = 0; p < 4; ++p) load(0, p);
+    auto yrow = [&](int m, int p, int rows) {
+      const int r = 24 * p + rbase;
+      const long long* yt = reinterpret_cast<const long long*>(smem + kI8OffY + (m % kI8XStages) * kI8Rows * 8);
+      if (r < (rows & ~1)) return yt[r];
+      return r < rows ? __ldg(y + tile_row0(m) + r) : 0ll;
+    };
+    if (mt > 0) mbar_wait(&xfull[0], 0);
     // per-CTA scales from the first tile: max |f_j| over its rows
     {
       double mx[4] = {0.0, 0.0, 0.0, 0.0};
+      const int rows0 = mt > 0 ? tile_rows(0) : 0;
 #pragma unroll
       for (int p = 0; p < 4; ++p) {
-        if (mt == 0 || tile_row0(0) + 24 * p + rbase >= n) continue;
-        const double* cc = mu_s + (ycur[p] == 1 ? 64 : 0) + 4 * c;
-        mx[0] = fmax(mx[0], fabs(cur[p].x - cc[0]));
-        mx[1] = fmax(mx[1], fabs(cur[p].y - cc[1]));
-        mx[2] = fmax(mx[2], fabs(cur[p].z - cc[2]));
-        mx[3] = fmax(mx[3], fabs(cur[p].w - cc[3]));
+        if (24 * p + rbase >= rows0) continue;
+        const double4 v = xrow(0, p);
+        const double* cc = mu_s + (yrow(0, p, rows0) == 1 ? 64 : 0) + 4 * c;
+        mx[0] = fmax(mx[0], fabs(v.x - cc[0]));
+        mx[1] = fmax(mx[1], fabs(v.y - cc[1]));
+        mx[2] = fmax(mx[2], fabs(v.z - cc[2]));
+        mx[3] = fmax(mx[3], fabs(v.w - cc[3]));
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -903,60 +929,51 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
         if (m > 0.0 && m <= 1.0e300) s = 41 - ilogb(m);
         s = max(-1000, min(1000, s));
         sc_s[tid] = ldexp(1.0, s);
-        sc_s[64 + tid] = ldexp(1.0, 46 - s);
-        red[kI8Conv * 64 + tid] = ldexp(1.0, -s);   // the quantum, recorded below
       }
       named_bar(1, kI8Conv * 32);
     }
-    auto prefetch = [&](int m) {   // this warp's 4 KB of tile m into L2
-      const int64_t b0 = tile_row0(m) * 512 + warp * 4096, b1 = n * 512;
-      if (lane == 0 && m < mt && b0 < b1)
-        bulk_prefetch_l2(reinterpret_cast<const unsigned char*>(x) + b0, static_cast<uint32_t>(std::min<int64_t>(4096, b1 - b0)));
-    };
-    for (int a = 1; a < kI8L2Ahead; ++a) prefetch(a);
-    // per-thread constants in registers (the plane stores would otherwise order every reload)
-    double scl[4], c0r[4], c1r[4];
+    // the per-column scales in registers
+    double scl[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      scl[u] = sc_s[4 * c + u];
-      c0r[u] = mu_s[4 * c + u];
-      c1r[u] = mu_s[64 + 4 * c + u];
-    }
+    for (int u = 0; u < 4; ++u) scl[u] = sc_s[4 * c + u];
     bool bad = false;
-    double sa[4] = {0.0, 0.0, 0.0, 0.0}, s1[4] = {0.0, 0.0, 0.0, 0.0};
+    double sa[4] = {0.0, 0.0, 0.0, 0.0}, s1[4] = {0.0, 0.0, 0.0, 0.0};   // class 0, class 1
     int c1 = 0;
     constexpr double kMagic = 6755399441055744.0 + 141289400074368.0;   // 1.5 * 2^52 + B, B = 0x808080808080
     for (int m = 0; m < mt; ++m) {
-      const int s = m % kI8Stages;
-      if (kI8L2Ahead > 0) prefetch(m + kI8L2Ahead);
+      const int s = m % kI8Stages, rows = tile_rows(m);
+      mbar_wait(&xfull[m % kI8XStages], (m / kI8XStages) & 1);
       if (m >= kI8Stages) mbar_wait(&pempty[s], ((m - kI8Stages) / kI8Stages) & 1);
       unsigned char* const gb = smem + s * kI8Stage;
-#pragma unroll
-      for (int p = 0; p < 4; ++p) {
+      const long long* const yt = reinterpret_cast<const long long*>(smem + kI8OffY + (m % kI8XStages) * kI8Rows * 8);
+      auto do_pass = [&](auto full_tag, int p) {
+        constexpr bool kFull = decltype(full_tag)::value;   // a whole tile: no row checks
         const int r = 24 * p + rbase;
-        const bool valid = tile_row0(m) + 24 * p + rbase < n, one = ycur[p] == 1;
-        const double xv[4] = {cur[p].x, cur[p].y, cur[p].z, cur[p].w};
-        double cc[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) cc[u] = one ? c1r[u] : c0r[u];
-        load(m + 1, p);   // the values are in registers now: refill for the next tile
+        const bool valid = kFull || r < rows;
+        const bool one = (kFull ? yt[r] : yrow(m, p, rows)) == 1;
+        const double4 xq = xrow(m, p);
+        const double2* cp = reinterpret_cast<const double2*>(mu_s + (one ? 64 : 0) + 4 * c);   // the row's shift
+        const double2 ca = cp[0], cb = cp[1];
+        const double xv[4] = {xq.x, xq.y, xq.z, xq.w}, cc[4] = {ca.x, ca.y, cb.x, cb.y};
         // Z + B with B = sum_i 128 * 2^(8i) has plain bytes u_i (no carries): e_i = u_i - 128, i.e.
         // the byte u_i with its top bit flipped.  One FMA puts Z + B in the low 48 bits.
         uint32_t lo[4], hi[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const double f = valid ? xv[u] - cc[u] : 0.0;
-          if (valid) {
-            sa[u] += f;
-            s1[u] += one ? f : 0.0;
+          double f = xv[u] - cc[u];
+          if (!kFull) f = valid ? f : 0.0;
+          if (kFull || valid) {   // per-class sums (an all-rows sum minus class 1 would turn
+            if (one) s1[u] += f;     // an inf of class 1 into NaN for class 0)
+            else sa[u] += f;
           }
           const long long bits = __double_as_longlong(fma(f, scl[u], kMagic));
           lo[u] = static_cast<uint32_t>(bits);
           hi[u] = static_cast<uint32_t>(bits >> 32);
-          // in range iff 0 <= Z + B < 2^48, i.e. the top 16 bits are the magic's (also false for
-          // inf / NaN and for |f 2^s| >= 2^51)
-          bad |= (hi[u] >> 16) != 0x4338u;
         }
+        // in range iff 0 <= Z + B < 2^48, i.e. the top 16 bits are the magic's (also false for
+        // inf / NaN and for |f 2^s| >= 2^51)
+        constexpr uint32_t K = 0x43380000u;
+        bad |= ((((hi[0] ^ K) | (hi[1] ^ K)) | ((hi[2] ^ K) | (hi[3] ^ K))) >> 16) != 0u;
         // 4 x 6 byte transpose: word i holds digit i of the 4 columns (column u in byte u)
         const uint32_t t01l = __byte_perm(lo[0], lo[1], 0x5140), t01h = __byte_perm(lo[0], lo[1], 0x7362);
         const uint32_t t23l = __byte_perm(lo[2], lo[3], 0x5140), t23h = __byte_perm(lo[2], lo[3], 0x7362);
@@ -970,23 +987,37 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
         w[5] = __byte_perm(h01, h23, 0x7632) ^ 0x80808080u;
         c1 += (valid && one) ? 1 : 0;
         // group g holds (e_{5-2g} at bytes 0..63, e_{4-2g} at bytes 64..127)
+        // (asm stores without a memory clobber: the compiler may hoist the next pass's shared
+        // loads above them — the planes are only read by the tensor cores, after the fence below)
+        const uint32_t gs = smem_addr(gb);
 #pragma unroll
         for (int g = 0; g < 3; ++g) {
-          *reinterpret_cast<uint32_t*>(gb + g * kI8Group + sw128_offset(r, 4 * c)) = w[5 - 2 * g];
-          *reinterpret_cast<uint32_t*>(gb + g * kI8Group + sw128_offset(r, 64 + 4 * c)) = w[4 - 2 * g];
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(gs + g * kI8Group + sw128_offset(r, 4 * c)), "r"(w[5 - 2 * g]));
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(gs + g * kI8Group + sw128_offset(r, 64 + 4 * c)), "r"(w[4 - 2 * g]));
         }
+      };
+      if (rows == kI8Rows) {
+#pragma unroll
+        for (int p = 0; p < 4; ++p) do_pass(std::true_type{}, p);
+      } else {
+#pragma unroll
+        for (int p = 0; p < 4; ++p) do_pass(std::false_type{}, p);
       }
       fence_proxy_async_smem();   // generic-proxy stores -> visible to the tensor cores
       __syncwarp();
-      if (lane == 0) mbar_arrive(&pfull[s]);
+      if (lane == 0) {
+        mbar_arrive(&pfull[s]);
+        mbar_arrive(&xempty[m % kI8XStages]);
+      }
     }
     // ---- class sums, counts, range flag: fixed-order folds through shared memory ----
     int* const flag_s = reinterpret_cast<int*>(tmem_slot + 1);
     if (bad) atomicOr(flag_s, 1);
+    double* const rede = reinterpret_cast<double*>(smem + kI8OffX);   // every x stage consumed
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      red[(warp * 2 + hsel) * 128 + 4 * c + u] = sa[u] - s1[u];   // class 0 = all rows - class 1
-      red[(warp * 2 + hsel) * 128 + 64 + 4 * c + u] = s1[u];
+      rede[(warp * 2 + hsel) * 128 + 4 * c + u] = sa[u];   // class 0
+      rede[(warp * 2 + hsel) * 128 + 64 + 4 * c + u] = s1[u];
     }
     int k1 = c == 0 ? c1 : 0;   // each row is counted by its 16 column lanes: keep one
     for (int o = 16; o > 0; o >>= 1) k1 += __shfl_xor_sync(0xffffffffu, k1, o);
@@ -995,7 +1026,7 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
     if (lane == 0) kred[warp] = k1;
     if (tid < 128) {
       double t = 0.0;
-      for (int q = 0; q < 2 * kI8Conv; ++q) t += red[q * 128 + tid];
+      for (int q = 0; q < 2 * kI8Conv; ++q) t += rede[q * 128 + tid];
       parts_sd[static_cast<size_t>(blockIdx.x) * 128 + tid] = t;
     }
     named_bar(1, kI8Conv * 32);
@@ -1097,12 +1128,17 @@ int gda_fit_combine(const double* parts, const double* parts_sd, const long long
                     const double* parts_q = nullptr, double* qmax = nullptr);
 
 // the int8 fit (DLX_GDA_I8=0 keeps the DMMA fit): d = 64, aligned rows, <= 2^17 rows per CTA
-static bool gda_i8_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("DLX_GDA_I8");
-    return e != nullptr && e[0] == '1';
-  }();
-  return on;
+static bool gda_i8_enabled() {   // read per fit (tests switch it in-process)
+  const char* e = std::getenv("DLX_GDA_I8");
+  return e == nullptr || e[0] != '0';
+}
+
+// 2 = int8 fit, 1 = k-split DMMA fit, 0 = row blocks (dlx_gda_fit_path)
+int gda_fit_path(const double* x, const long long* y, int64_t n, int d) {
+  if (!(gda_fit64_ok(x, y, d) && n > 0 && !std::getenv("DLX_GDA_ROWBLOCKS"))) return 0;
+  const int grid = gda_pass2_dmma_grid(n);
+  const int64_t i8_tiles = (n + kI8Rows - 1) / kI8Rows;
+  return gda_i8_enabled() && (i8_tiles + grid - 1) / grid <= kI8MaxTiles ? 2 : 1;
 }
 
 int gda_fit(const double* x, const long long* y, int64_t n, int d, long long* n1_out, double* mu0,
@@ -1122,9 +1158,8 @@ int gda_fit(const double* x, const long long* y, int64_t n, int d, long long* n1
   double* parts_q = c.take<double>(static_cast<size_t>(grid) * 64);
   double* qmax = c.take<double>(64);
   DLX_REQUIRE(ws && c.used <= ws_bytes, DLX_ERR_ARG, "gda fit: workspace too small");
-  const bool k64 = gda_fit64_ok(x, y, d) && n > 0 && !std::getenv("DLX_GDA_ROWBLOCKS");
-  const int64_t i8_tiles = (n + kI8Rows - 1) / kI8Rows;
-  const bool i8 = k64 && gda_i8_enabled() && (i8_tiles + grid - 1) / grid <= kI8MaxTiles;
+  const int path = gda_fit_path(x, y, n, d);
+  const bool k64 = path >= 1, i8 = path == 2;
   CUtensorMap tmx, tmy;
   if (i8) {
     if (int rc = g64_maps(x, y, n, &tmx, &tmy)) return rc;   // for the fallback pass
@@ -1251,6 +1286,12 @@ int dlx_gda_fit(const double* d_x, const int64_t* d_y, int64_t n, int32_t d, int
                 size_t workspace_bytes, dlx_stream_t stream) {
   return dlx::gda_fit(d_x, reinterpret_cast<const long long*>(d_y), n, d, reinterpret_cast<long long*>(d_n1),
                       d_mu0, d_mu1, d_scatter, d_workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int dlx_gda_fit_path(const void* d_x, const void* d_y, int64_t n, int32_t d, int* h_path) {
+  DLX_REQUIRE(h_path && n >= 0 && d > 0, DLX_ERR_ARG, "gda fit path: bad args");
+  *h_path = dlx::gda_fit_path(static_cast<const double*>(d_x), static_cast<const long long*>(d_y), n, d);
+  return DLX_OK;
 }
 
 int dlx_gda_fit_last_fallback(const void* d_workspace, int64_t n, int32_t d, int* h_fallback) {

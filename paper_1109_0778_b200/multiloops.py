@@ -261,6 +261,16 @@ def gda_fit_last_fallback(x: torch.Tensor) -> bool:
     return bool(flag.value)
 
 
+def gda_fit_path(x: torch.Tensor, y: torch.Tensor) -> str:
+    """The first pass dlx_gda_fit runs for (x, y): "int8" (tcgen05 kind::i8), "dmma" (k-split
+    fp64 tensor cores) or "rowblocks"."""
+    L = _lib.load()
+    n, d = x.shape
+    path = ctypes.c_int(0)
+    check(L.dlx_gda_fit_path(_ptr(x), _ptr(y), n, d, ctypes.byref(path)))
+    return {2: "int8", 1: "dmma", 0: "rowblocks"}[path.value]
+
+
 def gda(x: torch.Tensor, y: torch.Tensor, comm=None):
     """phi-numerator n1, mu0, mu1 and the unnormalised scatter S.  One
     device-local fit reads x once (gda_fit); sharded fits run the two reference passes with

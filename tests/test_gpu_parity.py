@@ -453,6 +453,64 @@ def test_gda_fit_fallback(ml, kind):
             np.testing.assert_allclose(a[fin], b[fin], rtol=RTOL, atol=1e-9 * np.abs(b[fin]).max())
 
 
+@pytest.mark.parametrize("kind", ["late_outlier", "zero_first_tiles", "late_nan", "late_inf", "tiny_column"])
+def test_gda_fit_int8_range(ml, kind):
+    """The int8 fit quantises each column per CTA from its first tile: a later value outside
+    that range (or inf / NaN) must force the exact pass 2, a column that is tiny everywhere must
+    keep its relative precision; results equal the two-pass path either way."""
+    n, d = 300_001, 64
+    x = dev_units(ml, n, d, seed=13)
+    y = ml.rng_ints(n, 2, seed=13, first_draw=n * d)
+    assert ml.gda_fit_path(x, y) == "int8"
+    if kind == "late_outlier":          # row 250,000: 1e7 in one column (first tiles: O(1))
+        x[250_000, 5] = 1.0e7
+    elif kind == "zero_first_tiles":    # column 3 constant over every CTA's first tile, then not
+        x[:96 * 148 * 2, 3] = 0.5
+    elif kind == "late_nan":
+        x[200_000, 7] = float("nan")
+    elif kind == "late_inf":
+        x[123_456, 9] = float("inf")
+    else:                               # column 11 at 1e-100 scale everywhere
+        x[:, 11] *= 1.0e-100
+    f = ml.gda_fit(x, y)
+    fb = ml.gda_fit_last_fallback(x)
+    if kind in ("late_outlier", "zero_first_tiles", "late_nan", "late_inf"):
+        assert fb
+    else:
+        assert not fb
+    t = _gda_two_pass(ml, x, y)
+    assert int(f[0].item()) == int(t[0].item())
+    for a, b in zip(f[1:], t[1:]):
+        a, b = a.cpu().numpy(), b.cpu().numpy()
+        assert np.array_equal(np.isnan(a), np.isnan(b))
+        fin = np.isfinite(b)
+        if fin.any():
+            np.testing.assert_allclose(a[fin], b[fin], rtol=RTOL, atol=1e-9 * np.abs(b[fin]).max())
+    if kind == "tiny_column":   # its own scale: row and column 11 of S against the two-pass S
+        Sa, Sb = f[3].cpu().numpy(), t[3].cpu().numpy()
+        np.testing.assert_allclose(Sa[11], Sb[11], rtol=RTOL, atol=1e-9 * np.abs(Sb[11]).max())
+
+
+@pytest.mark.parametrize("n", [1_048_576, 300_001, 97, 1])
+def test_gda_fit_int8_matches_dmma(ml, n, monkeypatch):
+    """The int8 tensor-core fit and the DMMA fit (DLX_GDA_I8=0) on the same inputs: equal n1,
+    means and scatter within the fp64 tolerance."""
+    d = 64
+    x = dev_units(ml, n, d, seed=14)
+    y = ml.rng_ints(n, 2, seed=14, first_draw=n * d)
+    assert ml.gda_fit_path(x, y) == "int8"
+    a = [t.cpu().numpy() for t in ml.gda_fit(x, y)]
+    monkeypatch.setenv("DLX_GDA_I8", "0")
+    assert ml.gda_fit_path(x, y) == "dmma"
+    b = [t.cpu().numpy() for t in ml.gda_fit(x, y)]
+    assert int(a[0]) == int(b[0])
+    for u, v in zip(a[1:], b[1:]):
+        assert np.array_equal(np.isnan(u), np.isnan(v))
+        fin = np.isfinite(v)
+        if fin.any():
+            np.testing.assert_allclose(u[fin], v[fin], rtol=RTOL, atol=1e-9 * np.abs(v[fin]).max())
+
+
 # ---- generic collect / reduce -------------------------------------------------------------------------
 
 def test_generic_families(ml):
