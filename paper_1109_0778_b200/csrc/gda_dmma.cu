@@ -765,6 +765,9 @@ constexpr int kI8MaxTiles = (1 << 17) / kI8Rows;      // 2^17 rows per CTA (int3
 static_assert(2 * 128 * 129 * 4 <= kI8OffY, "TMEM staging must fit below the y stages");
 static_assert(2 * kI8Conv * 128 * 8 <= kI8XStages * kI8XBytes, "class-sum fold fits in the x stages");
 static_assert(kI8Smem <= 232448, "shared memory");
+// plane byte L (the logical column) holds physical column i8_phys(L): converter c packs columns
+// 2c, 2c+1, 32+2c, 33+2c, so a phase of 8 lanes reads 128 contiguous bytes of x (no conflicts)
+__host__ __device__ constexpr int i8_phys(int L) { return (L & 3) < 2 ? 2 * (L >> 2) + (L & 3) : 32 + 2 * (L >> 2) + (L & 3) - 2; }
 
 __global__ void __launch_bounds__(kI8Threads, 1)
 gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y, int64_t n,
@@ -891,8 +894,8 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
     // end read stale stage bytes and are excluded by their index)
     auto xrow = [&](int m, int p) {
       const double* xt = reinterpret_cast<const double*>(smem + kI8OffX + (m % kI8XStages) * kI8XBytes);
-      const double2* src = reinterpret_cast<const double2*>(xt + (24 * p + rbase) * 64 + 4 * c);
-      const double2 a = src[0], b = src[1];
+      const double* src = xt + (24 * p + rbase) * 64 + 2 * c;   // physical columns 2c, 2c+1 | 32+2c, 33+2c
+      const double2 a = *reinterpret_cast<const double2*>(src), b = *reinterpret_cast<const double2*>(src + 32);
       return make_double4(a.x, a.y, b.x, b.y);
     };
     auto yrow = [&](int m, int p, int rows) {
@@ -910,16 +913,16 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
       for (int p = 0; p < 4; ++p) {
         if (24 * p + rbase >= rows0) continue;
         const double4 v = xrow(0, p);
-        const double* cc = mu_s + (yrow(0, p, rows0) == 1 ? 64 : 0) + 4 * c;
-        mx[0] = fmax(mx[0], fabs(v.x - cc[0]));
-        mx[1] = fmax(mx[1], fabs(v.y - cc[1]));
-        mx[2] = fmax(mx[2], fabs(v.z - cc[2]));
-        mx[3] = fmax(mx[3], fabs(v.w - cc[3]));
+        const double* cc = mu_s + (yrow(0, p, rows0) == 1 ? 64 : 0);
+        mx[0] = fmax(mx[0], fabs(v.x - cc[i8_phys(4 * c)]));
+        mx[1] = fmax(mx[1], fabs(v.y - cc[i8_phys(4 * c + 1)]));
+        mx[2] = fmax(mx[2], fabs(v.z - cc[i8_phys(4 * c + 2)]));
+        mx[3] = fmax(mx[3], fabs(v.w - cc[i8_phys(4 * c + 3)]));
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         mx[u] = fmax(mx[u], __shfl_xor_sync(0xffffffffu, mx[u], 16));
-        if (hsel == 0) red[warp * 64 + 4 * c + u] = mx[u];
+        if (hsel == 0) red[warp * 64 + i8_phys(4 * c + u)] = mx[u];
       }
       named_bar(1, kI8Conv * 32);
       if (tid < 64) {
@@ -935,7 +938,7 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
     // the per-column scales in registers
     double scl[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) scl[u] = sc_s[4 * c + u];
+    for (int u = 0; u < 4; ++u) scl[u] = sc_s[i8_phys(4 * c + u)];
     bool bad = false;
     double sa[4] = {0.0, 0.0, 0.0, 0.0}, s1[4] = {0.0, 0.0, 0.0, 0.0};   // class 0, class 1
     int c1 = 0;
@@ -952,8 +955,8 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
         const bool valid = kFull || r < rows;
         const bool one = (kFull ? yt[r] : yrow(m, p, rows)) == 1;
         const double4 xq = xrow(m, p);
-        const double2* cp = reinterpret_cast<const double2*>(mu_s + (one ? 64 : 0) + 4 * c);   // the row's shift
-        const double2 ca = cp[0], cb = cp[1];
+        const double* cp = mu_s + (one ? 64 : 0) + 2 * c;   // the row's shift, same columns
+        const double2 ca = *reinterpret_cast<const double2*>(cp), cb = *reinterpret_cast<const double2*>(cp + 32);
         const double xv[4] = {xq.x, xq.y, xq.z, xq.w}, cc[4] = {ca.x, ca.y, cb.x, cb.y};
         // Z + B with B = sum_i 128 * 2^(8i) has plain bytes u_i (no carries): e_i = u_i - 128, i.e.
         // the byte u_i with its top bit flipped.  One FMA puts Z + B in the low 48 bits.
@@ -1016,8 +1019,8 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
     double* const rede = reinterpret_cast<double*>(smem + kI8OffX);   // every x stage consumed
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      rede[(warp * 2 + hsel) * 128 + 4 * c + u] = sa[u];   // class 0
-      rede[(warp * 2 + hsel) * 128 + 64 + 4 * c + u] = s1[u];
+      rede[(warp * 2 + hsel) * 128 + i8_phys(4 * c + u)] = sa[u];   // class 0
+      rede[(warp * 2 + hsel) * 128 + 64 + i8_phys(4 * c + u)] = s1[u];
     }
     int k1 = c == 0 ? c1 : 0;   // each row is counted by its 16 column lanes: keep one
     for (int o = 16; o > 0; o >>= 1) k1 += __shfl_xor_sync(0xffffffffu, k1, o);
@@ -1088,11 +1091,14 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
       named_bar(1, kI8Conv * 32);
     }
     double* const out = parts + static_cast<size_t>(blockIdx.x) * 4096;
-    const int sk = ilogb(sc_s[k]);
+    const int pk = i8_phys(k), sk = ilogb(sc_s[pk]);
 #pragma unroll
     for (int v = 0; v < kV; ++v) {
       const int j = j0 + kJ * v;
-      if (j < 64) out[j * 64 + k] = scalbn(acc[v], -(ilogb(sc_s[j]) + sk));
+      if (j < 64) {
+        const int pj = i8_phys(j);
+        out[pj * 64 + pk] = scalbn(acc[v], -(ilogb(sc_s[pj]) + sk));
+      }
     }
     }
   }
