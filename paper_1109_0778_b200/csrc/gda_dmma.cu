@@ -961,18 +961,27 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
         // Z + B with B = sum_i 128 * 2^(8i) has plain bytes u_i (no carries): e_i = u_i - 128, i.e.
         // the byte u_i with its top bit flipped.  One FMA puts Z + B in the low 48 bits.
         uint32_t lo[4], hi[4];
+        double f[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          double f = xv[u] - cc[u];
-          if (!kFull) f = valid ? f : 0.0;
-          if (kFull || valid) {   // per-class sums (an all-rows sum minus class 1 would turn
-            if (one) s1[u] += f;     // an inf of class 1 into NaN for class 0)
-            else sa[u] += f;
-          }
-          const long long bits = __double_as_longlong(fma(f, scl[u], kMagic));
+          f[u] = xv[u] - cc[u];
+          if (!kFull) f[u] = valid ? f[u] : 0.0;   // padding rows: zero digits, no class
+          const long long bits = __double_as_longlong(fma(f[u], scl[u], kMagic));
           lo[u] = static_cast<uint32_t>(bits);
           hi[u] = static_cast<uint32_t>(bits >> 32);
         }
+        // per-class sums as predicated adds (one predicate per row; selects would cost four
+        // FSELs per element; an all-rows sum minus class 1 would turn a class-1 inf into NaN)
+        const uint32_t cls = (kFull || valid) ? (one ? 1u : 2u) : 0u;
+        asm("{\n.reg .pred p1, p0;\n"
+            "setp.eq.u32 p1, %12, 1;\n"
+            "setp.eq.u32 p0, %12, 2;\n"
+            "@p1 add.f64 %0, %0, %8;\n@p0 add.f64 %4, %4, %8;\n"
+            "@p1 add.f64 %1, %1, %9;\n@p0 add.f64 %5, %5, %9;\n"
+            "@p1 add.f64 %2, %2, %10;\n@p0 add.f64 %6, %6, %10;\n"
+            "@p1 add.f64 %3, %3, %11;\n@p0 add.f64 %7, %7, %11;\n}"
+            : "+d"(s1[0]), "+d"(s1[1]), "+d"(s1[2]), "+d"(s1[3]), "+d"(sa[0]), "+d"(sa[1]), "+d"(sa[2]), "+d"(sa[3])
+            : "d"(f[0]), "d"(f[1]), "d"(f[2]), "d"(f[3]), "r"(cls));
         // in range iff 0 <= Z + B < 2^48, i.e. the top 16 bits are the magic's (also false for
         // inf / NaN and for |f 2^s| >= 2^51)
         constexpr uint32_t K = 0x43380000u;
