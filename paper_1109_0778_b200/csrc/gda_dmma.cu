@@ -940,7 +940,7 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
 #pragma unroll
     for (int u = 0; u < 4; ++u) scl[u] = sc_s[i8_phys(4 * c + u)];
     bool bad = false;
-    double sa[4] = {0.0, 0.0, 0.0, 0.0}, s1[4] = {0.0, 0.0, 0.0, 0.0};   // class 0, class 1
+    double sa[4] = {0.0, 0.0, 0.0, 0.0}, s1[4] = {0.0, 0.0, 0.0, 0.0};   // all rows, class 1
     int c1 = 0;
     constexpr double kMagic = 6755399441055744.0 + 141289400074368.0;   // 1.5 * 2^52 + B, B = 0x808080808080
     for (int m = 0; m < mt; ++m) {
@@ -970,18 +970,16 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
           lo[u] = static_cast<uint32_t>(bits);
           hi[u] = static_cast<uint32_t>(bits >> 32);
         }
-        // per-class sums as predicated adds (one predicate per row; selects would cost four
-        // FSELs per element; an all-rows sum minus class 1 would turn a class-1 inf into NaN)
-        const uint32_t cls = (kFull || valid) ? (one ? 1u : 2u) : 0u;
-        asm("{\n.reg .pred p1, p0;\n"
-            "setp.eq.u32 p1, %12, 1;\n"
-            "setp.eq.u32 p0, %12, 2;\n"
-            "@p1 add.f64 %0, %0, %8;\n@p0 add.f64 %4, %4, %8;\n"
-            "@p1 add.f64 %1, %1, %9;\n@p0 add.f64 %5, %5, %9;\n"
-            "@p1 add.f64 %2, %2, %10;\n@p0 add.f64 %6, %6, %10;\n"
-            "@p1 add.f64 %3, %3, %11;\n@p0 add.f64 %7, %7, %11;\n}"
-            : "+d"(s1[0]), "+d"(s1[1]), "+d"(s1[2]), "+d"(s1[3]), "+d"(sa[0]), "+d"(sa[1]), "+d"(sa[2]), "+d"(sa[3])
-            : "d"(f[0]), "d"(f[1]), "d"(f[2]), "d"(f[3]), "r"(cls));
+        // class sums without selects: all rows (a padding row adds f = 0) and class 1 through an
+        // FMA with the row's 0 / 1 weight, on the fp64 pipe; class 0 = all - class 1.  Only a
+        // non-finite value (inf * 0 = NaN) breaks that — it also sets the range flag, and the
+        // CTA then recomputes its class sums directly (below)
+        const double w1 = one ? 1.0 : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          sa[u] += f[u];
+          s1[u] = fma(f[u], w1, s1[u]);
+        }
         // in range iff 0 <= Z + B < 2^48, i.e. the top 16 bits are the magic's (also false for
         // inf / NaN and for |f 2^s| >= 2^51)
         constexpr uint32_t K = 0x43380000u;
@@ -1026,14 +1024,35 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
     int* const flag_s = reinterpret_cast<int*>(tmem_slot + 1);
     if (bad) atomicOr(flag_s, 1);
     double* const rede = reinterpret_cast<double*>(smem + kI8OffX);   // every x stage consumed
+    named_bar(1, kI8Conv * 32);
+    if (*flag_s == 0) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      rede[(warp * 2 + hsel) * 128 + i8_phys(4 * c + u)] = sa[u];   // class 0
-      rede[(warp * 2 + hsel) * 128 + 64 + i8_phys(4 * c + u)] = s1[u];
+      for (int u = 0; u < 4; ++u) {
+        rede[(warp * 2 + hsel) * 128 + i8_phys(4 * c + u)] = sa[u] - s1[u];   // class 0
+        rede[(warp * 2 + hsel) * 128 + 64 + i8_phys(4 * c + u)] = s1[u];
+      }
+    } else {
+      // a value outside the CTA's range (possibly inf / NaN): the exact per-class sums of the
+      // CTA's rows, re-read from global memory (thread: column tid & 63, rows of group tid >> 6)
+      constexpr int kG = kI8Conv * 32 / 64;
+      const int j = tid & 63, rg = tid >> 6;
+      double q0 = 0.0, q1 = 0.0;
+      for (int m = 0; m < mt; ++m) {
+        const int64_t row0 = tile_row0(m);
+        const int rows = tile_rows(m);
+        for (int r = rg; r < rows; r += kG) {
+          const double f = x[(row0 + r) * 64 + j] - mu_s[(y[row0 + r] == 1 ? 64 : 0) + j];
+          if (y[row0 + r] == 1) q1 += f; else q0 += f;
+        }
+      }
+      for (int q = tid; q < 2 * kI8Conv * 128; q += kI8Conv * 32) rede[q] = 0.0;
+      named_bar(1, kI8Conv * 32);
+      rede[rg * 128 + j] = q0;
+      rede[rg * 128 + 64 + j] = q1;
     }
     int k1 = c == 0 ? c1 : 0;   // each row is counted by its 16 column lanes: keep one
     for (int o = 16; o > 0; o >>= 1) k1 += __shfl_xor_sync(0xffffffffu, k1, o);
-    int* const kred = reinterpret_cast<int*>(mu_s);   // the shift is no longer read
+    int* const kred = reinterpret_cast<int*>(sc_s + 64);   // the upper half of the scale area
     named_bar(1, kI8Conv * 32);
     if (lane == 0) kred[warp] = k1;
     if (tid < 128) {
