@@ -949,15 +949,27 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
       if (m >= kI8Stages) mbar_wait(&pempty[s], ((m - kI8Stages) / kI8Stages) & 1);
       unsigned char* const gb = smem + s * kI8Stage;
       const long long* const yt = reinterpret_cast<const long long*>(smem + kI8OffY + (m % kI8XStages) * kI8Rows * 8);
-      auto do_pass = [&](auto full_tag, int p) {
+      struct Row {   // one pass's operands: the row's 4 values, its class and its shift
+        double4 xq;
+        double2 ca, cb;
+        bool one;
+      };
+      auto fetch = [&](auto full_tag, int p) {
+        constexpr bool kFull = decltype(full_tag)::value;
+        Row o;
+        o.one = (kFull ? yt[24 * p + rbase] : yrow(m, p, rows)) == 1;
+        o.xq = xrow(m, p);
+        const double* cp = mu_s + (o.one ? 64 : 0) + 2 * c;   // the row's shift, same columns
+        o.ca = *reinterpret_cast<const double2*>(cp);
+        o.cb = *reinterpret_cast<const double2*>(cp + 32);
+        return o;
+      };
+      auto do_pass = [&](auto full_tag, int p, const Row& o) {
         constexpr bool kFull = decltype(full_tag)::value;   // a whole tile: no row checks
         const int r = 24 * p + rbase;
         const bool valid = kFull || r < rows;
-        const bool one = (kFull ? yt[r] : yrow(m, p, rows)) == 1;
-        const double4 xq = xrow(m, p);
-        const double* cp = mu_s + (one ? 64 : 0) + 2 * c;   // the row's shift, same columns
-        const double2 ca = *reinterpret_cast<const double2*>(cp), cb = *reinterpret_cast<const double2*>(cp + 32);
-        const double xv[4] = {xq.x, xq.y, xq.z, xq.w}, cc[4] = {ca.x, ca.y, cb.x, cb.y};
+        const bool one = o.one;
+        const double xv[4] = {o.xq.x, o.xq.y, o.xq.z, o.xq.w}, cc[4] = {o.ca.x, o.ca.y, o.cb.x, o.cb.y};
         // Z + B with B = sum_i 128 * 2^(8i) has plain bytes u_i (no carries): e_i = u_i - 128, i.e.
         // the byte u_i with its top bit flipped.  One FMA puts Z + B in the low 48 bits.
         uint32_t lo[4], hi[4];
@@ -1007,11 +1019,17 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
         }
       };
       if (rows == kI8Rows) {
+        Row cur = fetch(std::true_type{}, 0);
 #pragma unroll
-        for (int p = 0; p < 4; ++p) do_pass(std::true_type{}, p);
+        for (int p = 0; p < 4; ++p) {   // the next pass's shared loads issue before this pass's math
+          Row nxt = cur;
+          if (p < 3) nxt = fetch(std::true_type{}, p + 1);
+          do_pass(std::true_type{}, p, cur);
+          cur = nxt;
+        }
       } else {
 #pragma unroll
-        for (int p = 0; p < 4; ++p) do_pass(std::false_type{}, p);
+        for (int p = 0; p < 4; ++p) do_pass(std::false_type{}, p, fetch(std::false_type{}, p));
       }
       fence_proxy_async_smem();   // generic-proxy stores -> visible to the tensor cores
       __syncwarp();
