@@ -1,5 +1,5 @@
-# int8 GDA fit: next-pass operands fetched a pass ahead; GDA tests + C3 bench + profile
-OUT=gpurun_out/r357; mkdir -p $OUT
+# int8 GDA fit: pass-0 fetch before the plane-stage wait; GDA tests + C3 bench + profile
+OUT=gpurun_out/r359; mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
 timeout 300 python -m pytest tests -m gpu -q -x -k "gda or c3" --timeout 100 > $OUT/pytest_gda.log 2>&1; echo "rc=$?" >> $OUT/pytest_gda.log
 for i in 1 2; do
