@@ -121,20 +121,24 @@ gda_fit_combine_kernel(const double* __restrict__ parts, const double* __restric
   __syncthreads();
   if (!last) return;
   __threadfence();
-  __shared__ double sd_s[128];   // the class sums, once from L2 (d <= 64)
-  for (int e = threadIdx.x; e < 2 * d; e += blockDim.x) sd_s[e] = __ldcg(sd + e);
-  __syncthreads();
+  __shared__ double sd_s[128], sq_s[128];   // the class sums (d <= 64) and sums / n_c
   const long long n1 = __ldcg(n1p), n0 = n - n1;
   const double dn0 = static_cast<double>(n0), dn1 = static_cast<double>(n1);
-  auto corr = [&](int a, int b) {
+  for (int e = threadIdx.x; e < 2 * d; e += blockDim.x) {
+    sd_s[e] = __ldcg(sd + e);
+    sq_s[e] = sd_s[e] / (e < d ? dn0 : dn1);   // one division per (class, column), not per entry
+  }
+  __syncthreads();
+  auto corr = [&](int a, int b) {   // sum_c sd_c[a] sd_c[b] / n_c, the same value for (a, b), (b, a)
+    const int lo = min(a, b), hi = max(a, b);
     double c = 0.0;
-    if (n0 > 0) c += sd_s[a] * sd_s[b] / dn0;
-    if (n1 > 0) c += sd_s[d + a] * sd_s[d + b] / dn1;
+    if (n0 > 0) c += sd_s[lo] * sq_s[hi];
+    if (n1 > 0) c += sd_s[d + lo] * sq_s[d + hi];
     return c;
   };
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    mu0[j] = __ldcg(shift + j) + sd_s[j] / dn0;        // an empty class: 0 / 0 -> NaN, as the reference
-    mu1[j] = __ldcg(shift + 64 + j) + sd_s[d + j] / dn1;
+    mu0[j] = __ldcg(shift + j) + sq_s[j];        // an empty class: 0 / 0 -> NaN, as the reference
+    mu1[j] = __ldcg(shift + 64 + j) + sq_s[d + j];
     const double cj = corr(j, j), sj = __ldcg(Sp + j * d + j);
     if (!(cj <= 0.99 * sj)) bad = 1;
     // int8 fit: every CTA's quantum <= 2^-30 of the column's RMS deviation about the shift

@@ -1136,6 +1136,15 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
       }
       named_bar(1, kI8Conv * 32);
     }
+    // S' symmetric by construction: (j, k) and (k, j) both take the value formed for the cell
+    // with j <= k (the two are sums of the same products in different orders)
+    double* const sym = reinterpret_cast<double*>(smem);   // [64][65], the staging is consumed
+#pragma unroll
+    for (int v = 0; v < kV; ++v) {
+      const int j = j0 + kJ * v;
+      if (j < 64 && j <= k) sym[j * 65 + k] = acc[v];
+    }
+    named_bar(1, kI8Conv * 32);
     double* const out = parts + static_cast<size_t>(blockIdx.x) * 4096;
     const int pk = i8_phys(k), sk = ilogb(sc_s[pk]);
 #pragma unroll
@@ -1143,7 +1152,7 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
       const int j = j0 + kJ * v;
       if (j < 64) {
         const int pj = i8_phys(j);
-        out[pj * 64 + pk] = scalbn(acc[v], -(ilogb(sc_s[pj]) + sk));
+        out[pj * 64 + pk] = scalbn(sym[min(j, k) * 65 + max(j, k)], -(ilogb(sc_s[pj]) + sk));
       }
     }
     }

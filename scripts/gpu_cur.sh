@@ -1,9 +1,9 @@
-# validation of the committed state: smoke, full GPU suite, default bench (C4), C3/C1 lines, launch lists
-OUT=gpurun_out/r360; mkdir -p $OUT
-bash scripts/gpu_round.sh r360 smoke tests
-timeout 600 python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err
-for c in c3 c1 c2 l16 c5 c4shard8; do
-  timeout 300 python bench.py --config $c --steps 10 --warmup 3 > $OUT/bench_$c.json 2> $OUT/bench_$c.err
+# GDA combine: one division per (class, column); symmetric S' / S by construction
+OUT=gpurun_out/r361; mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+timeout 300 python -m pytest tests -m gpu -q -x -k "gda or c3 or staged or program" --timeout 100 > $OUT/pytest_gda.log 2>&1; echo "rc=$?" >> $OUT/pytest_gda.log
+for i in 1 2; do
+  timeout 120 python bench.py --config c3 --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/c3_$i.json 2>&1
 done
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 30 --csv --log-file $OUT/launches_c3.csv python bench.py --config c3 --steps 4 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_l3.log 2>&1
-echo done > $OUT/DONE2
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 12 --csv --log-file $OUT/launches_c3.csv python bench.py --config c3 --steps 4 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_l3.log 2>&1
+echo done > $OUT/DONE

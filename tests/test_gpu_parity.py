@@ -494,7 +494,7 @@ def test_gda_fit_int8_range(ml, kind):
 @pytest.mark.parametrize("n", [1_048_576, 300_001, 97, 1])
 def test_gda_fit_int8_matches_dmma(ml, n, monkeypatch):
     """The int8 tensor-core fit and the DMMA fit (DLX_GDA_I8=0) on the same inputs: equal n1,
-    means and scatter within the fp64 tolerance."""
+    means and scatter within the fp64 tolerance; both scatters bitwise symmetric."""
     d = 64
     x = dev_units(ml, n, d, seed=14)
     y = ml.rng_ints(n, 2, seed=14, first_draw=n * d)
@@ -504,6 +504,7 @@ def test_gda_fit_int8_matches_dmma(ml, n, monkeypatch):
     assert ml.gda_fit_path(x, y) == "dmma"
     b = [t.cpu().numpy() for t in ml.gda_fit(x, y)]
     assert int(a[0]) == int(b[0])
+    assert np.array_equal(a[3], a[3].T, equal_nan=True) and np.array_equal(b[3], b[3].T, equal_nan=True)
     for u, v in zip(a[1:], b[1:]):
         assert np.array_equal(np.isnan(u), np.isnan(v))
         fin = np.isfinite(v)
