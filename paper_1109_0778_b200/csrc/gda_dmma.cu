@@ -852,8 +852,9 @@ gda_fit_i8_kernel(const double* __restrict__ x, const long long* __restrict__ y,
     __syncwarp();
   } else {
     double* const red = reinterpret_cast<double*>(smem);   // prologue folds: the plane buffers
-    // ---- converters: warp w, lane l: columns 4c..4c+3 (c = l & 15) of rows {r, r + 4} of an
-    // 8-row swizzle atom (disjoint bank halves), 4 row passes of 24 rows per tile ----
+    // ---- converters: warp w, lane l: plane bytes 4c..4c+3 (c = l & 15; physical columns 2c,
+    // 2c+1, 32+2c, 33+2c, i8_phys) of rows {r, r + 4} of an 8-row swizzle atom (disjoint bank
+    // halves), 4 row passes of 24 rows per tile ----
     const int c = lane & 15, hsel = lane >> 4;
     const int rbase = (warp >> 2) * 8 + (warp & 3) + 4 * hsel;   // + 24 pass
     // shift c_y: class means of the first R <= 64 rows (every CTA, same order)
