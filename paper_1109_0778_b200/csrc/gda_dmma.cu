@@ -483,7 +483,7 @@ gda_fit64_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant_
       }
     }
     __syncwarp();
-    __syncthreads();   // (A)
+    named_bar_split(3, kG64Threads);   // (A), met by the tensor-core warps below
     return;
   }
 
@@ -576,7 +576,7 @@ gda_fit64_kernel(const __grid_constant__ CUtensorMap tmx, const __grid_constant_
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
-  __syncthreads();   // (A) every tile consumed, no copy outstanding: the ring becomes the fold area
+  named_bar_split(3, kG64Threads);   // (A) every tile consumed, no copy outstanding: the ring becomes the fold area
   double* fold = reinterpret_cast<double*>(raw);
 #pragma unroll
   for (int b = 0; b < 36; ++b)

@@ -480,7 +480,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
       if (lane == 0) mbar_arrive(&S.dec_empty[b]);
     }
     if (lane == 0) pend_count[blockIdx.x] = pending;
-    named_bar(7, 160);
+    named_bar_split(7, 160);   // met by the epilogue warps' barrier 7 below
   }
   } else if (warp >= kWarpC0) {
     if constexpr (kRegsConv > kRegsLaunch) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsConv));
@@ -787,7 +787,7 @@ kmeans_screened_kernel(const double* __restrict__ x, int64_t n, int d, int k,
     mbar_wait(&S.fold_done, 0);
     if (q == 0) TRACE_PH(2);
     tc_fence_after();
-    named_bar(7, 160);   // with the tail warp: every count is in S.cnt
+    named_bar_split(7, 160);   // with the tail warp: every count is in S.cnt
     unsigned long long* scratch = reinterpret_cast<unsigned long long*>(smem + kOffA);
     {
       const int half = q >> 6, j = q & 63;

@@ -66,6 +66,11 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
+// the same barrier reached from different code locations (warp-specialised branches that
+// meet once): the non-aligned form, which does not require every thread at the same instruction
+__device__ __forceinline__ void named_bar_split(uint32_t id, uint32_t threads) {
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 
 // ---- tcgen05 ------------------------------------------------------------------------------
 template <uint32_t kCols>
