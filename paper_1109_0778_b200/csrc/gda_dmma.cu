@@ -750,8 +750,8 @@ int gda_pass2_dmma(const double* x, const long long* y, int64_t n, int d, const 
 constexpr int kI8Conv = 12;                           // converter warps (then the epilogue)
 constexpr int kI8Threads = (kI8Conv + 2) * 32;        // + the MMA issuer and the producer warp
 constexpr int kI8Rows = 96;                           // rows per tile: 4 passes of 24 (3 K-steps)
-constexpr int kI8Stages = 3;                          // digit-plane buffers in flight
-constexpr int kI8XStages = 2;                         // x / y tiles in flight
+constexpr int kI8Stages = 2;                          // digit-plane buffers in flight
+constexpr int kI8XStages = 3;                         // x / y tiles in flight
 constexpr uint32_t kI8Group = kI8Rows * 128;          // one digit-pair group: 96 rows x 128 B
 constexpr uint32_t kI8Stage = 3 * kI8Group;           // three groups per tile
 constexpr uint32_t kI8XBytes = kI8Rows * 512;         // one x tile
